@@ -1,0 +1,149 @@
+"""Generate tests/golden/ref_vectors.json from the REFERENCE itself.
+
+TEST INFRASTRUCTURE.  Runs only where oracle/_ref/libirismpc_ref.so was built
+from /root/reference (`make -C oracle ref`).  Every expected value below comes
+from a reference entry point (ref_driver.cpp -> unmodified reference code); the
+C restatement is NOT used to produce expectations, only to regenerate inputs
+whose generator (Rng / random_record) is itself pinned by the KATs recorded
+here.
+
+    python oracle/gen_golden.py
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import pyoracle as O  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                   "ref_vectors.json")
+
+# (backend, l, s, persons, rotations, seed, membership, ratio, planted)
+CASES = [
+    (0, 64, 4, 1, 1, 101, True, 0.375, True),
+    (1, 64, 4, 1, 1, 102, True, 0.375, True),
+    (0, 8, 3, 1, 1, 103, True, 0.375, False),
+    (1, 8, 5, 1, 1, 104, True, 0.375, False),
+    (0, 64, 64, 1, 1, 105, True, 0.3, True),
+    (1, 64, 64, 1, 1, 106, True, 0.3, False),
+    (0, 128, 3, 3, 3, 107, False, 0.375, True),
+    (1, 128, 3, 3, 3, 108, False, 0.375, True),
+    (0, 128, 0, 4, 31, 109, False, 0.2, False),
+    (1, 256, 7, 2, 31, 110, False, 0.375, True),
+    (0, 256, 9, 2, 31, 111, False, 0.375, False),
+    (1, 12800, 2, 1, 31, 112, False, 0.375, True),
+    (0, 12800, 3, 1, 31, 113, False, 0.375, True),
+    (1, 12800, 40, 2, 31, 114, False, 0.375, True),
+]
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).astype("<u2").tobytes()).hexdigest()
+
+
+def inputs(l, s, persons, seed, membership, planted):
+    """Synthetic records: Rng(seed) draws s DB rows then the query codes."""
+    rng = O.Rng(seed)
+    dc, dm = O.records(rng, l, s, 0.85)
+    nq = 1 if membership else 2 * persons
+    qc, qm = O.records(rng, l, nq, 0.85)
+    if planted and s > 0:
+        qc[0] = dc[s // 2]
+        qm[0] = dm[s // 2]
+    return dc, dm, qc, qm
+
+
+def main():
+    R = O.ref()
+    g = {"generated_by": "oracle/gen_golden.py from oracle/_ref (reference compiled from /root/reference/proj)"}
+
+    s42 = np.zeros(16, np.uint8)
+    R.ref_seed_from_u64(42, O._p(s42, O.u8p))
+    blk = np.zeros(16, np.uint32)
+    R.ref_chacha_block(O._p(s42, O.u8p), 0, 0, O._p(blk, O.u32p))
+    blk5 = np.zeros(16, np.uint32)
+    R.ref_chacha_block(O._p(s42, O.u8p), 5, 3, O._p(blk5, O.u32p))
+    ps = np.zeros(48, np.uint8)
+    R.ref_party_seeds(7, O._p(ps, O.u8p))
+    lam = np.zeros(6, np.uint16)
+    R.ref_lambda16(O._p(lam, O.u16p))
+    rng_draws = np.zeros(20, np.uint64)
+    R.ref_rng_u64(2, 20, O._p(rng_draws, O.u64p))
+    g["prf"] = {
+        "seed_from_u64_42": bytes(s42).hex(),
+        "chacha12_seed42_block0_stream0": [int(x) for x in blk],
+        "chacha12_seed42_block5_stream3": [int(x) for x in blk5],
+        "party_seeds_7": bytes(ps).hex(),
+        "rng2_first20": [str(int(x)) for x in rng_draws],
+    }
+    g["lambda16"] = [int(x) for x in lam]
+
+    # random_record(l, Rng(11), density) sequence
+    dens = np.array([0.85, 0.9, 0.0, 1.0, 0.3], np.float64)
+    l = 128
+    rc = np.zeros((5, 2), np.uint64)
+    rm = np.zeros((5, 2), np.uint64)
+    R.ref_random_records(11, l, 5, dens.ctypes.data_as(C.POINTER(C.c_double)), O._p(rc, O.u64p), O._p(rm, O.u64p))
+    g["random_records_rng11_l128"] = {"density": dens.tolist(), "code": [[str(int(w)) for w in r] for r in rc],
+                                      "mask": [[str(int(w)) for w in r] for r in rm]}
+
+    # dealer payload hashes
+    deals = []
+    for be in (0, 1):
+        for l in (64, 12800):
+            dc, dm = rc[:3, :1] if l == 64 else None, None
+            rng = O.Rng(21)
+            dc, dm = O.records(rng, l, 3, 0.9)
+            rb = O.record_bytes(be, l)
+            outs = [np.zeros(3 * rb, np.uint8) for _ in range(3)]
+            R.ref_deal(be, l, 7, 1, 3, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
+            deals.append({"backend": be, "l": l, "records_rng": 21, "nrec": 3, "deal_seed": 7, "tag": 1,
+                          "sha256": [hashlib.sha256(x.tobytes()).hexdigest() for x in outs],
+                          "head_hex": [x[:32].tobytes().hex() for x in outs]})
+    g["deal"] = deals
+
+    cases = []
+    for (be, l, s, persons, r, seed, membership, ratio, planted) in CASES:
+        dc, dm, qc, qm = inputs(l, s, persons, seed, membership, planted)
+        res = O.ref_run_local(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership, debug_rows=True)
+        db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)))
+        q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)))
+        # the dealt payloads must equal the reference dealer's (pinned above) — recheck here
+        outs = [np.zeros(max(1, s * O.record_bytes(be, l)), np.uint8) for _ in range(3)]
+        if s:
+            R.ref_deal(be, l, seed, 1, s, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
+            assert all((a == b[: len(a)]).all() for a, b in zip(db, outs))
+        seeds = O.party_seeds(seed)
+        dh, dmm, rh, rm = O.ref_dots_reshare(be, l, r, seeds, db, s, q, persons, membership)
+        n = int(res["lanes"])
+        case = {
+            "backend": be, "l": l, "s": s, "persons": persons, "rotations": r, "seed": seed,
+            "membership": membership, "ratio": ratio, "planted": planted, "lanes": n,
+            "person_match": [int(x) for x in res["person_match"]],
+            "row_bits_hex": np.packbits(res["row_bits"], bitorder="little").tobytes().hex(),
+            "stats": res["stats"],
+            "sha256": {"dot_hd": sha(dh), "dot_ml": sha(dmm), "rs_hd": sha(rh), "rs_ml": sha(rm)},
+        }
+        if n <= 64:
+            case["dot_hd"] = dh.tolist()
+            case["dot_ml"] = dmm.tolist()
+            case["rs_hd"] = rh.tolist()
+            case["rs_ml"] = rm.tolist()
+        cases.append(case)
+        print(f"case be={be} l={l} s={s} persons={persons} r={r} lanes={n} match={case['person_match']}")
+    g["cases"] = cases
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    with open(OUT, "w") as f:
+        json.dump(g, f, indent=1)
+    print("wrote", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,340 @@
+"""ctypes bindings for the test-side checkers (TEST INFRASTRUCTURE ONLY).
+
+Loaded only by tests/, ``__graft_entry__.smoke()`` and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs.  Two libraries:
+
+* ``liboracle.so`` — the C restatement (oracle/irismpc_oracle.c), always built;
+* ``_ref/libirismpc_ref.so`` — the reference compiled from /root/reference by
+  oracle/Makefile (present only where that tree existed at build time).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libirismpc_ref.so")
+
+REPLICATED, SHAMIR = 0, 1
+
+u8p = C.POINTER(C.c_uint8)
+u16p = C.POINTER(C.c_uint16)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [("backend", C.c_int32), ("l", C.c_uint32), ("a", C.c_uint32), ("b", C.c_uint32),
+                ("rotations", C.c_uint32), ("debug_rows", C.c_int32)]
+
+
+class OrcStats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in (
+        "dot_bytes", "lift_bytes", "msb_bytes", "or_tree_bytes",
+        "dot_rounds", "lift_rounds", "msb_rounds", "or_tree_rounds")]
+
+
+class OrcOut(C.Structure):
+    _fields_ = [("person_match", u8p), ("row_bits", u8p), ("dot_hd", u16p), ("dot_ml", u16p),
+                ("rs_hd", u16p), ("rs_ml", u16p), ("ml32", u32p), ("diff", u32p), ("msb", u8p),
+                ("stream_pos", u64p), ("stats", C.POINTER(OrcStats))]
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle`")
+        L = C.CDLL(LIB_PATH)
+        L.orc_chacha_block.argtypes = [u8p, C.c_uint64, C.c_uint64, u32p]
+        L.orc_seed_from_u64.argtypes = [C.c_uint64, u8p]
+        L.orc_derive.argtypes = [u8p, C.c_uint64, u8p]
+        L.orc_stream_at.argtypes = [u8p, C.c_uint64, C.c_uint64]
+        L.orc_stream_at.restype = C.c_uint64
+        L.orc_party_seeds.argtypes = [C.c_uint64, u8p]
+        L.orc_rng_new.argtypes = [C.c_uint64]
+        L.orc_rng_new.restype = C.c_void_p
+        L.orc_rng_sub.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_rng_sub.restype = C.c_void_p
+        L.orc_rng_free.argtypes = [C.c_void_p]
+        L.orc_rng_next.argtypes = [C.c_void_p]
+        L.orc_rng_next.restype = C.c_uint64
+        L.orc_rng_below.argtypes = [C.c_void_p, C.c_uint64]
+        L.orc_rng_below.restype = C.c_uint64
+        L.orc_rng_record.argtypes = [C.c_void_p, C.c_uint32, C.c_double, u64p, u64p]
+        L.orc_lambda16.argtypes = [u16p]
+        L.orc_code_record_bytes.argtypes = [C.c_int, C.c_uint32]
+        L.orc_code_record_bytes.restype = C.c_size_t
+        L.orc_mask_record_bytes.argtypes = [C.c_int, C.c_uint32]
+        L.orc_mask_record_bytes.restype = C.c_size_t
+        L.orc_deal_payload.argtypes = [C.c_int, C.c_uint32, C.c_uint64, u64p, u64p, C.c_void_p,
+                                       u8p, u8p, u8p]
+        L.orc_lane_count.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_int]
+        L.orc_lane_count.restype = C.c_uint64
+        L.orc_query.argtypes = [C.POINTER(OrcConfig), u8p, u8p, u8p, u8p, C.c_uint64, u8p, u8p, u8p,
+                                C.c_uint32, C.c_int, u64p, C.POINTER(OrcOut)]
+        L.orc_run_local.argtypes = [C.POINTER(OrcConfig), C.c_uint64, C.c_uint64, u64p, u64p,
+                                    C.c_uint32, u64p, u64p, C.c_int, C.POINTER(OrcOut)]
+        L.orc_match_a.argtypes = [C.c_double]
+        L.orc_match_a.restype = C.c_uint32
+        L.orc_validate.argtypes = [C.POINTER(OrcConfig)]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise RuntimeError(f"{REF_PATH} missing: run `make -C oracle ref` where /root/reference exists")
+        R = C.CDLL(REF_PATH)
+        R.ref_chacha_block.argtypes = [u8p, C.c_uint64, C.c_uint64, u32p]
+        R.ref_seed_from_u64.argtypes = [C.c_uint64, u8p]
+        R.ref_party_seeds.argtypes = [C.c_uint64, u8p]
+        R.ref_rng_u64.argtypes = [C.c_uint64, C.c_uint64, u64p]
+        R.ref_random_records.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_double),
+                                         u64p, u64p]
+        R.ref_lambda16.argtypes = [u16p]
+        R.ref_deal.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p,
+                               u8p, u8p, u8p]
+        R.ref_deal.restype = C.c_uint64
+        R.ref_run_local.argtypes = [C.c_int, C.c_uint32, C.c_double, C.c_uint32, C.c_int, C.c_int,
+                                    C.c_uint64, C.c_uint64, u64p, u64p, C.c_uint32, u64p, u64p,
+                                    C.c_int, u8p, u8p, u64p, C.POINTER(C.c_double), u64p]
+        R.ref_dots_reshare.argtypes = [C.c_int, C.c_uint32, C.c_uint32, u8p, C.POINTER(u8p),
+                                       C.c_uint64, C.POINTER(u8p), C.c_uint32, C.c_int,
+                                       u16p, u16p, u16p, u16p]
+        R.ref_bench_prepare.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint32]
+        R.ref_bench_prepare.restype = C.c_void_p
+        R.ref_bench_step.argtypes = [C.c_void_p, u8p]
+        R.ref_bench_step.restype = C.c_double
+        R.ref_bench_free.argtypes = [C.c_void_p]
+        _ref = R
+    return _ref
+
+
+# ---------------------------------------------------------------- helpers
+
+def words(l: int) -> int:
+    return (l + 63) // 64
+
+
+def record_bytes(backend: int, l: int) -> int:
+    L = lib()
+    return int(L.orc_code_record_bytes(backend, l) + L.orc_mask_record_bytes(backend, l))
+
+
+def party_seeds(master: int) -> np.ndarray:
+    out = np.zeros(48, np.uint8)
+    lib().orc_party_seeds(master, _p(out, u8p))
+    return out
+
+
+def chacha_block(seed: np.ndarray, block: int, stream: int = 0) -> np.ndarray:
+    out = np.zeros(16, np.uint32)
+    lib().orc_chacha_block(_p(np.ascontiguousarray(seed, np.uint8), u8p), block, stream, _p(out, u32p))
+    return out
+
+
+def seed_from_u64(v: int) -> np.ndarray:
+    out = np.zeros(16, np.uint8)
+    lib().orc_seed_from_u64(v, _p(out, u8p))
+    return out
+
+
+def lambda16() -> np.ndarray:
+    out = np.zeros(6, np.uint16)
+    lib().orc_lambda16(_p(out, u16p))
+    return out
+
+
+class Rng:
+    """Rng(seed) of prf.hpp:138 (stream of u64 draws) — C restatement."""
+
+    def __init__(self, seed: int | None = None, sub: tuple[int, int] | None = None):
+        L = lib()
+        self.h = L.orc_rng_sub(*sub) if sub is not None else L.orc_rng_new(seed)
+
+    def __del__(self):
+        try:
+            lib().orc_rng_free(self.h)
+        except Exception:
+            pass
+
+    def next(self) -> int:
+        return int(lib().orc_rng_next(self.h))
+
+    def below(self, bound: int) -> int:
+        return int(lib().orc_rng_below(self.h, bound))
+
+    def record(self, l: int, density: float):
+        c = np.zeros(words(l), np.uint64)
+        m = np.zeros(words(l), np.uint64)
+        lib().orc_rng_record(self.h, l, density, _p(c, u64p), _p(m, u64p))
+        return c, m
+
+
+def records(rng: Rng, l: int, n: int, density: float = 0.9):
+    codes = np.zeros((n, words(l)), np.uint64)
+    masks = np.zeros((n, words(l)), np.uint64)
+    for i in range(n):
+        codes[i], masks[i] = rng.record(l, density)
+    return codes, masks
+
+
+def deal(backend: int, l: int, codes: np.ndarray, masks: np.ndarray, rng: Rng):
+    """deal_db_payload / deal_query_payload -> three uint8 payloads."""
+    n = codes.shape[0]
+    rb = record_bytes(backend, l)
+    outs = [np.zeros(max(1, n * rb), np.uint8) for _ in range(3)]
+    lib().orc_deal_payload(backend, l, n, _p(np.ascontiguousarray(codes), u64p),
+                           _p(np.ascontiguousarray(masks), u64p), rng.h,
+                           *[_p(o, u8p) for o in outs])
+    return [o[: n * rb] for o in outs]
+
+
+@dataclass
+class QueryResult:
+    person_match: np.ndarray
+    row_bits: np.ndarray | None = None
+    dot_hd: np.ndarray | None = None
+    dot_ml: np.ndarray | None = None
+    rs_hd: np.ndarray | None = None
+    rs_ml: np.ndarray | None = None
+    ml32: np.ndarray | None = None
+    diff: np.ndarray | None = None
+    msb: np.ndarray | None = None
+    stream_pos: np.ndarray | None = None
+    stats: list | None = None
+
+
+def make_config(backend: int, l: int, ratio: float = 0.375, rotations: int = 31,
+                debug_rows: bool = False) -> OrcConfig:
+    L = lib()
+    return OrcConfig(backend, l, L.orc_match_a(ratio), 1 << 16, rotations, 1 if debug_rows else 0)
+
+
+def _alloc_out(n: int, ngroups: int, want_all: bool):
+    arrs = dict(person_match=np.zeros(max(1, ngroups), np.uint8), row_bits=np.zeros(max(1, n), np.uint8))
+    if want_all:
+        arrs.update(dot_hd=np.zeros(3 * max(1, n), np.uint16), dot_ml=np.zeros(3 * max(1, n), np.uint16),
+                    rs_hd=np.zeros(3 * max(1, n), np.uint16), rs_ml=np.zeros(3 * max(1, n), np.uint16),
+                    ml32=np.zeros(3 * max(1, n), np.uint32), diff=np.zeros(3 * max(1, n), np.uint32),
+                    msb=np.zeros(3 * max(1, n), np.uint8))
+    stats = (OrcStats * 3)()
+    pos = np.zeros(3, np.uint64)
+    out = OrcOut(_p(arrs["person_match"], u8p), _p(arrs["row_bits"], u8p),
+                 _p(arrs.get("dot_hd"), u16p), _p(arrs.get("dot_ml"), u16p),
+                 _p(arrs.get("rs_hd"), u16p), _p(arrs.get("rs_ml"), u16p),
+                 _p(arrs.get("ml32"), u32p), _p(arrs.get("diff"), u32p), _p(arrs.get("msb"), u8p),
+                 _p(pos, u64p), C.cast(stats, C.POINTER(OrcStats)))
+    return out, arrs, stats, pos
+
+
+def _finish(arrs, stats, pos, n, ngroups, want_all, debug_rows):
+    res = QueryResult(person_match=arrs["person_match"][:ngroups].copy())
+    if debug_rows:
+        res.row_bits = arrs["row_bits"][:n].copy()
+    if want_all:
+        for k, dt in (("dot_hd", None), ("dot_ml", None), ("rs_hd", None), ("rs_ml", None),
+                      ("ml32", None), ("diff", None), ("msb", None)):
+            setattr(res, k, arrs[k][: 3 * n].reshape(3, n).copy())
+    res.stream_pos = pos.copy()
+    res.stats = [{f: getattr(stats[p], f) for f, _ in OrcStats._fields_} for p in range(3)]
+    return res
+
+
+def query(cfg: OrcConfig, seeds: np.ndarray, db: list, s: int, q: list, persons: int,
+          membership: bool = False, want_all: bool = False, stream_start=None) -> QueryResult:
+    L = lib()
+    n = int(L.orc_lane_count(persons, s, cfg.rotations, 1 if membership else 0))
+    ngroups = 1 if membership else persons
+    out, arrs, stats, pos = _alloc_out(n, ngroups, want_all)
+    ss = None if stream_start is None else np.ascontiguousarray(stream_start, np.uint64)
+    dbb = [np.ascontiguousarray(x, np.uint8) if len(x) else np.zeros(1, np.uint8) for x in db]
+    qb = [np.ascontiguousarray(x, np.uint8) for x in q]
+    rc = L.orc_query(C.byref(cfg), _p(np.ascontiguousarray(seeds, np.uint8), u8p),
+                     *[_p(x, u8p) for x in dbb], s, *[_p(x, u8p) for x in qb], persons,
+                     1 if membership else 0, _p(ss, u64p), C.byref(out))
+    if rc:
+        raise RuntimeError(f"orc_query failed with status {rc}")
+    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows)
+
+
+def run_local(cfg: OrcConfig, seed: int, db_codes, db_masks, q_codes, q_masks, persons: int,
+              membership: bool = False, want_all: bool = False) -> QueryResult:
+    L = lib()
+    s = db_codes.shape[0]
+    n = int(L.orc_lane_count(persons, s, cfg.rotations, 1 if membership else 0))
+    ngroups = 1 if membership else persons
+    out, arrs, stats, pos = _alloc_out(n, ngroups, want_all)
+    dc = np.ascontiguousarray(db_codes if s else np.zeros((1, words(cfg.l)), np.uint64))
+    dm = np.ascontiguousarray(db_masks if s else np.zeros((1, words(cfg.l)), np.uint64))
+    rc = L.orc_run_local(C.byref(cfg), seed, s, _p(dc, u64p), _p(dm, u64p), persons,
+                         _p(np.ascontiguousarray(q_codes), u64p), _p(np.ascontiguousarray(q_masks), u64p),
+                         1 if membership else 0, C.byref(out))
+    if rc:
+        raise RuntimeError(f"orc_run_local failed with status {rc}")
+    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows)
+
+
+# ------------------------------------------------------- the reference (_ref)
+
+def ref_run_local(backend: int, l: int, ratio: float, rotations: int, seed: int, db_codes, db_masks,
+                  q_codes, q_masks, persons: int, membership: bool = False, debug_rows: bool = False,
+                  parallel_dot: bool = True):
+    R = ref()
+    s = db_codes.shape[0]
+    n = int(lib().orc_lane_count(persons, s, rotations, 1 if membership else 0))
+    ngroups = 1 if membership else persons
+    pm = np.zeros(max(1, ngroups), np.uint8)
+    rb = np.zeros(max(1, n), np.uint8)
+    st = np.zeros(24, np.uint64)
+    wall = C.c_double(0)
+    lanes = C.c_uint64(0)
+    dc = np.ascontiguousarray(db_codes if s else np.zeros((1, words(l)), np.uint64))
+    dm = np.ascontiguousarray(db_masks if s else np.zeros((1, words(l)), np.uint64))
+    rc = R.ref_run_local(backend, l, ratio, rotations, 1 if debug_rows else 0, 1 if parallel_dot else 0,
+                         seed, s, _p(dc, u64p), _p(dm, u64p), persons,
+                         _p(np.ascontiguousarray(q_codes), u64p), _p(np.ascontiguousarray(q_masks), u64p),
+                         1 if membership else 0, _p(pm, u8p), _p(rb, u8p), _p(st, u64p),
+                         C.byref(wall), C.byref(lanes))
+    if rc:
+        raise RuntimeError(f"ref_run_local failed with status {rc}")
+    keys = ["dot_bytes", "lift_bytes", "msb_bytes", "or_tree_bytes",
+            "dot_rounds", "lift_rounds", "msb_rounds", "or_tree_rounds"]
+    stats = [{k: int(st[8 * p + i]) for i, k in enumerate(keys)} for p in range(3)]
+    return dict(person_match=pm[:ngroups].copy(), row_bits=rb[:n].copy() if debug_rows else None,
+                stats=stats, wall_ms=wall.value, lanes=lanes.value)
+
+
+def ref_dots_reshare(backend: int, l: int, rotations: int, seeds, db: list, s: int, q: list,
+                     persons: int, membership: bool = False):
+    R = ref()
+    n = int(lib().orc_lane_count(persons, s, rotations, 1 if membership else 0))
+    outs = [np.zeros(3 * max(1, n), np.uint16) for _ in range(4)]
+    dbb = [np.ascontiguousarray(x, np.uint8) if len(x) else np.zeros(1, np.uint8) for x in db]
+    qb = [np.ascontiguousarray(x, np.uint8) for x in q]
+    dbp = (u8p * 3)(*[_p(x, u8p) for x in dbb])
+    qp = (u8p * 3)(*[_p(x, u8p) for x in qb])
+    rc = R.ref_dots_reshare(backend, l, rotations, _p(np.ascontiguousarray(seeds, np.uint8), u8p),
+                            dbp, s, qp, persons, 1 if membership else 0, *[_p(o, u16p) for o in outs])
+    if rc:
+        raise RuntimeError(f"ref_dots_reshare failed with status {rc}")
+    return [o[: 3 * n].reshape(3, n) for o in outs]

@@ -1,0 +1,164 @@
+/*
+ * irismpc_gpu.h — C-ABI of the B200-native irismpc hot path.
+ *
+ * Drop-in boundary for the reference's query path.  Each
+ * entry point replaces a reference interface, cited as
+ * /root/reference/proj/<file>:<line>:
+ *
+ *   irismpc_gpu_create         Session ctor + EngineConfig::validate
+ *                              (include/irismpc/engine.hpp:238, src/engine.cpp:21-34)
+ *                              + run_parties seed setup (include/irismpc/cluster.hpp:30-36)
+ *   irismpc_gpu_load_db        Session::load_db (engine.hpp:240, engine.cpp:136-193)
+ *   irismpc_gpu_batch_query    Session::batch_query / party_batch_query
+ *                              (engine.hpp:248, engine.hpp:311-313, engine.cpp:234-295,436-446)
+ *   irismpc_gpu_membership     Session::membership / party_membership
+ *                              (engine.hpp:243, engine.hpp:307-309, engine.cpp:221-232)
+ *   irismpc_gpu_record_bytes   code_record_bytes + mask_record_bytes (shares.hpp:135-136)
+ *   irismpc_gpu_seeds_from_master  deal_seeds(Rng(derive(seed_from_u64(seed),0x5eed)))
+ *                              (cluster.hpp:35-36, rep3.hpp:116-122)
+ *   irismpc_gpu_deal_*         deal_db_payload / deal_query_payload (shares.hpp:143-148),
+ *                              random_record (iris.hpp:294-296) — device dealer
+ *   irismpc_gpu_partial / irismpc_gpu_or_open
+ *                              multi-GPU split of the OR tree + open
+ *                              (circuits.hpp:387-486, engine.cpp:376-390)
+ *
+ * All three parties run inside one context on one GPU (their exchanges are
+ * device-local buffer reads); a context holds one DB shard.  Plain pointers
+ * and sizes only.  Return value: status code below (0 = ok).  Caller owns
+ * every output buffer; the library owns device memory.  One host thread per
+ * context.  Exceptions of the reference map to statuses as the reference CLI
+ * maps them to exit codes (tools/irismpc_cli.cpp:552-564).
+ */
+#ifndef IRISMPC_GPU_H
+#define IRISMPC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRISMPC_GPU_OK 0
+#define IRISMPC_GPU_ERR_GENERIC 1
+#define IRISMPC_GPU_ERR_CONFIG 2       /* Error / ConfigMismatchError (payload size, config) */
+#define IRISMPC_GPU_ERR_DEVICE 3       /* TransportError analogue: CUDA failure, no device */
+#define IRISMPC_GPU_ERR_BOUNDS 4       /* BoundsError (EngineConfig::validate) */
+#define IRISMPC_GPU_ERR_INCONSISTENT 5 /* InconsistentShareError (replication cross-check) */
+
+#define IRISMPC_GPU_BACKEND_REPLICATED 0
+#define IRISMPC_GPU_BACKEND_SHAMIR 1
+#define IRISMPC_GPU_VARIANT_MPC_LIFT 1 /* Variant::mpc_lift (shares.hpp:29) */
+
+typedef struct irismpc_gpu_ctx irismpc_gpu_ctx;
+
+/* EngineConfig (engine.hpp:33-44) + party seeds + shard placement. */
+typedef struct irismpc_gpu_config {
+  uint32_t backend;       /* IRISMPC_GPU_BACKEND_* */
+  uint32_t variant;       /* IRISMPC_GPU_VARIANT_MPC_LIFT */
+  uint32_t l;             /* code length (bits), multiple of 8 */
+  uint32_t a, b, m;       /* MatchParams integers (iris.hpp:157-174); b = 2^m, m = 16 */
+  uint32_t rotations;     /* odd */
+  uint32_t debug_rows;    /* open per-lane bits to P1 (engine.cpp:371-374) */
+  uint8_t seeds[48];      /* seed_1 | seed_2 | seed_3 (16 bytes each) */
+  int32_t device;         /* CUDA device ordinal */
+  uint32_t shard_rank;    /* this context's shard (0 = holds the inner-batch pairs) */
+  uint64_t db_rows_total; /* s of the whole DB across shards (0: = local s) */
+  uint64_t db_row_offset; /* first global DB row held by this context */
+  uint64_t reserved[4];
+} irismpc_gpu_config;
+
+/* QueryStats (engine.hpp:46-56) for each party, plus device phase timings. */
+typedef struct irismpc_gpu_stats {
+  uint64_t s, l, batch, lanes;
+  uint64_t dot_bytes[3], lift_bytes[3], msb_bytes[3], or_tree_bytes[3];
+  uint64_t dot_rounds, lift_rounds, msb_rounds, or_tree_rounds;
+  double wall_ms;      /* device time of the whole query (CUDA events) */
+  double prep_ms, gemm_ms, threshold_ms, or_ms;
+  uint64_t gemm_launches, kernel_launches;
+} irismpc_gpu_stats;
+
+/* ---- setup ------------------------------------------------------------ */
+int irismpc_gpu_seeds_from_master(uint64_t master, uint8_t out[48]);
+size_t irismpc_gpu_record_bytes(uint32_t backend, uint32_t variant, uint32_t l);
+uint64_t irismpc_gpu_lane_count(uint32_t persons, uint64_t s, uint32_t rotations, int membership);
+
+int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out);
+void irismpc_gpu_destroy(irismpc_gpu_ctx* ctx);
+const char* irismpc_gpu_last_error(const irismpc_gpu_ctx* ctx);
+/* Opaque cudaStream_t the context launches on (for caller-side events). */
+void* irismpc_gpu_stream(irismpc_gpu_ctx* ctx);
+
+/* ---- DB ---------------------------------------------------------------- */
+/* payload[p]: party p+1's IRS1 row stream, len[p] == s * record_bytes. */
+int irismpc_gpu_load_db(irismpc_gpu_ctx* ctx, const uint8_t* const payload[3],
+                        const size_t len[3], uint64_t s);
+/* Same, payloads already in device memory. */
+int irismpc_gpu_load_db_device(irismpc_gpu_ctx* ctx, const uint8_t* const dpayload[3],
+                               const size_t len[3], uint64_t s);
+
+/* ---- queries ------------------------------------------------------------ */
+/* q[p]: party p+1's query payload (2*persons code records).  person_match_out
+ * [persons] receives the bits opened at P1; row_bits_out [lanes] (may be NULL)
+ * receives the debug_rows opening.  stats may be NULL. */
+int irismpc_gpu_batch_query(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
+                            uint32_t persons, uint8_t* person_match_out, uint8_t* row_bits_out,
+                            irismpc_gpu_stats* stats);
+/* Same with device-resident query payloads; outputs still host pointers. */
+int irismpc_gpu_batch_query_device(irismpc_gpu_ctx* ctx, const uint8_t* const dq[3],
+                                   const size_t qlen[3], uint32_t persons,
+                                   uint8_t* person_match_out, uint8_t* row_bits_out,
+                                   irismpc_gpu_stats* stats);
+/* Single code, no rotation, one group (Session::membership). */
+int irismpc_gpu_membership(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
+                           uint8_t* match_out, uint8_t* row_bits_out, irismpc_gpu_stats* stats);
+
+/* Multi-GPU: run the query on this shard but stop before the final OR/open.
+ * partial_out_dev: DEVICE buffer [3][persons] bytes — bit 0 of each byte is one
+ * XOR component of the shard's per-person aggregate (never opened). */
+int irismpc_gpu_batch_query_partial(irismpc_gpu_ctx* ctx, const uint8_t* const dq[3],
+                                    const size_t qlen[3], uint32_t persons,
+                                    uint8_t* partial_out_dev, irismpc_gpu_stats* stats);
+/* MPC-OR of G gathered shard partials (DEVICE [G][3][persons]) and the open
+ * at P1 into host person_match_out[persons]. */
+int irismpc_gpu_or_open(irismpc_gpu_ctx* ctx, const uint8_t* partials_dev, uint32_t G,
+                        uint32_t persons, uint8_t* person_match_out);
+
+/* PRF stream positions (per seed); a fresh context starts at 0 like
+ * run_parties; the reference CLI keeps PartyCtx across queries. */
+int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* ctx, uint64_t pos[3]);
+int irismpc_gpu_set_stream_positions(irismpc_gpu_ctx* ctx, const uint64_t pos[3]);
+
+/* ---- device dealer (bit-compatible with the reference Rng streams) ------- */
+/* `count` records random_record(l, Rng(rng_seed), mask_density) starting at
+ * record index `first` of that stream (each record consumes 2l draws), into
+ * DEVICE code/mask word arrays [count][(l+63)/64]. */
+int irismpc_gpu_synth_records(irismpc_gpu_ctx* ctx, uint64_t rng_seed, uint64_t first,
+                              uint64_t count, double mask_density, uint64_t* codes_dev,
+                              uint64_t* masks_dev);
+/* deal_*_payload with Rng(derive(seed_from_u64(deal_seed), tag)) starting at
+ * record `first_record` of the dealing stream: DEVICE records -> DEVICE payloads. */
+int irismpc_gpu_deal_payload(irismpc_gpu_ctx* ctx, uint64_t deal_seed, uint64_t tag,
+                             uint64_t first_record, uint64_t nrec, const uint64_t* codes_dev,
+                             const uint64_t* masks_dev, uint8_t* const out_dev[3]);
+/* Synthetic DB straight into HBM: records [first, first+s) of Rng(rng_seed),
+ * dealt with (deal_seed, tag 1) from record `first`, loaded as this shard. */
+int irismpc_gpu_synth_db(irismpc_gpu_ctx* ctx, uint64_t s, uint64_t rng_seed, uint64_t first,
+                         double mask_density, uint64_t deal_seed);
+
+/* ---- debug / parity taps (tests) ------------------------------------------ */
+#define IRISMPC_GPU_TAP_DOT_HD 1  /* uint16 [3][n] per-party additive hd dot (L1) */
+#define IRISMPC_GPU_TAP_DOT_ML 2
+#define IRISMPC_GPU_TAP_RS_HD 3   /* uint16 [3][n] components after reshare (L2) */
+#define IRISMPC_GPU_TAP_RS_ML 4
+#define IRISMPC_GPU_TAP_ML32 5    /* uint32 [3][n] lift output components */
+#define IRISMPC_GPU_TAP_DIFF 6    /* uint32 [3][n] a*ml32 - b*hd components */
+#define IRISMPC_GPU_TAP_MSB 7     /* uint8  [3][n] match bit components */
+/* Enable capture of all taps for the next query (costly; tests only). */
+int irismpc_gpu_enable_taps(irismpc_gpu_ctx* ctx, int enable);
+int irismpc_gpu_read_tap(irismpc_gpu_ctx* ctx, int tap, void* host_out, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IRISMPC_GPU_H */

@@ -1,0 +1,364 @@
+"""B200-native irismpc hot path: Python mirror of the reference query API.
+
+The product is ``libirismpc_gpu.so`` (hand-written sm_100a CUDA behind the
+C-ABI in ``include/irismpc_gpu.h``).  This module is a thin ctypes layer with
+the reference's names and error behaviour:
+
+* ``EngineConfig``          — irismpc::EngineConfig (engine.hpp:33-44)
+* ``Session``               — Session::load_db / batch_query / membership
+                              (engine.hpp:225-275), all three parties in one GPU
+* ``run_batch_local`` / ``run_membership_local`` — cluster.hpp:82-87
+* ``BoundsError`` / ``ConfigError`` / ``DeviceError`` / ``InconsistentShareError``
+  — errors.hpp:22-50 mapped from the C-ABI status codes
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call raises ``DeviceError`` unless the CUDA library loads and a B200 is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libirismpc_gpu.so")
+
+REPLICATED, SHAMIR = 0, 1
+MPC_LIFT = 1
+
+TAP_DOT_HD, TAP_DOT_ML, TAP_RS_HD, TAP_RS_ML, TAP_ML32, TAP_DIFF, TAP_MSB = range(1, 8)
+
+EXPORTED = [
+    "irismpc_gpu_seeds_from_master", "irismpc_gpu_record_bytes", "irismpc_gpu_lane_count",
+    "irismpc_gpu_create", "irismpc_gpu_destroy", "irismpc_gpu_last_error", "irismpc_gpu_stream",
+    "irismpc_gpu_load_db", "irismpc_gpu_load_db_device", "irismpc_gpu_batch_query",
+    "irismpc_gpu_batch_query_device", "irismpc_gpu_membership", "irismpc_gpu_batch_query_partial",
+    "irismpc_gpu_or_open", "irismpc_gpu_get_stream_positions", "irismpc_gpu_set_stream_positions",
+    "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
+    "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap",
+]
+
+
+class IrisError(RuntimeError):
+    code = 1
+
+
+class ConfigError(IrisError):
+    """irismpc::Error / ConfigMismatchError (payload size, unsupported config)."""
+    code = 2
+
+
+class DeviceError(IrisError):
+    """TransportError analogue: CUDA failure or no B200."""
+    code = 3
+
+
+class BoundsError(IrisError):
+    """irismpc::BoundsError (EngineConfig::validate)."""
+    code = 4
+
+
+class InconsistentShareError(IrisError):
+    """irismpc::InconsistentShareError (replication cross-check)."""
+    code = 5
+
+
+_ERRORS = {c.code: c for c in (IrisError, ConfigError, DeviceError, BoundsError, InconsistentShareError)}
+
+
+class _Config(C.Structure):
+    _fields_ = [("backend", C.c_uint32), ("variant", C.c_uint32), ("l", C.c_uint32), ("a", C.c_uint32),
+                ("b", C.c_uint32), ("m", C.c_uint32), ("rotations", C.c_uint32), ("debug_rows", C.c_uint32),
+                ("seeds", C.c_uint8 * 48), ("device", C.c_int32), ("shard_rank", C.c_uint32),
+                ("db_rows_total", C.c_uint64), ("db_row_offset", C.c_uint64), ("reserved", C.c_uint64 * 4)]
+
+
+class Stats(C.Structure):
+    """QueryStats (engine.hpp:46-56) per party + device phase times."""
+    _fields_ = [("s", C.c_uint64), ("l", C.c_uint64), ("batch", C.c_uint64), ("lanes", C.c_uint64),
+                ("dot_bytes", C.c_uint64 * 3), ("lift_bytes", C.c_uint64 * 3), ("msb_bytes", C.c_uint64 * 3),
+                ("or_tree_bytes", C.c_uint64 * 3), ("dot_rounds", C.c_uint64), ("lift_rounds", C.c_uint64),
+                ("msb_rounds", C.c_uint64), ("or_tree_rounds", C.c_uint64), ("wall_ms", C.c_double),
+                ("prep_ms", C.c_double), ("gemm_ms", C.c_double), ("threshold_ms", C.c_double),
+                ("or_ms", C.c_double), ("gemm_launches", C.c_uint64), ("kernel_launches", C.c_uint64)]
+
+    def party(self, p: int) -> dict:
+        return dict(dot_bytes=self.dot_bytes[p], lift_bytes=self.lift_bytes[p], msb_bytes=self.msb_bytes[p],
+                    or_tree_bytes=self.or_tree_bytes[p], dot_rounds=self.dot_rounds,
+                    lift_rounds=self.lift_rounds, msb_rounds=self.msb_rounds, or_tree_rounds=self.or_tree_rounds)
+
+
+_lib = None
+vp = C.c_void_p
+u8p = C.POINTER(C.c_uint8)
+u64p = C.POINTER(C.c_uint64)
+szp = C.POINTER(C.c_size_t)
+
+
+def lib() -> C.CDLL:
+    """Loads the CUDA library; raises DeviceError if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} is missing: run `python -m paper_2405_04463_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.irismpc_gpu_seeds_from_master.argtypes = [C.c_uint64, u8p]
+        L.irismpc_gpu_record_bytes.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+        L.irismpc_gpu_record_bytes.restype = C.c_size_t
+        L.irismpc_gpu_lane_count.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_int]
+        L.irismpc_gpu_lane_count.restype = C.c_uint64
+        L.irismpc_gpu_create.argtypes = [C.POINTER(_Config), C.POINTER(vp)]
+        L.irismpc_gpu_destroy.argtypes = [vp]
+        L.irismpc_gpu_last_error.argtypes = [vp]
+        L.irismpc_gpu_last_error.restype = C.c_char_p
+        L.irismpc_gpu_stream.argtypes = [vp]
+        L.irismpc_gpu_stream.restype = vp
+        P3 = vp * 3
+        S3 = C.c_size_t * 3
+        for f in ("irismpc_gpu_load_db", "irismpc_gpu_load_db_device"):
+            getattr(L, f).argtypes = [vp, P3, S3, C.c_uint64]
+        for f in ("irismpc_gpu_batch_query", "irismpc_gpu_batch_query_device"):
+            getattr(L, f).argtypes = [vp, P3, S3, C.c_uint32, vp, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_membership.argtypes = [vp, P3, S3, vp, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_batch_query_partial.argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_or_open.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp]
+        L.irismpc_gpu_get_stream_positions.argtypes = [vp, u64p]
+        L.irismpc_gpu_set_stream_positions.argtypes = [vp, u64p]
+        L.irismpc_gpu_synth_records.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, vp, vp]
+        L.irismpc_gpu_deal_payload.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp, P3]
+        L.irismpc_gpu_synth_db.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64]
+        L.irismpc_gpu_enable_taps.argtypes = [vp, C.c_int]
+        L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
+        _lib = L
+    return _lib
+
+
+def seeds_from_master(seed: int) -> np.ndarray:
+    out = np.zeros(48, np.uint8)
+    lib().irismpc_gpu_seeds_from_master(seed, out.ctypes.data_as(u8p))
+    return out
+
+
+def record_bytes(backend: int, l: int) -> int:
+    return int(lib().irismpc_gpu_record_bytes(backend, MPC_LIFT, l))
+
+
+def lane_count(persons: int, s: int, rotations: int, membership: bool = False) -> int:
+    return int(lib().irismpc_gpu_lane_count(persons, s, rotations, 1 if membership else 0))
+
+
+def match_a(ratio: float) -> int:
+    """MatchParams::make(ratio, 16).a (iris.hpp:163-174)."""
+    b = 1 << 16
+    x = (1.0 - 2.0 * ratio) * b  # llround: halves away from zero
+    a = int(np.floor(x + 0.5)) if x >= 0 else -int(np.floor(-x + 0.5))
+    return min(a, b)
+
+
+@dataclass
+class EngineConfig:
+    """irismpc::EngineConfig (engine.hpp:33-44), mpc-lift variant."""
+    backend: int = SHAMIR
+    l: int = 12800
+    match_ratio: float = 0.375
+    rotations: int = 31
+    debug_rows: bool = False
+    variant: int = MPC_LIFT
+    m: int = 16
+    a: int | None = None
+    b: int = 1 << 16
+
+    def params(self) -> tuple[int, int]:
+        return (self.a if self.a is not None else match_a(self.match_ratio)), self.b
+
+
+def _ptr(x) -> int:
+    """Data pointer of a numpy array or torch tensor."""
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    return int(x.ctypes.data)
+
+
+def _nbytes(x) -> int:
+    if hasattr(x, "element_size"):
+        return int(x.numel() * x.element_size())
+    return int(x.nbytes)
+
+
+class Session:
+    """All three parties of one DB shard on one GPU (Session<B,16,16>)."""
+
+    def __init__(self, cfg: EngineConfig, seeds: np.ndarray | None = None, master_seed: int | None = None,
+                 device: int = 0, shard_rank: int = 0, db_rows_total: int = 0, db_row_offset: int = 0):
+        L = lib()
+        self.cfg = cfg
+        a, b = cfg.params()
+        c = _Config()
+        c.backend, c.variant, c.l, c.a, c.b, c.m = cfg.backend, cfg.variant, cfg.l, a, b, cfg.m
+        c.rotations, c.debug_rows = cfg.rotations, 1 if cfg.debug_rows else 0
+        if seeds is None:
+            seeds = seeds_from_master(master_seed if master_seed is not None else 0)
+        for i in range(48):
+            c.seeds[i] = int(seeds[i])
+        c.device, c.shard_rank, c.db_rows_total, c.db_row_offset = device, shard_rank, db_rows_total, db_row_offset
+        h = vp()
+        rc = L.irismpc_gpu_create(C.byref(c), C.byref(h))
+        if rc:
+            raise _ERRORS.get(rc, IrisError)(f"irismpc_gpu_create failed ({rc})")
+        self._h = h
+        self.s = 0
+        self.rec = record_bytes(cfg.backend, cfg.l)
+        self.last_stats = Stats()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().irismpc_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc: int):
+        if rc:
+            msg = lib().irismpc_gpu_last_error(self._h).decode()
+            raise _ERRORS.get(rc, IrisError)(msg)
+
+    @property
+    def stream(self) -> int:
+        return int(lib().irismpc_gpu_stream(self._h) or 0)
+
+    # -- DB ---------------------------------------------------------------
+    def load_db(self, payloads, s: int):
+        """Session::load_db: three host payloads (bytes/np.uint8) or device tensors."""
+        dev = hasattr(payloads[0], "is_cuda") and payloads[0].is_cuda
+        arrs = [p if hasattr(p, "data_ptr") else np.ascontiguousarray(np.frombuffer(p, np.uint8) if isinstance(p, (bytes, bytearray)) else p)
+                for p in payloads]
+        ptrs = (vp * 3)(*[_ptr(a) for a in arrs])
+        lens = (C.c_size_t * 3)(*[_nbytes(a) for a in arrs])
+        f = lib().irismpc_gpu_load_db_device if dev else lib().irismpc_gpu_load_db
+        self._check(f(self._h, ptrs, lens, s))
+        self.s = s
+
+    def synth_db(self, s: int, rng_seed: int = 2, first: int = 0, mask_density: float = 0.9, deal_seed: int = 7):
+        """Device dealer: rows [first, first+s) of Rng(rng_seed) random_record, dealt with sub_rng(deal_seed,1)."""
+        self._check(lib().irismpc_gpu_synth_db(self._h, s, rng_seed, first, mask_density, deal_seed))
+        self.s = s
+
+    def synth_records(self, rng_seed: int, first: int, count: int, mask_density: float, codes, masks):
+        self._check(lib().irismpc_gpu_synth_records(self._h, rng_seed, first, count, mask_density,
+                                                    _ptr(codes), _ptr(masks)))
+
+    def deal_payload(self, deal_seed: int, tag: int, first_record: int, codes, masks, outs):
+        nrec = codes.shape[0]
+        ptrs = (vp * 3)(*[_ptr(o) for o in outs])
+        self._check(lib().irismpc_gpu_deal_payload(self._h, deal_seed, tag, first_record, nrec, _ptr(codes),
+                                                   _ptr(masks), ptrs))
+
+    # -- queries ------------------------------------------------------------
+    def _q(self, q):
+        dev = hasattr(q[0], "is_cuda") and q[0].is_cuda
+        arrs = [x if hasattr(x, "data_ptr") else np.ascontiguousarray(x, np.uint8) for x in q]
+        return dev, arrs, (vp * 3)(*[_ptr(a) for a in arrs]), (C.c_size_t * 3)(*[_nbytes(a) for a in arrs])
+
+    def batch_query(self, q, persons: int, want_rows: bool = False) -> np.ndarray:
+        """Session::batch_query: q = three payloads of 2*persons codes; returns person_match at P1."""
+        dev, arrs, ptrs, lens = self._q(q)
+        out = np.zeros(max(1, persons), np.uint8)
+        rows = np.zeros(max(1, lane_count(persons, self.s, self.cfg.rotations)), np.uint8) if want_rows else None
+        f = lib().irismpc_gpu_batch_query_device if dev else lib().irismpc_gpu_batch_query
+        self._check(f(self._h, ptrs, lens, persons, out.ctypes.data, rows.ctypes.data if want_rows else None,
+                      C.byref(self.last_stats)))
+        self.row_bits = rows
+        return out[:persons]
+
+    def membership(self, q, want_rows: bool = False) -> bool:
+        """Session::membership: one code, no rotation."""
+        dev, arrs, ptrs, lens = self._q(q)
+        if dev:
+            arrs = [a.cpu().numpy() for a in arrs]
+            ptrs = (vp * 3)(*[_ptr(a) for a in arrs])
+        out = np.zeros(1, np.uint8)
+        rows = np.zeros(max(1, self.s), np.uint8) if want_rows else None
+        self._check(lib().irismpc_gpu_membership(self._h, ptrs, lens, out.ctypes.data,
+                                                 rows.ctypes.data if want_rows else None,
+                                                 C.byref(self.last_stats)))
+        self.row_bits = rows
+        return bool(out[0])
+
+    def batch_query_partial(self, q, persons: int, partial_out):
+        """Shard query up to the per-person shared aggregate (device [3][persons] bytes, unopened)."""
+        dev, arrs, ptrs, lens = self._q(q)
+        if not dev:
+            raise ConfigError("batch_query_partial expects device-resident payloads")
+        self._check(lib().irismpc_gpu_batch_query_partial(self._h, ptrs, lens, persons, _ptr(partial_out),
+                                                          C.byref(self.last_stats)))
+
+    def or_open(self, partials, G: int, persons: int) -> np.ndarray:
+        out = np.zeros(max(1, persons), np.uint8)
+        self._check(lib().irismpc_gpu_or_open(self._h, _ptr(partials), G, persons, out.ctypes.data))
+        return out[:persons]
+
+    # -- streams / taps --------------------------------------------------------
+    def stream_positions(self) -> np.ndarray:
+        p = np.zeros(3, np.uint64)
+        self._check(lib().irismpc_gpu_get_stream_positions(self._h, p.ctypes.data_as(u64p)))
+        return p
+
+    def set_stream_positions(self, pos):
+        p = np.ascontiguousarray(pos, np.uint64)
+        self._check(lib().irismpc_gpu_set_stream_positions(self._h, p.ctypes.data_as(u64p)))
+
+    def enable_taps(self, on: bool = True):
+        self._check(lib().irismpc_gpu_enable_taps(self._h, 1 if on else 0))
+
+    def read_tap(self, tap: int, n: int) -> np.ndarray:
+        dt = {TAP_DOT_HD: np.uint16, TAP_DOT_ML: np.uint16, TAP_RS_HD: np.uint16, TAP_RS_ML: np.uint16,
+              TAP_ML32: np.uint32, TAP_DIFF: np.uint32, TAP_MSB: np.uint8}[tap]
+        out = np.zeros(3 * n, dt)
+        self._check(lib().irismpc_gpu_read_tap(self._h, tap, out.ctypes.data, out.nbytes))
+        return out.reshape(3, n)
+
+
+def _dealt_on_device(sess: Session, codes: np.ndarray, masks: np.ndarray, seed: int, tag: int):
+    import torch
+    dc = torch.from_numpy(np.ascontiguousarray(codes).view(np.int64)).cuda()
+    dm = torch.from_numpy(np.ascontiguousarray(masks).view(np.int64)).cuda()
+    n = codes.shape[0]
+    outs = [torch.empty(max(1, n * sess.rec), dtype=torch.uint8, device="cuda") for _ in range(3)]
+    if n:
+        sess.deal_payload(seed, tag, 0, dc, dm, outs)
+    return [o[: n * sess.rec] for o in outs]
+
+
+def run_batch_local(cfg: EngineConfig, q_codes: np.ndarray, q_masks: np.ndarray, db_codes: np.ndarray,
+                    db_masks: np.ndarray, seed: int, persons: int | None = None, membership: bool = False,
+                    want_rows: bool = False, taps: bool = False, device: int = 0):
+    """run_batch_local / run_membership_local (cluster.cpp:30-79) on one B200.
+
+    Deals the DB with sub_rng(seed,1) and the queries with sub_rng(seed,2) on the
+    device (bit-identical payloads to the reference dealer), party seeds from
+    `seed`.  Returns (person_match, session)."""
+    sess = Session(cfg, master_seed=seed, device=device)
+    s = db_codes.shape[0]
+    db = _dealt_on_device(sess, db_codes, db_masks, seed, 1)
+    sess.load_db(db, s)
+    q = _dealt_on_device(sess, q_codes, q_masks, seed, 2)
+    if taps:
+        sess.enable_taps(True)
+    if membership:
+        m = np.array([sess.membership(q, want_rows)], np.uint8)
+    else:
+        m = sess.batch_query(q, persons if persons is not None else q_codes.shape[0] // 2, want_rows)
+    return m, sess

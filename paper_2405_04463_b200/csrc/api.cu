@@ -1,0 +1,872 @@
+// C-ABI of the B200 irismpc hot path (include/irismpc_gpu.h).
+//
+// One context = the three parties of one DB shard on one GPU.  A query runs
+//   K1 parse/rotate query -> (pairs) -> per column chunk: K2 limb GEMM ->
+//   K4 threshold (+ fused first OR level) -> K5 per-person OR -> open at P1
+// on a single CUDA stream.  Mirrors Session::load_db / batch_query /
+// membership (/root/reference/proj/src/engine.cpp:136-398).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/irismpc_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace irisgpu;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return -1;
+    cap = bytes ? bytes : 16;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+
+// ---- host-side ChaCha / seeds / lambda (setup only) ------------------------
+void host_block(const uint8_t seed[16], uint64_t block, uint64_t stream, uint32_t out[16]) {
+  SeedKey k;
+  std::memcpy(k.k, seed, 16);
+  chacha12_block(k, block, stream, out);
+}
+void host_derive(const uint8_t parent[16], uint64_t tag, uint8_t out[16]) {
+  uint32_t blk[16];
+  host_block(parent, tag, 0xD5A1u, blk);  // CtrPrf::derive (prf.hpp:106-112)
+  std::memcpy(out, blk, 16);
+}
+void host_seed_from_u64(uint64_t v, uint8_t out[16]) {
+  uint8_t s[16] = {0};
+  std::memcpy(s, &v, 8);
+  host_derive(s, 0, out);
+}
+SeedKey key_of(const uint8_t* seed) {
+  SeedKey k;
+  std::memcpy(k.k, seed, 16);
+  return k;
+}
+
+// party_lagrange_at_zero<16> over {1, X, 1+X} (galois.hpp:66-128)
+struct Gr {
+  uint32_t c0, c1;
+};
+Gr gmul(Gr a, Gr b) {
+  return {(a.c0 * b.c0 + a.c1 * b.c1) & 0xFFFF, (a.c0 * b.c1 + a.c1 * b.c0 + a.c1 * b.c1) & 0xFFFF};
+}
+Gr gsub(Gr a, Gr b) { return {(a.c0 - b.c0) & 0xFFFF, (a.c1 - b.c1) & 0xFFFF}; }
+Gr ginv(Gr a) {
+  Gr y = (a.c1 & 1) == 0 ? Gr{1, 0} : ((a.c0 & 1) == 0 ? Gr{1, 1} : Gr{0, 1});
+  for (unsigned c = 1; c < 16; c *= 2) y = gmul(y, gsub(Gr{2, 0}, gmul(a, y)));
+  return y;
+}
+void lambdas(uint16_t out[6]) {
+  const Gr xs[3] = {{1, 0}, {0, 1}, {1, 1}};
+  for (int i = 0; i < 3; ++i) {
+    Gr num{1, 0}, den{1, 0};
+    for (int j = 0; j < 3; ++j) {
+      if (j == i) continue;
+      num = gmul(num, xs[j]);
+      den = gmul(den, gsub(xs[j], xs[i]));
+    }
+    const Gr l = gmul(num, ginv(den));
+    out[2 * i] = (uint16_t)l.c0;
+    out[2 * i + 1] = (uint16_t)l.c1;
+  }
+}
+
+size_t record_bytes(uint32_t backend, uint32_t l) {
+  // code_record_bytes + mask_record_bytes for mpc-lift (shares.cpp:49-59)
+  return backend == IRISMPC_GPU_BACKEND_REPLICATED ? (size_t)l * 8 : (size_t)l * 4;
+}
+
+// Reference or_tree_batch zero_word draws for `groups` equal groups of `len`
+// lanes (circuits.hpp:394-427): keeps the seed streams in lockstep with the
+// reference across queries on a persistent context.
+uint64_t ref_or_draws(uint64_t groups, uint64_t len, uint64_t* rounds, uint64_t* bytes) {
+  uint64_t draws = 0, r = 0, b = 0;
+  while (len > 1) {
+    const uint64_t na = (len + 1) / 2, nb = len - na;
+    draws += groups * ceil_div(nb, 64);
+    b += groups * ceil_div(nb, 8);
+    len = na;
+    ++r;
+  }
+  if (rounds) *rounds = r;
+  if (bytes) *bytes = b;
+  return draws;
+}
+
+}  // namespace
+
+struct irismpc_gpu_ctx {
+  irismpc_gpu_config cfg{};
+  std::string err;
+  cudaStream_t st = nullptr;
+  int shamir = 0;
+  uint32_t l = 0, l_pad = 0, nseg = 1;
+  SeedKey keys[3];
+  // DB shard
+  uint64_t s = 0, s_pad = 0;
+  bool db_loaded = false;
+  Buf db_lo, db_hi;
+  CUtensorMap tA_lo, tA_hi;
+  // query scratch
+  Buf q_lo, q_hi, q_pa, q_pb, q_pay[3];
+  uint64_t q_rows_mapped = 0;
+  CUtensorMap tB_lo, tB_hi;
+  uint32_t ncols_pad_cur = 0;
+  Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
+  std::vector<Seg> h_segs;
+  Seg* h_segs_pinned = nullptr;
+  size_t h_segs_cap = 0;
+  // PRF stream state
+  uint64_t pos[3] = {0, 0, 0};
+  uint64_t query_id = 0;
+  // taps
+  bool taps = false;
+  Buf tap_buf[7];
+  uint64_t tap_n = 0;
+  cudaEvent_t ev[6];
+};
+
+namespace {
+
+int fail(irismpc_gpu_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(ctx, x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ctx, IRISMPC_GPU_ERR_DEVICE, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int validate(const irismpc_gpu_config* c, std::string* why) {
+  // EngineConfig::validate (engine.cpp:21-34) for the shared-mask variant
+  if (c->variant != IRISMPC_GPU_VARIANT_MPC_LIFT) {
+    *why = "only the mpc-lift variant is implemented on the GPU path";
+    return IRISMPC_GPU_ERR_CONFIG;
+  }
+  if (c->backend > 1) {
+    *why = "unknown backend";
+    return IRISMPC_GPU_ERR_CONFIG;
+  }
+  if (c->l == 0 || c->l % 8 != 0) {
+    *why = "l must be a positive multiple of 8";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  if (c->a > c->b) {
+    *why = "threshold numerator exceeds denominator";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  if (c->m != 16 || c->b != (1u << 16)) {
+    *why = "shared-mask variants fix b = 2^16";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  const uint64_t t = 1ull << 32, bl = (uint64_t)c->b * c->l;
+  if (!(bl < t / 4 && bl < t - (t >> 1))) {
+    *why = "comparison ring too small for b*l (shared masks)";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  if (c->rotations % 2 == 0) {
+    *why = "rotations must be odd";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  if (c->backend == IRISMPC_GPU_BACKEND_SHAMIR && c->rotations > 1 && (c->l / 64) % 2 != 0) {
+    *why = "shamir packing needs an even rotation stride (l/64)";
+    return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  return 0;
+}
+
+uint64_t s_total(const irismpc_gpu_ctx* c) {
+  return c->cfg.db_rows_total ? c->cfg.db_rows_total : c->s;
+}
+
+int alloc_planes(irismpc_gpu_ctx* c, uint64_t s) {
+  c->db_lo.release();
+  c->db_hi.release();
+  c->db_loaded = false;
+  c->s = s;
+  c->s_pad = round_up(s ? s : 1, kGemmBM);
+  const size_t bytes = 6ull * c->s_pad * c->l_pad;
+  if (c->db_lo.ensure(bytes) || c->db_hi.ensure(bytes))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for the DB planes");
+  CK(c, cudaMemsetAsync(c->db_lo.p, 0, bytes, c->st));
+  CK(c, cudaMemsetAsync(c->db_hi.p, 0, bytes, c->st));
+  if (make_plane_tmap(&c->tA_lo, c->db_lo.p, 6ull * c->s_pad, c->l_pad, kGemmBM) ||
+      make_plane_tmap(&c->tA_hi, c->db_hi.p, 6ull * c->s_pad, c->l_pad, kGemmBM))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the DB planes");
+  return 0;
+}
+
+// parse `rows` rows (device payloads) into planes at row0
+int parse_rows(irismpc_gpu_ctx* c, const uint8_t* const dp[3], uint64_t rows, uint64_t row0, Buf* bad) {
+  if (!c->shamir) {
+    if (bad) launch_check_rep(dp[0], dp[1], dp[2], rows * record_bytes(0, c->l), bad->as<int>(), c->st);
+  }
+  for (int p = 0; p < 3; ++p)
+    launch_parse_db(dp[p], rows, row0, c->l, c->l_pad, c->s_pad, p, c->shamir, c->db_lo.as<uint8_t>(),
+                    c->db_hi.as<uint8_t>(), c->st);
+  CK(c, cudaGetLastError());
+  return 0;
+}
+
+int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
+  if (bad) {
+    int h = 0;
+    CK(c, cudaMemcpyAsync(&h, bad->p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    if (h) return fail(c, IRISMPC_GPU_ERR_INCONSISTENT, "replicated share cross-check failed at load");
+  }
+  CK(c, cudaStreamSynchronize(c->st));
+  c->db_loaded = true;
+  return 0;
+}
+
+int ensure_query_buffers(irismpc_gpu_ctx* c, uint32_t ncodes, uint32_t ncols_pad) {
+  const size_t bplane = 6ull * c->nseg * ncols_pad * c->l_pad;
+  if (bplane > c->q_lo.cap || ncols_pad != c->ncols_pad_cur) {
+    if (c->q_lo.ensure(bplane) || c->q_hi.ensure(bplane))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query planes");
+    CK(c, cudaMemsetAsync(c->q_lo.p, 0, bplane, c->st));
+    CK(c, cudaMemsetAsync(c->q_hi.p, 0, bplane, c->st));
+    if (make_plane_tmap(&c->tB_lo, c->q_lo.p, 6ull * c->nseg * ncols_pad, c->l_pad, kGemmBN) ||
+        make_plane_tmap(&c->tB_hi, c->q_hi.p, 6ull * c->nseg * ncols_pad, c->l_pad, kGemmBN))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the query planes");
+    c->ncols_pad_cur = ncols_pad;
+  }
+  const size_t pinst = 6ull * ncodes * c->l * sizeof(uint16_t);
+  if (c->q_pa.ensure(pinst) || c->q_pb.ensure(pinst))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query instances");
+  return 0;
+}
+
+int ensure_host_segs(irismpc_gpu_ctx* c, size_t n) {
+  if (n <= c->h_segs_cap) return 0;
+  if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
+  c->h_segs_pinned = nullptr;
+  CK(c, cudaMallocHost(&c->h_segs_pinned, n * sizeof(Seg)));
+  c->h_segs_cap = n;
+  return 0;
+}
+
+// Core query on device payloads.  mode 0: final (open into match_out host),
+// 1: partial (component bits into partial_dev).
+int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3], uint32_t persons,
+              int membership, int mode, uint8_t* match_out, uint8_t* row_bits_out, uint8_t* partial_dev,
+              irismpc_gpu_stats* stats, bool host_input, const uint8_t* const hq[3]) {
+  if (!c->db_loaded) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no database loaded");
+  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const uint32_t ncodes = membership ? 1u : 2u * persons;
+  for (int p = 0; p < 3; ++p) {
+    if (qlen[p] % rec != 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "query payload size mismatch");
+    if (qlen[p] / rec != ncodes)
+      return fail(c, IRISMPC_GPU_ERR_CONFIG,
+                  membership ? "membership expects exactly one query code"
+                             : "batch query expects 2 codes per person");
+  }
+  const uint32_t r = membership ? 1u : c->cfg.rotations;
+  const uint64_t ncols = (uint64_t)ncodes * r;
+  const uint32_t ncols_pad = (uint32_t)round_up(ncols ? ncols : 1, kGemmBN);
+  const uint64_t S = s_total(c);
+  const bool rank0 = c->cfg.shard_rank == 0;
+  const uint64_t npairs_all = membership ? 0 : (uint64_t)persons * (persons ? persons - 1 : 0) / 2 * 4 * r;
+  const uint64_t npairs = rank0 ? npairs_all : 0;
+  const uint64_t n = ncols * S + npairs_all;  // global lane count (all shards)
+  const uint64_t W = ceil_div(n, 64);
+  const uint32_t ngroups = membership ? 1u : persons;
+  const uint64_t qid = c->query_id++;
+  const uint64_t rank = c->cfg.shard_rank;
+
+  cudaStream_t st = c->st;
+  CK(c, cudaEventRecord(c->ev[0], st));
+  const uint8_t* dqp[3] = {dq[0], dq[1], dq[2]};
+  if (host_input) {
+    for (int p = 0; p < 3; ++p) {
+      if (c->q_pay[p].ensure(qlen[p])) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query payload)");
+      CK(c, cudaMemcpyAsync(c->q_pay[p].p, hq[p], qlen[p], cudaMemcpyHostToDevice, st));
+      dqp[p] = c->q_pay[p].as<uint8_t>();
+    }
+  }
+  int rc = ensure_query_buffers(c, ncodes, ncols_pad);
+  if (rc) return rc;
+  launch_parse_query(dqp[0], dqp[1], dqp[2], ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir,
+                     c->q_lo.as<uint8_t>(), c->q_hi.as<uint8_t>(), c->q_pa.as<uint16_t>(),
+                     c->q_pb.as<uint16_t>(), st);
+  CK(c, cudaGetLastError());
+  uint64_t launches = 1;
+
+  if (npairs) {
+    if (c->pair_dots.ensure(6 * npairs * sizeof(uint16_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    launch_pairs(c->q_pa.as<uint16_t>(), c->q_pb.as<uint16_t>(), ncodes, persons, c->l, r, c->shamir,
+                 c->pair_dots.as<uint16_t>(), c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
+    CK(c, cudaGetLastError());
+    ++launches;
+  }
+  CK(c, cudaEventRecord(c->ev[1], st));
+
+  // ---- taps
+  if (c->taps) {
+    c->tap_n = n;
+    const size_t sz[7] = {2, 2, 2, 2, 4, 4, 1};
+    for (int t = 0; t < 7; ++t) {
+      if (c->tap_buf[t].ensure(3 * n * sz[t] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (taps)");
+      CK(c, cudaMemsetAsync(c->tap_buf[t].p, 0, 3 * n * sz[t] + 16, st));
+    }
+  }
+
+  // ---- per-person slot ranges (fused OR partials) and debug/pair match words
+  const uint64_t s_loc = c->s;
+  const uint64_t row_off = c->cfg.db_row_offset;
+  std::vector<uint64_t> col_slot(ncols + 1, 0);
+  uint64_t total_slots = 0;
+  for (uint64_t col = 0; col < ncols; ++col) {
+    col_slot[col] = total_slots;
+    if (s_loc) {
+      const uint64_t lb = col * S + row_off, le = lb + s_loc;
+      total_slots += (le - 1) / 1024 - lb / 1024 + 1;
+    }
+  }
+  col_slot[ncols] = total_slots;
+  std::vector<uint64_t> h_slot_begin(ngroups + 1);
+  for (uint32_t g = 0; g <= ngroups; ++g)
+    h_slot_begin[g] = membership ? (g == 0 ? 0 : total_slots) : col_slot[(uint64_t)g * 2 * r];
+  if (c->partial.ensure(3 * total_slots + 16) || c->slot_begin.ensure((ngroups + 1) * sizeof(uint64_t)) ||
+      c->person_out.ensure(3ull * ngroups + 16))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or buffers)");
+  CK(c, cudaMemcpyAsync(c->slot_begin.p, h_slot_begin.data(), (ngroups + 1) * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice, st));
+
+  const bool dbg = c->cfg.debug_rows != 0 && row_bits_out;
+  uint64_t match_w0 = 0, match_words = 0;
+  if (dbg) {
+    match_words = ceil_div(n, 32) + 1;
+  } else if (npairs) {
+    match_w0 = (ncols * S) / 32;
+    match_words = ceil_div(n, 32) - match_w0 + 1;
+  }
+  if (match_words) {
+    for (int p = 0; p < 3; ++p) {
+      if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
+      CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
+    }
+  }
+
+  ThrArgs ta{};
+  ta.n = n;
+  ta.W = W;
+  for (int k = 0; k < 3; ++k) {
+    ta.pos[k] = c->pos[k];
+    ta.key[k] = c->keys[k];
+  }
+  ta.a = c->cfg.a;
+  ta.b = c->cfg.b;
+  ta.partial = c->partial.as<uint8_t>();
+  ta.nslots = total_slots;
+  ta.or_elem_base = (qid << 48) | (rank << 40);
+  if (c->taps) {
+    ta.tap_rs_hd = c->tap_buf[2].as<uint16_t>();
+    ta.tap_rs_ml = c->tap_buf[3].as<uint16_t>();
+    ta.tap_ml32 = c->tap_buf[4].as<uint32_t>();
+    ta.tap_diff = c->tap_buf[5].as<uint32_t>();
+    ta.tap_msb = c->tap_buf[6].as<uint8_t>();
+  }
+
+  // ---- DB lanes: column chunks (GEMM then threshold)
+  double gemm_ms = 0, thr_ms = 0;
+  uint64_t gemm_launches = 0;
+  if (s_loc && ncols) {
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    const uint64_t per_col = 12ull * s_loc;
+    uint64_t budget = std::min<uint64_t>(freeb / 2 + c->dots.cap, 8ull << 30);
+    uint64_t chunk = std::max<uint64_t>(kGemmBN, (budget / per_col) / kGemmBN * kGemmBN);
+    chunk = std::min<uint64_t>(chunk, ncols_pad);
+    if (c->dots.ensure(6 * chunk * s_loc * sizeof(uint16_t)))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dot buffer)");
+    if (ensure_host_segs(c, ncols + 1)) return IRISMPC_GPU_ERR_DEVICE;
+    if (c->segs.ensure((ncols + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
+    // one segment per column; task_begin is relative to the column chunk
+    std::vector<uint64_t> chunk_tasks;
+    for (uint64_t c0 = 0; c0 < ncols; c0 += chunk) {
+      const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
+      uint64_t ntasks = 0;
+      for (uint64_t col = c0; col < c1; ++col) {
+        Seg& sg = c->h_segs_pinned[col];
+        sg.lane_begin = col * S + row_off;
+        sg.lane_end = sg.lane_begin + s_loc;
+        sg.src = (col - c0) * s_loc;
+        sg.q_first = sg.lane_begin / 1024;
+        sg.task_begin = ntasks;
+        sg.slot = (int64_t)col_slot[col];
+        ntasks += (sg.lane_end - 1) / 1024 - sg.q_first + 1;
+      }
+      chunk_tasks.push_back(ntasks);
+    }
+    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, ncols * sizeof(Seg), cudaMemcpyHostToDevice, st));
+    for (uint64_t c0 = 0, ci = 0; c0 < ncols; c0 += chunk, ++ci) {
+      const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
+      GemmArgs g{};
+      g.s_pad = (uint32_t)c->s_pad;
+      g.nb_rows = ncols_pad;
+      g.nkb_seg = c->l_pad / kGemmBK;
+      g.nseg = c->nseg;
+      g.rep = c->shamir ? 0 : 1;
+      g.s_valid = (uint32_t)s_loc;
+      g.col0 = (uint32_t)c0;
+      g.ncols = (uint32_t)(c1 - c0);
+      g.out = c->dots.as<uint16_t>();
+      g.out_pstride = (c1 - c0) * s_loc;
+      g.out_cstride = (uint32_t)s_loc;
+      launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(c->s_pad / kGemmBM),
+                  (uint32_t)ceil_div(c1 - c0, kGemmBN), st);
+      CK(c, cudaGetLastError());
+      ++gemm_launches;
+      ++launches;
+      if (c->taps && c->cfg.db_rows_total == 0) {
+        // L1 tap: lanes [c0*s, c1*s) are contiguous in the dot buffer
+        for (int p = 0; p < 3; ++p) {
+          CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint16_t>() + p * n + c0 * s_loc,
+                                c->dots.as<uint16_t>() + (2 * p) * g.out_pstride, g.out_pstride * 2,
+                                cudaMemcpyDeviceToDevice, st));
+          CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint16_t>() + p * n + c0 * s_loc,
+                                c->dots.as<uint16_t>() + (2 * p + 1) * g.out_pstride, g.out_pstride * 2,
+                                cudaMemcpyDeviceToDevice, st));
+        }
+      }
+      const uint64_t ntasks = chunk_tasks[ci];
+      ThrArgs t = ta;
+      t.segs = c->segs.as<Seg>() + c0;
+      t.nsegs = (uint32_t)(c1 - c0);
+      t.ntasks = ntasks;
+      for (int p = 0; p < 3; ++p) {
+        t.hd[p] = c->dots.as<uint16_t>() + (2 * p) * g.out_pstride;
+        t.ml[p] = c->dots.as<uint16_t>() + (2 * p + 1) * g.out_pstride;
+        t.match[p] = dbg ? c->match[p].as<uint32_t>() : nullptr;
+      }
+      t.match_w0 = 0;
+      launch_threshold(t, st);
+      CK(c, cudaGetLastError());
+      ++launches;
+    }
+  }
+  CK(c, cudaEventRecord(c->ev[2], st));
+
+  // ---- pair lanes (shard 0): threshold into match words
+  if (npairs) {
+    if (c->taps && c->cfg.db_rows_total == 0) {
+      for (int p = 0; p < 3; ++p) {
+        CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint16_t>() + p * n + ncols * S,
+                              c->pair_dots.as<uint16_t>() + p * 2 * npairs, npairs * 2,
+                              cudaMemcpyDeviceToDevice, st));
+        CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint16_t>() + p * n + ncols * S,
+                              c->pair_dots.as<uint16_t>() + npairs + p * 2 * npairs, npairs * 2,
+                              cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    if (ensure_host_segs(c, 1)) return IRISMPC_GPU_ERR_DEVICE;
+    if (c->segs.ensure(sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
+    Seg& sg = c->h_segs_pinned[0];
+    sg.lane_begin = ncols * S;
+    sg.lane_end = n;
+    sg.src = 0;
+    sg.q_first = sg.lane_begin / 1024;
+    sg.task_begin = 0;
+    sg.slot = -1;
+    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, sizeof(Seg), cudaMemcpyHostToDevice, st));
+    ThrArgs t = ta;
+    t.segs = c->segs.as<Seg>();
+    t.nsegs = 1;
+    t.ntasks = (sg.lane_end - 1) / 1024 - sg.q_first + 1;
+    for (int p = 0; p < 3; ++p) {
+      t.hd[p] = c->pair_dots.as<uint16_t>() + p * 2 * npairs;
+      t.ml[p] = c->pair_dots.as<uint16_t>() + p * 2 * npairs + npairs;
+      t.match[p] = c->match[p].as<uint32_t>();
+    }
+    t.match_w0 = match_w0;
+    launch_threshold(t, st);
+    CK(c, cudaGetLastError());
+    ++launches;
+  }
+  CK(c, cudaEventRecord(c->ev[3], st));
+
+  // ---- per-person OR
+  OrArgs oa{};
+  oa.partial = c->partial.as<uint8_t>();
+  oa.nslots = total_slots;
+  oa.slot_begin = c->slot_begin.as<uint64_t>();
+  for (int p = 0; p < 3; ++p) oa.pair_match[p] = npairs ? c->match[p].as<uint32_t>() : nullptr;
+  oa.pair_w0 = match_w0;
+  oa.pair_lane0 = ncols * S;
+  oa.persons = ngroups;
+  oa.rot = r;
+  for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
+  oa.elem_base = (qid << 48) | (rank << 40);
+  oa.out = c->person_out.as<uint8_t>();
+  launch_or_persons(oa, st);
+  CK(c, cudaGetLastError());
+  ++launches;
+
+  if (mode == 0) {
+    if (c->open_out.ensure(ngroups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, qid << 48,
+                   c->open_out.as<uint8_t>(), st);
+    CK(c, cudaGetLastError());
+    ++launches;
+    CK(c, cudaMemcpyAsync(match_out, c->open_out.p, ngroups, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(c, cudaMemcpyAsync(partial_dev, c->person_out.p, 3ull * ngroups, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(c, cudaEventRecord(c->ev[4], st));
+  if (dbg) {
+    std::vector<uint32_t> w[3];
+    const uint64_t nw = ceil_div(n, 32);
+    for (int p = 0; p < 3; ++p) {
+      w[p].resize(nw);
+      CK(c, cudaMemcpyAsync(w[p].data(), c->match[p].p, nw * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(c, cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n; ++i)
+      row_bits_out[i] = (uint8_t)(((w[0][i / 32] ^ w[1][i / 32] ^ w[2][i / 32]) >> (i % 32)) & 1u);
+  }
+  CK(c, cudaStreamSynchronize(st));
+
+  // ---- advance the seed streams exactly as the reference does (A.3)
+  const uint64_t glen = membership ? S : 2ull * r * S + (uint64_t)(persons ? persons - 1 : 0) * 4 * r;
+  uint64_t or_rounds = 0, or_bytes = 0;
+  const uint64_t ord = ref_or_draws(ngroups, glen, &or_rounds, &or_bytes);
+  c->pos[0] += 4 * n + 125 * W + ord;
+  c->pos[1] += 2 * n + 125 * W + ord;
+  c->pos[2] += 8 * n + 125 * W + ord;
+
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->s = S;
+    stats->l = c->l;
+    stats->batch = membership ? 1 : persons;
+    stats->lanes = n;
+    const uint64_t nb8 = ceil_div(n, 8), open_b = ceil_div(ngroups, 8);
+    for (int p = 0; p < 3; ++p) {
+      stats->dot_bytes[p] = 4 * n;
+      stats->lift_bytes[p] = 64 * nb8 + (p == 0 ? 8 * n : 4 * n);
+      stats->msb_bytes[p] = 61 * nb8;
+      stats->or_tree_bytes[p] = or_bytes + (p == 0 ? 0 : open_b) + (c->cfg.debug_rows && p != 0 ? nb8 : 0);
+    }
+    stats->dot_rounds = 1;
+    stats->lift_rounds = 21;
+    stats->msb_rounds = 31;
+    stats->or_tree_rounds = or_rounds + 1 + (c->cfg.debug_rows ? 1 : 0);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
+    stats->wall_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    stats->prep_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]);
+    stats->gemm_ms = gemm_ms;
+    stats->threshold_ms = ms;  // gemm + threshold interleaved per chunk
+    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
+    stats->or_ms = ms;
+    stats->gemm_launches = gemm_launches;
+    stats->kernel_launches = launches;
+  }
+  (void)thr_ms;
+  return 0;
+}
+
+}  // namespace
+
+// =========================================================================== ABI
+
+extern "C" {
+
+int irismpc_gpu_seeds_from_master(uint64_t master, uint8_t out[48]) {
+  uint8_t s[16], d[16];
+  host_seed_from_u64(master, s);
+  host_derive(s, 0x5eed, d);
+  // Rng(d): 48 draws, one byte (low) each (deal_seeds, rep3.hpp:116-122)
+  for (int i = 0; i < 48; ++i) {
+    uint32_t blk[16];
+    host_block(d, (uint64_t)i / 8, 0, blk);
+    out[i] = (uint8_t)blk[2 * (i % 8)];
+  }
+  return 0;
+}
+
+size_t irismpc_gpu_record_bytes(uint32_t backend, uint32_t variant, uint32_t l) {
+  if (variant != IRISMPC_GPU_VARIANT_MPC_LIFT) return 0;
+  return record_bytes(backend, l);
+}
+
+uint64_t irismpc_gpu_lane_count(uint32_t persons, uint64_t s, uint32_t rotations, int membership) {
+  if (membership) return s;
+  return 2ull * persons * rotations * s + (uint64_t)persons * (persons ? persons - 1 : 0) / 2 * 4 * rotations;
+}
+
+int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
+  if (!cfg || !out) return IRISMPC_GPU_ERR_CONFIG;
+  *out = nullptr;
+  std::string why;
+  int rc = validate(cfg, &why);
+  if (rc) {
+    std::fprintf(stderr, "irismpc_gpu_create: %s\n", why.c_str());
+    return rc;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
+    std::fprintf(stderr, "irismpc_gpu_create: no CUDA device %d\n", cfg->device);
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return IRISMPC_GPU_ERR_DEVICE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) {
+    std::fprintf(stderr, "irismpc_gpu_create: device is not sm_100 (B200)\n");
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  auto* c = new irismpc_gpu_ctx;
+  c->cfg = *cfg;
+  c->shamir = cfg->backend == IRISMPC_GPU_BACKEND_SHAMIR;
+  c->l = cfg->l;
+  c->l_pad = (uint32_t)round_up(cfg->l, kGemmBK);
+  c->nseg = c->shamir ? 1 : 2;
+  for (int k = 0; k < 3; ++k) c->keys[k] = key_of(cfg->seeds + 16 * k);
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  uint16_t lam[6];
+  lambdas(lam);
+  set_lambda(lam);
+  *out = c;
+  return 0;
+}
+
+void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  cudaStreamSynchronize(c->st);
+  Buf* bufs[] = {&c->db_lo, &c->db_hi, &c->q_lo, &c->q_hi, &c->q_pa, &c->q_pb, &c->q_pay[0], &c->q_pay[1],
+                 &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial, &c->slot_begin,
+                 &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out};
+  for (Buf* b : bufs) b->release();
+  for (auto& t : c->tap_buf) t.release();
+  if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+const char* irismpc_gpu_last_error(const irismpc_gpu_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void* irismpc_gpu_stream(irismpc_gpu_ctx* c) { return c ? (void*)c->st : nullptr; }
+
+int irismpc_gpu_load_db(irismpc_gpu_ctx* c, const uint8_t* const payload[3], const size_t len[3], uint64_t s) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  for (int p = 0; p < 3; ++p)
+    if (len[p] != s * rec) return fail(c, IRISMPC_GPU_ERR_CONFIG, "db payload size mismatch");
+  int rc = alloc_planes(c, s);
+  if (rc) return rc;
+  const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / rec);
+  Buf stage[3], bad;
+  for (int p = 0; p < 3; ++p)
+    if (stage[p].ensure(std::min<uint64_t>(chunk, s ? s : 1) * rec))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (load staging)");
+  if (bad.ensure(sizeof(int))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  CK(c, cudaMemsetAsync(bad.p, 0, sizeof(int), c->st));
+  for (uint64_t r0 = 0; r0 < s; r0 += chunk) {
+    const uint64_t nr = std::min<uint64_t>(chunk, s - r0);
+    for (int p = 0; p < 3; ++p)
+      CK(c, cudaMemcpyAsync(stage[p].p, payload[p] + r0 * rec, nr * rec, cudaMemcpyHostToDevice, c->st));
+    const uint8_t* dp[3] = {stage[0].as<uint8_t>(), stage[1].as<uint8_t>(), stage[2].as<uint8_t>()};
+    rc = parse_rows(c, dp, nr, r0, &bad);
+    if (rc) return rc;
+    CK(c, cudaStreamSynchronize(c->st));
+  }
+  rc = finish_load(c, c->shamir ? nullptr : &bad);
+  for (auto& b : stage) b.release();
+  bad.release();
+  return rc;
+}
+
+int irismpc_gpu_load_db_device(irismpc_gpu_ctx* c, const uint8_t* const dpayload[3], const size_t len[3],
+                               uint64_t s) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  for (int p = 0; p < 3; ++p)
+    if (len[p] != s * rec) return fail(c, IRISMPC_GPU_ERR_CONFIG, "db payload size mismatch");
+  int rc = alloc_planes(c, s);
+  if (rc) return rc;
+  Buf bad;
+  if (bad.ensure(sizeof(int))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  CK(c, cudaMemsetAsync(bad.p, 0, sizeof(int), c->st));
+  rc = parse_rows(c, dpayload, s, 0, &bad);
+  if (rc) return rc;
+  rc = finish_load(c, c->shamir ? nullptr : &bad);
+  bad.release();
+  return rc;
+}
+
+int irismpc_gpu_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint32_t persons,
+                            uint8_t* person_match_out, uint8_t* row_bits_out, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  const uint8_t* none[3] = {nullptr, nullptr, nullptr};
+  return run_query(c, none, qlen, persons, 0, 0, person_match_out, row_bits_out, nullptr, stats, true, q);
+}
+
+int irismpc_gpu_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
+                                   uint32_t persons, uint8_t* person_match_out, uint8_t* row_bits_out,
+                                   irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return run_query(c, dq, qlen, persons, 0, 0, person_match_out, row_bits_out, nullptr, stats, false, nullptr);
+}
+
+int irismpc_gpu_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint8_t* match_out,
+                           uint8_t* row_bits_out, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  const uint8_t* none[3] = {nullptr, nullptr, nullptr};
+  return run_query(c, none, qlen, 1, 1, 0, match_out, row_bits_out, nullptr, stats, true, q);
+}
+
+int irismpc_gpu_batch_query_partial(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
+                                    uint32_t persons, uint8_t* partial_out_dev, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return run_query(c, dq, qlen, persons, 0, 1, nullptr, nullptr, partial_out_dev, stats, false, nullptr);
+}
+
+int irismpc_gpu_or_open(irismpc_gpu_ctx* c, const uint8_t* partials_dev, uint32_t G, uint32_t persons,
+                        uint8_t* person_match_out) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  if (c->open_out.ensure(persons + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  // query_id was advanced by the partial query; final OR uses stream 3 of that query
+  launch_or_open(partials_dev, G, persons, c->keys, (c->query_id - 1) << 48, c->open_out.as<uint8_t>(), c->st);
+  CK(c, cudaGetLastError());
+  CK(c, cudaMemcpyAsync(person_match_out, c->open_out.p, persons, cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* c, uint64_t pos[3]) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  for (int k = 0; k < 3; ++k) pos[k] = c->pos[k];
+  return 0;
+}
+
+int irismpc_gpu_set_stream_positions(irismpc_gpu_ctx* c, const uint64_t pos[3]) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  for (int k = 0; k < 3; ++k) c->pos[k] = pos[k];
+  return 0;
+}
+
+int irismpc_gpu_synth_records(irismpc_gpu_ctx* c, uint64_t rng_seed, uint64_t first, uint64_t count,
+                              double mask_density, uint64_t* codes_dev, uint64_t* masks_dev) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  uint8_t s[16];
+  host_seed_from_u64(rng_seed, s);
+  launch_synth_records(key_of(s), first, count, c->l, mask_density, codes_dev, masks_dev, c->st);
+  CK(c, cudaGetLastError());
+  CK(c, cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int irismpc_gpu_deal_payload(irismpc_gpu_ctx* c, uint64_t deal_seed, uint64_t tag, uint64_t first_record,
+                             uint64_t nrec, const uint64_t* codes_dev, const uint64_t* masks_dev,
+                             uint8_t* const out_dev[3]) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  uint8_t s[16], d[16];
+  host_seed_from_u64(deal_seed, s);
+  host_derive(s, tag, d);
+  launch_deal(key_of(d), first_record, nrec, c->l, c->shamir, codes_dev, masks_dev, out_dev[0], out_dev[1],
+              out_dev[2], c->st);
+  CK(c, cudaGetLastError());
+  CK(c, cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint64_t first, double mask_density,
+                         uint64_t deal_seed) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  int rc = alloc_planes(c, s);
+  if (rc) return rc;
+  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const uint64_t wl = (c->l + 63) / 64;
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s ? s : 1, (512ull << 20) / rec));
+  Buf codes, masks, pay[3];
+  if (codes.ensure(chunk * wl * 8) || masks.ensure(chunk * wl * 8)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  for (auto& p : pay)
+    if (p.ensure(chunk * rec)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  uint8_t sr[16], sd[16], dd[16];
+  host_seed_from_u64(rng_seed, sr);
+  host_seed_from_u64(deal_seed, sd);
+  host_derive(sd, 1, dd);
+  for (uint64_t r0 = 0; r0 < s; r0 += chunk) {
+    const uint64_t nr = std::min<uint64_t>(chunk, s - r0);
+    launch_synth_records(key_of(sr), first + r0, nr, c->l, mask_density, codes.as<uint64_t>(),
+                         masks.as<uint64_t>(), c->st);
+    launch_deal(key_of(dd), first + r0, nr, c->l, c->shamir, codes.as<uint64_t>(), masks.as<uint64_t>(),
+                pay[0].as<uint8_t>(), pay[1].as<uint8_t>(), pay[2].as<uint8_t>(), c->st);
+    const uint8_t* dp[3] = {pay[0].as<uint8_t>(), pay[1].as<uint8_t>(), pay[2].as<uint8_t>()};
+    rc = parse_rows(c, dp, nr, r0, nullptr);
+    if (rc) return rc;
+  }
+  CK(c, cudaGetLastError());
+  rc = finish_load(c, nullptr);
+  codes.release();
+  masks.release();
+  for (auto& p : pay) p.release();
+  return rc;
+}
+
+int irismpc_gpu_enable_taps(irismpc_gpu_ctx* c, int enable) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  c->taps = enable != 0;
+  return 0;
+}
+
+int irismpc_gpu_read_tap(irismpc_gpu_ctx* c, int tap, void* host_out, size_t bytes) {
+  if (!c || tap < 1 || tap > 7) return IRISMPC_GPU_ERR_CONFIG;
+  if (!c->tap_buf[tap - 1].p) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap not captured");
+  const size_t sz[7] = {2, 2, 2, 2, 4, 4, 1};
+  const size_t have = 3 * c->tap_n * sz[tap - 1];
+  if (bytes > have) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap read larger than captured");
+  cudaSetDevice(c->cfg.device);
+  CK(c, cudaMemcpy(host_out, c->tap_buf[tap - 1].p, bytes, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+// K2: Z_2^16 share dot products as u8-limb GEMMs on the 5th-gen tensor cores.
+//
+// Replaces kernels::dot_gr_ct_rows<16> / dot_prep_rows<16>
+// (/root/reference/proj/src/kernels.cpp:29-53, include/irismpc/kernels.hpp:38-62):
+// for every party p and dot d (code -> hd, mask -> ml)
+//     C_p[row, col] = sum_k A_p[row, k] * B_p[col, k]   (mod 2^16)
+// with 16-bit operands split into u8 limbs, V = lo + 256 hi:
+//     C = A_lo.B_lo^T + 256 (A_lo.B_hi^T + A_hi.B_lo^T)   (mod 2^16)
+// i.e. three tcgen05.mma.kind::i8 per k-step into two s32 TMEM accumulators
+// (no saturation: the s32 wrap is harmless, only the low 16 bits survive).
+// The epilogue recombines (acc0 + (acc1 << 8)) & 0xffff and writes the
+// per-party additive shares in lane order (lane = col * s + row).
+//
+// Structure: one 128x256 output tile per CTA, warp-specialised:
+//   warp 0   TMA producer (128B-swizzled K-major tiles, 2-stage mbarrier ring)
+//   warp 1   single-thread tcgen05.mma issuer, tcgen05.commit -> mbarriers
+//   warp 2   TMEM allocator (512 columns: acc0 | acc1)
+//   warps 4-7 epilogue: tcgen05.ld -> recombine -> global stores
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace irisgpu {
+
+namespace {
+
+constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
+constexpr int STAGES = 2;
+constexpr int A_TILE = BM * BK;  // 16 KB
+constexpr int B_TILE = BN * BK;  // 32 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t TMEM_COLS = 512;
+
+// UMMA shared-memory descriptor, K-major operand, 128B swizzle:
+// start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major -> 1),
+// SBO>>4 [32,46) = 1024 B between 8-row core groups, version 1 [46,48),
+// layout SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::i8: c_format S32 (2) [4,6), a/b format u8 (0),
+// K-major A and B, N>>3 [17,23), M>>4 [24,29).
+constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 1)
+    k_limb_gemm(const __grid_constant__ CUtensorMap tA_lo, const __grid_constant__ CUtensorMap tA_hi,
+                const __grid_constant__ CUtensorMap tB_lo, const __grid_constant__ CUtensorMap tB_hi,
+                const GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_tile = blockIdx.x;
+  const int m_tile = blockIdx.y;
+  const int prob = blockIdx.z;  // p * 2 + d
+  const int p = prob >> 1, d = prob & 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tA_lo);
+    tma_prefetch_desc(&tA_hi);
+    tma_prefetch_desc(&tB_lo);
+    tma_prefetch_desc(&tB_hi);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t nkb = g.nkb_seg * g.nseg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        const uint32_t stage = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t seg = kb / g.nkb_seg;
+        const uint32_t kk = kb % g.nkb_seg;
+        const int pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;  // A = [x_p | x_{p-1}]
+        const int32_t arow = (int32_t)((uint32_t)(pa * 2 + d) * g.s_pad + m_tile * BM);
+        const int32_t brow = (int32_t)(((uint32_t)prob * g.nseg + seg) * g.nb_rows + g.col0 + n_tile * BN);
+        uint8_t* st = smem + stage * STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+        tma_load_2d(st, &tA_lo, &full[stage], (int32_t)(kk * BK), arow);
+        tma_load_2d(st + A_TILE, &tA_hi, &full[stage], (int32_t)(kk * BK), arow);
+        tma_load_2d(st + 2 * A_TILE, &tB_lo, &full[stage], (int32_t)(kk * BK), brow);
+        tma_load_2d(st + 2 * A_TILE + B_TILE, &tB_hi, &full[stage], (int32_t)(kk * BK), brow);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        const uint32_t stage = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
+        const uint64_t dAlo = make_desc(st);
+        const uint64_t dAhi = make_desc(st + A_TILE);
+        const uint64_t dBlo = make_desc(st + 2 * A_TILE);
+        const uint64_t dBhi = make_desc(st + 2 * A_TILE + B_TILE);
+#pragma unroll
+        for (int ks = 0; ks < BK / 32; ++ks) {
+          const uint64_t off = (uint64_t)(ks * 32) >> 4;  // +32 bytes along K
+          const uint32_t acc = (kb | ks) != 0;
+          umma_i8(tmem, dAlo + off, dBlo + off, kIdesc, acc);            // lo.lo   -> acc0
+          umma_i8(tmem + BN, dAlo + off, dBhi + off, kIdesc, acc);       // lo.hi   -> acc1
+          umma_i8(tmem + BN, dAhi + off, dBlo + off, kIdesc, 1u);        // hi.lo   -> acc1
+        }
+        umma_commit(&empty[stage]);
+      }
+      umma_commit(accum);
+    }
+  } else if (warp >= 4) {
+    mbar_wait(accum, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const uint32_t row = (uint32_t)m_tile * BM + q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint16_t* out = g.out + (uint64_t)prob * g.out_pstride;
+    const bool row_ok = row < g.s_valid;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t a0[16], a1[16];
+      tmem_ld16(tmem + lane_addr + c, a0);
+      tmem_ld16(tmem + lane_addr + BN + c, a1);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t col = (uint32_t)n_tile * BN + c + j;
+        if (row_ok && col < g.ncols) {
+          out[(uint64_t)col * g.out_cstride + row] = (uint16_t)((a0[j] + (a1[j] << 8)) & 0xFFFFu);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad,
+                    uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  const cuuint64_t dims[2] = {k_pad, rows};
+  const cuuint64_t strides[1] = {k_pad};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtensorMap& b_lo,
+                 const CUtensorMap& b_hi, const GemmArgs& g, uint32_t m_tiles, uint32_t n_tiles,
+                 cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_limb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  dim3 grid(n_tiles, m_tiles, 6);
+  k_limb_gemm<<<grid, 256, SMEM_BYTES, st>>>(a_lo, a_hi, b_lo, b_hi, g);
+}
+
+}  // namespace irisgpu

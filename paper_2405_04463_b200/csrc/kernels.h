@@ -1,0 +1,110 @@
+// Internal launcher declarations shared by the .cu files and the C-ABI layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace irisgpu {
+
+// ---- K1 prep / dealer (prep.cu)
+void set_lambda(const uint16_t lam[6]);
+void launch_parse_db(const uint8_t* pay, uint64_t nrows, uint64_t row0, uint32_t l, uint32_t l_pad,
+                     uint64_t s_pad, int party, int shamir, uint8_t* lo, uint8_t* hi,
+                     cudaStream_t st);
+void launch_check_rep(const uint8_t* p1, const uint8_t* p2, const uint8_t* p3, uint64_t bytes,
+                      int* bad, cudaStream_t st);
+void launch_parse_query(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes,
+                        uint32_t l, uint32_t l_pad, uint32_t rot, uint32_t ncols_pad, int shamir,
+                        uint8_t* blo, uint8_t* bhi, uint16_t* pa, uint16_t* pb, cudaStream_t st);
+void launch_synth_records(SeedKey key, uint64_t first, uint64_t count, uint32_t l, double density,
+                          uint64_t* codes, uint64_t* masks, cudaStream_t st);
+void launch_deal(SeedKey key, uint64_t first_record, uint64_t nrec, uint32_t l, int shamir,
+                 const uint64_t* codes, const uint64_t* masks, uint8_t* o1, uint8_t* o2,
+                 uint8_t* o3, cudaStream_t st);
+
+// ---- K2 limb GEMM (gemm.cu)
+constexpr int kGemmBM = 128;
+constexpr int kGemmBN = 256;
+constexpr int kGemmBK = 128;
+
+struct GemmArgs {
+  uint32_t s_pad;     // rows per A plane
+  uint32_t nb_rows;   // rows per B plane (ncols_pad)
+  uint32_t nkb_seg;   // k-blocks per K segment (l_pad / 128)
+  uint32_t nseg;      // 1 (Shamir) or 2 (replicated [x_p | x_{p-1}])
+  uint32_t rep;
+  uint32_t s_valid;   // rows written
+  uint32_t col0;      // first B row of this launch (chunk start column)
+  uint32_t ncols;     // columns written (from col0)
+  uint16_t* out;      // [6][ncols * out_cstride]
+  uint64_t out_pstride;
+  uint32_t out_cstride;
+};
+// Encodes the TMA map for a [rows][k_pad] u8 plane stack with a box of
+// (128 bytes, box_rows) and 128B swizzle.
+int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad,
+                    uint32_t box_rows);
+void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtensorMap& b_lo,
+                 const CUtensorMap& b_hi, const GemmArgs& g, uint32_t m_tiles, uint32_t n_tiles,
+                 cudaStream_t st);
+
+// ---- inner-batch pairs (pairs.cu)
+void launch_pairs(const uint16_t* pa, const uint16_t* pb, uint32_t ncodes, uint32_t persons,
+                  uint32_t l, uint32_t rot, int shamir, uint16_t* out_hd, uint16_t* out_ml,
+                  uint64_t out_pstride, cudaStream_t st);
+
+// ---- K4 threshold (threshold.cu)
+struct Seg {
+  uint64_t lane_begin, lane_end;  // global lanes [begin, end)
+  uint64_t src;                   // dot-buffer index of lane_begin
+  uint64_t task_begin;            // first task (warp block) of this segment
+  uint64_t q_first;               // lane_begin / 1024
+  int64_t slot;                   // partial slot of its first task, -1 = no fused OR
+};
+
+struct ThrArgs {
+  const Seg* segs;
+  uint32_t nsegs;
+  uint64_t ntasks;
+  const uint16_t* hd[3];
+  const uint16_t* ml[3];
+  uint64_t n, W;
+  uint64_t pos[3];
+  SeedKey key[3];
+  uint32_t a, b;
+  uint32_t* match[3];    // optional 32-lane words (atomicOr), word = lane/32 - match_w0
+  uint64_t match_w0;
+  uint8_t* partial;      // [3][nslots]
+  uint64_t nslots;
+  uint64_t or_elem_base; // OR-stream (stream id 1) element base of this launch
+  // taps (tests), global-lane indexed, may be null
+  uint16_t* tap_rs_hd;
+  uint16_t* tap_rs_ml;
+  uint32_t* tap_ml32;
+  uint32_t* tap_diff;
+  uint8_t* tap_msb;
+};
+void launch_threshold(const ThrArgs& a, cudaStream_t st);
+
+// ---- K5 OR reduction + open (orreduce.cu)
+struct OrArgs {
+  const uint8_t* partial;   // [3][nslots]
+  uint64_t nslots;
+  const uint64_t* slot_begin;  // [persons + 1] per-person slot ranges (device)
+  const uint32_t* pair_match[3];  // pair lane bits (words), may be null
+  uint64_t pair_w0;          // word index of pair lane 0's word
+  uint64_t pair_lane0;       // global lane of pair lane 0
+  uint32_t persons, rot;
+  SeedKey key[3];
+  uint64_t elem_base;        // OR stream (stream id 2) element base
+  uint8_t* out;              // [3][persons] component bits
+};
+void launch_or_persons(const OrArgs& a, cudaStream_t st);
+void launch_or_open(const uint8_t* partials, uint32_t G, uint32_t persons, const SeedKey key[3],
+                    uint64_t elem_base, uint8_t* match_out, cudaStream_t st);
+
+}  // namespace irisgpu

@@ -1,0 +1,57 @@
+"""CPU-side checks of the C-ABI library: it builds, loads without a GPU and
+exports every entry point include/irismpc_gpu.h declares (no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2405_04463_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "irismpc_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(irismpc_gpu_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_and_python_binding_agree():
+    assert _declared() == sorted(P.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    L = P.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+
+
+def test_pure_host_entry_points():
+    from oracle import pyoracle as O
+    # seeds_from_master == deal_seeds of run_parties (reference-pinned oracle)
+    assert bytes(P.seeds_from_master(7)) == bytes(O.party_seeds(7))
+    assert P.record_bytes(P.SHAMIR, 12800) == O.record_bytes(O.SHAMIR, 12800)
+    assert P.record_bytes(P.REPLICATED, 64) == O.record_bytes(O.REPLICATED, 64)
+    for persons, s, r, m in [(16, 100_000, 31, False), (1, 10, 1, True), (3, 0, 31, False)]:
+        assert P.lane_count(persons, s, r, m) == O.lib().orc_lane_count(persons, s, r, 1 if m else 0)
+    for ratio in (0.375, 0.3, 0.2, 0.0, 0.5):
+        assert P.match_a(ratio) == O.lib().orc_match_a(ratio)
+
+
+def test_bounds_rejected_before_device():
+    # EngineConfig::validate: Shamir needs an even rotation stride (l/64)
+    with pytest.raises(P.BoundsError):
+        P.Session(P.EngineConfig(backend=P.SHAMIR, l=192, rotations=3), master_seed=1)
+    with pytest.raises(P.BoundsError):
+        P.Session(P.EngineConfig(backend=P.SHAMIR, l=64, rotations=2), master_seed=1)
+    with pytest.raises(P.BoundsError):
+        P.Session(P.EngineConfig(backend=P.REPLICATED, l=12), master_seed=1)
+
+
+@pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is not None and False, reason="")
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.DeviceError):
+        P.Session(P.EngineConfig(backend=P.SHAMIR, l=64, rotations=1), master_seed=1)

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle and the golden
+vectors of the reference (SURVEY.md §8c levels L1..L5).
+
+L1 per-party additive dots, L2 reshared components, lift/diff/MSB components
+(the GPU draws the reference PRF stream layout, so every share through the
+MSB is identical), L3 reconstructed distances, L4 per-lane match bits
+(debug_rows), L5 opened person bits; plus ledgers and stream positions.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2405_04463_b200 as P  # noqa: E402
+from oracle import pyoracle as O  # noqa: E402
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_vectors.json")))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).astype("<u2").tobytes()).hexdigest()
+
+
+def _inputs(l, s, persons, seed, membership, planted, density=0.85):
+    rng = O.Rng(seed)
+    dc, dm = O.records(rng, l, s, density)
+    nq = 1 if membership else 2 * persons
+    qc, qm = O.records(rng, l, nq, density)
+    if planted and s > 0:
+        qc[0] = dc[s // 2]
+        qm[0] = dm[s // 2]
+    return dc, dm, qc, qm
+
+
+def _gpu(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership):
+    cfg = P.EngineConfig(backend=be, l=l, match_ratio=ratio, rotations=r, debug_rows=True)
+    m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, membership=membership,
+                                want_rows=True, taps=True)
+    n = P.lane_count(persons, dc.shape[0], r, membership)
+    taps = {k: sess.read_tap(t, n) for k, t in (("dot_hd", P.TAP_DOT_HD), ("dot_ml", P.TAP_DOT_ML),
+                                                ("rs_hd", P.TAP_RS_HD), ("rs_ml", P.TAP_RS_ML),
+                                                ("ml32", P.TAP_ML32), ("diff", P.TAP_DIFF),
+                                                ("msb", P.TAP_MSB))}
+    return m, sess, taps, n
+
+
+@pytest.mark.parametrize("idx", range(len(GOLD["cases"])))
+def test_golden_cases(idx):
+    c = GOLD["cases"][idx]
+    dc, dm, qc, qm = _inputs(c["l"], c["s"], c["persons"], c["seed"], c["membership"], c["planted"])
+    m, sess, taps, n = _gpu(c["backend"], c["l"], c["ratio"], c["rotations"], c["seed"], dc, dm, qc, qm,
+                            c["persons"], c["membership"])
+    assert n == c["lanes"]
+    assert [int(x) for x in m] == c["person_match"]                                   # L5
+    assert np.packbits(sess.row_bits[:n], bitorder="little").tobytes().hex() == c["row_bits_hex"]  # L4
+    assert _sha(taps["dot_hd"]) == c["sha256"]["dot_hd"]                              # L1
+    assert _sha(taps["dot_ml"]) == c["sha256"]["dot_ml"]
+    assert _sha(taps["rs_hd"]) == c["sha256"]["rs_hd"]                                # L2
+    assert _sha(taps["rs_ml"]) == c["sha256"]["rs_ml"]
+    st = sess.last_stats
+    for p in range(3):
+        assert st.party(p) == c["stats"][p]
+
+
+@pytest.mark.parametrize("be,l,s,persons,r,seed", [
+    (O.SHAMIR, 12800, 300, 3, 31, 21),
+    (O.REPLICATED, 12800, 300, 3, 31, 22),
+    (O.SHAMIR, 12800, 1031, 1, 31, 23),     # s not a multiple of 64/128/1024
+    (O.REPLICATED, 256, 2500, 2, 5, 24),
+    (O.SHAMIR, 128, 1, 4, 31, 25),          # one DB row
+    (O.REPLICATED, 128, 0, 5, 31, 26),      # empty DB, pairs only
+])
+def test_shares_through_msb_match_oracle(be, l, s, persons, r, seed):
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    m, sess, taps, n = _gpu(be, l, 0.375, r, seed, dc, dm, qc, qm, persons, False)
+    cfg = O.make_config(be, l, 0.375, r, debug_rows=True)
+    ref = O.run_local(cfg, seed, dc, dm, qc, qm, persons, want_all=True)
+    for k in ("dot_hd", "dot_ml", "rs_hd", "rs_ml", "ml32", "diff", "msb"):
+        np.testing.assert_array_equal(taps[k], getattr(ref, k), err_msg=k)
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+    np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
+    # L3: reconstructed distances equal the plaintext ones
+    rec_ml = taps["rs_ml"].astype(np.uint32).sum(0) & 0xFFFF
+    rec_hd = taps["rs_hd"].astype(np.uint32).sum(0) & 0xFFFF
+    np.testing.assert_array_equal(rec_ml, ref.rs_ml.astype(np.uint32).sum(0) & 0xFFFF)
+    np.testing.assert_array_equal(rec_hd, ref.rs_hd.astype(np.uint32).sum(0) & 0xFFFF)
+
+
+@pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])
+def test_membership_and_planted(be):
+    l, s = 64, 200
+    dc, dm, qc, qm = _inputs(l, s, 1, 77, True, True, 0.8)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=1, debug_rows=True)
+    m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, 77, membership=True, want_rows=True)
+    ref = O.run_local(O.make_config(be, l, 0.375, 1, True), 77, dc, dm, qc, qm, 1, membership=True)
+    assert m[0] == ref.person_match[0] == 1
+    np.testing.assert_array_equal(sess.row_bits[:s], ref.row_bits)
+
+
+@pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])
+def test_device_dealer_matches_reference_dealer(be):
+    l, n = 12800, 5
+    sess = P.Session(P.EngineConfig(backend=be, l=l), master_seed=1)
+    wl = (l + 63) // 64
+    codes = torch.empty((n, wl), dtype=torch.int64, device="cuda")
+    masks = torch.empty((n, wl), dtype=torch.int64, device="cuda")
+    sess.synth_records(2, 3, n, 0.9, codes, masks)
+    rng = O.Rng(2)
+    O.records(rng, l, 3, 0.9)  # skip 3 records
+    oc, om = O.records(rng, l, n, 0.9)
+    np.testing.assert_array_equal(codes.cpu().numpy().view(np.uint64), oc)
+    np.testing.assert_array_equal(masks.cpu().numpy().view(np.uint64), om)
+    outs = [torch.empty(n * sess.rec, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    sess.deal_payload(7, 1, 0, codes, masks, outs)
+    ref = O.deal(be, l, oc, om, O.Rng(sub=(7, 1)))
+    for a, b in zip(outs, ref):
+        np.testing.assert_array_equal(a.cpu().numpy(), b)
+
+
+def test_host_and_device_payload_paths_agree():
+    l, s, persons, seed = 12800, 64, 2, 31
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    db = O.deal(O.SHAMIR, l, dc, dm, O.Rng(sub=(seed, 1)))
+    q = O.deal(O.SHAMIR, l, qc, qm, O.Rng(sub=(seed, 2)))
+    cfg = P.EngineConfig(backend=P.SHAMIR, l=l)
+    a = P.Session(cfg, master_seed=seed)
+    a.load_db(db, s)
+    ma = a.batch_query(q, persons)
+    b = P.Session(cfg, master_seed=seed)
+    b.load_db([torch.from_numpy(x).cuda() for x in db], s)
+    mb = b.batch_query([torch.from_numpy(x).cuda() for x in q], persons)
+    ref = O.run_local(O.make_config(O.SHAMIR, l), seed, dc, dm, qc, qm, persons)
+    np.testing.assert_array_equal(ma, ref.person_match)
+    np.testing.assert_array_equal(mb, ref.person_match)
+    # persistent context: second query continues the streams like the reference CLI
+    np.testing.assert_array_equal(a.stream_positions(), ref.stream_pos)
+    ma2 = a.batch_query(q, persons)
+    ref2 = O.query(O.make_config(O.SHAMIR, l), O.party_seeds(seed), db, s, q, persons,
+                   stream_start=ref.stream_pos)
+    np.testing.assert_array_equal(ma2, ref2.person_match)
+    np.testing.assert_array_equal(a.stream_positions(), ref2.stream_pos)
+
+
+def test_payload_errors_map_to_reference_exceptions():
+    l = 64
+    sess = P.Session(P.EngineConfig(backend=P.REPLICATED, l=l, rotations=1), master_seed=3)
+    rec = sess.rec
+    with pytest.raises(P.ConfigError):          # "db payload size mismatch"
+        sess.load_db([np.zeros(rec * 2 + 1, np.uint8)] * 3, 2)
+    with pytest.raises(P.InconsistentShareError):  # replication cross-check
+        sess.load_db([np.random.default_rng(0).integers(0, 255, rec * 2, dtype=np.uint8) for _ in range(3)], 2)
+    dc, dm, qc, qm = _inputs(l, 4, 1, 5, False, False)
+    db = O.deal(O.REPLICATED, l, dc, dm, O.Rng(sub=(5, 1)))
+    sess.load_db(db, 4)
+    with pytest.raises(P.ConfigError):          # "batch query expects 2 codes per person"
+        sess.batch_query([np.zeros(rec, np.uint8)] * 3, 1)
+
+
+def test_sharded_db_matches_single_gpu():
+    """Two shards on one GPU (rows split), partial shares + MPC OR + open."""
+    l, s, persons, seed = 12800, 700, 2, 41
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    db = O.deal(O.SHAMIR, l, dc, dm, O.Rng(sub=(seed, 1)))
+    q = O.deal(O.SHAMIR, l, qc, qm, O.Rng(sub=(seed, 2)))
+    rec = O.record_bytes(O.SHAMIR, l)
+    cfg = P.EngineConfig(backend=P.SHAMIR, l=l)
+    split = 333
+    qd = [torch.from_numpy(x).cuda() for x in q]
+    parts = torch.zeros((2, 3, persons), dtype=torch.uint8, device="cuda")
+    sessions = []
+    for rank, (r0, r1) in enumerate([(0, split), (split, s)]):
+        sh = P.Session(cfg, master_seed=seed, shard_rank=rank, db_rows_total=s, db_row_offset=r0)
+        sh.load_db([x[r0 * rec:r1 * rec] for x in db], r1 - r0)
+        sh.batch_query_partial(qd, persons, parts[rank])
+        sessions.append(sh)
+    m = sessions[0].or_open(parts, 2, persons)
+    ref = O.run_local(O.make_config(O.SHAMIR, l), seed, dc, dm, qc, qm, persons)
+    np.testing.assert_array_equal(m, ref.person_match)
+    assert m[0] == 1
+
+
+def test_full_size_synthetic_planted_match():
+    """Size-independent property at the headline scale: a planted rotated
+    near-copy of DB row s/2 is found; a DB of fresh random rows is not."""
+    l, s, persons = 12800, 100_000, 16
+    cfg = P.EngineConfig(backend=P.SHAMIR, l=l)
+    sess = P.Session(cfg, master_seed=7)
+    sess.synth_db(s, rng_seed=2, first=0, mask_density=0.9, deal_seed=7)
+    wl = l // 64
+    codes = torch.empty((2 * persons, wl), dtype=torch.int64, device="cuda")
+    masks = torch.empty((2 * persons, wl), dtype=torch.int64, device="cuda")
+    sess.synth_records(2, s, 2 * persons, 0.9, codes, masks)
+    row = torch.empty((1, wl), dtype=torch.int64, device="cuda")
+    rowm = torch.empty((1, wl), dtype=torch.int64, device="cuda")
+    sess.synth_records(2, s // 2, 1, 0.9, row, rowm)
+    c = np.unpackbits(row.cpu().numpy().view(np.uint8), bitorder="little")
+    mk = np.unpackbits(rowm.cpu().numpy().view(np.uint8), bitorder="little")
+    by = 2 * (l // 64)
+    c, mk = np.roll(c, by), np.roll(mk, by)
+    for f in range(4):
+        c[f * (l // 4) + 7] ^= 1
+    codes[0] = torch.from_numpy(np.packbits(c, bitorder="little").view(np.int64).copy())
+    masks[0] = torch.from_numpy(np.packbits(mk, bitorder="little").view(np.int64).copy())
+    outs = [torch.empty(2 * persons * sess.rec, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    sess.deal_payload(7, 2, 0, codes, masks, outs)
+    m = sess.batch_query(outs, persons)
+    assert m[0] == 1 and m[1:].sum() == 0
+    assert sess.last_stats.lanes == P.lane_count(persons, s, 31)

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -138,17 +139,20 @@ struct irismpc_gpu_ctx {
   CUtensorMap tB_lo, tB_hi;
   uint32_t ncols_pad_cur = 0;
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
+  Buf ml_rs, diff, gate, bits;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
   // PRF stream state
   uint64_t pos[3] = {0, 0, 0};
   uint64_t query_id = 0;
+  uint64_t dots_budget = 0;
   // taps
   bool taps = false;
   Buf tap_buf[7];
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
+  std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
 };
 
 namespace {
@@ -318,6 +322,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   launch_parse_query(dqp[0], dqp[1], dqp[2], ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir,
                      c->q_lo.as<uint8_t>(), c->q_hi.as<uint8_t>(), c->q_pa.as<uint16_t>(),
                      c->q_pb.as<uint16_t>(), st);
+  debug_check("k_parse_query", st);
   CK(c, cudaGetLastError());
   uint64_t launches = 1;
 
@@ -325,6 +330,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     if (c->pair_dots.ensure(6 * npairs * sizeof(uint16_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
     launch_pairs(c->q_pa.as<uint16_t>(), c->q_pb.as<uint16_t>(), ncodes, persons, c->l, r, c->shamir,
                  c->pair_dots.as<uint16_t>(), c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
+    debug_check("k_pairs", st);
     CK(c, cudaGetLastError());
     ++launches;
   }
@@ -397,38 +403,121 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     ta.tap_msb = c->tap_buf[6].as<uint8_t>();
   }
 
-  // ---- DB lanes: column chunks (GEMM then threshold)
-  double gemm_ms = 0, thr_ms = 0;
+  // ---- threshold jobs: one segment per DB column (+ the pair segment); jobs are
+  // column sub-chunks of at most kThrLanes lanes sharing the work buffers
+  double gemm_ms = 0;
   uint64_t gemm_launches = 0;
+  static const uint64_t kThrLanes = [] {
+    const char* e = std::getenv("IRISMPC_THR_LANES");  // test hook: force multi-job splits
+    return e ? std::strtoull(e, nullptr, 10) : (1ull << 26);
+  }();
+  uint64_t chunk = 0;
   if (s_loc && ncols) {
-    size_t freeb = 0, totalb = 0;
-    cudaMemGetInfo(&freeb, &totalb);
-    const uint64_t per_col = 12ull * s_loc;
-    uint64_t budget = std::min<uint64_t>(freeb / 2 + c->dots.cap, 8ull << 30);
-    uint64_t chunk = std::max<uint64_t>(kGemmBN, (budget / per_col) / kGemmBN * kGemmBN);
+    // dot-buffer budget, sized once per context (cudaMemGetInfo takes the RM lock)
+    if (!c->dots_budget) {
+      size_t freeb = 0, totalb = 0;
+      cudaMemGetInfo(&freeb, &totalb);
+      c->dots_budget = std::min<uint64_t>(freeb / 3, 12ull << 30);
+    }
+    const uint64_t per_col = 30ull * s_loc;  // dots 12 B + ml_rs 6 B + diff 12 B per lane
+    uint64_t budget = std::max<uint64_t>(c->dots_budget, c->dots.cap + c->ml_rs.cap + c->diff.cap);
+    chunk = std::max<uint64_t>(kGemmBN, (budget / per_col) / kGemmBN * kGemmBN);
     chunk = std::min<uint64_t>(chunk, ncols_pad);
-    if (c->dots.ensure(6 * chunk * s_loc * sizeof(uint16_t)))
-      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dot buffer)");
-    if (ensure_host_segs(c, ncols + 1)) return IRISMPC_GPU_ERR_DEVICE;
-    if (c->segs.ensure((ncols + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
-    // one segment per column; task_begin is relative to the column chunk
-    std::vector<uint64_t> chunk_tasks;
+  }
+  struct Job {
+    uint64_t seg0, nseg, ntasks, ngrp, ngblk, gwords, chunk_c0;
+    bool pair;
+  };
+  std::vector<Job> jobs;
+  const uint64_t nsegs_all = (s_loc ? ncols : 0) + (npairs ? 1 : 0);
+  if (ensure_host_segs(c, nsegs_all + 1)) return IRISMPC_GPU_ERR_DEVICE;
+  if (c->segs.ensure((nsegs_all + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
+  auto add_job = [&](uint64_t seg0, uint64_t nseg, bool pair, uint64_t cc0) {
+    Job j{seg0, nseg, 0, 0, 0, 0, cc0, pair};
+    for (uint64_t i = seg0; i < seg0 + nseg; ++i) {
+      Seg& sg = c->h_segs_pinned[i];
+      sg.q_first = sg.lane_begin / 1024;
+      sg.w_first = sg.lane_begin / 64;
+      sg.task_begin = j.ntasks;
+      sg.grp_begin = j.ngrp;
+      sg.gblk_begin = j.ngblk;
+      sg.g_off = j.gwords;
+      const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
+      j.ntasks += (sg.lane_end - 1) / 1024 - sg.q_first + 1;
+      j.ngrp += (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
+      j.ngblk += 3ull * 125 * (nw / 8 + 2);
+      j.gwords += 3ull * 125 * nw;
+    }
+    jobs.push_back(j);
+  };
+  uint64_t cstride = 0;
+  if (s_loc && ncols) {
     for (uint64_t c0 = 0; c0 < ncols; c0 += chunk) {
       const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
-      uint64_t ntasks = 0;
       for (uint64_t col = c0; col < c1; ++col) {
         Seg& sg = c->h_segs_pinned[col];
         sg.lane_begin = col * S + row_off;
         sg.lane_end = sg.lane_begin + s_loc;
         sg.src = (col - c0) * s_loc;
-        sg.q_first = sg.lane_begin / 1024;
-        sg.task_begin = ntasks;
         sg.slot = (int64_t)col_slot[col];
-        ntasks += (sg.lane_end - 1) / 1024 - sg.q_first + 1;
       }
-      chunk_tasks.push_back(ntasks);
+      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / s_loc);
+      for (uint64_t a = c0; a < c1; a += per_job) add_job(a, std::min<uint64_t>(per_job, c1 - a), false, c0);
+      cstride = std::max<uint64_t>(cstride, (c1 - c0) * s_loc);
     }
-    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, ncols * sizeof(Seg), cudaMemcpyHostToDevice, st));
+  }
+  if (npairs) {
+    Seg& sg = c->h_segs_pinned[nsegs_all - 1];
+    sg.lane_begin = ncols * S;
+    sg.lane_end = n;
+    sg.src = 0;
+    sg.slot = -1;
+    add_job(nsegs_all - 1, 1, true, 0);
+    cstride = std::max<uint64_t>(cstride, npairs);
+  }
+  uint64_t max_g = 0, max_bits = 0;
+  for (const Job& j : jobs) {
+    max_g = std::max(max_g, j.gwords);
+    max_bits = std::max(max_bits, j.ntasks * 32);
+  }
+  if (nsegs_all) {
+    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
+    if ((s_loc && ncols && c->dots.ensure(6 * chunk * s_loc * sizeof(uint16_t))) ||
+        c->ml_rs.ensure(3 * cstride * sizeof(uint16_t) + 16) || c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) ||
+        c->gate.ensure(max_g * sizeof(uint64_t) + 16) || c->bits.ensure(6 * max_bits * sizeof(uint32_t) + 16))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
+  }
+  ta.ml_rs = c->ml_rs.as<uint16_t>();
+  ta.diff = c->diff.as<uint32_t>();
+  ta.cstride = cstride;
+  ta.gate = c->gate.as<uint64_t>();
+  uint64_t task_off = 0;
+  auto run_job = [&](const Job& j, const uint16_t* src_base, uint64_t pstride_hd, uint64_t off_ml) -> int {
+    ThrArgs t = ta;
+    t.segs = c->segs.as<Seg>() + j.seg0;
+    t.nsegs = (uint32_t)j.nseg;
+    t.ntasks = j.ntasks;
+    t.ngrp = j.ngrp;
+    t.ngblk = j.ngblk;
+    t.bits = c->bits.as<uint32_t>();
+    t.nbits = j.ntasks * 32;
+    t.or_elem_base = ta.or_elem_base + task_off * 64;
+    task_off += j.ntasks;
+    for (int p = 0; p < 3; ++p) {
+      t.hd[p] = src_base + p * pstride_hd;
+      t.ml[p] = src_base + p * pstride_hd + off_ml;
+      t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
+    }
+    t.match_w0 = j.pair ? match_w0 : 0;
+    launch_threshold(t, st);
+    CK(c, cudaGetLastError());
+    launches += 5;
+    return 0;
+  };
+
+  // ---- DB lanes: per column chunk, GEMM then its threshold jobs
+  if (s_loc && ncols) {
+    size_t ji = 0;
     for (uint64_t c0 = 0, ci = 0; c0 < ncols; c0 += chunk, ++ci) {
       const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
       GemmArgs g{};
@@ -443,9 +532,17 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       g.out = c->dots.as<uint16_t>();
       g.out_pstride = (c1 - c0) * s_loc;
       g.out_cstride = (uint32_t)s_loc;
+      while (c->gev.size() < 2 * (ci + 1)) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));
+        c->gev.push_back(e);
+      }
+      CK(c, cudaEventRecord(c->gev[2 * ci], st));
       launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(c->s_pad / kGemmBM),
                   (uint32_t)ceil_div(c1 - c0, kGemmBN), st);
+      debug_check("k_limb_gemm", st);
       CK(c, cudaGetLastError());
+      CK(c, cudaEventRecord(c->gev[2 * ci + 1], st));
       ++gemm_launches;
       ++launches;
       if (c->taps && c->cfg.db_rows_total == 0) {
@@ -459,20 +556,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                                 cudaMemcpyDeviceToDevice, st));
         }
       }
-      const uint64_t ntasks = chunk_tasks[ci];
-      ThrArgs t = ta;
-      t.segs = c->segs.as<Seg>() + c0;
-      t.nsegs = (uint32_t)(c1 - c0);
-      t.ntasks = ntasks;
-      for (int p = 0; p < 3; ++p) {
-        t.hd[p] = c->dots.as<uint16_t>() + (2 * p) * g.out_pstride;
-        t.ml[p] = c->dots.as<uint16_t>() + (2 * p + 1) * g.out_pstride;
-        t.match[p] = dbg ? c->match[p].as<uint32_t>() : nullptr;
+      for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk_c0 == c0; ++ji) {
+        int rc2 = run_job(jobs[ji], c->dots.as<uint16_t>(), 2 * g.out_pstride, g.out_pstride);
+        if (rc2) return rc2;
       }
-      t.match_w0 = 0;
-      launch_threshold(t, st);
-      CK(c, cudaGetLastError());
-      ++launches;
     }
   }
   CK(c, cudaEventRecord(c->ev[2], st));
@@ -489,29 +576,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                               cudaMemcpyDeviceToDevice, st));
       }
     }
-    if (ensure_host_segs(c, 1)) return IRISMPC_GPU_ERR_DEVICE;
-    if (c->segs.ensure(sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
-    Seg& sg = c->h_segs_pinned[0];
-    sg.lane_begin = ncols * S;
-    sg.lane_end = n;
-    sg.src = 0;
-    sg.q_first = sg.lane_begin / 1024;
-    sg.task_begin = 0;
-    sg.slot = -1;
-    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, sizeof(Seg), cudaMemcpyHostToDevice, st));
-    ThrArgs t = ta;
-    t.segs = c->segs.as<Seg>();
-    t.nsegs = 1;
-    t.ntasks = (sg.lane_end - 1) / 1024 - sg.q_first + 1;
-    for (int p = 0; p < 3; ++p) {
-      t.hd[p] = c->pair_dots.as<uint16_t>() + p * 2 * npairs;
-      t.ml[p] = c->pair_dots.as<uint16_t>() + p * 2 * npairs + npairs;
-      t.match[p] = c->match[p].as<uint32_t>();
-    }
-    t.match_w0 = match_w0;
-    launch_threshold(t, st);
-    CK(c, cudaGetLastError());
-    ++launches;
+    int rc2 = run_job(jobs.back(), c->pair_dots.as<uint16_t>(), 2 * npairs, npairs);
+    if (rc2) return rc2;
   }
   CK(c, cudaEventRecord(c->ev[3], st));
 
@@ -529,6 +595,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   oa.elem_base = (qid << 48) | (rank << 40);
   oa.out = c->person_out.as<uint8_t>();
   launch_or_persons(oa, st);
+  debug_check("k_or_persons", st);
   CK(c, cudaGetLastError());
   ++launches;
 
@@ -586,15 +653,18 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     stats->wall_ms = ms;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     stats->prep_ms = ms;
-    cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]);
+    for (uint64_t i = 0; i < gemm_launches; ++i) {
+      cudaEventElapsedTime(&ms, c->gev[2 * i], c->gev[2 * i + 1]);
+      gemm_ms += ms;
+    }
     stats->gemm_ms = gemm_ms;
-    stats->threshold_ms = ms;  // gemm + threshold interleaved per chunk
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]);
+    stats->threshold_ms = ms - gemm_ms;  // chunks interleave GEMM and threshold
     cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
     stats->or_ms = ms;
     stats->gemm_launches = gemm_launches;
     stats->kernel_launches = launches;
   }
-  (void)thr_ms;
   return 0;
 }
 
@@ -672,11 +742,13 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   cudaStreamSynchronize(c->st);
   Buf* bufs[] = {&c->db_lo, &c->db_hi, &c->q_lo, &c->q_hi, &c->q_pa, &c->q_pb, &c->q_pay[0], &c->q_pay[1],
                  &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial, &c->slot_begin,
-                 &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out};
+                 &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
   for (Buf* b : bufs) b->release();
   for (auto& t : c->tap_buf) t.release();
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->gev) cudaEventDestroy(e);
   cudaStreamDestroy(c->st);
   delete c;
 }

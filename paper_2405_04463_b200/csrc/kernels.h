@@ -10,6 +10,10 @@
 
 namespace irisgpu {
 
+// IRISMPC_DEBUG_SYNC=1: synchronize after every launch and abort with the
+// kernel's name on a device fault (no sanitizer on this pool).
+void debug_check(const char* what, cudaStream_t st);
+
 // ---- K1 prep / dealer (prep.cu)
 void set_lambda(const uint16_t lam[6]);
 void launch_parse_db(const uint8_t* pay, uint64_t nrows, uint64_t row0, uint32_t l, uint32_t l_pad,
@@ -60,22 +64,33 @@ void launch_pairs(const uint16_t* pa, const uint16_t* pb, uint32_t ncodes, uint3
 // ---- K4 threshold (threshold.cu)
 struct Seg {
   uint64_t lane_begin, lane_end;  // global lanes [begin, end)
-  uint64_t src;                   // dot-buffer index of lane_begin
-  uint64_t task_begin;            // first task (warp block) of this segment
+  uint64_t src;                   // chunk-buffer index of lane_begin
+  uint64_t task_begin;            // first 1024-lane task of this segment (chunk-relative)
   uint64_t q_first;               // lane_begin / 1024
+  uint64_t w_first;               // lane_begin / 64 (first reference word)
+  uint64_t g_off;                 // u64 offset of this segment's gate randomness block
+  uint64_t grp_begin;             // first 8-lane group (chunk-relative)
+  uint64_t gblk_begin;            // first gate-keystream thread (chunk-relative)
   int64_t slot;                   // partial slot of its first task, -1 = no fused OR
 };
 
 struct ThrArgs {
   const Seg* segs;
   uint32_t nsegs;
-  uint64_t ntasks;
+  uint64_t ntasks, ngrp, ngblk;
   const uint16_t* hd[3];
   const uint16_t* ml[3];
   uint64_t n, W;
   uint64_t pos[3];
   SeedKey key[3];
   uint32_t a, b;
+  // chunk work buffers
+  uint64_t* gate;        // gate randomness, per segment [3*125][nwords]
+  uint16_t* ml_rs;       // [3][cstride] reshared ml
+  uint32_t* diff;        // [3][cstride] a*ml32 - b*hd
+  uint64_t cstride;
+  uint32_t* bits;        // [6][nbits] injected-bit rows (bit16 comps, bit17 comps)
+  uint64_t nbits;
   uint32_t* match[3];    // optional 32-lane words (atomicOr), word = lane/32 - match_w0
   uint64_t match_w0;
   uint8_t* partial;      // [3][nslots]

@@ -35,21 +35,28 @@ __global__ void k_pairs(const uint16_t* __restrict__ pa, const uint16_t* __restr
   const uint64_t xbase = ((uint64_t)prob * ncodes + 2 * i + ea) * l;
   const uint64_t ybase = ((uint64_t)prob * ncodes + 2 * j + eb) * l;
   uint32_t acc = 0;
+  // rotated index src = (kk - by) mod len, advanced by 32 with a conditional wrap
   if (shamir) {
     const uint32_t h = l / 2;
-    const int64_t bp = by / 2;
-    for (uint32_t kk = lane; kk < l; kk += 32) {
-      const uint32_t seg = kk >= h ? h : 0;
-      int64_t src = ((int64_t)(kk - seg) - bp) % (int64_t)h;
-      if (src < 0) src += h;
-      acc += (uint32_t)pa[xbase + seg + src] * (uint32_t)pb[ybase + kk];
+    int64_t bp = (by / 2) % (int64_t)h;
+    if (bp < 0) bp += h;
+    for (uint32_t seg = 0; seg < l; seg += h) {
+      uint32_t src = (uint32_t)((lane + h - (uint32_t)bp) % h);
+      for (uint32_t kk = lane; kk < h; kk += 32) {
+        acc += (uint32_t)pa[xbase + seg + src] * (uint32_t)pb[ybase + seg + kk];
+        src += 32;
+        while (src >= h) src -= h;
+      }
     }
   } else {
+    int64_t b0 = by % (int64_t)l;
+    if (b0 < 0) b0 += l;
+    uint32_t src = (uint32_t)((lane + l - (uint32_t)b0) % l);
     for (uint32_t kk = lane; kk < l; kk += 32) {
-      int64_t src = ((int64_t)kk - by) % (int64_t)l;
-      if (src < 0) src += l;
       acc += (uint32_t)pa[xbase + src] * (uint32_t)pa[ybase + kk];
       acc -= (uint32_t)pb[xbase + src] * (uint32_t)pb[ybase + kk];
+      src += 32;
+      while (src >= l) src -= l;
     }
   }
 #pragma unroll

@@ -215,3 +215,31 @@ def test_full_size_synthetic_planted_match():
     m = sess.batch_query(outs, persons)
     assert m[0] == 1 and m[1:].sum() == 0
     assert sess.last_stats.lanes == P.lane_count(persons, s, 31)
+
+
+def test_threshold_job_splits(monkeypatch):
+    """The threshold runs in column sub-chunks ("jobs"); splits must not change anything."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys, numpy as np
+        sys.path.insert(0, '.')
+        import paper_2405_04463_b200 as P
+        from oracle import pyoracle as O
+        l, s, persons, seed = 256, 3000, 3, 61
+        rng = O.Rng(seed)
+        dc, dm = O.records(rng, l, s, 0.9)
+        qc, qm = O.records(rng, l, 2 * persons, 0.9)
+        qc[2], qm[2] = dc[17], dm[17]
+        cfg = P.EngineConfig(backend=P.SHAMIR, l=l, rotations=5, debug_rows=True)
+        m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, want_rows=True)
+        ref = O.run_local(O.make_config(O.SHAMIR, l, 0.375, 5, True), seed, dc, dm, qc, qm, persons)
+        n = P.lane_count(persons, s, 5)
+        assert (m == ref.person_match).all(), (m, ref.person_match)
+        assert (sess.row_bits[:n] == ref.row_bits).all()
+        print("ok", m)
+    """)
+    import os
+    env = dict(os.environ, IRISMPC_THR_LANES="7000")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout + r.stderr

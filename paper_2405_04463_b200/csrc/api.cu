@@ -124,7 +124,7 @@ uint64_t ref_or_draws(uint64_t groups, uint64_t len, uint64_t* rounds, uint64_t*
 struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr;
   int shamir = 0;
   uint32_t l = 0, l_pad = 0, nseg = 1;
   SeedKey keys[3];
@@ -153,6 +153,7 @@ struct irismpc_gpu_ctx {
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
   std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
+  std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done / threshold done
 };
 
 namespace {
@@ -216,7 +217,7 @@ int alloc_planes(irismpc_gpu_ctx* c, uint64_t s) {
   c->db_hi.release();
   c->db_loaded = false;
   c->s = s;
-  c->s_pad = round_up(s ? s : 1, kGemmBM);
+  c->s_pad = round_up(s ? s : 1, 2 * kGemmBM);  // CTA-pair tiles cover 256 rows
   const size_t bytes = 6ull * c->s_pad * c->l_pad;
   if (c->db_lo.ensure(bytes) || c->db_hi.ensure(bytes))
     return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for the DB planes");
@@ -259,8 +260,8 @@ int ensure_query_buffers(irismpc_gpu_ctx* c, uint32_t ncodes, uint32_t ncols_pad
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query planes");
     CK(c, cudaMemsetAsync(c->q_lo.p, 0, bplane, c->st));
     CK(c, cudaMemsetAsync(c->q_hi.p, 0, bplane, c->st));
-    if (make_plane_tmap(&c->tB_lo, c->q_lo.p, 6ull * c->nseg * ncols_pad, c->l_pad, kGemmBN) ||
-        make_plane_tmap(&c->tB_hi, c->q_hi.p, 6ull * c->nseg * ncols_pad, c->l_pad, kGemmBN))
+    if (make_plane_tmap(&c->tB_lo, c->q_lo.p, 6ull * c->nseg * ncols_pad, c->l_pad, 128) ||
+        make_plane_tmap(&c->tB_hi, c->q_hi.p, 6ull * c->nseg * ncols_pad, c->l_pad, 128))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the query planes");
     c->ncols_pad_cur = ncols_pad;
   }
@@ -281,6 +282,11 @@ int ensure_host_segs(irismpc_gpu_ctx* c, size_t n) {
 
 // Core query on device payloads.  mode 0: final (open into match_out host),
 // 1: partial (component bits into partial_dev).
+//
+// DB lanes run in row chunks: K2 GEMM(chunk i) on stream st while the K4
+// threshold pipeline of chunk i-1 runs on stream st2 (tensor pipe vs ALU
+// pipes), dot outputs double-buffered.  The pair lanes, the per-person OR and
+// the open follow on st2 / st.
 int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3], uint32_t persons,
               int membership, int mode, uint8_t* match_out, uint8_t* row_bits_out, uint8_t* partial_dev,
               irismpc_gpu_stats* stats, bool host_input, const uint8_t* const hq[3]) {
@@ -306,8 +312,11 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint32_t ngroups = membership ? 1u : persons;
   const uint64_t qid = c->query_id++;
   const uint64_t rank = c->cfg.shard_rank;
+  const uint64_t s_loc = c->s;
+  const uint64_t row_off = c->cfg.db_row_offset;
+  cudaStream_t st = c->st, st2 = c->st2;
+  uint64_t launches = 0;
 
-  cudaStream_t st = c->st;
   CK(c, cudaEventRecord(c->ev[0], st));
   const uint8_t* dqp[3] = {dq[0], dq[1], dq[2]};
   if (host_input) {
@@ -324,8 +333,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                      c->q_pb.as<uint16_t>(), st);
   debug_check("k_parse_query", st);
   CK(c, cudaGetLastError());
-  uint64_t launches = 1;
-
+  ++launches;
   if (npairs) {
     if (c->pair_dots.ensure(6 * npairs * sizeof(uint16_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
     launch_pairs(c->q_pa.as<uint16_t>(), c->q_pb.as<uint16_t>(), ncodes, persons, c->l, r, c->shamir,
@@ -336,7 +344,6 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   CK(c, cudaEventRecord(c->ev[1], st));
 
-  // ---- taps
   if (c->taps) {
     c->tap_n = n;
     const size_t sz[7] = {2, 2, 2, 2, 4, 4, 1};
@@ -346,16 +353,27 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
   }
 
-  // ---- per-person slot ranges (fused OR partials) and debug/pair match words
-  const uint64_t s_loc = c->s;
-  const uint64_t row_off = c->cfg.db_row_offset;
+  // ---- row-chunk plan
+  uint64_t rows_chunk = 0, nchunks = 0;
+  if (s_loc && ncols) {
+    static const uint64_t target = [] {
+      const char* e = std::getenv("IRISMPC_CHUNK_LANES");  // test hook
+      return e ? std::strtoull(e, nullptr, 10) : (1ull << 24);
+    }();
+    rows_chunk = round_up(std::max<uint64_t>(target / ncols, 1), 2 * kGemmBM);
+    rows_chunk = std::min<uint64_t>(rows_chunk, round_up(s_loc, 2 * kGemmBM));
+    nchunks = ceil_div(s_loc, rows_chunk);
+  }
+  auto chunk_rows = [&](uint64_t i) { return std::min<uint64_t>(rows_chunk, s_loc - i * rows_chunk); };
+  auto seg_tasks = [](uint64_t lb, uint64_t le) { return (le - 1) / 1024 - lb / 1024 + 1; };
+  // fused-OR slots: per column contiguous (all its lanes belong to one person)
   std::vector<uint64_t> col_slot(ncols + 1, 0);
   uint64_t total_slots = 0;
   for (uint64_t col = 0; col < ncols; ++col) {
     col_slot[col] = total_slots;
-    if (s_loc) {
-      const uint64_t lb = col * S + row_off, le = lb + s_loc;
-      total_slots += (le - 1) / 1024 - lb / 1024 + 1;
+    for (uint64_t i = 0; i < nchunks; ++i) {
+      const uint64_t lb = col * S + row_off + i * rows_chunk;
+      total_slots += seg_tasks(lb, lb + chunk_rows(i));
     }
   }
   col_slot[ncols] = total_slots;
@@ -376,64 +394,22 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     match_w0 = (ncols * S) / 32;
     match_words = ceil_div(n, 32) - match_w0 + 1;
   }
-  if (match_words) {
-    for (int p = 0; p < 3; ++p) {
-      if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
-      CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
-    }
+  for (int p = 0; p < 3 && match_words; ++p) {
+    if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
+    CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
   }
 
-  ThrArgs ta{};
-  ta.n = n;
-  ta.W = W;
-  for (int k = 0; k < 3; ++k) {
-    ta.pos[k] = c->pos[k];
-    ta.key[k] = c->keys[k];
-  }
-  ta.a = c->cfg.a;
-  ta.b = c->cfg.b;
-  ta.partial = c->partial.as<uint8_t>();
-  ta.nslots = total_slots;
-  ta.or_elem_base = (qid << 48) | (rank << 40);
-  if (c->taps) {
-    ta.tap_rs_hd = c->tap_buf[2].as<uint16_t>();
-    ta.tap_rs_ml = c->tap_buf[3].as<uint16_t>();
-    ta.tap_ml32 = c->tap_buf[4].as<uint32_t>();
-    ta.tap_diff = c->tap_buf[5].as<uint32_t>();
-    ta.tap_msb = c->tap_buf[6].as<uint8_t>();
-  }
-
-  // ---- threshold jobs: one segment per DB column (+ the pair segment); jobs are
-  // column sub-chunks of at most kThrLanes lanes sharing the work buffers
-  double gemm_ms = 0;
-  uint64_t gemm_launches = 0;
-  static const uint64_t kThrLanes = [] {
-    const char* e = std::getenv("IRISMPC_THR_LANES");  // test hook: force multi-job splits
-    return e ? std::strtoull(e, nullptr, 10) : (1ull << 26);
-  }();
-  uint64_t chunk = 0;
-  if (s_loc && ncols) {
-    // dot-buffer budget, sized once per context (cudaMemGetInfo takes the RM lock)
-    if (!c->dots_budget) {
-      size_t freeb = 0, totalb = 0;
-      cudaMemGetInfo(&freeb, &totalb);
-      c->dots_budget = std::min<uint64_t>(freeb / 3, 12ull << 30);
-    }
-    const uint64_t per_col = 30ull * s_loc;  // dots 12 B + ml_rs 6 B + diff 12 B per lane
-    uint64_t budget = std::max<uint64_t>(c->dots_budget, c->dots.cap + c->ml_rs.cap + c->diff.cap);
-    chunk = std::max<uint64_t>(kGemmBN, (budget / per_col) / kGemmBN * kGemmBN);
-    chunk = std::min<uint64_t>(chunk, ncols_pad);
-  }
+  // ---- segments [chunk][col] then the pair segment; jobs group segments
   struct Job {
-    uint64_t seg0, nseg, ntasks, ngrp, ngblk, gwords, chunk_c0;
+    uint64_t seg0, nseg, ntasks, ngrp, ngblk, gwords, chunk;
     bool pair;
   };
   std::vector<Job> jobs;
-  const uint64_t nsegs_all = (s_loc ? ncols : 0) + (npairs ? 1 : 0);
+  const uint64_t nsegs_all = nchunks * ncols + (npairs ? 1 : 0);
   if (ensure_host_segs(c, nsegs_all + 1)) return IRISMPC_GPU_ERR_DEVICE;
   if (c->segs.ensure((nsegs_all + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
-  auto add_job = [&](uint64_t seg0, uint64_t nseg, bool pair, uint64_t cc0) {
-    Job j{seg0, nseg, 0, 0, 0, 0, cc0, pair};
+  auto add_job = [&](uint64_t seg0, uint64_t nseg, bool pair, uint64_t chunk) {
+    Job j{seg0, nseg, 0, 0, 0, 0, chunk, pair};
     for (uint64_t i = seg0; i < seg0 + nseg; ++i) {
       Seg& sg = c->h_segs_pinned[i];
       sg.q_first = sg.lane_begin / 1024;
@@ -443,27 +419,34 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       sg.gblk_begin = j.ngblk;
       sg.g_off = j.gwords;
       const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
-      j.ntasks += (sg.lane_end - 1) / 1024 - sg.q_first + 1;
+      j.ntasks += seg_tasks(sg.lane_begin, sg.lane_end);
       j.ngrp += (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
       j.ngblk += 3ull * 125 * (nw / 8 + 2);
       j.gwords += 3ull * 125 * nw;
     }
     jobs.push_back(j);
   };
+  static const uint64_t kThrLanes = [] {
+    const char* e = std::getenv("IRISMPC_THR_LANES");  // test hook: force multi-job splits
+    return e ? std::strtoull(e, nullptr, 10) : (1ull << 26);
+  }();
   uint64_t cstride = 0;
-  if (s_loc && ncols) {
-    for (uint64_t c0 = 0; c0 < ncols; c0 += chunk) {
-      const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
-      for (uint64_t col = c0; col < c1; ++col) {
-        Seg& sg = c->h_segs_pinned[col];
-        sg.lane_begin = col * S + row_off;
-        sg.lane_end = sg.lane_begin + s_loc;
-        sg.src = (col - c0) * s_loc;
-        sg.slot = (int64_t)col_slot[col];
+  {
+    std::vector<uint64_t> col_fill(col_slot.begin(), col_slot.end());
+    for (uint64_t i = 0; i < nchunks; ++i) {
+      const uint64_t nr = chunk_rows(i);
+      for (uint64_t col = 0; col < ncols; ++col) {
+        Seg& sg = c->h_segs_pinned[i * ncols + col];
+        sg.lane_begin = col * S + row_off + i * rows_chunk;
+        sg.lane_end = sg.lane_begin + nr;
+        sg.src = col * nr;
+        sg.slot = (int64_t)col_fill[col];
+        col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
-      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / s_loc);
-      for (uint64_t a = c0; a < c1; a += per_job) add_job(a, std::min<uint64_t>(per_job, c1 - a), false, c0);
-      cstride = std::max<uint64_t>(cstride, (c1 - c0) * s_loc);
+      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
+      for (uint64_t a = 0; a < ncols; a += per_job)
+        add_job(i * ncols + a, std::min<uint64_t>(per_job, ncols - a), false, i);
+      cstride = std::max<uint64_t>(cstride, ncols * nr);
     }
   }
   if (npairs) {
@@ -480,17 +463,38 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     max_g = std::max(max_g, j.gwords);
     max_bits = std::max(max_bits, j.ntasks * 32);
   }
+  const uint64_t dots_half = 6 * ncols * rows_chunk;  // one dot buffer (u16 elements)
   if (nsegs_all) {
     CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
-    if ((s_loc && ncols && c->dots.ensure(6 * chunk * s_loc * sizeof(uint16_t))) ||
+    if ((nchunks && c->dots.ensure(2 * dots_half * sizeof(uint16_t))) ||
         c->ml_rs.ensure(3 * cstride * sizeof(uint16_t) + 16) || c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) ||
         c->gate.ensure(max_g * sizeof(uint64_t) + 16) || c->bits.ensure(6 * max_bits * sizeof(uint32_t) + 16))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
+
+  ThrArgs ta{};
+  ta.n = n;
+  ta.W = W;
+  for (int k = 0; k < 3; ++k) {
+    ta.pos[k] = c->pos[k];
+    ta.key[k] = c->keys[k];
+  }
+  ta.a = c->cfg.a;
+  ta.b = c->cfg.b;
+  ta.partial = c->partial.as<uint8_t>();
+  ta.nslots = total_slots;
+  ta.or_elem_base = (qid << 48) | (rank << 40);
   ta.ml_rs = c->ml_rs.as<uint16_t>();
   ta.diff = c->diff.as<uint32_t>();
   ta.cstride = cstride;
   ta.gate = c->gate.as<uint64_t>();
+  if (c->taps) {
+    ta.tap_rs_hd = c->tap_buf[2].as<uint16_t>();
+    ta.tap_rs_ml = c->tap_buf[3].as<uint16_t>();
+    ta.tap_ml32 = c->tap_buf[4].as<uint32_t>();
+    ta.tap_diff = c->tap_buf[5].as<uint32_t>();
+    ta.tap_msb = c->tap_buf[6].as<uint8_t>();
+  }
   uint64_t task_off = 0;
   auto run_job = [&](const Job& j, const uint16_t* src_base, uint64_t pstride_hd, uint64_t off_ml) -> int {
     ThrArgs t = ta;
@@ -509,60 +513,76 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
-    launch_threshold(t, st);
+    launch_threshold(t, st2);
     CK(c, cudaGetLastError());
     launches += 5;
     return 0;
   };
-
-  // ---- DB lanes: per column chunk, GEMM then its threshold jobs
-  if (s_loc && ncols) {
-    size_t ji = 0;
-    for (uint64_t c0 = 0, ci = 0; c0 < ncols; c0 += chunk, ++ci) {
-      const uint64_t c1 = std::min<uint64_t>(ncols, c0 + chunk);
-      GemmArgs g{};
-      g.s_pad = (uint32_t)c->s_pad;
-      g.nb_rows = ncols_pad;
-      g.nkb_seg = c->l_pad / kGemmBK;
-      g.nseg = c->nseg;
-      g.rep = c->shamir ? 0 : 1;
-      g.s_valid = (uint32_t)s_loc;
-      g.col0 = (uint32_t)c0;
-      g.ncols = (uint32_t)(c1 - c0);
-      g.out = c->dots.as<uint16_t>();
-      g.out_pstride = (c1 - c0) * s_loc;
-      g.out_cstride = (uint32_t)s_loc;
-      while (c->gev.size() < 2 * (ci + 1)) {
-        cudaEvent_t e;
-        CK(c, cudaEventCreate(&e));
-        c->gev.push_back(e);
-      }
-      CK(c, cudaEventRecord(c->gev[2 * ci], st));
-      launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(c->s_pad / kGemmBM),
-                  (uint32_t)ceil_div(c1 - c0, kGemmBN), st);
-      debug_check("k_limb_gemm", st);
-      CK(c, cudaGetLastError());
-      CK(c, cudaEventRecord(c->gev[2 * ci + 1], st));
-      ++gemm_launches;
-      ++launches;
-      if (c->taps && c->cfg.db_rows_total == 0) {
-        // L1 tap: lanes [c0*s, c1*s) are contiguous in the dot buffer
-        for (int p = 0; p < 3; ++p) {
-          CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint16_t>() + p * n + c0 * s_loc,
-                                c->dots.as<uint16_t>() + (2 * p) * g.out_pstride, g.out_pstride * 2,
-                                cudaMemcpyDeviceToDevice, st));
-          CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint16_t>() + p * n + c0 * s_loc,
-                                c->dots.as<uint16_t>() + (2 * p + 1) * g.out_pstride, g.out_pstride * 2,
-                                cudaMemcpyDeviceToDevice, st));
-        }
-      }
-      for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk_c0 == c0; ++ji) {
-        int rc2 = run_job(jobs[ji], c->dots.as<uint16_t>(), 2 * g.out_pstride, g.out_pstride);
-        if (rc2) return rc2;
-      }
+  auto ensure_events = [&](std::vector<cudaEvent_t>& v, size_t n_) -> int {
+    while (v.size() < n_) {
+      cudaEvent_t e;
+      CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      v.push_back(e);
     }
+    return 0;
+  };
+  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1)) return IRISMPC_GPU_ERR_DEVICE;
+  while (c->gev.size() < 2 * nchunks) {
+    cudaEvent_t e;
+    CK(c, cudaEventCreate(&e));
+    c->gev.push_back(e);
   }
-  CK(c, cudaEventRecord(c->ev[2], st));
+
+  // st2 starts once the prep on st (payload parse, pairs, memsets, uploads) is queued before it
+  CK(c, cudaEventRecord(c->evg[nchunks], st));
+  CK(c, cudaStreamWaitEvent(st2, c->evg[nchunks], 0));
+  CK(c, cudaEventRecord(c->ev[2], st2));
+
+  // ---- DB lanes: GEMM(i) on st || threshold(i-1) on st2
+  double gemm_ms = 0;
+  uint64_t gemm_launches = 0;
+  size_t ji = 0;
+  for (uint64_t i = 0; i < nchunks; ++i) {
+    const uint64_t nr = chunk_rows(i);
+    uint16_t* dots = c->dots.as<uint16_t>() + (i % 2) * dots_half;
+    if (i >= 2) CK(c, cudaStreamWaitEvent(st, c->evt[i - 2], 0));  // buffer i%2 released
+    GemmArgs g{};
+    g.s_pad = (uint32_t)c->s_pad;
+    g.nb_rows = ncols_pad;
+    g.nkb_seg = c->l_pad / kGemmBK;
+    g.nseg = c->nseg;
+    g.rep = c->shamir ? 0 : 1;
+    g.s_valid = (uint32_t)nr;
+    g.row0 = (uint32_t)(i * rows_chunk);
+    g.col0 = 0;
+    g.ncols = (uint32_t)ncols;
+    g.out = dots;
+    g.out_pstride = ncols * nr;
+    g.out_cstride = (uint32_t)nr;
+    CK(c, cudaEventRecord(c->gev[2 * i], st));
+    launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM),
+                (uint32_t)ceil_div(ncols, kGemmBN), st);
+    debug_check("k_limb_gemm", st);
+    CK(c, cudaGetLastError());
+    CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
+    ++gemm_launches;
+    ++launches;
+    if (c->taps && c->cfg.db_rows_total == 0) {
+      // L1 tap: dots[(col, row - r0)] -> lane col*S + row
+      for (int p = 0; p < 3; ++p)
+        for (int d = 0; d < 2; ++d)
+          CK(c, cudaMemcpy2DAsync(c->tap_buf[d].as<uint16_t>() + p * n + i * rows_chunk, S * 2,
+                                  dots + (2 * p + d) * g.out_pstride, nr * 2, nr * 2, ncols,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+    CK(c, cudaEventRecord(c->evg[i], st));
+    CK(c, cudaStreamWaitEvent(st2, c->evg[i], 0));
+    for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji) {
+      int rc2 = run_job(jobs[ji], dots, 2 * g.out_pstride, g.out_pstride);
+      if (rc2) return rc2;
+    }
+    CK(c, cudaEventRecord(c->evt[i], st2));
+  }
 
   // ---- pair lanes (shard 0): threshold into match words
   if (npairs) {
@@ -570,18 +590,18 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       for (int p = 0; p < 3; ++p) {
         CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint16_t>() + p * n + ncols * S,
                               c->pair_dots.as<uint16_t>() + p * 2 * npairs, npairs * 2,
-                              cudaMemcpyDeviceToDevice, st));
+                              cudaMemcpyDeviceToDevice, st2));
         CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint16_t>() + p * n + ncols * S,
                               c->pair_dots.as<uint16_t>() + npairs + p * 2 * npairs, npairs * 2,
-                              cudaMemcpyDeviceToDevice, st));
+                              cudaMemcpyDeviceToDevice, st2));
       }
     }
     int rc2 = run_job(jobs.back(), c->pair_dots.as<uint16_t>(), 2 * npairs, npairs);
     if (rc2) return rc2;
   }
-  CK(c, cudaEventRecord(c->ev[3], st));
+  CK(c, cudaEventRecord(c->ev[3], st2));
 
-  // ---- per-person OR
+  // ---- per-person OR (st2), then the open on st
   OrArgs oa{};
   oa.partial = c->partial.as<uint8_t>();
   oa.nslots = total_slots;
@@ -594,15 +614,16 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
   oa.elem_base = (qid << 48) | (rank << 40);
   oa.out = c->person_out.as<uint8_t>();
-  launch_or_persons(oa, st);
-  debug_check("k_or_persons", st);
+  launch_or_persons(oa, st2);
+  debug_check("k_or_persons", st2);
   CK(c, cudaGetLastError());
   ++launches;
+  CK(c, cudaEventRecord(c->evt[nchunks], st2));
+  CK(c, cudaStreamWaitEvent(st, c->evt[nchunks], 0));
 
   if (mode == 0) {
     if (c->open_out.ensure(ngroups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
-    launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, qid << 48,
-                   c->open_out.as<uint8_t>(), st);
+    launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, qid << 48, c->open_out.as<uint8_t>(), st);
     CK(c, cudaGetLastError());
     ++launches;
     CK(c, cudaMemcpyAsync(match_out, c->open_out.p, ngroups, cudaMemcpyDeviceToHost, st));
@@ -658,8 +679,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       gemm_ms += ms;
     }
     stats->gemm_ms = gemm_ms;
-    cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]);
-    stats->threshold_ms = ms - gemm_ms;  // chunks interleave GEMM and threshold
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    stats->threshold_ms = ms;  // stream-2 span: threshold of all chunks (overlaps the GEMMs)
     cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
     stats->or_ms = ms;
     stats->gemm_launches = gemm_launches;
@@ -724,7 +745,12 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   c->l_pad = (uint32_t)round_up(cfg->l, kGemmBK);
   c->nseg = c->shamir ? 1 : 2;
   for (int k = 0; k < 3; ++k) c->keys[k] = key_of(cfg->seeds + 16 * k);
-  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+  // the GEMM stream gets the higher priority: when GEMM and threshold blocks
+  // compete for SM residency the tensor-pipe work is scheduled first
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
     delete c;
     return IRISMPC_GPU_ERR_DEVICE;
   }
@@ -749,6 +775,10 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->gev) cudaEventDestroy(e);
+  for (auto& e : c->evg) cudaEventDestroy(e);
+  for (auto& e : c->evt) cudaEventDestroy(e);
+  cudaStreamSynchronize(c->st2);
+  cudaStreamDestroy(c->st2);
   cudaStreamDestroy(c->st);
   delete c;
 }

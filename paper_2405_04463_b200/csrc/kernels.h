@@ -41,7 +41,8 @@ struct GemmArgs {
   uint32_t nkb_seg;   // k-blocks per K segment (l_pad / 128)
   uint32_t nseg;      // 1 (Shamir) or 2 (replicated [x_p | x_{p-1}])
   uint32_t rep;
-  uint32_t s_valid;   // rows written
+  uint32_t s_valid;   // rows written (relative to row0)
+  uint32_t row0;      // first DB row of this launch (multiple of 256)
   uint32_t col0;      // first B row of this launch (chunk start column)
   uint32_t ncols;     // columns written (from col0)
   uint16_t* out;      // [6][ncols * out_cstride]

@@ -217,8 +217,11 @@ def test_full_size_synthetic_planted_match():
     assert sess.last_stats.lanes == P.lane_count(persons, s, 31)
 
 
-def test_threshold_job_splits(monkeypatch):
-    """The threshold runs in column sub-chunks ("jobs"); splits must not change anything."""
+@pytest.mark.parametrize("chunk_lanes,thr_lanes", [("1000000000", "7000"), ("60000", "1000000000"),
+                                                   ("30000", "7000")])
+def test_threshold_job_splits(chunk_lanes, thr_lanes):
+    """DB lanes run in row chunks (GEMM || threshold on two streams) and each
+    chunk's threshold in column jobs; neither split may change any output."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import sys, numpy as np
@@ -239,7 +242,7 @@ def test_threshold_job_splits(monkeypatch):
         print("ok", m)
     """)
     import os
-    env = dict(os.environ, IRISMPC_THR_LANES="7000")
+    env = dict(os.environ, IRISMPC_THR_LANES=thr_lanes, IRISMPC_CHUNK_LANES=chunk_lanes)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout + r.stderr

@@ -1,0 +1,252 @@
+// irismpc_b200.hpp — header-only C++ host API over the C-ABI (irismpc_gpu.h),
+// shaped like the reference library so existing callers drop in:
+//
+//   reference (/root/reference/proj)                      here
+//   EngineConfig            engine.hpp:33-44        ->    irismpc_b200::EngineConfig
+//   Session<B,16,16>        engine.hpp:225-275      ->    irismpc_b200::Session (all 3 parties, one GPU)
+//   party_batch_query       engine.hpp:311-313      ->    irismpc_b200::ThreePartyGpu::party_batch_query
+//   party_membership        engine.hpp:307-309      ->    irismpc_b200::ThreePartyGpu::party_membership
+//   MembershipResult        engine.hpp:58-66        ->    irismpc_b200::MembershipResult
+//   QueryStats              engine.hpp:46-56        ->    irismpc_b200::QueryStats
+//   Error / BoundsError / TransportError / InconsistentShareError (errors.hpp:22-50)
+//
+// Per-party callers keep their three threads: each calls party_batch_query with
+// its own payloads; the last one to arrive launches the fused 3-party GPU query
+// and every caller returns its MembershipResult (person_match filled at P1, as
+// kOutputParty = p1, engine.hpp:68).
+#pragma once
+
+#include <array>
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "irismpc_gpu.h"
+
+namespace irismpc_b200 {
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct TransportError : Error {  // device failure: the in-process "transport" is the GPU
+  using Error::Error;
+};
+struct BoundsError : Error {
+  using Error::Error;
+};
+struct InconsistentShareError : Error {
+  using Error::Error;
+};
+
+inline void check(int rc, const char* what, const irismpc_gpu_ctx* ctx = nullptr) {
+  if (rc == IRISMPC_GPU_OK) return;
+  std::string msg = std::string(what) + ": " + (ctx ? irismpc_gpu_last_error(ctx) : "");
+  switch (rc) {
+    case IRISMPC_GPU_ERR_BOUNDS: throw BoundsError(msg);
+    case IRISMPC_GPU_ERR_DEVICE: throw TransportError(msg);
+    case IRISMPC_GPU_ERR_INCONSISTENT: throw InconsistentShareError(msg);
+    default: throw Error(msg);
+  }
+}
+
+enum class Backend : std::uint8_t { replicated = 0, shamir = 1 };
+
+struct MatchParams {  // iris.hpp:157-174
+  double match_ratio = 0.375;
+  unsigned m = 16;
+  std::uint32_t a = 1u << 14;
+  std::uint32_t b = 1u << 16;
+  static MatchParams make(double ratio, unsigned m_bits = 16) {
+    if (!(ratio >= 0.0 && ratio <= 0.5)) throw BoundsError("match_ratio must lie in [0, 0.5]");
+    MatchParams p;
+    p.match_ratio = ratio;
+    p.m = m_bits;
+    p.b = 1u << m_bits;
+    const double x = (1.0 - 2.0 * ratio) * p.b;
+    p.a = static_cast<std::uint32_t>(x + 0.5);
+    if (p.a > p.b) p.a = p.b;
+    return p;
+  }
+};
+
+struct EngineConfig {  // engine.hpp:33-44, variant fixed to mpc-lift
+  Backend backend = Backend::shamir;
+  std::uint32_t l = 12800;
+  MatchParams params{};
+  unsigned rotations = 31;
+  bool debug_rows = false;
+};
+
+struct QueryStats {
+  std::string variant = "mpc-lift", backend;
+  std::uint64_t s = 0, l = 0, batch = 0;
+  std::uint64_t dot_bytes = 0, lift_bytes = 0, msb_bytes = 0, or_tree_bytes = 0;
+  std::uint64_t dot_rounds = 0, lift_rounds = 0, msb_rounds = 0, or_tree_rounds = 0;
+  double wall_ms = 0.0;
+};
+
+struct MembershipResult {
+  std::vector<std::uint8_t> person_match;  // filled for P1
+  std::vector<std::uint8_t> row_bits;      // debug mode, P1
+  QueryStats stats;
+  std::uint64_t lane_count = 0;
+};
+
+using Payloads = std::array<std::span<const std::uint8_t>, 3>;
+
+inline std::array<std::uint8_t, 48> seeds_from_master(std::uint64_t seed) {
+  std::array<std::uint8_t, 48> s{};
+  irismpc_gpu_seeds_from_master(seed, s.data());
+  return s;
+}
+
+// All three parties of one DB shard on one B200.
+class Session {
+ public:
+  Session(const EngineConfig& cfg, const std::array<std::uint8_t, 48>& seeds, int device = 0,
+          std::uint32_t shard_rank = 0, std::uint64_t db_rows_total = 0, std::uint64_t db_row_offset = 0)
+      : cfg_(cfg) {
+    irismpc_gpu_config c{};
+    c.backend = static_cast<std::uint32_t>(cfg.backend);
+    c.variant = IRISMPC_GPU_VARIANT_MPC_LIFT;
+    c.l = cfg.l;
+    c.a = cfg.params.a;
+    c.b = cfg.params.b;
+    c.m = cfg.params.m;
+    c.rotations = cfg.rotations;
+    c.debug_rows = cfg.debug_rows ? 1 : 0;
+    for (int i = 0; i < 48; ++i) c.seeds[i] = seeds[i];
+    c.device = device;
+    c.shard_rank = shard_rank;
+    c.db_rows_total = db_rows_total;
+    c.db_row_offset = db_row_offset;
+    check(irismpc_gpu_create(&c, &ctx_), "irismpc_gpu_create");
+  }
+  ~Session() { irismpc_gpu_destroy(ctx_); }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  void load_db(const Payloads& payload, std::uint64_t s) {  // Session::load_db
+    const std::uint8_t* p[3] = {payload[0].data(), payload[1].data(), payload[2].data()};
+    const std::size_t len[3] = {payload[0].size(), payload[1].size(), payload[2].size()};
+    check(irismpc_gpu_load_db(ctx_, p, len, s), "load_db", ctx_);
+    s_ = s;
+  }
+
+  std::array<MembershipResult, 3> batch_query(const Payloads& q, unsigned persons) {
+    return query(q, persons, false);
+  }
+  std::array<MembershipResult, 3> membership(const Payloads& q) { return query(q, 1, true); }
+
+  irismpc_gpu_ctx* raw() { return ctx_; }
+  std::uint64_t rows() const { return s_; }
+
+ private:
+  std::array<MembershipResult, 3> query(const Payloads& q, unsigned persons, bool membership) {
+    const std::uint8_t* p[3] = {q[0].data(), q[1].data(), q[2].data()};
+    const std::size_t len[3] = {q[0].size(), q[1].size(), q[2].size()};
+    const std::uint64_t n = irismpc_gpu_lane_count(persons, s_, membership ? 1 : cfg_.rotations, membership);
+    std::array<MembershipResult, 3> out;
+    auto& o = out[0];
+    o.person_match.resize(persons);
+    if (cfg_.debug_rows) o.row_bits.resize(n);
+    irismpc_gpu_stats st{};
+    const int rc = membership
+                       ? irismpc_gpu_membership(ctx_, p, len, o.person_match.data(),
+                                                cfg_.debug_rows ? o.row_bits.data() : nullptr, &st)
+                       : irismpc_gpu_batch_query(ctx_, p, len, persons, o.person_match.data(),
+                                                 cfg_.debug_rows ? o.row_bits.data() : nullptr, &st);
+    check(rc, membership ? "membership" : "batch_query", ctx_);
+    for (int i = 0; i < 3; ++i) {
+      auto& r = out[i];
+      r.lane_count = n;
+      r.stats.backend = cfg_.backend == Backend::shamir ? "shamir-galois" : "replicated";
+      r.stats.s = st.s;
+      r.stats.l = st.l;
+      r.stats.batch = st.batch;
+      r.stats.dot_bytes = st.dot_bytes[i];
+      r.stats.lift_bytes = st.lift_bytes[i];
+      r.stats.msb_bytes = st.msb_bytes[i];
+      r.stats.or_tree_bytes = st.or_tree_bytes[i];
+      r.stats.dot_rounds = st.dot_rounds;
+      r.stats.lift_rounds = st.lift_rounds;
+      r.stats.msb_rounds = st.msb_rounds;
+      r.stats.or_tree_rounds = st.or_tree_rounds;
+      r.stats.wall_ms = st.wall_ms;
+    }
+    return out;
+  }
+
+  EngineConfig cfg_;
+  irismpc_gpu_ctx* ctx_ = nullptr;
+  std::uint64_t s_ = 0;
+};
+
+// Drop-in for the per-party entry points: three party threads rendezvous and
+// the last arrival runs the fused 3-party query.  The DB is (re)loaded only
+// when the payload spans change (the reference reloads on every call,
+// engine.cpp:404-420; here it stays resident).
+class ThreePartyGpu {
+ public:
+  ThreePartyGpu(const EngineConfig& cfg, std::uint64_t seed, int device = 0)
+      : session_(cfg, seeds_from_master(seed), device) {}
+
+  MembershipResult party_batch_query(unsigned party /* 1..3 */, std::span<const std::uint8_t> db_payload,
+                                     std::uint64_t s, std::span<const std::uint8_t> query_payload, unsigned persons) {
+    return arrive(party, db_payload, s, query_payload, persons, false);
+  }
+  MembershipResult party_membership(unsigned party, std::span<const std::uint8_t> db_payload, std::uint64_t s,
+                                    std::span<const std::uint8_t> query_payload) {
+    return arrive(party, db_payload, s, query_payload, 1, true);
+  }
+
+ private:
+  MembershipResult arrive(unsigned party, std::span<const std::uint8_t> db, std::uint64_t s,
+                          std::span<const std::uint8_t> q, unsigned persons, bool membership) {
+    if (party < 1 || party > 3) throw Error("party must be 1..3");
+    std::unique_lock<std::mutex> lk(mu_);
+    const std::uint64_t gen = gen_;
+    db_[party - 1] = db;
+    q_[party - 1] = q;
+    if (++arrived_ == 3) {
+      arrived_ = 0;
+      try {
+        if (!same(db_, loaded_) || s != session_.rows()) {
+          session_.load_db(db_, s);
+          loaded_ = db_;
+        }
+        results_ = membership ? session_.membership(q_) : session_.batch_query(q_, persons);
+        error_.clear();
+      } catch (const std::exception& e) {
+        error_ = e.what();
+      }
+      ++gen_;
+      cv_.notify_all();
+    } else {
+      cv_.wait(lk, [&] { return gen_ != gen; });
+    }
+    if (!error_.empty()) throw Error(error_);
+    return results_[party - 1];
+  }
+
+  static bool same(const Payloads& a, const Payloads& b) {
+    for (int i = 0; i < 3; ++i)
+      if (a[i].data() != b[i].data() || a[i].size() != b[i].size()) return false;
+    return true;
+  }
+
+  Session session_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  unsigned arrived_ = 0;
+  std::uint64_t gen_ = 0;
+  Payloads db_{}, q_{}, loaded_{};
+  std::array<MembershipResult, 3> results_{};
+  std::string error_;
+};
+
+}  // namespace irismpc_b200

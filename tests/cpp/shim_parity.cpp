@@ -1,0 +1,95 @@
+// C++ drop-in check: three party threads call ThreePartyGpu::party_batch_query
+// (the reference's per-party entry point shape, engine.hpp:311-313) and P1's
+// person_match must equal the oracle's; error paths map to the reference's
+// exception types.  Built and run by tests/test_cpp_shim.py.
+#include <cstdio>
+#include <thread>
+#include <vector>
+
+#include "../../include/irismpc_b200.hpp"
+#include "../../oracle/irismpc_oracle.h"
+
+using namespace irismpc_b200;
+
+int main() {
+  const std::uint32_t l = 12800, persons = 3;
+  const std::uint64_t s = 500, seed = 99;
+  const int be = ORC_SHAMIR;
+  const std::uint32_t wl = l / 64;
+  std::vector<std::uint64_t> dc(s * wl), dm(s * wl), qc(2 * persons * wl), qm(2 * persons * wl);
+  orc_rng* rng = orc_rng_new(seed);
+  for (std::uint64_t r = 0; r < s; ++r) orc_rng_record(rng, l, 0.9, &dc[r * wl], &dm[r * wl]);
+  for (std::uint32_t r = 0; r < 2 * persons; ++r) orc_rng_record(rng, l, 0.9, &qc[r * wl], &qm[r * wl]);
+  orc_rng_free(rng);
+  for (std::uint32_t w = 0; w < wl; ++w) {  // person 1's right eye is DB row 123
+    qc[3 * wl + w] = dc[123 * wl + w];
+    qm[3 * wl + w] = dm[123 * wl + w];
+  }
+  const std::size_t rec = orc_code_record_bytes(be, l) + orc_mask_record_bytes(be, l);
+  std::array<std::vector<std::uint8_t>, 3> db, q;
+  for (int p = 0; p < 3; ++p) {
+    db[p].resize(s * rec);
+    q[p].resize(2 * persons * rec);
+  }
+  orc_rng* dr = orc_rng_sub(seed, 1);
+  orc_rng* qr = orc_rng_sub(seed, 2);
+  orc_deal_payload(be, l, s, dc.data(), dm.data(), dr, db[0].data(), db[1].data(), db[2].data());
+  orc_deal_payload(be, l, 2 * persons, qc.data(), qm.data(), qr, q[0].data(), q[1].data(), q[2].data());
+  orc_rng_free(dr);
+  orc_rng_free(qr);
+
+  orc_config oc{be, l, orc_match_a(0.375), 1u << 16, 31, 0};
+  std::vector<std::uint8_t> want(persons);
+  orc_out out{};
+  out.person_match = want.data();
+  std::uint8_t seeds[48];
+  orc_party_seeds(seed, seeds);
+  if (orc_query(&oc, seeds, db[0].data(), db[1].data(), db[2].data(), s, q[0].data(), q[1].data(),
+                q[2].data(), persons, 0, nullptr, &out) != 0) {
+    std::puts("oracle failed");
+    return 2;
+  }
+
+  EngineConfig cfg;
+  cfg.backend = Backend::shamir;
+  cfg.l = l;
+  cfg.params = MatchParams::make(0.375, 16);
+  cfg.rotations = 31;
+  ThreePartyGpu gpu(cfg, seed);
+  for (int round = 0; round < 2; ++round) {  // second round: DB stays resident
+    std::array<MembershipResult, 3> res;
+    std::vector<std::thread> th;
+    for (unsigned p = 1; p <= 3; ++p)
+      th.emplace_back([&, p] { res[p - 1] = gpu.party_batch_query(p, db[p - 1], s, q[p - 1], persons); });
+    for (auto& t : th) t.join();
+    if (round == 0 && res[0].person_match != want) {
+      std::printf("MISMATCH person_match\n");
+      return 1;
+    }
+    if (res[0].lane_count != irismpc_gpu_lane_count(persons, s, 31, 0)) return 1;
+    if (res[1].stats.lift_bytes != res[2].stats.lift_bytes) return 1;  // P2, P3 send 4n OT bytes
+  }
+  if (want[1] != 1) return 1;
+
+  // error mapping: db payload size mismatch -> Error (engine.cpp:142)
+  Session sess(cfg, seeds_from_master(seed));
+  bool threw = false;
+  try {
+    sess.load_db({std::span<const std::uint8_t>(db[0].data(), 7), db[1], db[2]}, s);
+  } catch (const Error&) {
+    threw = true;
+  }
+  if (!threw) return 1;
+  // bounds: Shamir with an odd rotation stride (engine.cpp:31-33)
+  threw = false;
+  try {
+    EngineConfig bad = cfg;
+    bad.l = 192;
+    Session b(bad, seeds_from_master(seed));
+  } catch (const BoundsError&) {
+    threw = true;
+  }
+  if (!threw) return 1;
+  std::printf("shim ok: person_match = %d %d %d\n", want[0], want[1], want[2]);
+  return 0;
+}

@@ -101,10 +101,11 @@ def ncu_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("gemm_dram_bytes_per_launch")
+            d = json.load(open(p))
+            return d.get("gemm_dram_bytes_per_launch"), d.get("tensor_pipe_active_pct")
         except Exception:
-            return None
-    return None
+            return None, None
+    return None, None
 
 
 # ------------------------------------------------------------------ CPU baseline
@@ -310,9 +311,10 @@ def main_gpu(args):
                        "parallelism": f"db-shard x{world}"},
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons},
-            "roofline": {"bound": "tensor", "kernel": "k_limb_gemm (tcgen05 kind::i8)",
+            "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(),
+                         "traffic": ncu_traffic()[0],
+                         "ncu_tensor_pipe_active_pct": ncu_traffic()[1],
                          "note": f"int8 ops = {OPS_PER_LANE[backend]}/lane; peak = {peak_note}"},
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),

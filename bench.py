@@ -170,21 +170,22 @@ def main_gpu(args):
     import torch
     import torch.distributed as dist
     import paper_2405_04463_b200 as P
+    from paper_2405_04463_b200.dist import shard_rows, sharded_batch_query
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     backend = P.SHAMIR if args.backend == "shamir" else P.REPLICATED
-    rows = args.rows
-    S = rows * world
+    S = args.rows * world
+    row_off, rows = shard_rows(S, world, rank)
     persons = args.persons
     ncodes = 2 * persons
     cfg = P.EngineConfig(backend=backend, l=L, rotations=ROT)
     sess = P.Session(cfg, master_seed=7, device=local, shard_rank=rank, db_rows_total=S if world > 1 else 0,
-                     db_row_offset=rank * rows)
+                     db_row_offset=row_off)
     t0 = time.time()
-    sess.synth_db(rows, rng_seed=2, first=rank * rows, mask_density=0.9, deal_seed=7)
+    sess.synth_db(rows, rng_seed=2, first=row_off, mask_density=0.9, deal_seed=7)
     setup_s = time.time() - t0
 
     # query records: Rng(2) records after the DB; person 0's left eye = DB row S/2
@@ -223,16 +224,7 @@ def main_gpu(args):
         if from_host and rank == 0:
             for d, h in zip(qpay, host_q):
                 d.copy_(h, non_blocking=True)
-        for d in qpay:                                   # NCCL query-share broadcast
-            dist.broadcast(d, src=0)
-        torch.cuda.current_stream().synchronize()
-        mine = torch.empty((3, persons), dtype=torch.uint8, device="cuda")
-        sess.batch_query_partial(qpay, persons, mine)
-        dist.all_gather_into_tensor(parts.view(-1), mine.view(-1))  # gather per-person shares
-        torch.cuda.current_stream().synchronize()
-        if rank == 0:
-            return sess.or_open(parts, world, persons)
-        return None
+        return sharded_batch_query(sess, qpay, persons, dist, world, rank, parts)
 
     for _ in range(args.warmup):
         out = step(False)

@@ -193,7 +193,7 @@ constexpr uint32_t kIdescPair = (2u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uin
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA_lo, const __grid_constant__ CUtensorMap tA_hi,
                      const __grid_constant__ CUtensorMap tB_lo, const __grid_constant__ CUtensorMap tB_hi,
-                     const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs) {
+                     const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs, uint32_t grouped) {
   // Persistent: clusters form groups of n_tiles; cluster c owns n_tile = c % n_tiles
   // and its group sweeps (prob, m_pair) units g, g + groups, ...  The n_tiles
   // clusters of a group read the same DB (A) k-blocks at the same time, so every
@@ -212,10 +212,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const bool leader = rank == 0;
   const uint32_t ncl = gridDim.x >> 1;
   const uint32_t cl = blockIdx.x >> 1;
-  const uint32_t groups = ncl / n_tiles;
-  const uint32_t my_n = cl % n_tiles;
-  const uint32_t g0 = cl / n_tiles;
-  const uint32_t nunits = 6 * m_pairs;
+  // grouped: n_tiles clusters per group sweep the same (prob, m_pair) units;
+  // flat (when grouping would idle SMs): a 1-cluster "group" walks tiles
+  // t = cl, cl + ncl, ... over (unit, n_tile) with n_tile fastest.
+  const bool flat = grouped == 0;
+  const uint32_t tiles_per_unit = flat ? 1 : n_tiles;
+  const uint32_t groups = ncl / tiles_per_unit;
+  const uint32_t my_n = flat ? 0 : cl % n_tiles;
+  const uint32_t g0 = flat ? cl : cl / n_tiles;
+  const uint32_t nunits = flat ? 6 * m_pairs * n_tiles : 6 * m_pairs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tA_lo);
@@ -245,9 +250,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (lane == 0) {
       uint32_t it = 0;
       for (uint32_t u = g0; u < nunits; u += groups) {
-        const uint32_t n_tile = my_n;
-        const uint32_t m_pair = u % m_pairs;
-        const int prob = (int)(u / m_pairs);
+        const uint32_t n_tile = flat ? u % n_tiles : my_n;
+        const uint32_t uu = flat ? u / n_tiles : u;
+        const uint32_t m_pair = uu % m_pairs;
+        const int prob = (int)(uu / m_pairs);
         const int p = prob >> 1, d = prob & 1;
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t stage = it % P_STAGES;
@@ -306,9 +312,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t te = mapa_shared(tmem_empty, 0);
     uint32_t ti = 0;
     for (uint32_t u = g0; u < nunits; u += groups, ++ti) {
-      const uint32_t n_tile = my_n;
-      const uint32_t m_pair = u % m_pairs;
-      const int prob = (int)(u / m_pairs);
+      const uint32_t n_tile = flat ? u % n_tiles : my_n;
+      const uint32_t uu = flat ? u / n_tiles : u;
+      const uint32_t m_pair = uu % m_pairs;
+      const int prob = (int)(uu / m_pairs);
       mbar_wait(accum, ti & 1);
       tc_fence_after();
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
@@ -396,9 +403,12 @@ void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtenso
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t m_pairs = m_tiles / 2;
     const uint32_t units = 6 * m_pairs;
-    const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(units, (uint32_t)(nsm / 2) / n_tiles));
-    const uint32_t ncl = groups * n_tiles;
-    k_limb_gemm_pair<<<dim3(2 * ncl), 256, P_SMEM, st>>>(a_lo, a_hi, b_lo, b_hi, g, n_tiles, m_pairs);
+    const uint32_t max_cl = (uint32_t)(nsm / 2);
+    const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
+    const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
+    const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
+    k_limb_gemm_pair<<<dim3(2 * ncl), 256, P_SMEM, st>>>(a_lo, a_hi, b_lo, b_hi, g, n_tiles, m_pairs,
+                                                          grouped ? 1u : 0u);
   }
 }
 

@@ -336,8 +336,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   ++launches;
   if (npairs) {
     if (c->pair_dots.ensure(6 * npairs * sizeof(uint16_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    void* ph = prof_begin(st);
     launch_pairs(c->q_pa.as<uint16_t>(), c->q_pb.as<uint16_t>(), ncodes, persons, c->l, r, c->shamir,
                  c->pair_dots.as<uint16_t>(), c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
+    prof_end(ph, "k_pairs", st);
     debug_check("k_pairs", st);
     CK(c, cudaGetLastError());
     ++launches;
@@ -458,6 +460,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     add_job(nsegs_all - 1, 1, true, 0);
     cstride = std::max<uint64_t>(cstride, npairs);
   }
+  cstride = round_up(cstride, 8);  // 16-byte aligned component planes
   uint64_t max_g = 0, max_bits = 0;
   for (const Job& j : jobs) {
     max_g = std::max(max_g, j.gwords);
@@ -560,8 +563,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     g.out_pstride = ncols * nr;
     g.out_cstride = (uint32_t)nr;
     CK(c, cudaEventRecord(c->gev[2 * i], st));
+    void* ph = prof_begin(st);
     launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM),
                 (uint32_t)ceil_div(ncols, kGemmBN), st);
+    prof_end(ph, "k_limb_gemm_pair", st);
     debug_check("k_limb_gemm", st);
     CK(c, cudaGetLastError());
     CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
@@ -614,7 +619,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
   oa.elem_base = (qid << 48) | (rank << 40);
   oa.out = c->person_out.as<uint8_t>();
+  void* ph2 = prof_begin(st2);
   launch_or_persons(oa, st2);
+  prof_end(ph2, "k_or_persons", st2);
   debug_check("k_or_persons", st2);
   CK(c, cudaGetLastError());
   ++launches;

@@ -13,6 +13,10 @@ namespace irisgpu {
 // IRISMPC_DEBUG_SYNC=1: synchronize after every launch and abort with the
 // kernel's name on a device fault (no sanitizer on this pool).
 void debug_check(const char* what, cudaStream_t st);
+// IRISMPC_PROFILE=1: bracket launches with CUDA events (per-kernel totals at exit)
+bool prof_on();
+void* prof_begin(cudaStream_t st);
+void prof_end(void* h, const char* name, cudaStream_t st);
 
 // ---- K1 prep / dealer (prep.cu)
 void set_lambda(const uint16_t lam[6]);

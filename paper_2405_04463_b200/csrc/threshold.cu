@@ -114,6 +114,39 @@ __device__ __forceinline__ void prf24(const SeedKey& key, uint64_t e, uint64_t o
   }
 }
 
+// low 32 bits of elements e + 3i, i = 0..7 (the bit-inject c3 draws; the two
+// OT pads in between are consumed but unused).  e % 8 is launch-uniform, so the
+// switch picks one statically indexed extraction for the whole launch.
+template <int R>
+__device__ __forceinline__ void every3_r(const SeedKey& key, uint64_t b, uint32_t out[8]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    constexpr int kLast = (R + 21) / 8;  // block holding element e + 21
+    if (q > kLast) break;
+    uint32_t blk[16];
+    chacha12_block(key, b + q, 0, blk);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int pos = 8 * q + w - R;  // offset from e
+      if (pos >= 0 && pos <= 21 && pos % 3 == 0) out[pos / 3] = blk[2 * w];
+    }
+  }
+}
+
+__device__ __forceinline__ void prf_every3(const SeedKey& key, uint64_t e, uint32_t out[8]) {
+  const uint64_t b = e / 8;
+  switch ((int)(e % 8)) {
+    case 0: every3_r<0>(key, b, out); break;
+    case 1: every3_r<1>(key, b, out); break;
+    case 2: every3_r<2>(key, b, out); break;
+    case 3: every3_r<3>(key, b, out); break;
+    case 4: every3_r<4>(key, b, out); break;
+    case 5: every3_r<5>(key, b, out); break;
+    case 6: every3_r<6>(key, b, out); break;
+    default: every3_r<7>(key, b, out); break;
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- gate keystream
@@ -135,6 +168,12 @@ __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ 
   uint32_t blk[16];
   chacha12_block(A.key[k], b, 0, blk);
   uint64_t* G = A.gate + sg.g_off + (uint64_t)kg * nw;
+  if (b * 8 >= E && b * 8 + 8 <= E + nw) {  // interior block: no per-word range checks
+    uint64_t* dst = G + (b * 8 - E);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) dst[w] = chacha_word(blk, w);
+    return;
+  }
 #pragma unroll
   for (int w = 0; w < 8; ++w) {
     const uint64_t e = b * 8 + w;
@@ -150,46 +189,88 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
   const uint32_t si = seg_search(A.segs, A.nsegs, tid, [](const Seg& s) { return s.grp_begin; });
   const Seg& sg = A.segs[si];
   const uint64_t L8 = (sg.lane_begin / 8 + (tid - sg.grp_begin)) * 8;
-  uint32_t hd[3][8], ml[3][8];
+  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);  // valid only when `full`
+  bool full = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t ln = L8 + i;
-    const bool ok = ln >= sg.lane_begin && ln < sg.lane_end;
-    const uint64_t src = sg.src + (ln - sg.lane_begin);
+  for (int p = 0; p < 3; ++p)  // 16-byte alignment of every vector access
+    full = full && ((reinterpret_cast<uintptr_t>(A.hd[p] + src0) | reinterpret_cast<uintptr_t>(A.ml[p] + src0) |
+                     reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) |
+                     reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0)) & 15) == 0;
+  // two passes with one 3x8 state each: ml (stream offset n) then hd (offset 0)
+  uint32_t ml16[3][8];
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      hd[p][i] = ok ? A.hd[p][src] : 0u;
-      ml[p][i] = ok ? A.ml[p][src] : 0u;
+  for (int part = 0; part < 2; ++part) {
+    const uint16_t* const* srcs = part == 0 ? A.ml : A.hd;
+    uint32_t v[3][8];
+    if (full) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const uint4 x = *reinterpret_cast<const uint4*>(srcs[p] + src0);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[p][2 * i] = w[i] & 0xFFFFu;
+          v[p][2 * i + 1] = w[i] >> 16;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t ln = L8 + i;
+        const bool ok = ln >= sg.lane_begin && ln < sg.lane_end;
+        const uint64_t src = sg.src + (ln - sg.lane_begin);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) v[p][i] = ok ? srcs[p][src] : 0u;
+      }
     }
-  }
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    uint64_t fh[8], fm[8];
-    prf8(A.key[k], A.pos[k] + L8, fh);
-    prf8(A.key[k], A.pos[k] + A.n + L8, fm);
-    const int kn = (k + 1) % 3;
+    for (int k = 0; k < 3; ++k) {
+      uint64_t f[8];
+      prf8(A.key[k], A.pos[k] + (part == 0 ? A.n : 0) + L8, f);
+      const int kn = (k + 1) % 3;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[k][i] += (uint32_t)f[i];
+        v[kn][i] -= (uint32_t)f[i];
+      }
+    }
+    if (part == 0) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ml16[p][i] = v[p][i] & 0xFFFFu;
+      continue;
+    }
+    if (full) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        uint32_t mw[4], dw[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mw[i] = ml16[p][2 * i] | (ml16[p][2 * i + 1] << 16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dw[i] = A.a * ml16[p][i] - A.b * (v[p][i] & 0xFFFFu);
+        *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
+        dd[0] = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+        dd[1] = make_uint4(dw[4], dw[5], dw[6], dw[7]);
+      }
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      hd[k][i] += (uint32_t)fh[i];
-      hd[kn][i] -= (uint32_t)fh[i];
-      ml[k][i] += (uint32_t)fm[i];
-      ml[kn][i] -= (uint32_t)fm[i];
-    }
-  }
+      const uint64_t ln = L8 + i;
+      if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
+      const uint64_t src = sg.src + (ln - sg.lane_begin);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t ln = L8 + i;
-    if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
-    const uint64_t src = sg.src + (ln - sg.lane_begin);
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      const uint32_t m16 = ml[p][i] & 0xFFFFu, h16 = hd[p][i] & 0xFFFFu;
-      A.ml_rs[p * A.cstride + src] = (uint16_t)m16;
-      A.diff[p * A.cstride + src] = A.a * m16 - A.b * h16;
-      if (A.tap_rs_hd) {
-        A.tap_rs_hd[p * A.n + ln] = (uint16_t)h16;
-        A.tap_rs_ml[p * A.n + ln] = (uint16_t)m16;
-        A.tap_ml32[p * A.n + ln] = m16;
+      for (int p = 0; p < 3; ++p) {
+        const uint32_t m16 = ml16[p][i], h16 = v[p][i] & 0xFFFFu;
+        A.ml_rs[p * A.cstride + src] = (uint16_t)m16;
+        A.diff[p * A.cstride + src] = A.a * m16 - A.b * h16;
+        if (A.tap_rs_hd) {
+          A.tap_rs_hd[p * A.n + ln] = (uint16_t)h16;
+          A.tap_rs_ml[p * A.n + ln] = (uint16_t)m16;
+          A.tap_ml32[p * A.n + ln] = m16;
+        }
       }
     }
   }
@@ -296,8 +377,21 @@ __global__ void __launch_bounds__(128) k_lift(const __grid_constant__ ThrArgs A)
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
     uint32_t a[32];
-    if (vm == 0xFFFFFFFFu) {
-      const uint16_t* src = A.ml_rs + p * A.cstride + t.sg.src + (Lt - t.sg.lane_begin);
+    const uint64_t so = t.sg.src + (Lt - t.sg.lane_begin);
+    if (vm == 0xFFFFFFFFu && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + so) & 15) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(A.ml_rs + p * A.cstride + so);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 x = src[q];
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a[8 * q + 2 * i] = w[i] & 0xFFFFu;
+          a[8 * q + 2 * i + 1] = w[i] >> 16;
+        }
+      }
+    } else if (vm == 0xFFFFFFFFu) {
+      const uint16_t* src = A.ml_rs + p * A.cstride + so;
 #pragma unroll
       for (int i = 0; i < 32; ++i) a[i] = src[i];
     } else {
@@ -348,18 +442,35 @@ __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs 
     const int shift = which == 0 ? 17 : 16;
     const uint64_t o1 = A.pos[0] + 2 * n + 64 * W + (which == 0 ? 0 : n) + L8;
     const uint64_t o3 = A.pos[2] + 2 * n + 64 * W + (which == 0 ? 0 : 3 * n) + 3 * L8;
-    uint64_t c1[8], c3[24];
+    uint64_t c1[8];
+    uint32_t c3[8];
     prf8(A.key[0], o1, c1);
-    prf24(A.key[2], o3, c3);
+    prf_every3(A.key[2], o3, c3);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t b1 = (uint32_t)c1[i] & mask;
-      const uint32_t b3 = (uint32_t)c3[3 * i] & mask;
+      const uint32_t b3 = c3[i] & mask;
       const uint32_t b2 = (((x >> i) & 1u) - b1 - b3) & mask;
       d[0][i] += b1 << shift;
       d[1][i] += b2 << shift;
       d[2][i] += b3 << shift;
     }
+  }
+  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
+  bool vec = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_ml32;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) vec = vec && (reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0) & 15) == 0;
+  if (vec) {
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
+      uint4 x = dd[0], y = dd[1];
+      x.x -= A.a * d[p][0]; x.y -= A.a * d[p][1]; x.z -= A.a * d[p][2]; x.w -= A.a * d[p][3];
+      y.x -= A.a * d[p][4]; y.y -= A.a * d[p][5]; y.z -= A.a * d[p][6]; y.w -= A.a * d[p][7];
+      dd[0] = x;
+      dd[1] = y;
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -441,8 +552,19 @@ __global__ void __launch_bounds__(128) k_msb(const __grid_constant__ ThrArgs A) 
   uint32_t D[3][32];
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
-    if (vm == 0xFFFFFFFFu) {
-      const uint32_t* src = A.diff + p * A.cstride + t.sg.src + (Lt - t.sg.lane_begin);
+    const uint64_t so = t.sg.src + (Lt - t.sg.lane_begin);
+    if (vm == 0xFFFFFFFFu && (reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + so) & 15) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(A.diff + p * A.cstride + so);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = src[q];
+        D[p][4 * q] = x.x;
+        D[p][4 * q + 1] = x.y;
+        D[p][4 * q + 2] = x.z;
+        D[p][4 * q + 3] = x.w;
+      }
+    } else if (vm == 0xFFFFFFFFu) {
+      const uint32_t* src = A.diff + p * A.cstride + so;
 #pragma unroll
       for (int i = 0; i < 32; ++i) D[p][i] = src[i];
     } else {
@@ -476,15 +598,25 @@ __global__ void __launch_bounds__(128) k_msb(const __grid_constant__ ThrArgs A) 
 
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   if (!a.ntasks) return;
+  void* h = prof_begin(st);
   k_gate_keystream<<<(unsigned)((a.ngblk + 255) / 256), 256, 0, st>>>(a);
+  prof_end(h, "k_gate_keystream", st);
   debug_check("k_gate_keystream", st);
+  h = prof_begin(st);
   k_reshare<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
+  prof_end(h, "k_reshare", st);
   debug_check("k_reshare", st);
+  h = prof_begin(st);
   k_lift<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+  prof_end(h, "k_lift", st);
   debug_check("k_lift", st);
+  h = prof_begin(st);
   k_inject<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
+  prof_end(h, "k_inject", st);
   debug_check("k_inject", st);
+  h = prof_begin(st);
   k_msb<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+  prof_end(h, "k_msb", st);
   debug_check("k_msb", st);
 }
 

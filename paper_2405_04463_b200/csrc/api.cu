@@ -139,7 +139,9 @@ struct irismpc_gpu_ctx {
   CUtensorMap tB_lo, tB_hi;
   uint32_t ncols_pad_cur = 0;
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
-  Buf ml_rs, diff, gate, bits;
+  Buf ml_rs, diff, gate, bits, qa_lo, qa_hi, pair_c;
+  CUtensorMap tQA_lo, tQA_hi;
+  uint64_t qa_spad = 0;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
@@ -200,6 +202,10 @@ int validate(const irismpc_gpu_config* c, std::string* why) {
   if (c->rotations % 2 == 0) {
     *why = "rotations must be odd";
     return IRISMPC_GPU_ERR_BOUNDS;
+  }
+  if (c->rotations > 31) {
+    *why = "the GPU path supports at most 31 rotations";
+    return IRISMPC_GPU_ERR_CONFIG;
   }
   if (c->backend == IRISMPC_GPU_BACKEND_SHAMIR && c->rotations > 1 && (c->l / 64) % 2 != 0) {
     *why = "shamir packing needs an even rotation stride (l/64)";
@@ -265,9 +271,6 @@ int ensure_query_buffers(irismpc_gpu_ctx* c, uint32_t ncodes, uint32_t ncols_pad
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the query planes");
     c->ncols_pad_cur = ncols_pad;
   }
-  const size_t pinst = 6ull * ncodes * c->l * sizeof(uint16_t);
-  if (c->q_pa.ensure(pinst) || c->q_pb.ensure(pinst))
-    return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query instances");
   return 0;
 }
 
@@ -329,20 +332,53 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   int rc = ensure_query_buffers(c, ncodes, ncols_pad);
   if (rc) return rc;
   launch_parse_query(dqp[0], dqp[1], dqp[2], ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir,
-                     c->q_lo.as<uint8_t>(), c->q_hi.as<uint8_t>(), c->q_pa.as<uint16_t>(),
-                     c->q_pb.as<uint16_t>(), st);
+                     c->q_lo.as<uint8_t>(), c->q_hi.as<uint8_t>(), nullptr, nullptr, st);
   debug_check("k_parse_query", st);
   CK(c, cudaGetLastError());
   ++launches;
   if (npairs) {
-    if (c->pair_dots.ensure(6 * npairs * sizeof(uint16_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    // pair dots as one limb GEMM: A = the unrotated query codes in the DB plane
+    // layout, B = the rotated query planes (see pairs.cu)
+    const uint64_t spq = round_up(ncodes, 2 * kGemmBM);
+    const size_t abytes = 6ull * spq * c->l_pad;
+    if (spq != c->qa_spad) {
+      if (c->qa_lo.ensure(abytes) || c->qa_hi.ensure(abytes))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair planes)");
+      CK(c, cudaMemsetAsync(c->qa_lo.p, 0, abytes, st));
+      CK(c, cudaMemsetAsync(c->qa_hi.p, 0, abytes, st));
+      if (make_plane_tmap(&c->tQA_lo, c->qa_lo.p, 6ull * spq, c->l_pad, kGemmBM) ||
+          make_plane_tmap(&c->tQA_hi, c->qa_hi.p, 6ull * spq, c->l_pad, kGemmBM))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the pair planes");
+      c->qa_spad = spq;
+    }
+    for (int p = 0; p < 3; ++p)
+      launch_parse_db(dqp[p], ncodes, 0, c->l, c->l_pad, spq, p, c->shamir, c->qa_lo.as<uint8_t>(),
+                      c->qa_hi.as<uint8_t>(), st);
+    if (c->pair_c.ensure(6 * ncols * ncodes * sizeof(uint16_t)) ||
+        c->pair_dots.ensure(6 * npairs * sizeof(uint16_t)))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
+    GemmArgs pg{};
+    pg.s_pad = (uint32_t)spq;
+    pg.nb_rows = ncols_pad;
+    pg.nkb_seg = c->l_pad / kGemmBK;
+    pg.nseg = c->nseg;
+    pg.rep = c->shamir ? 0 : 1;
+    pg.s_valid = ncodes;
+    pg.row0 = 0;
+    pg.col0 = 0;
+    pg.ncols = (uint32_t)ncols;
+    pg.out = c->pair_c.as<uint16_t>();
+    pg.out_pstride = ncols * ncodes;
+    pg.out_cstride = ncodes;
     void* ph = prof_begin(st);
-    launch_pairs(c->q_pa.as<uint16_t>(), c->q_pb.as<uint16_t>(), ncodes, persons, c->l, r, c->shamir,
-                 c->pair_dots.as<uint16_t>(), c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
-    prof_end(ph, "k_pairs", st);
-    debug_check("k_pairs", st);
+    launch_gemm(c->tQA_lo, c->tQA_hi, c->tB_lo, c->tB_hi, pg, (uint32_t)(spq / kGemmBM),
+                (uint32_t)ceil_div(ncols, kGemmBN), st);
+    launch_pair_gather(c->pair_c.as<uint16_t>(), ncodes, (uint32_t)ncols, persons, r, c->pair_dots.as<uint16_t>(),
+                       c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
+    prof_end(ph, "pairs (gemm+gather)", st);
+    debug_check("pairs", st);
     CK(c, cudaGetLastError());
-    ++launches;
+    launches += 5;  // 3 parse + gemm + gather
   }
   CK(c, cudaEventRecord(c->ev[1], st));
 
@@ -776,7 +812,7 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   Buf* bufs[] = {&c->db_lo, &c->db_hi, &c->q_lo, &c->q_hi, &c->q_pa, &c->q_pb, &c->q_pay[0], &c->q_pay[1],
                  &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial, &c->slot_begin,
                  &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
-                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->qa_lo, &c->qa_hi, &c->pair_c};
   for (Buf* b : bufs) b->release();
   for (auto& t : c->tap_buf) t.release();
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);

@@ -62,9 +62,8 @@ void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtenso
                  cudaStream_t st);
 
 // ---- inner-batch pairs (pairs.cu)
-void launch_pairs(const uint16_t* pa, const uint16_t* pb, uint32_t ncodes, uint32_t persons,
-                  uint32_t l, uint32_t rot, int shamir, uint16_t* out_hd, uint16_t* out_ml,
-                  uint64_t out_pstride, cudaStream_t st);
+void launch_pair_gather(const uint16_t* C, uint32_t ncodes, uint32_t ncols, uint32_t persons, uint32_t rot,
+                        uint16_t* out_hd, uint16_t* out_ml, uint64_t out_pstride, cudaStream_t st);
 
 // ---- K4 threshold (threshold.cu)
 struct Seg {

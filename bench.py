@@ -118,7 +118,7 @@ def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int):
     cores = os.cpu_count() or 1
     if O.ref_available():
         R = O.ref()
-        h = R.ref_bench_prepare(backend, L, rows, persons)
+        h = R.ref_bench_prepare(backend, O.MPC_LIFT, L, rows, persons)
         times = []
         m0 = C.c_uint8(0)
         for _ in range(steps):

@@ -25,7 +25,9 @@ from oracle import pyoracle as O  # noqa: E402
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
                    "ref_vectors.json")
 
-# (backend, l, s, persons, rotations, seed, membership, ratio, planted)
+# (backend, l, s, persons, rotations, seed, membership, ratio, planted[, variant])
+# variant defaults to mpc-lift (the north-star path); the tail covers the
+# other three variants (shares.hpp:28) on both backends.
 CASES = [
     (0, 64, 4, 1, 1, 101, True, 0.375, True),
     (1, 64, 4, 1, 1, 102, True, 0.375, True),
@@ -41,11 +43,23 @@ CASES = [
     (1, 12800, 2, 1, 31, 112, False, 0.375, True),
     (0, 12800, 3, 1, 31, 113, False, 0.375, True),
     (1, 12800, 40, 2, 31, 114, False, 0.375, True),
+] + [
+    (be, l, s, persons, r, 200 + 10 * var + 2 * i + be, memb, ratio, planted, var)
+    for var in (O.PLAIN_MASK, O.CONST_LIFT, O.NO_LIFT)
+    for i, (l, s, persons, r, memb, ratio, planted) in enumerate([
+        (64, 6, 1, 1, True, 0.375, True),
+        (128, 3, 3, 3, False, 0.375, True),
+        (256, 9, 2, 31, False, 0.3, False),
+        (12800, 3, 1, 31, False, 0.375, True),
+    ])
+    for be in (0, 1)
 ]
 
 
 def sha(a: np.ndarray) -> str:
-    return hashlib.sha256(np.ascontiguousarray(a).astype("<u2").tobytes()).hexdigest()
+    """sha256 of the little-endian bytes at the array's ring width (u16 / u32 / i64)."""
+    dt = {np.dtype(np.uint16): "<u2", np.dtype(np.uint32): "<u4", np.dtype(np.int64): "<i8"}[a.dtype]
+    return hashlib.sha256(np.ascontiguousarray(a).astype(dt).tobytes()).hexdigest()
 
 
 def inputs(l, s, persons, seed, membership, planted):
@@ -103,25 +117,40 @@ def main():
             dc, dm = O.records(rng, l, 3, 0.9)
             rb = O.record_bytes(be, l)
             outs = [np.zeros(3 * rb, np.uint8) for _ in range(3)]
-            R.ref_deal(be, l, 7, 1, 3, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
+            R.ref_deal(be, O.MPC_LIFT, l, 7, 1, 3, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
             deals.append({"backend": be, "l": l, "records_rng": 21, "nrec": 3, "deal_seed": 7, "tag": 1,
                           "sha256": [hashlib.sha256(x.tobytes()).hexdigest() for x in outs],
                           "head_hex": [x[:32].tobytes().hex() for x in outs]})
+    for var in (O.PLAIN_MASK, O.CONST_LIFT, O.NO_LIFT):
+        for be in (0, 1):
+            l = 128
+            rng = O.Rng(21)
+            dc, dm = O.records(rng, l, 3, 0.9)
+            rb = O.record_bytes(be, l, var)
+            outs = [np.zeros(3 * rb, np.uint8) for _ in range(3)]
+            R.ref_deal(be, var, l, 7, 1, 3, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
+            deals.append({"backend": be, "variant": var, "l": l, "records_rng": 21, "nrec": 3, "deal_seed": 7,
+                          "tag": 1, "sha256": [hashlib.sha256(x.tobytes()).hexdigest() for x in outs],
+                          "head_hex": [x[:32].tobytes().hex() for x in outs]})
     g["deal"] = deals
+    lam32 = O.lambda_k(32)
+    g["lambda32_restated"] = [int(x) for x in lam32]
 
     cases = []
-    for (be, l, s, persons, r, seed, membership, ratio, planted) in CASES:
+    for spec in CASES:
+        (be, l, s, persons, r, seed, membership, ratio, planted), var = spec[:9], (spec[9] if len(spec) > 9 else O.MPC_LIFT)
         dc, dm, qc, qm = inputs(l, s, persons, seed, membership, planted)
-        res = O.ref_run_local(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership, debug_rows=True)
-        db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)))
-        q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)))
+        res = O.ref_run_local(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership, debug_rows=True,
+                              variant=var)
+        db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)), variant=var)
+        q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)), variant=var)
         # the dealt payloads must equal the reference dealer's (pinned above) — recheck here
-        outs = [np.zeros(max(1, s * O.record_bytes(be, l)), np.uint8) for _ in range(3)]
+        outs = [np.zeros(max(1, s * O.record_bytes(be, l, var)), np.uint8) for _ in range(3)]
         if s:
-            R.ref_deal(be, l, seed, 1, s, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
+            R.ref_deal(be, var, l, seed, 1, s, O._p(dc, O.u64p), O._p(dm, O.u64p), *[O._p(x, O.u8p) for x in outs])
             assert all((a == b[: len(a)]).all() for a, b in zip(db, outs))
         seeds = O.party_seeds(seed)
-        dh, dmm, rh, rm = O.ref_dots_reshare(be, l, r, seeds, db, s, q, persons, membership)
+        dh, dmm, rh, rm = O.ref_dots_reshare(be, l, r, seeds, db, s, q, persons, membership, variant=var)
         n = int(res["lanes"])
         case = {
             "backend": be, "l": l, "s": s, "persons": persons, "rotations": r, "seed": seed,
@@ -129,15 +158,24 @@ def main():
             "person_match": [int(x) for x in res["person_match"]],
             "row_bits_hex": np.packbits(res["row_bits"], bitorder="little").tobytes().hex(),
             "stats": res["stats"],
-            "sha256": {"dot_hd": sha(dh), "dot_ml": sha(dmm), "rs_hd": sha(rh), "rs_ml": sha(rm)},
+            "sha256": {"dot_hd": sha(dh), "rs_hd": sha(rh)},
         }
+        if var != O.MPC_LIFT:
+            case["variant"] = var
+        if O.mask_bits(var):
+            case["sha256"].update(dot_ml=sha(dmm), rs_ml=sha(rm))
+        else:
+            case["sha256"]["public_ml"] = sha(O.ref_dots_reshare.public_ml)
         if n <= 64:
             case["dot_hd"] = dh.tolist()
-            case["dot_ml"] = dmm.tolist()
             case["rs_hd"] = rh.tolist()
-            case["rs_ml"] = rm.tolist()
+            if O.mask_bits(var):
+                case["dot_ml"] = dmm.tolist()
+                case["rs_ml"] = rm.tolist()
+            else:
+                case["public_ml"] = O.ref_dots_reshare.public_ml.tolist()
         cases.append(case)
-        print(f"case be={be} l={l} s={s} persons={persons} r={r} lanes={n} match={case['person_match']}")
+        print(f"case var={var} be={be} l={l} s={s} persons={persons} r={r} lanes={n} match={case['person_match']}")
     g["cases"] = cases
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:

@@ -181,30 +181,33 @@ void orc_party_seeds(uint64_t master, uint8_t out[48]) {
 }
 
 /* ====================================================================== */
-/* Galois ring Z_2^16[X]/(X^2-X-1) — galois.hpp:30-128                     */
+/* Galois ring Z_2^K[X]/(X^2-X-1), K = 16 or 32 — galois.hpp:30-128         */
 /* ====================================================================== */
 
-typedef struct { uint16_t c0, c1; } gr16;
+typedef struct { uint32_t c0, c1; } gr;
 
-static gr16 gr_mul(gr16 a, gr16 b) {
-  gr16 r;
-  r.c0 = (uint16_t)((uint32_t)a.c0 * b.c0 + (uint32_t)a.c1 * b.c1);
-  r.c1 = (uint16_t)((uint32_t)a.c0 * b.c1 + (uint32_t)a.c1 * b.c0 + (uint32_t)a.c1 * b.c1);
+static inline uint32_t kmask(unsigned K) { return K == 32 ? 0xFFFFFFFFu : ((1u << K) - 1); }
+
+static gr gr_mul(gr a, gr b, unsigned K) {
+  const uint32_t m = kmask(K);
+  gr r;
+  r.c0 = (uint32_t)((uint64_t)a.c0 * b.c0 + (uint64_t)a.c1 * b.c1) & m;
+  r.c1 = (uint32_t)((uint64_t)a.c0 * b.c1 + (uint64_t)a.c1 * b.c0 + (uint64_t)a.c1 * b.c1) & m;
   return r;
 }
-static gr16 gr_sub(gr16 a, gr16 b) {
-  gr16 r = {(uint16_t)(a.c0 - b.c0), (uint16_t)(a.c1 - b.c1)};
+static gr gr_sub(gr a, gr b, unsigned K) {
+  gr r = {(a.c0 - b.c0) & kmask(K), (a.c1 - b.c1) & kmask(K)};
   return r;
 }
-static gr16 gr_add(gr16 a, gr16 b) {
-  gr16 r = {(uint16_t)(a.c0 + b.c0), (uint16_t)(a.c1 + b.c1)};
+static gr gr_add(gr a, gr b, unsigned K) {
+  gr r = {(a.c0 + b.c0) & kmask(K), (a.c1 + b.c1) & kmask(K)};
   return r;
 }
 
 /* gr_inverse (galois.hpp:66-87): F_4 seed then Newton y <- y(2 - a y). */
-static gr16 gr_inverse(gr16 a) {
+static gr gr_inverse(gr a, unsigned K) {
   const unsigned p0 = a.c0 & 1, p1 = a.c1 & 1;
-  gr16 y;
+  gr y;
   if (p1 == 0) {
     y.c0 = 1; y.c1 = 0;
   } else if (p0 == 0) {
@@ -212,103 +215,146 @@ static gr16 gr_inverse(gr16 a) {
   } else {
     y.c0 = 0; y.c1 = 1;
   }
-  const gr16 two = {2, 0};
-  for (unsigned correct = 1; correct < 16; correct *= 2) y = gr_mul(y, gr_sub(two, gr_mul(a, y)));
+  const gr two = {2, 0};
+  for (unsigned correct = 1; correct < K; correct *= 2) y = gr_mul(y, gr_sub(two, gr_mul(a, y, K), K), K);
   return y;
 }
 
 /* party_lagrange_at_zero over the exceptional points {1, X, 1+X}
  * (galois.hpp:92-128). */
-void orc_lambda16(uint16_t out[6]) {
-  const gr16 xs[3] = {{1, 0}, {0, 1}, {1, 1}};
+void orc_lambda(unsigned K, uint32_t out[6]) {
+  const gr xs[3] = {{1, 0}, {0, 1}, {1, 1}};
   for (int i = 0; i < 3; ++i) {
-    gr16 num = {1, 0}, den = {1, 0};
+    gr num = {1, 0}, den = {1, 0};
     for (int j = 0; j < 3; ++j) {
       if (j == i) continue;
-      num = gr_mul(num, xs[j]);
-      den = gr_mul(den, gr_sub(xs[j], xs[i]));
+      num = gr_mul(num, xs[j], K);
+      den = gr_mul(den, gr_sub(xs[j], xs[i], K), K);
     }
-    const gr16 li = gr_mul(num, gr_inverse(den));
+    const gr li = gr_mul(num, gr_inverse(den, K), K);
     out[2 * i] = li.c0;
     out[2 * i + 1] = li.c1;
   }
 }
 
+void orc_lambda16(uint16_t out[6]) {
+  uint32_t l32[6];
+  orc_lambda(16, l32);
+  for (int i = 0; i < 6; ++i) out[i] = (uint16_t)l32[i];
+}
+
 /* ====================================================================== */
-/* Dealer — shares.hpp:52-130, shares.cpp:49-90 (mpc-lift: 16/16 bits)     */
+/* Variant widths (shares.hpp:28-48) and dealer (shares.hpp:52-130,        */
+/* shares.cpp:49-90)                                                       */
 /* ====================================================================== */
+
+unsigned orc_code_bits(int variant) { return variant == ORC_NO_LIFT ? 32 : 16; }
+unsigned orc_mask_bits(int variant) {
+  switch (variant) {
+    case ORC_PLAIN_MASK: return 0;
+    case ORC_MPC_LIFT: return 16;
+    default: return 32;
+  }
+}
+unsigned orc_cmp_bits(int variant) { return variant == ORC_PLAIN_MASK ? 16 : 32; }
 
 /* code_record_bytes / mask_record_bytes (shares.cpp:49-59) */
-size_t orc_code_record_bytes(int backend, uint32_t l) {
-  return backend == ORC_REPLICATED ? (size_t)l * 2 * 2 : (size_t)(l / 2) * 2 * 2;
+size_t orc_code_record_bytes(int backend, int variant, uint32_t l) {
+  const size_t w = orc_code_bits(variant) / 8;
+  return backend == ORC_REPLICATED ? (size_t)l * 2 * w : (size_t)(l / 2) * 2 * w;
 }
-size_t orc_mask_record_bytes(int backend, uint32_t l) { return orc_code_record_bytes(backend, l); }
+size_t orc_mask_record_bytes(int backend, int variant, uint32_t l) {
+  const unsigned km = orc_mask_bits(variant);
+  if (km == 0) return l / 8;
+  const size_t w = km / 8;
+  return backend == ORC_REPLICATED ? (size_t)l * 2 * w : (size_t)(l / 2) * 2 * w;
+}
 
-static inline void put16(uint8_t** p, uint16_t v) {
-  (*p)[0] = (uint8_t)v;
-  (*p)[1] = (uint8_t)(v >> 8);
-  *p += 2;
+static inline void putw(uint8_t** p, uint32_t v, unsigned K) {
+  for (unsigned b = 0; b < K / 8; ++b) (*p)[b] = (uint8_t)(v >> (8 * b));
+  *p += K / 8;
+}
+static inline uint32_t getw(const uint8_t* p, unsigned K) {
+  uint32_t v = 0;
+  for (unsigned b = 0; b < K / 8; ++b) v |= (uint32_t)p[b] << (8 * b);
+  return v;
 }
 
 static inline int bit_at(const uint64_t* w, uint32_t i) { return (int)((w[i / 64] >> (i % 64)) & 1); }
 
 /* emit_rep_record (shares.hpp:63-73) with share<K> (rep3.hpp:74-80) */
-static void emit_rep(const uint16_t* vals, uint32_t n, orc_rng* rng, uint8_t** o) {
+static void emit_rep(const uint32_t* vals, uint32_t n, unsigned K, orc_rng* rng, uint8_t** o) {
+  const uint32_t m = kmask(K);
   for (uint32_t i = 0; i < n; ++i) {
-    const uint16_t x1 = (uint16_t)orc_rng_next(rng);
-    const uint16_t x2 = (uint16_t)orc_rng_next(rng);
-    const uint16_t x3 = (uint16_t)(vals[i] - x1 - x2);
-    put16(&o[0], x1); put16(&o[0], x3);
-    put16(&o[1], x2); put16(&o[1], x1);
-    put16(&o[2], x3); put16(&o[2], x2);
+    const uint32_t x1 = (uint32_t)orc_rng_next(rng) & m;
+    const uint32_t x2 = (uint32_t)orc_rng_next(rng) & m;
+    const uint32_t x3 = (vals[i] - x1 - x2) & m;
+    putw(&o[0], x1, K); putw(&o[0], x3, K);
+    putw(&o[1], x2, K); putw(&o[1], x1, K);
+    putw(&o[2], x3, K); putw(&o[2], x2, K);
   }
 }
 
 /* emit_gr_record (shares.hpp:75-85) with shamir_share_packed (shamir.hpp:46-59).
  * `Gr<K> r(rng.ring(), rng.ring())` gives the FIRST draw to c1 under GCC
  * (SURVEY.md A.4).  Share at point x_p: g + r * x_p with x = {1, X, 1+X}. */
-static void emit_gr(const uint16_t* vals, uint32_t n, orc_rng* rng, uint8_t** o) {
-  const gr16 pts[3] = {{1, 0}, {0, 1}, {1, 1}};
+static void emit_gr(const uint32_t* vals, uint32_t n, unsigned K, orc_rng* rng, uint8_t** o) {
+  const gr pts[3] = {{1, 0}, {0, 1}, {1, 1}};
+  const uint32_t m = kmask(K);
   for (uint32_t i = 0; i < n / 2; ++i) {
-    gr16 g = {vals[2 * i], vals[2 * i + 1]};
-    gr16 r;
-    r.c1 = (uint16_t)orc_rng_next(rng);
-    r.c0 = (uint16_t)orc_rng_next(rng);
+    gr g = {vals[2 * i], vals[2 * i + 1]};
+    gr r;
+    r.c1 = (uint32_t)orc_rng_next(rng) & m;
+    r.c0 = (uint32_t)orc_rng_next(rng) & m;
     for (int p = 0; p < 3; ++p) {
-      const gr16 sh = gr_add(g, gr_mul(r, pts[p]));
-      put16(&o[p], sh.c0);
-      put16(&o[p], sh.c1);
+      const gr sh = gr_add(g, gr_mul(r, pts[p], K), K);
+      putw(&o[p], sh.c0, K);
+      putw(&o[p], sh.c1, K);
     }
   }
 }
 
 /* emit_record (shares.cpp:61-74): masked code entries m - 2(c&m) (iris.hpp:108-112)
- * then mask entries (shares.hpp:99-104). */
-void orc_deal_payload(int backend, uint32_t l, uint64_t nrec, const uint64_t* codes,
-                      const uint64_t* masks, orc_rng* rng, uint8_t* out1, uint8_t* out2,
-                      uint8_t* out3) {
+ * at code_bits, then the mask: shares at mask_bits, or l/8 plain mask bytes
+ * identical for all parties (emit_mask_bits, shares.hpp:87-95). */
+void orc_deal_payload_v(int backend, int variant, uint32_t l, uint64_t nrec, const uint64_t* codes,
+                        const uint64_t* masks, orc_rng* rng, uint8_t* out1, uint8_t* out2, uint8_t* out3) {
   const uint32_t wl = (l + 63) / 64;
-  uint16_t* cv = (uint16_t*)malloc(sizeof(uint16_t) * l);
-  uint16_t* mv = (uint16_t*)malloc(sizeof(uint16_t) * l);
+  const unsigned KH = orc_code_bits(variant), KM = orc_mask_bits(variant);
+  uint32_t* cv = (uint32_t*)malloc(sizeof(uint32_t) * l);
+  uint32_t* mv = (uint32_t*)malloc(sizeof(uint32_t) * l);
   uint8_t* o[3] = {out1, out2, out3};
   for (uint64_t r = 0; r < nrec; ++r) {
     const uint64_t* c = codes + r * wl;
     const uint64_t* m = masks + r * wl;
     for (uint32_t i = 0; i < l; ++i) {
       const int mb = bit_at(m, i), cb = bit_at(c, i) & mb;
-      cv[i] = (uint16_t)(mb - 2 * cb);
-      mv[i] = (uint16_t)mb;
+      cv[i] = (uint32_t)(mb - 2 * cb) & kmask(KH);
+      mv[i] = (uint32_t)mb;
     }
-    if (backend == ORC_REPLICATED) {
-      emit_rep(cv, l, rng, o);
-      emit_rep(mv, l, rng, o);
+    if (backend == ORC_REPLICATED)
+      emit_rep(cv, l, KH, rng, o);
+    else
+      emit_gr(cv, l, KH, rng, o);
+    if (KM == 0) {
+      for (int p = 0; p < 3; ++p)
+        for (uint32_t i = 0; i < l / 8; ++i) o[p][i] = (uint8_t)(m[i / 8] >> (8 * (i % 8)));
+      for (int p = 0; p < 3; ++p) o[p] += l / 8;
+    } else if (backend == ORC_REPLICATED) {
+      emit_rep(mv, l, KM, rng, o);
     } else {
-      emit_gr(cv, l, rng, o);
-      emit_gr(mv, l, rng, o);
+      emit_gr(mv, l, KM, rng, o);
     }
   }
   free(cv);
   free(mv);
+}
+
+/* legacy entry: mpc-lift widths */
+size_t orc_code_record_bytes16(int backend, uint32_t l) { return orc_code_record_bytes(backend, ORC_MPC_LIFT, l); }
+void orc_deal_payload(int backend, uint32_t l, uint64_t nrec, const uint64_t* codes, const uint64_t* masks,
+                      orc_rng* rng, uint8_t* out1, uint8_t* out2, uint8_t* out3) {
+  orc_deal_payload_v(backend, ORC_MPC_LIFT, l, nrec, codes, masks, rng, out1, out2, out3);
 }
 
 /* ====================================================================== */
@@ -323,15 +369,21 @@ uint32_t orc_match_a(double ratio) {
   return (uint32_t)a;
 }
 
-/* EngineConfig::validate (engine.cpp:21-34), mpc-lift variant */
+/* EngineConfig::validate (engine.cpp:21-34) */
 int orc_validate(const orc_config* cfg) {
   if (cfg->l == 0 || cfg->l % 8 != 0) return 4;
   if (cfg->a > cfg->b) return 4;
-  if (cfg->b != (1u << 16)) return 4;
-  /* check_shared_mask_bound(l, b, 32) (iris.hpp:199-205) */
-  const uint64_t t = (uint64_t)1 << 32;
-  const uint64_t bl = (uint64_t)cfg->b * cfg->l;
-  if (!(bl < t / 4 && bl < t - (t >> 1))) return 4;
+  if (cfg->variant == ORC_PLAIN_MASK) {
+    /* check_public_mask_bound(l, 16) (iris.hpp:190-196) */
+    const uint64_t t = (uint64_t)1 << 16;
+    if (!(cfg->l < t / 4 && cfg->l < t - (t >> 1))) return 4;
+  } else {
+    if (cfg->b != (1u << 16)) return 4;
+    /* check_shared_mask_bound(l, b, 32) (iris.hpp:199-205) */
+    const uint64_t t = (uint64_t)1 << 32;
+    const uint64_t bl = (uint64_t)cfg->b * cfg->l;
+    if (!(bl < t / 4 && bl < t - (t >> 1))) return 4;
+  }
   if (cfg->rotations % 2 == 0) return 4;
   if (cfg->backend == ORC_SHAMIR && cfg->rotations > 1 && (cfg->l / 64) % 2 != 0) return 4;
   return 0;
@@ -344,31 +396,31 @@ uint64_t orc_lane_count(uint32_t persons, uint64_t s, uint32_t rotations, int me
   return blocks * s + pairs;
 }
 
-/* Per-party parsed instance (engine.hpp:141-197).  rep: sum/prev (l each);
- * shamir: c0,c1 raw and lc0,lc1 lambda-scaled (l/2 each). */
+/* Per-party parsed instance (engine.hpp:141-197) at width K.  rep: sum/prev;
+ * shamir: a = lambda-scaled [lc0 | lc1], b = raw [c0 | c1]. */
 typedef struct {
-  uint16_t* a; /* rep: sum       shamir: lc0 | lc1  (l entries) */
-  uint16_t* b; /* rep: prev      shamir: c0  | c1   (l entries) */
+  uint32_t* a;
+  uint32_t* b;
 } inst;
 
-/* parse_rep_inst (engine.hpp:162-176) / parse_gr_inst (engine.hpp:178-197).
- * Shamir instances are stored as [lc0 | lc1] and [c0 | c1]. */
-static void parse_inst(int backend, const uint8_t* p, uint32_t l, const gr16 lambda, inst* out) {
-  out->a = (uint16_t*)malloc(sizeof(uint16_t) * l);
-  out->b = (uint16_t*)malloc(sizeof(uint16_t) * l);
+/* parse_rep_inst (engine.hpp:162-176) / parse_gr_inst (engine.hpp:178-197) */
+static void parse_inst(int backend, const uint8_t* p, uint32_t l, unsigned K, const gr lambda, inst* out) {
+  const unsigned w = K / 8;
+  const uint32_t m = kmask(K);
+  out->a = (uint32_t*)malloc(sizeof(uint32_t) * l);
+  out->b = (uint32_t*)malloc(sizeof(uint32_t) * l);
   if (backend == ORC_REPLICATED) {
     for (uint32_t i = 0; i < l; ++i) {
-      const uint16_t own = (uint16_t)(p[4 * i] | (p[4 * i + 1] << 8));
-      const uint16_t prev = (uint16_t)(p[4 * i + 2] | (p[4 * i + 3] << 8));
-      out->a[i] = (uint16_t)(own + prev);
+      const uint32_t own = getw(p + 2 * w * i, K);
+      const uint32_t prev = getw(p + 2 * w * i + w, K);
+      out->a[i] = (own + prev) & m;
       out->b[i] = prev;
     }
   } else {
     const uint32_t h = l / 2;
     for (uint32_t i = 0; i < h; ++i) {
-      gr16 g = {(uint16_t)(p[4 * i] | (p[4 * i + 1] << 8)),
-                (uint16_t)(p[4 * i + 2] | (p[4 * i + 3] << 8))};
-      const gr16 lg = gr_mul(lambda, g);
+      gr g = {getw(p + 2 * w * i, K), getw(p + 2 * w * i + w, K)};
+      const gr lg = gr_mul(lambda, g, K);
       out->a[i] = lg.c0;
       out->a[h + i] = lg.c1;
       out->b[i] = g.c0;
@@ -383,17 +435,16 @@ static void free_inst(inst* x) {
 }
 
 /* rotate_vec (engine.hpp:126-136): out[(i + by) mod n] = v[i]. */
-static void rotate(const uint16_t* v, uint32_t n, int64_t by, uint16_t* out) {
+static void rotate(const uint32_t* v, uint32_t n, int64_t by, uint32_t* out) {
   int64_t s = n ? by % (int64_t)n : 0;
   if (s < 0) s += n;
   for (uint32_t i = 0; i < n; ++i) out[(i + (uint64_t)s) % n] = v[i];
 }
 
-/* RepInst::rotated / GrInst::rotated (engine.hpp:149-159): shamir pairs move
- * by by/2 within each coefficient array. */
+/* RepInst::rotated / GrInst::rotated (engine.hpp:149-159) */
 static void rotate_inst(int backend, const inst* x, uint32_t l, int64_t by, inst* out) {
-  out->a = (uint16_t*)malloc(sizeof(uint16_t) * l);
-  out->b = (uint16_t*)malloc(sizeof(uint16_t) * l);
+  out->a = (uint32_t*)malloc(sizeof(uint32_t) * l);
+  out->b = (uint32_t*)malloc(sizeof(uint32_t) * l);
   if (backend == ORC_REPLICATED) {
     rotate(x->a, l, by, out->a);
     rotate(x->b, l, by, out->b);
@@ -407,11 +458,8 @@ static void rotate_inst(int backend, const inst* x, uint32_t l, int64_t by, inst
   }
 }
 
-/* dot_prep_row (kernels.hpp:38-48): sum(db_sum*q_sum) - sum(db_prev*q_prev)
- * where the query side of party p is (sum, prev) of its own instance.
- * dot_gr_ct_row (kernels.hpp:52-62): sum(lc0*c0 + lc1*c1). */
-static uint16_t dot_row(int backend, const uint16_t* xa, const uint16_t* xb, const inst* y,
-                        uint32_t l) {
+/* dot_prep_row (kernels.hpp:38-48) / dot_gr_ct_row (kernels.hpp:52-62), mod 2^K */
+static uint32_t dot_row(int backend, const uint32_t* xa, const uint32_t* xb, const inst* y, uint32_t l, unsigned K) {
   uint64_t acc = 0;
   if (backend == ORC_REPLICATED) {
     for (uint32_t i = 0; i < l; ++i) {
@@ -421,7 +469,30 @@ static uint16_t dot_row(int backend, const uint16_t* xa, const uint16_t* xb, con
   } else {
     for (uint32_t i = 0; i < l; ++i) acc += (uint64_t)xa[i] * y->b[i];
   }
-  return (uint16_t)acc;
+  return (uint32_t)acc & kmask(K);
+}
+
+/* parse_mask_bits (engine.hpp:199-206) + BitVec::rotated (iris.hpp:56-66) */
+static void mask_bits(const uint8_t* p, uint32_t l, uint64_t* w) {
+  const uint32_t wl = (l + 63) / 64;
+  memset(w, 0, sizeof(uint64_t) * wl);
+  for (uint32_t i = 0; i < l / 8; ++i) w[i / 8] |= (uint64_t)p[i] << (8 * (i % 8));
+}
+static void rotate_bits(const uint64_t* in, uint32_t l, int64_t by, uint64_t* out) {
+  const uint32_t wl = (l + 63) / 64;
+  memset(out, 0, sizeof(uint64_t) * wl);
+  int64_t s = l ? by % (int64_t)l : 0;
+  if (s < 0) s += l;
+  for (uint32_t i = 0; i < l; ++i)
+    if ((in[i / 64] >> (i % 64)) & 1) {
+      const uint32_t j = (uint32_t)((i + (uint64_t)s) % l);
+      out[j / 64] |= (uint64_t)1 << (j % 64);
+    }
+}
+static int64_t popcount_and(const uint64_t* a, const uint64_t* b, uint32_t l) {
+  int64_t c = 0;
+  for (uint32_t i = 0; i < (l + 63) / 64; ++i) c += __builtin_popcountll(a[i] & b[i]);
+  return c;
 }
 
 /* ---- bit-sliced 3-party simulation (circuits.hpp) ---------------------- */
@@ -480,7 +551,6 @@ static void and_gate(prf_state* ps, const brow* x, const brow* y, brow* z, uint6
  * shared with only component k non-zero).  indices ascending as given. */
 static void bit_extract(prf_state* ps, uint64_t n, uint64_t W, unsigned K, uint64_t* const* xs[3],
                         const unsigned* idx, unsigned nidx, brow* result) {
-  /* rows: xs[k][j] = word array of bit j of component k (j < K), else zero */
   typedef struct {
     unsigned m;
     brow* s;
@@ -488,8 +558,6 @@ static void bit_extract(prf_state* ps, uint64_t n, uint64_t W, unsigned K, uint6
     brow chain, u, v, res;
   } instance;
   instance inst[4];
-  brow zero = brow_new(W);
-  /* summand rows in component form */
   brow* a_rows[3];
   unsigned maxj = 0;
   for (unsigned k = 0; k < nidx; ++k) maxj = idx[k] > maxj ? idx[k] : maxj;
@@ -563,7 +631,6 @@ static void bit_extract(prf_state* ps, uint64_t n, uint64_t W, unsigned K, uint6
     }
   }
   for (int q = 0; q < 3; ++q) ps->pos[q] += g * W;
-  /* cleanup */
   for (unsigned k = 0; k < nidx; ++k) {
     instance* I = &inst[k];
     for (unsigned j = 0; j <= I->m; ++j) brow_free(&I->s[j]);
@@ -581,7 +648,6 @@ static void bit_extract(prf_state* ps, uint64_t n, uint64_t W, unsigned K, uint6
   }
   brow_free(&t1);
   brow_free(&t2);
-  brow_free(&zero);
 }
 
 /* share_split (circuits.hpp:152-172): bit j of component k, 64 lanes/word */
@@ -635,12 +701,17 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
               const uint64_t* stream_start, orc_out* out) {
   int rc = orc_validate(cfg);
   if (rc) return rc;
-  const int be = cfg->backend;
+  const int be = cfg->backend, var = cfg->variant;
+  const unsigned KH = orc_code_bits(var), KMs = orc_mask_bits(var), KC = orc_cmp_bits(var);
+  const unsigned KM = KMs ? KMs : 16; /* storage width when shared */
+  const int plain = KMs == 0;
   const uint32_t l = cfg->l;
+  const uint32_t wl = (l + 63) / 64;
   const uint32_t r = membership ? 1 : cfg->rotations;
   const uint32_t half = (r - 1) / 2;
   const int64_t stride = l / 64;
-  const size_t rec = orc_code_record_bytes(be, l) + orc_mask_record_bytes(be, l);
+  const size_t crec = orc_code_record_bytes(be, var, l);
+  const size_t rec = crec + orc_mask_record_bytes(be, var, l);
   const uint8_t* dbp[3] = {db1, db2, db3};
   const uint8_t* qp[3] = {q1, q2, q3};
   const uint32_t ncodes = membership ? 1 : 2 * persons;
@@ -648,44 +719,70 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   const uint64_t npairs = membership ? 0 : (uint64_t)persons * (persons ? persons - 1 : 0) / 2 * 4 * r;
   const uint64_t n = ncols * s + npairs;
   const uint64_t W = ceil_div(n, 64);
+  const uint32_t mH = kmask(KH), mM = kmask(KM);
 
-  uint16_t lam16[6];
-  orc_lambda16(lam16);
+  uint32_t lamH[6], lamM[6];
+  orc_lambda(KH, lamH);
+  orc_lambda(KM, lamM);
 
   /* ---- dot phase (engine.cpp:304-354), per party ---- */
-  uint16_t* hd_add = (uint16_t*)malloc(sizeof(uint16_t) * 3 * (n ? n : 1));
-  uint16_t* ml_add = (uint16_t*)malloc(sizeof(uint16_t) * 3 * (n ? n : 1));
+  uint32_t* hd_add = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
+  uint32_t* ml_add = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
+  int64_t* public_ml = (int64_t*)calloc(n ? n : 1, sizeof(int64_t));
+  /* plain masks: the same bits in every party's payload; parse from party 1 */
+  uint64_t* qmask = NULL;
+  if (plain) {
+    qmask = (uint64_t*)calloc((size_t)ncols * wl, sizeof(uint64_t));
+    uint64_t* tmp = (uint64_t*)calloc(wl, sizeof(uint64_t));
+    for (uint32_t c = 0; c < ncodes; ++c) {
+      mask_bits(qp[0] + c * rec + crec, l, tmp);
+      for (uint32_t j = 0; j < r; ++j) rotate_bits(tmp, l, ((int64_t)j - (int64_t)half) * stride, qmask + (c * r + j) * wl);
+    }
+    free(tmp);
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < (int64_t)s; ++row) {
+      uint64_t dm[256];
+      uint64_t* dmw = wl <= 256 ? dm : (uint64_t*)malloc(sizeof(uint64_t) * wl);
+      mask_bits(dbp[0] + row * rec + crec, l, dmw);
+      for (uint64_t col = 0; col < ncols; ++col) public_ml[col * s + row] = popcount_and(qmask + col * wl, dmw, l);
+      if (dmw != dm) free(dmw);
+    }
+    uint64_t k = ncols * s;
+    for (uint32_t i = 0; i < persons && !membership; ++i)
+      for (uint32_t j = i + 1; j < persons; ++j)
+        for (uint32_t ea = 0; ea < 2; ++ea)
+          for (uint32_t eb = 0; eb < 2; ++eb)
+            for (uint32_t rot = 0; rot < r; ++rot, ++k)
+              public_ml[k] = popcount_and(qmask + ((2 * i + ea) * r + rot) * wl, qmask + ((2 * j + eb) * r + half) * wl, l);
+  }
   for (int p = 0; p < 3; ++p) {
-    const gr16 lam = {lam16[2 * p], lam16[2 * p + 1]};
-    /* query instances, rotated per column */
+    const gr lh = {lamH[2 * p], lamH[2 * p + 1]}, lm = {lamM[2 * p], lamM[2 * p + 1]};
     inst* qc = (inst*)malloc(sizeof(inst) * ncols);
     inst* qm = (inst*)malloc(sizeof(inst) * ncols);
     for (uint32_t c = 0; c < ncodes; ++c) {
       inst code, mask;
-      parse_inst(be, qp[p] + c * rec, l, lam, &code);
-      parse_inst(be, qp[p] + c * rec + orc_code_record_bytes(be, l), l, lam, &mask);
+      parse_inst(be, qp[p] + c * rec, l, KH, lh, &code);
+      if (!plain) parse_inst(be, qp[p] + c * rec + crec, l, KM, lm, &mask);
       for (uint32_t j = 0; j < r; ++j) {
         const int64_t by = ((int64_t)j - (int64_t)half) * stride;
         rotate_inst(be, &code, l, by, &qc[c * r + j]);
-        rotate_inst(be, &mask, l, by, &qm[c * r + j]);
+        if (!plain) rotate_inst(be, &mask, l, by, &qm[c * r + j]);
       }
       free_inst(&code);
-      free_inst(&mask);
+      if (!plain) free_inst(&mask);
     }
-    /* DB rows x every column (lane = col*s + row, engine.cpp:265-274) */
 #pragma omp parallel for schedule(static)
     for (int64_t row = 0; row < (int64_t)s; ++row) {
       inst dc, dm;
-      parse_inst(be, dbp[p] + row * rec, l, lam, &dc);
-      parse_inst(be, dbp[p] + row * rec + orc_code_record_bytes(be, l), l, lam, &dm);
+      parse_inst(be, dbp[p] + row * rec, l, KH, lh, &dc);
+      if (!plain) parse_inst(be, dbp[p] + row * rec + crec, l, KM, lm, &dm);
       for (uint64_t col = 0; col < ncols; ++col) {
-        hd_add[p * n + col * s + row] = dot_row(be, dc.a, dc.b, &qc[col], l);
-        ml_add[p * n + col * s + row] = dot_row(be, dm.a, dm.b, &qm[col], l);
+        hd_add[p * n + col * s + row] = dot_row(be, dc.a, dc.b, &qc[col], l, KH);
+        if (!plain) ml_add[p * n + col * s + row] = dot_row(be, dm.a, dm.b, &qm[col], l, KM);
       }
       free_inst(&dc);
-      free_inst(&dm);
+      if (!plain) free_inst(&dm);
     }
-    /* inner-batch pairs (engine.cpp:275-293, engine.hpp:208-219) */
     uint64_t k = 0;
     for (uint32_t i = 0; i < persons && !membership; ++i)
       for (uint32_t j = i + 1; j < persons; ++j)
@@ -694,20 +791,24 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
             for (uint32_t rot = 0; rot < r; ++rot, ++k) {
               const inst* xs_c = &qc[(2 * i + ea) * r + rot];
               const inst* ys_c = &qc[(2 * j + eb) * r + half];
-              const inst* xs_m = &qm[(2 * i + ea) * r + rot];
-              const inst* ys_m = &qm[(2 * j + eb) * r + half];
-              hd_add[p * n + ncols * s + k] = dot_row(be, xs_c->a, xs_c->b, ys_c, l);
-              ml_add[p * n + ncols * s + k] = dot_row(be, xs_m->a, xs_m->b, ys_m, l);
+              hd_add[p * n + ncols * s + k] = dot_row(be, xs_c->a, xs_c->b, ys_c, l, KH);
+              if (!plain) {
+                const inst* xs_m = &qm[(2 * i + ea) * r + rot];
+                const inst* ys_m = &qm[(2 * j + eb) * r + half];
+                ml_add[p * n + ncols * s + k] = dot_row(be, xs_m->a, xs_m->b, ys_m, l, KM);
+              }
             }
     for (uint64_t c = 0; c < ncols; ++c) {
       free_inst(&qc[c]);
-      free_inst(&qm[c]);
+      if (!plain) free_inst(&qm[c]);
     }
     free(qc);
     free(qm);
   }
-  if (out && out->dot_hd) memcpy(out->dot_hd, hd_add, sizeof(uint16_t) * 3 * n);
-  if (out && out->dot_ml) memcpy(out->dot_ml, ml_add, sizeof(uint16_t) * 3 * n);
+  free(qmask);
+  if (out && out->dot_hd) memcpy(out->dot_hd, hd_add, sizeof(uint32_t) * 3 * n);
+  if (out && out->dot_ml) memcpy(out->dot_ml, ml_add, sizeof(uint32_t) * 3 * n);
+  if (out && out->public_ml) memcpy(out->public_ml, public_ml, sizeof(int64_t) * n);
 
   /* ---- PRF streams (A.3) ---- */
   prf_state ps;
@@ -717,65 +818,77 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
     ps.pos[k] = stream_start ? stream_start[k] : 0;
   }
 
-  /* ---- reshare_pair<16,16> (engine.cpp:80-106): own = z + F(s_p) - F(s_{p-1}),
-   * hd lanes at stream index i, ml lanes at n + i. ---- */
-  uint32_t* hd = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
-  uint32_t* ml = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
+  /* ---- reshare_pair<KH, KM> (engine.cpp:80-106): own = z + F(s_p) - F(s_{p-1}),
+   * hd lanes at stream index i, ml lanes (shared masks only) at n + i. ---- */
+  const uint64_t nml = plain ? 0 : n;
+  uint32_t* hd = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
+  uint32_t* ml = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
   for (uint64_t i = 0; i < n; ++i) {
-    uint16_t fh[3], fm[3];
-    for (int k = 0; k < 3; ++k) {
-      fh[k] = (uint16_t)reader_at(&ps.rd[k], ps.pos[k] + i);
-    }
-    for (int k = 0; k < 3; ++k) {
-      fm[k] = (uint16_t)reader_at(&ps.rd[k], ps.pos[k] + n + i);
-    }
+    uint32_t fh[3], fm[3] = {0, 0, 0};
+    for (int k = 0; k < 3; ++k) fh[k] = (uint32_t)reader_at(&ps.rd[k], ps.pos[k] + i) & mH;
+    if (!plain)
+      for (int k = 0; k < 3; ++k) fm[k] = (uint32_t)reader_at(&ps.rd[k], ps.pos[k] + n + i) & mM;
     for (int p = 0; p < 3; ++p) {
       const int q = (p + 2) % 3;
-      hd[p * n + i] = (uint16_t)(hd_add[p * n + i] + fh[p] - fh[q]);
-      ml[p * n + i] = (uint16_t)(ml_add[p * n + i] + fm[p] - fm[q]);
+      hd[p * n + i] = (hd_add[p * n + i] + fh[p] - fh[q]) & mH;
+      ml[p * n + i] = plain ? 0 : ((ml_add[p * n + i] + fm[p] - fm[q]) & mM);
     }
   }
-  for (int k = 0; k < 3; ++k) ps.pos[k] += 2 * n;
-  if (out && out->rs_hd)
-    for (uint64_t i = 0; i < 3 * n; ++i) out->rs_hd[i] = (uint16_t)hd[i];
-  if (out && out->rs_ml)
-    for (uint64_t i = 0; i < 3 * n; ++i) out->rs_ml[i] = (uint16_t)ml[i];
+  for (int k = 0; k < 3; ++k) ps.pos[k] += n + nml;
+  if (out && out->rs_hd) memcpy(out->rs_hd, hd, sizeof(uint32_t) * 3 * n);
+  if (out && out->rs_ml) memcpy(out->rs_ml, ml, sizeof(uint32_t) * 3 * n);
 
-  /* ---- lift<16,16> (convert.hpp:169-192) ---- */
-  const uint32_t* mlc[3] = {ml, ml + n, ml + 2 * n};
-  uint64_t*** xs = share_split(mlc, n, W, 16);
-  const unsigned lidx[2] = {16, 17};
-  brow ext[2] = {brow_new(W), brow_new(W)};
-  bit_extract(&ps, n, W, 16, (uint64_t* const**)xs, lidx, 2, ext);
-  free_split(xs, 16);
-  uint32_t* inj17 = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
-  uint32_t* inj16 = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
-  uint32_t* i17[3] = {inj17, inj17 + n, inj17 + 2 * n};
-  uint32_t* i16[3] = {inj16, inj16 + n, inj16 + 2 * n};
-  bit_inject(&ps, &ext[1], n, 15, i17); /* bit K+1 into Z_2^(M-1) first */
-  bit_inject(&ps, &ext[0], n, 16, i16);
-  brow_free(&ext[0]);
-  brow_free(&ext[1]);
-  uint32_t* ml32 = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
-  uint32_t* diff = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
-  for (uint64_t i = 0; i < 3 * n; ++i) {
-    /* wide = recast(ml) - const_lift(inj17, 2^17) - const_lift(inj16, 2^16) */
-    ml32[i] = ml[i] - (inj17[i] << 17) - (inj16[i] << 16);
-    /* shared_diff_lanes (engine.hpp:94-120): a*ml32 - const_lift(hd, b) */
-    diff[i] = cfg->a * ml32[i] - cfg->b * hd[i];
+  /* ---- comparison input ---- */
+  uint32_t* ml32 = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
+  uint32_t* diff = (uint32_t*)calloc(3 * (n ? n : 1), sizeof(uint32_t));
+  uint64_t lift_gates = 0;
+  if (plain) {
+    /* plain_diff_lanes<16> (engine.hpp:77-90): public_minus(ceil((1-2r) ml), hd):
+     * component 1 absorbs the public constant (rep3.hpp:59-65). */
+    for (uint64_t i = 0; i < n; ++i) {
+      const int64_t t = (int64_t)ceil((1.0 - 2.0 * cfg->ratio) * (double)public_ml[i]);
+      diff[i] = ((uint32_t)(uint64_t)t - hd[i]) & 0xFFFFu;
+      diff[n + i] = (0u - hd[n + i]) & 0xFFFFu;
+      diff[2 * n + i] = (0u - hd[2 * n + i]) & 0xFFFFu;
+    }
+  } else {
+    if (KMs == 16) {
+      /* ---- lift<16,16> (convert.hpp:169-192) ---- */
+      const uint32_t* mlc[3] = {ml, ml + n, ml + 2 * n};
+      uint64_t*** xs = share_split(mlc, n, W, 16);
+      const unsigned lidx[2] = {16, 17};
+      brow ext[2] = {brow_new(W), brow_new(W)};
+      bit_extract(&ps, n, W, 16, (uint64_t* const**)xs, lidx, 2, ext);
+      free_split(xs, 16);
+      lift_gates = 64;
+      uint32_t* inj17 = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
+      uint32_t* inj16 = (uint32_t*)malloc(sizeof(uint32_t) * 3 * (n ? n : 1));
+      uint32_t* i17[3] = {inj17, inj17 + n, inj17 + 2 * n};
+      uint32_t* i16[3] = {inj16, inj16 + n, inj16 + 2 * n};
+      bit_inject(&ps, &ext[1], n, 15, i17); /* bit K+1 into Z_2^(M-1) first */
+      bit_inject(&ps, &ext[0], n, 16, i16);
+      brow_free(&ext[0]);
+      brow_free(&ext[1]);
+      for (uint64_t i = 0; i < 3 * n; ++i) ml32[i] = ml[i] - (inj17[i] << 17) - (inj16[i] << 16);
+      free(inj17);
+      free(inj16);
+    } else {
+      memcpy(ml32, ml, sizeof(uint32_t) * 3 * n); /* KM = 32: already wide */
+    }
+    /* shared_diff_lanes (engine.hpp:94-120): a*ml32 - b*hd (const_lift for KH=16,
+     * mul_public for KH=32: the same product in Z_2^32) */
+    for (uint64_t i = 0; i < 3 * n; ++i) diff[i] = cfg->a * ml32[i] - cfg->b * hd[i];
   }
-  free(inj17);
-  free(inj16);
   if (out && out->ml32) memcpy(out->ml32, ml32, sizeof(uint32_t) * 3 * n);
   if (out && out->diff) memcpy(out->diff, diff, sizeof(uint32_t) * 3 * n);
 
-  /* ---- msb_batch<32> (circuits.hpp:300-306) ---- */
+  /* ---- msb_batch<KC> (circuits.hpp:300-306) ---- */
   const uint32_t* dc[3] = {diff, diff + n, diff + 2 * n};
-  xs = share_split(dc, n, W, 32);
-  const unsigned midx[1] = {31};
+  uint64_t*** xs = share_split(dc, n, W, KC);
+  const unsigned midx[1] = {KC - 1};
   brow bits = brow_new(W);
-  bit_extract(&ps, n, W, 32, (uint64_t* const**)xs, midx, 1, &bits);
-  free_split(xs, 32);
+  bit_extract(&ps, n, W, KC, (uint64_t* const**)xs, midx, 1, &bits);
+  free_split(xs, KC);
   if (out && out->msb)
     for (int p = 0; p < 3; ++p)
       for (uint64_t i = 0; i < n; ++i) out->msb[p * n + i] = (bits.c[p][i / 64] >> (i % 64)) & 1;
@@ -790,11 +903,7 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   uint64_t* glen = (uint64_t*)calloc(ngroups ? ngroups : 1, sizeof(uint64_t));
   uint64_t** glanes = (uint64_t**)calloc(ngroups ? ngroups : 1, sizeof(uint64_t*));
   for (uint32_t g = 0; g < ngroups; ++g) {
-    uint64_t cnt;
-    if (membership)
-      cnt = s;
-    else
-      cnt = 2ull * r * s + (uint64_t)(persons - 1) * 4 * r;
+    const uint64_t cnt = membership ? s : 2ull * r * s + (uint64_t)(persons - 1) * 4 * r;
     glanes[g] = (uint64_t*)malloc(sizeof(uint64_t) * (cnt ? cnt : 1));
   }
   if (membership) {
@@ -813,7 +922,6 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
           glanes[j][glen[j]++] = k;
         }
   }
-  /* gather group lanes into rows */
   brow* grp = (brow*)malloc(sizeof(brow) * (ngroups ? ngroups : 1));
   uint64_t* gl = (uint64_t*)malloc(sizeof(uint64_t) * (ngroups ? ngroups : 1));
   for (uint32_t g = 0; g < ngroups; ++g) {
@@ -828,7 +936,7 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   uint64_t or_rounds = 0, or_bytes = 0;
   for (;;) {
     int progress = 0;
-    uint64_t used = 0; /* stream words consumed this level (same for all seeds) */
+    uint64_t used = 0;
     for (uint32_t g = 0; g < ngroups; ++g) {
       if (gl[g] <= 1) continue;
       progress = 1;
@@ -862,10 +970,9 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   }
   /* open_bits_to(agg, P1) (circuits.hpp:449-486) */
   if (out && out->person_match)
-    for (uint32_t g = 0; g < ngroups; ++g) {
+    for (uint32_t g = 0; g < ngroups; ++g)
       out->person_match[g] =
           gl[g] == 0 ? 0 : (uint8_t)((grp[g].c[0][0] ^ grp[g].c[1][0] ^ grp[g].c[2][0]) & 1);
-    }
   if (out && out->stream_pos)
     for (int k = 0; k < 3; ++k) out->stream_pos[k] = ps.pos[k];
 
@@ -873,17 +980,17 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   if (out && out->stats) {
     const uint64_t nb8 = ceil_div(n, 8);
     const uint64_t open_bytes = ceil_div(ngroups, 8);
+    const uint64_t msb_gates = 2 * KC - 3;
     for (int p = 0; p < 3; ++p) {
       orc_stats* st = &out->stats[p];
-      st->dot_bytes = 4 * n;
+      st->dot_bytes = n * (KH / 8) + nml * (KM / 8);
       st->dot_rounds = 1;
-      const uint64_t ot = (p == 0) ? 8 * n : 4 * n;
-      st->lift_bytes = 64 * nb8 + ot;
-      st->lift_rounds = 17 + 4;
-      st->msb_bytes = 61 * nb8;
-      st->msb_rounds = 31;
-      st->or_tree_bytes = or_bytes + (p == 0 ? 0 : open_bytes) +
-                          (cfg->debug_rows && p != 0 ? nb8 : 0);
+      const uint64_t ot = lift_gates ? ((p == 0) ? 8 * n : 4 * n) : 0;
+      st->lift_bytes = lift_gates * nb8 + ot;
+      st->lift_rounds = lift_gates ? 17 + 4 : 0;
+      st->msb_bytes = msb_gates * nb8;
+      st->msb_rounds = KC - 1;
+      st->or_tree_bytes = or_bytes + (p == 0 ? 0 : open_bytes) + (cfg->debug_rows && p != 0 ? nb8 : 0);
       st->or_tree_rounds = or_rounds + 1 + (cfg->debug_rows ? 1 : 0);
     }
   }
@@ -899,6 +1006,7 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
   brow_free(&bits);
   free(hd_add);
   free(ml_add);
+  free(public_ml);
   free(hd);
   free(ml);
   free(ml32);
@@ -911,8 +1019,8 @@ int orc_run_local(const orc_config* cfg, uint64_t seed, uint64_t s, const uint64
                   const uint64_t* q_masks, int membership, orc_out* out) {
   int rc = orc_validate(cfg);
   if (rc) return rc;
-  const size_t rec = orc_code_record_bytes(cfg->backend, cfg->l) +
-                     orc_mask_record_bytes(cfg->backend, cfg->l);
+  const size_t rec = orc_code_record_bytes(cfg->backend, cfg->variant, cfg->l) +
+                     orc_mask_record_bytes(cfg->backend, cfg->variant, cfg->l);
   const uint32_t ncodes = membership ? 1 : 2 * persons;
   uint8_t* db[3];
   uint8_t* q[3];
@@ -922,14 +1030,13 @@ int orc_run_local(const orc_config* cfg, uint64_t seed, uint64_t s, const uint64
   }
   orc_rng* dr = orc_rng_sub(seed, 1);
   orc_rng* qr = orc_rng_sub(seed, 2);
-  orc_deal_payload(cfg->backend, cfg->l, s, db_codes, db_masks, dr, db[0], db[1], db[2]);
-  orc_deal_payload(cfg->backend, cfg->l, ncodes, q_codes, q_masks, qr, q[0], q[1], q[2]);
+  orc_deal_payload_v(cfg->backend, cfg->variant, cfg->l, s, db_codes, db_masks, dr, db[0], db[1], db[2]);
+  orc_deal_payload_v(cfg->backend, cfg->variant, cfg->l, ncodes, q_codes, q_masks, qr, q[0], q[1], q[2]);
   orc_rng_free(dr);
   orc_rng_free(qr);
   uint8_t seeds[48];
   orc_party_seeds(seed, seeds);
-  rc = orc_query(cfg, seeds, db[0], db[1], db[2], s, q[0], q[1], q[2], persons, membership, NULL,
-                 out);
+  rc = orc_query(cfg, seeds, db[0], db[1], db[2], s, q[0], q[1], q[2], persons, membership, NULL, out);
   for (int p = 0; p < 3; ++p) {
     free(db[p]);
     free(q[p]);

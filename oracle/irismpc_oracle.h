@@ -6,8 +6,9 @@
  * only as the checker or the CPU baseline — never as the product path.
  *
  * It restates, in plain C, the reference algorithm of
- *   /root/reference/proj (irismpc), Session<B,16,16>::run_schedule
- *   (src/engine.cpp:297-398) and everything it calls, with the exact PRF
+ *   /root/reference/proj (irismpc), Session<B,KH,KM>::run_schedule
+ *   (src/engine.cpp:297-398) for all four variants (plain-mask <16,0>,
+ *   mpc-lift <16,16>, const-lift <16,32>, no-lift <32,32>) and everything it calls, with the exact PRF
  *   consumption order of the reference so that the GPU path can be checked
  *   share-for-share (parity levels L1..L5 of SURVEY.md §8c).
  *
@@ -31,6 +32,8 @@ extern "C" {
 #endif
 
 enum { ORC_REPLICATED = 0, ORC_SHAMIR = 1 };
+/* Variant (shares.hpp:28) */
+enum { ORC_PLAIN_MASK = 0, ORC_MPC_LIFT = 1, ORC_CONST_LIFT = 2, ORC_NO_LIFT = 3 };
 
 /* ---- L0: ChaCha12 counter PRF (prf.hpp:46-135) ---------------------- */
 void orc_chacha_block(const uint8_t seed[16], uint64_t block, uint64_t stream,
@@ -60,14 +63,25 @@ void orc_rng_record(orc_rng* r, uint32_t l, double mask_density, uint64_t* code,
                     uint64_t* mask);
 
 /* ---- L1 Galois ring (galois.hpp:66-128) ------------------------------ */
-/* lambda_p for p=1..3 at 16 bits: out = {l1c0,l1c1,l2c0,l2c1,l3c0,l3c1} */
+/* lambda_p for p=1..3 at K bits: out = {l1c0,l1c1,l2c0,l2c1,l3c0,l3c1} */
+void orc_lambda(unsigned K, uint32_t out[6]);
 void orc_lambda16(uint16_t out[6]);
 
-/* ---- Dealer (shares.hpp:52-130, shares.cpp:61-90), mpc-lift widths ---- */
-size_t orc_code_record_bytes(int backend, uint32_t l);
-size_t orc_mask_record_bytes(int backend, uint32_t l);
+/* ---- Variant widths (shares.hpp:37-48) ---------------------------------- */
+unsigned orc_code_bits(int variant);
+unsigned orc_mask_bits(int variant); /* 0 = public mask bits */
+unsigned orc_cmp_bits(int variant);
+
+/* ---- Dealer (shares.hpp:52-130, shares.cpp:49-90) ----------------------- */
+size_t orc_code_record_bytes(int backend, int variant, uint32_t l);
+size_t orc_mask_record_bytes(int backend, int variant, uint32_t l);
 /* Emits nrec records (code record then mask record per row) for the three
  * parties, drawing from rng exactly as deal_db_payload / deal_query_payload. */
+void orc_deal_payload_v(int backend, int variant, uint32_t l, uint64_t nrec, const uint64_t* codes,
+                        const uint64_t* masks, orc_rng* rng, uint8_t* out1, uint8_t* out2,
+                        uint8_t* out3);
+/* mpc-lift shorthands */
+size_t orc_code_record_bytes16(int backend, uint32_t l);
 void orc_deal_payload(int backend, uint32_t l, uint64_t nrec, const uint64_t* codes,
                       const uint64_t* masks, orc_rng* rng, uint8_t* out1, uint8_t* out2,
                       uint8_t* out3);
@@ -75,10 +89,12 @@ void orc_deal_payload(int backend, uint32_t l, uint64_t nrec, const uint64_t* co
 /* ---- Engine (engine.cpp:21-398) --------------------------------------- */
 typedef struct orc_config {
   int32_t backend;      /* ORC_REPLICATED / ORC_SHAMIR */
+  int32_t variant;      /* ORC_PLAIN_MASK .. ORC_NO_LIFT */
   uint32_t l;           /* code length in bits, multiple of 8 */
-  uint32_t a, b;        /* MatchParams (iris.hpp:157-174); b = 2^16 for mpc-lift */
+  uint32_t a, b;        /* MatchParams (iris.hpp:157-174); b = 2^16 for shared masks */
   uint32_t rotations;   /* odd */
   int32_t debug_rows;   /* open per-lane bits to P1 */
+  double ratio;         /* MatchParams::match_ratio (plain_threshold, iris.hpp:182-184) */
 } orc_config;
 
 /* Analytic communication ledger per party (transport.hpp:54-86), as filled
@@ -93,12 +109,14 @@ typedef struct orc_stats {
 typedef struct orc_out {
   uint8_t* person_match;   /* [persons]  opened at P1 */
   uint8_t* row_bits;       /* [n]        debug_rows opening (cfg.debug_rows) */
-  uint16_t* dot_hd;        /* [3][n] per-party additive hd dots (L1) */
-  uint16_t* dot_ml;        /* [3][n] per-party additive ml dots (L1) */
-  uint16_t* rs_hd;         /* [3][n] components after reshare_pair (L2) */
-  uint16_t* rs_ml;         /* [3][n] */
-  uint32_t* ml32;          /* [3][n] lift<16,16> output components */
-  uint32_t* diff;          /* [3][n] a*ml32 - b*hd32 components */
+  uint32_t* dot_hd;        /* [3][n] per-party additive hd dots mod 2^KH (L1) */
+  uint32_t* dot_ml;        /* [3][n] per-party additive ml dots mod 2^KM (L1) */
+  int64_t* public_ml;      /* [n] plain-mask popcounts (plain-mask only) */
+  uint32_t* rs_hd;         /* [3][n] components after reshare_pair (L2) */
+  uint32_t* rs_ml;         /* [3][n] */
+  uint32_t* ml32;          /* [3][n] 32-bit ml components (lift output / KM=32 copy) */
+  uint32_t* diff;          /* [3][n] comparison input: a*ml32 - b*hd (mod 2^32), or
+                              ceil((1-2r)ml) - hd (mod 2^16, plain-mask) */
   uint8_t* msb;            /* [3][n] MSB (match) bit components */
   uint64_t* stream_pos;    /* [3]   seed stream positions after the query */
   orc_stats* stats;        /* [3]   per party */
@@ -123,7 +141,7 @@ int orc_run_local(const orc_config* cfg, uint64_t seed, uint64_t s, const uint64
 
 /* MatchParams::make(ratio, 16).a (iris.hpp:163-174) */
 uint32_t orc_match_a(double ratio);
-/* EngineConfig::validate (engine.cpp:21-34) for mpc-lift: 0 ok, 4 bounds */
+/* EngineConfig::validate (engine.cpp:21-34): 0 ok, 4 bounds */
 int orc_validate(const orc_config* cfg);
 
 #ifdef __cplusplus

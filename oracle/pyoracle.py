@@ -20,6 +20,8 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 REF_PATH = os.path.join(HERE, "_ref", "libirismpc_ref.so")
 
 REPLICATED, SHAMIR = 0, 1
+PLAIN_MASK, MPC_LIFT, CONST_LIFT, NO_LIFT = 0, 1, 2, 3
+VARIANT_NAMES = {"plain-mask": PLAIN_MASK, "mpc-lift": MPC_LIFT, "const-lift": CONST_LIFT, "no-lift": NO_LIFT}
 
 u8p = C.POINTER(C.c_uint8)
 u16p = C.POINTER(C.c_uint16)
@@ -32,8 +34,9 @@ def _p(a, t):
 
 
 class OrcConfig(C.Structure):
-    _fields_ = [("backend", C.c_int32), ("l", C.c_uint32), ("a", C.c_uint32), ("b", C.c_uint32),
-                ("rotations", C.c_uint32), ("debug_rows", C.c_int32)]
+    _fields_ = [("backend", C.c_int32), ("variant", C.c_int32), ("l", C.c_uint32), ("a", C.c_uint32),
+                ("b", C.c_uint32), ("rotations", C.c_uint32), ("debug_rows", C.c_int32),
+                ("ratio", C.c_double)]
 
 
 class OrcStats(C.Structure):
@@ -43,9 +46,9 @@ class OrcStats(C.Structure):
 
 
 class OrcOut(C.Structure):
-    _fields_ = [("person_match", u8p), ("row_bits", u8p), ("dot_hd", u16p), ("dot_ml", u16p),
-                ("rs_hd", u16p), ("rs_ml", u16p), ("ml32", u32p), ("diff", u32p), ("msb", u8p),
-                ("stream_pos", u64p), ("stats", C.POINTER(OrcStats))]
+    _fields_ = [("person_match", u8p), ("row_bits", u8p), ("dot_hd", u32p), ("dot_ml", u32p),
+                ("public_ml", C.POINTER(C.c_int64)), ("rs_hd", u32p), ("rs_ml", u32p), ("ml32", u32p),
+                ("diff", u32p), ("msb", u8p), ("stream_pos", u64p), ("stats", C.POINTER(OrcStats))]
 
 
 _lib = None
@@ -75,10 +78,16 @@ def lib():
         L.orc_rng_below.restype = C.c_uint64
         L.orc_rng_record.argtypes = [C.c_void_p, C.c_uint32, C.c_double, u64p, u64p]
         L.orc_lambda16.argtypes = [u16p]
-        L.orc_code_record_bytes.argtypes = [C.c_int, C.c_uint32]
+        L.orc_lambda.argtypes = [C.c_uint, u32p]
+        L.orc_code_record_bytes.argtypes = [C.c_int, C.c_int, C.c_uint32]
         L.orc_code_record_bytes.restype = C.c_size_t
-        L.orc_mask_record_bytes.argtypes = [C.c_int, C.c_uint32]
+        L.orc_mask_record_bytes.argtypes = [C.c_int, C.c_int, C.c_uint32]
         L.orc_mask_record_bytes.restype = C.c_size_t
+        for f in ("orc_code_bits", "orc_mask_bits", "orc_cmp_bits"):
+            getattr(L, f).argtypes = [C.c_int]
+            getattr(L, f).restype = C.c_uint
+        L.orc_deal_payload_v.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint64, u64p, u64p, C.c_void_p,
+                                         u8p, u8p, u8p]
         L.orc_deal_payload.argtypes = [C.c_int, C.c_uint32, C.c_uint64, u64p, u64p, C.c_void_p,
                                        u8p, u8p, u8p]
         L.orc_lane_count.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_int]
@@ -111,16 +120,16 @@ def ref():
         R.ref_random_records.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_double),
                                          u64p, u64p]
         R.ref_lambda16.argtypes = [u16p]
-        R.ref_deal.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p,
+        R.ref_deal.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p,
                                u8p, u8p, u8p]
         R.ref_deal.restype = C.c_uint64
-        R.ref_run_local.argtypes = [C.c_int, C.c_uint32, C.c_double, C.c_uint32, C.c_int, C.c_int,
+        R.ref_run_local.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_double, C.c_uint32, C.c_int, C.c_int,
                                     C.c_uint64, C.c_uint64, u64p, u64p, C.c_uint32, u64p, u64p,
                                     C.c_int, u8p, u8p, u64p, C.POINTER(C.c_double), u64p]
-        R.ref_dots_reshare.argtypes = [C.c_int, C.c_uint32, C.c_uint32, u8p, C.POINTER(u8p),
+        R.ref_dots_reshare.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint32, u8p, C.POINTER(u8p),
                                        C.c_uint64, C.POINTER(u8p), C.c_uint32, C.c_int,
-                                       u16p, u16p, u16p, u16p]
-        R.ref_bench_prepare.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint32]
+                                       u32p, u32p, C.POINTER(C.c_int64), u32p, u32p]
+        R.ref_bench_prepare.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint32]
         R.ref_bench_prepare.restype = C.c_void_p
         R.ref_bench_step.argtypes = [C.c_void_p, u8p]
         R.ref_bench_step.restype = C.c_double
@@ -135,9 +144,21 @@ def words(l: int) -> int:
     return (l + 63) // 64
 
 
-def record_bytes(backend: int, l: int) -> int:
+def record_bytes(backend: int, l: int, variant: int = MPC_LIFT) -> int:
     L = lib()
-    return int(L.orc_code_record_bytes(backend, l) + L.orc_mask_record_bytes(backend, l))
+    return int(L.orc_code_record_bytes(backend, variant, l) + L.orc_mask_record_bytes(backend, variant, l))
+
+
+def code_bits(variant: int) -> int:
+    return int(lib().orc_code_bits(variant))
+
+
+def mask_bits(variant: int) -> int:
+    return int(lib().orc_mask_bits(variant))
+
+
+def cmp_bits(variant: int) -> int:
+    return int(lib().orc_cmp_bits(variant))
 
 
 def party_seeds(master: int) -> np.ndarray:
@@ -161,6 +182,12 @@ def seed_from_u64(v: int) -> np.ndarray:
 def lambda16() -> np.ndarray:
     out = np.zeros(6, np.uint16)
     lib().orc_lambda16(_p(out, u16p))
+    return out
+
+
+def lambda_k(K: int) -> np.ndarray:
+    out = np.zeros(6, np.uint32)
+    lib().orc_lambda(K, _p(out, u32p))
     return out
 
 
@@ -198,14 +225,14 @@ def records(rng: Rng, l: int, n: int, density: float = 0.9):
     return codes, masks
 
 
-def deal(backend: int, l: int, codes: np.ndarray, masks: np.ndarray, rng: Rng):
+def deal(backend: int, l: int, codes: np.ndarray, masks: np.ndarray, rng: Rng, variant: int = MPC_LIFT):
     """deal_db_payload / deal_query_payload -> three uint8 payloads."""
     n = codes.shape[0]
-    rb = record_bytes(backend, l)
+    rb = record_bytes(backend, l, variant)
     outs = [np.zeros(max(1, n * rb), np.uint8) for _ in range(3)]
-    lib().orc_deal_payload(backend, l, n, _p(np.ascontiguousarray(codes), u64p),
-                           _p(np.ascontiguousarray(masks), u64p), rng.h,
-                           *[_p(o, u8p) for o in outs])
+    lib().orc_deal_payload_v(backend, variant, l, n, _p(np.ascontiguousarray(codes), u64p),
+                             _p(np.ascontiguousarray(masks), u64p), rng.h,
+                             *[_p(o, u8p) for o in outs])
     return [o[: n * rb] for o in outs]
 
 
@@ -215,6 +242,7 @@ class QueryResult:
     row_bits: np.ndarray | None = None
     dot_hd: np.ndarray | None = None
     dot_ml: np.ndarray | None = None
+    public_ml: np.ndarray | None = None
     rs_hd: np.ndarray | None = None
     rs_ml: np.ndarray | None = None
     ml32: np.ndarray | None = None
@@ -225,36 +253,47 @@ class QueryResult:
 
 
 def make_config(backend: int, l: int, ratio: float = 0.375, rotations: int = 31,
-                debug_rows: bool = False) -> OrcConfig:
+                debug_rows: bool = False, variant: int = MPC_LIFT) -> OrcConfig:
     L = lib()
-    return OrcConfig(backend, l, L.orc_match_a(ratio), 1 << 16, rotations, 1 if debug_rows else 0)
+    return OrcConfig(backend, variant, l, L.orc_match_a(ratio), 1 << 16, rotations, 1 if debug_rows else 0,
+                     ratio)
 
 
 def _alloc_out(n: int, ngroups: int, want_all: bool):
     arrs = dict(person_match=np.zeros(max(1, ngroups), np.uint8), row_bits=np.zeros(max(1, n), np.uint8))
     if want_all:
-        arrs.update(dot_hd=np.zeros(3 * max(1, n), np.uint16), dot_ml=np.zeros(3 * max(1, n), np.uint16),
-                    rs_hd=np.zeros(3 * max(1, n), np.uint16), rs_ml=np.zeros(3 * max(1, n), np.uint16),
-                    ml32=np.zeros(3 * max(1, n), np.uint32), diff=np.zeros(3 * max(1, n), np.uint32),
-                    msb=np.zeros(3 * max(1, n), np.uint8))
+        arrs.update({k: np.zeros(3 * max(1, n), np.uint32)
+                     for k in ("dot_hd", "dot_ml", "rs_hd", "rs_ml", "ml32", "diff")})
+        arrs.update(public_ml=np.zeros(max(1, n), np.int64), msb=np.zeros(3 * max(1, n), np.uint8))
     stats = (OrcStats * 3)()
     pos = np.zeros(3, np.uint64)
     out = OrcOut(_p(arrs["person_match"], u8p), _p(arrs["row_bits"], u8p),
-                 _p(arrs.get("dot_hd"), u16p), _p(arrs.get("dot_ml"), u16p),
-                 _p(arrs.get("rs_hd"), u16p), _p(arrs.get("rs_ml"), u16p),
+                 _p(arrs.get("dot_hd"), u32p), _p(arrs.get("dot_ml"), u32p),
+                 _p(arrs.get("public_ml"), C.POINTER(C.c_int64)),
+                 _p(arrs.get("rs_hd"), u32p), _p(arrs.get("rs_ml"), u32p),
                  _p(arrs.get("ml32"), u32p), _p(arrs.get("diff"), u32p), _p(arrs.get("msb"), u8p),
                  _p(pos, u64p), C.cast(stats, C.POINTER(OrcStats)))
     return out, arrs, stats, pos
 
 
-def _finish(arrs, stats, pos, n, ngroups, want_all, debug_rows):
+def _width_dtype(bits: int):
+    return np.uint16 if bits == 16 else np.uint32
+
+
+def _finish(arrs, stats, pos, n, ngroups, want_all, debug_rows, variant=MPC_LIFT):
     res = QueryResult(person_match=arrs["person_match"][:ngroups].copy())
     if debug_rows:
         res.row_bits = arrs["row_bits"][:n].copy()
     if want_all:
-        for k, dt in (("dot_hd", None), ("dot_ml", None), ("rs_hd", None), ("rs_ml", None),
-                      ("ml32", None), ("diff", None), ("msb", None)):
-            setattr(res, k, arrs[k][: 3 * n].reshape(3, n).copy())
+        # dot / reshare arrays in their ring's width (u16 for 16-bit rings)
+        kh, km = code_bits(variant), mask_bits(variant)
+        widths = dict(dot_hd=kh, rs_hd=kh, dot_ml=km or 16, rs_ml=km or 16, ml32=32,
+                      diff=cmp_bits(variant))
+        for k, bits in widths.items():
+            setattr(res, k, arrs[k][: 3 * n].reshape(3, n).astype(_width_dtype(bits)))
+        res.msb = arrs["msb"][: 3 * n].reshape(3, n).copy()
+        if km == 0:
+            res.public_ml = arrs["public_ml"][:n].copy()
     res.stream_pos = pos.copy()
     res.stats = [{f: getattr(stats[p], f) for f, _ in OrcStats._fields_} for p in range(3)]
     return res
@@ -274,7 +313,7 @@ def query(cfg: OrcConfig, seeds: np.ndarray, db: list, s: int, q: list, persons:
                      1 if membership else 0, _p(ss, u64p), C.byref(out))
     if rc:
         raise RuntimeError(f"orc_query failed with status {rc}")
-    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows)
+    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows, cfg.variant)
 
 
 def run_local(cfg: OrcConfig, seed: int, db_codes, db_masks, q_codes, q_masks, persons: int,
@@ -291,14 +330,14 @@ def run_local(cfg: OrcConfig, seed: int, db_codes, db_masks, q_codes, q_masks, p
                          1 if membership else 0, C.byref(out))
     if rc:
         raise RuntimeError(f"orc_run_local failed with status {rc}")
-    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows)
+    return _finish(arrs, stats, pos, n, ngroups, want_all, cfg.debug_rows, cfg.variant)
 
 
 # ------------------------------------------------------- the reference (_ref)
 
 def ref_run_local(backend: int, l: int, ratio: float, rotations: int, seed: int, db_codes, db_masks,
                   q_codes, q_masks, persons: int, membership: bool = False, debug_rows: bool = False,
-                  parallel_dot: bool = True):
+                  parallel_dot: bool = True, variant: int = MPC_LIFT):
     R = ref()
     s = db_codes.shape[0]
     n = int(lib().orc_lane_count(persons, s, rotations, 1 if membership else 0))
@@ -310,7 +349,7 @@ def ref_run_local(backend: int, l: int, ratio: float, rotations: int, seed: int,
     lanes = C.c_uint64(0)
     dc = np.ascontiguousarray(db_codes if s else np.zeros((1, words(l)), np.uint64))
     dm = np.ascontiguousarray(db_masks if s else np.zeros((1, words(l)), np.uint64))
-    rc = R.ref_run_local(backend, l, ratio, rotations, 1 if debug_rows else 0, 1 if parallel_dot else 0,
+    rc = R.ref_run_local(backend, variant, l, ratio, rotations, 1 if debug_rows else 0, 1 if parallel_dot else 0,
                          seed, s, _p(dc, u64p), _p(dm, u64p), persons,
                          _p(np.ascontiguousarray(q_codes), u64p), _p(np.ascontiguousarray(q_masks), u64p),
                          1 if membership else 0, _p(pm, u8p), _p(rb, u8p), _p(st, u64p),
@@ -325,16 +364,24 @@ def ref_run_local(backend: int, l: int, ratio: float, rotations: int, seed: int,
 
 
 def ref_dots_reshare(backend: int, l: int, rotations: int, seeds, db: list, s: int, q: list,
-                     persons: int, membership: bool = False):
+                     persons: int, membership: bool = False, variant: int = MPC_LIFT):
+    """Reference L1/L2 arrays (dot_hd, dot_ml, rs_hd, rs_ml) in their ring widths;
+    for plain-mask dot_ml / rs_ml are empty and `ref_dots_reshare.public_ml`
+    holds the public popcounts of the last call."""
     R = ref()
     n = int(lib().orc_lane_count(persons, s, rotations, 1 if membership else 0))
-    outs = [np.zeros(3 * max(1, n), np.uint16) for _ in range(4)]
+    outs = [np.zeros(3 * max(1, n), np.uint32) for _ in range(4)]
+    pub = np.zeros(max(1, n), np.int64)
     dbb = [np.ascontiguousarray(x, np.uint8) if len(x) else np.zeros(1, np.uint8) for x in db]
     qb = [np.ascontiguousarray(x, np.uint8) for x in q]
     dbp = (u8p * 3)(*[_p(x, u8p) for x in dbb])
     qp = (u8p * 3)(*[_p(x, u8p) for x in qb])
-    rc = R.ref_dots_reshare(backend, l, rotations, _p(np.ascontiguousarray(seeds, np.uint8), u8p),
-                            dbp, s, qp, persons, 1 if membership else 0, *[_p(o, u16p) for o in outs])
+    rc = R.ref_dots_reshare(backend, variant, l, rotations, _p(np.ascontiguousarray(seeds, np.uint8), u8p),
+                            dbp, s, qp, persons, 1 if membership else 0, _p(outs[0], u32p), _p(outs[1], u32p),
+                            _p(pub, C.POINTER(C.c_int64)), _p(outs[2], u32p), _p(outs[3], u32p))
     if rc:
         raise RuntimeError(f"ref_dots_reshare failed with status {rc}")
-    return [o[: 3 * n].reshape(3, n) for o in outs]
+    kh, km = code_bits(variant), mask_bits(variant)
+    ref_dots_reshare.public_ml = pub[:n].copy() if km == 0 else None
+    w = [kh, km or 16, kh, km or 16]
+    return [o[: 3 * n].reshape(3, n).astype(_width_dtype(b)) for o, b in zip(outs, w)]

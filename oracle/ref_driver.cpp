@@ -9,6 +9,7 @@
 // kernels::dot_*_rows (kernels.cpp:29-53), detail::parse_*_inst and the
 // SeedPair zero shares in the order of reshare_pair (engine.cpp:80-106).
 
+#include <bit>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -36,11 +37,11 @@ IrisRecord to_record(std::uint32_t l, const std::uint64_t* code, const std::uint
   return IrisRecord(std::move(c), std::move(m));
 }
 
-EngineConfig make_cfg(int backend, std::uint32_t l, double ratio, std::uint32_t rotations,
+EngineConfig make_cfg(int backend, int variant, std::uint32_t l, double ratio, std::uint32_t rotations,
                       int debug_rows, int parallel_dot) {
   EngineConfig cfg;
   cfg.backend = backend ? Backend::shamir : Backend::replicated;
-  cfg.variant = Variant::mpc_lift;
+  cfg.variant = static_cast<Variant>(variant);
   cfg.l = l;
   cfg.params = MatchParams::make(ratio, 16);
   cfg.rotations = rotations;
@@ -74,6 +75,156 @@ void fill_stats(const MembershipResult& r, std::uint64_t* st) {
   st[5] = r.stats.lift_rounds;
   st[6] = r.stats.msb_rounds;
   st[7] = r.stats.or_tree_rounds;
+}
+
+}  // namespace
+
+namespace {
+
+// Rotated query instances, rotated[c][j] at offset (j - half) * l/64
+// (Session::batch_query, engine.cpp:240-256).
+template <typename Inst, typename Parse>
+std::vector<std::vector<Inst>> rotated_queries(Parse parse, std::uint32_t ncodes, unsigned r,
+                                               std::ptrdiff_t stride) {
+  const int half = static_cast<int>(r - 1) / 2;
+  std::vector<std::vector<Inst>> out(ncodes);
+  for (std::uint32_t c = 0; c < ncodes; ++c) {
+    const Inst base = parse(c);
+    for (unsigned j = 0; j < r; ++j) out[c].push_back(base.rotated((static_cast<int>(j) - half) * stride));
+  }
+  return out;
+}
+
+// Per-party additive dots of one record field (code at byte offset 0 or the
+// mask at `off`) at width K: db blocks via kernels::dot_*_rows, then the pair
+// lanes via detail::*_pair_dot, in the schedule order of engine.cpp:262-293.
+template <unsigned K>
+void field_dots(Backend be, PartyId self, std::uint32_t l, const std::uint8_t* db, std::size_t rec,
+                std::size_t off, std::uint64_t s, const std::uint8_t* q, std::uint32_t ncodes, unsigned r,
+                std::uint32_t persons, bool membership, std::vector<Ring<K>>& out) {
+  const std::ptrdiff_t stride = static_cast<std::ptrdiff_t>(l / 64);
+  const unsigned half = (r - 1) / 2;
+  const std::uint64_t ncols = static_cast<std::uint64_t>(ncodes) * r;
+  if (be == Backend::replicated) {
+    kernels::PrepMatrix<K> m;
+    m.rows = s;
+    m.len = l;
+    for (std::uint64_t row = 0; row < s; ++row) {
+      const std::uint8_t* p = db + row * rec + off;
+      auto ci = detail::parse_rep_inst<K>(p, l);
+      m.own_sum.insert(m.own_sum.end(), ci.sum.begin(), ci.sum.end());
+      m.prev.insert(m.prev.end(), ci.prev.begin(), ci.prev.end());
+    }
+    auto qs = rotated_queries<detail::RepInst<K>>(
+        [&](std::uint32_t c) {
+          const std::uint8_t* p = q + c * rec + off;
+          return detail::parse_rep_inst<K>(p, l);
+        },
+        ncodes, r, stride);
+    for (std::uint64_t col = 0; col < ncols; ++col) {
+      const auto& y = qs[col / r][col % r];
+      kernels::dot_prep_rows<K>(m, y.sum, y.prev, std::span<Ring<K>>(out.data() + col * s, s), true);
+    }
+    std::uint64_t k = ncols * s;
+    for (std::uint32_t i = 0; i < persons && !membership; ++i)
+      for (std::uint32_t j = i + 1; j < persons; ++j)
+        for (unsigned ea = 0; ea < 2; ++ea)
+          for (unsigned eb = 0; eb < 2; ++eb)
+            for (unsigned rot = 0; rot < r; ++rot, ++k)
+              out[k] = detail::rep_pair_dot<K>(qs[2 * i + ea][rot], qs[2 * j + eb][half]);
+  } else {
+    kernels::GrMatrix<K> m;
+    m.rows = s;
+    m.len = l / 2;
+    for (std::uint64_t row = 0; row < s; ++row) {
+      const std::uint8_t* p = db + row * rec + off;
+      auto ci = detail::parse_gr_inst<K>(p, l, self);
+      m.c0.insert(m.c0.end(), ci.lc0.begin(), ci.lc0.end());
+      m.c1.insert(m.c1.end(), ci.lc1.begin(), ci.lc1.end());
+    }
+    auto qs = rotated_queries<detail::GrInst<K>>(
+        [&](std::uint32_t c) {
+          const std::uint8_t* p = q + c * rec + off;
+          return detail::parse_gr_inst<K>(p, l, self);
+        },
+        ncodes, r, stride);
+    for (std::uint64_t col = 0; col < ncols; ++col) {
+      const auto& y = qs[col / r][col % r];
+      kernels::dot_gr_ct_rows<K>(m, y.c0, y.c1, std::span<Ring<K>>(out.data() + col * s, s), true);
+    }
+    std::uint64_t k = ncols * s;
+    for (std::uint32_t i = 0; i < persons && !membership; ++i)
+      for (std::uint32_t j = i + 1; j < persons; ++j)
+        for (unsigned ea = 0; ea < 2; ++ea)
+          for (unsigned eb = 0; eb < 2; ++eb)
+            for (unsigned rot = 0; rot < r; ++rot, ++k)
+              out[k] = detail::gr_pair_dot<K>(qs[2 * i + ea][rot], qs[2 * j + eb][half]);
+  }
+}
+
+// Public-mask popcounts (engine.cpp:329-334, 349-350) over parse_mask_bits +
+// BitVec::rotated; popcount_and is restated (it is file-local to engine.cpp).
+void plain_ml(std::uint32_t l, const std::uint8_t* db, std::size_t rec, std::size_t off, std::uint64_t s,
+              const std::uint8_t* q, std::uint32_t ncodes, unsigned r, std::uint32_t persons,
+              bool membership, std::int64_t* out) {
+  auto pc = [](const BitVec& a, const BitVec& b) {
+    std::int64_t c = 0;
+    for (std::size_t i = 0; i < a.words().size(); ++i) c += std::popcount(a.words()[i] & b.words()[i]);
+    return c;
+  };
+  const std::ptrdiff_t stride = static_cast<std::ptrdiff_t>(l / 64);
+  const int half = static_cast<int>(r - 1) / 2;
+  std::vector<std::vector<BitVec>> qs(ncodes);
+  for (std::uint32_t c = 0; c < ncodes; ++c) {
+    const std::uint8_t* p = q + c * rec + off;
+    const BitVec m = detail::parse_mask_bits(p, l);
+    for (unsigned j = 0; j < r; ++j) qs[c].push_back(m.rotated((static_cast<int>(j) - half) * stride));
+  }
+  const std::uint64_t ncols = static_cast<std::uint64_t>(ncodes) * r;
+  for (std::uint64_t row = 0; row < s; ++row) {
+    const std::uint8_t* p = db + row * rec + off;
+    const BitVec m = detail::parse_mask_bits(p, l);
+    for (std::uint64_t col = 0; col < ncols; ++col) out[col * s + row] = pc(qs[col / r][col % r], m);
+  }
+  std::uint64_t k = ncols * s;
+  for (std::uint32_t i = 0; i < persons && !membership; ++i)
+    for (std::uint32_t j = i + 1; j < persons; ++j)
+      for (unsigned ea = 0; ea < 2; ++ea)
+        for (unsigned eb = 0; eb < 2; ++eb)
+          for (unsigned rot = 0; rot < r; ++rot, ++k) out[k] = pc(qs[2 * i + ea][rot], qs[2 * j + eb][half]);
+}
+
+template <unsigned KH, unsigned KM>
+void dots_reshare_t(Backend be, Variant v, std::uint32_t l, unsigned r, const std::array<Seed, 3>& seeds,
+                    const std::uint8_t* const* db, std::uint64_t s, const std::uint8_t* const* q,
+                    std::uint32_t persons, bool membership, std::uint64_t n, std::uint32_t* dot_hd,
+                    std::uint32_t* dot_ml, std::int64_t* public_ml, std::uint32_t* rs_hd,
+                    std::uint32_t* rs_ml) {
+  const std::size_t crec = code_record_bytes(be, v, l);
+  const std::size_t rec = crec + mask_record_bytes(be, v, l);
+  const std::uint32_t ncodes = membership ? 1 : 2 * persons;
+  if (KM == 0 && public_ml) plain_ml(l, db[0], rec, crec, s, q[0], ncodes, r, persons, membership, public_ml);
+  for (unsigned pi = 0; pi < 3; ++pi) {
+    const PartyId self = static_cast<PartyId>(pi + 1);
+    std::vector<Ring<KH>> hd(n);
+    field_dots<KH>(be, self, l, db[pi], rec, 0, s, q[pi], ncodes, r, persons, membership, hd);
+    constexpr unsigned KMs = KM == 0 ? 16 : KM;
+    std::vector<Ring<KMs>> ml(KM == 0 ? 0 : n);
+    if constexpr (KM != 0)
+      field_dots<KM>(be, self, l, db[pi], rec, crec, s, q[pi], ncodes, r, persons, membership, ml);
+    // reshare_pair<KH, KM> order (engine.cpp:80-106): hd lanes, then ml lanes.
+    SeedPair sp = seed_pair_for(self, seeds);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      if (dot_hd) dot_hd[pi * n + i] = static_cast<std::uint32_t>(hd[i].value());
+      const auto z = hd[i] + sp.zero_ring<KH>();
+      if (rs_hd) rs_hd[pi * n + i] = static_cast<std::uint32_t>(z.value());
+    }
+    for (std::uint64_t i = 0; i < ml.size(); ++i) {
+      if (dot_ml) dot_ml[pi * n + i] = static_cast<std::uint32_t>(ml[i].value());
+      const auto z = ml[i] + sp.zero_ring<KMs>();
+      if (rs_ml) rs_ml[pi * n + i] = static_cast<std::uint32_t>(z.value());
+    }
+  }
 }
 
 }  // namespace
@@ -126,7 +277,7 @@ void ref_lambda16(std::uint16_t out[6]) {
 }
 
 // deal_db_payload with sub_rng(seed, tag) (cluster.cpp:24-26,55-57).
-std::uint64_t ref_deal(int backend, std::uint32_t l, std::uint64_t seed, std::uint64_t tag,
+std::uint64_t ref_deal(int backend, int variant, std::uint32_t l, std::uint64_t seed, std::uint64_t tag,
                        std::uint64_t nrec, const std::uint64_t* codes, const std::uint64_t* masks,
                        std::uint8_t* out1, std::uint8_t* out2, std::uint8_t* out3) {
   IrisDb db(l);
@@ -134,7 +285,7 @@ std::uint64_t ref_deal(int backend, std::uint32_t l, std::uint64_t seed, std::ui
   for (std::uint64_t r = 0; r < nrec; ++r) db.add(to_record(l, codes + r * wl, masks + r * wl));
   Rng rng(CtrPrf::derive(CtrPrf::seed_from_u64(seed), tag));
   const auto pay = deal_db_payload(db, backend ? Backend::shamir : Backend::replicated,
-                                   Variant::mpc_lift, rng);
+                                   static_cast<Variant>(variant), rng);
   std::memcpy(out1, pay[0].data(), pay[0].size());
   std::memcpy(out2, pay[1].data(), pay[1].size());
   std::memcpy(out3, pay[2].data(), pay[2].size());
@@ -144,7 +295,7 @@ std::uint64_t ref_deal(int backend, std::uint32_t l, std::uint64_t seed, std::ui
 // run_batch_local / run_membership_local.  stats: [3][8] per party
 // (dot, lift, msb, or bytes; dot, lift, msb, or rounds); wall_ms: max over
 // parties of QueryStats.wall_ms (run_schedule only).
-int ref_run_local(int backend, std::uint32_t l, double ratio, std::uint32_t rotations,
+int ref_run_local(int backend, int variant, std::uint32_t l, double ratio, std::uint32_t rotations,
                   int debug_rows, int parallel_dot, std::uint64_t seed, std::uint64_t s,
                   const std::uint64_t* db_codes, const std::uint64_t* db_masks,
                   std::uint32_t persons, const std::uint64_t* q_codes,
@@ -152,7 +303,7 @@ int ref_run_local(int backend, std::uint32_t l, double ratio, std::uint32_t rota
                   std::uint8_t* row_bits, std::uint64_t* stats, double* wall_ms,
                   std::uint64_t* lanes) {
   try {
-    const auto cfg = make_cfg(backend, l, ratio, rotations, debug_rows, parallel_dot);
+    const auto cfg = make_cfg(backend, variant, l, ratio, rotations, debug_rows, parallel_dot);
     const std::size_t wl = (l + 63) / 64;
     IrisDb db(l);
     for (std::uint64_t r = 0; r < s; ++r) db.add(to_record(l, db_codes + r * wl, db_masks + r * wl));
@@ -183,122 +334,41 @@ int ref_run_local(int backend, std::uint32_t l, double ratio, std::uint32_t rota
   }
 }
 
-// L1 + L2: per-party additive dot outputs and reshared components, computed
-// with the reference's parse/dot kernels and SeedPair zero shares in the
-// reshare_pair order.  Arrays are [party][lane].
-int ref_dots_reshare(int backend, std::uint32_t l, std::uint32_t rotations,
+
+// L1 + L2: per-party additive dot outputs (mod 2^KH / 2^KM; public popcounts
+// for plain-mask) and reshared components, computed with the reference's
+// parse/dot kernels and SeedPair zero shares in the reshare_pair order.
+// Arrays are [party][lane].
+int ref_dots_reshare(int backend, int variant, std::uint32_t l, std::uint32_t rotations,
                      const std::uint8_t seeds48[48], const std::uint8_t* const* db,
                      std::uint64_t s, const std::uint8_t* const* q, std::uint32_t persons,
-                     int membership, std::uint16_t* dot_hd, std::uint16_t* dot_ml,
-                     std::uint16_t* rs_hd, std::uint16_t* rs_ml) {
+                     int membership, std::uint32_t* dot_hd, std::uint32_t* dot_ml,
+                     std::int64_t* public_ml, std::uint32_t* rs_hd, std::uint32_t* rs_ml) {
   try {
     const Backend be = backend ? Backend::shamir : Backend::replicated;
-    const std::size_t crec = code_record_bytes(be, Variant::mpc_lift, l);
-    const std::size_t rec = crec + mask_record_bytes(be, Variant::mpc_lift, l);
+    const Variant v = static_cast<Variant>(variant);
     const unsigned r = membership ? 1 : rotations;
-    const int half = static_cast<int>(r - 1) / 2;
-    const std::ptrdiff_t stride = static_cast<std::ptrdiff_t>(l / 64);
     const std::uint32_t ncodes = membership ? 1 : 2 * persons;
-    const std::uint64_t ncols = static_cast<std::uint64_t>(ncodes) * r;
-    const std::uint64_t npairs =
-        membership ? 0 : static_cast<std::uint64_t>(persons) * (persons ? persons - 1 : 0) / 2 * 4 * r;
-    const std::uint64_t n = ncols * s + npairs;
+    const std::uint64_t n = static_cast<std::uint64_t>(ncodes) * r * s +
+        (membership ? 0 : static_cast<std::uint64_t>(persons) * (persons ? persons - 1 : 0) / 2 * 4 * r);
     std::array<Seed, 3> seeds;
     for (int k = 0; k < 3; ++k) std::memcpy(seeds[k].bytes.data(), seeds48 + 16 * k, 16);
-
-    for (unsigned pi = 0; pi < 3; ++pi) {
-      const PartyId self = static_cast<PartyId>(pi + 1);
-      std::vector<R16> hd(n), ml(n);
-      if (be == Backend::replicated) {
-        kernels::PrepMatrix<16> mc, mm;
-        mc.rows = mm.rows = s;
-        mc.len = mm.len = l;
-        for (std::uint64_t row = 0; row < s; ++row) {
-          const std::uint8_t* p = db[pi] + row * rec;
-          auto ci = detail::parse_rep_inst<16>(p, l);
-          auto mi = detail::parse_rep_inst<16>(p, l);
-          mc.own_sum.insert(mc.own_sum.end(), ci.sum.begin(), ci.sum.end());
-          mc.prev.insert(mc.prev.end(), ci.prev.begin(), ci.prev.end());
-          mm.own_sum.insert(mm.own_sum.end(), mi.sum.begin(), mi.sum.end());
-          mm.prev.insert(mm.prev.end(), mi.prev.begin(), mi.prev.end());
-        }
-        std::vector<std::vector<detail::RepInst<16>>> qc(ncodes), qm(ncodes);
-        for (std::uint32_t c = 0; c < ncodes; ++c) {
-          const std::uint8_t* p = q[pi] + c * rec;
-          auto ci = detail::parse_rep_inst<16>(p, l);
-          auto mi = detail::parse_rep_inst<16>(p, l);
-          for (unsigned j = 0; j < r; ++j) {
-            const std::ptrdiff_t by = (static_cast<int>(j) - half) * stride;
-            qc[c].push_back(ci.rotated(by));
-            qm[c].push_back(mi.rotated(by));
-          }
-        }
-        for (std::uint64_t col = 0; col < ncols; ++col) {
-          const auto& yc = qc[col / r][col % r];
-          const auto& ym = qm[col / r][col % r];
-          kernels::dot_prep_rows<16>(mc, yc.sum, yc.prev, std::span<R16>(hd.data() + col * s, s), true);
-          kernels::dot_prep_rows<16>(mm, ym.sum, ym.prev, std::span<R16>(ml.data() + col * s, s), true);
-        }
-        std::uint64_t k = ncols * s;
-        for (std::uint32_t i = 0; i < persons && !membership; ++i)
-          for (std::uint32_t j = i + 1; j < persons; ++j)
-            for (unsigned ea = 0; ea < 2; ++ea)
-              for (unsigned eb = 0; eb < 2; ++eb)
-                for (unsigned rot = 0; rot < r; ++rot, ++k) {
-                  hd[k] = detail::rep_pair_dot<16>(qc[2 * i + ea][rot], qc[2 * j + eb][half]);
-                  ml[k] = detail::rep_pair_dot<16>(qm[2 * i + ea][rot], qm[2 * j + eb][half]);
-                }
-      } else {
-        kernels::GrMatrix<16> mc, mm;
-        mc.rows = mm.rows = s;
-        mc.len = mm.len = l / 2;
-        for (std::uint64_t row = 0; row < s; ++row) {
-          const std::uint8_t* p = db[pi] + row * rec;
-          auto ci = detail::parse_gr_inst<16>(p, l, self);
-          auto mi = detail::parse_gr_inst<16>(p, l, self);
-          mc.c0.insert(mc.c0.end(), ci.lc0.begin(), ci.lc0.end());
-          mc.c1.insert(mc.c1.end(), ci.lc1.begin(), ci.lc1.end());
-          mm.c0.insert(mm.c0.end(), mi.lc0.begin(), mi.lc0.end());
-          mm.c1.insert(mm.c1.end(), mi.lc1.begin(), mi.lc1.end());
-        }
-        std::vector<std::vector<detail::GrInst<16>>> qc(ncodes), qm(ncodes);
-        for (std::uint32_t c = 0; c < ncodes; ++c) {
-          const std::uint8_t* p = q[pi] + c * rec;
-          auto ci = detail::parse_gr_inst<16>(p, l, self);
-          auto mi = detail::parse_gr_inst<16>(p, l, self);
-          for (unsigned j = 0; j < r; ++j) {
-            const std::ptrdiff_t by = (static_cast<int>(j) - half) * stride;
-            qc[c].push_back(ci.rotated(by));
-            qm[c].push_back(mi.rotated(by));
-          }
-        }
-        for (std::uint64_t col = 0; col < ncols; ++col) {
-          const auto& yc = qc[col / r][col % r];
-          const auto& ym = qm[col / r][col % r];
-          kernels::dot_gr_ct_rows<16>(mc, yc.c0, yc.c1, std::span<R16>(hd.data() + col * s, s), true);
-          kernels::dot_gr_ct_rows<16>(mm, ym.c0, ym.c1, std::span<R16>(ml.data() + col * s, s), true);
-        }
-        std::uint64_t k = ncols * s;
-        for (std::uint32_t i = 0; i < persons && !membership; ++i)
-          for (std::uint32_t j = i + 1; j < persons; ++j)
-            for (unsigned ea = 0; ea < 2; ++ea)
-              for (unsigned eb = 0; eb < 2; ++eb)
-                for (unsigned rot = 0; rot < r; ++rot, ++k) {
-                  hd[k] = detail::gr_pair_dot<16>(qc[2 * i + ea][rot], qc[2 * j + eb][half]);
-                  ml[k] = detail::gr_pair_dot<16>(qm[2 * i + ea][rot], qm[2 * j + eb][half]);
-                }
-      }
-      // reshare_pair<16,16> order: hd lanes then ml lanes, own = z + zero_ring.
-      SeedPair sp = seed_pair_for(self, seeds);
-      for (std::uint64_t i = 0; i < n; ++i) {
-        if (dot_hd) dot_hd[pi * n + i] = hd[i].value();
-        if (rs_hd) rs_hd[pi * n + i] = (hd[i] + sp.zero_ring<16>()).value();
-      }
-      for (std::uint64_t i = 0; i < n; ++i) {
-        if (dot_ml) dot_ml[pi * n + i] = ml[i].value();
-        if (rs_ml) rs_ml[pi * n + i] = (ml[i] + sp.zero_ring<16>()).value();
-      }
-      if (!rs_hd && !rs_ml) continue;
+    const bool m = membership != 0;
+    switch (v) {
+      case Variant::plain_mask:
+        dots_reshare_t<16, 0>(be, v, l, r, seeds, db, s, q, persons, m, n, dot_hd, dot_ml, public_ml, rs_hd, rs_ml);
+        break;
+      case Variant::mpc_lift:
+        dots_reshare_t<16, 16>(be, v, l, r, seeds, db, s, q, persons, m, n, dot_hd, dot_ml, public_ml, rs_hd, rs_ml);
+        break;
+      case Variant::const_lift:
+        dots_reshare_t<16, 32>(be, v, l, r, seeds, db, s, q, persons, m, n, dot_hd, dot_ml, public_ml, rs_hd, rs_ml);
+        break;
+      case Variant::no_lift:
+        dots_reshare_t<32, 32>(be, v, l, r, seeds, db, s, q, persons, m, n, dot_hd, dot_ml, public_ml, rs_hd, rs_ml);
+        break;
+      default:
+        return 2;
     }
     return 0;
   } catch (...) {
@@ -318,9 +388,9 @@ struct RefBench {
 // Deals a synthetic workload: DB rows random_record(l, Rng(2), 0.9),
 // then 2*persons query codes from the same stream; person 0's left eye is a planted
 // copy of row s/2.  Dealing seed 7: DB sub_rng(7,1), queries sub_rng(7,2).
-void* ref_bench_prepare(int backend, std::uint32_t l, std::uint64_t s, std::uint32_t persons) {
+void* ref_bench_prepare(int backend, int variant, std::uint32_t l, std::uint64_t s, std::uint32_t persons) {
   auto* b = new RefBench;
-  b->cfg = make_cfg(backend, l, 0.375, 31, 0, 1);
+  b->cfg = make_cfg(backend, variant, l, 0.375, 31, 0, 1);
   b->s = s;
   b->persons = persons;
   Rng rng(2);

@@ -25,7 +25,7 @@ int main() {
     qc[3 * wl + w] = dc[123 * wl + w];
     qm[3 * wl + w] = dm[123 * wl + w];
   }
-  const std::size_t rec = orc_code_record_bytes(be, l) + orc_mask_record_bytes(be, l);
+  const std::size_t rec = orc_code_record_bytes(be, ORC_MPC_LIFT, l) + orc_mask_record_bytes(be, ORC_MPC_LIFT, l);
   std::array<std::vector<std::uint8_t>, 3> db, q;
   for (int p = 0; p < 3; ++p) {
     db[p].resize(s * rec);
@@ -38,7 +38,7 @@ int main() {
   orc_rng_free(dr);
   orc_rng_free(qr);
 
-  orc_config oc{be, l, orc_match_a(0.375), 1u << 16, 31, 0};
+  orc_config oc{be, ORC_MPC_LIFT, l, orc_match_a(0.375), 1u << 16, 31, 0, 0.375};
   std::vector<std::uint8_t> want(persons);
   orc_out out{};
   out.person_match = want.data();

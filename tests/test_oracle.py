@@ -17,7 +17,9 @@ GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_vec
 
 
 def _sha(a):
-    return hashlib.sha256(np.ascontiguousarray(a).astype("<u2").tobytes()).hexdigest()
+    """gen_golden.sha: little-endian bytes at the array's ring width."""
+    dt = {np.dtype(np.uint16): "<u2", np.dtype(np.uint32): "<u4", np.dtype(np.int64): "<i8"}[a.dtype]
+    return hashlib.sha256(np.ascontiguousarray(a).astype(dt).tobytes()).hexdigest()
 
 
 def test_prf_kats():
@@ -41,6 +43,9 @@ def test_galois_lambda():
     assert [int(x) for x in lam] == GOLD["lambda16"]
     # closed forms (test_galois.cpp:113-115): 1+2X, -(1+2X), 1
     assert [int(x) for x in lam] == [1, 2, 0xFFFF, 0xFFFE, 1, 0]
+    # the 32-bit lambdas used by const-lift / no-lift: same closed forms mod 2^32
+    assert [int(x) for x in O.lambda_k(32)] == [1, 2, 0xFFFFFFFF, 0xFFFFFFFE, 1, 0]
+    assert [int(x) for x in O.lambda_k(32)] == GOLD["lambda32_restated"]
 
 
 def test_random_records():
@@ -52,11 +57,12 @@ def test_random_records():
         assert [str(int(w)) for w in m] == g["mask"][i]
 
 
-@pytest.mark.parametrize("idx", range(4))
+@pytest.mark.parametrize("idx", range(len(GOLD["deal"])))
 def test_dealer(idx):
     d = GOLD["deal"][idx]
     dc, dm = O.records(O.Rng(d["records_rng"]), d["l"], d["nrec"], 0.9)
-    pay = O.deal(d["backend"], d["l"], dc, dm, O.Rng(sub=(d["deal_seed"], d["tag"])))
+    var = d.get("variant", O.MPC_LIFT)
+    pay = O.deal(d["backend"], d["l"], dc, dm, O.Rng(sub=(d["deal_seed"], d["tag"])), variant=var)
     assert [hashlib.sha256(p.tobytes()).hexdigest() for p in pay] == d["sha256"]
 
 
@@ -75,7 +81,8 @@ def _case_inputs(c):
 def test_protocol_golden(idx):
     c = GOLD["cases"][idx]
     dc, dm, qc, qm = _case_inputs(c)
-    cfg = O.make_config(c["backend"], c["l"], c["ratio"], c["rotations"], debug_rows=True)
+    var = c.get("variant", O.MPC_LIFT)
+    cfg = O.make_config(c["backend"], c["l"], c["ratio"], c["rotations"], debug_rows=True, variant=var)
     res = O.run_local(cfg, c["seed"], dc, dm, qc, qm, c["persons"], c["membership"], want_all=True)
     n = c["lanes"]
     assert res.row_bits.size == n
@@ -83,8 +90,19 @@ def test_protocol_golden(idx):
     assert np.packbits(res.row_bits, bitorder="little").tobytes().hex() == c["row_bits_hex"]
     assert res.stats == c["stats"]
     assert _sha(res.dot_hd) == c["sha256"]["dot_hd"]        # L1
-    assert _sha(res.dot_ml) == c["sha256"]["dot_ml"]
     assert _sha(res.rs_hd) == c["sha256"]["rs_hd"]          # L2
+    kc = O.cmp_bits(var)
+    dsum = res.diff.astype(np.uint64).sum(0) & ((1 << kc) - 1)
+    assert (((dsum >> (kc - 1)) & 1).astype(np.uint8) == res.row_bits).all()
+    assert ((res.msb[0] ^ res.msb[1] ^ res.msb[2]) == res.row_bits).all()
+    if var != O.MPC_LIFT:
+        if O.mask_bits(var):
+            assert _sha(res.dot_ml) == c["sha256"]["dot_ml"]
+            assert _sha(res.rs_ml) == c["sha256"]["rs_ml"]
+        else:
+            assert _sha(res.public_ml) == c["sha256"]["public_ml"]
+        return
+    assert _sha(res.dot_ml) == c["sha256"]["dot_ml"]
     assert _sha(res.rs_ml) == c["sha256"]["rs_ml"]
     # L3: reconstructed distances are the plaintext masked dot and mask length
     rec_hd = (res.rs_hd.astype(np.uint32).sum(0) & 0xFFFF)
@@ -120,6 +138,32 @@ def test_reconstructed_distances_match_plaintext():
         assert int(res.rs_hd[:, row].astype(np.uint32).sum() & 0xFFFF) == dot & 0xFFFF
         assert int(res.rs_ml[:, row].astype(np.uint32).sum() & 0xFFFF) == ml
         assert bool(res.row_bits[row]) == (b * dot > a * ml)   # oracle.hpp:49-57
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference here)")
+@pytest.mark.parametrize("var", [O.PLAIN_MASK, O.CONST_LIFT, O.NO_LIFT])
+@pytest.mark.parametrize("be", [0, 1])
+def test_variant_restatement_vs_live_reference(var, be):
+    rng = O.Rng(3000 + var)
+    l, s, persons, r = 128, 6, 3, 3
+    dc, dm = O.records(rng, l, s, 0.85)
+    qc, qm = O.records(rng, l, 2 * persons, 0.85)
+    qc[2] = dc[4]
+    qm[2] = dm[4]
+    cfg = O.make_config(be, l, 0.375, r, debug_rows=True, variant=var)
+    a = O.run_local(cfg, 9, dc, dm, qc, qm, persons, want_all=True)
+    b = O.ref_run_local(be, l, 0.375, r, 9, dc, dm, qc, qm, persons, debug_rows=True, variant=var)
+    assert (a.person_match == b["person_match"]).all()
+    assert (a.row_bits == b["row_bits"]).all()
+    assert a.stats == b["stats"]
+    db = O.deal(be, l, dc, dm, O.Rng(sub=(9, 1)), variant=var)
+    q = O.deal(be, l, qc, qm, O.Rng(sub=(9, 2)), variant=var)
+    dh, dmm, rh, rm = O.ref_dots_reshare(be, l, r, O.party_seeds(9), db, s, q, persons, variant=var)
+    assert (dh == a.dot_hd).all() and (rh == a.rs_hd).all()
+    if O.mask_bits(var):
+        assert (dmm == a.dot_ml).all() and (rm == a.rs_ml).all()
+    else:
+        assert (O.ref_dots_reshare.public_ml == a.public_ml).all()
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference here)")

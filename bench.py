@@ -33,7 +33,19 @@ PERSONS = 16            # 32 eye codes
 ROWS_PER_GPU = 100_000  # configs[1]
 METRIC = "iris comparisons/sec (query x rotation x DB)"
 UNIT = "comparisons/s"
-OPS_PER_LANE = {1: 460_800, 0: 921_600}  # int8 tensor ops per comparison lane
+VARIANTS = {"plain-mask": 0, "mpc-lift": 1, "const-lift": 2, "no-lift": 3}
+LIMB_PRODUCTS = {0: 0, 16: 3, 32: 10}  # u8-limb MMAs per k-step of a Z_2^K dot (gemm.cu)
+WIDTHS = {0: (16, 0), 1: (16, 16), 2: (16, 32), 3: (32, 32)}
+
+
+def ops_per_lane(backend: int, variant: int = 1) -> int:
+    """int8 tensor ops per comparison lane, all 3 parties (460,800
+    for mpc-lift Shamir, 921,600 replicated); the public-mask popcount is one
+    party-independent 1-limb GEMM with K = l."""
+    kh, km = WIDTHS[variant]
+    k = L if backend == 1 else 2 * L
+    macs = 3 * LIMB_PRODUCTS[kh] * k + (3 * LIMB_PRODUCTS[km] * k if km else L)
+    return 2 * macs
 ALG_BYTES_PER_LANE = 12.75               # compare/reduce phase (SURVEY §8d)
 
 
@@ -110,7 +122,7 @@ def ncu_traffic():
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int):
+def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int, variant: int = 1):
     """The reference (oracle/_ref, compiled from the reference sources) on the
     host cores: run_parties + party_batch_query per step; QueryStats.wall_ms."""
     from oracle import pyoracle as O
@@ -118,7 +130,7 @@ def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int):
     cores = os.cpu_count() or 1
     if O.ref_available():
         R = O.ref()
-        h = R.ref_bench_prepare(backend, O.MPC_LIFT, L, rows, persons)
+        h = R.ref_bench_prepare(backend, variant, L, rows, persons)
         times = []
         m0 = C.c_uint8(0)
         for _ in range(steps):
@@ -135,7 +147,7 @@ def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int):
     rng = O.Rng(2)
     dc, dm = O.records(rng, L, rows, 0.9)
     qc, qm = O.records(rng, L, 2 * persons, 0.9)
-    cfg = O.make_config(backend, L)
+    cfg = O.make_config(backend, L, variant=variant)
     t0 = time.perf_counter()
     O.run_local(cfg, 7, dc, dm, qc, qm, persons)
     dt = time.perf_counter() - t0
@@ -151,13 +163,15 @@ def run_reference_arm(args):
     rows = args.ref_rows
     for _ in range(args.warmup and 1):
         pass
-    res = cpu_reference_rate(backend, rows, 1, max(1, args.steps))
+    variant = VARIANTS[args.variant]
+    res = cpu_reference_rate(backend, rows, 1, max(1, args.steps), variant)
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 2 * ROT * rows / res["value"] * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"cfg2-shape sample: 1 person (2 codes) x {ROT} rot x {rows} rows, "
-                                   f"l={L}, mpc-lift, {args.backend}", "l": L, "rotations": ROT},
+                                   f"l={L}, {args.variant}, {args.backend}", "l": L, "rotations": ROT,
+                       "variant": args.variant},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -181,7 +195,8 @@ def main_gpu(args):
     row_off, rows = shard_rows(S, world, rank)
     persons = args.persons
     ncodes = 2 * persons
-    cfg = P.EngineConfig(backend=backend, l=L, rotations=ROT)
+    variant = VARIANTS[args.variant]
+    cfg = P.EngineConfig(backend=backend, l=L, rotations=ROT, variant=variant)
     sess = P.Session(cfg, master_seed=7, device=local, shard_rank=rank, db_rows_total=S if world > 1 else 0,
                      db_row_offset=row_off)
     t0 = time.time()
@@ -281,7 +296,10 @@ def main_gpu(args):
         peaks, src = load_peaks()
         gemm_ms = stats_acc["gemm_ms"] / max(1, stats_acc["gemm_launches"])
         local_lanes = ncodes * ROT * rows
-        ops_launch = local_lanes * OPS_PER_LANE[backend] / max(1, stats_acc["gemm_launches"] // args.steps)
+        opl = ops_per_lane(backend, variant)
+        kh, km = WIDTHS[variant]
+        plane_kb = L * (3 * kh // 8 + (3 * km // 8 if km else 1)) / 1e3
+        ops_launch = local_lanes * opl / max(1, stats_acc["gemm_launches"] // args.steps)
         achieved = ops_launch / (gemm_ms / 1e3) / 1e12
         i8 = os.path.join(ROOT, "profiles", "int8_peak.json")
         if os.path.exists(i8):
@@ -290,16 +308,17 @@ def main_gpu(args):
         else:
             peak = 2.0 * peaks["bf16_tflops"]
             peak_note = f"2 x {src} bf16 ({peaks['bf16_tflops']} TF/s); dense int8 = 2x bf16 on sm_100"
-        cpu = cpu_reference_rate(backend, args.ref_rows, 1, 1) if (world == 1 and not args.no_cpu) else None
+        cpu = cpu_reference_rate(backend, args.ref_rows, 1, 1, variant) if (world == 1 and not args.no_cpu) else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"configs[1]: {ncodes} query codes ({persons} persons) x {ROT} rotations vs "
-                                   f"{rows} DB rows per GPU (total {S}), l={L}, 3-party mpc-lift, "
+                                   f"{rows} DB rows per GPU (total {S}), l={L}, 3-party {args.variant}, "
                                    f"{args.backend} backend", "l": L, "rotations": ROT, "persons": persons,
                        "db_rows_total": S, "db_rows_per_gpu": rows, "backend": args.backend,
-                       "l2": "inputs larger than L2 (DB shares 153.6 KB/row resident in HBM)",
+                       "variant": args.variant,
+                       "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM)",
                        "parallelism": f"db-shard x{world}"},
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons},
@@ -307,7 +326,7 @@ def main_gpu(args):
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic()[0],
                          "ncu_tensor_pipe_active_pct": ncu_traffic()[1],
-                         "note": f"int8 ops = {OPS_PER_LANE[backend]}/lane; peak = {peak_note}"},
+                         "note": f"int8 ops = {opl}/lane; peak = {peak_note}"},
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),
             "phase_ms": {"gemm": gemm_ms, "threshold": sess.last_stats.threshold_ms, "or": sess.last_stats.or_ms,
@@ -330,6 +349,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--backend", default="shamir", choices=["shamir", "replicated"])
+    ap.add_argument("--variant", default="mpc-lift", choices=list(VARIANTS))
     ap.add_argument("--rows", type=int, default=ROWS_PER_GPU)
     ap.add_argument("--persons", type=int, default=PERSONS)
     ap.add_argument("--ref-rows", type=int, default=3000, dest="ref_rows")

@@ -54,6 +54,17 @@ inline void check(int rc, const char* what, const irismpc_gpu_ctx* ctx = nullptr
 }
 
 enum class Backend : std::uint8_t { replicated = 0, shamir = 1 };
+enum class Variant : std::uint8_t { plain_mask = 0, mpc_lift = 1, const_lift = 2, no_lift = 3 };  // shares.hpp:28
+
+inline const char* to_string(Variant v) {  // shares.cpp:22-33
+  switch (v) {
+    case Variant::plain_mask: return "plain-mask";
+    case Variant::mpc_lift: return "mpc-lift";
+    case Variant::const_lift: return "const-lift";
+    case Variant::no_lift: return "no-lift";
+  }
+  return "?";
+}
 
 struct MatchParams {  // iris.hpp:157-174
   double match_ratio = 0.375;
@@ -73,8 +84,9 @@ struct MatchParams {  // iris.hpp:157-174
   }
 };
 
-struct EngineConfig {  // engine.hpp:33-44, variant fixed to mpc-lift
+struct EngineConfig {  // engine.hpp:33-44
   Backend backend = Backend::shamir;
+  Variant variant = Variant::mpc_lift;
   std::uint32_t l = 12800;
   MatchParams params{};
   unsigned rotations = 31;
@@ -112,7 +124,8 @@ class Session {
       : cfg_(cfg) {
     irismpc_gpu_config c{};
     c.backend = static_cast<std::uint32_t>(cfg.backend);
-    c.variant = IRISMPC_GPU_VARIANT_MPC_LIFT;
+    c.variant = static_cast<std::uint32_t>(cfg.variant);
+    c.match_ratio = cfg.params.match_ratio;
     c.l = cfg.l;
     c.a = cfg.params.a;
     c.b = cfg.params.b;
@@ -165,6 +178,7 @@ class Session {
       auto& r = out[i];
       r.lane_count = n;
       r.stats.backend = cfg_.backend == Backend::shamir ? "shamir-galois" : "replicated";
+      r.stats.variant = to_string(cfg_.variant);
       r.stats.s = st.s;
       r.stats.l = st.l;
       r.stats.batch = st.batch;

@@ -48,14 +48,18 @@ extern "C" {
 
 #define IRISMPC_GPU_BACKEND_REPLICATED 0
 #define IRISMPC_GPU_BACKEND_SHAMIR 1
-#define IRISMPC_GPU_VARIANT_MPC_LIFT 1 /* Variant::mpc_lift (shares.hpp:29) */
+/* Variant (shares.hpp:28): ring widths (hd dot, ml dot, comparison) */
+#define IRISMPC_GPU_VARIANT_PLAIN_MASK 0 /* 16, public mask bits, 16 */
+#define IRISMPC_GPU_VARIANT_MPC_LIFT 1   /* 16, 16 lifted in MPC, 32 (the north-star path) */
+#define IRISMPC_GPU_VARIANT_CONST_LIFT 2 /* 16, 32, 32 */
+#define IRISMPC_GPU_VARIANT_NO_LIFT 3    /* 32, 32, 32 */
 
 typedef struct irismpc_gpu_ctx irismpc_gpu_ctx;
 
 /* EngineConfig (engine.hpp:33-44) + party seeds + shard placement. */
 typedef struct irismpc_gpu_config {
   uint32_t backend;       /* IRISMPC_GPU_BACKEND_* */
-  uint32_t variant;       /* IRISMPC_GPU_VARIANT_MPC_LIFT */
+  uint32_t variant;       /* IRISMPC_GPU_VARIANT_* */
   uint32_t l;             /* code length (bits), multiple of 8 */
   uint32_t a, b, m;       /* MatchParams integers (iris.hpp:157-174); b = 2^m, m = 16 */
   uint32_t rotations;     /* odd */
@@ -65,7 +69,9 @@ typedef struct irismpc_gpu_config {
   uint32_t shard_rank;    /* this context's shard (0 = holds the inner-batch pairs) */
   uint64_t db_rows_total; /* s of the whole DB across shards (0: = local s) */
   uint64_t db_row_offset; /* first global DB row held by this context */
-  uint64_t reserved[4];
+  double match_ratio;     /* MatchParams::match_ratio; the plain-mask threshold
+                             ceil((1 - 2 r) ml) uses it (iris.hpp:182-184) */
+  uint64_t reserved[3];
 } irismpc_gpu_config;
 
 /* QueryStats (engine.hpp:46-56) for each party, plus device phase timings. */
@@ -147,12 +153,12 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* ctx, uint64_t s, uint64_t rng_seed, ui
                          double mask_density, uint64_t deal_seed);
 
 /* ---- debug / parity taps (tests) ------------------------------------------ */
-#define IRISMPC_GPU_TAP_DOT_HD 1  /* uint16 [3][n] per-party additive hd dot (L1) */
-#define IRISMPC_GPU_TAP_DOT_ML 2
-#define IRISMPC_GPU_TAP_RS_HD 3   /* uint16 [3][n] components after reshare (L2) */
-#define IRISMPC_GPU_TAP_RS_ML 4
-#define IRISMPC_GPU_TAP_ML32 5    /* uint32 [3][n] lift output components */
-#define IRISMPC_GPU_TAP_DIFF 6    /* uint32 [3][n] a*ml32 - b*hd components */
+#define IRISMPC_GPU_TAP_DOT_HD 1  /* [3][n] per-party additive hd dot (L1), u16 (KH = 16) / u32 */
+#define IRISMPC_GPU_TAP_DOT_ML 2  /* [3][n] ml dot u16 / u32; plain-mask: [n] u16 public popcount */
+#define IRISMPC_GPU_TAP_RS_HD 3   /* uint32 [3][n] components after reshare (L2) */
+#define IRISMPC_GPU_TAP_RS_ML 4   /* uint32 [3][n] (0 for plain-mask) */
+#define IRISMPC_GPU_TAP_ML32 5    /* uint32 [3][n] 32-bit ml components (lift output) */
+#define IRISMPC_GPU_TAP_DIFF 6    /* uint32 [3][n] comparison input components */
 #define IRISMPC_GPU_TAP_MSB 7     /* uint8  [3][n] match bit components */
 /* Enable capture of all taps for the next query (costly; tests only). */
 int irismpc_gpu_enable_taps(irismpc_gpu_ctx* ctx, int enable);

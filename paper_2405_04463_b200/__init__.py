@@ -26,7 +26,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libirismpc_gpu.so")
 
 REPLICATED, SHAMIR = 0, 1
-MPC_LIFT = 1
+PLAIN_MASK, MPC_LIFT, CONST_LIFT, NO_LIFT = 0, 1, 2, 3  # Variant (shares.hpp:28)
+VARIANTS = {"plain-mask": PLAIN_MASK, "mpc-lift": MPC_LIFT, "const-lift": CONST_LIFT, "no-lift": NO_LIFT}
+# (hamming dot bits, mask dot bits (0 = public mask bits), comparison bits), shares.hpp:37-48
+VARIANT_WIDTHS = {PLAIN_MASK: (16, 0, 16), MPC_LIFT: (16, 16, 32), CONST_LIFT: (16, 32, 32), NO_LIFT: (32, 32, 32)}
 
 TAP_DOT_HD, TAP_DOT_ML, TAP_RS_HD, TAP_RS_ML, TAP_ML32, TAP_DIFF, TAP_MSB = range(1, 8)
 
@@ -72,7 +75,8 @@ class _Config(C.Structure):
     _fields_ = [("backend", C.c_uint32), ("variant", C.c_uint32), ("l", C.c_uint32), ("a", C.c_uint32),
                 ("b", C.c_uint32), ("m", C.c_uint32), ("rotations", C.c_uint32), ("debug_rows", C.c_uint32),
                 ("seeds", C.c_uint8 * 48), ("device", C.c_int32), ("shard_rank", C.c_uint32),
-                ("db_rows_total", C.c_uint64), ("db_row_offset", C.c_uint64), ("reserved", C.c_uint64 * 4)]
+                ("db_rows_total", C.c_uint64), ("db_row_offset", C.c_uint64), ("match_ratio", C.c_double),
+                ("reserved", C.c_uint64 * 3)]
 
 
 class Stats(C.Structure):
@@ -142,8 +146,9 @@ def seeds_from_master(seed: int) -> np.ndarray:
     return out
 
 
-def record_bytes(backend: int, l: int) -> int:
-    return int(lib().irismpc_gpu_record_bytes(backend, MPC_LIFT, l))
+def record_bytes(backend: int, l: int, variant: int = MPC_LIFT) -> int:
+    """code_record_bytes + mask_record_bytes (shares.cpp:49-59)."""
+    return int(lib().irismpc_gpu_record_bytes(backend, variant, l))
 
 
 def lane_count(persons: int, s: int, rotations: int, membership: bool = False) -> int:
@@ -160,7 +165,7 @@ def match_a(ratio: float) -> int:
 
 @dataclass
 class EngineConfig:
-    """irismpc::EngineConfig (engine.hpp:33-44), mpc-lift variant."""
+    """irismpc::EngineConfig (engine.hpp:33-44); variant defaults to mpc-lift."""
     backend: int = SHAMIR
     l: int = 12800
     match_ratio: float = 0.375
@@ -199,6 +204,7 @@ class Session:
         c = _Config()
         c.backend, c.variant, c.l, c.a, c.b, c.m = cfg.backend, cfg.variant, cfg.l, a, b, cfg.m
         c.rotations, c.debug_rows = cfg.rotations, 1 if cfg.debug_rows else 0
+        c.match_ratio = cfg.match_ratio
         if seeds is None:
             seeds = seeds_from_master(master_seed if master_seed is not None else 0)
         for i in range(48):
@@ -210,7 +216,7 @@ class Session:
             raise _ERRORS.get(rc, IrisError)(f"irismpc_gpu_create failed ({rc})")
         self._h = h
         self.s = 0
-        self.rec = record_bytes(cfg.backend, cfg.l)
+        self.rec = record_bytes(cfg.backend, cfg.l, cfg.variant)
         self.last_stats = Stats()
 
     def close(self):
@@ -324,11 +330,23 @@ class Session:
         self._check(lib().irismpc_gpu_enable_taps(self._h, 1 if on else 0))
 
     def read_tap(self, tap: int, n: int) -> np.ndarray:
-        dt = {TAP_DOT_HD: np.uint16, TAP_DOT_ML: np.uint16, TAP_RS_HD: np.uint16, TAP_RS_ML: np.uint16,
-              TAP_ML32: np.uint32, TAP_DIFF: np.uint32, TAP_MSB: np.uint8}[tap]
-        out = np.zeros(3 * n, dt)
+        """Tap arrays [3][n] (plain-mask TAP_DOT_ML: [n] public popcounts), in the
+        ring's width: u16 for 16-bit dots and reshared 16-bit shares, else u32."""
+        kh, km, kc = VARIANT_WIDTHS[self.cfg.variant]
+        rows = 1 if (tap == TAP_DOT_ML and km == 0) else 3
+        dt = {TAP_DOT_HD: np.uint16 if kh == 16 else np.uint32,
+              TAP_DOT_ML: np.uint32 if km == 32 else np.uint16,
+              TAP_MSB: np.uint8}.get(tap, np.uint32)
+        out = np.zeros(rows * n, dt)
         self._check(lib().irismpc_gpu_read_tap(self._h, tap, out.ctypes.data, out.nbytes))
-        return out.reshape(3, n)
+        out = out.reshape(rows, n)
+        if rows == 1:
+            return out[0]
+        if (tap == TAP_RS_HD and kh == 16) or (tap == TAP_RS_ML and km == 16):
+            return out.astype(np.uint16)
+        if tap == TAP_DIFF and kc == 16:
+            return out.astype(np.uint16)
+        return out
 
 
 def _dealt_on_device(sess: Session, codes: np.ndarray, masks: np.ndarray, seed: int, tag: int):

@@ -69,20 +69,21 @@ SeedKey key_of(const uint8_t* seed) {
   return k;
 }
 
-// party_lagrange_at_zero<16> over {1, X, 1+X} (galois.hpp:66-128)
+// party_lagrange_at_zero<32> over {1, X, 1+X} (galois.hpp:66-128); the 16-bit
+// lambdas are its low halves (the same closed forms 1+2X, -(1+2X), 1)
 struct Gr {
   uint32_t c0, c1;
 };
 Gr gmul(Gr a, Gr b) {
-  return {(a.c0 * b.c0 + a.c1 * b.c1) & 0xFFFF, (a.c0 * b.c1 + a.c1 * b.c0 + a.c1 * b.c1) & 0xFFFF};
+  return {a.c0 * b.c0 + a.c1 * b.c1, a.c0 * b.c1 + a.c1 * b.c0 + a.c1 * b.c1};
 }
-Gr gsub(Gr a, Gr b) { return {(a.c0 - b.c0) & 0xFFFF, (a.c1 - b.c1) & 0xFFFF}; }
+Gr gsub(Gr a, Gr b) { return {a.c0 - b.c0, a.c1 - b.c1}; }
 Gr ginv(Gr a) {
   Gr y = (a.c1 & 1) == 0 ? Gr{1, 0} : ((a.c0 & 1) == 0 ? Gr{1, 1} : Gr{0, 1});
-  for (unsigned c = 1; c < 16; c *= 2) y = gmul(y, gsub(Gr{2, 0}, gmul(a, y)));
+  for (unsigned c = 1; c < 32; c *= 2) y = gmul(y, gsub(Gr{2, 0}, gmul(a, y)));
   return y;
 }
-void lambdas(uint16_t out[6]) {
+void lambdas(uint32_t out[6]) {
   const Gr xs[3] = {{1, 0}, {0, 1}, {1, 1}};
   for (int i = 0; i < 3; ++i) {
     Gr num{1, 0}, den{1, 0};
@@ -92,14 +93,19 @@ void lambdas(uint16_t out[6]) {
       den = gmul(den, gsub(xs[j], xs[i]));
     }
     const Gr l = gmul(num, ginv(den));
-    out[2 * i] = (uint16_t)l.c0;
-    out[2 * i + 1] = (uint16_t)l.c1;
+    out[2 * i] = l.c0;
+    out[2 * i + 1] = l.c1;
   }
 }
 
-size_t record_bytes(uint32_t backend, uint32_t l) {
-  // code_record_bytes + mask_record_bytes for mpc-lift (shares.cpp:49-59)
-  return backend == IRISMPC_GPU_BACKEND_REPLICATED ? (size_t)l * 8 : (size_t)l * 4;
+// code_record_bytes / mask_record_bytes (shares.cpp:49-59)
+uint64_t field_bytes(uint32_t backend, int bits, uint32_t l) {
+  if (bits == 0) return l / 8;
+  return backend == IRISMPC_GPU_BACKEND_REPLICATED ? (uint64_t)l * 2 * (bits / 8) : (uint64_t)l * (bits / 8);
+}
+size_t record_bytes(uint32_t backend, uint32_t variant, uint32_t l) {
+  const VariantWidths w = variant_widths((int)variant);
+  return field_bytes(backend, w.kh, l) + field_bytes(backend, w.km, l);
 }
 
 // Reference or_tree_batch zero_word draws for `groups` equal groups of `len`
@@ -121,37 +127,57 @@ uint64_t ref_or_draws(uint64_t groups, uint64_t len, uint64_t* rounds, uint64_t*
 
 }  // namespace
 
+// Device planes of one record field (code -> hd, mask -> ml): DB limb planes
+// (A), rotated query planes (B), the unrotated query planes of the pair GEMM
+// (A) and its output.
+struct FieldPlanes {
+  FieldFmt fmt{};
+  uint32_t nparty = 3;  // 3 share planes, or 1 public bit plane
+  uint32_t nseg = 1;    // 2 for replicated shares ([x_p | x_{p-1}])
+  int out_bytes = 2;    // GEMM output element: u16, or u32 for 4 limbs
+  Buf db, q, qa, pair_c;
+  CUtensorMap tA, tB, tQA;
+  uint32_t ncols_pad_cur = 0;
+  uint64_t qa_spad = 0;
+  uint32_t bn() const { return gemm_bn((uint32_t)fmt.limbs); }
+  void release() {
+    db.release();
+    q.release();
+    qa.release();
+    pair_c.release();
+    ncols_pad_cur = 0;
+    qa_spad = 0;
+  }
+};
+
 struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
   cudaStream_t st = nullptr, st2 = nullptr;
   int shamir = 0;
-  uint32_t l = 0, l_pad = 0, nseg = 1;
+  int variant = kMpcLift;
+  VariantWidths vw{16, 16, 32};
+  uint32_t l = 0, l_pad = 0;
+  uint64_t rec = 0;
   SeedKey keys[3];
   // DB shard
   uint64_t s = 0, s_pad = 0;
   bool db_loaded = false;
-  Buf db_lo, db_hi;
-  CUtensorMap tA_lo, tA_hi;
+  FieldPlanes fld[2];  // 0 code, 1 mask
   // query scratch
-  Buf q_lo, q_hi, q_pa, q_pb, q_pay[3];
-  uint64_t q_rows_mapped = 0;
-  CUtensorMap tB_lo, tB_hi;
-  uint32_t ncols_pad_cur = 0;
+  Buf q_pay[3];
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
-  Buf ml_rs, diff, gate, bits, qa_lo, qa_hi, pair_c;
-  CUtensorMap tQA_lo, tQA_hi;
-  uint64_t qa_spad = 0;
+  Buf ml_rs, diff, gate, bits;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
   // PRF stream state
   uint64_t pos[3] = {0, 0, 0};
   uint64_t query_id = 0;
-  uint64_t dots_budget = 0;
   // taps
   bool taps = false;
   Buf tap_buf[7];
+  size_t tap_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
   std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
@@ -173,9 +199,9 @@ int fail(irismpc_gpu_ctx* c, int code, const std::string& msg) {
   } while (0)
 
 int validate(const irismpc_gpu_config* c, std::string* why) {
-  // EngineConfig::validate (engine.cpp:21-34) for the shared-mask variant
-  if (c->variant != IRISMPC_GPU_VARIANT_MPC_LIFT) {
-    *why = "only the mpc-lift variant is implemented on the GPU path";
+  // EngineConfig::validate (engine.cpp:21-34)
+  if (c->variant > IRISMPC_GPU_VARIANT_NO_LIFT) {
+    *why = "unknown variant";
     return IRISMPC_GPU_ERR_CONFIG;
   }
   if (c->backend > 1) {
@@ -190,14 +216,23 @@ int validate(const irismpc_gpu_config* c, std::string* why) {
     *why = "threshold numerator exceeds denominator";
     return IRISMPC_GPU_ERR_BOUNDS;
   }
-  if (c->m != 16 || c->b != (1u << 16)) {
-    *why = "shared-mask variants fix b = 2^16";
-    return IRISMPC_GPU_ERR_BOUNDS;
-  }
-  const uint64_t t = 1ull << 32, bl = (uint64_t)c->b * c->l;
-  if (!(bl < t / 4 && bl < t - (t >> 1))) {
-    *why = "comparison ring too small for b*l (shared masks)";
-    return IRISMPC_GPU_ERR_BOUNDS;
+  if (c->variant == IRISMPC_GPU_VARIANT_PLAIN_MASK) {
+    // check_public_mask_bound(l, 16) (iris.hpp:189-194, 207-211)
+    const uint64_t t = 1ull << 16;
+    if (!(c->l < t / 4 && c->l < t - (t >> 1))) {
+      *why = "comparison ring too small for vector length (public masks)";
+      return IRISMPC_GPU_ERR_BOUNDS;
+    }
+  } else {
+    if (c->m != 16 || c->b != (1u << 16)) {
+      *why = "shared-mask variants fix b = 2^16";
+      return IRISMPC_GPU_ERR_BOUNDS;
+    }
+    const uint64_t t = 1ull << 32, bl = (uint64_t)c->b * c->l;
+    if (!(bl < t / 4 && bl < t - (t >> 1))) {
+      *why = "comparison ring too small for b*l (shared masks)";
+      return IRISMPC_GPU_ERR_BOUNDS;
+    }
   }
   if (c->rotations % 2 == 0) {
     *why = "rotations must be odd";
@@ -219,30 +254,29 @@ uint64_t s_total(const irismpc_gpu_ctx* c) {
 }
 
 int alloc_planes(irismpc_gpu_ctx* c, uint64_t s) {
-  c->db_lo.release();
-  c->db_hi.release();
+  for (auto& f : c->fld) f.db.release();
   c->db_loaded = false;
   c->s = s;
   c->s_pad = round_up(s ? s : 1, 2 * kGemmBM);  // CTA-pair tiles cover 256 rows
-  const size_t bytes = 6ull * c->s_pad * c->l_pad;
-  if (c->db_lo.ensure(bytes) || c->db_hi.ensure(bytes))
-    return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for the DB planes");
-  CK(c, cudaMemsetAsync(c->db_lo.p, 0, bytes, c->st));
-  CK(c, cudaMemsetAsync(c->db_hi.p, 0, bytes, c->st));
-  if (make_plane_tmap(&c->tA_lo, c->db_lo.p, 6ull * c->s_pad, c->l_pad, kGemmBM) ||
-      make_plane_tmap(&c->tA_hi, c->db_hi.p, 6ull * c->s_pad, c->l_pad, kGemmBM))
-    return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the DB planes");
+  for (auto& f : c->fld) {
+    const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
+    const size_t bytes = rows * c->l_pad;
+    if (f.db.ensure(bytes)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for the DB planes");
+    CK(c, cudaMemsetAsync(f.db.p, 0, bytes, c->st));
+    if (make_plane_tmap(&f.tA, f.db.p, rows, c->l_pad, kGemmBM))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the DB planes");
+  }
   return 0;
 }
 
 // parse `rows` rows (device payloads) into planes at row0
 int parse_rows(irismpc_gpu_ctx* c, const uint8_t* const dp[3], uint64_t rows, uint64_t row0, Buf* bad) {
-  if (!c->shamir) {
-    if (bad) launch_check_rep(dp[0], dp[1], dp[2], rows * record_bytes(0, c->l), bad->as<int>(), c->st);
+  for (auto& f : c->fld) {
+    if (!c->shamir && bad) launch_check_rep(dp[0], dp[1], dp[2], rows, f.fmt, c->l, bad->as<int>(), c->st);
+    for (uint32_t p = 0; p < f.nparty; ++p)
+      launch_parse_field(dp[p], rows, row0, c->l, c->l_pad, c->s_pad, (int)p, c->shamir, f.fmt, f.db.as<uint8_t>(),
+                         c->st);
   }
-  for (int p = 0; p < 3; ++p)
-    launch_parse_db(dp[p], rows, row0, c->l, c->l_pad, c->s_pad, p, c->shamir, c->db_lo.as<uint8_t>(),
-                    c->db_hi.as<uint8_t>(), c->st);
   CK(c, cudaGetLastError());
   return 0;
 }
@@ -259,17 +293,17 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
   return 0;
 }
 
-int ensure_query_buffers(irismpc_gpu_ctx* c, uint32_t ncodes, uint32_t ncols_pad) {
-  const size_t bplane = 6ull * c->nseg * ncols_pad * c->l_pad;
-  if (bplane > c->q_lo.cap || ncols_pad != c->ncols_pad_cur) {
-    if (c->q_lo.ensure(bplane) || c->q_hi.ensure(bplane))
-      return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query planes");
-    CK(c, cudaMemsetAsync(c->q_lo.p, 0, bplane, c->st));
-    CK(c, cudaMemsetAsync(c->q_hi.p, 0, bplane, c->st));
-    if (make_plane_tmap(&c->tB_lo, c->q_lo.p, 6ull * c->nseg * ncols_pad, c->l_pad, 128) ||
-        make_plane_tmap(&c->tB_hi, c->q_hi.p, 6ull * c->nseg * ncols_pad, c->l_pad, 128))
-      return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the query planes");
-    c->ncols_pad_cur = ncols_pad;
+int ensure_query_buffers(irismpc_gpu_ctx* c, uint32_t ncols_pad) {
+  for (auto& f : c->fld) {
+    const uint64_t rows = (uint64_t)f.nparty * f.nseg * f.fmt.limbs * ncols_pad;
+    const size_t bytes = rows * c->l_pad;
+    if (bytes > f.q.cap || ncols_pad != f.ncols_pad_cur) {
+      if (f.q.ensure(bytes)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for query planes");
+      CK(c, cudaMemsetAsync(f.q.p, 0, bytes, c->st));
+      if (make_plane_tmap(&f.tB, f.q.p, rows, c->l_pad, f.bn() / 2))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the query planes");
+      f.ncols_pad_cur = ncols_pad;
+    }
   }
   return 0;
 }
@@ -283,18 +317,29 @@ int ensure_host_segs(irismpc_gpu_ctx* c, size_t n) {
   return 0;
 }
 
+GemmArgs field_gemm_args(const irismpc_gpu_ctx* c, const FieldPlanes& f, uint32_t ncols_pad) {
+  GemmArgs g{};
+  g.nb_rows = ncols_pad;
+  g.nkb_seg = c->l_pad / kGemmBK;
+  g.nseg = f.nseg;
+  g.rep = f.nseg == 2 ? 1 : 0;
+  g.nprob = f.nparty;
+  g.limbs = (uint32_t)f.fmt.limbs;
+  return g;
+}
+
 // Core query on device payloads.  mode 0: final (open into match_out host),
 // 1: partial (component bits into partial_dev).
 //
-// DB lanes run in row chunks: K2 GEMM(chunk i) on stream st while the K4
-// threshold pipeline of chunk i-1 runs on stream st2 (tensor pipe vs ALU
-// pipes), dot outputs double-buffered.  The pair lanes, the per-person OR and
-// the open follow on st2 / st.
+// DB lanes run in row chunks: K2 GEMMs (code field, mask field) of chunk i on
+// stream st while the K4 threshold pipeline of chunk i-1 runs on stream st2
+// (tensor pipe vs ALU pipes), dot outputs double-buffered.  The pair lanes,
+// the per-person OR and the open follow on st2 / st.
 int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3], uint32_t persons,
               int membership, int mode, uint8_t* match_out, uint8_t* row_bits_out, uint8_t* partial_dev,
               irismpc_gpu_stats* stats, bool host_input, const uint8_t* const hq[3]) {
   if (!c->db_loaded) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no database loaded");
-  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const size_t rec = c->rec;
   const uint32_t ncodes = membership ? 1u : 2u * persons;
   for (int p = 0; p < 3; ++p) {
     if (qlen[p] % rec != 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "query payload size mismatch");
@@ -303,6 +348,12 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                   membership ? "membership expects exactly one query code"
                              : "batch query expects 2 codes per person");
   }
+  const int V = c->variant;
+  const VariantWidths vw = c->vw;
+  const bool shared_ml = vw.km != 0;
+  FieldPlanes& fh = c->fld[0];
+  FieldPlanes& fm = c->fld[1];
+  const uint64_t hb = (uint64_t)fh.out_bytes, mb = (uint64_t)fm.out_bytes;  // dot element bytes
   const uint32_t r = membership ? 1u : c->cfg.rotations;
   const uint64_t ncols = (uint64_t)ncodes * r;
   const uint32_t ncols_pad = (uint32_t)round_up(ncols ? ncols : 1, kGemmBN);
@@ -312,6 +363,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t npairs = rank0 ? npairs_all : 0;
   const uint64_t n = ncols * S + npairs_all;  // global lane count (all shards)
   const uint64_t W = ceil_div(n, 64);
+  const uint64_t nml = shared_ml ? n : 0;
+  const uint32_t nlift = V == kMpcLift ? 64u : 0u;
+  const uint32_t ngates = nlift + 2u * vw.kc - 3u;
   const uint32_t ngroups = membership ? 1u : persons;
   const uint64_t qid = c->query_id++;
   const uint64_t rank = c->cfg.shard_rank;
@@ -329,65 +383,62 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       dqp[p] = c->q_pay[p].as<uint8_t>();
     }
   }
-  int rc = ensure_query_buffers(c, ncodes, ncols_pad);
+  int rc = ensure_query_buffers(c, ncols_pad);
   if (rc) return rc;
-  launch_parse_query(dqp[0], dqp[1], dqp[2], ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir,
-                     c->q_lo.as<uint8_t>(), c->q_hi.as<uint8_t>(), nullptr, nullptr, st);
-  debug_check("k_parse_query", st);
+  for (auto& f : c->fld) {
+    launch_parse_query_field(dqp[0], dqp[1], dqp[2], ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir, f.fmt,
+                             f.q.as<uint8_t>(), st);
+    ++launches;
+  }
+  debug_check("k_parse_query_field", st);
   CK(c, cudaGetLastError());
-  ++launches;
   if (npairs) {
-    // pair dots as one limb GEMM: A = the unrotated query codes in the DB plane
-    // layout, B = the rotated query planes (see pairs.cu)
+    // pair dots as one limb GEMM per field: A = the unrotated query codes in the
+    // DB plane layout, B = the rotated query planes (see pairs.cu)
     const uint64_t spq = round_up(ncodes, 2 * kGemmBM);
-    const size_t abytes = 6ull * spq * c->l_pad;
-    if (spq != c->qa_spad) {
-      if (c->qa_lo.ensure(abytes) || c->qa_hi.ensure(abytes))
-        return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair planes)");
-      CK(c, cudaMemsetAsync(c->qa_lo.p, 0, abytes, st));
-      CK(c, cudaMemsetAsync(c->qa_hi.p, 0, abytes, st));
-      if (make_plane_tmap(&c->tQA_lo, c->qa_lo.p, 6ull * spq, c->l_pad, kGemmBM) ||
-          make_plane_tmap(&c->tQA_hi, c->qa_hi.p, 6ull * spq, c->l_pad, kGemmBM))
-        return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the pair planes");
-      c->qa_spad = spq;
-    }
-    for (int p = 0; p < 3; ++p)
-      launch_parse_db(dqp[p], ncodes, 0, c->l, c->l_pad, spq, p, c->shamir, c->qa_lo.as<uint8_t>(),
-                      c->qa_hi.as<uint8_t>(), st);
-    if (c->pair_c.ensure(6 * ncols * ncodes * sizeof(uint16_t)) ||
-        c->pair_dots.ensure(6 * npairs * sizeof(uint16_t)))
+    if (c->pair_dots.ensure(npairs * (3 * hb + fm.nparty * mb) + 64))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
-    GemmArgs pg{};
-    pg.s_pad = (uint32_t)spq;
-    pg.nb_rows = ncols_pad;
-    pg.nkb_seg = c->l_pad / kGemmBK;
-    pg.nseg = c->nseg;
-    pg.rep = c->shamir ? 0 : 1;
-    pg.s_valid = ncodes;
-    pg.row0 = 0;
-    pg.col0 = 0;
-    pg.ncols = (uint32_t)ncols;
-    pg.out = c->pair_c.as<uint16_t>();
-    pg.out_pstride = ncols * ncodes;
-    pg.out_cstride = ncodes;
+    uint8_t* pd_out[2] = {c->pair_dots.as<uint8_t>(), c->pair_dots.as<uint8_t>() + 3 * npairs * hb};
     void* ph = prof_begin(st);
-    launch_gemm(c->tQA_lo, c->tQA_hi, c->tB_lo, c->tB_hi, pg, (uint32_t)(spq / kGemmBM),
-                (uint32_t)ceil_div(ncols, kGemmBN), st);
-    launch_pair_gather(c->pair_c.as<uint16_t>(), ncodes, (uint32_t)ncols, persons, r, c->pair_dots.as<uint16_t>(),
-                       c->pair_dots.as<uint16_t>() + npairs, 2 * npairs, st);
+    for (int fi = 0; fi < 2; ++fi) {
+      FieldPlanes& f = c->fld[fi];
+      const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * spq;
+      if (spq != f.qa_spad) {
+        if (f.qa.ensure(rows * c->l_pad)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair planes)");
+        CK(c, cudaMemsetAsync(f.qa.p, 0, rows * c->l_pad, st));
+        if (make_plane_tmap(&f.tQA, f.qa.p, rows, c->l_pad, kGemmBM))
+          return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the pair planes");
+        f.qa_spad = spq;
+      }
+      for (uint32_t p = 0; p < f.nparty; ++p)
+        launch_parse_field(dqp[p], ncodes, 0, c->l, c->l_pad, spq, (int)p, c->shamir, f.fmt, f.qa.as<uint8_t>(), st);
+      if (f.pair_c.ensure(f.nparty * ncols * ncodes * f.out_bytes + 16))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
+      GemmArgs pg = field_gemm_args(c, f, ncols_pad);
+      pg.s_pad = (uint32_t)spq;
+      pg.s_valid = ncodes;
+      pg.ncols = (uint32_t)ncols;
+      pg.out = f.pair_c.p;
+      pg.out_pstride = ncols * ncodes;
+      pg.out_cstride = ncodes;
+      launch_gemm(f.tQA, f.tB, pg, (uint32_t)(spq / kGemmBM), (uint32_t)ceil_div(ncols, f.bn()), st);
+      launch_pair_gather(f.pair_c.p, f.out_bytes, f.nparty, ncodes, (uint32_t)ncols, persons, r, pd_out[fi], npairs,
+                         st);
+      launches += f.nparty + 2;  // parse + gemm + gather
+    }
     prof_end(ph, "pairs (gemm+gather)", st);
     debug_check("pairs", st);
     CK(c, cudaGetLastError());
-    launches += 5;  // 3 parse + gemm + gather
   }
   CK(c, cudaEventRecord(c->ev[1], st));
 
   if (c->taps) {
     c->tap_n = n;
-    const size_t sz[7] = {2, 2, 2, 2, 4, 4, 1};
+    const size_t tb[7] = {3 * n * hb, fm.nparty * n * mb, 3 * n * 4, 3 * n * 4, 3 * n * 4, 3 * n * 4, 3 * n};
     for (int t = 0; t < 7; ++t) {
-      if (c->tap_buf[t].ensure(3 * n * sz[t] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (taps)");
-      CK(c, cudaMemsetAsync(c->tap_buf[t].p, 0, 3 * n * sz[t] + 16, st));
+      c->tap_bytes[t] = tb[t];
+      if (c->tap_buf[t].ensure(tb[t] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (taps)");
+      CK(c, cudaMemsetAsync(c->tap_buf[t].p, 0, tb[t] + 16, st));
     }
   }
 
@@ -459,8 +510,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
       j.ntasks += seg_tasks(sg.lane_begin, sg.lane_end);
       j.ngrp += (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
-      j.ngblk += 3ull * 125 * (nw / 8 + 2);
-      j.gwords += 3ull * 125 * nw;
+      j.ngblk += 3ull * ngates * (nw / 8 + 2);
+      j.gwords += 3ull * ngates * nw;
     }
     jobs.push_back(j);
   };
@@ -502,24 +553,35 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     max_g = std::max(max_g, j.gwords);
     max_bits = std::max(max_bits, j.ntasks * 32);
   }
-  const uint64_t dots_half = 6 * ncols * rows_chunk;  // one dot buffer (u16 elements)
+  // one dot buffer half: hd [3][ncols * rows_chunk] then ml [nparty][ncols * rows_chunk]
+  const uint64_t hd_half = 3 * ncols * rows_chunk * hb;
+  const uint64_t dots_half = round_up(hd_half + fm.nparty * ncols * rows_chunk * mb, 16);
   if (nsegs_all) {
     CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
-    if ((nchunks && c->dots.ensure(2 * dots_half * sizeof(uint16_t))) ||
-        c->ml_rs.ensure(3 * cstride * sizeof(uint16_t) + 16) || c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) ||
-        c->gate.ensure(max_g * sizeof(uint64_t) + 16) || c->bits.ensure(6 * max_bits * sizeof(uint32_t) + 16))
+    if ((nchunks && c->dots.ensure(2 * dots_half)) ||
+        c->ml_rs.ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
+        c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) || c->gate.ensure(max_g * sizeof(uint64_t) + 16) ||
+        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
 
   ThrArgs ta{};
+  ta.variant = V;
   ta.n = n;
   ta.W = W;
   for (int k = 0; k < 3; ++k) {
     ta.pos[k] = c->pos[k];
     ta.key[k] = c->keys[k];
+    // stream layout: reshare n (+ n), lift 64W + inject, msb
+    const uint64_t inj = V == kMpcLift ? 64 * W + (k == 0 ? 2 * n : (k == 1 ? 0 : 6 * n)) : 0;
+    ta.lift_base[k] = c->pos[k] + n + nml;
+    ta.msb_base[k] = c->pos[k] + n + nml + inj;
   }
+  ta.nlift = nlift;
+  ta.ngates = ngates;
   ta.a = c->cfg.a;
   ta.b = c->cfg.b;
+  ta.coef = 1.0 - 2.0 * c->cfg.match_ratio;
   ta.partial = c->partial.as<uint8_t>();
   ta.nslots = total_slots;
   ta.or_elem_base = (qid << 48) | (rank << 40);
@@ -528,14 +590,15 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   ta.cstride = cstride;
   ta.gate = c->gate.as<uint64_t>();
   if (c->taps) {
-    ta.tap_rs_hd = c->tap_buf[2].as<uint16_t>();
-    ta.tap_rs_ml = c->tap_buf[3].as<uint16_t>();
+    ta.tap_rs_hd = c->tap_buf[2].as<uint32_t>();
+    ta.tap_rs_ml = c->tap_buf[3].as<uint32_t>();
     ta.tap_ml32 = c->tap_buf[4].as<uint32_t>();
     ta.tap_diff = c->tap_buf[5].as<uint32_t>();
     ta.tap_msb = c->tap_buf[6].as<uint8_t>();
   }
   uint64_t task_off = 0;
-  auto run_job = [&](const Job& j, const uint16_t* src_base, uint64_t pstride_hd, uint64_t off_ml) -> int {
+  // hd_base: [3][pstride] hd dots; ml_base: [nparty][pstride] ml dots / public popcounts
+  auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride) -> int {
     ThrArgs t = ta;
     t.segs = c->segs.as<Seg>() + j.seg0;
     t.nsegs = (uint32_t)j.nseg;
@@ -547,14 +610,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.or_elem_base = ta.or_elem_base + task_off * 64;
     task_off += j.ntasks;
     for (int p = 0; p < 3; ++p) {
-      t.hd[p] = src_base + p * pstride_hd;
-      t.ml[p] = src_base + p * pstride_hd + off_ml;
+      t.hd[p] = hd_base + p * pstride * hb;
+      t.ml[p] = ml_base + (fm.nparty == 3 ? p : 0) * pstride * mb;
       t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
     launch_threshold(t, st2);
     CK(c, cudaGetLastError());
-    launches += 5;
+    launches += V == kMpcLift ? 5 : 3;
     return 0;
   };
   auto ensure_events = [&](std::vector<cudaEvent_t>& v, size_t n_) -> int {
@@ -577,49 +640,50 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   CK(c, cudaStreamWaitEvent(st2, c->evg[nchunks], 0));
   CK(c, cudaEventRecord(c->ev[2], st2));
 
-  // ---- DB lanes: GEMM(i) on st || threshold(i-1) on st2
+  // ---- DB lanes: GEMMs(i) on st || threshold(i-1) on st2
   double gemm_ms = 0;
   uint64_t gemm_launches = 0;
   size_t ji = 0;
   for (uint64_t i = 0; i < nchunks; ++i) {
     const uint64_t nr = chunk_rows(i);
-    uint16_t* dots = c->dots.as<uint16_t>() + (i % 2) * dots_half;
+    uint8_t* dots = c->dots.as<uint8_t>() + (i % 2) * dots_half;
+    uint8_t* dots_ml = dots + hd_half;
     if (i >= 2) CK(c, cudaStreamWaitEvent(st, c->evt[i - 2], 0));  // buffer i%2 released
-    GemmArgs g{};
-    g.s_pad = (uint32_t)c->s_pad;
-    g.nb_rows = ncols_pad;
-    g.nkb_seg = c->l_pad / kGemmBK;
-    g.nseg = c->nseg;
-    g.rep = c->shamir ? 0 : 1;
-    g.s_valid = (uint32_t)nr;
-    g.row0 = (uint32_t)(i * rows_chunk);
-    g.col0 = 0;
-    g.ncols = (uint32_t)ncols;
-    g.out = dots;
-    g.out_pstride = ncols * nr;
-    g.out_cstride = (uint32_t)nr;
     CK(c, cudaEventRecord(c->gev[2 * i], st));
-    void* ph = prof_begin(st);
-    launch_gemm(c->tA_lo, c->tA_hi, c->tB_lo, c->tB_hi, g, (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM),
-                (uint32_t)ceil_div(ncols, kGemmBN), st);
-    prof_end(ph, "k_limb_gemm_pair", st);
-    debug_check("k_limb_gemm", st);
-    CK(c, cudaGetLastError());
+    for (int fi = 0; fi < 2; ++fi) {
+      FieldPlanes& f = c->fld[fi];
+      GemmArgs g = field_gemm_args(c, f, ncols_pad);
+      g.s_pad = (uint32_t)c->s_pad;
+      g.s_valid = (uint32_t)nr;
+      g.row0 = (uint32_t)(i * rows_chunk);
+      g.ncols = (uint32_t)ncols;
+      g.out = fi == 0 ? dots : dots_ml;
+      g.out_pstride = ncols * nr;
+      g.out_cstride = (uint32_t)nr;
+      void* ph = prof_begin(st);
+      launch_gemm(f.tA, f.tB, g, (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM), (uint32_t)ceil_div(ncols, f.bn()),
+                  st);
+      prof_end(ph, fi == 0 ? "k_limb_gemm_pair (hd)" : "k_limb_gemm_pair (ml)", st);
+      debug_check("k_limb_gemm_pair", st);
+      CK(c, cudaGetLastError());
+      ++gemm_launches;
+      ++launches;
+    }
     CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
-    ++gemm_launches;
-    ++launches;
     if (c->taps && c->cfg.db_rows_total == 0) {
       // L1 tap: dots[(col, row - r0)] -> lane col*S + row
-      for (int p = 0; p < 3; ++p)
-        for (int d = 0; d < 2; ++d)
-          CK(c, cudaMemcpy2DAsync(c->tap_buf[d].as<uint16_t>() + p * n + i * rows_chunk, S * 2,
-                                  dots + (2 * p + d) * g.out_pstride, nr * 2, nr * 2, ncols,
-                                  cudaMemcpyDeviceToDevice, st));
+      for (uint32_t p = 0; p < 3; ++p)
+        CK(c, cudaMemcpy2DAsync(c->tap_buf[0].as<uint8_t>() + (p * n + i * rows_chunk) * hb, S * hb,
+                                dots + p * ncols * nr * hb, nr * hb, nr * hb, ncols, cudaMemcpyDeviceToDevice, st));
+      for (uint32_t p = 0; p < fm.nparty; ++p)
+        CK(c, cudaMemcpy2DAsync(c->tap_buf[1].as<uint8_t>() + (p * n + i * rows_chunk) * mb, S * mb,
+                                dots_ml + p * ncols * nr * mb, nr * mb, nr * mb, ncols, cudaMemcpyDeviceToDevice,
+                                st));
     }
     CK(c, cudaEventRecord(c->evg[i], st));
     CK(c, cudaStreamWaitEvent(st2, c->evg[i], 0));
     for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji) {
-      int rc2 = run_job(jobs[ji], dots, 2 * g.out_pstride, g.out_pstride);
+      int rc2 = run_job(jobs[ji], dots, dots_ml, ncols * nr);
       if (rc2) return rc2;
     }
     CK(c, cudaEventRecord(c->evt[i], st2));
@@ -627,17 +691,17 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
 
   // ---- pair lanes (shard 0): threshold into match words
   if (npairs) {
+    const uint8_t* pd_hd = c->pair_dots.as<uint8_t>();
+    const uint8_t* pd_ml = pd_hd + 3 * npairs * hb;
     if (c->taps && c->cfg.db_rows_total == 0) {
-      for (int p = 0; p < 3; ++p) {
-        CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint16_t>() + p * n + ncols * S,
-                              c->pair_dots.as<uint16_t>() + p * 2 * npairs, npairs * 2,
-                              cudaMemcpyDeviceToDevice, st2));
-        CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint16_t>() + p * n + ncols * S,
-                              c->pair_dots.as<uint16_t>() + npairs + p * 2 * npairs, npairs * 2,
-                              cudaMemcpyDeviceToDevice, st2));
-      }
+      for (uint32_t p = 0; p < 3; ++p)
+        CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint8_t>() + (p * n + ncols * S) * hb, pd_hd + p * npairs * hb,
+                              npairs * hb, cudaMemcpyDeviceToDevice, st2));
+      for (uint32_t p = 0; p < fm.nparty; ++p)
+        CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint8_t>() + (p * n + ncols * S) * mb, pd_ml + p * npairs * mb,
+                              npairs * mb, cudaMemcpyDeviceToDevice, st2));
     }
-    int rc2 = run_job(jobs.back(), c->pair_dots.as<uint16_t>(), 2 * npairs, npairs);
+    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs);
     if (rc2) return rc2;
   }
   CK(c, cudaEventRecord(c->ev[3], st2));
@@ -691,9 +755,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t glen = membership ? S : 2ull * r * S + (uint64_t)(persons ? persons - 1 : 0) * 4 * r;
   uint64_t or_rounds = 0, or_bytes = 0;
   const uint64_t ord = ref_or_draws(ngroups, glen, &or_rounds, &or_bytes);
-  c->pos[0] += 4 * n + 125 * W + ord;
-  c->pos[1] += 2 * n + 125 * W + ord;
-  c->pos[2] += 8 * n + 125 * W + ord;
+  const uint64_t msb_draws = (uint64_t)(2 * vw.kc - 3) * W;
+  for (int k = 0; k < 3; ++k) c->pos[k] = ta.msb_base[k] + msb_draws + ord;
 
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
@@ -703,21 +766,21 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     stats->lanes = n;
     const uint64_t nb8 = ceil_div(n, 8), open_b = ceil_div(ngroups, 8);
     for (int p = 0; p < 3; ++p) {
-      stats->dot_bytes[p] = 4 * n;
-      stats->lift_bytes[p] = 64 * nb8 + (p == 0 ? 8 * n : 4 * n);
-      stats->msb_bytes[p] = 61 * nb8;
+      stats->dot_bytes[p] = n * (vw.kh / 8) + nml * (vw.km / 8);
+      stats->lift_bytes[p] = V == kMpcLift ? 64 * nb8 + (p == 0 ? 8 * n : 4 * n) : 0;
+      stats->msb_bytes[p] = (uint64_t)(2 * vw.kc - 3) * nb8;
       stats->or_tree_bytes[p] = or_bytes + (p == 0 ? 0 : open_b) + (c->cfg.debug_rows && p != 0 ? nb8 : 0);
     }
     stats->dot_rounds = 1;
-    stats->lift_rounds = 21;
-    stats->msb_rounds = 31;
+    stats->lift_rounds = V == kMpcLift ? 21 : 0;
+    stats->msb_rounds = (uint64_t)vw.kc - 1;
     stats->or_tree_rounds = or_rounds + 1 + (c->cfg.debug_rows ? 1 : 0);
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
     stats->wall_ms = ms;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     stats->prep_ms = ms;
-    for (uint64_t i = 0; i < gemm_launches; ++i) {
+    for (uint64_t i = 0; i < nchunks; ++i) {
       cudaEventElapsedTime(&ms, c->gev[2 * i], c->gev[2 * i + 1]);
       gemm_ms += ms;
     }
@@ -752,8 +815,8 @@ int irismpc_gpu_seeds_from_master(uint64_t master, uint8_t out[48]) {
 }
 
 size_t irismpc_gpu_record_bytes(uint32_t backend, uint32_t variant, uint32_t l) {
-  if (variant != IRISMPC_GPU_VARIANT_MPC_LIFT) return 0;
-  return record_bytes(backend, l);
+  if (variant > IRISMPC_GPU_VARIANT_NO_LIFT || backend > 1) return 0;
+  return record_bytes(backend, variant, l);
 }
 
 uint64_t irismpc_gpu_lane_count(uint32_t persons, uint64_t s, uint32_t rotations, int membership) {
@@ -784,9 +847,25 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   auto* c = new irismpc_gpu_ctx;
   c->cfg = *cfg;
   c->shamir = cfg->backend == IRISMPC_GPU_BACKEND_SHAMIR;
+  c->variant = (int)cfg->variant;
+  c->vw = variant_widths(c->variant);
   c->l = cfg->l;
   c->l_pad = (uint32_t)round_up(cfg->l, kGemmBK);
-  c->nseg = c->shamir ? 1 : 2;
+  c->rec = record_bytes(cfg->backend, cfg->variant, cfg->l);
+  {
+    const uint64_t code_b = field_bytes(cfg->backend, c->vw.kh, cfg->l);
+    const int widths[2] = {c->vw.kh / 8, c->vw.km / 8};
+    for (int fi = 0; fi < 2; ++fi) {
+      FieldPlanes& f = c->fld[fi];
+      f.fmt.rec_bytes = c->rec;
+      f.fmt.off = fi == 0 ? 0 : code_b;
+      f.fmt.width = widths[fi];
+      f.fmt.limbs = widths[fi] == 0 ? 1 : widths[fi];
+      f.nparty = widths[fi] == 0 ? 1 : 3;
+      f.nseg = (widths[fi] != 0 && !c->shamir) ? 2 : 1;
+      f.out_bytes = f.fmt.limbs == 4 ? 4 : 2;
+    }
+  }
   for (int k = 0; k < 3; ++k) c->keys[k] = key_of(cfg->seeds + 16 * k);
   // the GEMM stream gets the higher priority: when GEMM and threshold blocks
   // compete for SM residency the tensor-pipe work is scheduled first
@@ -798,7 +877,7 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
     return IRISMPC_GPU_ERR_DEVICE;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
-  uint16_t lam[6];
+  uint32_t lam[6];
   lambdas(lam);
   set_lambda(lam);
   *out = c;
@@ -809,11 +888,11 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
   cudaStreamSynchronize(c->st);
-  Buf* bufs[] = {&c->db_lo, &c->db_hi, &c->q_lo, &c->q_hi, &c->q_pa, &c->q_pb, &c->q_pay[0], &c->q_pay[1],
-                 &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial, &c->slot_begin,
-                 &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
-                 &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->qa_lo, &c->qa_hi, &c->pair_c};
+  Buf* bufs[] = {&c->q_pay[0], &c->q_pay[1], &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial,
+                 &c->slot_begin, &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
   for (Buf* b : bufs) b->release();
+  for (auto& f : c->fld) f.release();
   for (auto& t : c->tap_buf) t.release();
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
   for (auto& e : c->ev) cudaEventDestroy(e);
@@ -833,7 +912,7 @@ void* irismpc_gpu_stream(irismpc_gpu_ctx* c) { return c ? (void*)c->st : nullptr
 int irismpc_gpu_load_db(irismpc_gpu_ctx* c, const uint8_t* const payload[3], const size_t len[3], uint64_t s) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
   cudaSetDevice(c->cfg.device);
-  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const size_t rec = c->rec;
   for (int p = 0; p < 3; ++p)
     if (len[p] != s * rec) return fail(c, IRISMPC_GPU_ERR_CONFIG, "db payload size mismatch");
   int rc = alloc_planes(c, s);
@@ -864,7 +943,7 @@ int irismpc_gpu_load_db_device(irismpc_gpu_ctx* c, const uint8_t* const dpayload
                                uint64_t s) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
   cudaSetDevice(c->cfg.device);
-  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const size_t rec = c->rec;
   for (int p = 0; p < 3; ++p)
     if (len[p] != s * rec) return fail(c, IRISMPC_GPU_ERR_CONFIG, "db payload size mismatch");
   int rc = alloc_planes(c, s);
@@ -955,8 +1034,8 @@ int irismpc_gpu_deal_payload(irismpc_gpu_ctx* c, uint64_t deal_seed, uint64_t ta
   uint8_t s[16], d[16];
   host_seed_from_u64(deal_seed, s);
   host_derive(s, tag, d);
-  launch_deal(key_of(d), first_record, nrec, c->l, c->shamir, codes_dev, masks_dev, out_dev[0], out_dev[1],
-              out_dev[2], c->st);
+  launch_deal(key_of(d), first_record, nrec, c->l, c->shamir, c->variant, codes_dev, masks_dev, out_dev[0],
+              out_dev[1], out_dev[2], c->st);
   CK(c, cudaGetLastError());
   CK(c, cudaStreamSynchronize(c->st));
   return 0;
@@ -968,7 +1047,7 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint
   cudaSetDevice(c->cfg.device);
   int rc = alloc_planes(c, s);
   if (rc) return rc;
-  const size_t rec = record_bytes(c->cfg.backend, c->l);
+  const size_t rec = c->rec;
   const uint64_t wl = (c->l + 63) / 64;
   const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s ? s : 1, (512ull << 20) / rec));
   Buf codes, masks, pay[3];
@@ -983,7 +1062,7 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint
     const uint64_t nr = std::min<uint64_t>(chunk, s - r0);
     launch_synth_records(key_of(sr), first + r0, nr, c->l, mask_density, codes.as<uint64_t>(),
                          masks.as<uint64_t>(), c->st);
-    launch_deal(key_of(dd), first + r0, nr, c->l, c->shamir, codes.as<uint64_t>(), masks.as<uint64_t>(),
+    launch_deal(key_of(dd), first + r0, nr, c->l, c->shamir, c->variant, codes.as<uint64_t>(), masks.as<uint64_t>(),
                 pay[0].as<uint8_t>(), pay[1].as<uint8_t>(), pay[2].as<uint8_t>(), c->st);
     const uint8_t* dp[3] = {pay[0].as<uint8_t>(), pay[1].as<uint8_t>(), pay[2].as<uint8_t>()};
     rc = parse_rows(c, dp, nr, r0, nullptr);
@@ -1006,8 +1085,7 @@ int irismpc_gpu_enable_taps(irismpc_gpu_ctx* c, int enable) {
 int irismpc_gpu_read_tap(irismpc_gpu_ctx* c, int tap, void* host_out, size_t bytes) {
   if (!c || tap < 1 || tap > 7) return IRISMPC_GPU_ERR_CONFIG;
   if (!c->tap_buf[tap - 1].p) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap not captured");
-  const size_t sz[7] = {2, 2, 2, 2, 4, 4, 1};
-  const size_t have = 3 * c->tap_n * sz[tap - 1];
+  const size_t have = c->tap_bytes[tap - 1];
   if (bytes > have) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap read larger than captured");
   cudaSetDevice(c->cfg.device);
   CK(c, cudaMemcpy(host_out, c->tap_buf[tap - 1].p, bytes, cudaMemcpyDeviceToHost));

@@ -1,20 +1,27 @@
-// K2: Z_2^16 share dot products as u8-limb GEMMs on the 5th-gen tensor cores.
+// K2: share dot products as u8-limb GEMMs on the 5th-gen tensor cores.
 //
-// Replaces kernels::dot_gr_ct_rows<16> / dot_prep_rows<16>
-// (/root/reference/proj/src/kernels.cpp:29-53, include/irismpc/kernels.hpp:38-62):
-// for every party p and dot d (code -> hd, mask -> ml)
-//     C_p[row, col] = sum_k A_p[row, k] * B_p[col, k]   (mod 2^16)
-// with 16-bit operands split into u8 limbs, V = lo + 256 hi:
-//     C = A_lo.B_lo^T + 256 (A_lo.B_hi^T + A_hi.B_lo^T)   (mod 2^16)
-// i.e. three tcgen05.mma.kind::i8 per k-step into two s32 TMEM accumulators
-// (no saturation: the s32 wrap is harmless, only the low 16 bits survive).
-// The epilogue recombines (acc0 + (acc1 << 8)) & 0xffff and writes the
-// per-party additive shares in lane order (lane = col * s + row).
+// Replaces kernels::dot_gr_ct_rows<K> / dot_prep_rows<K>
+// (/root/reference/proj/src/kernels.cpp:29-61, include/irismpc/kernels.hpp:38-62)
+// and the public-mask popcount_and (src/engine.cpp:62-68, 329-334): for every
+// party p of one record field
+//     C_p[row, col] = sum_k A_p[row, k] * B_p[col, k]   (mod 2^K)
+// with the K-bit operands split into u8 limbs, V = sum_i 2^(8i) V_i:
+//     C = sum_{i+j < L} 2^(8(i+j)) A_i.B_j^T            (mod 2^(8L))
+// i.e. per k-step L(L+1)/2 tcgen05.mma.kind::i8 into L s32 TMEM accumulators
+// (acc_s collects the products with i + j = s; the s32 wrap is harmless, only
+// the low 8(L - s) bits of acc_s survive the recombination):
+//     L = 1  public 0/1 mask bits: popcount(q & db) = acc0 (< 2^14)
+//     L = 2  Z_2^16: 3 MMAs, 2 accumulators, N = 256
+//     L = 4  Z_2^32: 10 MMAs, 4 accumulators, N = 128 (4 x 128 TMEM columns)
+// The epilogue recombines sum_s acc_s << 8s and writes the per-party additive
+// shares in lane order (lane = col * s + row).
 //
-// Structure: one 128x256 output tile per CTA, warp-specialised:
-//   warp 0   TMA producer (128B-swizzled K-major tiles, 2-stage mbarrier ring)
-//   warp 1   single-thread tcgen05.mma issuer, tcgen05.commit -> mbarriers
-//   warp 2   TMEM allocator (512 columns: acc0 | acc1)
+// cta_group::2: a cluster of 2 CTAs computes a 256 x N tile; each CTA stages
+// its own 128 DB rows and N/2 query columns per limb, the leader CTA issues
+// tcgen05.mma.cta_group::2 (M = 256) and commits to both CTAs' barriers.
+// Warp-specialised and persistent:
+//   warp 0   TMA producer (128B-swizzled K-major tiles, mbarrier ring)
+//   warp 1   TMEM allocator; the leader's lane 0 issues the MMAs
 //   warps 4-7 epilogue: tcgen05.ld -> recombine -> global stores
 #include <cstdio>
 #include <algorithm>
@@ -27,13 +34,9 @@ namespace irisgpu {
 
 namespace {
 
-constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-constexpr int STAGES = 2;
-constexpr int A_TILE = BM * BK;  // 16 KB
-constexpr int B_TILE = BN * BK;  // 32 KB
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int BK = kGemmBK;
 constexpr uint32_t TMEM_COLS = 512;
+constexpr int kStageBudget = 200 * 1024;
 
 // UMMA shared-memory descriptor, K-major operand, 128B swizzle:
 // start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major -> 1),
@@ -49,160 +52,36 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor, kind::i8: c_format S32 (2) [4,6), a/b format u8 (0),
-// K-major A and B, N>>3 [17,23), M>>4 [24,29).
-constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+template <int L>
+struct Tile {
+  static constexpr int BN = L == 4 ? 128 : 256;       // output columns per tile
+  static constexpr int A_T = 128 * BK;                // this CTA's 128 rows, one limb
+  static constexpr int B_T = (BN / 2) * BK;           // this CTA's BN/2 columns, one limb
+  static constexpr int STAGE = L * (A_T + B_T);
+  static constexpr int STAGES = kStageBudget / STAGE > 6 ? 6 : kStageBudget / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  // Instruction descriptor, kind::i8: c_format S32 (2) [4,6), a/b format u8 (0),
+  // K-major A and B, N>>3 [17,23), M>>4 [24,29) with M = 256 (CTA pair).
+  static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+};
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 1)
-    k_limb_gemm(const __grid_constant__ CUtensorMap tA_lo, const __grid_constant__ CUtensorMap tA_hi,
-                const __grid_constant__ CUtensorMap tB_lo, const __grid_constant__ CUtensorMap tB_hi,
-                const GemmArgs g) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x;
-  const int m_tile = blockIdx.y;
-  const int prob = blockIdx.z;  // p * 2 + d
-  const int p = prob >> 1, d = prob & 1;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tA_lo);
-    tma_prefetch_desc(&tA_hi);
-    tma_prefetch_desc(&tB_lo);
-    tma_prefetch_desc(&tB_hi);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(accum, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t nkb = g.nkb_seg * g.nseg;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        const uint32_t stage = kb % STAGES;
-        const uint32_t phase = (kb / STAGES) & 1;
-        mbar_wait(&empty[stage], phase ^ 1);
-        const uint32_t seg = kb / g.nkb_seg;
-        const uint32_t kk = kb % g.nkb_seg;
-        const int pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;  // A = [x_p | x_{p-1}]
-        const int32_t arow = (int32_t)((uint32_t)(pa * 2 + d) * g.s_pad + g.row0 + m_tile * BM);
-        const int32_t brow = (int32_t)(((uint32_t)prob * g.nseg + seg) * g.nb_rows + g.col0 + n_tile * BN);
-        uint8_t* st = smem + stage * STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-        tma_load_2d(st, &tA_lo, &full[stage], (int32_t)(kk * BK), arow);
-        tma_load_2d(st + A_TILE, &tA_hi, &full[stage], (int32_t)(kk * BK), arow);
-        // B maps have a 128-row box (the CTA-pair kernel loads half tiles): two loads each
-        tma_load_2d(st + 2 * A_TILE, &tB_lo, &full[stage], (int32_t)(kk * BK), brow);
-        tma_load_2d(st + 2 * A_TILE + B_TILE / 2, &tB_lo, &full[stage], (int32_t)(kk * BK), brow + 128);
-        tma_load_2d(st + 2 * A_TILE + B_TILE, &tB_hi, &full[stage], (int32_t)(kk * BK), brow);
-        tma_load_2d(st + 2 * A_TILE + B_TILE + B_TILE / 2, &tB_hi, &full[stage], (int32_t)(kk * BK), brow + 128);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        const uint32_t stage = kb % STAGES;
-        const uint32_t phase = (kb / STAGES) & 1;
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
-        const uint64_t dAlo = make_desc(st);
-        const uint64_t dAhi = make_desc(st + A_TILE);
-        const uint64_t dBlo = make_desc(st + 2 * A_TILE);
-        const uint64_t dBhi = make_desc(st + 2 * A_TILE + B_TILE);
-#pragma unroll
-        for (int ks = 0; ks < BK / 32; ++ks) {
-          const uint64_t off = (uint64_t)(ks * 32) >> 4;  // +32 bytes along K
-          const uint32_t acc = (kb | ks) != 0;
-          umma_i8(tmem, dAlo + off, dBlo + off, kIdesc, acc);            // lo.lo   -> acc0
-          umma_i8(tmem + BN, dAlo + off, dBhi + off, kIdesc, acc);       // lo.hi   -> acc1
-          umma_i8(tmem + BN, dAhi + off, dBlo + off, kIdesc, 1u);        // hi.lo   -> acc1
-        }
-        umma_commit(&empty[stage]);
-      }
-      umma_commit(accum);
-    }
-  } else if (warp >= 4) {
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const uint32_t row = (uint32_t)m_tile * BM + q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    uint16_t* out = g.out + (uint64_t)prob * g.out_pstride;
-    const bool row_ok = row < g.s_valid;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t a0[16], a1[16];
-      tmem_ld16(tmem + lane_addr + c, a0);
-      tmem_ld16(tmem + lane_addr + BN + c, a1);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t col = (uint32_t)n_tile * BN + c + j;
-        if (row_ok && col < g.ncols) {
-          out[(uint64_t)col * g.out_cstride + row] = (uint16_t)((a0[j] + (a1[j] << 8)) & 0xFFFFu);
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-  }
-}
-
-// ---------------------------------------------------------------- CTA pair
-// cta_group::2 variant: a cluster of 2 CTAs computes a 256x256 tile; each CTA
-// stages its own 128 DB rows and half (128 columns) of the query tile, the
-// leader CTA issues tcgen05.mma.cta_group::2 (M = 256) and commits to both
-// CTAs' barriers.  Per SM this halves the B traffic of the 1-CTA kernel
-// (64 KB instead of 96 KB per 1536-cycle stage), which is what bounded it
-// (L2 -> SM bandwidth, ncu: 69.8% tensor-pipe active).
-namespace {
-constexpr int P_STAGES = 3;
-constexpr int PA_TILE = 128 * BK;  // 16 KB (this CTA's 128 rows)
-constexpr int PB_TILE = 128 * BK;  // 16 KB (this CTA's 128 of 256 columns)
-constexpr int P_STAGE = 2 * PA_TILE + 2 * PB_TILE;  // 64 KB
-constexpr int P_SMEM = P_STAGES * P_STAGE + 1024 + 256;
-constexpr uint32_t kIdescPair = (2u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-}  // namespace
-
+template <int L>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA_lo, const __grid_constant__ CUtensorMap tA_hi,
-                     const __grid_constant__ CUtensorMap tB_lo, const __grid_constant__ CUtensorMap tB_hi,
+    k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs, uint32_t grouped) {
   // Persistent: clusters form groups of n_tiles; cluster c owns n_tile = c % n_tiles
   // and its group sweeps (prob, m_pair) units g, g + groups, ...  The n_tiles
   // clusters of a group read the same DB (A) k-blocks at the same time, so every
-  // A byte comes from DRAM once; B (one problem's query tile, 26 MB) stays in L2.
+  // A byte comes from DRAM once; B (one problem's query tile) stays in L2.
+  using T = Tile<L>;
+  constexpr int BN = T::BN, STAGES = T::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE);
-  uint64_t* empty = full + P_STAGES;
-  uint64_t* accum = empty + P_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * T::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
   uint64_t* tmem_empty = accum + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
@@ -220,14 +99,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t groups = ncl / tiles_per_unit;
   const uint32_t my_n = flat ? 0 : cl % n_tiles;
   const uint32_t g0 = flat ? cl : cl / n_tiles;
-  const uint32_t nunits = flat ? 6 * m_pairs * n_tiles : 6 * m_pairs;
+  const uint32_t nunits = flat ? g.nprob * m_pairs * n_tiles : g.nprob * m_pairs;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tA_lo);
-    tma_prefetch_desc(&tA_hi);
-    tma_prefetch_desc(&tB_lo);
-    tma_prefetch_desc(&tB_hi);
-    for (int s = 0; s < P_STAGES; ++s) {
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tB);
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -253,25 +130,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const uint32_t n_tile = flat ? u % n_tiles : my_n;
         const uint32_t uu = flat ? u / n_tiles : u;
         const uint32_t m_pair = uu % m_pairs;
-        const int prob = (int)(uu / m_pairs);
-        const int p = prob >> 1, d = prob & 1;
+        const uint32_t p = uu / m_pairs;
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-          const uint32_t stage = it % P_STAGES;
-          const uint32_t phase = (it / P_STAGES) & 1;
+          const uint32_t stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t seg = kb / g.nkb_seg;
           const uint32_t kk = kb % g.nkb_seg;
-          const int pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;  // A = [x_p | x_{p-1}]
-          const int32_t arow = (int32_t)((uint32_t)(pa * 2 + d) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
-          const int32_t brow =
-              (int32_t)(((uint32_t)prob * g.nseg + seg) * g.nb_rows + g.col0 + n_tile * 256 + rank * 128);
-          uint8_t* st = smem + stage * P_STAGE;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE);
+          const uint32_t pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;  // A = [x_p | x_{p-1}]
+          uint8_t* st = smem + stage * T::STAGE;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * T::STAGE);
           const uint32_t fb = mapa_shared(&full[stage], 0);
-          tma_load_2d_pair(st, &tA_lo, fb, (int32_t)(kk * BK), arow);
-          tma_load_2d_pair(st + PA_TILE, &tA_hi, fb, (int32_t)(kk * BK), arow);
-          tma_load_2d_pair(st + 2 * PA_TILE, &tB_lo, fb, (int32_t)(kk * BK), brow);
-          tma_load_2d_pair(st + 2 * PA_TILE + PB_TILE, &tB_hi, fb, (int32_t)(kk * BK), brow);
+#pragma unroll
+          for (int limb = 0; limb < L; ++limb) {
+            const int32_t arow =
+                (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
+            const int32_t brow = (int32_t)(((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 + n_tile * BN +
+                                           rank * (BN / 2));
+            tma_load_2d_pair(st + limb * T::A_T, &tA, fb, (int32_t)(kk * BK), arow);
+            tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
+          }
         }
       }
     }
@@ -284,22 +162,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           tc_fence_after();
         }
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-          const uint32_t stage = it % P_STAGES;
-          const uint32_t phase = (it / P_STAGES) & 1;
+          const uint32_t stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + stage * P_STAGE);
-          const uint64_t dAlo = make_desc(st);
-          const uint64_t dAhi = make_desc(st + PA_TILE);
-          const uint64_t dBlo = make_desc(st + 2 * PA_TILE);
-          const uint64_t dBhi = make_desc(st + 2 * PA_TILE + PB_TILE);
+          const uint32_t st = smem_u32(smem + stage * T::STAGE);
 #pragma unroll
           for (int ks = 0; ks < BK / 32; ++ks) {
-            const uint64_t off = (uint64_t)(ks * 32) >> 4;
-            const uint32_t acc = (kb | ks) != 0;
-            umma_i8_pair(tmem, dAlo + off, dBlo + off, kIdescPair, acc);        // lo.lo -> acc0
-            umma_i8_pair(tmem + 256, dAlo + off, dBhi + off, kIdescPair, acc);  // lo.hi -> acc1
-            umma_i8_pair(tmem + 256, dAhi + off, dBlo + off, kIdescPair, 1u);   // hi.lo -> acc1
+            const uint64_t off = (uint64_t)(ks * 32) >> 4;  // +32 bytes along K
+#pragma unroll
+            for (int i = 0; i < L; ++i)
+#pragma unroll
+              for (int j = 0; i + j < L; ++j) {
+                const uint64_t da = make_desc(st + i * T::A_T) + off;
+                const uint64_t db = make_desc(st + L * T::A_T + j * T::B_T) + off;
+                const uint32_t acc = ((kb | ks) != 0 || i > 0) ? 1u : 0u;  // (0, s) opens acc_s
+                umma_i8_pair(tmem + (i + j) * BN, da, db, T::IDESC, acc);
+              }
           }
           umma_commit_pair(&empty[stage], 0x3);
         }
@@ -315,23 +194,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const uint32_t n_tile = flat ? u % n_tiles : my_n;
       const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
-      const int prob = (int)(uu / m_pairs);
+      const uint32_t p = uu / m_pairs;
       mbar_wait(accum, ti & 1);
       tc_fence_after();
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
-      uint16_t* out = g.out + (uint64_t)prob * g.out_pstride;
       const bool row_ok = row < g.s_valid;
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 16) {
-        uint32_t a0[16], a1[16];
-        tmem_ld16(tmem + lane_addr + c, a0);
-        tmem_ld16(tmem + lane_addr + 256 + c, a1);
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t acc[L][16];
+#pragma unroll
+        for (int s = 0; s < L; ++s) tmem_ld16(tmem + lane_addr + s * BN + c, acc[s]);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const uint32_t col = n_tile * 256 + c + j;
-          if (row_ok && col < g.ncols)
-            out[(uint64_t)col * g.out_cstride + row] = (uint16_t)((a0[j] + (a1[j] << 8)) & 0xFFFFu);
+          const uint32_t col = n_tile * BN + c + j;
+          if (!row_ok || col >= g.ncols) continue;
+          uint32_t v = acc[0][j];
+#pragma unroll
+          for (int s = 1; s < L; ++s) v += acc[s][j] << (8 * s);
+          const uint64_t o = (uint64_t)p * g.out_pstride + (uint64_t)col * g.out_cstride + row;
+          if (L == 4)
+            static_cast<uint32_t*>(g.out)[o] = v;
+          else
+            static_cast<uint16_t*>(g.out)[o] = (uint16_t)v;
         }
       }
       tc_fence_before();
@@ -380,35 +265,34 @@ int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
-void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtensorMap& b_lo,
-                 const CUtensorMap& b_hi, const GemmArgs& g, uint32_t m_tiles, uint32_t n_tiles,
-                 cudaStream_t st) {
+template <int L>
+static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
+                               uint32_t n_tiles, cudaStream_t st) {
+  using T = Tile<L>;
   static bool attr = false;
-  static const bool one_cta = [] {
-    const char* e = std::getenv("IRISMPC_GEMM_1CTA");  // A/B switch for the 1-CTA kernel
-    return e && e[0] == '1';
-  }();
   if (!attr) {
-    cudaFuncSetAttribute(k_limb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(k_limb_gemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    cudaFuncSetAttribute(k_limb_gemm_pair<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
     attr = true;
   }
-  if (one_cta) {
-    dim3 grid(n_tiles, m_tiles, 6);
-    k_limb_gemm<<<grid, 256, SMEM_BYTES, st>>>(a_lo, a_hi, b_lo, b_hi, g);
-  } else {
-    // m_tiles counts 128-row tiles; pairs cover 256 rows (s_pad is a multiple of 256).
-    // Persistent: one CTA pair per two SMs.
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const uint32_t m_pairs = m_tiles / 2;
-    const uint32_t units = 6 * m_pairs;
-    const uint32_t max_cl = (uint32_t)(nsm / 2);
-    const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
-    const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
-    const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
-    k_limb_gemm_pair<<<dim3(2 * ncl), 256, P_SMEM, st>>>(a_lo, a_hi, b_lo, b_hi, g, n_tiles, m_pairs,
-                                                          grouped ? 1u : 0u);
+  // m_tiles counts 128-row tiles; pairs cover 256 rows (s_pad is a multiple of 256).
+  // Persistent: one CTA pair per two SMs.
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const uint32_t m_pairs = m_tiles / 2;
+  const uint32_t units = g.nprob * m_pairs;
+  const uint32_t max_cl = (uint32_t)(nsm / 2);
+  const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
+  const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
+  const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
+  k_limb_gemm_pair<L><<<dim3(2 * ncl), 256, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
+}
+
+void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
+                 uint32_t n_tiles, cudaStream_t st) {
+  switch (g.limbs) {
+    case 1: launch_pair_kernel<1>(a, b, g, m_tiles, n_tiles, st); break;
+    case 2: launch_pair_kernel<2>(a, b, g, m_tiles, n_tiles, st); break;
+    default: launch_pair_kernel<4>(a, b, g, m_tiles, n_tiles, st); break;
   }
 }
 

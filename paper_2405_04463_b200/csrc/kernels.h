@@ -18,19 +18,42 @@ bool prof_on();
 void* prof_begin(cudaStream_t st);
 void prof_end(void* h, const char* name, cudaStream_t st);
 
+// ---- variants (shares.hpp:28-48): ring widths of the hamming dot, the mask
+// dot (0 = public mask bits) and the comparison
+enum { kPlainMask = 0, kMpcLift = 1, kConstLift = 2, kNoLift = 3 };
+struct VariantWidths {
+  int kh, km, kc;
+};
+__host__ __device__ inline VariantWidths variant_widths(int v) {
+  return {v == kNoLift ? 32 : 16, v == kPlainMask ? 0 : (v == kMpcLift ? 16 : 32), v == kPlainMask ? 16 : 32};
+}
+
+// One record field as stored in an IRS1 payload row (shares.hpp:52-56):
+// `width` bytes per ring element (2 / 4) or 0 for l/8 public mask bytes.
+struct FieldFmt {
+  uint64_t rec_bytes;  // whole record (code + mask field)
+  uint64_t off;        // byte offset of the field inside the record
+  int width;           // 2, 4 or 0 (plain mask bits)
+  int limbs;           // u8 limb planes of the field (width, or 1 for bits)
+};
+
 // ---- K1 prep / dealer (prep.cu)
-void set_lambda(const uint16_t lam[6]);
-void launch_parse_db(const uint8_t* pay, uint64_t nrows, uint64_t row0, uint32_t l, uint32_t l_pad,
-                     uint64_t s_pad, int party, int shamir, uint8_t* lo, uint8_t* hi,
-                     cudaStream_t st);
-void launch_check_rep(const uint8_t* p1, const uint8_t* p2, const uint8_t* p3, uint64_t bytes,
-                      int* bad, cudaStream_t st);
-void launch_parse_query(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes,
-                        uint32_t l, uint32_t l_pad, uint32_t rot, uint32_t ncols_pad, int shamir,
-                        uint8_t* blo, uint8_t* bhi, uint16_t* pa, uint16_t* pb, cudaStream_t st);
+void set_lambda(const uint32_t lam[6]);
+// DB-side planes of one field: planes[((c * limbs + limb) * s_pad + row0 + row) * l_pad + k]
+// (c = party; bits: one public plane, c = 0)
+void launch_parse_field(const uint8_t* pay, uint64_t nrows, uint64_t row0, uint32_t l, uint32_t l_pad,
+                        uint64_t s_pad, int party, int shamir, const FieldFmt& f, uint8_t* planes,
+                        cudaStream_t st);
+void launch_check_rep(const uint8_t* p1, const uint8_t* p2, const uint8_t* p3, uint64_t nrows,
+                      const FieldFmt& f, uint32_t l, int* bad, cudaStream_t st);
+// Query-side rotated B planes of one field:
+// planes[(((p * nseg + seg) * limbs + limb) * ncols_pad + col) * l_pad + k]
+void launch_parse_query_field(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes,
+                              uint32_t l, uint32_t l_pad, uint32_t rot, uint32_t ncols_pad, int shamir,
+                              const FieldFmt& f, uint8_t* planes, cudaStream_t st);
 void launch_synth_records(SeedKey key, uint64_t first, uint64_t count, uint32_t l, double density,
                           uint64_t* codes, uint64_t* masks, cudaStream_t st);
-void launch_deal(SeedKey key, uint64_t first_record, uint64_t nrec, uint32_t l, int shamir,
+void launch_deal(SeedKey key, uint64_t first_record, uint64_t nrec, uint32_t l, int shamir, int variant,
                  const uint64_t* codes, const uint64_t* masks, uint8_t* o1, uint8_t* o2,
                  uint8_t* o3, cudaStream_t st);
 
@@ -43,27 +66,32 @@ struct GemmArgs {
   uint32_t s_pad;     // rows per A plane
   uint32_t nb_rows;   // rows per B plane (ncols_pad)
   uint32_t nkb_seg;   // k-blocks per K segment (l_pad / 128)
-  uint32_t nseg;      // 1 (Shamir) or 2 (replicated [x_p | x_{p-1}])
+  uint32_t nseg;      // 1 (Shamir, public bits) or 2 (replicated [x_p | x_{p-1}])
   uint32_t rep;
+  uint32_t nprob;     // 3 (one per party) or 1 (public mask popcount)
+  uint32_t limbs;     // 1 (0/1 bits), 2 (Z_2^16) or 4 (Z_2^32)
   uint32_t s_valid;   // rows written (relative to row0)
   uint32_t row0;      // first DB row of this launch (multiple of 256)
   uint32_t col0;      // first B row of this launch (chunk start column)
   uint32_t ncols;     // columns written (from col0)
-  uint16_t* out;      // [6][ncols * out_cstride]
+  void* out;          // [nprob][ncols * out_cstride], u16 (limbs <= 2) or u32 (limbs = 4)
   uint64_t out_pstride;
   uint32_t out_cstride;
 };
+// N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
+inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }
 // Encodes the TMA map for a [rows][k_pad] u8 plane stack with a box of
-// (128 bytes, box_rows) and 128B swizzle.
+// (128 bytes, box_rows) and 128B swizzle.  A maps use 128-row boxes; B maps
+// gemm_bn(limbs) / 2 (each CTA of the pair stages half the tile's columns).
 int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad,
                     uint32_t box_rows);
-void launch_gemm(const CUtensorMap& a_lo, const CUtensorMap& a_hi, const CUtensorMap& b_lo,
-                 const CUtensorMap& b_hi, const GemmArgs& g, uint32_t m_tiles, uint32_t n_tiles,
-                 cudaStream_t st);
+void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
+                 uint32_t n_tiles, cudaStream_t st);
 
 // ---- inner-batch pairs (pairs.cu)
-void launch_pair_gather(const uint16_t* C, uint32_t ncodes, uint32_t ncols, uint32_t persons, uint32_t rot,
-                        uint16_t* out_hd, uint16_t* out_ml, uint64_t out_pstride, cudaStream_t st);
+// C: [nprob][ncols][ncodes] (elem_bytes each) -> out[p * out_pstride + pair lane]
+void launch_pair_gather(const void* C, int elem_bytes, uint32_t nprob, uint32_t ncodes, uint32_t ncols,
+                        uint32_t persons, uint32_t rot, void* out, uint64_t out_pstride, cudaStream_t st);
 
 // ---- K4 threshold (threshold.cu)
 struct Seg {
@@ -82,14 +110,20 @@ struct ThrArgs {
   const Seg* segs;
   uint32_t nsegs;
   uint64_t ntasks, ngrp, ngblk;
-  const uint16_t* hd[3];
-  const uint16_t* ml[3];
+  int variant;
+  const void* hd[3];     // additive hd dots, u16 (KH = 16) or u32
+  const void* ml[3];     // additive ml dots (u16 / u32), or the public popcount (u16, all three equal)
   uint64_t n, W;
   uint64_t pos[3];
   SeedKey key[3];
   uint32_t a, b;
+  double coef;           // plain-mask: 1 - 2 * match_ratio (plain_threshold, iris.hpp:182-184)
+  // AND-gate layout: gates [0, nlift) are the lift adder at lift_base[k] + g W,
+  // gates [nlift, ngates) the MSB adder at msb_base[k] + (g - nlift) W
+  uint32_t nlift, ngates;
+  uint64_t lift_base[3], msb_base[3];
   // chunk work buffers
-  uint64_t* gate;        // gate randomness, per segment [3*125][nwords]
+  uint64_t* gate;        // gate randomness, per segment [3*ngates][nwords]
   uint16_t* ml_rs;       // [3][cstride] reshared ml
   uint32_t* diff;        // [3][cstride] a*ml32 - b*hd
   uint64_t cstride;
@@ -101,8 +135,8 @@ struct ThrArgs {
   uint64_t nslots;
   uint64_t or_elem_base; // OR-stream (stream id 1) element base of this launch
   // taps (tests), global-lane indexed, may be null
-  uint16_t* tap_rs_hd;
-  uint16_t* tap_rs_ml;
+  uint32_t* tap_rs_hd;
+  uint32_t* tap_rs_ml;
   uint32_t* tap_ml32;
   uint32_t* tap_diff;
   uint8_t* tap_msb;

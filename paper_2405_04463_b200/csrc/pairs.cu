@@ -17,13 +17,14 @@
 
 namespace irisgpu {
 
-// C: [6][ncols][ncodes] u16 (GEMM output, col = code*rot + rotation, row = code)
-__global__ void k_pair_gather(const uint16_t* __restrict__ C, uint32_t ncodes, uint32_t ncols, uint32_t persons,
-                              uint32_t rot, uint64_t npairs, uint16_t* __restrict__ out_hd,
-                              uint16_t* __restrict__ out_ml, uint64_t out_pstride) {
+// C: [nprob][ncols][ncodes] (GEMM output, col = code*rot + rotation, row = code)
+template <typename T>
+__global__ void k_pair_gather(const T* __restrict__ C, uint32_t nprob, uint32_t ncodes, uint32_t ncols,
+                              uint32_t persons, uint32_t rot, uint64_t npairs, T* __restrict__ out,
+                              uint64_t out_pstride) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (tid >= npairs * 6) return;
-  const int prob = (int)(tid / npairs);
+  if (tid >= npairs * nprob) return;
+  const uint32_t prob = (uint32_t)(tid / npairs);
   const uint64_t k = tid % npairs;  // pair lane: ((pidx * 2 + ea) * 2 + eb) * rot + rr
   const uint32_t rr = (uint32_t)(k % rot);
   uint64_t t = k / rot;
@@ -39,18 +40,20 @@ __global__ void k_pair_gather(const uint16_t* __restrict__ C, uint32_t ncodes, u
   const uint32_t j = i + 1 + (uint32_t)pidx;
   const uint64_t col = (uint64_t)(2 * j + eb) * rot + (rot - 1 - rr);
   const uint64_t row = 2 * i + ea;
-  const uint16_t v = C[(uint64_t)prob * ncols * ncodes + col * ncodes + row];
-  uint16_t* out = (prob & 1) ? out_ml : out_hd;
-  out[(uint64_t)(prob >> 1) * out_pstride + k] = v;
+  out[(uint64_t)prob * out_pstride + k] = C[(uint64_t)prob * ncols * ncodes + col * ncodes + row];
 }
 
-void launch_pair_gather(const uint16_t* C, uint32_t ncodes, uint32_t ncols, uint32_t persons, uint32_t rot,
-                        uint16_t* out_hd, uint16_t* out_ml, uint64_t out_pstride, cudaStream_t st) {
+void launch_pair_gather(const void* C, int elem_bytes, uint32_t nprob, uint32_t ncodes, uint32_t ncols,
+                        uint32_t persons, uint32_t rot, void* out, uint64_t out_pstride, cudaStream_t st) {
   if (persons < 2) return;
   const uint64_t npairs = (uint64_t)persons * (persons - 1) / 2 * 4 * rot;
-  const uint64_t threads = npairs * 6;
-  k_pair_gather<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(C, ncodes, ncols, persons, rot, npairs, out_hd,
-                                                                     out_ml, out_pstride);
+  const unsigned blocks = (unsigned)((npairs * nprob + 255) / 256);
+  if (elem_bytes == 4)
+    k_pair_gather<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(C), nprob, ncodes, ncols, persons,
+                                                    rot, npairs, static_cast<uint32_t*>(out), out_pstride);
+  else
+    k_pair_gather<uint16_t><<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(C), nprob, ncodes, ncols, persons,
+                                                    rot, npairs, static_cast<uint16_t*>(out), out_pstride);
 }
 
 }  // namespace irisgpu

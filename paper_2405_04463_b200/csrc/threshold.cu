@@ -29,14 +29,14 @@
 //   k_inject          lane-major: bit_inject<15>, <16>, const-lifted into diff
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
 //                     match-bit shares, fused first MPC-OR level per warp
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace irisgpu {
 
 namespace {
-
-constexpr int kGates = 125;  // 64 lift + 61 msb gates
 
 __device__ __forceinline__ void and3(const uint32_t x[3], const uint32_t y[3], const uint32_t f[3],
                                      uint32_t z[3]) {
@@ -59,10 +59,8 @@ __device__ __forceinline__ uint32_t seg_search(const Seg* segs, uint32_t nsegs, 
 }
 
 __device__ __forceinline__ uint64_t gate_base(const ThrArgs& A, int k, int g) {
-  const uint64_t n = A.n, W = A.W;
-  if (g < 64) return A.pos[k] + 2 * n + (uint64_t)g * W;
-  const uint64_t m = (uint64_t)(g - 64) * W + 64 * W;
-  return A.pos[k] + (k == 0 ? 4 * n : (k == 1 ? 2 * n : 8 * n)) + m;
+  if ((uint32_t)g < A.nlift) return A.lift_base[k] + (uint64_t)g * A.W;
+  return A.msb_base[k] + (uint64_t)(g - (int)A.nlift) * A.W;
 }
 
 // element range [e, e+8) of seed k, stream 0 -> out[0..7] (1 or 2 blocks).
@@ -161,7 +159,7 @@ __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ 
   const uint64_t nb = nw / 8 + 2;  // blocks per (k, g), upper bound
   const uint64_t j = local % nb;
   const uint32_t kg = (uint32_t)(local / nb);
-  const int k = kg / kGates, g = kg % kGates;
+  const int k = kg / A.ngates, g = kg % A.ngates;
   const uint64_t E = gate_base(A, k, g) + sg.w_first;
   const uint64_t b = E / 8 + j;
   if (b > (E + nw - 1) / 8) return;
@@ -182,8 +180,72 @@ __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- reshare
-// thread -> 8-lane group (global lane multiple of 8) of one segment
+namespace {
+
+// 8 lanes [L8, L8+8) of a dot array (u16 or u32) -> v[0..7]; `full`: one aligned vector access
+template <typename T>
+__device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, bool full, uint32_t v[8]) {
+  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
+  if (full) {
+    if (sizeof(T) == 2) {
+      const uint4 x = *reinterpret_cast<const uint4*>(src + src0);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[2 * i] = w[i] & 0xFFFFu;
+        v[2 * i + 1] = w[i] >> 16;
+      }
+    } else {
+      const uint4 x = reinterpret_cast<const uint4*>(src + src0)[0];
+      const uint4 y = reinterpret_cast<const uint4*>(src + src0)[1];
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+      v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t ln = L8 + i;
+    const bool ok = ln >= sg.lane_begin && ln < sg.lane_end;
+    v[i] = ok ? (uint32_t)src[sg.src + (ln - sg.lane_begin)] : 0u;
+  }
+}
+
+// reshare one dot (zero_ring<K>, rep3.hpp:110-112): component k gains F_k and
+// component k+1 loses it -- own_p = z_p + F(seed_p) - F(seed_{p-1})
+__device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, uint32_t v[3][8], uint32_t kmask) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    uint64_t f[8];
+    prf8(A.key[k], A.pos[k] + e_off, f);
+    const int kn = (k + 1) % 3;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[k][i] += (uint32_t)f[i];
+      v[kn][i] -= (uint32_t)f[i];
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[p][i] &= kmask;
+}
+
+}  // namespace
+
+// thread -> 8-lane group (global lane multiple of 8) of one segment.
+// reshare_pair<KH, KM> (engine.cpp:80-106: hd lanes at stream offset 0, ml at
+// n) followed by the comparison input:
+//   mpc-lift   : ml_rs = ml (u16, lifted later), diff = a ml - b hd (partial)
+//   const-lift : diff = a ml32 - const_lift(hd, b)      (engine.hpp:94-120)
+//   no-lift    : diff = a ml32 - b hd32
+//   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
+template <int V>
 __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs A) {
+  using HT = typename std::conditional<V == kNoLift, uint32_t, uint16_t>::type;
+  using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
+  constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
+  constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (tid >= A.ngrp) return;
   const uint32_t si = seg_search(A.segs, A.nsegs, tid, [](const Seg& s) { return s.grp_begin; });
@@ -191,86 +253,70 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
   const uint64_t L8 = (sg.lane_begin / 8 + (tid - sg.grp_begin)) * 8;
   const uint64_t src0 = sg.src + (L8 - sg.lane_begin);  // valid only when `full`
   bool full = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
+  const HT* hd[3];
+  const MT* ml[3];
 #pragma unroll
-  for (int p = 0; p < 3; ++p)  // 16-byte alignment of every vector access
-    full = full && ((reinterpret_cast<uintptr_t>(A.hd[p] + src0) | reinterpret_cast<uintptr_t>(A.ml[p] + src0) |
-                     reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) |
+  for (int p = 0; p < 3; ++p) {
+    hd[p] = static_cast<const HT*>(A.hd[p]);
+    ml[p] = static_cast<const MT*>(A.ml[p]);
+    // 16-byte alignment of every vector access
+    full = full && ((reinterpret_cast<uintptr_t>(hd[p] + src0) | reinterpret_cast<uintptr_t>(ml[p] + src0) |
                      reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0)) & 15) == 0;
-  // two passes with one 3x8 state each: ml (stream offset n) then hd (offset 0)
-  uint32_t ml16[3][8];
+    if (V == kMpcLift) full = full && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) & 15) == 0;
+  }
+  uint32_t h[3][8], m[3][8];
 #pragma unroll
-  for (int part = 0; part < 2; ++part) {
-    const uint16_t* const* srcs = part == 0 ? A.ml : A.hd;
-    uint32_t v[3][8];
-    if (full) {
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const uint4 x = *reinterpret_cast<const uint4*>(srcs[p] + src0);
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          v[p][2 * i] = w[i] & 0xFFFFu;
-          v[p][2 * i + 1] = w[i] >> 16;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint64_t ln = L8 + i;
-        const bool ok = ln >= sg.lane_begin && ln < sg.lane_end;
-        const uint64_t src = sg.src + (ln - sg.lane_begin);
-#pragma unroll
-        for (int p = 0; p < 3; ++p) v[p][i] = ok ? srcs[p][src] : 0u;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      uint64_t f[8];
-      prf8(A.key[k], A.pos[k] + (part == 0 ? A.n : 0) + L8, f);
-      const int kn = (k + 1) % 3;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[k][i] += (uint32_t)f[i];
-        v[kn][i] -= (uint32_t)f[i];
-      }
-    }
-    if (part == 0) {
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ml16[p][i] = v[p][i] & 0xFFFFu;
-      continue;
-    }
-    if (full) {
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        uint32_t mw[4], dw[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mw[i] = ml16[p][2 * i] | (ml16[p][2 * i + 1] << 16);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dw[i] = A.a * ml16[p][i] - A.b * (v[p][i] & 0xFFFFu);
-        *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-        uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
-        dd[0] = make_uint4(dw[0], dw[1], dw[2], dw[3]);
-        dd[1] = make_uint4(dw[4], dw[5], dw[6], dw[7]);
-      }
-      continue;
-    }
+  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, h[p]);
+  reshare8(A, L8, h, HM);
+  uint32_t d[3][8];
+  if (V == kPlainMask) {
+    // m[0] = public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
+    load8<MT>(ml[0], sg, L8, full, m[0]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint64_t ln = L8 + i;
-      if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
-      const uint64_t src = sg.src + (ln - sg.lane_begin);
+      const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)m[0][i]));
+      d[0][i] = (t - h[0][i]) & 0xFFFFu;
+      d[1][i] = (0u - h[1][i]) & 0xFFFFu;
+      d[2][i] = (0u - h[2][i]) & 0xFFFFu;
+      m[0][i] = m[1][i] = m[2][i] = 0u;
+    }
+  } else {
 #pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const uint32_t m16 = ml16[p][i], h16 = v[p][i] & 0xFFFFu;
-        A.ml_rs[p * A.cstride + src] = (uint16_t)m16;
-        A.diff[p * A.cstride + src] = A.a * m16 - A.b * h16;
-        if (A.tap_rs_hd) {
-          A.tap_rs_hd[p * A.n + ln] = (uint16_t)h16;
-          A.tap_rs_ml[p * A.n + ln] = (uint16_t)m16;
-          A.tap_ml32[p * A.n + ln] = m16;
-        }
+    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], sg, L8, full, m[p]);
+    reshare8(A, A.n + L8, m, MM);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[p][i] = A.a * m[p][i] - A.b * h[p][i];
+  }
+  if (full) {
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      if (V == kMpcLift) {
+        uint32_t mw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mw[i] = m[p][2 * i] | (m[p][2 * i + 1] << 16);
+        *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+      }
+      uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
+      dd[0] = make_uint4(d[p][0], d[p][1], d[p][2], d[p][3]);
+      dd[1] = make_uint4(d[p][4], d[p][5], d[p][6], d[p][7]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t ln = L8 + i;
+    if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
+    const uint64_t src = sg.src + (ln - sg.lane_begin);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      if (V == kMpcLift) A.ml_rs[p * A.cstride + src] = (uint16_t)m[p][i];
+      A.diff[p * A.cstride + src] = d[p][i];
+      if (A.tap_rs_hd) {
+        A.tap_rs_hd[p * A.n + ln] = h[p][i];
+        A.tap_rs_ml[p * A.n + ln] = m[p][i];
+        A.tap_ml32[p * A.n + ln] = m[p][i];
       }
     }
   }
@@ -310,7 +356,7 @@ __device__ __forceinline__ void gate_rand(const ThrArgs& A, const Seg& sg, uint6
   const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
   const uint64_t* G = A.gate + sg.g_off + (w64 - sg.w_first);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) f[k] = (uint32_t)(__ldg(G + (uint64_t)(k * kGates + g) * nw) >> (32 * half));
+  for (int k = 0; k < 3; ++k) f[k] = (uint32_t)(__ldg(G + (uint64_t)(k * A.ngates + g) * nw) >> (32 * half));
 }
 
 // bit_extract_sum for one index M over summand rows R[c][j] (component c of
@@ -541,7 +587,9 @@ __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t 
 
 }  // namespace
 
-// warp -> 1024-lane task: msb<32> of diff, outputs, fused first OR level
+// warp -> 1024-lane task: msb<KC> of diff (circuits.hpp:300-306), outputs,
+// fused first OR level.  Gates: FA j -> nlift + j, chain t -> nlift + KC - 1 + (t - 1).
+template <int KC>
 __global__ void __launch_bounds__(128) k_msb(const __grid_constant__ ThrArgs A) {
   const uint64_t task = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -579,7 +627,9 @@ __global__ void __launch_bounds__(128) k_msb(const __grid_constant__ ThrArgs A) 
     transpose32(D[p]);
   }
   uint32_t bit[3] = {0u, 0u, 0u};
-  if (vm) extract_bit<31, 32>(A, t.sg, Lt / 64, lane & 1, D, 64, 95, 1, 124, bit);
+  // rows >= KC of the transposed diff are never read (extract_bit<KC - 1, 32> touches rows <= KC - 1)
+  const int nl = (int)A.nlift;
+  if (vm) extract_bit<KC - 1, 32>(A, t.sg, Lt / 64, lane & 1, D, nl, nl + KC - 1, 1, nl + 2 * KC - 4, bit);
 #pragma unroll
   for (int c = 0; c < 3; ++c) bit[c] &= vm;
   if (A.tap_msb) {
@@ -603,19 +653,30 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   prof_end(h, "k_gate_keystream", st);
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
-  k_reshare<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
+  const unsigned rb = (unsigned)((a.ngrp + 255) / 256);
+  switch (a.variant) {
+    case kPlainMask: k_reshare<kPlainMask><<<rb, 256, 0, st>>>(a); break;
+    case kMpcLift: k_reshare<kMpcLift><<<rb, 256, 0, st>>>(a); break;
+    case kConstLift: k_reshare<kConstLift><<<rb, 256, 0, st>>>(a); break;
+    default: k_reshare<kNoLift><<<rb, 256, 0, st>>>(a); break;
+  }
   prof_end(h, "k_reshare", st);
   debug_check("k_reshare", st);
+  if (a.variant == kMpcLift) {
+    h = prof_begin(st);
+    k_lift<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+    prof_end(h, "k_lift", st);
+    debug_check("k_lift", st);
+    h = prof_begin(st);
+    k_inject<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
+    prof_end(h, "k_inject", st);
+    debug_check("k_inject", st);
+  }
   h = prof_begin(st);
-  k_lift<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
-  prof_end(h, "k_lift", st);
-  debug_check("k_lift", st);
-  h = prof_begin(st);
-  k_inject<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
-  prof_end(h, "k_inject", st);
-  debug_check("k_inject", st);
-  h = prof_begin(st);
-  k_msb<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+  if (a.variant == kPlainMask)
+    k_msb<16><<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+  else
+    k_msb<32><<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
   prof_end(h, "k_msb", st);
   debug_check("k_msb", st);
 }

@@ -32,6 +32,10 @@ def test_pure_host_entry_points():
     assert bytes(P.seeds_from_master(7)) == bytes(O.party_seeds(7))
     assert P.record_bytes(P.SHAMIR, 12800) == O.record_bytes(O.SHAMIR, 12800)
     assert P.record_bytes(P.REPLICATED, 64) == O.record_bytes(O.REPLICATED, 64)
+    for var in (P.PLAIN_MASK, P.MPC_LIFT, P.CONST_LIFT, P.NO_LIFT):
+        for be in (P.SHAMIR, P.REPLICATED):
+            for l in (8, 64, 12800):
+                assert P.record_bytes(be, l, var) == O.record_bytes(be, l, var), (var, be, l)
     for persons, s, r, m in [(16, 100_000, 31, False), (1, 10, 1, True), (3, 0, 31, False)]:
         assert P.lane_count(persons, s, r, m) == O.lib().orc_lane_count(persons, s, r, 1 if m else 0)
     for ratio in (0.375, 0.3, 0.2, 0.0, 0.5):
@@ -46,6 +50,16 @@ def test_bounds_rejected_before_device():
         P.Session(P.EngineConfig(backend=P.SHAMIR, l=64, rotations=2), master_seed=1)
     with pytest.raises(P.BoundsError):
         P.Session(P.EngineConfig(backend=P.REPLICATED, l=12), master_seed=1)
+    # plain-mask: check_public_mask_bound(l, 16) needs l < 2^14 (iris.hpp:189-194)
+    with pytest.raises(P.BoundsError):
+        P.Session(P.EngineConfig(backend=P.SHAMIR, l=16384, rotations=1, variant=P.PLAIN_MASK), master_seed=1)
+    # shared-mask variants fix m = 16 (engine.cpp:26)
+    with pytest.raises(P.BoundsError):
+        P.Session(P.EngineConfig(backend=P.SHAMIR, l=64, rotations=1, variant=P.NO_LIFT, m=15), master_seed=1)
+    # oracle agrees on the same configs
+    from oracle import pyoracle as O
+    assert O.lib().orc_validate(O.make_config(O.SHAMIR, 16384, 0.375, 1, variant=O.PLAIN_MASK)) == 4
+    assert O.lib().orc_validate(O.make_config(O.SHAMIR, 16376, 0.375, 1, variant=O.PLAIN_MASK)) == 0
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is not None and False, reason="")

@@ -26,7 +26,9 @@ GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_vec
 
 
 def _sha(a):
-    return hashlib.sha256(np.ascontiguousarray(a).astype("<u2").tobytes()).hexdigest()
+    """oracle/gen_golden.sha: little-endian bytes at the array's ring width."""
+    dt = {np.dtype(np.uint16): "<u2", np.dtype(np.uint32): "<u4", np.dtype(np.int64): "<i8"}[a.dtype]
+    return hashlib.sha256(np.ascontiguousarray(a).astype(dt).tobytes()).hexdigest()
 
 
 def _inputs(l, s, persons, seed, membership, planted, density=0.85):
@@ -40,8 +42,8 @@ def _inputs(l, s, persons, seed, membership, planted, density=0.85):
     return dc, dm, qc, qm
 
 
-def _gpu(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership):
-    cfg = P.EngineConfig(backend=be, l=l, match_ratio=ratio, rotations=r, debug_rows=True)
+def _gpu(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership, variant=P.MPC_LIFT):
+    cfg = P.EngineConfig(backend=be, l=l, match_ratio=ratio, rotations=r, debug_rows=True, variant=variant)
     m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, membership=membership,
                                 want_rows=True, taps=True)
     n = P.lane_count(persons, dc.shape[0], r, membership)
@@ -55,16 +57,20 @@ def _gpu(be, l, ratio, r, seed, dc, dm, qc, qm, persons, membership):
 @pytest.mark.parametrize("idx", range(len(GOLD["cases"])))
 def test_golden_cases(idx):
     c = GOLD["cases"][idx]
+    var = c.get("variant", P.MPC_LIFT)
     dc, dm, qc, qm = _inputs(c["l"], c["s"], c["persons"], c["seed"], c["membership"], c["planted"])
     m, sess, taps, n = _gpu(c["backend"], c["l"], c["ratio"], c["rotations"], c["seed"], dc, dm, qc, qm,
-                            c["persons"], c["membership"])
+                            c["persons"], c["membership"], var)
     assert n == c["lanes"]
     assert [int(x) for x in m] == c["person_match"]                                   # L5
     assert np.packbits(sess.row_bits[:n], bitorder="little").tobytes().hex() == c["row_bits_hex"]  # L4
     assert _sha(taps["dot_hd"]) == c["sha256"]["dot_hd"]                              # L1
-    assert _sha(taps["dot_ml"]) == c["sha256"]["dot_ml"]
     assert _sha(taps["rs_hd"]) == c["sha256"]["rs_hd"]                                # L2
-    assert _sha(taps["rs_ml"]) == c["sha256"]["rs_ml"]
+    if P.VARIANT_WIDTHS[var][1]:
+        assert _sha(taps["dot_ml"]) == c["sha256"]["dot_ml"]
+        assert _sha(taps["rs_ml"]) == c["sha256"]["rs_ml"]
+    else:
+        assert _sha(taps["dot_ml"].astype(np.int64)) == c["sha256"]["public_ml"]
     st = sess.last_stats
     for p in range(3):
         assert st.party(p) == c["stats"][p]
@@ -93,6 +99,86 @@ def test_shares_through_msb_match_oracle(be, l, s, persons, r, seed):
     rec_hd = taps["rs_hd"].astype(np.uint32).sum(0) & 0xFFFF
     np.testing.assert_array_equal(rec_ml, ref.rs_ml.astype(np.uint32).sum(0) & 0xFFFF)
     np.testing.assert_array_equal(rec_hd, ref.rs_hd.astype(np.uint32).sum(0) & 0xFFFF)
+
+
+@pytest.mark.parametrize("var", [P.PLAIN_MASK, P.CONST_LIFT, P.NO_LIFT])
+@pytest.mark.parametrize("be,l,s,persons,r,seed", [
+    (O.SHAMIR, 12800, 300, 3, 31, 41),
+    (O.REPLICATED, 12800, 260, 2, 31, 42),
+    (O.SHAMIR, 256, 1031, 2, 5, 43),
+    (O.REPLICATED, 128, 1, 4, 31, 44),      # one DB row
+    (O.SHAMIR, 128, 0, 3, 3, 45),           # empty DB, pairs only
+])
+def test_variant_shares_through_msb_match_oracle(var, be, l, s, persons, r, seed):
+    """f1: plain-mask / const-lift / no-lift, every share through the MSB."""
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    m, sess, taps, n = _gpu(be, l, 0.375, r, seed, dc, dm, qc, qm, persons, False, var)
+    ref = O.run_local(O.make_config(be, l, 0.375, r, debug_rows=True, variant=var), seed, dc, dm, qc, qm,
+                      persons, want_all=True)
+    for k in ("dot_hd", "rs_hd", "rs_ml", "ml32", "diff", "msb"):
+        np.testing.assert_array_equal(taps[k], getattr(ref, k), err_msg=k)
+    if P.VARIANT_WIDTHS[var][1]:
+        np.testing.assert_array_equal(taps["dot_ml"], ref.dot_ml)
+    else:
+        np.testing.assert_array_equal(taps["dot_ml"], ref.public_ml)
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+    np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
+    st = sess.last_stats
+    for p in range(3):
+        assert st.party(p) == ref.stats[p]
+
+
+@pytest.mark.parametrize("var", [P.PLAIN_MASK, P.CONST_LIFT, P.NO_LIFT])
+@pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])
+def test_variant_membership(var, be):
+    l, s = 64, 300
+    dc, dm, qc, qm = _inputs(l, s, 1, 78, True, True, 0.8)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=1, debug_rows=True, variant=var)
+    m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, 78, membership=True, want_rows=True)
+    ref = O.run_local(O.make_config(be, l, 0.375, 1, True, variant=var), 78, dc, dm, qc, qm, 1, membership=True)
+    assert m[0] == ref.person_match[0] == 1
+    np.testing.assert_array_equal(sess.row_bits[:s], ref.row_bits)
+
+
+@pytest.mark.parametrize("var", [P.PLAIN_MASK, P.CONST_LIFT, P.NO_LIFT])
+@pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])
+def test_variant_device_dealer(var, be):
+    l, n = 256, 7
+    sess = P.Session(P.EngineConfig(backend=be, l=l, variant=var), master_seed=1)
+    rng = O.Rng(5)
+    oc, om = O.records(rng, l, n, 0.9)
+    codes = torch.from_numpy(oc.view(np.int64)).cuda()
+    masks = torch.from_numpy(om.view(np.int64)).cuda()
+    outs = [torch.empty(n * sess.rec, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    sess.deal_payload(7, 1, 0, codes, masks, outs)
+    ref = O.deal(be, l, oc, om, O.Rng(sub=(7, 1)), variant=var)
+    for a, b in zip(outs, ref):
+        np.testing.assert_array_equal(a.cpu().numpy(), b)
+
+
+@pytest.mark.parametrize("var", [P.MPC_LIFT, P.NO_LIFT])
+def test_accumulator_wraparound_all_ones_shares(var):
+    """Replicated all-0xFF payloads are consistent shares whose limb products
+    overflow the s32 TMEM accumulators (K = 2l = 25600: 2 x 25600 x 255^2 > 2^31);
+    the dots are only needed mod 2^K, so the wrap must be exact."""
+    l, s, persons, r, seed = 12800, 256, 1, 31, 61
+    rec = O.record_bytes(O.REPLICATED, l, var)
+    db = [np.full(s * rec, 0xFF, np.uint8) for _ in range(3)]
+    q = [np.full(2 * persons * rec, 0xFF, np.uint8) for _ in range(3)]
+    seeds = O.party_seeds(seed)
+    cfg = P.EngineConfig(backend=O.REPLICATED, l=l, rotations=r, debug_rows=True, variant=var)
+    sess = P.Session(cfg, seeds=seeds)
+    sess.load_db(db, s)
+    sess.enable_taps(True)
+    m = sess.batch_query(q, persons, want_rows=True)
+    n = P.lane_count(persons, s, r)
+    ref = O.query(O.make_config(O.REPLICATED, l, 0.375, r, debug_rows=True, variant=var), seeds, db, s, q,
+                  persons, want_all=True)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_HD, n), ref.dot_hd)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_ML, n), ref.dot_ml)
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+    np.testing.assert_array_equal(m, ref.person_match)
 
 
 @pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])

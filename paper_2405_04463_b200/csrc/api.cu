@@ -371,7 +371,11 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t rank = c->cfg.shard_rank;
   const uint64_t s_loc = c->s;
   const uint64_t row_off = c->cfg.db_row_offset;
-  cudaStream_t st = c->st, st2 = c->st2;
+  static const bool serial = [] {
+    const char* e = std::getenv("IRISMPC_SERIAL");  // profiling hook: no GEMM/threshold overlap
+    return e && e[0] == '1';
+  }();
+  cudaStream_t st = c->st, st2 = serial ? c->st : c->st2;
   uint64_t launches = 0;
 
   CK(c, cudaEventRecord(c->ev[0], st));

@@ -63,86 +63,79 @@ __device__ __forceinline__ uint64_t gate_base(const ThrArgs& A, int k, int g) {
   return A.msb_base[k] + (uint64_t)(g - (int)A.nlift) * A.W;
 }
 
-// element range [e, e+8) of seed k, stream 0 -> out[0..7] (1 or 2 blocks).
-// e % 8 is uniform across a launch, so the realignment is a uniform shift loop
-// over a static register window (no dynamically indexed local arrays).
-__device__ __forceinline__ void prf8(const SeedKey& key, uint64_t e, uint64_t out[8]) {
-  uint32_t blk[16];
-  const uint64_t b = e / 8;
-  const int r = (int)(e % 8);
-  chacha12_block(key, b, 0, blk);
+// ---- warp-cooperative stream windows.  The lane-major kernels map 31
+// consecutive 8-lane groups to a warp (lane 31 only helps).  A lane's window
+// of 8 * NB elements starting at e spans NB blocks + 1 when e % 8 != 0
+// (warp-uniform: e = stream offset + 8 * group); the extra block is the next
+// lane's first block and arrives by shuffle, so every ChaCha block is
+// computed once instead of up to twice.  Only the low 32 bits of each u64
+// element are consumed (Ring<K <= 32> draws).
+template <int NB, int R>
+__device__ __forceinline__ void take_window(const uint32_t (&w)[8 * (NB + 1)], uint32_t (&out)[8 * NB]) {
 #pragma unroll
-  for (int w = 0; w < 8; ++w) out[w] = chacha_word(blk, w);
-  if (r == 0) return;
-  uint64_t hi[8];
-  chacha12_block(key, b + 1, 0, blk);
-#pragma unroll
-  for (int w = 0; w < 8; ++w) hi[w] = chacha_word(blk, w);
-  for (int s = 0; s < r; ++s) {
-#pragma unroll
-    for (int w = 0; w < 7; ++w) out[w] = out[w + 1];
-    out[7] = hi[0];
-#pragma unroll
-    for (int w = 0; w < 7; ++w) hi[w] = hi[w + 1];
-  }
+  for (int i = 0; i < 8 * NB; ++i) out[i] = w[R + i];
 }
 
-// element range [e, e+24) of seed k -> out[0..23] (3 or 4 blocks)
-__device__ __forceinline__ void prf24(const SeedKey& key, uint64_t e, uint64_t out[24]) {
-  uint32_t blk[16];
+// next_contig: lane + 1 owns the window starting at e + 8 * NB (else this lane
+// computes the extra block itself -- segment boundaries, the last group).
+// Must be called by all 32 lanes in convergent code.
+template <int NB>
+__device__ __forceinline__ void prf_window(const SeedKey& key, uint64_t e, bool next_contig,
+                                           uint32_t (&out)[8 * NB]) {
+  uint32_t w[8 * (NB + 1)];
   const uint64_t b = e / 8;
-  const int r = (int)(e % 8);
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    chacha12_block(key, b + q, 0, blk);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) out[8 * q + w] = chacha_word(blk, w);
-  }
-  if (r == 0) return;
-  uint64_t hi[8];
-  chacha12_block(key, b + 3, 0, blk);
-#pragma unroll
-  for (int w = 0; w < 8; ++w) hi[w] = chacha_word(blk, w);
-  for (int s = 0; s < r; ++s) {
-#pragma unroll
-    for (int w = 0; w < 23; ++w) out[w] = out[w + 1];
-    out[23] = hi[0];
-#pragma unroll
-    for (int w = 0; w < 7; ++w) hi[w] = hi[w + 1];
-  }
-}
-
-// low 32 bits of elements e + 3i, i = 0..7 (the bit-inject c3 draws; the two
-// OT pads in between are consumed but unused).  e % 8 is launch-uniform, so the
-// switch picks one statically indexed extraction for the whole launch.
-template <int R>
-__device__ __forceinline__ void every3_r(const SeedKey& key, uint64_t b, uint32_t out[8]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    constexpr int kLast = (R + 21) / 8;  // block holding element e + 21
-    if (q > kLast) break;
+  for (int q = 0; q < NB; ++q) {
     uint32_t blk[16];
     chacha12_block(key, b + q, 0, blk);
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int pos = 8 * q + w - R;  // offset from e
-      if (pos >= 0 && pos <= 21 && pos % 3 == 0) out[pos / 3] = blk[2 * w];
-    }
+    for (int i = 0; i < 8; ++i) w[8 * q + i] = blk[2 * i];
+  }
+  const int r = (int)(e % 8);
+  if (r == 0) {
+#pragma unroll
+    for (int i = 0; i < 8 * NB; ++i) out[i] = w[i];
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[8 * NB + i] = __shfl_down_sync(0xFFFFFFFFu, w[i], 1);
+  if (!next_contig) {
+    uint32_t blk[16];
+    chacha12_block(key, b + NB, 0, blk);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[8 * NB + i] = blk[2 * i];
+  }
+  switch (r) {
+    case 1: take_window<NB, 1>(w, out); break;
+    case 2: take_window<NB, 2>(w, out); break;
+    case 3: take_window<NB, 3>(w, out); break;
+    case 4: take_window<NB, 4>(w, out); break;
+    case 5: take_window<NB, 5>(w, out); break;
+    case 6: take_window<NB, 6>(w, out); break;
+    default: take_window<NB, 7>(w, out); break;
   }
 }
 
-__device__ __forceinline__ void prf_every3(const SeedKey& key, uint64_t e, uint32_t out[8]) {
-  const uint64_t b = e / 8;
-  switch ((int)(e % 8)) {
-    case 0: every3_r<0>(key, b, out); break;
-    case 1: every3_r<1>(key, b, out); break;
-    case 2: every3_r<2>(key, b, out); break;
-    case 3: every3_r<3>(key, b, out); break;
-    case 4: every3_r<4>(key, b, out); break;
-    case 5: every3_r<5>(key, b, out); break;
-    case 6: every3_r<6>(key, b, out); break;
-    default: every3_r<7>(key, b, out); break;
-  }
+// lane -> 8-lane group of a lane-major kernel (31 groups per warp)
+struct GroupCtx {
+  uint64_t L8;       // first global lane of the group
+  bool mine;         // this lane owns a real group (lane < 31, group < ngrp)
+  bool next_contig;  // lane + 1 owns the group at L8 + 8
+  const Seg* sg;
+};
+
+__device__ __forceinline__ GroupCtx group_ctx(const ThrArgs& A, uint64_t gtid) {
+  GroupCtx c;
+  const int lane = (int)(gtid & 31);
+  const uint64_t gi = (gtid >> 5) * 31 + lane;
+  c.mine = lane < 31 && gi < A.ngrp;
+  const uint64_t gq = gi < A.ngrp ? gi : A.ngrp - 1;
+  const uint32_t si = seg_search(A.segs, A.nsegs, gq, [](const Seg& s) { return s.grp_begin; });
+  c.sg = &A.segs[si];
+  c.L8 = (c.sg->lane_begin / 8 + (gq - c.sg->grp_begin)) * 8;
+  const uint64_t Ln = __shfl_down_sync(0xFFFFFFFFu, c.L8, 1);
+  c.next_contig = lane == 31 || (Ln == c.L8 + 8 && gi + 1 < A.ngrp);
+  return c;
 }
 
 }  // namespace
@@ -184,7 +177,7 @@ namespace {
 
 // 8 lanes [L8, L8+8) of a dot array (u16 or u32) -> v[0..7]; `full`: one aligned vector access
 template <typename T>
-__device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, bool full, uint32_t v[8]) {
+__device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, bool full, bool mine, uint32_t v[8]) {
   const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
   if (full) {
     if (sizeof(T) == 2) {
@@ -206,23 +199,24 @@ __device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, 
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint64_t ln = L8 + i;
-    const bool ok = ln >= sg.lane_begin && ln < sg.lane_end;
+    const bool ok = mine && ln >= sg.lane_begin && ln < sg.lane_end;
     v[i] = ok ? (uint32_t)src[sg.src + (ln - sg.lane_begin)] : 0u;
   }
 }
 
 // reshare one dot (zero_ring<K>, rep3.hpp:110-112): component k gains F_k and
 // component k+1 loses it -- own_p = z_p + F(seed_p) - F(seed_{p-1})
-__device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, uint32_t v[3][8], uint32_t kmask) {
+__device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, bool next_contig, uint32_t v[3][8],
+                                         uint32_t kmask) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    uint64_t f[8];
-    prf8(A.key[k], A.pos[k] + e_off, f);
+    uint32_t f[8];
+    prf_window<1>(A.key[k], A.pos[k] + e_off, next_contig, f);
     const int kn = (k + 1) % 3;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      v[k][i] += (uint32_t)f[i];
-      v[kn][i] -= (uint32_t)f[i];
+      v[k][i] += f[i];
+      v[kn][i] -= f[i];
     }
   }
 #pragma unroll
@@ -246,13 +240,13 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (tid >= A.ngrp) return;
-  const uint32_t si = seg_search(A.segs, A.nsegs, tid, [](const Seg& s) { return s.grp_begin; });
-  const Seg& sg = A.segs[si];
-  const uint64_t L8 = (sg.lane_begin / 8 + (tid - sg.grp_begin)) * 8;
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if ((gtid >> 5) * 31 >= A.ngrp) return;  // whole warp past the end
+  const GroupCtx gc = group_ctx(A, gtid);
+  const Seg& sg = *gc.sg;
+  const uint64_t L8 = gc.L8;
   const uint64_t src0 = sg.src + (L8 - sg.lane_begin);  // valid only when `full`
-  bool full = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
+  bool full = gc.mine && L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
   const HT* hd[3];
   const MT* ml[3];
 #pragma unroll
@@ -266,12 +260,12 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
   }
   uint32_t h[3][8], m[3][8];
 #pragma unroll
-  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, h[p]);
-  reshare8(A, L8, h, HM);
+  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, gc.mine, h[p]);
+  reshare8(A, L8, gc.next_contig, h, HM);
   uint32_t d[3][8];
   if (V == kPlainMask) {
     // m[0] = public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
-    load8<MT>(ml[0], sg, L8, full, m[0]);
+    load8<MT>(ml[0], sg, L8, full, gc.mine, m[0]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)m[0][i]));
@@ -282,13 +276,14 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
     }
   } else {
 #pragma unroll
-    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], sg, L8, full, m[p]);
-    reshare8(A, A.n + L8, m, MM);
+    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], sg, L8, full, gc.mine, m[p]);
+    reshare8(A, A.n + L8, gc.next_contig, m, MM);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
       for (int i = 0; i < 8; ++i) d[p][i] = A.a * m[p][i] - A.b * h[p][i];
   }
+  if (!gc.mine) return;
   if (full) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
@@ -464,17 +459,20 @@ __global__ void __launch_bounds__(128) k_lift(const __grid_constant__ ThrArgs A)
 
 // thread -> 8-lane group: bit_inject<15>(bit17) then bit_inject<16>(bit16)
 __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs A) {
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (tid >= A.ngrp) return;
-  const uint32_t si = seg_search(A.segs, A.nsegs, tid, [](const Seg& s) { return s.grp_begin; });
-  const Seg& sg = A.segs[si];
-  const uint64_t L8 = (sg.lane_begin / 8 + (tid - sg.grp_begin)) * 8;
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if ((gtid >> 5) * 31 >= A.ngrp) return;  // whole warp past the end
+  const GroupCtx gc = group_ctx(A, gtid);
+  const Seg& sg = *gc.sg;
+  const uint64_t L8 = gc.L8;
   // injected bits: the k_lift thread that owns these lanes
   const uint64_t task = sg.task_begin + (L8 / 1024 - sg.q_first);
   const uint64_t o = task * 32 + (L8 % 1024) / 32;
   const int sh = (int)(L8 % 32);
-  const uint32_t x17 = (A.bits[3 * A.nbits + o] ^ A.bits[4 * A.nbits + o] ^ A.bits[5 * A.nbits + o]) >> sh;
-  const uint32_t x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
+  uint32_t x17 = 0, x16 = 0;
+  if (gc.mine) {
+    x17 = (A.bits[3 * A.nbits + o] ^ A.bits[4 * A.nbits + o] ^ A.bits[5 * A.nbits + o]) >> sh;
+    x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
+  }
   uint32_t d[3][8];
   const uint64_t n = A.n, W = A.W;
 #pragma unroll
@@ -488,20 +486,20 @@ __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs 
     const int shift = which == 0 ? 17 : 16;
     const uint64_t o1 = A.pos[0] + 2 * n + 64 * W + (which == 0 ? 0 : n) + L8;
     const uint64_t o3 = A.pos[2] + 2 * n + 64 * W + (which == 0 ? 0 : 3 * n) + 3 * L8;
-    uint64_t c1[8];
-    uint32_t c3[8];
-    prf8(A.key[0], o1, c1);
-    prf_every3(A.key[2], o3, c3);
+    uint32_t c1[8], w3[24];
+    prf_window<1>(A.key[0], o1, gc.next_contig, c1);
+    prf_window<3>(A.key[2], o3, gc.next_contig, w3);  // (c3, w0, w1) per lane; only c3 is used
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint32_t b1 = (uint32_t)c1[i] & mask;
-      const uint32_t b3 = c3[i] & mask;
+      const uint32_t b1 = c1[i] & mask;
+      const uint32_t b3 = w3[3 * i] & mask;
       const uint32_t b2 = (((x >> i) & 1u) - b1 - b3) & mask;
       d[0][i] += b1 << shift;
       d[1][i] += b2 << shift;
       d[2][i] += b3 << shift;
     }
   }
+  if (!gc.mine) return;
   const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
   bool vec = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_ml32;
 #pragma unroll
@@ -653,7 +651,9 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   prof_end(h, "k_gate_keystream", st);
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
-  const unsigned rb = (unsigned)((a.ngrp + 255) / 256);
+  // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
+  const unsigned grp_blocks = (unsigned)((a.ngrp + 8 * 31 - 1) / (8 * 31));
+  const unsigned rb = grp_blocks;
   switch (a.variant) {
     case kPlainMask: k_reshare<kPlainMask><<<rb, 256, 0, st>>>(a); break;
     case kMpcLift: k_reshare<kMpcLift><<<rb, 256, 0, st>>>(a); break;
@@ -668,7 +668,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    k_inject<<<(unsigned)((a.ngrp + 255) / 256), 256, 0, st>>>(a);
+    k_inject<<<grp_blocks, 256, 0, st>>>(a);
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }

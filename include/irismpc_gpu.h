@@ -152,6 +152,37 @@ int irismpc_gpu_deal_payload(irismpc_gpu_ctx* ctx, uint64_t deal_seed, uint64_t 
 int irismpc_gpu_synth_db(irismpc_gpu_ctx* ctx, uint64_t s, uint64_t rng_seed, uint64_t first,
                          double mask_density, uint64_t deal_seed);
 
+/* ---- share / seed / plaintext files (io.hpp:28-60, src/io.cpp) ----------- */
+/* IRS1 per-party share file: magic "IRS1", version 1, backend u8, variant u8,
+ * party u8, code_k u8, mask_k u8, reserved u16, l u32, s u64, then the row
+ * payload (24-byte header). */
+typedef struct irismpc_gpu_share_header {
+  uint32_t backend, variant, party, l;
+  uint64_t s;
+} irismpc_gpu_share_header;
+/* read_share_file's checks (io.cpp:125-146): magic, version, width fields vs
+ * the variant, file size == 24 + s * record_bytes.  2 on any violation. */
+int irismpc_gpu_read_share_header(const char* path, irismpc_gpu_share_header* out);
+int irismpc_gpu_write_share_file(const char* path, const irismpc_gpu_share_header* h,
+                                 const uint8_t* payload, size_t len);
+/* Session::load_db from the three parties' IRS1 files (party 1, 2, 3),
+ * streamed from disk into HBM (pinned double buffer, H2D overlapped with the
+ * parse).  Backend / variant / l must match the context (ConfigMismatchError
+ * -> 2, like the CLI's share-file check, irismpc_cli.cpp:211-215). */
+int irismpc_gpu_load_db_files(irismpc_gpu_ctx* ctx, const char* const paths[3]);
+/* IRSD seed files (io.cpp:148-170) of parties 1..3 -> seed_1 | seed_2 | seed_3;
+ * each file's prev seed must equal the previous party's own seed (2 if not). */
+int irismpc_gpu_read_seed_files(const char* const paths[3], uint8_t seeds_out[48]);
+int irismpc_gpu_write_seed_file(const char* path, uint32_t party, const uint8_t own[16],
+                                const uint8_t prev[16]);
+/* IRMP plaintext DB (dealer side, io.cpp:74-108): header then packed code bits
+ * of all rows, then mask bits.  Words are LSB-first, (l + 63) / 64 per row. */
+int irismpc_gpu_read_iris_db_header(const char* path, uint32_t* l_out, uint64_t* s_out);
+int irismpc_gpu_read_iris_db(const char* path, uint64_t* codes_out, uint64_t* masks_out,
+                             uint64_t rows_cap);
+int irismpc_gpu_write_iris_db(const char* path, uint32_t l, uint64_t s, const uint64_t* codes,
+                              const uint64_t* masks);
+
 /* ---- debug / parity taps (tests) ------------------------------------------ */
 #define IRISMPC_GPU_TAP_DOT_HD 1  /* [3][n] per-party additive hd dot (L1), u16 (KH = 16) / u32 */
 #define IRISMPC_GPU_TAP_DOT_ML 2  /* [3][n] ml dot u16 / u32; plain-mask: [n] u16 public popcount */

@@ -74,6 +74,28 @@ def inputs(l, s, persons, seed, membership, planted):
     return dc, dm, qc, qm
 
 
+FILES = os.path.join(os.path.dirname(OUT), "files")
+
+
+def gen_files():
+    """Reference-written IRMP / IRSD / IRS1 files (io.cpp) for the file-format tests:
+    the `irismpc share` dealer over a 3-row l=64 DB, seed 9, every variant (Shamir)
+    plus replicated mpc-lift."""
+    os.makedirs(FILES, exist_ok=True)
+    l, s, seed = 64, 3, 9
+    dc, dm = O.records(O.Rng(31), l, s, 0.85)
+    db = os.path.join(FILES, "db.irmp")
+    O.ref_write_iris_db(db, dc, dm, l)
+    out = {"db": "db.irmp", "l": l, "s": s, "records_rng": 31, "seed": seed, "shares": []}
+    for be, var in [(1, 0), (1, 1), (1, 2), (1, 3), (0, 1)]:
+        names = [f"db.b{be}.v{var}.p{p}.irs" for p in (1, 2, 3)]
+        seeds = [f"seeds.b{be}.v{var}.p{p}.irsd" for p in (1, 2, 3)]
+        O.ref_share_files(db, be, var, seed, [os.path.join(FILES, n) for n in names],
+                          [os.path.join(FILES, n) for n in seeds])
+        out["shares"].append({"backend": be, "variant": var, "files": names, "seed_files": seeds})
+    return out
+
+
 def main():
     R = O.ref()
     g = {"generated_by": "oracle/gen_golden.py from oracle/_ref (reference compiled from /root/reference/proj)"}
@@ -177,6 +199,7 @@ def main():
         cases.append(case)
         print(f"case var={var} be={be} l={l} s={s} persons={persons} r={r} lanes={n} match={case['person_match']}")
     g["cases"] = cases
+    g["files"] = gen_files()
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:
         json.dump(g, f, indent=1)

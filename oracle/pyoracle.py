@@ -129,6 +129,9 @@ def ref():
         R.ref_dots_reshare.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint32, u8p, C.POINTER(u8p),
                                        C.c_uint64, C.POINTER(u8p), C.c_uint32, C.c_int,
                                        u32p, u32p, C.POINTER(C.c_int64), u32p, u32p]
+        R.ref_write_iris_db.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, u64p, u64p]
+        R.ref_share_files.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.c_char_p * 3, C.c_char_p * 3]
+        R.ref_read_share_file.argtypes = [C.c_char_p, u32p, u64p, u64p]
         R.ref_bench_prepare.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint32]
         R.ref_bench_prepare.restype = C.c_void_p
         R.ref_bench_step.argtypes = [C.c_void_p, u8p]
@@ -385,3 +388,31 @@ def ref_dots_reshare(backend: int, l: int, rotations: int, seeds, db: list, s: i
     ref_dots_reshare.public_ml = pub[:n].copy() if km == 0 else None
     w = [kh, km or 16, kh, km or 16]
     return [o[: 3 * n].reshape(3, n).astype(_width_dtype(b)) for o, b in zip(outs, w)]
+
+
+def ref_write_iris_db(path: str, codes, masks, l: int):
+    c = np.ascontiguousarray(codes, np.uint64)
+    m = np.ascontiguousarray(masks, np.uint64)
+    rc = ref().ref_write_iris_db(os.fsencode(path), l, c.shape[0], _p(c, u64p), _p(m, u64p))
+    if rc:
+        raise RuntimeError(f"ref_write_iris_db failed with status {rc}")
+
+
+def ref_share_files(db_path: str, backend: int, variant: int, seed: int, share_paths, seed_paths):
+    """The reference `irismpc share` dealer for one variant (IRSD + IRS1 files)."""
+    rc = ref().ref_share_files(os.fsencode(db_path), backend, variant, seed,
+                               (C.c_char_p * 3)(*[os.fsencode(p) for p in share_paths]),
+                               (C.c_char_p * 3)(*[os.fsencode(p) for p in seed_paths]))
+    if rc:
+        raise RuntimeError(f"ref_share_files failed with status {rc}")
+
+
+def ref_read_share_file(path: str):
+    """read_share_file: (backend, variant, party, l, s, payload_len) or the reference's status code."""
+    hdr = np.zeros(4, np.uint32)
+    s = C.c_uint64(0)
+    n = C.c_uint64(0)
+    rc = ref().ref_read_share_file(os.fsencode(path), _p(hdr, u32p), C.byref(s), C.byref(n))
+    if rc:
+        return rc
+    return (*[int(x) for x in hdr], int(s.value), int(n.value))

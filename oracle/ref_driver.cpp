@@ -19,6 +19,7 @@
 #include "irismpc/cluster.hpp"
 #include "irismpc/engine.hpp"
 #include "irismpc/galois.hpp"
+#include "irismpc/io.hpp"
 #include "irismpc/kernels.hpp"
 #include "irismpc/prf.hpp"
 #include "irismpc/shares.hpp"
@@ -370,6 +371,72 @@ int ref_dots_reshare(int backend, int variant, std::uint32_t l, std::uint32_t ro
       default:
         return 2;
     }
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// --- files (io.cpp) ---------------------------------------------------------
+
+// write_iris_db of the given records (io.cpp:74-88)
+int ref_write_iris_db(const char* path, std::uint32_t l, std::uint64_t s, const std::uint64_t* codes,
+                      const std::uint64_t* masks) {
+  try {
+    IrisDb db(l);
+    const std::size_t wl = (l + 63) / 64;
+    for (std::uint64_t r = 0; r < s; ++r) db.add(to_record(l, codes + r * wl, masks + r * wl));
+    write_iris_db(path, db);
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// The `irismpc share` dealer (tools/irismpc_cli.cpp:137-172) for one variant:
+// read_iris_db, seeds deal_seeds(Rng(derive(seed_from_u64(seed), 0x5eed))),
+// payload deal_db_payload with Rng(derive(seed_from_u64(seed), variant + 1)),
+// one IRSD + one IRS1 file per party.  (The CLI itself needs CLI11, which is
+// not vendored; this calls the same library functions in the same order.)
+int ref_share_files(const char* db_path, int backend, int variant, std::uint64_t seed,
+                    const char* const* share_paths, const char* const* seed_paths) {
+  try {
+    const auto db = read_iris_db(db_path);
+    const Backend be = backend ? Backend::shamir : Backend::replicated;
+    const Variant v = static_cast<Variant>(variant);
+    Rng seed_rng(CtrPrf::derive(CtrPrf::seed_from_u64(seed), 0x5eed));
+    const auto seeds = deal_seeds(seed_rng);
+    for (unsigned p = 1; p <= 3; ++p) {
+      const auto prev = seeds[party_index(prev_party(static_cast<PartyId>(p))) - 1];
+      write_seed_file(seed_paths[p - 1], p, seeds[p - 1], prev);
+    }
+    Rng rng(CtrPrf::derive(CtrPrf::seed_from_u64(seed), static_cast<std::uint64_t>(v) + 1));
+    const auto payload = deal_db_payload(db, be, v, rng);
+    for (unsigned p = 1; p <= 3; ++p) {
+      ShareFileHeader h;
+      h.backend = be;
+      h.variant = v;
+      h.party = p;
+      h.l = db.l;
+      h.s = db.size();
+      write_share_file(share_paths[p - 1], h, payload[p - 1]);
+    }
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// read_share_file: header fields + payload size (2 on the reference's errors)
+int ref_read_share_file(const char* path, std::uint32_t* hdr, std::uint64_t* s, std::uint64_t* payload_len) {
+  try {
+    const auto [h, bytes] = read_share_file(path);
+    hdr[0] = static_cast<std::uint32_t>(h.backend);
+    hdr[1] = static_cast<std::uint32_t>(h.variant);
+    hdr[2] = h.party;
+    hdr[3] = h.l;
+    *s = h.s;
+    *payload_len = bytes.size();
     return 0;
   } catch (...) {
     return map_error();

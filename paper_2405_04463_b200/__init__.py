@@ -41,6 +41,9 @@ EXPORTED = [
     "irismpc_gpu_or_open", "irismpc_gpu_get_stream_positions", "irismpc_gpu_set_stream_positions",
     "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
     "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap",
+    "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
+    "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
+    "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
 ]
 
 
@@ -77,6 +80,12 @@ class _Config(C.Structure):
                 ("seeds", C.c_uint8 * 48), ("device", C.c_int32), ("shard_rank", C.c_uint32),
                 ("db_rows_total", C.c_uint64), ("db_row_offset", C.c_uint64), ("match_ratio", C.c_double),
                 ("reserved", C.c_uint64 * 3)]
+
+
+class ShareHeader(C.Structure):
+    """ShareFileHeader (io.hpp:38-47)."""
+    _fields_ = [("backend", C.c_uint32), ("variant", C.c_uint32), ("party", C.c_uint32), ("l", C.c_uint32),
+                ("s", C.c_uint64)]
 
 
 class Stats(C.Structure):
@@ -136,6 +145,15 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_synth_db.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64]
         L.irismpc_gpu_enable_taps.argtypes = [vp, C.c_int]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
+        cp3 = C.c_char_p * 3
+        L.irismpc_gpu_read_share_header.argtypes = [C.c_char_p, C.POINTER(ShareHeader)]
+        L.irismpc_gpu_write_share_file.argtypes = [C.c_char_p, C.POINTER(ShareHeader), vp, C.c_size_t]
+        L.irismpc_gpu_load_db_files.argtypes = [vp, cp3]
+        L.irismpc_gpu_read_seed_files.argtypes = [cp3, u8p]
+        L.irismpc_gpu_write_seed_file.argtypes = [C.c_char_p, C.c_uint32, u8p, u8p]
+        L.irismpc_gpu_read_iris_db_header.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
+        L.irismpc_gpu_read_iris_db.argtypes = [C.c_char_p, vp, vp, C.c_uint64]
+        L.irismpc_gpu_write_iris_db.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, vp, vp]
         _lib = L
     return _lib
 
@@ -149,6 +167,63 @@ def seeds_from_master(seed: int) -> np.ndarray:
 def record_bytes(backend: int, l: int, variant: int = MPC_LIFT) -> int:
     """code_record_bytes + mask_record_bytes (shares.cpp:49-59)."""
     return int(lib().irismpc_gpu_record_bytes(backend, variant, l))
+
+
+# ---- files (io.hpp:28-60) -------------------------------------------------------
+
+def _b(path) -> bytes:
+    return os.fsencode(path)
+
+
+def read_share_header(path) -> ShareHeader:
+    """read_share_file's header and size checks; raises ConfigError like the reference's Error."""
+    h = ShareHeader()
+    if lib().irismpc_gpu_read_share_header(_b(path), C.byref(h)):
+        raise ConfigError(f"not a valid IRS1 share file: {path}")
+    return h
+
+
+def write_share_file(path, backend: int, variant: int, party: int, l: int, s: int, payload) -> None:
+    h = ShareHeader(backend, variant, party, l, s)
+    buf = np.ascontiguousarray(np.frombuffer(payload, np.uint8) if isinstance(payload, (bytes, bytearray))
+                               else payload, np.uint8)
+    if lib().irismpc_gpu_write_share_file(_b(path), C.byref(h), buf.ctypes.data, buf.nbytes):
+        raise ConfigError(f"cannot write {path}")
+
+
+def read_seed_files(paths) -> np.ndarray:
+    """Three IRSD files (parties 1..3) -> seed_1 | seed_2 | seed_3, cross-checked."""
+    out = np.zeros(48, np.uint8)
+    if lib().irismpc_gpu_read_seed_files((C.c_char_p * 3)(*[_b(p) for p in paths]), out.ctypes.data_as(u8p)):
+        raise ConfigError("bad or inconsistent IRSD seed files")
+    return out
+
+
+def write_seed_file(path, party: int, own, prev) -> None:
+    o = np.ascontiguousarray(own, np.uint8)
+    p = np.ascontiguousarray(prev, np.uint8)
+    if lib().irismpc_gpu_write_seed_file(_b(path), party, o.ctypes.data_as(u8p), p.ctypes.data_as(u8p)):
+        raise ConfigError(f"cannot write {path}")
+
+
+def read_iris_db(path):
+    """IRMP plaintext DB -> (codes, masks) uint64 word arrays [s][(l+63)/64], and l."""
+    l, s = C.c_uint32(0), C.c_uint64(0)
+    if lib().irismpc_gpu_read_iris_db_header(_b(path), C.byref(l), C.byref(s)):
+        raise ConfigError(f"not a valid IRMP file: {path}")
+    wl = (l.value + 63) // 64
+    codes = np.zeros((max(1, s.value), wl), np.uint64)
+    masks = np.zeros((max(1, s.value), wl), np.uint64)
+    if lib().irismpc_gpu_read_iris_db(_b(path), codes.ctypes.data, masks.ctypes.data, s.value):
+        raise ConfigError(f"cannot read {path}")
+    return codes[: s.value], masks[: s.value], l.value
+
+
+def write_iris_db(path, codes: np.ndarray, masks: np.ndarray, l: int) -> None:
+    c = np.ascontiguousarray(codes, np.uint64)
+    m = np.ascontiguousarray(masks, np.uint64)
+    if lib().irismpc_gpu_write_iris_db(_b(path), l, c.shape[0], c.ctypes.data, m.ctypes.data):
+        raise ConfigError(f"cannot write {path}")
 
 
 def lane_count(persons: int, s: int, rotations: int, membership: bool = False) -> int:
@@ -256,6 +331,12 @@ class Session:
         f = lib().irismpc_gpu_load_db_device if dev else lib().irismpc_gpu_load_db
         self._check(f(self._h, ptrs, lens, s))
         self.s = s
+
+    def load_db_files(self, paths):
+        """Session::load_db from the parties' IRS1 share files (streamed into HBM)."""
+        h = read_share_header(paths[0])
+        self._check(lib().irismpc_gpu_load_db_files(self._h, (C.c_char_p * 3)(*[_b(p) for p in paths])))
+        self.s = int(h.s)
 
     def synth_db(self, s: int, rng_seed: int = 2, first: int = 0, mask_density: float = 0.9, deal_seed: int = 7):
         """Device dealer: rows [first, first+s) of Rng(rng_seed) random_record, dealt with sub_rng(deal_seed,1)."""

@@ -962,6 +962,81 @@ int irismpc_gpu_load_db_device(irismpc_gpu_ctx* c, const uint8_t* const dpayload
   return rc;
 }
 
+int irismpc_gpu_load_db_files(irismpc_gpu_ctx* c, const char* const paths[3]) {
+  if (!c || !paths) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  irismpc_gpu_share_header h[3];
+  for (int p = 0; p < 3; ++p) {
+    if (irismpc_gpu_read_share_header(paths[p], &h[p]))
+      return fail(c, IRISMPC_GPU_ERR_CONFIG, std::string("not a valid IRS1 share file: ") + (paths[p] ? paths[p] : "(null)"));
+    if (h[p].party != (uint32_t)(p + 1)) return fail(c, IRISMPC_GPU_ERR_CONFIG, "share file belongs to another party");
+    if (h[p].backend != c->cfg.backend || h[p].variant != c->cfg.variant || h[p].l != c->l)
+      return fail(c, IRISMPC_GPU_ERR_CONFIG, "share file does not match config");
+    if (h[p].s != h[0].s) return fail(c, IRISMPC_GPU_ERR_CONFIG, "share files disagree on s");
+  }
+  const uint64_t s = h[0].s, rec = c->rec;
+  int rc = alloc_planes(c, s);
+  if (rc) return rc;
+  FILE* f[3] = {nullptr, nullptr, nullptr};
+  auto close_all = [&] {
+    for (auto& x : f)
+      if (x) std::fclose(x);
+  };
+  for (int p = 0; p < 3; ++p) {
+    f[p] = std::fopen(paths[p], "rb");
+    if (!f[p] || std::fseek(f[p], 24, SEEK_SET) != 0) {
+      close_all();
+      return fail(c, IRISMPC_GPU_ERR_CONFIG, "cannot open share file");
+    }
+  }
+  // two pinned slots: the disk read of chunk i+1 overlaps the H2D + parse of chunk i
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s ? s : 1, (128ull << 20) / rec));
+  uint8_t* host[2] = {nullptr, nullptr};
+  Buf dev[2], bad;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int status = 0;
+  for (int k = 0; k < 2 && !status; ++k) {
+    if (cudaMallocHost(&host[k], 3 * chunk * rec) != cudaSuccess || dev[k].ensure(3 * chunk * rec) ||
+        cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming) != cudaSuccess)
+      status = fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (file load staging)");
+  }
+  if (!status && (bad.ensure(sizeof(int)) || cudaMemsetAsync(bad.p, 0, sizeof(int), c->st) != cudaSuccess))
+    status = fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  for (uint64_t r0 = 0, i = 0; r0 < s && !status; r0 += chunk, ++i) {
+    const int k = (int)(i % 2);
+    const uint64_t nr = std::min<uint64_t>(chunk, s - r0);
+    if (i >= 2 && cudaEventSynchronize(done[k]) != cudaSuccess) {
+      status = fail(c, IRISMPC_GPU_ERR_DEVICE, "file load: device fault");
+      break;
+    }
+    for (int p = 0; p < 3 && !status; ++p)
+      if (std::fread(host[k] + p * chunk * rec, 1, nr * rec, f[p]) != nr * rec)
+        status = fail(c, IRISMPC_GPU_ERR_CONFIG, "short read: share file");
+    if (status) break;
+    const uint8_t* dp[3];
+    for (int p = 0; p < 3; ++p) {
+      dp[p] = dev[k].as<uint8_t>() + p * chunk * rec;
+      if (cudaMemcpyAsync(const_cast<uint8_t*>(dp[p]), host[k] + p * chunk * rec, nr * rec, cudaMemcpyHostToDevice,
+                          c->st) != cudaSuccess)
+        status = fail(c, IRISMPC_GPU_ERR_DEVICE, "file load: H2D failed");
+    }
+    if (status) break;
+    status = parse_rows(c, dp, nr, r0, c->shamir ? nullptr : &bad);
+    if (!status && cudaEventRecord(done[k], c->st) != cudaSuccess)
+      status = fail(c, IRISMPC_GPU_ERR_DEVICE, "file load: event");
+  }
+  close_all();
+  if (!status) status = finish_load(c, c->shamir ? nullptr : &bad);
+  cudaStreamSynchronize(c->st);
+  for (int k = 0; k < 2; ++k) {
+    if (host[k]) cudaFreeHost(host[k]);
+    if (done[k]) cudaEventDestroy(done[k]);
+    dev[k].release();
+  }
+  bad.release();
+  return status;
+}
+
 int irismpc_gpu_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint32_t persons,
                             uint8_t* person_match_out, uint8_t* row_bits_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;

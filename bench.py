@@ -58,7 +58,7 @@ class Clocks:
     during the timed region (B200_PROFILING.md clocks line)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -86,7 +86,7 @@ class Clocks:
             out = ""
         for line in out.splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
+            if len(parts) == 7:
                 self.samples.append(parts)
 
     def summary(self):
@@ -96,8 +96,15 @@ class Clocks:
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        pw = []
+        for s in self.samples:
+            try:
+                pw.append(float(s[6]))
+            except ValueError:
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
 
 
 def load_peaks():

@@ -22,7 +22,9 @@
 // Warp-specialised and persistent:
 //   warp 0   TMA producer (128B-swizzled K-major tiles, mbarrier ring)
 //   warp 1   TMEM allocator; the leader's lane 0 issues the MMAs
-//   warps 4-7 epilogue: tcgen05.ld -> recombine -> global stores
+//   warps 2-5 epilogue: tcgen05.ld -> recombine -> global stores
+// (6 warps: the registers and warp slots left free go to the threshold
+// kernels that run concurrently on the second stream)
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
@@ -68,7 +70,7 @@ struct Tile {
 }  // namespace
 
 template <int L>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs, uint32_t grouped) {
   // Persistent: clusters form groups of n_tiles; cluster c owns n_tile = c % n_tiles
@@ -185,8 +187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         umma_commit_pair(accum, 0x3);
       }
     }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
+  } else if (warp >= 2) {
+    const int q = warp & 3;  // tcgen05.ld: warp w reads TMEM lanes 32 (w % 4) .. + 31
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t te = mapa_shared(tmem_empty, 0);
     uint32_t ti = 0;
@@ -277,14 +279,17 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   // m_tiles counts 128-row tiles; pairs cover 256 rows (s_pad is a multiple of 256).
   // Persistent: one CTA pair per two SMs.
   static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  if (!nsm) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) nsm = std::max(2, std::min(nsm, std::atoi(e)));  // experiment hook
+  }
   const uint32_t m_pairs = m_tiles / 2;
   const uint32_t units = g.nprob * m_pairs;
   const uint32_t max_cl = (uint32_t)(nsm / 2);
   const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
   const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
   const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
-  k_limb_gemm_pair<L><<<dim3(2 * ncl), 256, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
+  k_limb_gemm_pair<L><<<dim3(2 * ncl), 192, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
 }
 
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,

@@ -47,10 +47,27 @@ __device__ __forceinline__ void and3(const uint32_t x[3], const uint32_t y[3], c
   }
 }
 
-// last segment with key(seg) <= x (warp-uniform when x is)
+// last segment with key(seg) <= x, x < total.  The segments of a job are
+// near-uniform (one DB column of a row chunk each), so an interpolated guess
+// followed by a local walk touches 1-3 entries instead of a ~10-step binary
+// search: those dependent loads miss L1 when the co-resident GEMM's 193 KB of
+// shared memory shrinks the L1 carve-out.
 template <typename F>
-__device__ __forceinline__ uint32_t seg_search(const Seg* segs, uint32_t nsegs, uint64_t x, F key) {
+__device__ __forceinline__ uint32_t seg_search(const Seg* segs, uint32_t nsegs, uint64_t x, uint64_t total, F key) {
+  uint64_t guess = (uint64_t)((double)x * nsegs / (double)total);
+  uint32_t i = guess < nsegs ? (uint32_t)guess : nsegs - 1;
   uint32_t lo = 0, hi = nsegs - 1;
+  for (int it = 0; it < 4; ++it) {  // local walk, then binary search in the remaining bracket
+    if (key(segs[i]) > x) {
+      hi = i - 1;
+      i = i - 1;
+    } else if (i + 1 < nsegs && key(segs[i + 1]) <= x) {
+      lo = i + 1;
+      i = i + 1;
+    } else {
+      return i;
+    }
+  }
   while (lo < hi) {
     const uint32_t mid = (lo + hi + 1) >> 1;
     if (key(segs[mid]) <= x) lo = mid; else hi = mid - 1;
@@ -130,7 +147,7 @@ __device__ __forceinline__ GroupCtx group_ctx(const ThrArgs& A, uint64_t gtid) {
   const uint64_t gi = (gtid >> 5) * 31 + lane;
   c.mine = lane < 31 && gi < A.ngrp;
   const uint64_t gq = gi < A.ngrp ? gi : A.ngrp - 1;
-  const uint32_t si = seg_search(A.segs, A.nsegs, gq, [](const Seg& s) { return s.grp_begin; });
+  const uint32_t si = seg_search(A.segs, A.nsegs, gq, A.ngrp, [](const Seg& s) { return s.grp_begin; });
   c.sg = &A.segs[si];
   c.L8 = (c.sg->lane_begin / 8 + (gq - c.sg->grp_begin)) * 8;
   const uint64_t Ln = __shfl_down_sync(0xFFFFFFFFu, c.L8, 1);
@@ -145,7 +162,7 @@ __device__ __forceinline__ GroupCtx group_ctx(const ThrArgs& A, uint64_t gtid) {
 __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ ThrArgs A) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (tid >= A.ngblk) return;
-  const uint32_t si = seg_search(A.segs, A.nsegs, tid, [](const Seg& s) { return s.gblk_begin; });
+  const uint32_t si = seg_search(A.segs, A.nsegs, tid, A.ngblk, [](const Seg& s) { return s.gblk_begin; });
   const Seg& sg = A.segs[si];
   const uint64_t local = tid - sg.gblk_begin;
   const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
@@ -235,7 +252,7 @@ __device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, bool 
 //   no-lift    : diff = a ml32 - b hd32
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
 template <int V>
-__global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrArgs A) {
   using HT = typename std::conditional<V == kNoLift, uint32_t, uint16_t>::type;
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
@@ -258,41 +275,73 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
                      reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0)) & 15) == 0;
     if (V == kMpcLift) full = full && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) & 15) == 0;
   }
-  uint32_t h[3][8], m[3][8];
-#pragma unroll
-  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, gc.mine, h[p]);
-  reshare8(A, L8, gc.next_contig, h, HM);
-  uint32_t d[3][8];
-  if (V == kPlainMask) {
-    // m[0] = public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
-    load8<MT>(ml[0], sg, L8, full, gc.mine, m[0]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)m[0][i]));
-      d[0][i] = (t - h[0][i]) & 0xFFFFu;
-      d[1][i] = (0u - h[1][i]) & 0xFFFFu;
-      d[2][i] = (0u - h[2][i]) & 0xFFFFu;
-      m[0][i] = m[1][i] = m[2][i] = 0u;
-    }
-  } else {
+  // ml first (stream offset n): d = a * ml, the reshared ml leaves the registers,
+  // then hd (offset 0): d -= b * hd -- keeps two 3 x 8 arrays live, not three
+  uint32_t d[3][8], m[3][8];
+  if (V != kPlainMask) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) load8<MT>(ml[p], sg, L8, full, gc.mine, m[p]);
     reshare8(A, A.n + L8, gc.next_contig, m, MM);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) d[p][i] = A.a * m[p][i] - A.b * h[p][i];
+      for (int i = 0; i < 8; ++i) d[p][i] = A.a * m[p][i];
+    if (gc.mine && V == kMpcLift) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        if (full) {
+          uint32_t mw[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) mw[i] = m[p][2 * i] | (m[p][2 * i + 1] << 16);
+          *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint64_t ln = L8 + i;
+            if (ln >= sg.lane_begin && ln < sg.lane_end)
+              A.ml_rs[p * A.cstride + sg.src + (ln - sg.lane_begin)] = (uint16_t)m[p][i];
+          }
+        }
+      }
+    }
+    if (gc.mine && A.tap_rs_ml) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t ln = L8 + i;
+        if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          A.tap_rs_ml[p * A.n + ln] = m[p][i];
+          A.tap_ml32[p * A.n + ln] = m[p][i];
+        }
+      }
+    }
+  }
+  uint32_t (&h)[3][8] = m;  // reuse the registers
+#pragma unroll
+  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, gc.mine, h[p]);
+  reshare8(A, L8, gc.next_contig, h, HM);
+  if (V == kPlainMask) {
+    // public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
+    uint32_t cnt[8];
+    load8<MT>(ml[0], sg, L8, full, gc.mine, cnt);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)cnt[i]));
+      d[0][i] = (t - h[0][i]) & 0xFFFFu;
+      d[1][i] = (0u - h[1][i]) & 0xFFFFu;
+      d[2][i] = (0u - h[2][i]) & 0xFFFFu;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[p][i] -= A.b * h[p][i];
   }
   if (!gc.mine) return;
   if (full) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
-      if (V == kMpcLift) {
-        uint32_t mw[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mw[i] = m[p][2 * i] | (m[p][2 * i + 1] << 16);
-        *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-      }
       uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
       dd[0] = make_uint4(d[p][0], d[p][1], d[p][2], d[p][3]);
       dd[1] = make_uint4(d[p][4], d[p][5], d[p][6], d[p][7]);
@@ -306,13 +355,8 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
     const uint64_t src = sg.src + (ln - sg.lane_begin);
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
-      if (V == kMpcLift) A.ml_rs[p * A.cstride + src] = (uint16_t)m[p][i];
       A.diff[p * A.cstride + src] = d[p][i];
-      if (A.tap_rs_hd) {
-        A.tap_rs_hd[p * A.n + ln] = h[p][i];
-        A.tap_rs_ml[p * A.n + ln] = m[p][i];
-        A.tap_ml32[p * A.n + ln] = m[p][i];
-      }
+      if (A.tap_rs_hd) A.tap_rs_hd[p * A.n + ln] = h[p][i];
     }
   }
 }
@@ -328,7 +372,7 @@ struct TaskCtx {
 
 __device__ __forceinline__ TaskCtx task_ctx(const ThrArgs& A, uint64_t task) {
   TaskCtx t;
-  const uint32_t si = seg_search(A.segs, A.nsegs, task, [](const Seg& s) { return s.task_begin; });
+  const uint32_t si = seg_search(A.segs, A.nsegs, task, A.ntasks, [](const Seg& s) { return s.task_begin; });
   t.sg = A.segs[si];
   t.task = task;
   t.L0 = (t.sg.q_first + (task - t.sg.task_begin)) * 1024;

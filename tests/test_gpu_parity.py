@@ -251,6 +251,28 @@ def test_payload_errors_map_to_reference_exceptions():
         sess.batch_query([np.zeros(rec, np.uint8)] * 3, 1)
 
 
+@pytest.mark.parametrize("be,var", [(O.SHAMIR, P.MPC_LIFT), (O.REPLICATED, P.PLAIN_MASK), (O.SHAMIR, P.NO_LIFT)])
+def test_configs2_batch_shape_32_persons(be, var):
+    """configs[2]'s batch shape: 64 codes (32 persons) x 31 rotations = 1984 columns
+    (8 column tiles of 256) and 61 504 inner-batch pair lanes, at a DB size the
+    oracle finishes quickly; every lane bit and person bit vs the oracle.  Persons
+    5 and 20 carry planted DB rows; person 11's right eye is person 3's left eye."""
+    l, s, persons, r, seed = 2048, 300, 32, 31, 51
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, False, 0.9)
+    qc[10], qm[10] = dc[17], dm[17]
+    qc[41], qm[41] = dc[250], dm[250]
+    qc[23], qm[23] = qc[6], qm[6]
+    cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True, variant=var)
+    m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, want_rows=True)
+    ref = O.run_local(O.make_config(be, l, 0.375, r, debug_rows=True, variant=var), seed, dc, dm, qc, qm, persons)
+    n = P.lane_count(persons, s, r)
+    assert n == 64 * r * s + 61_504
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+    np.testing.assert_array_equal(m, ref.person_match)
+    assert m[5] == 1 and m[20] == 1 and m[11] == 1 and m[3] == 1
+    np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
+
+
 def test_sharded_db_matches_single_gpu():
     """Two shards on one GPU (rows split), partial shares + MPC OR + open."""
     l, s, persons, seed = 12800, 700, 2, 41

@@ -453,8 +453,32 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       const char* e = std::getenv("IRISMPC_CHUNK_LANES");  // test hook
       return e ? std::strtoull(e, nullptr, 10) : (1ull << 24);
     }();
-    rows_chunk = round_up(std::max<uint64_t>(target / ncols, 1), 2 * kGemmBM);
-    rows_chunk = std::min<uint64_t>(rows_chunk, round_up(s_loc, 2 * kGemmBM));
+    // Row granule: a chunk's (problem, 256-row block) units should fill whole
+    // waves of the persistent GEMM's cluster groups, for every field.
+    uint64_t granule = 2 * kGemmBM;
+    static const bool no_granule = std::getenv("IRISMPC_NO_GRANULE") != nullptr;  // A/B hook
+    for (const auto& f : c->fld) {
+      if (no_granule) break;
+      const uint64_t g = gemm_groups((uint32_t)ceil_div(ncols, f.bn()));
+      uint64_t a = g, b = f.nparty;  // m_pairs multiple of g / gcd(g, nprob)
+      while (b) {
+        const uint64_t t = a % b;
+        a = b;
+        b = t;
+      }
+      const uint64_t need = 2 * kGemmBM * (g / a);
+      uint64_t x = granule, y = need;  // lcm(granule, need)
+      while (y) {
+        const uint64_t t = x % y;
+        x = y;
+        y = t;
+      }
+      granule = granule / x * need;
+    }
+    rows_chunk = round_up(std::max<uint64_t>(target / ncols, 1), granule);
+    nchunks = ceil_div(s_loc, rows_chunk);
+    // equal chunks (the last one takes the remainder)
+    rows_chunk = std::min<uint64_t>(round_up(ceil_div(s_loc, nchunks), granule), round_up(s_loc, 2 * kGemmBM));
     nchunks = ceil_div(s_loc, rows_chunk);
   }
   auto chunk_rows = [&](uint64_t i) { return std::min<uint64_t>(rows_chunk, s_loc - i * rows_chunk); };

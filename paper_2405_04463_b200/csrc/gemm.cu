@@ -292,6 +292,13 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   k_limb_gemm_pair<L><<<dim3(2 * ncl), 192, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
 }
 
+uint32_t gemm_groups(uint32_t n_tiles) {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) nsm = std::max(2, std::min(nsm, std::atoi(e)));
+  return std::max<uint32_t>(1, (uint32_t)(nsm / 2) / std::max<uint32_t>(1, n_tiles));
+}
+
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
                  uint32_t n_tiles, cudaStream_t st) {
   switch (g.limbs) {

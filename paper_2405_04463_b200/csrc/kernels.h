@@ -87,6 +87,9 @@ int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
                     uint32_t box_rows);
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
                  uint32_t n_tiles, cudaStream_t st);
+// cluster groups of the persistent GEMM: n_tiles clusters sweep one 256-row
+// block of one problem in lockstep, groups of them run side by side
+uint32_t gemm_groups(uint32_t n_tiles);
 
 // ---- inner-batch pairs (pairs.cu)
 // C: [nprob][ncols][ncodes] (elem_bytes each) -> out[p * out_pstride + pair lane]

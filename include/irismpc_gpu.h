@@ -152,6 +152,53 @@ int irismpc_gpu_deal_payload(irismpc_gpu_ctx* ctx, uint64_t deal_seed, uint64_t 
 int irismpc_gpu_synth_db(irismpc_gpu_ctx* ctx, uint64_t s, uint64_t rng_seed, uint64_t first,
                          double mask_density, uint64_t deal_seed);
 
+/* ---- party mode: one party per process / GPU ---------------
+ * The reference's deployment: each party holds only its own payloads and its
+ * two seeds (own, prev) and exchanges the protocol's messages with the other
+ * two every round (PartyComm / TcpMesh, transport.hpp:54-154), here over NCCL
+ * send/recv (ranks 0, 1, 2 = parties 1, 2, 3) or an in-process mailbox
+ * (three parties in one process, like InProcNet).  mpc-lift only.  The
+ * per-phase byte/round ledger is counted from the messages actually sent
+ * (CommLedger semantics), not derived analytically. */
+typedef struct irismpc_gpu_party irismpc_gpu_party;
+typedef struct irismpc_gpu_inproc irismpc_gpu_inproc;
+
+/* Per-party QueryStats (engine.hpp:46-56) from the measured ledger. */
+typedef struct irismpc_gpu_party_stats {
+  uint64_t s, l, batch, lanes;
+  uint64_t dot_bytes, lift_bytes, msb_bytes, or_tree_bytes;
+  uint64_t dot_rounds, lift_rounds, msb_rounds, or_tree_rounds;
+  uint64_t wire_bytes;  /* bytes this party actually handed to the transport */
+  double wall_ms;       /* device time of the query on this party's GPU */
+} irismpc_gpu_party_stats;
+
+/* 128-byte ncclUniqueId for the three ranks (rank 0 creates, all receive it). */
+int irismpc_gpu_nccl_unique_id(uint8_t out[128]);
+/* cfg.seeds: bytes 0..15 = this party's own seed, 16..31 = its prev seed
+ * (read_seed_file, io.cpp:157-170).  party = 1, 2, 3.  NCCL rank = party - 1. */
+int irismpc_gpu_party_create_nccl(const irismpc_gpu_config* cfg, uint32_t party, const uint8_t nccl_id[128],
+                                  irismpc_gpu_party** out);
+int irismpc_gpu_inproc_create(irismpc_gpu_inproc** out);
+void irismpc_gpu_inproc_destroy(irismpc_gpu_inproc* net);
+int irismpc_gpu_party_create_inproc(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_inproc* net,
+                                    irismpc_gpu_party** out);
+void irismpc_gpu_party_destroy(irismpc_gpu_party* pc);
+const char* irismpc_gpu_party_last_error(const irismpc_gpu_party* pc);
+/* This party's IRS1 payload (host). */
+int irismpc_gpu_party_load_db(irismpc_gpu_party* pc, const uint8_t* payload, size_t len, uint64_t s);
+/* party_batch_query / party_membership (engine.hpp:307-313): this party's
+ * query payload; person_match_out / row_bits_out are filled at P1 only. */
+int irismpc_gpu_party_batch_query(irismpc_gpu_party* pc, const uint8_t* q, size_t qlen, uint32_t persons,
+                                  uint8_t* person_match_out, uint8_t* row_bits_out,
+                                  irismpc_gpu_party_stats* stats);
+int irismpc_gpu_party_membership(irismpc_gpu_party* pc, const uint8_t* q, size_t qlen, uint8_t* match_out,
+                                 uint8_t* row_bits_out, irismpc_gpu_party_stats* stats);
+/* Parity taps of the last query: this party's (own, prev) components,
+ * tap = IRISMPC_GPU_TAP_* (DOT_* = own additive dot only, [n]; others [2][n],
+ * MSB as bytes). */
+int irismpc_gpu_party_read_tap(irismpc_gpu_party* pc, int tap, void* host_out, size_t bytes);
+int irismpc_gpu_party_stream_positions(const irismpc_gpu_party* pc, uint64_t pos_own_prev[2]);
+
 /* ---- share / seed / plaintext files (io.hpp:28-60, src/io.cpp) ----------- */
 /* IRS1 per-party share file: magic "IRS1", version 1, backend u8, variant u8,
  * party u8, code_k u8, mask_k u8, reserved u16, l u32, s u64, then the row

@@ -44,6 +44,10 @@ EXPORTED = [
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
+    "irismpc_gpu_nccl_unique_id", "irismpc_gpu_party_create_nccl", "irismpc_gpu_inproc_create",
+    "irismpc_gpu_inproc_destroy", "irismpc_gpu_party_create_inproc", "irismpc_gpu_party_destroy",
+    "irismpc_gpu_party_last_error", "irismpc_gpu_party_load_db", "irismpc_gpu_party_batch_query",
+    "irismpc_gpu_party_membership", "irismpc_gpu_party_read_tap", "irismpc_gpu_party_stream_positions",
 ]
 
 
@@ -86,6 +90,17 @@ class ShareHeader(C.Structure):
     """ShareFileHeader (io.hpp:38-47)."""
     _fields_ = [("backend", C.c_uint32), ("variant", C.c_uint32), ("party", C.c_uint32), ("l", C.c_uint32),
                 ("s", C.c_uint64)]
+
+
+class PartyStats(C.Structure):
+    """One party's QueryStats from the measured ledger (party mode)."""
+    _fields_ = [(k, C.c_uint64) for k in ("s", "l", "batch", "lanes", "dot_bytes", "lift_bytes", "msb_bytes",
+                                          "or_tree_bytes", "dot_rounds", "lift_rounds", "msb_rounds",
+                                          "or_tree_rounds", "wire_bytes")] + [("wall_ms", C.c_double)]
+
+    def ledger(self) -> dict:
+        return {k: getattr(self, k) for k in ("dot_bytes", "lift_bytes", "msb_bytes", "or_tree_bytes", "dot_rounds",
+                                              "lift_rounds", "msb_rounds", "or_tree_rounds")}
 
 
 class Stats(C.Structure):
@@ -154,6 +169,19 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_read_iris_db_header.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
         L.irismpc_gpu_read_iris_db.argtypes = [C.c_char_p, vp, vp, C.c_uint64]
         L.irismpc_gpu_write_iris_db.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, vp, vp]
+        L.irismpc_gpu_nccl_unique_id.argtypes = [u8p]
+        L.irismpc_gpu_party_create_nccl.argtypes = [C.POINTER(_Config), C.c_uint32, u8p, C.POINTER(vp)]
+        L.irismpc_gpu_inproc_create.argtypes = [C.POINTER(vp)]
+        L.irismpc_gpu_inproc_destroy.argtypes = [vp]
+        L.irismpc_gpu_party_create_inproc.argtypes = [C.POINTER(_Config), C.c_uint32, vp, C.POINTER(vp)]
+        L.irismpc_gpu_party_destroy.argtypes = [vp]
+        L.irismpc_gpu_party_last_error.argtypes = [vp]
+        L.irismpc_gpu_party_last_error.restype = C.c_char_p
+        L.irismpc_gpu_party_load_db.argtypes = [vp, vp, C.c_size_t, C.c_uint64]
+        L.irismpc_gpu_party_batch_query.argtypes = [vp, vp, C.c_size_t, C.c_uint32, vp, vp, C.POINTER(PartyStats)]
+        L.irismpc_gpu_party_membership.argtypes = [vp, vp, C.c_size_t, vp, vp, C.POINTER(PartyStats)]
+        L.irismpc_gpu_party_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
+        L.irismpc_gpu_party_stream_positions.argtypes = [vp, u64p]
         _lib = L
     return _lib
 
@@ -461,3 +489,164 @@ def run_batch_local(cfg: EngineConfig, q_codes: np.ndarray, q_masks: np.ndarray,
     else:
         m = sess.batch_query(q, persons if persons is not None else q_codes.shape[0] // 2, want_rows)
     return m, sess
+
+
+# ---- party mode: one party per process / GPU ---------------------
+
+def _party_config(cfg: EngineConfig, own_prev, device: int) -> _Config:
+    a, b = cfg.params()
+    c = _Config()
+    c.backend, c.variant, c.l, c.a, c.b, c.m = cfg.backend, cfg.variant, cfg.l, a, b, cfg.m
+    c.rotations, c.debug_rows, c.match_ratio = cfg.rotations, 1 if cfg.debug_rows else 0, cfg.match_ratio
+    op = np.ascontiguousarray(own_prev, np.uint8)
+    for i in range(32):
+        c.seeds[i] = int(op[i])
+    c.device = device
+    return c
+
+
+def nccl_unique_id() -> bytes:
+    out = np.zeros(128, np.uint8)
+    if lib().irismpc_gpu_nccl_unique_id(out.ctypes.data_as(u8p)):
+        raise DeviceError("NCCL is not available")
+    return bytes(out)
+
+
+class InProcNet:
+    """InProcNet (transport.hpp:129-154): mailboxes for three parties in one process."""
+
+    def __init__(self):
+        h = vp()
+        if lib().irismpc_gpu_inproc_create(C.byref(h)):
+            raise DeviceError("inproc net")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().irismpc_gpu_inproc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Party:
+    """One MPC party (PartyCtx + Session<B,16,16>) on one GPU; its messages cross
+    NCCL (nccl_id) or an InProcNet (net).  own_prev = seed_own (16 B) + seed_prev (16 B)."""
+
+    def __init__(self, cfg: EngineConfig, party: int, own_prev, nccl_id: bytes | None = None,
+                 net: InProcNet | None = None, device: int = 0):
+        c = _party_config(cfg, own_prev, device)
+        h = vp()
+        if nccl_id is not None:
+            idb = np.frombuffer(nccl_id, np.uint8).copy()
+            rc = lib().irismpc_gpu_party_create_nccl(C.byref(c), party, idb.ctypes.data_as(u8p), C.byref(h))
+        else:
+            rc = lib().irismpc_gpu_party_create_inproc(C.byref(c), party, net._h, C.byref(h))
+        if rc:
+            raise _ERRORS.get(rc, IrisError)(f"party create failed ({rc})")
+        self._h, self.cfg, self.party, self.s = h, cfg, party, 0
+        self.rec = record_bytes(cfg.backend, cfg.l, cfg.variant)
+        self.last_stats = PartyStats()
+        self.row_bits = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().irismpc_gpu_party_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc:
+            raise _ERRORS.get(rc, IrisError)(lib().irismpc_gpu_party_last_error(self._h).decode())
+
+    def load_db(self, payload, s: int):
+        a = np.ascontiguousarray(payload, np.uint8)
+        self._check(lib().irismpc_gpu_party_load_db(self._h, a.ctypes.data, a.nbytes, s))
+        self.s = s
+
+    def batch_query(self, q, persons: int, want_rows: bool = False):
+        a = np.ascontiguousarray(q, np.uint8)
+        out = np.zeros(max(1, persons), np.uint8)
+        rows = np.zeros(max(1, lane_count(persons, self.s, self.cfg.rotations)), np.uint8) if want_rows else None
+        self._check(lib().irismpc_gpu_party_batch_query(self._h, a.ctypes.data, a.nbytes, persons, out.ctypes.data,
+                                                        rows.ctypes.data if want_rows else None,
+                                                        C.byref(self.last_stats)))
+        self.row_bits = rows
+        return out[:persons] if self.party == 1 else None
+
+    def membership(self, q, want_rows: bool = False):
+        a = np.ascontiguousarray(q, np.uint8)
+        out = np.zeros(1, np.uint8)
+        rows = np.zeros(max(1, self.s), np.uint8) if want_rows else None
+        self._check(lib().irismpc_gpu_party_membership(self._h, a.ctypes.data, a.nbytes, out.ctypes.data,
+                                                       rows.ctypes.data if want_rows else None,
+                                                       C.byref(self.last_stats)))
+        self.row_bits = rows
+        return bool(out[0]) if self.party == 1 else None
+
+    def read_tap(self, tap: int, n: int) -> np.ndarray:
+        """DOT_*: this party's own additive dot [n]; others: [own, prev] x [n]."""
+        if tap in (TAP_DOT_HD, TAP_DOT_ML):
+            out = np.zeros(n, np.uint16)
+        elif tap in (TAP_RS_HD, TAP_RS_ML):
+            out = np.zeros(2 * n, np.uint16)
+        elif tap == TAP_MSB:
+            out = np.zeros(2 * n, np.uint8)
+        else:
+            out = np.zeros(2 * n, np.uint32)
+        self._check(lib().irismpc_gpu_party_read_tap(self._h, tap, out.ctypes.data, out.nbytes))
+        return out if tap in (TAP_DOT_HD, TAP_DOT_ML) else out.reshape(2, n)
+
+    def stream_positions(self) -> np.ndarray:
+        p = np.zeros(2, np.uint64)
+        self._check(lib().irismpc_gpu_party_stream_positions(self._h, p.ctypes.data_as(u64p)))
+        return p
+
+
+def party_seeds(seeds48, party: int) -> np.ndarray:
+    """(seed_own, seed_prev) of party 1..3 from seed_1 | seed_2 | seed_3 (rep3.hpp:124-127)."""
+    s = np.ascontiguousarray(seeds48, np.uint8)
+    p = party - 1
+    q = (p + 2) % 3
+    return np.concatenate([s[16 * p:16 * p + 16], s[16 * q:16 * q + 16]])
+
+
+def run_parties_inproc(cfg: EngineConfig, seeds48, db_payloads, s: int, q_payloads, persons: int = 1,
+                       membership: bool = False, want_rows: bool = False, device: int = 0):
+    """run_parties (cluster.hpp:33-60) with one Party per host thread on one GPU,
+    messages through an InProcNet.  Returns the three Party objects (P1 holds the result)."""
+    import threading
+    net = InProcNet()
+    parties = [Party(cfg, p, party_seeds(seeds48, p), net=net, device=device) for p in (1, 2, 3)]
+    results, errors = [None] * 3, [None] * 3
+
+    def run(i):
+        try:
+            parties[i].load_db(db_payloads[i], s)
+            if membership:
+                results[i] = parties[i].membership(q_payloads[i], want_rows)
+            else:
+                results[i] = parties[i].batch_query(q_payloads[i], persons, want_rows)
+        except Exception as e:  # noqa: BLE001 - surfaced below
+            errors[i] = e
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errors:
+        if e is not None:
+            raise e
+    parties[0].result = results[0]
+    parties[0]._net = net  # keep the mailboxes alive with the parties
+    return parties

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libirismpc_gpu.so")
-SOURCES = ["prep.cu", "gemm.cu", "pairs.cu", "threshold.cu", "orreduce.cu", "share_io.cu", "api.cu"]
+SOURCES = ["prep.cu", "gemm.cu", "pairs.cu", "threshold.cu", "orreduce.cu", "share_io.cu", "party.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static"], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

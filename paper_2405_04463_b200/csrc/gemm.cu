@@ -139,7 +139,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t seg = kb / g.nkb_seg;
           const uint32_t kk = kb % g.nkb_seg;
-          const uint32_t pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;  // A = [x_p | x_{p-1}]
+          // A = [x_p | x_{p-1}]: the previous party's component plane, or plane 1
+          // of a single party's (own, prev) planes (party mode, nprob = 1)
+          const uint32_t pa = (g.rep && seg == 1) ? (g.nprob == 1 ? 1u : (p + 2) % 3) : p;
           uint8_t* st = smem + stage * T::STAGE;
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * T::STAGE);
           const uint32_t fb = mapa_shared(&full[stage], 0);

@@ -35,6 +35,8 @@ struct FieldFmt {
   uint64_t off;        // byte offset of the field inside the record
   int width;           // 2, 4 or 0 (plain mask bits)
   int limbs;           // u8 limb planes of the field (width, or 1 for bits)
+  int slot = -1;       // plane slot to write (-1: the party index)
+  int take_prev = 0;   // replicated: keep the `prev` component instead of `own`
 };
 
 // ---- K1 prep / dealer (prep.cu)
@@ -68,7 +70,7 @@ struct GemmArgs {
   uint32_t nkb_seg;   // k-blocks per K segment (l_pad / 128)
   uint32_t nseg;      // 1 (Shamir, public bits) or 2 (replicated [x_p | x_{p-1}])
   uint32_t rep;
-  uint32_t nprob;     // 3 (one per party) or 1 (public mask popcount)
+  uint32_t nprob;     // 3 (one per party) or 1 (public mask popcount / one party's own dot)
   uint32_t limbs;     // 1 (0/1 bits), 2 (Z_2^16) or 4 (Z_2^32)
   uint32_t s_valid;   // rows written (relative to row0)
   uint32_t row0;      // first DB row of this launch (multiple of 256)

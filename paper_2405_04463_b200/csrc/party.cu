@@ -1,0 +1,1309 @@
+// f3: the mpc-lift query with ONE PARTY per process / GPU (the reference's
+// deployment).  Each party holds only its own IRS1 payloads
+// and its two seeds (own = seed_p, prev = seed_{p-1}); every protocol message
+// of the reference crosses a real transport, round by round:
+//
+//   dot      reshare_pair<16,16>: own -> next party                 (engine.cpp:80-106)
+//   lift     bit_extract_sum {16,17}: 1 FA round + 16 chain rounds  (circuits.hpp:202-296)
+//   ot       bit_inject<15>, <16>: P1 -> P2, P3 -> P2, then P2 -> P3 (convert.hpp:42-155)
+//   msb      msb_batch<32>: 1 FA round + 30 chain rounds
+//   or_tree  [debug_rows open], or_tree_batch halving rounds, open_bits_to(P1)
+//            (circuits.hpp:387-486)
+//
+// Transports: NCCL send/recv (ranks 0,1,2 = parties 1,2,3; libnccl loaded at
+// run time so the library has no link-time NCCL dependency) or an in-process
+// mailbox for three party contexts in one process (InProcNet analogue,
+// transport.hpp:129-154).  The ledger counts what the reference's CommLedger
+// counts (bytes per phase as the reference serialises them, rounds per phase).
+//
+// Every share equals the reference's (component p and p-1 of the
+// component-form simulation): the PRF draws use the same stream indices as
+// the single-GPU engine, and the OR tree is the reference's
+// halving tree, so even the aggregate shares and the stream positions match.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/irismpc_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace irisgpu;
+
+namespace {
+
+constexpr int kThreads = 256;
+inline unsigned nblk(uint64_t n, unsigned b = kThreads) { return (unsigned)((n + b - 1) / b); }
+__host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline uint64_t rup(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
+
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes) {
+    if (p && bytes <= cap) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return false;
+    cap = bytes ? bytes : 16;
+    return true;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// ============================================================== transports
+
+enum Phase { kDot = 0, kLift = 1, kOt = 2, kMsb = 3, kOr = 4, kPhases = 5 };
+
+struct Msg {
+  int peer;      // party index 0..2
+  void* buf;     // device memory
+  size_t bytes;  // bytes on the wire
+};
+
+struct Transport {
+  virtual ~Transport() = default;
+  // One protocol step: all sends and receives, ordered on stream st.
+  virtual std::string exchange(int self, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
+                               cudaStream_t st) = 0;
+};
+
+// ---- NCCL, resolved at run time (the libnccl torch already loaded, else the system one)
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+    a.send = (decltype(a.send))dlsym(h, "ncclSend");
+    a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
+    a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
+    a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
+    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.group_start &&
+           a.group_end && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  ~NcclTransport() override {
+    if (comm && nccl().ok) nccl().comm_destroy(comm);
+  }
+  std::string exchange(int, const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t st) override {
+    const NcclApi& n = nccl();
+    ncclResult_t r = n.group_start();
+    for (const Msg& m : sends)
+      if (r == ncclSuccess && m.bytes) r = n.send(m.buf, m.bytes, ncclUint8, m.peer, comm, st);
+    for (const Msg& m : recvs)
+      if (r == ncclSuccess && m.bytes) r = n.recv(m.buf, m.bytes, ncclUint8, m.peer, comm, st);
+    const ncclResult_t r2 = n.group_end();
+    if (r != ncclSuccess) return std::string("nccl: ") + n.error_string(r);
+    if (r2 != ncclSuccess) return std::string("nccl: ") + n.error_string(r2);
+    return "";
+  }
+};
+
+}  // namespace
+
+// ---- in-process mailbox (three parties in one process, one host thread each)
+struct irismpc_gpu_inproc {
+  struct Item {
+    void* buf;
+    size_t bytes;
+    cudaEvent_t ev;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<Item> q[3][3];  // [from][to]
+};
+
+namespace {
+
+struct InProcTransport : Transport {
+  irismpc_gpu_inproc* net = nullptr;
+  std::string exchange(int self, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
+                       cudaStream_t st) override {
+    for (const Msg& m : sends) {
+      irismpc_gpu_inproc::Item it{nullptr, m.bytes, nullptr};
+      if (cudaMalloc(&it.buf, m.bytes ? m.bytes : 16) != cudaSuccess) return "inproc: oom";
+      if (m.bytes) cudaMemcpyAsync(it.buf, m.buf, m.bytes, cudaMemcpyDeviceToDevice, st);
+      cudaEventCreateWithFlags(&it.ev, cudaEventDisableTiming);
+      cudaEventRecord(it.ev, st);
+      std::lock_guard<std::mutex> g(net->mu);
+      net->q[self][m.peer].push_back(it);
+      net->cv.notify_all();
+    }
+    for (const Msg& m : recvs) {
+      irismpc_gpu_inproc::Item it;
+      {
+        std::unique_lock<std::mutex> g(net->mu);
+        auto& q = net->q[m.peer][self];
+        if (!net->cv.wait_for(g, std::chrono::seconds(120), [&] { return !q.empty(); }))
+          return "inproc: receive timed out";  // InProcNet::kTimeout
+        it = q.front();
+        q.pop_front();
+      }
+      if (it.bytes != m.bytes) return "inproc: bad payload size";
+      cudaStreamWaitEvent(st, it.ev, 0);
+      if (m.bytes) cudaMemcpyAsync(m.buf, it.buf, m.bytes, cudaMemcpyDeviceToDevice, st);
+      cudaStreamSynchronize(st);
+      cudaFree(it.buf);
+      cudaEventDestroy(it.ev);
+    }
+    return "";
+  }
+};
+
+// ============================================================== kernels
+
+// 64-bit stream words [e, e + 8) of one seed, warp-cooperative like prf_window
+// (the neighbour lane's block arrives by shuffle when e % 8 != 0).
+__device__ __forceinline__ void prf_window64(const SeedKey& key, uint64_t e, bool next_contig, uint64_t out[8]) {
+  uint32_t blk[16], nb[16];
+  const uint64_t b = e / 8;
+  chacha12_block(key, b, 0, blk);
+  const int r = (int)(e % 8);
+  if (r == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = chacha_word(blk, i);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) nb[i] = __shfl_down_sync(0xFFFFFFFFu, blk[i], 1);
+  if (!next_contig) chacha12_block(key, b + 1, 0, nb);
+  uint64_t w[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    w[i] = chacha_word(blk, i);
+    w[8 + i] = chacha_word(nb, i);
+  }
+  switch (r) {  // warp-uniform: one static selection
+#define SEL(R)                                   \
+  case R:                                        \
+    _Pragma("unroll") for (int i = 0; i < 8; ++i) out[i] = w[R + i]; \
+    break;
+    SEL(1) SEL(2) SEL(3) SEL(4) SEL(5) SEL(6)
+    default:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = w[7 + i];
+#undef SEL
+  }
+}
+
+// reshare (zero_ring<16>): own = z + F(seed_own) - F(seed_prev), hd at e = pos + i,
+// ml at pos + n + i.  Thread -> 8 lanes (warp-contiguous windows).
+__global__ void k_pty_reshare(const uint16_t* __restrict__ zh, const uint16_t* __restrict__ zm, uint64_t n,
+                              SeedKey own, SeedKey prev, uint64_t pos_own, uint64_t pos_prev,
+                              uint16_t* __restrict__ out_h, uint16_t* __restrict__ out_m) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t L8 = t * 8;
+  const uint64_t ngrp = cdiv(n, 8);
+  if ((t & ~31ull) >= ngrp) return;  // whole warp past the end
+  const bool next_contig = (t & 31) != 31;  // lane 31's neighbour window lives in the next warp
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const uint16_t* z = f == 0 ? zh : zm;
+    uint16_t* o = f == 0 ? out_h : out_m;
+    const uint64_t off = f == 0 ? 0 : n;
+    uint32_t fo[8], fp[8];
+    prf_window<1>(own, pos_own + off + L8, next_contig, fo);
+    prf_window<1>(prev, pos_prev + off + L8, next_contig, fp);
+    if (t >= ngrp) continue;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (L8 + i < n) o[L8 + i] = (uint16_t)(z[L8 + i] + fo[i] - fp[i]);
+  }
+}
+
+// share_split: K-bit lane values (own, prev components) -> bit rows
+// rows[c][j][w], lane i = bit i % 64 of word i / 64 (circuits.hpp:152-172).
+template <typename T, int K>
+__global__ void k_pty_split(const T* __restrict__ own, const T* __restrict__ prev, uint64_t n, uint64_t W,
+                            uint64_t* __restrict__ rows) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // lane
+  if ((i & ~31ull) >= n) return;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* r32 = reinterpret_cast<uint32_t*>(rows);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const uint32_t v = i < n ? (uint32_t)(c == 0 ? own[i] : prev[i]) : 0u;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t b = __ballot_sync(0xFFFFFFFFu, (v >> j) & 1u);
+      if (lane == 0) r32[((uint64_t)(c * K + j) * W) * 2 + (i >> 5)] = b;  // half-word i / 32
+    }
+  }
+}
+
+// One AND layer (and_layer, circuits.hpp:92-131) at one party: for gate g,
+// x = xa ^ xb, y = ya ^ yb (own and prev components, null rows are zero),
+// z_own = x_o y_o ^ x_p y_o ^ x_o y_p ^ F(seed_own, eo + w) ^ F(seed_prev, ep + w),
+// dead lanes of the last word masked.  Thread -> 8 words of one gate.
+struct GateDesc {
+  const uint64_t* xo[2];
+  const uint64_t* xp[2];
+  const uint64_t* yo[2];
+  const uint64_t* yp[2];
+  uint64_t* zo;
+  uint64_t eo, ep;   // stream elements of word 0 (own / prev seed)
+  uint64_t words;    // words of this gate
+  uint64_t lanes;    // live lanes
+};
+constexpr int kMaxGates = 64;
+struct GateBatch {
+  GateDesc g[kMaxGates];
+  uint32_t ngates;
+  uint64_t wblocks_per_gate;  // ceil(max words / 8)
+};
+
+__device__ __forceinline__ uint64_t ld2(const uint64_t* const a[2], uint64_t w) {
+  return (a[0] ? a[0][w] : 0ull) ^ (a[1] ? a[1][w] : 0ull);
+}
+
+__global__ void k_pty_and(const __grid_constant__ GateBatch B, SeedKey own, SeedKey prev) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t total = (uint64_t)B.ngates * B.wblocks_per_gate;
+  if ((t & ~31ull) >= total) return;
+  const uint64_t tq = t < total ? t : total - 1;
+  const uint32_t gi = (uint32_t)(tq / B.wblocks_per_gate);
+  const uint64_t wb = tq % B.wblocks_per_gate;
+  const GateDesc& G = B.g[gi];
+  const bool next_contig = (t & 31) != 31 && wb + 1 < B.wblocks_per_gate && t + 1 < total;
+  uint64_t fo[8], fp[8];
+  prf_window64(own, G.eo + 8 * wb, next_contig, fo);
+  prf_window64(prev, G.ep + 8 * wb, next_contig, fp);
+  if (t >= total) return;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t w = 8 * wb + i;
+    if (w >= G.words) break;
+    const uint64_t xo = ld2(G.xo, w), xp = ld2(G.xp, w), yo = ld2(G.yo, w), yp = ld2(G.yp, w);
+    uint64_t z = (xo & yo) ^ (xp & yo) ^ (xo & yp) ^ fo[i] ^ fp[i];
+    if (w == G.words - 1 && (G.lanes % 64)) z &= (1ull << (G.lanes % 64)) - 1;
+    G.zo[w] = z;
+  }
+}
+
+// dst = a ^ b over `words` (b may be null); a list of such ops
+struct XorOp {
+  uint64_t* dst;
+  const uint64_t* a;
+  const uint64_t* b;
+};
+constexpr int kMaxOps = 132;
+struct XorBatch {
+  XorOp op[kMaxOps];
+  uint32_t nops;
+  uint64_t words;
+};
+__global__ void k_pty_xor(const __grid_constant__ XorBatch X) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)X.nops * X.words) return;
+  const XorOp& o = X.op[t / X.words];
+  const uint64_t w = t % X.words;
+  o.dst[w] = o.a[w] ^ (o.b ? o.b[w] : 0ull);
+}
+
+// bit_inject<W> (convert.hpp:84-155), per role.  bits: own/prev bit rows of
+// the injected bit.  c1 from seed_1 at e1 + i, (c3, w0, w1) from seed_3 at e3 + 3i.
+// role 0 (P1): out (c1, c3), msg[2i], msg[2i+1] = w0 ^ m0, w1 ^ m1 -> P2
+// role 2 (P3): out own = c3, msg[i] = x2 ? w1 : w0 -> P2
+__global__ void k_pty_inject_send(int role, const uint64_t* __restrict__ bo, const uint64_t* __restrict__ bp,
+                                  uint64_t n, uint32_t mask, SeedKey own, SeedKey prev, uint64_t e1, uint64_t e3,
+                                  uint16_t* __restrict__ out_o, uint16_t* __restrict__ out_p,
+                                  uint16_t* __restrict__ msg) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (role == 0) {
+    const uint32_t x1 = (uint32_t)(bo[i / 64] >> (i % 64)) & 1u, x3 = (uint32_t)(bp[i / 64] >> (i % 64)) & 1u;
+    uint32_t blk[16];
+    chacha12_block(own, (e1 + i) / 8, 0, blk);
+    const uint32_t c1 = blk[2 * ((e1 + i) % 8)] & mask;
+    uint32_t c3w[3];
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t e = e3 + 3 * i + k;
+      chacha12_block(prev, e / 8, 0, blk);
+      c3w[k] = blk[2 * (e % 8)] & mask;
+    }
+    const uint32_t m0 = ((0u ^ x1 ^ x3) - c1 - c3w[0]) & mask, m1 = ((1u ^ x1 ^ x3) - c1 - c3w[0]) & mask;
+    msg[2 * i] = (uint16_t)((c3w[1] ^ m0) & mask);
+    msg[2 * i + 1] = (uint16_t)((c3w[2] ^ m1) & mask);
+    out_o[i] = (uint16_t)c1;
+    out_p[i] = (uint16_t)c3w[0];
+  } else {
+    const uint32_t x2 = (uint32_t)(bp[i / 64] >> (i % 64)) & 1u;
+    uint32_t blk[16], c3w[3];
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t e = e3 + 3 * i + k;
+      chacha12_block(own, e / 8, 0, blk);
+      c3w[k] = blk[2 * (e % 8)] & mask;
+    }
+    msg[i] = (uint16_t)(x2 ? c3w[2] : c3w[1]);
+    out_o[i] = (uint16_t)c3w[0];
+  }
+}
+// role 1 (P2): c1 from its prev stream, c2 = k_{x2} ^ w_{x2}; out (c2, c1); msg[i] = c2 -> P3
+__global__ void k_pty_inject_p2(const uint64_t* __restrict__ bo, uint64_t n, uint32_t mask, SeedKey prev,
+                                uint64_t e1, const uint16_t* __restrict__ ks, const uint16_t* __restrict__ ws,
+                                uint16_t* __restrict__ out_o, uint16_t* __restrict__ out_p,
+                                uint16_t* __restrict__ msg) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t x2 = (uint32_t)(bo[i / 64] >> (i % 64)) & 1u;
+  uint32_t blk[16];
+  chacha12_block(prev, (e1 + i) / 8, 0, blk);
+  const uint32_t c1 = blk[2 * ((e1 + i) % 8)] & mask;
+  const uint32_t c2 = ((uint32_t)ks[2 * i + x2] ^ (uint32_t)ws[i]) & mask;
+  msg[i] = (uint16_t)c2;
+  out_o[i] = (uint16_t)c2;
+  out_p[i] = (uint16_t)c1;
+}
+
+// lift output and comparison input per component (convert.hpp:169-192,
+// engine.hpp:94-120): ml32 = ml - (inj17 << 17) - (inj16 << 16), diff = a ml32 - b hd
+__global__ void k_pty_diff(const uint16_t* __restrict__ ml, const uint16_t* __restrict__ hd,
+                           const uint16_t* __restrict__ i17, const uint16_t* __restrict__ i16, uint64_t n2,
+                           uint32_t a, uint32_t b, uint32_t* __restrict__ ml32, uint32_t* __restrict__ diff) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // [comp][lane]
+  if (i >= n2) return;
+  const uint32_t m = (uint32_t)ml[i] - ((uint32_t)i17[i] << 17) - ((uint32_t)i16[i] << 16);
+  ml32[i] = m;
+  diff[i] = a * m - b * (uint32_t)hd[i];
+}
+
+// OR tree: gather each group's lanes of the MSB bit rows into its row
+struct OrGroup {
+  uint64_t len;        // lanes of the group
+  uint64_t db_lane0;   // first DB lane (contiguous DB part)
+  uint64_t db_len;     // DB lanes
+  uint64_t pair_off;   // offset of its pair-lane list in `pairs`
+  uint64_t row_off;    // word offset of its row in the pool
+};
+__global__ void k_pty_or_gather(const OrGroup* __restrict__ G, uint32_t ngroups, const uint64_t* __restrict__ pairs,
+                                const uint64_t* __restrict__ mo, const uint64_t* __restrict__ mp,
+                                uint64_t* __restrict__ pool_o, uint64_t* __restrict__ pool_p, uint64_t max_words) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)ngroups * max_words) return;
+  const OrGroup g = G[t / max_words];
+  const uint64_t w = t % max_words;
+  if (w * 64 >= g.len) return;
+  uint64_t o = 0, p = 0;
+  for (int b = 0; b < 64; ++b) {
+    const uint64_t i = w * 64 + b;
+    if (i >= g.len) break;
+    const uint64_t ln = i < g.db_len ? g.db_lane0 + i : pairs[g.pair_off + (i - g.db_len)];
+    o |= ((mo[ln / 64] >> (ln % 64)) & 1ull) << b;
+    p |= ((mp[ln / 64] >> (ln % 64)) & 1ull) << b;
+  }
+  pool_o[g.row_off + w] = o;
+  pool_p[g.row_off + w] = p;
+}
+
+// one or_tree_batch level: lo = lanes [0, na), hi = lanes [na, len)
+struct OrLevel {
+  uint64_t src_off, dst_off, na, nb, wa, wb;
+  uint64_t t_off;   // word offset into the AND output (concatenated over groups)
+  uint64_t eo, ep;  // stream elements (own / prev seed) of its first AND word
+};
+__device__ __forceinline__ uint64_t hi_word(const uint64_t* row, uint64_t na, uint64_t nb, uint64_t w) {
+  const uint64_t bit = na + 64 * w;
+  if (64 * w >= nb) return 0;
+  const uint64_t q = bit / 64, r = bit % 64;
+  uint64_t v = row[q] >> r;
+  if (r && 64 * w + (64 - r) < nb) v |= row[q + 1] << (64 - r);
+  const uint64_t left = nb - 64 * w;
+  if (left < 64) v &= (1ull << left) - 1;
+  return v;
+}
+__global__ void k_pty_or_and(const OrLevel* __restrict__ L, uint32_t nl, uint64_t max_wb, const uint64_t* __restrict__ po,
+                             const uint64_t* __restrict__ pp, SeedKey own, SeedKey prev, uint64_t* __restrict__ tz) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)nl * max_wb) return;
+  const OrLevel l = L[t / max_wb];
+  const uint64_t w = t % max_wb;
+  if (w >= l.wb) return;
+  const uint64_t lo_o = po[l.src_off + w], lo_p = pp[l.src_off + w];
+  const uint64_t hi_o = hi_word(po + l.src_off, l.na, l.nb, w), hi_p = hi_word(pp + l.src_off, l.na, l.nb, w);
+  uint32_t blk[16];
+  chacha12_block(own, (l.eo + w) / 8, 0, blk);
+  const uint64_t fo = chacha_word(blk, (int)((l.eo + w) % 8));
+  chacha12_block(prev, (l.ep + w) / 8, 0, blk);
+  const uint64_t fp = chacha_word(blk, (int)((l.ep + w) % 8));
+  uint64_t z = (lo_o & hi_o) ^ (lo_p & hi_o) ^ (lo_o & hi_p) ^ fo ^ fp;
+  if (w == l.wb - 1 && (l.nb % 64)) z &= (1ull << (l.nb % 64)) - 1;
+  tz[l.t_off + w] = z;
+}
+// fold: new = lo ^ hi ^ t over wa words, both components
+__global__ void k_pty_or_fold(const OrLevel* __restrict__ L, uint32_t nl, uint64_t max_wa, uint64_t* __restrict__ po,
+                              uint64_t* __restrict__ pp, const uint64_t* __restrict__ to,
+                              const uint64_t* __restrict__ tp, uint64_t* __restrict__ qo, uint64_t* __restrict__ qp) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)nl * max_wa) return;
+  const OrLevel l = L[t / max_wa];
+  const uint64_t w = t % max_wa;
+  if (w >= l.wa) return;
+  uint64_t lo_o = po[l.src_off + w], lo_p = pp[l.src_off + w];
+  const uint64_t rem = l.na - 64 * w;  // lo has na lanes
+  if (rem < 64) {
+    lo_o &= (1ull << rem) - 1;
+    lo_p &= (1ull << rem) - 1;
+  }
+  const uint64_t ho = hi_word(po + l.src_off, l.na, l.nb, w), hp = hi_word(pp + l.src_off, l.na, l.nb, w);
+  const uint64_t tzo = w < l.wb ? to[l.t_off + w] : 0, tzp = w < l.wb ? tp[l.t_off + w] : 0;
+  qo[l.dst_off + w] = lo_o ^ ho ^ tzo;
+  qp[l.dst_off + w] = lo_p ^ hp ^ tzp;
+}
+
+// pack bit 0 of group rows (or any word rows) into bytes for open_bits_to
+__global__ void k_pty_pack_groups(const uint64_t* __restrict__ pool, const uint64_t* __restrict__ row_off,
+                                  uint32_t ngroups, uint8_t* __restrict__ out) {
+  const uint32_t byte = blockIdx.x * blockDim.x + threadIdx.x;
+  if (byte >= (ngroups + 7) / 8) return;
+  uint32_t v = 0;
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t g = byte * 8 + b;
+    if (g < ngroups && row_off[g] != ~0ull) v |= (uint32_t)(pool[row_off[g]] & 1ull) << b;
+  }
+  out[byte] = (uint8_t)v;
+}
+
+}  // namespace
+
+// ============================================================== context
+
+struct PartyField {
+  FieldFmt fmt{};
+  uint32_t slots = 1;  // DB planes: own (+ prev for replicated)
+  uint32_t nseg = 1;
+  DBuf db, q, qa, pc;
+  CUtensorMap tA, tB, tQA;
+  uint32_t ncols_pad_cur = 0;
+  uint64_t qa_spad = 0;
+};
+
+struct irismpc_gpu_party {
+  irismpc_gpu_config cfg{};
+  int p = 0;  // 0..2
+  int shamir = 0;
+  uint32_t l = 0, l_pad = 0;
+  uint64_t rec = 0;
+  SeedKey own{}, prev{};
+  uint64_t pos[2] = {0, 0};  // stream positions of seed_own, seed_prev
+  Transport* net = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[2];
+  PartyField fld[2];
+  uint64_t s = 0, s_pad = 0;
+  bool db_loaded = false;
+  std::string err;
+  uint64_t led_bytes[kPhases] = {0, 0, 0, 0, 0}, led_rounds[kPhases] = {0, 0, 0, 0, 0}, wire = 0;
+  // work buffers
+  DBuf qpay, dots, rs, rows, carry, chain, zbuf, zrecv, inj, msg, msg2, ml32, diff, bits, pairs, groups, levels,
+      pool[2], tz[2], rowoff, open_buf[3];
+  uint64_t tap_n = 0;
+};
+
+namespace {
+
+int pfail(irismpc_gpu_party* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+#define PCK(c, x)                                                                                        \
+  do {                                                                                                   \
+    cudaError_t e_ = (x);                                                                                \
+    if (e_ != cudaSuccess) return pfail(c, IRISMPC_GPU_ERR_DEVICE, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int next_of(int p) { return (p + 1) % 3; }
+int prev_of(int p) { return (p + 2) % 3; }
+
+// one protocol step through the transport + the ledger (counted bytes per the
+// reference's serialisation; rounds per ctx.comm.round call of that phase)
+int step(irismpc_gpu_party* c, Phase ph, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
+         const std::vector<uint64_t>& counted, uint32_t rounds) {
+  for (size_t i = 0; i < sends.size(); ++i) {
+    c->led_bytes[ph] += i < counted.size() ? counted[i] : sends[i].bytes;
+    c->wire += sends[i].bytes;
+  }
+  c->led_rounds[ph] += rounds;
+  const std::string e = c->net->exchange(c->p, sends, recvs, c->st);
+  if (!e.empty()) return pfail(c, IRISMPC_GPU_ERR_DEVICE, e);
+  return 0;
+}
+
+int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party** out, std::string* why) {
+  if (!cfg || !out || party < 1 || party > 3) return IRISMPC_GPU_ERR_CONFIG;
+  if (cfg->variant != IRISMPC_GPU_VARIANT_MPC_LIFT) {
+    *why = "party mode implements the mpc-lift variant";
+    return IRISMPC_GPU_ERR_CONFIG;
+  }
+  if (cfg->backend > 1 || cfg->l == 0 || cfg->l % 8 != 0) return IRISMPC_GPU_ERR_BOUNDS;
+  if (cfg->a > cfg->b || cfg->m != 16 || cfg->b != (1u << 16) || cfg->rotations % 2 == 0) return IRISMPC_GPU_ERR_BOUNDS;
+  const uint64_t t = 1ull << 32, bl = (uint64_t)cfg->b * cfg->l;
+  if (!(bl < t / 4 && bl < t - (t >> 1))) return IRISMPC_GPU_ERR_BOUNDS;
+  if (cfg->rotations > 31) return IRISMPC_GPU_ERR_CONFIG;
+  if (cfg->backend == IRISMPC_GPU_BACKEND_SHAMIR && cfg->rotations > 1 && (cfg->l / 64) % 2 != 0)
+    return IRISMPC_GPU_ERR_BOUNDS;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return IRISMPC_GPU_ERR_DEVICE;
+  auto* c = new irismpc_gpu_party;
+  c->cfg = *cfg;
+  c->p = (int)party - 1;
+  c->shamir = cfg->backend == IRISMPC_GPU_BACKEND_SHAMIR;
+  c->l = cfg->l;
+  c->l_pad = (uint32_t)rup(cfg->l, kGemmBK);
+  c->rec = irismpc_gpu_record_bytes(cfg->backend, cfg->variant, cfg->l);
+  std::memcpy(c->own.k, cfg->seeds, 16);
+  std::memcpy(c->prev.k, cfg->seeds + 16, 16);
+  const uint64_t code_b = c->rec / 2;  // mpc-lift: code and mask records have the same size
+  for (int fi = 0; fi < 2; ++fi) {
+    PartyField& f = c->fld[fi];
+    f.fmt.rec_bytes = c->rec;
+    f.fmt.off = fi == 0 ? 0 : code_b;
+    f.fmt.width = 2;
+    f.fmt.limbs = 2;
+    f.slots = c->shamir ? 1 : 2;
+    f.nseg = c->shamir ? 1 : 2;
+  }
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  cudaEventCreate(&c->ev[0]);
+  cudaEventCreate(&c->ev[1]);
+  // lambda_p for the Shamir parse (the same constants as the 3-party context)
+  uint32_t lam[6] = {1, 2, 0xFFFFFFFFu, 0xFFFFFFFEu, 1, 0};  // 1+2X, -(1+2X), 1 (galois.hpp:124-128)
+  set_lambda(lam);
+  *out = c;
+  return 0;
+}
+
+// parse one payload (rows of this party's records) into a field's planes
+void parse_party_rows(irismpc_gpu_party* c, PartyField& f, const uint8_t* pay, uint64_t rows, uint64_t s_pad,
+                      uint8_t* planes) {
+  FieldFmt fo = f.fmt;
+  fo.slot = 0;
+  launch_parse_field(pay, rows, 0, c->l, c->l_pad, s_pad, c->p, c->shamir, fo, planes, c->st);
+  if (!c->shamir) {
+    FieldFmt fp = f.fmt;
+    fp.slot = 1;
+    fp.take_prev = 1;
+    launch_parse_field(pay, rows, 0, c->l, c->l_pad, s_pad, c->p, c->shamir, fp, planes, c->st);
+  }
+}
+
+// bit_extract_sum over summand rows X (own/prev components of summand p and
+// p-1 only, share_split) for instances `idx`, rows j >= K zero.  Gate g of the
+// call uses stream elements base[own|prev] + g W + w.  Results -> res_o/res_p rows.
+int bit_extract(irismpc_gpu_party* c, Phase ph, const uint64_t* Xo, const uint64_t* Xp, int K,
+                const std::vector<int>& idx, uint64_t n, uint64_t W, uint64_t base_o, uint64_t base_p,
+                uint64_t* res_o, uint64_t* res_p) {
+  const int p = c->p;
+  const int ninst = (int)idx.size();
+  int maxm = 0;
+  for (int m : idx) maxm = std::max(maxm, m);
+  auto XR = [&](int comp, int j) -> const uint64_t* {  // own / prev component of summand row j
+    if (j >= K) return nullptr;
+    return (comp == 0 ? Xo : Xp) + (uint64_t)j * W;
+  };
+  // component views of a_k_j: own comp nonzero iff k == p, prev iff k == p - 1
+  auto A = [&](int k, int comp, int j) -> const uint64_t* {
+    if (comp == 0) return k == p ? XR(0, j) : nullptr;
+    return k == prev_of(p) ? XR(1, j) : nullptr;
+  };
+  int total_fa = 0;
+  for (int m : idx) total_fa += m;
+  if (!c->carry.ensure(2ull * total_fa * W * 8 + 16) || !c->chain.ensure(2ull * ninst * W * 8 + 16) ||
+      !c->zbuf.ensure((uint64_t)std::max(total_fa, ninst) * W * 8 + 16) ||
+      !c->zrecv.ensure((uint64_t)std::max(total_fa, ninst) * W * 8 + 16))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (bit extract)");
+  uint64_t* carry = c->carry.as<uint64_t>();  // [comp][fa gate][W]
+  uint64_t* chain = c->chain.as<uint64_t>();  // [comp][inst][W]
+  uint64_t* zo = c->zbuf.as<uint64_t>();
+  uint64_t* zp = c->zrecv.as<uint64_t>();
+  auto carry_row = [&](int comp, int g) { return carry + ((uint64_t)comp * total_fa + g) * W; };
+  auto chain_row = [&](int comp, int k) { return chain + ((uint64_t)comp * ninst + k) * W; };
+  std::vector<int> fa0(ninst);
+  const uint64_t wbl = cdiv(W, 8);
+  const uint64_t row_bytes = cdiv(n, 8);
+  uint64_t g = 0;
+  // ---- FA layer: one round, gates in instance order then j
+  {
+    GateBatch B{};
+    int gi = 0;
+    for (int k = 0; k < ninst; ++k) {
+      fa0[k] = gi;
+      for (int j = 0; j < idx[k]; ++j, ++gi) {
+        GateDesc& d = B.g[gi];
+        // t1 = a0 ^ a2, t2 = a1 ^ a2
+        d.xo[0] = A(0, 0, j); d.xo[1] = A(2, 0, j);
+        d.xp[0] = A(0, 1, j); d.xp[1] = A(2, 1, j);
+        d.yo[0] = A(1, 0, j); d.yo[1] = A(2, 0, j);
+        d.yp[0] = A(1, 1, j); d.yp[1] = A(2, 1, j);
+        d.zo = zo + (uint64_t)gi * W;
+        d.eo = base_o + (g + gi) * W;
+        d.ep = base_p + (g + gi) * W;
+        d.words = W;
+        d.lanes = n;
+      }
+    }
+    B.ngates = (uint32_t)gi;
+    B.wblocks_per_gate = wbl;
+    k_pty_and<<<nblk(rup((uint64_t)gi * wbl, 32)), kThreads, 0, c->st>>>(B, c->own, c->prev);
+    PCK(c, cudaGetLastError());
+    int rc = step(c, ph, {{next_of(p), zo, (size_t)gi * W * 8}}, {{prev_of(p), zp, (size_t)gi * W * 8}},
+                  {(uint64_t)gi * row_bytes}, 1);
+    if (rc) return rc;
+    // carry = z ^ a2
+    XorBatch ops{};
+    ops.words = W;
+    for (int q = 0; q < gi; ++q) {
+      int k = 0;
+      while (k + 1 < ninst && fa0[k + 1] <= q) ++k;
+      const int j = q - fa0[k];
+      ops.op[ops.nops++] = {carry_row(0, q), zo + (uint64_t)q * W, A(2, 0, j)};
+      ops.op[ops.nops++] = {carry_row(1, q), zp + (uint64_t)q * W, A(2, 1, j)};
+    }
+    k_pty_xor<<<nblk((uint64_t)ops.nops * W), kThreads, 0, c->st>>>(ops);
+    g += gi;
+  }
+  // ---- ripple chain: round t, gates in instance order (circuits.hpp:263-288)
+  for (int t = 1; t + 1 <= maxm; ++t) {
+    GateBatch B{};
+    std::vector<int> which;
+    for (int k = 0; k < ninst; ++k) {
+      if (t + 1 > idx[k]) continue;
+      const int gi = (int)which.size();
+      GateDesc& d = B.g[gi];
+      const int cg = fa0[k] + (t - 1);  // carry_{t-1}
+      if (t == 1) {
+        d.xo[0] = XR(0, t); d.xp[0] = XR(1, t);  // s_1 (own comp = X row: exactly one summand per component)
+        d.yo[0] = carry_row(0, cg); d.yp[0] = carry_row(1, cg);
+      } else {
+        d.xo[0] = XR(0, t); d.xo[1] = chain_row(0, k);
+        d.xp[0] = XR(1, t); d.xp[1] = chain_row(1, k);
+        d.yo[0] = carry_row(0, cg); d.yo[1] = chain_row(0, k);
+        d.yp[0] = carry_row(1, cg); d.yp[1] = chain_row(1, k);
+      }
+      d.zo = zo + (uint64_t)gi * W;
+      d.eo = base_o + (g + gi) * W;
+      d.ep = base_p + (g + gi) * W;
+      d.words = W;
+      d.lanes = n;
+      which.push_back(k);
+    }
+    const int gn = (int)which.size();
+    B.ngates = (uint32_t)gn;
+    B.wblocks_per_gate = wbl;
+    k_pty_and<<<nblk(rup((uint64_t)gn * wbl, 32)), kThreads, 0, c->st>>>(B, c->own, c->prev);
+    PCK(c, cudaGetLastError());
+    int rc = step(c, ph, {{next_of(p), zo, (size_t)gn * W * 8}}, {{prev_of(p), zp, (size_t)gn * W * 8}},
+                  {(uint64_t)gn * row_bytes}, 1);
+    if (rc) return rc;
+    XorBatch ops{};
+    ops.words = W;
+    for (int q = 0; q < gn; ++q) {
+      const int k = which[q];
+      ops.op[ops.nops++] = {chain_row(0, k), zo + (uint64_t)q * W, t == 1 ? nullptr : chain_row(0, k)};
+      ops.op[ops.nops++] = {chain_row(1, k), zp + (uint64_t)q * W, t == 1 ? nullptr : chain_row(1, k)};
+    }
+    k_pty_xor<<<nblk((uint64_t)ops.nops * W), kThreads, 0, c->st>>>(ops);
+    g += gn;
+  }
+  // ---- result_k = s_m ^ carry_{m-1} ^ chain (m >= 2): two passes (the second XORs in place)
+  {
+    XorBatch first{}, second{};
+    first.words = second.words = W;
+    for (int k = 0; k < ninst; ++k) {
+      const int m = idx[k];
+      for (int comp = 0; comp < 2; ++comp) {
+        uint64_t* dst = (comp == 0 ? res_o : res_p) + (uint64_t)k * W;
+        first.op[first.nops++] = {dst, carry_row(comp, fa0[k] + m - 1), m >= 2 ? chain_row(comp, k) : nullptr};
+        if (const uint64_t* sm = XR(comp, m)) second.op[second.nops++] = {dst, dst, sm};
+      }
+    }
+    k_pty_xor<<<nblk((uint64_t)first.nops * W), kThreads, 0, c->st>>>(first);
+    if (second.nops) k_pty_xor<<<nblk((uint64_t)second.nops * W), kThreads, 0, c->st>>>(second);
+  }
+  PCK(c, cudaGetLastError());
+  return 0;
+}
+
+// bit_inject<Wd> of bit rows (bo, bp) -> out own/prev u16 components
+int bit_inject(irismpc_gpu_party* c, const uint64_t* bo, const uint64_t* bp, uint64_t n, int Wd, uint64_t e1,
+               uint64_t e3, uint16_t* out_o, uint16_t* out_p) {
+  const int p = c->p;
+  const uint32_t mask = (1u << Wd) - 1;
+  const size_t eb = 2;  // Ring<15>, Ring<16>: 2-byte elements
+  if (!c->msg.ensure(2 * n * eb + 16) || !c->msg2.ensure(2 * n * eb + 16))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (inject)");
+  uint16_t* m1 = c->msg.as<uint16_t>();
+  uint16_t* m2 = c->msg2.as<uint16_t>();
+  int rc = 0;
+  if (p == 0) {  // P1: sender
+    k_pty_inject_send<<<nblk(n), kThreads, 0, c->st>>>(0, bo, bp, n, mask, c->own, c->prev, e1, e3, out_o, out_p, m1);
+    rc = step(c, kOt, {{1, m1, 2 * n * eb}}, {}, {}, 1);
+    if (!rc) rc = step(c, kOt, {}, {}, {}, 1);  // c_2 forwarding stage, party 1 idle
+  } else if (p == 2) {  // P3: helper
+    k_pty_inject_send<<<nblk(n), kThreads, 0, c->st>>>(2, bo, bp, n, mask, c->own, c->prev, e1, e3, out_o, out_p, m1);
+    rc = step(c, kOt, {{1, m1, n * eb}}, {}, {}, 1);
+    if (!rc) rc = step(c, kOt, {}, {{1, out_p, n * eb}}, {}, 1);  // c_2 from P2 -> prev component
+  } else {  // P2: receiver
+    rc = step(c, kOt, {}, {{0, m1, 2 * n * eb}, {2, m2, n * eb}}, {}, 1);
+    if (rc) return rc;
+    if (!c->zbuf.ensure(n * eb + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (inject)");
+    uint16_t* c2 = c->zbuf.as<uint16_t>();
+    k_pty_inject_p2<<<nblk(n), kThreads, 0, c->st>>>(bo, n, mask, c->prev, e1, m1, m2, out_o, out_p, c2);
+    rc = step(c, kOt, {{2, c2, n * eb}}, {}, {}, 1);
+  }
+  if (rc) return rc;
+  PCK(c, cudaGetLastError());
+  return 0;
+}
+
+// open packed bits to P1 (open_bits_to, circuits.hpp:449-486); P1 gets `out`
+int open_to_p1(irismpc_gpu_party* c, const uint8_t* own_bytes, const uint8_t* prev_bytes, uint64_t lanes,
+               uint8_t* out_host) {
+  const uint64_t bytes = cdiv(lanes, 8);
+  const int p = c->p;
+  if (p == 0) {
+    if (!c->open_buf[0].ensure(bytes + 16) || !c->open_buf[1].ensure(bytes + 16))
+      return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (open)");
+    int rc = step(c, kOr, {}, {{1, c->open_buf[0].p, bytes}, {2, c->open_buf[1].p, bytes}}, {}, 1);
+    if (rc) return rc;
+    std::vector<uint8_t> a(bytes), b(bytes), mo(bytes), mp(bytes);
+    PCK(c, cudaMemcpyAsync(a.data(), c->open_buf[0].p, bytes, cudaMemcpyDeviceToHost, c->st));
+    PCK(c, cudaMemcpyAsync(b.data(), c->open_buf[1].p, bytes, cudaMemcpyDeviceToHost, c->st));
+    PCK(c, cudaMemcpyAsync(mo.data(), own_bytes, bytes, cudaMemcpyDeviceToHost, c->st));
+    PCK(c, cudaMemcpyAsync(mp.data(), prev_bytes, bytes, cudaMemcpyDeviceToHost, c->st));
+    PCK(c, cudaStreamSynchronize(c->st));
+    if (a != b) return pfail(c, IRISMPC_GPU_ERR_INCONSISTENT, "open_bits_to: cross-check failed");
+    for (uint64_t i = 0; i < lanes; ++i) out_host[i] = (uint8_t)(((mo[i / 8] ^ mp[i / 8] ^ a[i / 8]) >> (i % 8)) & 1);
+    return 0;
+  }
+  // P2 (next of P1) sends its own component, P3 its prev
+  const uint8_t* src = p == 1 ? own_bytes : prev_bytes;
+  return step(c, kOr, {{0, const_cast<uint8_t*>(src), bytes}}, {}, {}, 1);
+}
+
+uint64_t ref_or_draws(uint64_t groups, uint64_t len, uint64_t* rounds) {
+  uint64_t d = 0, r = 0;
+  while (len > 1) {
+    const uint64_t na = (len + 1) / 2, nb = len - na;
+    d += groups * cdiv(nb, 64);
+    len = na;
+    ++r;
+  }
+  if (rounds) *rounds = r;
+  return d;
+}
+
+int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t persons, int membership,
+                uint8_t* match_out, uint8_t* row_bits_out, irismpc_gpu_party_stats* stats) {
+  if (!c->db_loaded) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "no database loaded");
+  const uint32_t ncodes = membership ? 1u : 2u * persons;
+  if (qlen % c->rec != 0) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "query payload size mismatch");
+  if (qlen / c->rec != ncodes)
+    return pfail(c, IRISMPC_GPU_ERR_CONFIG,
+                 membership ? "membership expects exactly one query code" : "batch query expects 2 codes per person");
+  for (auto& x : c->led_bytes) x = 0;
+  for (auto& x : c->led_rounds) x = 0;
+  c->wire = 0;
+  const int p = c->p;
+  const uint32_t r = membership ? 1u : c->cfg.rotations;
+  const uint64_t S = c->s, ncols = (uint64_t)ncodes * r;
+  const uint32_t ncols_pad = (uint32_t)rup(ncols ? ncols : 1, kGemmBN);
+  const uint64_t npairs = membership ? 0 : (uint64_t)persons * (persons ? persons - 1 : 0) / 2 * 4 * r;
+  const uint64_t n = ncols * S + npairs;
+  const uint64_t W = cdiv(n, 64);
+  const uint32_t ngroups = membership ? 1u : persons;
+  const int ko = p, kp = prev_of(p);  // seed indices of own / prev
+  cudaStream_t st = c->st;
+  PCK(c, cudaEventRecord(c->ev[0], st));
+  // ---- payload + planes
+  if (!c->qpay.ensure(qlen)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query)");
+  PCK(c, cudaMemcpyAsync(c->qpay.p, hq, qlen, cudaMemcpyHostToDevice, st));
+  const uint8_t* dq = c->qpay.as<uint8_t>();
+  if (!c->dots.ensure(2 * (n + 8) * 2) || !c->rs.ensure(4 * (n + 8) * 2))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dots)");
+  uint16_t* dh = c->dots.as<uint16_t>();
+  uint16_t* dm = dh + n + 8;
+  for (int fi = 0; fi < 2; ++fi) {
+    PartyField& f = c->fld[fi];
+    const uint64_t rows = 3ull * f.nseg * f.fmt.limbs * ncols_pad;
+    if (ncols_pad != f.ncols_pad_cur) {
+      if (!f.q.ensure(rows * c->l_pad)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query planes)");
+      PCK(c, cudaMemsetAsync(f.q.p, 0, rows * c->l_pad, st));
+      if (make_plane_tmap(&f.tB, f.q.p, rows, c->l_pad, gemm_bn(2) / 2))
+        return pfail(c, IRISMPC_GPU_ERR_DEVICE, "tensor map (query)");
+      f.ncols_pad_cur = ncols_pad;
+    }
+    // B planes of this party's payload (problem 0; the kernel also fills 1, 2 from the same bytes)
+    launch_parse_query_field(dq, dq, dq, ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir, f.fmt, f.q.as<uint8_t>(), st);
+    uint16_t* out = fi == 0 ? dh : dm;
+    if (S) {
+      GemmArgs g{};
+      g.s_pad = (uint32_t)c->s_pad;
+      g.nb_rows = ncols_pad;
+      g.nkb_seg = c->l_pad / kGemmBK;
+      g.nseg = f.nseg;
+      g.rep = f.nseg == 2;
+      g.nprob = 1;
+      g.limbs = 2;
+      g.s_valid = (uint32_t)S;
+      g.ncols = (uint32_t)ncols;
+      g.out = out;
+      g.out_pstride = ncols * S;
+      g.out_cstride = (uint32_t)S;
+      launch_gemm(f.tA, f.tB, g, (uint32_t)(c->s_pad / kGemmBM), (uint32_t)cdiv(ncols, 256), st);
+    }
+    if (npairs) {
+      const uint64_t spq = rup(ncodes, 2 * kGemmBM);
+      const uint64_t arows = (uint64_t)f.slots * f.fmt.limbs * spq;
+      if (spq != f.qa_spad) {
+        if (!f.qa.ensure(arows * c->l_pad)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair planes)");
+        PCK(c, cudaMemsetAsync(f.qa.p, 0, arows * c->l_pad, st));
+        if (make_plane_tmap(&f.tQA, f.qa.p, arows, c->l_pad, kGemmBM))
+          return pfail(c, IRISMPC_GPU_ERR_DEVICE, "tensor map (pairs)");
+        f.qa_spad = spq;
+      }
+      parse_party_rows(c, f, dq, ncodes, spq, f.qa.as<uint8_t>());
+      if (!f.pc.ensure(ncols * ncodes * 2 + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
+      GemmArgs g{};
+      g.s_pad = (uint32_t)spq;
+      g.nb_rows = ncols_pad;
+      g.nkb_seg = c->l_pad / kGemmBK;
+      g.nseg = f.nseg;
+      g.rep = f.nseg == 2;
+      g.nprob = 1;
+      g.limbs = 2;
+      g.s_valid = ncodes;
+      g.ncols = (uint32_t)ncols;
+      g.out = f.pc.p;
+      g.out_pstride = ncols * ncodes;
+      g.out_cstride = ncodes;
+      launch_gemm(f.tQA, f.tB, g, (uint32_t)(spq / kGemmBM), (uint32_t)cdiv(ncols, 256), st);
+      launch_pair_gather(f.pc.p, 2, 1, ncodes, (uint32_t)ncols, persons, r, out + ncols * S, npairs, st);
+    }
+  }
+  PCK(c, cudaGetLastError());
+  // ---- dot phase: reshare_pair<16,16>, own -> next, prev <- previous
+  uint16_t* rs_own = c->rs.as<uint16_t>();        // [hd n+8 | ml n+8]
+  uint16_t* rs_prev = rs_own + 2 * (n + 8);
+  k_pty_reshare<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1],
+                                                                  rs_own, rs_own + n + 8);
+  PCK(c, cudaGetLastError());
+  int rc = step(c, kDot, {{next_of(p), rs_own, 2 * (n + 8) * 2}}, {{prev_of(p), rs_prev, 2 * (n + 8) * 2}}, {4 * n}, 1);
+  if (rc) return rc;
+  const uint16_t* hd_o = rs_own;
+  const uint16_t* ml_o = rs_own + n + 8;
+  const uint16_t* hd_p = rs_prev;
+  const uint16_t* ml_p = rs_prev + n + 8;
+  // ---- lift<16,16>
+  if (!c->rows.ensure(2ull * 32 * W * 8 + 64) || !c->bits.ensure(4ull * W * 8 + 64) ||
+      !c->inj.ensure(4ull * (n + 8) * 2 + 64))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (lift)");
+  uint64_t* rows = c->rows.as<uint64_t>();
+  PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));
+  k_pty_split<uint16_t, 16><<<nblk(rup(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
+  uint64_t* b_o = c->bits.as<uint64_t>();  // [inst][W]: bit16, bit17
+  uint64_t* b_p = b_o + 2 * W;
+  const uint64_t ecore[3] = {2 * n, 0, 6 * n};  // inject draws before the MSB, per seed
+  rc = bit_extract(c, kLift, rows, rows + 16 * W, 16, {16, 17}, n, W, c->pos[0] + 2 * n, c->pos[1] + 2 * n, b_o, b_p);
+  if (rc) return rc;
+  uint16_t* i17 = c->inj.as<uint16_t>();  // [comp][n+8]
+  uint16_t* i16 = i17 + 2 * (n + 8);
+  // seed_1 / seed_3 element bases (own/prev stream positions by role)
+  const uint64_t pos1 = p == 0 ? c->pos[0] : (p == 1 ? c->pos[1] : 0);
+  const uint64_t pos3 = p == 0 ? c->pos[1] : (p == 2 ? c->pos[0] : 0);
+  rc = bit_inject(c, b_o + W, b_p + W, n, 15, pos1 + 2 * n + 64 * W, pos3 + 2 * n + 64 * W, i17, i17 + n + 8);
+  if (rc) return rc;
+  rc = bit_inject(c, b_o, b_p, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
+  if (rc) return rc;
+  // ---- diff, msb<32>
+  if (!c->ml32.ensure(2 * (n + 8) * 4) || !c->diff.ensure(2 * (n + 8) * 4))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (diff)");
+  uint32_t* ml32 = c->ml32.as<uint32_t>();
+  uint32_t* diff = c->diff.as<uint32_t>();
+  // components laid out [own n+8 | prev n+8] for every array
+  {
+    // ml and hd: own and prev halves are in different buffers -> two launches
+    k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_o, hd_o, i17, i16, n, c->cfg.a, c->cfg.b, ml32, diff);
+    k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_p, hd_p, i17 + n + 8, i16 + n + 8, n, c->cfg.a, c->cfg.b,
+                                             ml32 + n + 8, diff + n + 8);
+  }
+  PCK(c, cudaMemsetAsync(rows, 0, 2ull * 32 * W * 8, st));
+  k_pty_split<uint32_t, 32><<<nblk(rup(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
+  uint64_t* mb_o = b_o + 2 * W;  // msb bit rows (own, prev) in the second half of `bits`
+  uint64_t* mb_p = b_o + 3 * W;
+  const uint64_t msb_o = c->pos[0] + 2 * n + 64 * W + ecore[ko];
+  const uint64_t msb_p = c->pos[1] + 2 * n + 64 * W + ecore[kp];
+  {
+    // results are written at res + k W for k = 0: own -> mb_o, prev -> mb_p
+    rc = bit_extract(c, kMsb, rows, rows + 32 * W, 32, {31}, n, W, msb_o, msb_p, mb_o, mb_p);
+    if (rc) return rc;
+  }
+  // ---- taps (parity tests)
+  c->tap_n = n;
+  // ---- debug rows open to P1
+  if (c->cfg.debug_rows && row_bits_out) {
+    rc = open_to_p1(c, reinterpret_cast<const uint8_t*>(mb_o), reinterpret_cast<const uint8_t*>(mb_p), n,
+                    p == 0 ? row_bits_out : nullptr);
+    if (rc) return rc;
+  }
+  // ---- or_tree_batch (circuits.hpp:387-434): groups of lanes (engine.cpp:262-293)
+  std::vector<OrGroup> grp(ngroups);
+  std::vector<uint64_t> pair_lanes;
+  std::vector<uint64_t> len(ngroups);
+  {
+    std::vector<std::vector<uint64_t>> pl(ngroups);
+    uint64_t k = ncols * S;
+    for (uint32_t i = 0; i < persons && !membership; ++i)
+      for (uint32_t j = i + 1; j < persons; ++j)
+        for (uint32_t e = 0; e < 4 * r; ++e, ++k) {
+          pl[i].push_back(k);
+          pl[j].push_back(k);
+        }
+    uint64_t off = 0, woff = 0;
+    for (uint32_t g2 = 0; g2 < ngroups; ++g2) {
+      OrGroup& G = grp[g2];
+      G.db_lane0 = membership ? 0 : (uint64_t)g2 * 2 * r * S;
+      G.db_len = membership ? S : 2ull * r * S;
+      G.pair_off = off;
+      G.len = G.db_len + pl[g2].size();
+      G.row_off = woff;
+      len[g2] = G.len;
+      pair_lanes.insert(pair_lanes.end(), pl[g2].begin(), pl[g2].end());
+      off += pl[g2].size();
+      woff += cdiv(G.len, 64) + 1;
+    }
+  }
+  uint64_t pool_words = 0, max_w = 0;
+  for (auto& G : grp) {
+    pool_words += cdiv(G.len, 64) + 1;
+    max_w = std::max(max_w, cdiv(G.len, 64));
+  }
+  if (!c->groups.ensure(ngroups * sizeof(OrGroup) + 16) || !c->pairs.ensure(pair_lanes.size() * 8 + 16) ||
+      !c->pool[0].ensure(2 * pool_words * 8 + 16) || !c->pool[1].ensure(2 * pool_words * 8 + 16) ||
+      !c->tz[0].ensure(2 * pool_words * 8 + 16) || !c->levels.ensure(ngroups * sizeof(OrLevel) + 16) ||
+      !c->rowoff.ensure(ngroups * 8 + 16))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or tree)");
+  PCK(c, cudaMemcpyAsync(c->groups.p, grp.data(), ngroups * sizeof(OrGroup), cudaMemcpyHostToDevice, st));
+  if (!pair_lanes.empty())
+    PCK(c, cudaMemcpyAsync(c->pairs.p, pair_lanes.data(), pair_lanes.size() * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* cur[2] = {c->pool[0].as<uint64_t>(), c->pool[0].as<uint64_t>() + pool_words};
+  uint64_t* nxt[2] = {c->pool[1].as<uint64_t>(), c->pool[1].as<uint64_t>() + pool_words};
+  if (max_w)
+    k_pty_or_gather<<<nblk(ngroups * max_w), kThreads, 0, st>>>(c->groups.as<OrGroup>(), ngroups,
+                                                                 c->pairs.as<uint64_t>(), mb_o, mb_p, cur[0], cur[1],
+                                                                 max_w);
+  const uint64_t or_o = msb_o + 61 * W, or_p = msb_p + 61 * W;
+  std::vector<uint64_t> roff(ngroups);
+  for (uint32_t g2 = 0; g2 < ngroups; ++g2) roff[g2] = grp[g2].row_off;
+  uint64_t used = 0;
+  uint64_t* tzo = c->tz[0].as<uint64_t>();
+  uint64_t* tzp = tzo + pool_words;
+  for (;;) {
+    std::vector<OrLevel> lv;
+    uint64_t t_words = 0, counted = 0, max_wb = 0, max_wa = 0;
+    for (uint32_t g2 = 0; g2 < ngroups; ++g2) {
+      if (len[g2] <= 1) continue;
+      OrLevel L{};
+      L.src_off = roff[g2];
+      L.dst_off = roff[g2];
+      L.na = (len[g2] + 1) / 2;
+      L.nb = len[g2] - L.na;
+      L.wa = cdiv(L.na, 64);
+      L.wb = cdiv(L.nb, 64);
+      L.t_off = t_words;
+      L.eo = or_o + used;
+      L.ep = or_p + used;
+      used += L.wb;
+      t_words += L.wb;
+      counted += cdiv(L.nb, 8);
+      max_wb = std::max(max_wb, L.wb);
+      max_wa = std::max(max_wa, L.wa);
+      lv.push_back(L);
+      len[g2] = L.na;
+    }
+    if (lv.empty()) break;
+    PCK(c, cudaMemcpyAsync(c->levels.p, lv.data(), lv.size() * sizeof(OrLevel), cudaMemcpyHostToDevice, st));
+    k_pty_or_and<<<nblk(lv.size() * max_wb), kThreads, 0, st>>>(c->levels.as<OrLevel>(), (uint32_t)lv.size(), max_wb,
+                                                               cur[0], cur[1], c->own, c->prev, tzo);
+    rc = step(c, kOr, {{next_of(p), tzo, t_words * 8}}, {{prev_of(p), tzp, t_words * 8}}, {counted}, 1);
+    if (rc) return rc;
+    k_pty_or_fold<<<nblk(lv.size() * max_wa), kThreads, 0, st>>>(c->levels.as<OrLevel>(), (uint32_t)lv.size(), max_wa,
+                                                                cur[0], cur[1], tzo, tzp, nxt[0], nxt[1]);
+    // groups that did not fold this round keep their rows: copy them across
+    for (uint32_t g2 = 0; g2 < ngroups; ++g2) {
+      bool folded = false;
+      for (auto& L : lv) folded |= L.src_off == roff[g2];
+      if (!folded && grp[g2].len)
+        for (int comp = 0; comp < 2; ++comp)
+          PCK(c, cudaMemcpyAsync(nxt[comp] + roff[g2], cur[comp] + roff[g2], 8, cudaMemcpyDeviceToDevice, st));
+    }
+    std::swap(cur[0], nxt[0]);
+    std::swap(cur[1], nxt[1]);
+    // level table reuse: wait before the next upload overwrites it
+    PCK(c, cudaStreamSynchronize(st));
+  }
+  // ---- open the per-person aggregates at P1
+  for (uint32_t g2 = 0; g2 < ngroups; ++g2)
+    if (grp[g2].len == 0) roff[g2] = ~0ull;
+  PCK(c, cudaMemcpyAsync(c->rowoff.p, roff.data(), ngroups * 8, cudaMemcpyHostToDevice, st));
+  if (!c->open_buf[2].ensure(2 * cdiv(ngroups, 8) + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (open)");
+  uint8_t* ob = c->open_buf[2].as<uint8_t>();
+  const uint64_t gb = cdiv(ngroups, 8);
+  k_pty_pack_groups<<<nblk(gb), kThreads, 0, st>>>(cur[0], c->rowoff.as<uint64_t>(), ngroups, ob);
+  k_pty_pack_groups<<<nblk(gb), kThreads, 0, st>>>(cur[1], c->rowoff.as<uint64_t>(), ngroups, ob + gb);
+  PCK(c, cudaGetLastError());
+  rc = open_to_p1(c, ob, ob + gb, ngroups, p == 0 ? match_out : nullptr);
+  if (rc) return rc;
+  PCK(c, cudaEventRecord(c->ev[1], st));
+  PCK(c, cudaStreamSynchronize(st));
+  // ---- stream positions advance exactly as the reference's (A.3)
+  const uint64_t glen = membership ? S : 2ull * r * S + (uint64_t)(persons ? persons - 1 : 0) * 4 * r;
+  const uint64_t ord = ref_or_draws(ngroups, glen, nullptr);
+  c->pos[0] = msb_o + 61 * W + ord;
+  c->pos[1] = msb_p + 61 * W + ord;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->s = S;
+    stats->l = c->l;
+    stats->batch = membership ? 1 : persons;
+    stats->lanes = n;
+    stats->dot_bytes = c->led_bytes[kDot];
+    stats->lift_bytes = c->led_bytes[kLift] + c->led_bytes[kOt];
+    stats->msb_bytes = c->led_bytes[kMsb];
+    stats->or_tree_bytes = c->led_bytes[kOr];
+    stats->dot_rounds = c->led_rounds[kDot];
+    stats->lift_rounds = c->led_rounds[kLift] + c->led_rounds[kOt];
+    stats->msb_rounds = c->led_rounds[kMsb];
+    stats->or_tree_rounds = c->led_rounds[kOr];
+    stats->wire_bytes = c->wire;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    stats->wall_ms = ms;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+
+extern "C" {
+
+int irismpc_gpu_nccl_unique_id(uint8_t out[128]) {
+  if (!out || !nccl().ok) return IRISMPC_GPU_ERR_DEVICE;
+  ncclUniqueId id;
+  if (nccl().get_unique_id(&id) != ncclSuccess) return IRISMPC_GPU_ERR_DEVICE;
+  std::memcpy(out, &id, 128);
+  return 0;
+}
+
+int irismpc_gpu_party_create_nccl(const irismpc_gpu_config* cfg, uint32_t party, const uint8_t nccl_id[128],
+                                  irismpc_gpu_party** out) {
+  std::string why;
+  int rc = party_init(cfg, party, out, &why);
+  if (rc) {
+    if (!why.empty()) std::fprintf(stderr, "irismpc_gpu_party_create: %s\n", why.c_str());
+    return rc;
+  }
+  if (!nccl().ok) {
+    irismpc_gpu_party_destroy(*out);
+    *out = nullptr;
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  auto* t = new NcclTransport;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, 128);
+  if (nccl().comm_init_rank(&t->comm, 3, id, (int)party - 1) != ncclSuccess) {
+    delete t;
+    irismpc_gpu_party_destroy(*out);
+    *out = nullptr;
+    return IRISMPC_GPU_ERR_DEVICE;
+  }
+  (*out)->net = t;
+  return 0;
+}
+
+int irismpc_gpu_inproc_create(irismpc_gpu_inproc** out) {
+  if (!out) return IRISMPC_GPU_ERR_CONFIG;
+  *out = new irismpc_gpu_inproc;
+  return 0;
+}
+
+void irismpc_gpu_inproc_destroy(irismpc_gpu_inproc* net) {
+  if (!net) return;
+  for (auto& row : net->q)
+    for (auto& q : row)
+      for (auto& it : q) {
+        cudaFree(it.buf);
+        cudaEventDestroy(it.ev);
+      }
+  delete net;
+}
+
+int irismpc_gpu_party_create_inproc(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_inproc* net,
+                                    irismpc_gpu_party** out) {
+  if (!net) return IRISMPC_GPU_ERR_CONFIG;
+  std::string why;
+  int rc = party_init(cfg, party, out, &why);
+  if (rc) {
+    if (!why.empty()) std::fprintf(stderr, "irismpc_gpu_party_create: %s\n", why.c_str());
+    return rc;
+  }
+  auto* t = new InProcTransport;
+  t->net = net;
+  (*out)->net = t;
+  return 0;
+}
+
+void irismpc_gpu_party_destroy(irismpc_gpu_party* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  cudaStreamSynchronize(c->st);
+  DBuf* bufs[] = {&c->qpay, &c->dots, &c->rs, &c->rows, &c->carry, &c->chain, &c->zbuf, &c->zrecv, &c->inj,
+                  &c->msg, &c->msg2, &c->ml32, &c->diff, &c->bits, &c->pairs, &c->groups, &c->levels, &c->pool[0],
+                  &c->pool[1], &c->tz[0], &c->tz[1], &c->rowoff, &c->open_buf[0], &c->open_buf[1], &c->open_buf[2]};
+  for (DBuf* b : bufs) b->release();
+  for (auto& f : c->fld) {
+    f.db.release();
+    f.q.release();
+    f.qa.release();
+    f.pc.release();
+  }
+  delete c->net;
+  cudaEventDestroy(c->ev[0]);
+  cudaEventDestroy(c->ev[1]);
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+const char* irismpc_gpu_party_last_error(const irismpc_gpu_party* c) { return c ? c->err.c_str() : "null context"; }
+
+int irismpc_gpu_party_load_db(irismpc_gpu_party* c, const uint8_t* payload, size_t len, uint64_t s) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  if (len != s * c->rec) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "db payload size mismatch");
+  c->db_loaded = false;
+  c->s = s;
+  c->s_pad = rup(s ? s : 1, 2 * kGemmBM);
+  DBuf stage;
+  if (!stage.ensure(len)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (db staging)");
+  PCK(c, cudaMemcpyAsync(stage.p, payload, len, cudaMemcpyHostToDevice, c->st));
+  for (auto& f : c->fld) {
+    const uint64_t rows = (uint64_t)f.slots * f.fmt.limbs * c->s_pad;
+    if (!f.db.ensure(rows * c->l_pad)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (db planes)");
+    PCK(c, cudaMemsetAsync(f.db.p, 0, rows * c->l_pad, c->st));
+    if (make_plane_tmap(&f.tA, f.db.p, rows, c->l_pad, kGemmBM))
+      return pfail(c, IRISMPC_GPU_ERR_DEVICE, "tensor map (db)");
+    parse_party_rows(c, f, stage.as<uint8_t>(), s, c->s_pad, f.db.as<uint8_t>());
+  }
+  PCK(c, cudaGetLastError());
+  PCK(c, cudaStreamSynchronize(c->st));
+  stage.release();
+  c->db_loaded = true;
+  return 0;
+}
+
+int irismpc_gpu_party_batch_query(irismpc_gpu_party* c, const uint8_t* q, size_t qlen, uint32_t persons,
+                                  uint8_t* person_match_out, uint8_t* row_bits_out, irismpc_gpu_party_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return party_query(c, q, qlen, persons, 0, person_match_out, row_bits_out, stats);
+}
+
+int irismpc_gpu_party_membership(irismpc_gpu_party* c, const uint8_t* q, size_t qlen, uint8_t* match_out,
+                                 uint8_t* row_bits_out, irismpc_gpu_party_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return party_query(c, q, qlen, 1, 1, match_out, row_bits_out, stats);
+}
+
+int irismpc_gpu_party_read_tap(irismpc_gpu_party* c, int tap, void* host_out, size_t bytes) {
+  if (!c || !host_out) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  const uint64_t n = c->tap_n, W = cdiv(n, 64);
+  std::vector<uint8_t> tmp;
+  auto copy2 = [&](const void* a, const void* b, size_t esz) -> int {  // [own n][prev n]
+    if (bytes < 2 * n * esz) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "tap buffer too small");
+    PCK(c, cudaMemcpy(host_out, a, n * esz, cudaMemcpyDeviceToHost));
+    PCK(c, cudaMemcpy(static_cast<uint8_t*>(host_out) + n * esz, b, n * esz, cudaMemcpyDeviceToHost));
+    return 0;
+  };
+  switch (tap) {
+    case IRISMPC_GPU_TAP_DOT_HD:
+    case IRISMPC_GPU_TAP_DOT_ML: {
+      if (bytes < n * 2) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "tap buffer too small");
+      const uint16_t* d = c->dots.as<uint16_t>() + (tap == IRISMPC_GPU_TAP_DOT_ML ? n + 8 : 0);
+      PCK(c, cudaMemcpy(host_out, d, n * 2, cudaMemcpyDeviceToHost));
+      return 0;
+    }
+    case IRISMPC_GPU_TAP_RS_HD:
+      return copy2(c->rs.as<uint16_t>(), c->rs.as<uint16_t>() + 2 * (n + 8), 2);
+    case IRISMPC_GPU_TAP_RS_ML:
+      return copy2(c->rs.as<uint16_t>() + n + 8, c->rs.as<uint16_t>() + 3 * (n + 8), 2);
+    case IRISMPC_GPU_TAP_ML32:
+      return copy2(c->ml32.as<uint32_t>(), c->ml32.as<uint32_t>() + n + 8, 4);
+    case IRISMPC_GPU_TAP_DIFF:
+      return copy2(c->diff.as<uint32_t>(), c->diff.as<uint32_t>() + n + 8, 4);
+    case IRISMPC_GPU_TAP_MSB: {
+      if (bytes < 2 * n) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "tap buffer too small");
+      std::vector<uint64_t> w(2 * W);
+      PCK(c, cudaMemcpy(w.data(), c->bits.as<uint64_t>() + 2 * W, 2 * W * 8, cudaMemcpyDeviceToHost));
+      uint8_t* o = static_cast<uint8_t*>(host_out);
+      for (int comp = 0; comp < 2; ++comp)
+        for (uint64_t i = 0; i < n; ++i) o[comp * n + i] = (uint8_t)((w[comp * W + i / 64] >> (i % 64)) & 1);
+      return 0;
+    }
+    default:
+      return pfail(c, IRISMPC_GPU_ERR_CONFIG, "unknown tap");
+  }
+}
+
+int irismpc_gpu_party_stream_positions(const irismpc_gpu_party* c, uint64_t pos[2]) {
+  if (!c || !pos) return IRISMPC_GPU_ERR_CONFIG;
+  pos[0] = c->pos[0];
+  pos[1] = c->pos[1];
+  return 0;
+}
+
+}  // extern "C"

@@ -80,59 +80,6 @@ __device__ __forceinline__ uint64_t gate_base(const ThrArgs& A, int k, int g) {
   return A.msb_base[k] + (uint64_t)(g - (int)A.nlift) * A.W;
 }
 
-// ---- warp-cooperative stream windows.  The lane-major kernels map 31
-// consecutive 8-lane groups to a warp (lane 31 only helps).  A lane's window
-// of 8 * NB elements starting at e spans NB blocks + 1 when e % 8 != 0
-// (warp-uniform: e = stream offset + 8 * group); the extra block is the next
-// lane's first block and arrives by shuffle, so every ChaCha block is
-// computed once instead of up to twice.  Only the low 32 bits of each u64
-// element are consumed (Ring<K <= 32> draws).
-template <int NB, int R>
-__device__ __forceinline__ void take_window(const uint32_t (&w)[8 * (NB + 1)], uint32_t (&out)[8 * NB]) {
-#pragma unroll
-  for (int i = 0; i < 8 * NB; ++i) out[i] = w[R + i];
-}
-
-// next_contig: lane + 1 owns the window starting at e + 8 * NB (else this lane
-// computes the extra block itself -- segment boundaries, the last group).
-// Must be called by all 32 lanes in convergent code.
-template <int NB>
-__device__ __forceinline__ void prf_window(const SeedKey& key, uint64_t e, bool next_contig,
-                                           uint32_t (&out)[8 * NB]) {
-  uint32_t w[8 * (NB + 1)];
-  const uint64_t b = e / 8;
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    uint32_t blk[16];
-    chacha12_block(key, b + q, 0, blk);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[8 * q + i] = blk[2 * i];
-  }
-  const int r = (int)(e % 8);
-  if (r == 0) {
-#pragma unroll
-    for (int i = 0; i < 8 * NB; ++i) out[i] = w[i];
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) w[8 * NB + i] = __shfl_down_sync(0xFFFFFFFFu, w[i], 1);
-  if (!next_contig) {
-    uint32_t blk[16];
-    chacha12_block(key, b + NB, 0, blk);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[8 * NB + i] = blk[2 * i];
-  }
-  switch (r) {
-    case 1: take_window<NB, 1>(w, out); break;
-    case 2: take_window<NB, 2>(w, out); break;
-    case 3: take_window<NB, 3>(w, out); break;
-    case 4: take_window<NB, 4>(w, out); break;
-    case 5: take_window<NB, 5>(w, out); break;
-    case 6: take_window<NB, 6>(w, out); break;
-    default: take_window<NB, 7>(w, out); break;
-  }
-}
-
 // lane -> 8-lane group of a lane-major kernel (31 groups per warp)
 struct GroupCtx {
   uint64_t L8;       // first global lane of the group

@@ -170,6 +170,8 @@ typedef struct irismpc_gpu_party_stats {
   uint64_t dot_rounds, lift_rounds, msb_rounds, or_tree_rounds;
   uint64_t wire_bytes;  /* bytes this party actually handed to the transport */
   double wall_ms;       /* device time of the query on this party's GPU */
+  double phase_ms[6];   /* device time: dot products, reshare, lift + inject, msb, or tree + open,
+                           and [5] the time inside transport steps (all phases) */
 } irismpc_gpu_party_stats;
 
 /* 128-byte ncclUniqueId for the three ranks (rank 0 creates, all receive it). */

@@ -96,7 +96,8 @@ class PartyStats(C.Structure):
     """One party's QueryStats from the measured ledger (party mode)."""
     _fields_ = [(k, C.c_uint64) for k in ("s", "l", "batch", "lanes", "dot_bytes", "lift_bytes", "msb_bytes",
                                           "or_tree_bytes", "dot_rounds", "lift_rounds", "msb_rounds",
-                                          "or_tree_rounds", "wire_bytes")] + [("wall_ms", C.c_double)]
+                                          "or_tree_rounds", "wire_bytes")] + [("wall_ms", C.c_double),
+                                                                                ("phase_ms", C.c_double * 6)]
 
     def ledger(self) -> dict:
         return {k: getattr(self, k) for k in ("dot_bytes", "lift_bytes", "msb_bytes", "or_tree_bytes", "dot_rounds",

@@ -253,22 +253,24 @@ __global__ void k_pty_reshare(const uint16_t* __restrict__ zh, const uint16_t* _
 
 // share_split: K-bit lane values (own, prev components) -> bit rows
 // rows[c][j][w], lane i = bit i % 64 of word i / 64 (circuits.hpp:152-172).
+// Thread -> 32 lanes of one component: 32x32 SWAR transpose, one u32 half-word per row.
 template <typename T, int K>
 __global__ void k_pty_split(const T* __restrict__ own, const T* __restrict__ prev, uint64_t n, uint64_t W,
                             uint64_t* __restrict__ rows) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // lane
-  if ((i & ~31ull) >= n) return;
-  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t ng = cdiv(n, 32);
+  if (t >= 2 * ng) return;
+  const int c = (int)(t / ng);
+  const uint64_t g = t % ng;
+  const T* src = (c == 0 ? own : prev) + 32 * g;
+  uint32_t a[32];
+  const uint64_t left = n - 32 * g;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = (uint64_t)i < left ? (uint32_t)src[i] : 0u;
+  transpose32(a);
   uint32_t* r32 = reinterpret_cast<uint32_t*>(rows);
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const uint32_t v = i < n ? (uint32_t)(c == 0 ? own[i] : prev[i]) : 0u;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const uint32_t b = __ballot_sync(0xFFFFFFFFu, (v >> j) & 1u);
-      if (lane == 0) r32[((uint64_t)(c * K + j) * W) * 2 + (i >> 5)] = b;  // half-word i / 32
-    }
-  }
+  for (int j = 0; j < K; ++j) r32[((uint64_t)(c * K + j) * W) * 2 + g] = a[j];
 }
 
 // One AND layer (and_layer, circuits.hpp:92-131) at one party: for gate g,
@@ -340,42 +342,47 @@ __global__ void k_pty_xor(const __grid_constant__ XorBatch X) {
   o.dst[w] = o.a[w] ^ (o.b ? o.b[w] : 0ull);
 }
 
-// bit_inject<W> (convert.hpp:84-155), per role.  bits: own/prev bit rows of
-// the injected bit.  c1 from seed_1 at e1 + i, (c3, w0, w1) from seed_3 at e3 + 3i.
+// bit_inject<W> (convert.hpp:84-155), per role; thread -> 8 lanes with
+// warp-cooperative stream windows (seed_1: 8 elements at e1 + L8, seed_3: 24
+// elements (c3, w0, w1 per lane) at e3 + 3 L8).  bits: own/prev bit rows.
 // role 0 (P1): out (c1, c3), msg[2i], msg[2i+1] = w0 ^ m0, w1 ^ m1 -> P2
 // role 2 (P3): out own = c3, msg[i] = x2 ? w1 : w0 -> P2
 __global__ void k_pty_inject_send(int role, const uint64_t* __restrict__ bo, const uint64_t* __restrict__ bp,
                                   uint64_t n, uint32_t mask, SeedKey own, SeedKey prev, uint64_t e1, uint64_t e3,
                                   uint16_t* __restrict__ out_o, uint16_t* __restrict__ out_p,
                                   uint16_t* __restrict__ msg) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t ngrp = cdiv(n, 8);
+  if ((t & ~31ull) >= ngrp) return;
+  const uint64_t L8 = 8 * t;
+  const bool next_contig = (t & 31) != 31;
+  const uint64_t wv = t < ngrp ? (bo[L8 / 64] >> (L8 % 64)) : 0, pv = t < ngrp ? (bp[L8 / 64] >> (L8 % 64)) : 0;
+  uint32_t w3[24];
+  prf_window<3>(role == 0 ? prev : own, e3 + 3 * L8, next_contig, w3);
   if (role == 0) {
-    const uint32_t x1 = (uint32_t)(bo[i / 64] >> (i % 64)) & 1u, x3 = (uint32_t)(bp[i / 64] >> (i % 64)) & 1u;
-    uint32_t blk[16];
-    chacha12_block(own, (e1 + i) / 8, 0, blk);
-    const uint32_t c1 = blk[2 * ((e1 + i) % 8)] & mask;
-    uint32_t c3w[3];
-    for (int k = 0; k < 3; ++k) {
-      const uint64_t e = e3 + 3 * i + k;
-      chacha12_block(prev, e / 8, 0, blk);
-      c3w[k] = blk[2 * (e % 8)] & mask;
+    uint32_t c1[8];
+    prf_window<1>(own, e1 + L8, next_contig, c1);
+    if (t >= ngrp) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (L8 + i >= n) break;
+      const uint32_t x1 = (uint32_t)(wv >> i) & 1u, x3 = (uint32_t)(pv >> i) & 1u;
+      const uint32_t a1 = c1[i] & mask, c3 = w3[3 * i] & mask;
+      const uint32_t m0 = ((0u ^ x1 ^ x3) - a1 - c3) & mask, m1 = ((1u ^ x1 ^ x3) - a1 - c3) & mask;
+      msg[2 * (L8 + i)] = (uint16_t)((w3[3 * i + 1] ^ m0) & mask);
+      msg[2 * (L8 + i) + 1] = (uint16_t)((w3[3 * i + 2] ^ m1) & mask);
+      out_o[L8 + i] = (uint16_t)a1;
+      out_p[L8 + i] = (uint16_t)c3;
     }
-    const uint32_t m0 = ((0u ^ x1 ^ x3) - c1 - c3w[0]) & mask, m1 = ((1u ^ x1 ^ x3) - c1 - c3w[0]) & mask;
-    msg[2 * i] = (uint16_t)((c3w[1] ^ m0) & mask);
-    msg[2 * i + 1] = (uint16_t)((c3w[2] ^ m1) & mask);
-    out_o[i] = (uint16_t)c1;
-    out_p[i] = (uint16_t)c3w[0];
   } else {
-    const uint32_t x2 = (uint32_t)(bp[i / 64] >> (i % 64)) & 1u;
-    uint32_t blk[16], c3w[3];
-    for (int k = 0; k < 3; ++k) {
-      const uint64_t e = e3 + 3 * i + k;
-      chacha12_block(own, e / 8, 0, blk);
-      c3w[k] = blk[2 * (e % 8)] & mask;
+    if (t >= ngrp) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (L8 + i >= n) break;
+      const uint32_t x2 = (uint32_t)(pv >> i) & 1u;
+      msg[L8 + i] = (uint16_t)((x2 ? w3[3 * i + 2] : w3[3 * i + 1]) & mask);
+      out_o[L8 + i] = (uint16_t)(w3[3 * i] & mask);
     }
-    msg[i] = (uint16_t)(x2 ? c3w[2] : c3w[1]);
-    out_o[i] = (uint16_t)c3w[0];
   }
 }
 // role 1 (P2): c1 from its prev stream, c2 = k_{x2} ^ w_{x2}; out (c2, c1); msg[i] = c2 -> P3
@@ -383,16 +390,24 @@ __global__ void k_pty_inject_p2(const uint64_t* __restrict__ bo, uint64_t n, uin
                                 uint64_t e1, const uint16_t* __restrict__ ks, const uint16_t* __restrict__ ws,
                                 uint16_t* __restrict__ out_o, uint16_t* __restrict__ out_p,
                                 uint16_t* __restrict__ msg) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t x2 = (uint32_t)(bo[i / 64] >> (i % 64)) & 1u;
-  uint32_t blk[16];
-  chacha12_block(prev, (e1 + i) / 8, 0, blk);
-  const uint32_t c1 = blk[2 * ((e1 + i) % 8)] & mask;
-  const uint32_t c2 = ((uint32_t)ks[2 * i + x2] ^ (uint32_t)ws[i]) & mask;
-  msg[i] = (uint16_t)c2;
-  out_o[i] = (uint16_t)c2;
-  out_p[i] = (uint16_t)c1;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t ngrp = cdiv(n, 8);
+  if ((t & ~31ull) >= ngrp) return;
+  const uint64_t L8 = 8 * t;
+  uint32_t c1[8];
+  prf_window<1>(prev, e1 + L8, (t & 31) != 31, c1);
+  if (t >= ngrp) return;
+  const uint64_t wv = bo[L8 / 64] >> (L8 % 64);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (L8 + i >= n) break;
+    const uint64_t j = L8 + i;
+    const uint32_t x2 = (uint32_t)(wv >> i) & 1u;
+    const uint32_t c2 = ((uint32_t)ks[2 * j + x2] ^ (uint32_t)ws[j]) & mask;
+    msg[j] = (uint16_t)c2;
+    out_o[j] = (uint16_t)c2;
+    out_p[j] = (uint16_t)(c1[i] & mask);
+  }
 }
 
 // lift output and comparison input per component (convert.hpp:169-192,
@@ -528,11 +543,14 @@ struct irismpc_gpu_party {
   Transport* net = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t ev[2];
+  cudaEvent_t pev[6];  // phase boundaries
   PartyField fld[2];
   uint64_t s = 0, s_pad = 0;
   bool db_loaded = false;
   std::string err;
   uint64_t led_bytes[kPhases] = {0, 0, 0, 0, 0}, led_rounds[kPhases] = {0, 0, 0, 0, 0}, wire = 0;
+  std::vector<cudaEvent_t> xev;  // exchange start/stop pairs of the current query (profiling)
+  size_t nxev = 0;
   // work buffers
   DBuf qpay, dots, rs, rows, carry, chain, zbuf, zrecv, inj, msg, msg2, ml32, diff, bits, pairs, groups, levels,
       pool[2], tz[2], rowoff, open_buf[3];
@@ -563,7 +581,15 @@ int step(irismpc_gpu_party* c, Phase ph, const std::vector<Msg>& sends, const st
     c->wire += sends[i].bytes;
   }
   c->led_rounds[ph] += rounds;
+  while (c->xev.size() < c->nxev + 2) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->xev.push_back(e);
+  }
+  cudaEventRecord(c->xev[c->nxev], c->st);
   const std::string e = c->net->exchange(c->p, sends, recvs, c->st);
+  cudaEventRecord(c->xev[c->nxev + 1], c->st);
+  c->nxev += 2;
   if (!e.empty()) return pfail(c, IRISMPC_GPU_ERR_DEVICE, e);
   return 0;
 }
@@ -607,6 +633,7 @@ int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party*
   }
   cudaEventCreate(&c->ev[0]);
   cudaEventCreate(&c->ev[1]);
+  for (auto& e : c->pev) cudaEventCreate(&e);
   // lambda_p for the Shamir parse (the same constants as the 3-party context)
   uint32_t lam[6] = {1, 2, 0xFFFFFFFFu, 0xFFFFFFFEu, 1, 0};  // 1+2X, -(1+2X), 1 (galois.hpp:124-128)
   set_lambda(lam);
@@ -777,11 +804,13 @@ int bit_inject(irismpc_gpu_party* c, const uint64_t* bo, const uint64_t* bp, uin
   uint16_t* m2 = c->msg2.as<uint16_t>();
   int rc = 0;
   if (p == 0) {  // P1: sender
-    k_pty_inject_send<<<nblk(n), kThreads, 0, c->st>>>(0, bo, bp, n, mask, c->own, c->prev, e1, e3, out_o, out_p, m1);
+    k_pty_inject_send<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(0, bo, bp, n, mask, c->own, c->prev, e1, e3,
+                                                                          out_o, out_p, m1);
     rc = step(c, kOt, {{1, m1, 2 * n * eb}}, {}, {}, 1);
     if (!rc) rc = step(c, kOt, {}, {}, {}, 1);  // c_2 forwarding stage, party 1 idle
   } else if (p == 2) {  // P3: helper
-    k_pty_inject_send<<<nblk(n), kThreads, 0, c->st>>>(2, bo, bp, n, mask, c->own, c->prev, e1, e3, out_o, out_p, m1);
+    k_pty_inject_send<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(2, bo, bp, n, mask, c->own, c->prev, e1, e3,
+                                                                          out_o, out_p, m1);
     rc = step(c, kOt, {{1, m1, n * eb}}, {}, {}, 1);
     if (!rc) rc = step(c, kOt, {}, {{1, out_p, n * eb}}, {}, 1);  // c_2 from P2 -> prev component
   } else {  // P2: receiver
@@ -789,7 +818,8 @@ int bit_inject(irismpc_gpu_party* c, const uint64_t* bo, const uint64_t* bp, uin
     if (rc) return rc;
     if (!c->zbuf.ensure(n * eb + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (inject)");
     uint16_t* c2 = c->zbuf.as<uint16_t>();
-    k_pty_inject_p2<<<nblk(n), kThreads, 0, c->st>>>(bo, n, mask, c->prev, e1, m1, m2, out_o, out_p, c2);
+    k_pty_inject_p2<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(bo, n, mask, c->prev, e1, m1, m2, out_o, out_p,
+                                                                        c2);
     rc = step(c, kOt, {{2, c2, n * eb}}, {}, {}, 1);
   }
   if (rc) return rc;
@@ -845,6 +875,7 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   for (auto& x : c->led_bytes) x = 0;
   for (auto& x : c->led_rounds) x = 0;
   c->wire = 0;
+  c->nxev = 0;
   const int p = c->p;
   const uint32_t r = membership ? 1u : c->cfg.rotations;
   const uint64_t S = c->s, ncols = (uint64_t)ncodes * r;
@@ -923,6 +954,7 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
     }
   }
   PCK(c, cudaGetLastError());
+  PCK(c, cudaEventRecord(c->pev[0], st));
   // ---- dot phase: reshare_pair<16,16>, own -> next, prev <- previous
   uint16_t* rs_own = c->rs.as<uint16_t>();        // [hd n+8 | ml n+8]
   uint16_t* rs_prev = rs_own + 2 * (n + 8);
@@ -935,13 +967,14 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   const uint16_t* ml_o = rs_own + n + 8;
   const uint16_t* hd_p = rs_prev;
   const uint16_t* ml_p = rs_prev + n + 8;
+  PCK(c, cudaEventRecord(c->pev[1], st));
   // ---- lift<16,16>
   if (!c->rows.ensure(2ull * 32 * W * 8 + 64) || !c->bits.ensure(4ull * W * 8 + 64) ||
       !c->inj.ensure(4ull * (n + 8) * 2 + 64))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (lift)");
   uint64_t* rows = c->rows.as<uint64_t>();
-  PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));
-  k_pty_split<uint16_t, 16><<<nblk(rup(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
+  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));  // odd trailing half-word
+  k_pty_split<uint16_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
   uint64_t* b_o = c->bits.as<uint64_t>();  // [inst][W]: bit16, bit17
   uint64_t* b_p = b_o + 2 * W;
   const uint64_t ecore[3] = {2 * n, 0, 6 * n};  // inject draws before the MSB, per seed
@@ -956,6 +989,7 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   if (rc) return rc;
   rc = bit_inject(c, b_o, b_p, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
   if (rc) return rc;
+  PCK(c, cudaEventRecord(c->pev[2], st));
   // ---- diff, msb<32>
   if (!c->ml32.ensure(2 * (n + 8) * 4) || !c->diff.ensure(2 * (n + 8) * 4))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (diff)");
@@ -968,8 +1002,8 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
     k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_p, hd_p, i17 + n + 8, i16 + n + 8, n, c->cfg.a, c->cfg.b,
                                              ml32 + n + 8, diff + n + 8);
   }
-  PCK(c, cudaMemsetAsync(rows, 0, 2ull * 32 * W * 8, st));
-  k_pty_split<uint32_t, 32><<<nblk(rup(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
+  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 32 * W * 8, st));
+  k_pty_split<uint32_t, 32><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
   uint64_t* mb_o = b_o + 2 * W;  // msb bit rows (own, prev) in the second half of `bits`
   uint64_t* mb_p = b_o + 3 * W;
   const uint64_t msb_o = c->pos[0] + 2 * n + 64 * W + ecore[ko];
@@ -979,6 +1013,7 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
     rc = bit_extract(c, kMsb, rows, rows + 32 * W, 32, {31}, n, W, msb_o, msb_p, mb_o, mb_p);
     if (rc) return rc;
   }
+  PCK(c, cudaEventRecord(c->pev[3], st));
   // ---- taps (parity tests)
   c->tap_n = n;
   // ---- debug rows open to P1
@@ -1120,6 +1155,18 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     stats->wall_ms = ms;
+    const cudaEvent_t b[5] = {c->ev[0], c->pev[0], c->pev[1], c->pev[2], c->pev[3]};
+    const cudaEvent_t e[5] = {c->pev[0], c->pev[1], c->pev[2], c->pev[3], c->ev[1]};
+    for (int i = 0; i < 5; ++i) {
+      cudaEventElapsedTime(&ms, b[i], e[i]);
+      stats->phase_ms[i] = ms;
+    }
+    double xms = 0;  // device time spent inside the transport steps
+    for (size_t i = 0; i + 1 < c->nxev; i += 2) {
+      cudaEventElapsedTime(&ms, c->xev[i], c->xev[i + 1]);
+      xms += ms;
+    }
+    stats->phase_ms[5] = xms;
   }
   return 0;
 }
@@ -1213,6 +1260,8 @@ void irismpc_gpu_party_destroy(irismpc_gpu_party* c) {
   delete c->net;
   cudaEventDestroy(c->ev[0]);
   cudaEventDestroy(c->ev[1]);
+  for (auto& e : c->pev) cudaEventDestroy(e);
+  for (auto& e : c->xev) cudaEventDestroy(e);
   cudaStreamDestroy(c->st);
   delete c;
 }

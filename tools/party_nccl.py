@@ -94,7 +94,7 @@ def main():
     led = torch.tensor(list(st.ledger().values()), dtype=torch.int64)
     leds = [torch.zeros_like(led) for _ in range(3)]
     dist.all_gather(leds, led)
-    wall = torch.tensor([float(np.median(ms)), st.wall_ms], dtype=torch.float64)
+    wall = torch.tensor([float(np.median(ms)), st.wall_ms] + list(st.phase_ms)[:6], dtype=torch.float64)
     walls = [torch.zeros_like(wall) for _ in range(3)]
     dist.all_gather(walls, wall)
     line = None
@@ -108,6 +108,8 @@ def main():
                 "persons": a.persons, "lanes": n, "person_match": [int(x) for x in out],
                 "ms_per_query_max_over_parties": host_ms,
                 "device_ms": [round(w[1].item(), 3) for w in walls],
+                "phase_ms_p1": dict(zip(["gemm", "dot_reshare", "lift_inject", "msb", "or_open", "in_transport"],
+                                        [round(x, 3) for x in walls[0][2:].tolist()])),
                 "comparisons_per_s": cmp_ / (host_ms / 1e3), "ledgers": ledgers,
                 "wire_bytes_p1": int(st.wire_bytes)}
         if a.check:

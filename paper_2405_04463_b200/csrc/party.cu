@@ -44,7 +44,9 @@ using namespace irisgpu;
 namespace {
 
 constexpr int kThreads = 256;
-inline unsigned nblk(uint64_t n, unsigned b = kThreads) { return (unsigned)((n + b - 1) / b); }
+// at least one block: a query with zero lanes still runs every protocol round
+// (empty messages, the reference's ledger); every kernel bounds-checks
+inline unsigned nblk(uint64_t n, unsigned b = kThreads) { return n ? (unsigned)((n + b - 1) / b) : 1u; }
 __host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t rup(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
 

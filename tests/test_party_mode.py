@@ -88,3 +88,26 @@ def test_party_mode_matches_single_context_engine():
     m = sess.batch_query(q, persons)
     np.testing.assert_array_equal(parties[0].result, m)
     assert m[0] == 1
+
+
+@pytest.mark.parametrize("be", [O.SHAMIR, O.REPLICATED])
+def test_empty_db_membership_both_engines(be):
+    """s = 0: zero lanes, every round still runs (empty messages); no match, and
+    the ledger equals the reference's (oracle pinned to the live reference)."""
+    l, seed = 128, 77
+    rng = O.Rng(seed)
+    qc, qm = O.records(rng, l, 1, 0.9)
+    q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)))
+    db = [np.zeros(0, np.uint8)] * 3
+    seeds = O.party_seeds(seed)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=1)
+    ref = O.query(O.make_config(be, l, 0.375, 1), seeds, db, 0, q, 1, membership=True)
+    assert int(ref.person_match[0]) == 0
+    parties = P.run_parties_inproc(cfg, seeds, db, 0, q, membership=True)
+    assert parties[0].result is False
+    for i, pt in enumerate(parties):
+        assert pt.last_stats.ledger() == ref.stats[i]
+    sess = P.Session(cfg, seeds=seeds)
+    sess.load_db(db, 0)
+    assert sess.membership(q) is False
+    np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)

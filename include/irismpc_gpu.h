@@ -157,9 +157,9 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* ctx, uint64_t s, uint64_t rng_seed, ui
  * two seeds (own, prev) and exchanges the protocol's messages with the other
  * two every round (PartyComm / TcpMesh, transport.hpp:54-154), here over NCCL
  * send/recv (ranks 0, 1, 2 = parties 1, 2, 3) or an in-process mailbox
- * (three parties in one process, like InProcNet).  mpc-lift only.  The
+ * (three parties in one process, like InProcNet).  The
  * per-phase byte/round ledger is counted from the messages actually sent
- * (CommLedger semantics), not derived analytically. */
+ * (CommLedger semantics), not derived analytically.  All four variants. */
 typedef struct irismpc_gpu_party irismpc_gpu_party;
 typedef struct irismpc_gpu_inproc irismpc_gpu_inproc;
 
@@ -196,8 +196,9 @@ int irismpc_gpu_party_batch_query(irismpc_gpu_party* pc, const uint8_t* q, size_
 int irismpc_gpu_party_membership(irismpc_gpu_party* pc, const uint8_t* q, size_t qlen, uint8_t* match_out,
                                  uint8_t* row_bits_out, irismpc_gpu_party_stats* stats);
 /* Parity taps of the last query: this party's (own, prev) components,
- * tap = IRISMPC_GPU_TAP_* (DOT_* = own additive dot only, [n]; others [2][n],
- * MSB as bytes). */
+ * tap = IRISMPC_GPU_TAP_* (DOT_* = own additive dot only, [n] at the ring's
+ * width, u16 / u32; plain-mask DOT_ML = the public popcount, u16); RS_*, ML32,
+ * DIFF: u32 [2][n]; MSB: bytes [2][n]. */
 int irismpc_gpu_party_read_tap(irismpc_gpu_party* pc, int tap, void* host_out, size_t bytes);
 int irismpc_gpu_party_stream_positions(const irismpc_gpu_party* pc, uint64_t pos_own_prev[2]);
 

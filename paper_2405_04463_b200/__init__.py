@@ -595,11 +595,12 @@ class Party:
         return bool(out[0]) if self.party == 1 else None
 
     def read_tap(self, tap: int, n: int) -> np.ndarray:
-        """DOT_*: this party's own additive dot [n]; others: [own, prev] x [n]."""
+        """DOT_*: this party's own additive dot [n] (plain-mask DOT_ML: the public
+        popcount); others: [own, prev] x [n]."""
+        kh, km, _ = VARIANT_WIDTHS[self.cfg.variant]
         if tap in (TAP_DOT_HD, TAP_DOT_ML):
-            out = np.zeros(n, np.uint16)
-        elif tap in (TAP_RS_HD, TAP_RS_ML):
-            out = np.zeros(2 * n, np.uint16)
+            bits = kh if tap == TAP_DOT_HD else km
+            out = np.zeros(n, np.uint32 if bits == 32 else np.uint16)
         elif tap == TAP_MSB:
             out = np.zeros(2 * n, np.uint8)
         else:

@@ -1,12 +1,12 @@
-// f3: the mpc-lift query with ONE PARTY per process / GPU (the reference's
-// deployment).  Each party holds only its own IRS1 payloads
+// f3: the query with ONE PARTY per process / GPU (the reference's deployment,
+// PAPER.md:508-512), all four variants.  Each party holds only its own IRS1 payloads
 // and its two seeds (own = seed_p, prev = seed_{p-1}); every protocol message
 // of the reference crosses a real transport, round by round:
 //
-//   dot      reshare_pair<16,16>: own -> next party                 (engine.cpp:80-106)
-//   lift     bit_extract_sum {16,17}: 1 FA round + 16 chain rounds  (circuits.hpp:202-296)
-//   ot       bit_inject<15>, <16>: P1 -> P2, P3 -> P2, then P2 -> P3 (convert.hpp:42-155)
-//   msb      msb_batch<32>: 1 FA round + 30 chain rounds
+//   dot      reshare_pair<KH,KM>: own -> next party                (engine.cpp:80-106)
+//   lift     (mpc-lift) bit_extract_sum {16,17}: 1 FA + 16 chain rounds (circuits.hpp:202-296)
+//   ot       (mpc-lift) bit_inject<15>, <16>: P1 -> P2, P3 -> P2, then P2 -> P3 (convert.hpp:42-155)
+//   msb      msb_batch<KC>: 1 FA round + KC - 2 chain rounds
 //   or_tree  [debug_rows open], or_tree_batch halving rounds, open_bits_to(P1)
 //            (circuits.hpp:387-486)
 //
@@ -228,11 +228,15 @@ __device__ __forceinline__ void prf_window64(const SeedKey& key, uint64_t e, boo
   }
 }
 
-// reshare (zero_ring<16>): own = z + F(seed_own) - F(seed_prev), hd at e = pos + i,
-// ml at pos + n + i.  Thread -> 8 lanes (warp-contiguous windows).
-__global__ void k_pty_reshare(const uint16_t* __restrict__ zh, const uint16_t* __restrict__ zm, uint64_t n,
-                              SeedKey own, SeedKey prev, uint64_t pos_own, uint64_t pos_prev,
-                              uint16_t* __restrict__ out_h, uint16_t* __restrict__ out_m) {
+// reshare_pair<KH, KM> (engine.cpp:80-106, zero_ring<K> = low K bits of the
+// u64 draws): own = z + F(seed_own) - F(seed_prev), hd at e = pos + i, ml at
+// pos + n + i (KM > 0).  Writes the own components as u32 and the message in
+// the reference's serialisation: n hd elements of HB bytes, then n ml elements
+// of MB bytes.  Thread -> 8 lanes (warp-contiguous windows).
+template <int HB, int MB>
+__global__ void k_pty_reshare(const void* __restrict__ zh, const void* __restrict__ zm, uint64_t n, SeedKey own,
+                              SeedKey prev, uint64_t pos_own, uint64_t pos_prev, uint32_t* __restrict__ out_h,
+                              uint32_t* __restrict__ out_m, uint8_t* __restrict__ msg) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t L8 = t * 8;
   const uint64_t ngrp = cdiv(n, 8);
@@ -240,16 +244,61 @@ __global__ void k_pty_reshare(const uint16_t* __restrict__ zh, const uint16_t* _
   const bool next_contig = (t & 31) != 31;  // lane 31's neighbour window lives in the next warp
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
-    const uint16_t* z = f == 0 ? zh : zm;
-    uint16_t* o = f == 0 ? out_h : out_m;
+    const int B = f == 0 ? HB : MB;
+    if (B == 0) continue;
     const uint64_t off = f == 0 ? 0 : n;
     uint32_t fo[8], fp[8];
     prf_window<1>(own, pos_own + off + L8, next_contig, fo);
     prf_window<1>(prev, pos_prev + off + L8, next_contig, fp);
     if (t >= ngrp) continue;
+    uint32_t* o = f == 0 ? out_h : out_m;
+    uint8_t* mg = msg + (f == 0 ? 0 : n * HB);
+    const uint32_t kmask = B == 4 ? 0xFFFFFFFFu : 0xFFFFu;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (L8 + i < n) o[L8 + i] = (uint16_t)(z[L8 + i] + fo[i] - fp[i]);
+    for (int i = 0; i < 8; ++i) {
+      const uint64_t j = L8 + i;
+      if (j >= n) break;
+      const uint32_t z = B == 4 ? static_cast<const uint32_t*>(f == 0 ? zh : zm)[j]
+                                : static_cast<const uint16_t*>(f == 0 ? zh : zm)[j];
+      const uint32_t v = (z + fo[i] - fp[i]) & kmask;
+      o[j] = v;
+      if (B == 4)
+        reinterpret_cast<uint32_t*>(mg)[j] = v;
+      else
+        reinterpret_cast<uint16_t*>(mg)[j] = (uint16_t)v;
+    }
+  }
+}
+
+// the previous party's message -> its own components as u32 (our prev components)
+template <int HB, int MB>
+__global__ void k_pty_unpack(const uint8_t* __restrict__ msg, uint64_t n, uint32_t* __restrict__ prev_h,
+                             uint32_t* __restrict__ prev_m) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  prev_h[j] = HB == 4 ? reinterpret_cast<const uint32_t*>(msg)[j] : reinterpret_cast<const uint16_t*>(msg)[j];
+  if (MB) {
+    const uint8_t* m = msg + n * HB;
+    prev_m[j] = MB == 4 ? reinterpret_cast<const uint32_t*>(m)[j] : reinterpret_cast<const uint16_t*>(m)[j];
+  }
+}
+
+// comparison input for the variants without the MPC lift (engine.hpp:77-120), per component:
+//   const-lift / no-lift : ml32 = ml, diff = a ml - b hd (mod 2^32; const_lift(hd16, b) = b hd)
+//   plain-mask           : diff = public_minus(ceil((1 - 2r) public_ml), hd) mod 2^16, the
+//                          constant entering component 1 (own at P1, prev at P2, rep3.hpp:59-71)
+__global__ void k_pty_cmp(int plain, const uint32_t* __restrict__ hd, const uint32_t* __restrict__ ml,
+                          const uint16_t* __restrict__ pub, uint64_t n, uint32_t a, uint32_t b, double coef,
+                          int add_t, uint32_t* __restrict__ ml32, uint32_t* __restrict__ diff) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  if (plain) {
+    const uint32_t t = add_t ? (uint32_t)(int64_t)ceil(__dmul_rn(coef, (double)pub[j])) : 0u;
+    diff[j] = (t - hd[j]) & 0xFFFFu;
+    ml32[j] = 0;
+  } else {
+    ml32[j] = ml[j];
+    diff[j] = a * ml[j] - b * hd[j];
   }
 }
 
@@ -414,7 +463,7 @@ __global__ void k_pty_inject_p2(const uint64_t* __restrict__ bo, uint64_t n, uin
 
 // lift output and comparison input per component (convert.hpp:169-192,
 // engine.hpp:94-120): ml32 = ml - (inj17 << 17) - (inj16 << 16), diff = a ml32 - b hd
-__global__ void k_pty_diff(const uint16_t* __restrict__ ml, const uint16_t* __restrict__ hd,
+__global__ void k_pty_diff(const uint32_t* __restrict__ ml, const uint32_t* __restrict__ hd,
                            const uint16_t* __restrict__ i17, const uint16_t* __restrict__ i16, uint64_t n2,
                            uint32_t a, uint32_t b, uint32_t* __restrict__ ml32, uint32_t* __restrict__ diff) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // [comp][lane]
@@ -538,6 +587,8 @@ struct irismpc_gpu_party {
   irismpc_gpu_config cfg{};
   int p = 0;  // 0..2
   int shamir = 0;
+  int variant = kMpcLift;
+  VariantWidths vw{16, 16, 32};
   uint32_t l = 0, l_pad = 0;
   uint64_t rec = 0;
   SeedKey own{}, prev{};
@@ -555,7 +606,7 @@ struct irismpc_gpu_party {
   size_t nxev = 0;
   // work buffers
   DBuf qpay, dots, rs, rows, carry, chain, zbuf, zrecv, inj, msg, msg2, ml32, diff, bits, pairs, groups, levels,
-      pool[2], tz[2], rowoff, open_buf[3];
+      pool[2], tz[2], rowoff, open_buf[3], xsend, xrecv;
   uint64_t tap_n = 0;
 };
 
@@ -598,14 +649,21 @@ int step(irismpc_gpu_party* c, Phase ph, const std::vector<Msg>& sends, const st
 
 int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party** out, std::string* why) {
   if (!cfg || !out || party < 1 || party > 3) return IRISMPC_GPU_ERR_CONFIG;
-  if (cfg->variant != IRISMPC_GPU_VARIANT_MPC_LIFT) {
-    *why = "party mode implements the mpc-lift variant";
+  if (cfg->variant > IRISMPC_GPU_VARIANT_NO_LIFT) {
+    *why = "unknown variant";
     return IRISMPC_GPU_ERR_CONFIG;
   }
-  if (cfg->backend > 1 || cfg->l == 0 || cfg->l % 8 != 0) return IRISMPC_GPU_ERR_BOUNDS;
-  if (cfg->a > cfg->b || cfg->m != 16 || cfg->b != (1u << 16) || cfg->rotations % 2 == 0) return IRISMPC_GPU_ERR_BOUNDS;
-  const uint64_t t = 1ull << 32, bl = (uint64_t)cfg->b * cfg->l;
-  if (!(bl < t / 4 && bl < t - (t >> 1))) return IRISMPC_GPU_ERR_BOUNDS;
+  // EngineConfig::validate (engine.cpp:21-34)
+  if (cfg->backend > 1) return IRISMPC_GPU_ERR_CONFIG;
+  if (cfg->l == 0 || cfg->l % 8 != 0 || cfg->a > cfg->b || cfg->rotations % 2 == 0) return IRISMPC_GPU_ERR_BOUNDS;
+  if (cfg->variant == IRISMPC_GPU_VARIANT_PLAIN_MASK) {
+    const uint64_t t = 1ull << 16;
+    if (!(cfg->l < t / 4 && cfg->l < t - (t >> 1))) return IRISMPC_GPU_ERR_BOUNDS;
+  } else {
+    if (cfg->m != 16 || cfg->b != (1u << 16)) return IRISMPC_GPU_ERR_BOUNDS;
+    const uint64_t t = 1ull << 32, bl = (uint64_t)cfg->b * cfg->l;
+    if (!(bl < t / 4 && bl < t - (t >> 1))) return IRISMPC_GPU_ERR_BOUNDS;
+  }
   if (cfg->rotations > 31) return IRISMPC_GPU_ERR_CONFIG;
   if (cfg->backend == IRISMPC_GPU_BACKEND_SHAMIR && cfg->rotations > 1 && (cfg->l / 64) % 2 != 0)
     return IRISMPC_GPU_ERR_BOUNDS;
@@ -619,15 +677,18 @@ int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party*
   c->rec = irismpc_gpu_record_bytes(cfg->backend, cfg->variant, cfg->l);
   std::memcpy(c->own.k, cfg->seeds, 16);
   std::memcpy(c->prev.k, cfg->seeds + 16, 16);
-  const uint64_t code_b = c->rec / 2;  // mpc-lift: code and mask records have the same size
+  c->variant = (int)cfg->variant;
+  c->vw = variant_widths(c->variant);
+  const int widths[2] = {c->vw.kh / 8, c->vw.km / 8};  // 0: public mask bits
+  const uint64_t code_b = (uint64_t)(c->shamir ? cfg->l : 2 * cfg->l) * widths[0];
   for (int fi = 0; fi < 2; ++fi) {
     PartyField& f = c->fld[fi];
     f.fmt.rec_bytes = c->rec;
     f.fmt.off = fi == 0 ? 0 : code_b;
-    f.fmt.width = 2;
-    f.fmt.limbs = 2;
-    f.slots = c->shamir ? 1 : 2;
-    f.nseg = c->shamir ? 1 : 2;
+    f.fmt.width = widths[fi];
+    f.fmt.limbs = widths[fi] ? widths[fi] : 1;
+    f.slots = (widths[fi] && !c->shamir) ? 2 : 1;
+    f.nseg = (widths[fi] && !c->shamir) ? 2 : 1;
   }
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -649,7 +710,7 @@ void parse_party_rows(irismpc_gpu_party* c, PartyField& f, const uint8_t* pay, u
   FieldFmt fo = f.fmt;
   fo.slot = 0;
   launch_parse_field(pay, rows, 0, c->l, c->l_pad, s_pad, c->p, c->shamir, fo, planes, c->st);
-  if (!c->shamir) {
+  if (!c->shamir && f.fmt.width) {
     FieldFmt fp = f.fmt;
     fp.slot = 1;
     fp.take_prev = 1;
@@ -893,23 +954,29 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   if (!c->qpay.ensure(qlen)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query)");
   PCK(c, cudaMemcpyAsync(c->qpay.p, hq, qlen, cudaMemcpyHostToDevice, st));
   const uint8_t* dq = c->qpay.as<uint8_t>();
-  if (!c->dots.ensure(2 * (n + 8) * 2) || !c->rs.ensure(4 * (n + 8) * 2))
+  const VariantWidths vw = c->vw;
+  const int V = c->variant;
+  const int hb = c->fld[0].fmt.limbs == 4 ? 4 : 2, mb = c->fld[1].fmt.limbs == 4 ? 4 : 2;  // dot element bytes
+  const uint64_t nml = vw.km ? n : 0;
+  if (!c->dots.ensure((n + 8) * (hb + mb) + 64) || !c->rs.ensure(4 * (n + 8) * 4 + 64))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dots)");
-  uint16_t* dh = c->dots.as<uint16_t>();
-  uint16_t* dm = dh + n + 8;
+  uint8_t* dh = c->dots.as<uint8_t>();
+  uint8_t* dm = dh + rup((n + 8) * hb, 16);
   for (int fi = 0; fi < 2; ++fi) {
     PartyField& f = c->fld[fi];
-    const uint64_t rows = 3ull * f.nseg * f.fmt.limbs * ncols_pad;
+    const uint32_t L = (uint32_t)f.fmt.limbs, bn = gemm_bn(L);
+    const int eb = L == 4 ? 4 : 2;
+    const uint64_t rows = 3ull * f.nseg * L * ncols_pad;
     if (ncols_pad != f.ncols_pad_cur) {
       if (!f.q.ensure(rows * c->l_pad)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query planes)");
       PCK(c, cudaMemsetAsync(f.q.p, 0, rows * c->l_pad, st));
-      if (make_plane_tmap(&f.tB, f.q.p, rows, c->l_pad, gemm_bn(2) / 2))
+      if (make_plane_tmap(&f.tB, f.q.p, rows, c->l_pad, bn / 2))
         return pfail(c, IRISMPC_GPU_ERR_DEVICE, "tensor map (query)");
       f.ncols_pad_cur = ncols_pad;
     }
     // B planes of this party's payload (problem 0; the kernel also fills 1, 2 from the same bytes)
     launch_parse_query_field(dq, dq, dq, ncodes, c->l, c->l_pad, r, ncols_pad, c->shamir, f.fmt, f.q.as<uint8_t>(), st);
-    uint16_t* out = fi == 0 ? dh : dm;
+    uint8_t* out = fi == 0 ? dh : dm;
     if (S) {
       GemmArgs g{};
       g.s_pad = (uint32_t)c->s_pad;
@@ -918,17 +985,17 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
       g.nseg = f.nseg;
       g.rep = f.nseg == 2;
       g.nprob = 1;
-      g.limbs = 2;
+      g.limbs = L;
       g.s_valid = (uint32_t)S;
       g.ncols = (uint32_t)ncols;
       g.out = out;
       g.out_pstride = ncols * S;
       g.out_cstride = (uint32_t)S;
-      launch_gemm(f.tA, f.tB, g, (uint32_t)(c->s_pad / kGemmBM), (uint32_t)cdiv(ncols, 256), st);
+      launch_gemm(f.tA, f.tB, g, (uint32_t)(c->s_pad / kGemmBM), (uint32_t)cdiv(ncols, bn), st);
     }
     if (npairs) {
       const uint64_t spq = rup(ncodes, 2 * kGemmBM);
-      const uint64_t arows = (uint64_t)f.slots * f.fmt.limbs * spq;
+      const uint64_t arows = (uint64_t)f.slots * L * spq;
       if (spq != f.qa_spad) {
         if (!f.qa.ensure(arows * c->l_pad)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair planes)");
         PCK(c, cudaMemsetAsync(f.qa.p, 0, arows * c->l_pad, st));
@@ -937,7 +1004,7 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
         f.qa_spad = spq;
       }
       parse_party_rows(c, f, dq, ncodes, spq, f.qa.as<uint8_t>());
-      if (!f.pc.ensure(ncols * ncodes * 2 + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
+      if (!f.pc.ensure(ncols * ncodes * eb + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
       GemmArgs g{};
       g.s_pad = (uint32_t)spq;
       g.nb_rows = ncols_pad;
@@ -945,76 +1012,106 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
       g.nseg = f.nseg;
       g.rep = f.nseg == 2;
       g.nprob = 1;
-      g.limbs = 2;
+      g.limbs = L;
       g.s_valid = ncodes;
       g.ncols = (uint32_t)ncols;
       g.out = f.pc.p;
       g.out_pstride = ncols * ncodes;
       g.out_cstride = ncodes;
-      launch_gemm(f.tQA, f.tB, g, (uint32_t)(spq / kGemmBM), (uint32_t)cdiv(ncols, 256), st);
-      launch_pair_gather(f.pc.p, 2, 1, ncodes, (uint32_t)ncols, persons, r, out + ncols * S, npairs, st);
+      launch_gemm(f.tQA, f.tB, g, (uint32_t)(spq / kGemmBM), (uint32_t)cdiv(ncols, bn), st);
+      launch_pair_gather(f.pc.p, eb, 1, ncodes, (uint32_t)ncols, persons, r, out + ncols * S * eb, npairs, st);
     }
   }
   PCK(c, cudaGetLastError());
   PCK(c, cudaEventRecord(c->pev[0], st));
-  // ---- dot phase: reshare_pair<16,16>, own -> next, prev <- previous
-  uint16_t* rs_own = c->rs.as<uint16_t>();        // [hd n+8 | ml n+8]
-  uint16_t* rs_prev = rs_own + 2 * (n + 8);
-  k_pty_reshare<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1],
-                                                                  rs_own, rs_own + n + 8);
-  PCK(c, cudaGetLastError());
-  int rc = step(c, kDot, {{next_of(p), rs_own, 2 * (n + 8) * 2}}, {{prev_of(p), rs_prev, 2 * (n + 8) * 2}}, {4 * n}, 1);
-  if (rc) return rc;
-  const uint16_t* hd_o = rs_own;
-  const uint16_t* ml_o = rs_own + n + 8;
-  const uint16_t* hd_p = rs_prev;
-  const uint16_t* ml_p = rs_prev + n + 8;
-  PCK(c, cudaEventRecord(c->pev[1], st));
-  // ---- lift<16,16>
-  if (!c->rows.ensure(2ull * 32 * W * 8 + 64) || !c->bits.ensure(4ull * W * 8 + 64) ||
-      !c->inj.ensure(4ull * (n + 8) * 2 + 64))
-    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (lift)");
-  uint64_t* rows = c->rows.as<uint64_t>();
-  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));  // odd trailing half-word
-  k_pty_split<uint16_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
-  uint64_t* b_o = c->bits.as<uint64_t>();  // [inst][W]: bit16, bit17
-  uint64_t* b_p = b_o + 2 * W;
-  const uint64_t ecore[3] = {2 * n, 0, 6 * n};  // inject draws before the MSB, per seed
-  rc = bit_extract(c, kLift, rows, rows + 16 * W, 16, {16, 17}, n, W, c->pos[0] + 2 * n, c->pos[1] + 2 * n, b_o, b_p);
-  if (rc) return rc;
-  uint16_t* i17 = c->inj.as<uint16_t>();  // [comp][n+8]
-  uint16_t* i16 = i17 + 2 * (n + 8);
-  // seed_1 / seed_3 element bases (own/prev stream positions by role)
-  const uint64_t pos1 = p == 0 ? c->pos[0] : (p == 1 ? c->pos[1] : 0);
-  const uint64_t pos3 = p == 0 ? c->pos[1] : (p == 2 ? c->pos[0] : 0);
-  rc = bit_inject(c, b_o + W, b_p + W, n, 15, pos1 + 2 * n + 64 * W, pos3 + 2 * n + 64 * W, i17, i17 + n + 8);
-  if (rc) return rc;
-  rc = bit_inject(c, b_o, b_p, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
-  if (rc) return rc;
-  PCK(c, cudaEventRecord(c->pev[2], st));
-  // ---- diff, msb<32>
-  if (!c->ml32.ensure(2 * (n + 8) * 4) || !c->diff.ensure(2 * (n + 8) * 4))
-    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (diff)");
-  uint32_t* ml32 = c->ml32.as<uint32_t>();
-  uint32_t* diff = c->diff.as<uint32_t>();
-  // components laid out [own n+8 | prev n+8] for every array
+  // ---- dot phase: reshare_pair<KH, KM>, own -> next, prev <- previous
+  uint32_t* hd_o = c->rs.as<uint32_t>();  // [hd own | ml own | hd prev | ml prev] x (n + 8) u32
+  uint32_t* ml_o = hd_o + (n + 8);
+  uint32_t* hd_p = hd_o + 2 * (n + 8);
+  uint32_t* ml_p = hd_o + 3 * (n + 8);
+  const uint64_t msg_bytes = n * (vw.kh / 8) + nml * (vw.km / 8);
+  if (!c->xsend.ensure(msg_bytes + 64) || !c->xrecv.ensure(msg_bytes + 64))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (reshare)");
   {
-    // ml and hd: own and prev halves are in different buffers -> two launches
+    const unsigned gr = nblk(rup(cdiv(n, 8), 32));
+    uint8_t* xs = c->xsend.as<uint8_t>();
+    if (vw.kh == 16 && vw.km == 0)
+      k_pty_reshare<2, 0><<<gr, kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1], hd_o, ml_o, xs);
+    else if (vw.kh == 16 && vw.km == 16)
+      k_pty_reshare<2, 2><<<gr, kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1], hd_o, ml_o, xs);
+    else if (vw.kh == 16)
+      k_pty_reshare<2, 4><<<gr, kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1], hd_o, ml_o, xs);
+    else
+      k_pty_reshare<4, 4><<<gr, kThreads, 0, st>>>(dh, dm, n, c->own, c->prev, c->pos[0], c->pos[1], hd_o, ml_o, xs);
+  }
+  PCK(c, cudaGetLastError());
+  int rc = step(c, kDot, {{next_of(p), c->xsend.p, msg_bytes}}, {{prev_of(p), c->xrecv.p, msg_bytes}}, {msg_bytes}, 1);
+  if (rc) return rc;
+  {
+    const uint8_t* xr = c->xrecv.as<uint8_t>();
+    if (vw.kh == 16 && vw.km == 0)
+      k_pty_unpack<2, 0><<<nblk(n), kThreads, 0, st>>>(xr, n, hd_p, ml_p);
+    else if (vw.kh == 16 && vw.km == 16)
+      k_pty_unpack<2, 2><<<nblk(n), kThreads, 0, st>>>(xr, n, hd_p, ml_p);
+    else if (vw.kh == 16)
+      k_pty_unpack<2, 4><<<nblk(n), kThreads, 0, st>>>(xr, n, hd_p, ml_p);
+    else
+      k_pty_unpack<4, 4><<<nblk(n), kThreads, 0, st>>>(xr, n, hd_p, ml_p);
+  }
+  PCK(c, cudaEventRecord(c->pev[1], st));
+  if (!c->rows.ensure(2ull * 32 * W * 8 + 64) || !c->bits.ensure(4ull * W * 8 + 64) ||
+      !c->inj.ensure(4ull * (n + 8) * 2 + 64) || !c->ml32.ensure(2 * (n + 8) * 4) || !c->diff.ensure(2 * (n + 8) * 4))
+    return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (comparison)");
+  uint64_t* rows = c->rows.as<uint64_t>();
+  uint64_t* b_o = c->bits.as<uint64_t>();  // [inst][W]: bit16, bit17 (mpc-lift)
+  uint64_t* b_p = b_o + 2 * W;
+  uint32_t* ml32 = c->ml32.as<uint32_t>();  // components laid out [own n+8 | prev n+8]
+  uint32_t* diff = c->diff.as<uint32_t>();
+  // stream layout: reshare n (+ n), then for mpc-lift the 64 lift
+  // gates and the injects (seed 1: 2n, seed 3: 6n), then the MSB gates
+  const uint64_t lift_draws[3] = {2 * n, 0, 6 * n};
+  uint64_t msb_o = c->pos[0] + n + nml, msb_p = c->pos[1] + n + nml;
+  if (V == kMpcLift) {
+    // ---- lift<16,16>
+    if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));  // odd trailing half-word
+    k_pty_split<uint32_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
+    rc = bit_extract(c, kLift, rows, rows + 16 * W, 16, {16, 17}, n, W, c->pos[0] + 2 * n, c->pos[1] + 2 * n, b_o, b_p);
+    if (rc) return rc;
+    uint16_t* i17 = c->inj.as<uint16_t>();  // [comp][n+8]
+    uint16_t* i16 = i17 + 2 * (n + 8);
+    // seed_1 / seed_3 element bases (own/prev stream positions by role)
+    const uint64_t pos1 = p == 0 ? c->pos[0] : (p == 1 ? c->pos[1] : 0);
+    const uint64_t pos3 = p == 0 ? c->pos[1] : (p == 2 ? c->pos[0] : 0);
+    rc = bit_inject(c, b_o + W, b_p + W, n, 15, pos1 + 2 * n + 64 * W, pos3 + 2 * n + 64 * W, i17, i17 + n + 8);
+    if (rc) return rc;
+    rc = bit_inject(c, b_o, b_p, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
+    if (rc) return rc;
     k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_o, hd_o, i17, i16, n, c->cfg.a, c->cfg.b, ml32, diff);
     k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_p, hd_p, i17 + n + 8, i16 + n + 8, n, c->cfg.a, c->cfg.b,
                                              ml32 + n + 8, diff + n + 8);
+    msb_o += 64 * W + lift_draws[ko];
+    msb_p += 64 * W + lift_draws[kp];
+  } else {
+    const int plain = V == kPlainMask;
+    const double coef = 1.0 - 2.0 * c->cfg.match_ratio;
+    const uint16_t* pub = reinterpret_cast<const uint16_t*>(dm);  // plain-mask: the public popcounts
+    k_pty_cmp<<<nblk(n), kThreads, 0, st>>>(plain, hd_o, ml_o, pub, n, c->cfg.a, c->cfg.b, coef, p == 0, ml32, diff);
+    k_pty_cmp<<<nblk(n), kThreads, 0, st>>>(plain, hd_p, ml_p, pub, n, c->cfg.a, c->cfg.b, coef, p == 1,
+                                            ml32 + n + 8, diff + n + 8);
   }
-  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 32 * W * 8, st));
-  k_pty_split<uint32_t, 32><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
+  PCK(c, cudaGetLastError());
+  PCK(c, cudaEventRecord(c->pev[2], st));
+  // ---- msb<KC>
+  const int KC = vw.kc;
+  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * KC * W * 8, st));
+  if (KC == 32)
+    k_pty_split<uint32_t, 32><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
+  else
+    k_pty_split<uint32_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
   uint64_t* mb_o = b_o + 2 * W;  // msb bit rows (own, prev) in the second half of `bits`
   uint64_t* mb_p = b_o + 3 * W;
-  const uint64_t msb_o = c->pos[0] + 2 * n + 64 * W + ecore[ko];
-  const uint64_t msb_p = c->pos[1] + 2 * n + 64 * W + ecore[kp];
-  {
-    // results are written at res + k W for k = 0: own -> mb_o, prev -> mb_p
-    rc = bit_extract(c, kMsb, rows, rows + 32 * W, 32, {31}, n, W, msb_o, msb_p, mb_o, mb_p);
-    if (rc) return rc;
-  }
+  rc = bit_extract(c, kMsb, rows, rows + (uint64_t)KC * W, KC, {KC - 1}, n, W, msb_o, msb_p, mb_o, mb_p);
+  if (rc) return rc;
   PCK(c, cudaEventRecord(c->pev[3], st));
   // ---- taps (parity tests)
   c->tap_n = n;
@@ -1070,7 +1167,8 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
     k_pty_or_gather<<<nblk(ngroups * max_w), kThreads, 0, st>>>(c->groups.as<OrGroup>(), ngroups,
                                                                  c->pairs.as<uint64_t>(), mb_o, mb_p, cur[0], cur[1],
                                                                  max_w);
-  const uint64_t or_o = msb_o + 61 * W, or_p = msb_p + 61 * W;
+  const uint64_t msb_gates = 2ull * KC - 3;
+  const uint64_t or_o = msb_o + msb_gates * W, or_p = msb_p + msb_gates * W;
   std::vector<uint64_t> roff(ngroups);
   for (uint32_t g2 = 0; g2 < ngroups; ++g2) roff[g2] = grp[g2].row_off;
   uint64_t used = 0;
@@ -1137,8 +1235,8 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   // ---- stream positions advance exactly as the reference's (A.3)
   const uint64_t glen = membership ? S : 2ull * r * S + (uint64_t)(persons ? persons - 1 : 0) * 4 * r;
   const uint64_t ord = ref_or_draws(ngroups, glen, nullptr);
-  c->pos[0] = msb_o + 61 * W + ord;
-  c->pos[1] = msb_p + 61 * W + ord;
+  c->pos[0] = or_o + ord;
+  c->pos[1] = or_p + ord;
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     stats->s = S;
@@ -1251,7 +1349,8 @@ void irismpc_gpu_party_destroy(irismpc_gpu_party* c) {
   cudaStreamSynchronize(c->st);
   DBuf* bufs[] = {&c->qpay, &c->dots, &c->rs, &c->rows, &c->carry, &c->chain, &c->zbuf, &c->zrecv, &c->inj,
                   &c->msg, &c->msg2, &c->ml32, &c->diff, &c->bits, &c->pairs, &c->groups, &c->levels, &c->pool[0],
-                  &c->pool[1], &c->tz[0], &c->tz[1], &c->rowoff, &c->open_buf[0], &c->open_buf[1], &c->open_buf[2]};
+                  &c->pool[1], &c->tz[0], &c->tz[1], &c->rowoff, &c->open_buf[0], &c->open_buf[1], &c->open_buf[2],
+                  &c->xsend, &c->xrecv};
   for (DBuf* b : bufs) b->release();
   for (auto& f : c->fld) {
     f.db.release();
@@ -1323,15 +1422,17 @@ int irismpc_gpu_party_read_tap(irismpc_gpu_party* c, int tap, void* host_out, si
   switch (tap) {
     case IRISMPC_GPU_TAP_DOT_HD:
     case IRISMPC_GPU_TAP_DOT_ML: {
-      if (bytes < n * 2) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "tap buffer too small");
-      const uint16_t* d = c->dots.as<uint16_t>() + (tap == IRISMPC_GPU_TAP_DOT_ML ? n + 8 : 0);
-      PCK(c, cudaMemcpy(host_out, d, n * 2, cudaMemcpyDeviceToHost));
+      const int fi = tap == IRISMPC_GPU_TAP_DOT_ML ? 1 : 0;
+      const int hbb = c->fld[0].fmt.limbs == 4 ? 4 : 2, eb = c->fld[fi].fmt.limbs == 4 ? 4 : 2;
+      if (bytes < n * eb) return pfail(c, IRISMPC_GPU_ERR_CONFIG, "tap buffer too small");
+      const uint8_t* d = c->dots.as<uint8_t>() + (fi ? rup((n + 8) * hbb, 16) : 0);
+      PCK(c, cudaMemcpy(host_out, d, n * eb, cudaMemcpyDeviceToHost));
       return 0;
     }
     case IRISMPC_GPU_TAP_RS_HD:
-      return copy2(c->rs.as<uint16_t>(), c->rs.as<uint16_t>() + 2 * (n + 8), 2);
+      return copy2(c->rs.as<uint32_t>(), c->rs.as<uint32_t>() + 2 * (n + 8), 4);
     case IRISMPC_GPU_TAP_RS_ML:
-      return copy2(c->rs.as<uint16_t>() + n + 8, c->rs.as<uint16_t>() + 3 * (n + 8), 2);
+      return copy2(c->rs.as<uint32_t>() + n + 8, c->rs.as<uint32_t>() + 3 * (n + 8), 4);
     case IRISMPC_GPU_TAP_ML32:
       return copy2(c->ml32.as<uint32_t>(), c->ml32.as<uint32_t>() + n + 8, 4);
     case IRISMPC_GPU_TAP_DIFF:

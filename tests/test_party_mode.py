@@ -111,3 +111,44 @@ def test_empty_db_membership_both_engines(be):
     sess.load_db(db, 0)
     assert sess.membership(q) is False
     np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
+
+
+@pytest.mark.parametrize("var", [P.PLAIN_MASK, P.CONST_LIFT, P.NO_LIFT])
+@pytest.mark.parametrize("be,l,s,persons,r,seed", [
+    (O.SHAMIR, 256, 300, 3, 5, 81),
+    (O.REPLICATED, 128, 90, 2, 31, 82),
+    (O.SHAMIR, 12800, 40, 2, 31, 83),
+])
+def test_party_mode_variants(var, be, l, s, persons, r, seed):
+    """Party mode for plain-mask / const-lift / no-lift: shares through the MSB,
+    ledger, stream positions, row and person bits vs the oracle."""
+    rng = O.Rng(seed)
+    dc, dm = O.records(rng, l, s, 0.9)
+    qc, qm = O.records(rng, l, 2 * persons, 0.9)
+    qc[0], qm[0] = dc[s // 2], dm[s // 2]
+    db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)), variant=var)
+    q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)), variant=var)
+    seeds = O.party_seeds(seed)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True, variant=var)
+    parties = P.run_parties_inproc(cfg, seeds, db, s, q, persons, want_rows=True)
+    ref = O.query(O.make_config(be, l, 0.375, r, debug_rows=True, variant=var), seeds, db, s, q, persons,
+                  want_all=True)
+    n = P.lane_count(persons, s, r)
+    np.testing.assert_array_equal(parties[0].result, ref.person_match)
+    np.testing.assert_array_equal(parties[0].row_bits[:n], ref.row_bits)
+    assert parties[0].result[0] == 1
+    for i, pt in enumerate(parties):
+        own, prev = i, (i + 2) % 3
+        np.testing.assert_array_equal(pt.read_tap(P.TAP_DOT_HD, n), ref.dot_hd[own], err_msg=f"P{i+1} dot_hd")
+        if P.VARIANT_WIDTHS[var][1]:
+            np.testing.assert_array_equal(pt.read_tap(P.TAP_DOT_ML, n), ref.dot_ml[own], err_msg=f"P{i+1} dot_ml")
+        else:
+            np.testing.assert_array_equal(pt.read_tap(P.TAP_DOT_ML, n), ref.public_ml, err_msg=f"P{i+1} public_ml")
+        for tap, name in ((P.TAP_RS_HD, "rs_hd"), (P.TAP_RS_ML, "rs_ml"), (P.TAP_ML32, "ml32"),
+                          (P.TAP_DIFF, "diff"), (P.TAP_MSB, "msb")):
+            got = pt.read_tap(tap, n)
+            want = getattr(ref, name)
+            np.testing.assert_array_equal(got[0], want[own], err_msg=f"P{i+1} {name} own")
+            np.testing.assert_array_equal(got[1], want[prev], err_msg=f"P{i+1} {name} prev")
+        assert pt.last_stats.ledger() == ref.stats[i], f"P{i+1} ledger"
+        np.testing.assert_array_equal(pt.stream_positions(), [ref.stream_pos[own], ref.stream_pos[prev]])

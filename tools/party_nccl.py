@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--backend", default="shamir", choices=["shamir", "replicated"])
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--variant", default="mpc-lift", choices=["plain-mask", "mpc-lift", "const-lift", "no-lift"])
     ap.add_argument("--check", action="store_true", help="small case, every share vs the oracle")
     a = ap.parse_args()
 
@@ -53,12 +54,13 @@ def main():
     seed = 7
     if a.check:
         a.rows, a.persons, a.l, a.rotations = 300, 3, 256, 5
-    cfg = P.EngineConfig(backend=be, l=a.l, rotations=a.rotations, debug_rows=a.check)
+    var = P.VARIANTS[a.variant]
+    cfg = P.EngineConfig(backend=be, l=a.l, rotations=a.rotations, debug_rows=a.check, variant=var)
     seeds = P.seeds_from_master(seed)
     party = P.Party(cfg, rank + 1, P.party_seeds(seeds, rank + 1), nccl_id=nccl_id, device=local)
 
     # deal on the device (every rank deals all three payloads and keeps its own)
-    dealer = P.Session(P.EngineConfig(backend=be, l=a.l, rotations=1), master_seed=seed, device=local)
+    dealer = P.Session(P.EngineConfig(backend=be, l=a.l, rotations=1, variant=var), master_seed=seed, device=local)
     wl = (a.l + 63) // 64
     s, ncodes = a.rows, 2 * a.persons
     codes = torch.empty((s, wl), dtype=torch.int64, device="cuda")
@@ -104,7 +106,8 @@ def main():
         ledgers = [dict(zip(keys, [int(v) for v in x.tolist()])) for x in leds]
         host_ms = max(w[0].item() for w in walls)
         cmp_ = ncodes * a.rotations * s
-        line = {"mode": "party (3 ranks over NCCL, one GPU per party)", "backend": a.backend, "rows": s,
+        line = {"mode": "party (3 ranks over NCCL, one GPU per party)", "backend": a.backend, "variant": a.variant,
+                "rows": s,
                 "persons": a.persons, "lanes": n, "person_match": [int(x) for x in out],
                 "ms_per_query_max_over_parties": host_ms,
                 "device_ms": [round(w[1].item(), 3) for w in walls],
@@ -114,8 +117,8 @@ def main():
                 "wire_bytes_p1": int(st.wire_bytes)}
         if a.check:
             from oracle import pyoracle as O
-            ref = O.query(O.make_config(be, a.l, 0.375, a.rotations, debug_rows=True), seeds, all_db, s, all_q,
-                          a.persons, want_all=True)
+            ref = O.query(O.make_config(be, a.l, 0.375, a.rotations, debug_rows=True, variant=var), seeds, all_db, s,
+                          all_q, a.persons, want_all=True)
             line["check"] = {
                 "person_match": bool((out == ref.person_match).all()),
                 "row_bits": bool((party.row_bits[:n] == ref.row_bits).all()),

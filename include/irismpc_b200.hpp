@@ -263,4 +263,150 @@ class ThreePartyGpu {
   std::string error_;
 };
 
+// ---- party mode: one party per process or thread, every
+// message of the protocol through a transport, like PartyCtx on a TcpMesh.
+using Seed16 = std::array<std::uint8_t, 16>;
+
+inline std::array<std::uint8_t, 128> nccl_unique_id() {
+  std::array<std::uint8_t, 128> id{};
+  check(irismpc_gpu_nccl_unique_id(id.data()), "nccl_unique_id");
+  return id;
+}
+
+// InProcNet (transport.hpp:129-154): mailboxes for three parties in one process.
+class InProcNet {
+ public:
+  InProcNet() { check(irismpc_gpu_inproc_create(&h_), "inproc_create"); }
+  ~InProcNet() { irismpc_gpu_inproc_destroy(h_); }
+  InProcNet(const InProcNet&) = delete;
+  InProcNet& operator=(const InProcNet&) = delete;
+  irismpc_gpu_inproc* handle() const { return h_; }
+
+ private:
+  irismpc_gpu_inproc* h_ = nullptr;
+};
+
+// One party: its own payloads and its (own, prev) seeds (read_seed_file).
+class GpuParty {
+ public:
+  // NCCL: rank = party - 1 of a 3-rank communicator built from `nccl_id`.
+  GpuParty(const EngineConfig& cfg, unsigned party, const Seed16& own, const Seed16& prev,
+           const std::array<std::uint8_t, 128>& nccl_id, int device = 0)
+      : cfg_(cfg), party_(party) {
+    const irismpc_gpu_config c = make(cfg, own, prev, device);
+    check(irismpc_gpu_party_create_nccl(&c, party, nccl_id.data(), &h_), "party_create_nccl");
+  }
+  // in-process: the three parties share `net`, one host thread each.
+  GpuParty(const EngineConfig& cfg, unsigned party, const Seed16& own, const Seed16& prev, InProcNet& net,
+           int device = 0)
+      : cfg_(cfg), party_(party) {
+    const irismpc_gpu_config c = make(cfg, own, prev, device);
+    check(irismpc_gpu_party_create_inproc(&c, party, net.handle(), &h_), "party_create_inproc");
+  }
+  ~GpuParty() { irismpc_gpu_party_destroy(h_); }
+  GpuParty(const GpuParty&) = delete;
+  GpuParty& operator=(const GpuParty&) = delete;
+
+  unsigned party() const { return party_; }
+  std::uint64_t rows() const { return s_; }
+
+  void load_db(std::span<const std::uint8_t> payload, std::uint64_t s) {  // Session::load_db
+    pcheck(irismpc_gpu_party_load_db(h_, payload.data(), payload.size(), s), "load_db");
+    s_ = s;
+    loaded_ = payload;
+  }
+  bool loaded(std::span<const std::uint8_t> payload, std::uint64_t s) const {
+    return payload.data() == loaded_.data() && payload.size() == loaded_.size() && s == s_;
+  }
+
+  // Session::batch_query / membership at this party: person_match and row_bits at P1;
+  // stats = the measured ledger of this party's messages.
+  MembershipResult batch_query(std::span<const std::uint8_t> q, unsigned persons) {
+    return run(q, persons, false);
+  }
+  MembershipResult membership(std::span<const std::uint8_t> q) { return run(q, 1, true); }
+
+ private:
+  static irismpc_gpu_config make(const EngineConfig& cfg, const Seed16& own, const Seed16& prev, int device) {
+    irismpc_gpu_config c{};
+    c.backend = static_cast<std::uint32_t>(cfg.backend);
+    c.variant = static_cast<std::uint32_t>(cfg.variant);
+    c.l = cfg.l;
+    c.a = cfg.params.a;
+    c.b = cfg.params.b;
+    c.m = cfg.params.m;
+    c.match_ratio = cfg.params.match_ratio;
+    c.rotations = cfg.rotations;
+    c.debug_rows = cfg.debug_rows ? 1 : 0;
+    for (int i = 0; i < 16; ++i) {
+      c.seeds[i] = own[i];
+      c.seeds[16 + i] = prev[i];
+    }
+    c.device = device;
+    return c;
+  }
+  void pcheck(int rc, const char* what) {
+    if (rc == IRISMPC_GPU_OK) return;
+    const std::string msg = std::string(what) + ": " + irismpc_gpu_party_last_error(h_);
+    switch (rc) {
+      case IRISMPC_GPU_ERR_BOUNDS: throw BoundsError(msg);
+      case IRISMPC_GPU_ERR_DEVICE: throw TransportError(msg);
+      case IRISMPC_GPU_ERR_INCONSISTENT: throw InconsistentShareError(msg);
+      default: throw Error(msg);
+    }
+  }
+  MembershipResult run(std::span<const std::uint8_t> q, unsigned persons, bool membership) {
+    MembershipResult r;
+    const std::uint64_t n = irismpc_gpu_lane_count(persons, s_, membership ? 1 : cfg_.rotations, membership ? 1 : 0);
+    std::vector<std::uint8_t> pm(membership ? 1 : persons), rows(cfg_.debug_rows ? n : 0);
+    irismpc_gpu_party_stats st{};
+    const int rc = membership
+                       ? irismpc_gpu_party_membership(h_, q.data(), q.size(), pm.data(),
+                                                      cfg_.debug_rows ? rows.data() : nullptr, &st)
+                       : irismpc_gpu_party_batch_query(h_, q.data(), q.size(), persons, pm.data(),
+                                                       cfg_.debug_rows ? rows.data() : nullptr, &st);
+    pcheck(rc, membership ? "membership" : "batch_query");
+    r.lane_count = n;
+    if (party_ == 1) {
+      r.person_match = std::move(pm);
+      r.row_bits = std::move(rows);
+    }
+    r.stats.backend = cfg_.backend == Backend::shamir ? "shamir-galois" : "replicated";
+    r.stats.variant = to_string(cfg_.variant);
+    r.stats.s = st.s;
+    r.stats.l = st.l;
+    r.stats.batch = st.batch;
+    r.stats.dot_bytes = st.dot_bytes;
+    r.stats.lift_bytes = st.lift_bytes;
+    r.stats.msb_bytes = st.msb_bytes;
+    r.stats.or_tree_bytes = st.or_tree_bytes;
+    r.stats.dot_rounds = st.dot_rounds;
+    r.stats.lift_rounds = st.lift_rounds;
+    r.stats.msb_rounds = st.msb_rounds;
+    r.stats.or_tree_rounds = st.or_tree_rounds;
+    r.stats.wall_ms = st.wall_ms;
+    return r;
+  }
+
+  EngineConfig cfg_;
+  unsigned party_;
+  irismpc_gpu_party* h_ = nullptr;
+  std::uint64_t s_ = 0;
+  std::span<const std::uint8_t> loaded_{};
+};
+
+// party_batch_query(PartyCtx&, cfg, db_payload, s, query_payload, persons)
+// (engine.hpp:311-313) at one party; the DB stays resident between calls
+// with the same payload span.
+inline MembershipResult party_batch_query(GpuParty& ctx, std::span<const std::uint8_t> db_payload, std::uint64_t s,
+                                          std::span<const std::uint8_t> query_payload, unsigned persons) {
+  if (!ctx.loaded(db_payload, s)) ctx.load_db(db_payload, s);
+  return ctx.batch_query(query_payload, persons);
+}
+inline MembershipResult party_membership(GpuParty& ctx, std::span<const std::uint8_t> db_payload, std::uint64_t s,
+                                         std::span<const std::uint8_t> query_payload) {
+  if (!ctx.loaded(db_payload, s)) ctx.load_db(db_payload, s);
+  return ctx.membership(query_payload);
+}
+
 }  // namespace irismpc_b200

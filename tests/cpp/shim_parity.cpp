@@ -3,6 +3,7 @@
 // person_match must equal the oracle's; error paths map to the reference's
 // exception types.  Built and run by tests/test_cpp_shim.py.
 #include <cstdio>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -70,6 +71,49 @@ int main() {
     if (res[1].stats.lift_bytes != res[2].stats.lift_bytes) return 1;  // P2, P3 send 4n OT bytes
   }
   if (want[1] != 1) return 1;
+
+  // party mode: three GpuParty objects on one InProcNet, one thread each,
+  // the reference's per-party call shape; P1's bits and every party's
+  // measured ledger equal the oracle's (the reference's QueryStats)
+  {
+    orc_stats ost[3];
+    orc_out o2{};
+    std::vector<std::uint8_t> want2(persons);
+    o2.person_match = want2.data();
+    o2.stats = ost;
+    if (orc_query(&oc, seeds, db[0].data(), db[1].data(), db[2].data(), s, q[0].data(), q[1].data(), q[2].data(),
+                  persons, 0, nullptr, &o2) != 0)
+      return 2;
+    InProcNet net;
+    std::array<std::unique_ptr<GpuParty>, 3> pt;
+    for (unsigned p = 1; p <= 3; ++p) {
+      Seed16 own{}, prev{};
+      const unsigned pv = (p + 1) % 3;  // index of seed_{p-1} (p = 1..3 -> 2, 0, 1)
+      for (int i = 0; i < 16; ++i) {
+        own[i] = seeds[16 * (p - 1) + i];
+        prev[i] = seeds[16 * pv + i];
+      }
+      pt[p - 1] = std::make_unique<GpuParty>(cfg, p, own, prev, net);
+    }
+    std::array<MembershipResult, 3> res;
+    std::vector<std::thread> th;
+    for (unsigned p = 1; p <= 3; ++p)
+      th.emplace_back([&, p] { res[p - 1] = party_batch_query(*pt[p - 1], db[p - 1], s, q[p - 1], persons); });
+    for (auto& t : th) t.join();
+    if (res[0].person_match != want2) {
+      std::printf("MISMATCH party-mode person_match\n");
+      return 1;
+    }
+    for (int p = 0; p < 3; ++p) {
+      const auto& st = res[p].stats;
+      if (st.dot_bytes != ost[p].dot_bytes || st.lift_bytes != ost[p].lift_bytes || st.msb_bytes != ost[p].msb_bytes ||
+          st.or_tree_bytes != ost[p].or_tree_bytes || st.lift_rounds != ost[p].lift_rounds ||
+          st.or_tree_rounds != ost[p].or_tree_rounds) {
+        std::printf("MISMATCH party-mode ledger P%d\n", p + 1);
+        return 1;
+      }
+    }
+  }
 
   // error mapping: db payload size mismatch -> Error (engine.cpp:142)
   Session sess(cfg, seeds_from_master(seed));

@@ -1030,6 +1030,10 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   uint32_t* hd_p = hd_o + 2 * (n + 8);
   uint32_t* ml_p = hd_o + 3 * (n + 8);
   const uint64_t msg_bytes = n * (vw.kh / 8) + nml * (vw.km / 8);
+  if (!vw.km) {  // plain-mask: no shared ml (the taps read zeros, like the oracle's)
+    PCK(c, cudaMemsetAsync(ml_o, 0, (n + 8) * 4, st));
+    PCK(c, cudaMemsetAsync(ml_p, 0, (n + 8) * 4, st));
+  }
   if (!c->xsend.ensure(msg_bytes + 64) || !c->xrecv.ensure(msg_bytes + 64))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (reshare)");
   {

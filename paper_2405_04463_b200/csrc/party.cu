@@ -307,15 +307,15 @@ __global__ void k_pty_cmp(int plain, const uint32_t* __restrict__ hd, const uint
 // Thread -> 32 lanes of one component: 32x32 SWAR transpose, one u32 half-word per row.
 template <typename T, int K>
 __global__ void k_pty_split(const T* __restrict__ own, const T* __restrict__ prev, uint64_t n, uint64_t W,
-                            uint64_t* __restrict__ rows) {
+                            uint64_t* __restrict__ rows, uint64_t half_words) {
+  // half_words: 2 x the chunk's words; the ones past the last lane are written as zeros
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t ng = cdiv(n, 32);
-  if (t >= 2 * ng) return;
-  const int c = (int)(t / ng);
-  const uint64_t g = t % ng;
+  if (t >= 2 * half_words) return;
+  const int c = (int)(t / half_words);
+  const uint64_t g = t % half_words;
   const T* src = (c == 0 ? own : prev) + 32 * g;
   uint32_t a[32];
-  const uint64_t left = n - 32 * g;
+  const uint64_t left = 32 * g < n ? n - 32 * g : 0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) a[i] = (uint64_t)i < left ? (uint32_t)src[i] : 0u;
   transpose32(a);
@@ -597,6 +597,10 @@ struct irismpc_gpu_party {
   cudaStream_t st = nullptr;
   cudaEvent_t ev[2];
   cudaEvent_t pev[6];  // phase boundaries
+  // comparison-phase pipeline: lane chunks compute on cs[k] while the comm
+  // stream carries the other chunk's messages (same order at every party)
+  cudaStream_t cst = nullptr, cs[2] = {nullptr, nullptr};
+  cudaEvent_t ea[2], eb[2], ej[3];
   PartyField fld[2];
   uint64_t s = 0, s_pad = 0;
   bool db_loaded = false;
@@ -606,7 +610,7 @@ struct irismpc_gpu_party {
   size_t nxev = 0;
   // work buffers
   DBuf qpay, dots, rs, rows, carry, chain, zbuf, zrecv, inj, msg, msg2, ml32, diff, bits, pairs, groups, levels,
-      pool[2], tz[2], rowoff, open_buf[3], xsend, xrecv;
+      pool[2], tz[2], rowoff, open_buf[3], xsend, xrecv, c2buf;
   uint64_t tap_n = 0;
 };
 
@@ -625,26 +629,53 @@ int pfail(irismpc_gpu_party* c, int code, const std::string& m) {
 int next_of(int p) { return (p + 1) % 3; }
 int prev_of(int p) { return (p + 2) % 3; }
 
+// one lane chunk of the pipelined comparison phase
+struct Chunk {
+  int idx;             // 0 counts the protocol rounds
+  uint64_t w0, words;  // 64-lane words [w0, w0 + words)
+  uint64_t lane0, lanes;
+  cudaStream_t st;     // compute stream
+};
+
 // one protocol step through the transport + the ledger (counted bytes per the
-// reference's serialisation; rounds per ctx.comm.round call of that phase)
-int step(irismpc_gpu_party* c, Phase ph, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
-         const std::vector<uint64_t>& counted, uint32_t rounds) {
+// reference's serialisation; rounds per ctx.comm.round call of that phase).
+// On a chunk stream the message hops to the comm stream and back, so this
+// chunk's transfer overlaps the other chunk's kernels.
+int step_on(irismpc_gpu_party* c, cudaStream_t cs, bool count_rounds, Phase ph, const std::vector<Msg>& sends,
+            const std::vector<Msg>& recvs, const std::vector<uint64_t>& counted, uint32_t rounds) {
   for (size_t i = 0; i < sends.size(); ++i) {
     c->led_bytes[ph] += i < counted.size() ? counted[i] : sends[i].bytes;
     c->wire += sends[i].bytes;
   }
-  c->led_rounds[ph] += rounds;
+  if (count_rounds) c->led_rounds[ph] += rounds;
   while (c->xev.size() < c->nxev + 2) {
     cudaEvent_t e;
     cudaEventCreate(&e);
     c->xev.push_back(e);
   }
-  cudaEventRecord(c->xev[c->nxev], c->st);
-  const std::string e = c->net->exchange(c->p, sends, recvs, c->st);
-  cudaEventRecord(c->xev[c->nxev + 1], c->st);
+  cudaStream_t xs = cs;
+  int k = -1;
+  if (cs != c->st) {
+    k = cs == c->cs[0] ? 0 : 1;
+    cudaEventRecord(c->ea[k], cs);
+    cudaStreamWaitEvent(c->cst, c->ea[k], 0);
+    xs = c->cst;
+  }
+  cudaEventRecord(c->xev[c->nxev], xs);
+  const std::string e = c->net->exchange(c->p, sends, recvs, xs);
+  cudaEventRecord(c->xev[c->nxev + 1], xs);
   c->nxev += 2;
+  if (k >= 0) {
+    cudaEventRecord(c->eb[k], c->cst);
+    cudaStreamWaitEvent(cs, c->eb[k], 0);
+  }
   if (!e.empty()) return pfail(c, IRISMPC_GPU_ERR_DEVICE, e);
   return 0;
+}
+
+int step(irismpc_gpu_party* c, Phase ph, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
+         const std::vector<uint64_t>& counted, uint32_t rounds) {
+  return step_on(c, c->st, true, ph, sends, recvs, counted, rounds);
 }
 
 int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party** out, std::string* why) {
@@ -697,6 +728,11 @@ int party_init(const irismpc_gpu_config* cfg, uint32_t party, irismpc_gpu_party*
   cudaEventCreate(&c->ev[0]);
   cudaEventCreate(&c->ev[1]);
   for (auto& e : c->pev) cudaEventCreate(&e);
+  cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking);
+  for (auto& x : c->cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  for (auto& e : c->ea) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  for (auto& e : c->eb) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  for (auto& e : c->ej) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   // lambda_p for the Shamir parse (the same constants as the 3-party context)
   uint32_t lam[6] = {1, 2, 0xFFFFFFFFu, 0xFFFFFFFEu, 1, 0};  // 1+2X, -(1+2X), 1 (galois.hpp:124-128)
   set_lambda(lam);
@@ -720,10 +756,12 @@ void parse_party_rows(irismpc_gpu_party* c, PartyField& f, const uint8_t* pay, u
 
 // bit_extract_sum over summand rows X (own/prev components of summand p and
 // p-1 only, share_split) for instances `idx`, rows j >= K zero.  Gate g of the
-// call uses stream elements base[own|prev] + g W + w.  Results -> res_o/res_p rows.
+// call uses stream elements base[own|prev] + g W + w (w global).  Results ->
+// res_o/res_p rows [inst][W].  Rows are full width; every round runs once per
+// lane chunk (on the chunk's stream), so the chunks' transfers and kernels overlap.
 int bit_extract(irismpc_gpu_party* c, Phase ph, const uint64_t* Xo, const uint64_t* Xp, int K,
-                const std::vector<int>& idx, uint64_t n, uint64_t W, uint64_t base_o, uint64_t base_p,
-                uint64_t* res_o, uint64_t* res_p) {
+                const std::vector<int>& idx, const std::vector<Chunk>& chunks, uint64_t n, uint64_t W,
+                uint64_t base_o, uint64_t base_p, uint64_t* res_o, uint64_t* res_p) {
   const int p = c->p;
   const int ninst = (int)idx.size();
   int maxm = 0;
@@ -737,155 +775,174 @@ int bit_extract(irismpc_gpu_party* c, Phase ph, const uint64_t* Xo, const uint64
     if (comp == 0) return k == p ? XR(0, j) : nullptr;
     return k == prev_of(p) ? XR(1, j) : nullptr;
   };
+  auto off = [](const uint64_t* r, uint64_t w0) -> const uint64_t* { return r ? r + w0 : nullptr; };
   int total_fa = 0;
   for (int m : idx) total_fa += m;
+  const int maxg = std::max(total_fa, ninst);
   if (!c->carry.ensure(2ull * total_fa * W * 8 + 16) || !c->chain.ensure(2ull * ninst * W * 8 + 16) ||
-      !c->zbuf.ensure((uint64_t)std::max(total_fa, ninst) * W * 8 + 16) ||
-      !c->zrecv.ensure((uint64_t)std::max(total_fa, ninst) * W * 8 + 16))
+      !c->zbuf.ensure((uint64_t)maxg * W * 8 + 16) || !c->zrecv.ensure((uint64_t)maxg * W * 8 + 16))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (bit extract)");
   uint64_t* carry = c->carry.as<uint64_t>();  // [comp][fa gate][W]
   uint64_t* chain = c->chain.as<uint64_t>();  // [comp][inst][W]
-  uint64_t* zo = c->zbuf.as<uint64_t>();
-  uint64_t* zp = c->zrecv.as<uint64_t>();
   auto carry_row = [&](int comp, int g) { return carry + ((uint64_t)comp * total_fa + g) * W; };
   auto chain_row = [&](int comp, int k) { return chain + ((uint64_t)comp * ninst + k) * W; };
   std::vector<int> fa0(ninst);
-  const uint64_t wbl = cdiv(W, 8);
-  const uint64_t row_bytes = cdiv(n, 8);
-  uint64_t g = 0;
-  // ---- FA layer: one round, gates in instance order then j
   {
-    GateBatch B{};
     int gi = 0;
     for (int k = 0; k < ninst; ++k) {
       fa0[k] = gi;
+      gi += idx[k];
+    }
+  }
+  // per chunk: a contiguous z area [gates][words] at maxg * w0
+  auto zarea = [&](uint64_t* z, const Chunk& ch) { return z + (uint64_t)maxg * ch.w0; };
+  uint64_t g = 0;
+  // ---- FA layer: one round, gates in instance order then j
+  for (const Chunk& ch : chunks) {
+    GateBatch B{};
+    uint64_t* zo = zarea(c->zbuf.as<uint64_t>(), ch);
+    uint64_t* zp = zarea(c->zrecv.as<uint64_t>(), ch);
+    int gi = 0;
+    for (int k = 0; k < ninst; ++k)
       for (int j = 0; j < idx[k]; ++j, ++gi) {
         GateDesc& d = B.g[gi];
         // t1 = a0 ^ a2, t2 = a1 ^ a2
-        d.xo[0] = A(0, 0, j); d.xo[1] = A(2, 0, j);
-        d.xp[0] = A(0, 1, j); d.xp[1] = A(2, 1, j);
-        d.yo[0] = A(1, 0, j); d.yo[1] = A(2, 0, j);
-        d.yp[0] = A(1, 1, j); d.yp[1] = A(2, 1, j);
-        d.zo = zo + (uint64_t)gi * W;
-        d.eo = base_o + (g + gi) * W;
-        d.ep = base_p + (g + gi) * W;
-        d.words = W;
-        d.lanes = n;
+        d.xo[0] = off(A(0, 0, j), ch.w0); d.xo[1] = off(A(2, 0, j), ch.w0);
+        d.xp[0] = off(A(0, 1, j), ch.w0); d.xp[1] = off(A(2, 1, j), ch.w0);
+        d.yo[0] = off(A(1, 0, j), ch.w0); d.yo[1] = off(A(2, 0, j), ch.w0);
+        d.yp[0] = off(A(1, 1, j), ch.w0); d.yp[1] = off(A(2, 1, j), ch.w0);
+        d.zo = zo + (uint64_t)gi * ch.words;
+        d.eo = base_o + (g + gi) * W + ch.w0;
+        d.ep = base_p + (g + gi) * W + ch.w0;
+        d.words = ch.words;
+        d.lanes = ch.lanes;
       }
-    }
     B.ngates = (uint32_t)gi;
-    B.wblocks_per_gate = wbl;
-    k_pty_and<<<nblk(rup((uint64_t)gi * wbl, 32)), kThreads, 0, c->st>>>(B, c->own, c->prev);
+    B.wblocks_per_gate = cdiv(ch.words, 8);
+    k_pty_and<<<nblk(rup((uint64_t)gi * B.wblocks_per_gate, 32)), kThreads, 0, ch.st>>>(B, c->own, c->prev);
     PCK(c, cudaGetLastError());
-    int rc = step(c, ph, {{next_of(p), zo, (size_t)gi * W * 8}}, {{prev_of(p), zp, (size_t)gi * W * 8}},
-                  {(uint64_t)gi * row_bytes}, 1);
+    int rc = step_on(c, ch.st, ch.idx == 0, ph, {{next_of(p), zo, (size_t)gi * ch.words * 8}},
+                     {{prev_of(p), zp, (size_t)gi * ch.words * 8}}, {(uint64_t)gi * cdiv(ch.lanes, 8)}, 1);
     if (rc) return rc;
     // carry = z ^ a2
     XorBatch ops{};
-    ops.words = W;
+    ops.words = ch.words;
     for (int q = 0; q < gi; ++q) {
       int k = 0;
       while (k + 1 < ninst && fa0[k + 1] <= q) ++k;
       const int j = q - fa0[k];
-      ops.op[ops.nops++] = {carry_row(0, q), zo + (uint64_t)q * W, A(2, 0, j)};
-      ops.op[ops.nops++] = {carry_row(1, q), zp + (uint64_t)q * W, A(2, 1, j)};
+      ops.op[ops.nops++] = {carry_row(0, q) + ch.w0, zo + (uint64_t)q * ch.words, off(A(2, 0, j), ch.w0)};
+      ops.op[ops.nops++] = {carry_row(1, q) + ch.w0, zp + (uint64_t)q * ch.words, off(A(2, 1, j), ch.w0)};
     }
-    k_pty_xor<<<nblk((uint64_t)ops.nops * W), kThreads, 0, c->st>>>(ops);
-    g += gi;
+    k_pty_xor<<<nblk((uint64_t)ops.nops * ch.words), kThreads, 0, ch.st>>>(ops);
   }
+  g += total_fa;
   // ---- ripple chain: round t, gates in instance order (circuits.hpp:263-288)
   for (int t = 1; t + 1 <= maxm; ++t) {
-    GateBatch B{};
     std::vector<int> which;
-    for (int k = 0; k < ninst; ++k) {
-      if (t + 1 > idx[k]) continue;
-      const int gi = (int)which.size();
-      GateDesc& d = B.g[gi];
-      const int cg = fa0[k] + (t - 1);  // carry_{t-1}
-      if (t == 1) {
-        d.xo[0] = XR(0, t); d.xp[0] = XR(1, t);  // s_1 (own comp = X row: exactly one summand per component)
-        d.yo[0] = carry_row(0, cg); d.yp[0] = carry_row(1, cg);
-      } else {
-        d.xo[0] = XR(0, t); d.xo[1] = chain_row(0, k);
-        d.xp[0] = XR(1, t); d.xp[1] = chain_row(1, k);
-        d.yo[0] = carry_row(0, cg); d.yo[1] = chain_row(0, k);
-        d.yp[0] = carry_row(1, cg); d.yp[1] = chain_row(1, k);
-      }
-      d.zo = zo + (uint64_t)gi * W;
-      d.eo = base_o + (g + gi) * W;
-      d.ep = base_p + (g + gi) * W;
-      d.words = W;
-      d.lanes = n;
-      which.push_back(k);
-    }
+    for (int k = 0; k < ninst; ++k)
+      if (t + 1 <= idx[k]) which.push_back(k);
     const int gn = (int)which.size();
-    B.ngates = (uint32_t)gn;
-    B.wblocks_per_gate = wbl;
-    k_pty_and<<<nblk(rup((uint64_t)gn * wbl, 32)), kThreads, 0, c->st>>>(B, c->own, c->prev);
-    PCK(c, cudaGetLastError());
-    int rc = step(c, ph, {{next_of(p), zo, (size_t)gn * W * 8}}, {{prev_of(p), zp, (size_t)gn * W * 8}},
-                  {(uint64_t)gn * row_bytes}, 1);
-    if (rc) return rc;
-    XorBatch ops{};
-    ops.words = W;
-    for (int q = 0; q < gn; ++q) {
-      const int k = which[q];
-      ops.op[ops.nops++] = {chain_row(0, k), zo + (uint64_t)q * W, t == 1 ? nullptr : chain_row(0, k)};
-      ops.op[ops.nops++] = {chain_row(1, k), zp + (uint64_t)q * W, t == 1 ? nullptr : chain_row(1, k)};
+    for (const Chunk& ch : chunks) {
+      GateBatch B{};
+      uint64_t* zo = zarea(c->zbuf.as<uint64_t>(), ch);
+      uint64_t* zp = zarea(c->zrecv.as<uint64_t>(), ch);
+      for (int gi = 0; gi < gn; ++gi) {
+        const int k = which[gi];
+        GateDesc& d = B.g[gi];
+        const int cg = fa0[k] + (t - 1);  // carry_{t-1}
+        if (t == 1) {
+          d.xo[0] = off(XR(0, t), ch.w0); d.xp[0] = off(XR(1, t), ch.w0);  // s_1 (own comp = X row)
+          d.yo[0] = carry_row(0, cg) + ch.w0; d.yp[0] = carry_row(1, cg) + ch.w0;
+        } else {
+          d.xo[0] = off(XR(0, t), ch.w0); d.xo[1] = chain_row(0, k) + ch.w0;
+          d.xp[0] = off(XR(1, t), ch.w0); d.xp[1] = chain_row(1, k) + ch.w0;
+          d.yo[0] = carry_row(0, cg) + ch.w0; d.yo[1] = chain_row(0, k) + ch.w0;
+          d.yp[0] = carry_row(1, cg) + ch.w0; d.yp[1] = chain_row(1, k) + ch.w0;
+        }
+        d.zo = zo + (uint64_t)gi * ch.words;
+        d.eo = base_o + (g + gi) * W + ch.w0;
+        d.ep = base_p + (g + gi) * W + ch.w0;
+        d.words = ch.words;
+        d.lanes = ch.lanes;
+      }
+      B.ngates = (uint32_t)gn;
+      B.wblocks_per_gate = cdiv(ch.words, 8);
+      k_pty_and<<<nblk(rup((uint64_t)gn * B.wblocks_per_gate, 32)), kThreads, 0, ch.st>>>(B, c->own, c->prev);
+      PCK(c, cudaGetLastError());
+      int rc = step_on(c, ch.st, ch.idx == 0, ph, {{next_of(p), zo, (size_t)gn * ch.words * 8}},
+                       {{prev_of(p), zp, (size_t)gn * ch.words * 8}}, {(uint64_t)gn * cdiv(ch.lanes, 8)}, 1);
+      if (rc) return rc;
+      XorBatch ops{};
+      ops.words = ch.words;
+      for (int q = 0; q < gn; ++q) {
+        const int k = which[q];
+        ops.op[ops.nops++] = {chain_row(0, k) + ch.w0, zo + (uint64_t)q * ch.words,
+                              t == 1 ? nullptr : chain_row(0, k) + ch.w0};
+        ops.op[ops.nops++] = {chain_row(1, k) + ch.w0, zp + (uint64_t)q * ch.words,
+                              t == 1 ? nullptr : chain_row(1, k) + ch.w0};
+      }
+      k_pty_xor<<<nblk((uint64_t)ops.nops * ch.words), kThreads, 0, ch.st>>>(ops);
     }
-    k_pty_xor<<<nblk((uint64_t)ops.nops * W), kThreads, 0, c->st>>>(ops);
     g += gn;
   }
   // ---- result_k = s_m ^ carry_{m-1} ^ chain (m >= 2): two passes (the second XORs in place)
-  {
+  for (const Chunk& ch : chunks) {
     XorBatch first{}, second{};
-    first.words = second.words = W;
+    first.words = second.words = ch.words;
     for (int k = 0; k < ninst; ++k) {
       const int m = idx[k];
       for (int comp = 0; comp < 2; ++comp) {
-        uint64_t* dst = (comp == 0 ? res_o : res_p) + (uint64_t)k * W;
-        first.op[first.nops++] = {dst, carry_row(comp, fa0[k] + m - 1), m >= 2 ? chain_row(comp, k) : nullptr};
-        if (const uint64_t* sm = XR(comp, m)) second.op[second.nops++] = {dst, dst, sm};
+        uint64_t* dst = (comp == 0 ? res_o : res_p) + (uint64_t)k * W + ch.w0;
+        first.op[first.nops++] = {dst, carry_row(comp, fa0[k] + m - 1) + ch.w0,
+                                  m >= 2 ? chain_row(comp, k) + ch.w0 : nullptr};
+        if (const uint64_t* sm = XR(comp, m)) second.op[second.nops++] = {dst, dst, sm + ch.w0};
       }
     }
-    k_pty_xor<<<nblk((uint64_t)first.nops * W), kThreads, 0, c->st>>>(first);
-    if (second.nops) k_pty_xor<<<nblk((uint64_t)second.nops * W), kThreads, 0, c->st>>>(second);
+    k_pty_xor<<<nblk((uint64_t)first.nops * ch.words), kThreads, 0, ch.st>>>(first);
+    if (second.nops) k_pty_xor<<<nblk((uint64_t)second.nops * ch.words), kThreads, 0, ch.st>>>(second);
   }
   PCK(c, cudaGetLastError());
   return 0;
 }
 
-// bit_inject<Wd> of bit rows (bo, bp) -> out own/prev u16 components
-int bit_inject(irismpc_gpu_party* c, const uint64_t* bo, const uint64_t* bp, uint64_t n, int Wd, uint64_t e1,
-               uint64_t e3, uint16_t* out_o, uint16_t* out_p) {
+// bit_inject<Wd> of bit rows (bo, bp) -> out own/prev u16 components; per
+// lane chunk, the 3-OT's two rounds (P1 -> P2 and P3 -> P2, then P2 -> P3)
+int bit_inject(irismpc_gpu_party* c, const uint64_t* bo, const uint64_t* bp, const std::vector<Chunk>& chunks,
+               uint64_t n, int Wd, uint64_t e1, uint64_t e3, uint16_t* out_o, uint16_t* out_p) {
   const int p = c->p;
   const uint32_t mask = (1u << Wd) - 1;
   const size_t eb = 2;  // Ring<15>, Ring<16>: 2-byte elements
-  if (!c->msg.ensure(2 * n * eb + 16) || !c->msg2.ensure(2 * n * eb + 16))
+  if (!c->msg.ensure(2 * n * eb + 16) || !c->msg2.ensure(2 * n * eb + 16) || !c->c2buf.ensure(n * eb + 16))
     return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (inject)");
-  uint16_t* m1 = c->msg.as<uint16_t>();
-  uint16_t* m2 = c->msg2.as<uint16_t>();
   int rc = 0;
-  if (p == 0) {  // P1: sender
-    k_pty_inject_send<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(0, bo, bp, n, mask, c->own, c->prev, e1, e3,
-                                                                          out_o, out_p, m1);
-    rc = step(c, kOt, {{1, m1, 2 * n * eb}}, {}, {}, 1);
-    if (!rc) rc = step(c, kOt, {}, {}, {}, 1);  // c_2 forwarding stage, party 1 idle
-  } else if (p == 2) {  // P3: helper
-    k_pty_inject_send<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(2, bo, bp, n, mask, c->own, c->prev, e1, e3,
-                                                                          out_o, out_p, m1);
-    rc = step(c, kOt, {{1, m1, n * eb}}, {}, {}, 1);
-    if (!rc) rc = step(c, kOt, {}, {{1, out_p, n * eb}}, {}, 1);  // c_2 from P2 -> prev component
-  } else {  // P2: receiver
-    rc = step(c, kOt, {}, {{0, m1, 2 * n * eb}, {2, m2, n * eb}}, {}, 1);
+  for (const Chunk& ch : chunks) {
+    const uint64_t L = ch.lane0, m = ch.lanes;
+    const bool first = ch.idx == 0;
+    const uint64_t* cbo = bo + ch.w0;
+    const uint64_t* cbp = bp + ch.w0;
+    uint16_t* m1 = c->msg.as<uint16_t>() + 2 * L;
+    uint16_t* m2 = c->msg2.as<uint16_t>() + L;
+    const unsigned gr = nblk(rup(cdiv(m, 8), 32));
+    if (p == 0) {  // P1: sender
+      k_pty_inject_send<<<gr, kThreads, 0, ch.st>>>(0, cbo, cbp, m, mask, c->own, c->prev, e1 + L, e3 + 3 * L,
+                                                     out_o + L, out_p + L, m1);
+      rc = step_on(c, ch.st, first, kOt, {{1, m1, 2 * m * eb}}, {}, {}, 1);
+      if (!rc) rc = step_on(c, ch.st, first, kOt, {}, {}, {}, 1);  // c_2 forwarding stage, party 1 idle
+    } else if (p == 2) {  // P3: helper
+      k_pty_inject_send<<<gr, kThreads, 0, ch.st>>>(2, cbo, cbp, m, mask, c->own, c->prev, e1 + L, e3 + 3 * L,
+                                                     out_o + L, out_p + L, m1);
+      rc = step_on(c, ch.st, first, kOt, {{1, m1, m * eb}}, {}, {}, 1);
+      if (!rc) rc = step_on(c, ch.st, first, kOt, {}, {{1, out_p + L, m * eb}}, {}, 1);  // c_2 -> prev component
+    } else {  // P2: receiver
+      rc = step_on(c, ch.st, first, kOt, {}, {{0, m1, 2 * m * eb}, {2, m2, m * eb}}, {}, 1);
+      if (rc) return rc;
+      uint16_t* c2 = c->c2buf.as<uint16_t>() + L;
+      k_pty_inject_p2<<<gr, kThreads, 0, ch.st>>>(cbo, m, mask, c->prev, e1 + L, m1, m2, out_o + L, out_p + L, c2);
+      rc = step_on(c, ch.st, first, kOt, {{2, c2, m * eb}}, {}, {}, 1);
+    }
     if (rc) return rc;
-    if (!c->zbuf.ensure(n * eb + 16)) return pfail(c, IRISMPC_GPU_ERR_DEVICE, "oom (inject)");
-    uint16_t* c2 = c->zbuf.as<uint16_t>();
-    k_pty_inject_p2<<<nblk(rup(cdiv(n, 8), 32)), kThreads, 0, c->st>>>(bo, n, mask, c->prev, e1, m1, m2, out_o, out_p,
-                                                                        c2);
-    rc = step(c, kOt, {{2, c2, n * eb}}, {}, {}, 1);
   }
-  if (rc) return rc;
   PCK(c, cudaGetLastError());
   return 0;
 }
@@ -1075,47 +1132,83 @@ int party_query(irismpc_gpu_party* c, const uint8_t* hq, size_t qlen, uint32_t p
   // gates and the injects (seed 1: 2n, seed 3: 6n), then the MSB gates
   const uint64_t lift_draws[3] = {2 * n, 0, 6 * n};
   uint64_t msb_o = c->pos[0] + n + nml, msb_p = c->pos[1] + n + nml;
+  // ---- lane chunks of the comparison phase (lanes are independent until the OR tree)
+  static const int env_chunks = [] {
+    const char* e = std::getenv("IRISMPC_PARTY_CHUNKS");  // test hook: force 1 or 2
+    return e ? std::atoi(e) : 0;
+  }();
+  const int nch = env_chunks ? std::max(1, std::min(2, env_chunks)) : (W >= 4096 ? 2 : 1);
+  std::vector<Chunk> chunks;
+  if (nch == 1 || W < 2) {
+    chunks.push_back({0, 0, W, 0, n, st});
+  } else {
+    const uint64_t w1 = W / 2;
+    chunks.push_back({0, 0, w1, 0, 64 * w1, c->cs[0]});
+    chunks.push_back({1, w1, W - w1, 64 * w1, n - 64 * w1, c->cs[1]});
+    PCK(c, cudaEventRecord(c->ej[0], st));
+    for (const Chunk& ch : chunks) PCK(c, cudaStreamWaitEvent(ch.st, c->ej[0], 0));
+  }
+  const int KC = vw.kc;
   if (V == kMpcLift) {
     // ---- lift<16,16>
-    if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * 16 * W * 8, st));  // odd trailing half-word
-    k_pty_split<uint32_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(ml_o, ml_p, n, W, rows);
-    rc = bit_extract(c, kLift, rows, rows + 16 * W, 16, {16, 17}, n, W, c->pos[0] + 2 * n, c->pos[1] + 2 * n, b_o, b_p);
-    if (rc) return rc;
     uint16_t* i17 = c->inj.as<uint16_t>();  // [comp][n+8]
     uint16_t* i16 = i17 + 2 * (n + 8);
+    for (const Chunk& ch : chunks)
+      k_pty_split<uint32_t, 16><<<nblk(4 * ch.words), kThreads, 0, ch.st>>>(ml_o + ch.lane0, ml_p + ch.lane0, ch.lanes,
+                                                                           W, rows + ch.w0, 2 * ch.words);
+    rc = bit_extract(c, kLift, rows, rows + 16 * W, 16, {16, 17}, chunks, n, W, c->pos[0] + 2 * n, c->pos[1] + 2 * n,
+                     b_o, b_p);
+    if (rc) return rc;
     // seed_1 / seed_3 element bases (own/prev stream positions by role)
     const uint64_t pos1 = p == 0 ? c->pos[0] : (p == 1 ? c->pos[1] : 0);
     const uint64_t pos3 = p == 0 ? c->pos[1] : (p == 2 ? c->pos[0] : 0);
-    rc = bit_inject(c, b_o + W, b_p + W, n, 15, pos1 + 2 * n + 64 * W, pos3 + 2 * n + 64 * W, i17, i17 + n + 8);
+    rc = bit_inject(c, b_o + W, b_p + W, chunks, n, 15, pos1 + 2 * n + 64 * W, pos3 + 2 * n + 64 * W, i17,
+                    i17 + n + 8);
     if (rc) return rc;
-    rc = bit_inject(c, b_o, b_p, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
+    rc = bit_inject(c, b_o, b_p, chunks, n, 16, pos1 + 3 * n + 64 * W, pos3 + 5 * n + 64 * W, i16, i16 + n + 8);
     if (rc) return rc;
-    k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_o, hd_o, i17, i16, n, c->cfg.a, c->cfg.b, ml32, diff);
-    k_pty_diff<<<nblk(n), kThreads, 0, st>>>(ml_p, hd_p, i17 + n + 8, i16 + n + 8, n, c->cfg.a, c->cfg.b,
-                                             ml32 + n + 8, diff + n + 8);
+    for (const Chunk& ch : chunks) {
+      const uint64_t L = ch.lane0;
+      k_pty_diff<<<nblk(ch.lanes), kThreads, 0, ch.st>>>(ml_o + L, hd_o + L, i17 + L, i16 + L, ch.lanes, c->cfg.a,
+                                                         c->cfg.b, ml32 + L, diff + L);
+      k_pty_diff<<<nblk(ch.lanes), kThreads, 0, ch.st>>>(ml_p + L, hd_p + L, i17 + n + 8 + L, i16 + n + 8 + L,
+                                                         ch.lanes, c->cfg.a, c->cfg.b, ml32 + n + 8 + L,
+                                                         diff + n + 8 + L);
+    }
     msb_o += 64 * W + lift_draws[ko];
     msb_p += 64 * W + lift_draws[kp];
   } else {
     const int plain = V == kPlainMask;
     const double coef = 1.0 - 2.0 * c->cfg.match_ratio;
     const uint16_t* pub = reinterpret_cast<const uint16_t*>(dm);  // plain-mask: the public popcounts
-    k_pty_cmp<<<nblk(n), kThreads, 0, st>>>(plain, hd_o, ml_o, pub, n, c->cfg.a, c->cfg.b, coef, p == 0, ml32, diff);
-    k_pty_cmp<<<nblk(n), kThreads, 0, st>>>(plain, hd_p, ml_p, pub, n, c->cfg.a, c->cfg.b, coef, p == 1,
-                                            ml32 + n + 8, diff + n + 8);
+    for (const Chunk& ch : chunks) {
+      const uint64_t L = ch.lane0;
+      k_pty_cmp<<<nblk(ch.lanes), kThreads, 0, ch.st>>>(plain, hd_o + L, ml_o + L, pub + L, ch.lanes, c->cfg.a,
+                                                        c->cfg.b, coef, p == 0, ml32 + L, diff + L);
+      k_pty_cmp<<<nblk(ch.lanes), kThreads, 0, ch.st>>>(plain, hd_p + L, ml_p + L, pub + L, ch.lanes, c->cfg.a,
+                                                        c->cfg.b, coef, p == 1, ml32 + n + 8 + L, diff + n + 8 + L);
+    }
   }
   PCK(c, cudaGetLastError());
-  PCK(c, cudaEventRecord(c->pev[2], st));
+  PCK(c, cudaEventRecord(c->pev[2], chunks[0].st));
   // ---- msb<KC>
-  const int KC = vw.kc;
-  if (W * 2 > cdiv(n, 32)) PCK(c, cudaMemsetAsync(rows, 0, 2ull * KC * W * 8, st));
-  if (KC == 32)
-    k_pty_split<uint32_t, 32><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
-  else
-    k_pty_split<uint32_t, 16><<<nblk(2 * cdiv(n, 32)), kThreads, 0, st>>>(diff, diff + n + 8, n, W, rows);
+  for (const Chunk& ch : chunks) {
+    if (KC == 32)
+      k_pty_split<uint32_t, 32><<<nblk(4 * ch.words), kThreads, 0, ch.st>>>(
+          diff + ch.lane0, diff + n + 8 + ch.lane0, ch.lanes, W, rows + ch.w0, 2 * ch.words);
+    else
+      k_pty_split<uint32_t, 16><<<nblk(4 * ch.words), kThreads, 0, ch.st>>>(
+          diff + ch.lane0, diff + n + 8 + ch.lane0, ch.lanes, W, rows + ch.w0, 2 * ch.words);
+  }
   uint64_t* mb_o = b_o + 2 * W;  // msb bit rows (own, prev) in the second half of `bits`
   uint64_t* mb_p = b_o + 3 * W;
-  rc = bit_extract(c, kMsb, rows, rows + (uint64_t)KC * W, KC, {KC - 1}, n, W, msb_o, msb_p, mb_o, mb_p);
+  rc = bit_extract(c, kMsb, rows, rows + (uint64_t)KC * W, KC, {KC - 1}, chunks, n, W, msb_o, msb_p, mb_o, mb_p);
   if (rc) return rc;
+  if (chunks.size() > 1)
+    for (size_t k = 0; k < chunks.size(); ++k) {
+      PCK(c, cudaEventRecord(c->ej[1 + k], chunks[k].st));
+      PCK(c, cudaStreamWaitEvent(st, c->ej[1 + k], 0));
+    }
   PCK(c, cudaEventRecord(c->pev[3], st));
   // ---- taps (parity tests)
   c->tap_n = n;
@@ -1354,7 +1447,7 @@ void irismpc_gpu_party_destroy(irismpc_gpu_party* c) {
   DBuf* bufs[] = {&c->qpay, &c->dots, &c->rs, &c->rows, &c->carry, &c->chain, &c->zbuf, &c->zrecv, &c->inj,
                   &c->msg, &c->msg2, &c->ml32, &c->diff, &c->bits, &c->pairs, &c->groups, &c->levels, &c->pool[0],
                   &c->pool[1], &c->tz[0], &c->tz[1], &c->rowoff, &c->open_buf[0], &c->open_buf[1], &c->open_buf[2],
-                  &c->xsend, &c->xrecv};
+                  &c->xsend, &c->xrecv, &c->c2buf};
   for (DBuf* b : bufs) b->release();
   for (auto& f : c->fld) {
     f.db.release();
@@ -1367,6 +1460,15 @@ void irismpc_gpu_party_destroy(irismpc_gpu_party* c) {
   cudaEventDestroy(c->ev[1]);
   for (auto& e : c->pev) cudaEventDestroy(e);
   for (auto& e : c->xev) cudaEventDestroy(e);
+  for (auto& e : c->ea) cudaEventDestroy(e);
+  for (auto& e : c->eb) cudaEventDestroy(e);
+  for (auto& e : c->ej) cudaEventDestroy(e);
+  cudaStreamSynchronize(c->cst);
+  for (auto& x : c->cs) {
+    cudaStreamSynchronize(x);
+    cudaStreamDestroy(x);
+  }
+  cudaStreamDestroy(c->cst);
   cudaStreamDestroy(c->st);
   delete c;
 }

@@ -354,3 +354,38 @@ def test_threshold_job_splits(chunk_lanes, thr_lanes):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("be,var", [(O.SHAMIR, P.MPC_LIFT), (O.REPLICATED, P.CONST_LIFT), (O.SHAMIR, P.PLAIN_MASK)])
+def test_persistent_session_varying_query_shapes(be, var):
+    """One context, queries of changing shape (persons 3 -> membership -> 9 -> 1 -> 5): buffers
+    are resized between calls and the PRF streams keep advancing like a CLI PartyCtx; every
+    query's row bits and person bits equal the oracle's started at the carried positions."""
+    l, s, r, seed = 256, 700, 5, 91
+    rng = O.Rng(seed)
+    dc, dm = O.records(rng, l, s, 0.9)
+    db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)), variant=var)
+    seeds = O.party_seeds(seed)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True, variant=var)
+    sess = P.Session(cfg, seeds=seeds)
+    sess.load_db(db, s)
+    pos = np.zeros(3, np.uint64)
+    for qi, (persons, memb) in enumerate([(3, False), (1, True), (9, False), (1, False), (5, False)]):
+        nq = 1 if memb else 2 * persons
+        qc, qm = O.records(rng, l, nq, 0.9)
+        qc[0], qm[0] = dc[(37 * qi) % s], dm[(37 * qi) % s]
+        q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 10 + qi)), variant=var)
+        rr = 1 if memb else r
+        ref = O.query(O.make_config(be, l, 0.375, rr, debug_rows=True, variant=var), seeds, db, s, q,
+                      persons, membership=memb, stream_start=pos)
+        if memb:
+            m = np.array([sess.membership(q, want_rows=True)], np.uint8)
+            n = s
+        else:
+            m = sess.batch_query(q, persons, want_rows=True)
+            n = P.lane_count(persons, s, r)
+        np.testing.assert_array_equal(m, ref.person_match, err_msg=f"query {qi}")
+        np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits, err_msg=f"query {qi}")
+        np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos, err_msg=f"query {qi}")
+        assert m[0] == 1
+        pos = ref.stream_pos

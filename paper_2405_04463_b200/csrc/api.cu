@@ -153,7 +153,7 @@ struct FieldPlanes {
 struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
-  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;
   int shamir = 0;
   int variant = kMpcLift;
   VariantWidths vw{16, 16, 32};
@@ -167,7 +167,7 @@ struct irismpc_gpu_ctx {
   // query scratch
   Buf q_pay[3];
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
-  Buf ml_rs, diff, gate, bits;
+  Buf ml_rs, diff, gate, bits, gate2, bits2;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
@@ -181,7 +181,7 @@ struct irismpc_gpu_ctx {
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
   std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
-  std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done / threshold done
+  std::vector<cudaEvent_t> evg, evt, evt3;  // chunk pipeline: GEMM done / threshold done (st2, st3)
 };
 
 namespace {
@@ -376,6 +376,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     return e && e[0] == '1';
   }();
   cudaStream_t st = c->st, st2 = serial ? c->st : c->st2;
+  // two threshold streams: a chunk's columns split into two jobs, so one job's
+  // latency-bound bit-sliced kernels overlap the other's ChaCha kernels
+  static const int thr_streams = [] {
+    const char* e = std::getenv("IRISMPC_THR_STREAMS");
+    return e ? std::max(1, std::min(2, std::atoi(e))) : 1;
+  }();
+  const bool two = thr_streams == 2 && !serial;
+  cudaStream_t st3 = two ? c->st3 : st2;
   uint64_t launches = 0;
 
   CK(c, cudaEventRecord(c->ev[0], st));
@@ -560,7 +568,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         sg.slot = (int64_t)col_fill[col];
         col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
-      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
+      uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
+      if (two && ncols >= 2) per_job = std::min<uint64_t>(per_job, ceil_div(ncols, 2));
       for (uint64_t a = 0; a < ncols; a += per_job)
         add_job(i * ncols + a, std::min<uint64_t>(per_job, ncols - a), false, i);
       cstride = std::max<uint64_t>(cstride, ncols * nr);
@@ -589,7 +598,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     if ((nchunks && c->dots.ensure(2 * dots_half)) ||
         c->ml_rs.ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
         c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) || c->gate.ensure(max_g * sizeof(uint64_t) + 16) ||
-        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))
+        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16) ||
+        (two && (c->gate2.ensure(max_g * sizeof(uint64_t) + 16) ||
+                 c->bits2.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
 
@@ -626,14 +637,16 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   uint64_t task_off = 0;
   // hd_base: [3][pstride] hd dots; ml_base: [nparty][pstride] ml dots / public popcounts
-  auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride) -> int {
+  auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride,
+                     int lane) -> int {
     ThrArgs t = ta;
     t.segs = c->segs.as<Seg>() + j.seg0;
     t.nsegs = (uint32_t)j.nseg;
     t.ntasks = j.ntasks;
     t.ngrp = j.ngrp;
     t.ngblk = j.ngblk;
-    t.bits = c->bits.as<uint32_t>();
+    t.bits = (lane ? c->bits2 : c->bits).as<uint32_t>();
+    t.gate = (lane ? c->gate2 : c->gate).as<uint64_t>();
     t.nbits = j.ntasks * 32;
     t.or_elem_base = ta.or_elem_base + task_off * 64;
     task_off += j.ntasks;
@@ -643,7 +656,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
-    launch_threshold(t, st2);
+    launch_threshold(t, lane ? st3 : st2);
     CK(c, cudaGetLastError());
     launches += V == kMpcLift ? 5 : 3;
     return 0;
@@ -656,7 +669,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     return 0;
   };
-  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1)) return IRISMPC_GPU_ERR_DEVICE;
+  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1) || ensure_events(c->evt3, nchunks + 1))
+    return IRISMPC_GPU_ERR_DEVICE;
   while (c->gev.size() < 2 * nchunks) {
     cudaEvent_t e;
     CK(c, cudaEventCreate(&e));
@@ -666,6 +680,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   // st2 starts once the prep on st (payload parse, pairs, memsets, uploads) is queued before it
   CK(c, cudaEventRecord(c->evg[nchunks], st));
   CK(c, cudaStreamWaitEvent(st2, c->evg[nchunks], 0));
+  if (two) CK(c, cudaStreamWaitEvent(st3, c->evg[nchunks], 0));
   CK(c, cudaEventRecord(c->ev[2], st2));
 
   // ---- DB lanes: GEMMs(i) on st || threshold(i-1) on st2
@@ -676,7 +691,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     const uint64_t nr = chunk_rows(i);
     uint8_t* dots = c->dots.as<uint8_t>() + (i % 2) * dots_half;
     uint8_t* dots_ml = dots + hd_half;
-    if (i >= 2) CK(c, cudaStreamWaitEvent(st, c->evt[i - 2], 0));  // buffer i%2 released
+    if (i >= 2) {  // buffer i%2 released
+      CK(c, cudaStreamWaitEvent(st, c->evt[i - 2], 0));
+      if (two) CK(c, cudaStreamWaitEvent(st, c->evt3[i - 2], 0));
+    }
     CK(c, cudaEventRecord(c->gev[2 * i], st));
     for (int fi = 0; fi < 2; ++fi) {
       FieldPlanes& f = c->fld[fi];
@@ -710,14 +728,23 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     CK(c, cudaEventRecord(c->evg[i], st));
     CK(c, cudaStreamWaitEvent(st2, c->evg[i], 0));
-    for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji) {
-      int rc2 = run_job(jobs[ji], dots, dots_ml, ncols * nr);
+    if (two) {
+      CK(c, cudaStreamWaitEvent(st3, c->evg[i], 0));
+      if (i >= 1) {  // the work buffers (ml_rs, diff) are chunk-relative: chunk i-1's jobs first
+        CK(c, cudaStreamWaitEvent(st2, c->evt3[i - 1], 0));
+        CK(c, cudaStreamWaitEvent(st3, c->evt[i - 1], 0));
+      }
+    }
+    for (int lane = 0; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji, lane ^= (two ? 1 : 0)) {
+      int rc2 = run_job(jobs[ji], dots, dots_ml, ncols * nr, lane);
       if (rc2) return rc2;
     }
     CK(c, cudaEventRecord(c->evt[i], st2));
+    if (two) CK(c, cudaEventRecord(c->evt3[i], st3));
   }
 
   // ---- pair lanes (shard 0): threshold into match words
+  if (two && nchunks) CK(c, cudaStreamWaitEvent(st2, c->evt3[nchunks - 1], 0));
   if (npairs) {
     const uint8_t* pd_hd = c->pair_dots.as<uint8_t>();
     const uint8_t* pd_ml = pd_hd + 3 * npairs * hb;
@@ -729,8 +756,12 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint8_t>() + (p * n + ncols * S) * mb, pd_ml + p * npairs * mb,
                               npairs * mb, cudaMemcpyDeviceToDevice, st2));
     }
-    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs);
+    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, 0);
     if (rc2) return rc2;
+  }
+  if (two) {  // the OR reads every job's partial slots (and the pair job reused the work buffers)
+    CK(c, cudaEventRecord(c->evt3[nchunks], st3));
+    CK(c, cudaStreamWaitEvent(st2, c->evt3[nchunks], 0));
   }
   CK(c, cudaEventRecord(c->ev[3], st2));
 
@@ -903,7 +934,8 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* e = std::getenv("IRISMPC_PRIO_SWAP"); e && e[0] == '1') std::swap(prio_lo, prio_hi);
   if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return IRISMPC_GPU_ERR_DEVICE;
   }
@@ -921,7 +953,7 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   cudaStreamSynchronize(c->st);
   Buf* bufs[] = {&c->q_pay[0], &c->q_pay[1], &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial,
                  &c->slot_begin, &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
-                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->gate2, &c->bits2};
   for (Buf* b : bufs) b->release();
   for (auto& f : c->fld) f.release();
   for (auto& t : c->tap_buf) t.release();
@@ -930,8 +962,11 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   for (auto& e : c->gev) cudaEventDestroy(e);
   for (auto& e : c->evg) cudaEventDestroy(e);
   for (auto& e : c->evt) cudaEventDestroy(e);
+  for (auto& e : c->evt3) cudaEventDestroy(e);
   cudaStreamSynchronize(c->st2);
+  cudaStreamSynchronize(c->st3);
   cudaStreamDestroy(c->st2);
+  cudaStreamDestroy(c->st3);
   cudaStreamDestroy(c->st);
   delete c;
 }

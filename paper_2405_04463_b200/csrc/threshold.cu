@@ -29,6 +29,7 @@
 //   k_inject          lane-major: bit_inject<15>, <16>, const-lifted into diff
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
 //                     match-bit shares, fused first MPC-OR level per warp
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"

@@ -35,6 +35,17 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// min blocks per SM for the latency-bound bit-sliced kernels: 4 x 128 threads
+// caps them at 128 registers (a few bytes of spill) for more resident warps;
+// measured best of 1 / 4 / 5 / 6 (lift 11.9 -> 8.5 ms, msb 15.1 -> 13.2 ms
+// per 10 serialized configs[1] queries)
+#ifndef MSB_LB
+#define MSB_LB 4
+#endif
+#ifndef LIFT_LB
+#define LIFT_LB 4
+#endif
+
 namespace irisgpu {
 
 namespace {
@@ -398,7 +409,7 @@ __device__ __forceinline__ void extract_bit(const ThrArgs& A, const Seg& sg, uin
 }  // namespace
 
 // warp -> 1024-lane task, thread -> 32 lanes
-__global__ void __launch_bounds__(128) k_lift(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ ThrArgs A) {
   const uint64_t task = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (task >= A.ntasks) return;
@@ -580,7 +591,7 @@ __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t 
 // warp -> 1024-lane task: msb<KC> of diff (circuits.hpp:300-306), outputs,
 // fused first OR level.  Gates: FA j -> nlift + j, chain t -> nlift + KC - 1 + (t - 1).
 template <int KC>
-__global__ void __launch_bounds__(128) k_msb(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(128, MSB_LB) k_msb(const __grid_constant__ ThrArgs A) {
   const uint64_t task = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (task >= A.ntasks) return;

@@ -366,34 +366,46 @@ __device__ __forceinline__ void extract_bit(const ThrArgs& A, const Seg& sg, uin
                                             const uint32_t (&R)[3][K], int fa0, int ch0, int chs, int chmax,
                                             uint32_t out[3]) {
   uint32_t carry[3] = {0, 0, 0}, chain[3] = {0, 0, 0};
+  // gate randomness one step ahead: the loads of step j + 1 are in flight while
+  // step j computes (the kernels are latency-bound on these L2 reads)
+  uint32_t fc_next[3] = {0, 0, 0}, ff_next[3];
+  gate_rand(A, sg, w64, half, fa0, ff_next);
 #pragma unroll
   for (int j = 0; j < M; ++j) {
+    uint32_t fc[3], ff[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      fc[c] = fc_next[c];
+      ff[c] = ff_next[c];
+    }
+    if (j + 1 < M) {
+      gate_rand(A, sg, w64, half, min(ch0 + chs * j, chmax), fc_next);  // chain gate of step j + 1
+      gate_rand(A, sg, w64, half, fa0 + j + 1, ff_next);
+    }
     uint32_t s[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) s[c] = j < K ? R[c][j] : 0u;
     if (j >= 1) {
-      uint32_t f[3], u[3], v[3], res[3];
-      gate_rand(A, sg, w64, half, min(ch0 + chs * (j - 1), chmax), f);
+      uint32_t u[3], v[3], res[3];
       if (j == 1) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) { u[c] = s[c]; v[c] = carry[c]; }
-        and3(u, v, f, res);
+        and3(u, v, fc, res);
 #pragma unroll
         for (int c = 0; c < 3; ++c) chain[c] = res[c];
       } else {
 #pragma unroll
         for (int c = 0; c < 3; ++c) { u[c] = s[c] ^ chain[c]; v[c] = carry[c] ^ chain[c]; }
-        and3(u, v, f, res);
+        and3(u, v, fc, res);
 #pragma unroll
         for (int c = 0; c < 3; ++c) chain[c] ^= res[c];
       }
     }
     {
-      uint32_t f[3], z[3];
-      gate_rand(A, sg, w64, half, fa0 + j, f);
+      uint32_t z[3];
       const uint32_t t1[3] = {s[0], 0u, s[2]};
       const uint32_t t2[3] = {0u, s[1], s[2]};
-      and3(t1, t2, f, z);
+      and3(t1, t2, ff, z);
       carry[0] = z[0];
       carry[1] = z[1];
       carry[2] = z[2] ^ s[2];

@@ -118,3 +118,26 @@ def test_bench_full(tmp_path, capsys):
     assert out.startswith("full query: backend=shamir-galois variant=mpc-lift s=3000 l=12800")
     d = json.load(open(js))
     assert d["s"] == 3000 and d["phase_bytes"]["dot"] == 4 * 3000 and d["rounds"]["msb"] == 31
+
+
+@pytest.mark.gpu
+def test_query_with_reference_config_json(tmp_path, capsys):
+    """`query --config` reads the reference's party config (share_dir, backend, l,
+    match_ratio, rotations; endpoints ignored) and answers a membership query."""
+    _gpu()
+    l, s, seed = 128, 25, 3
+    dc, dm = O.records(O.Rng(8), l, s, 0.9)
+    db = tmp_path / "db.irmp"
+    P.write_iris_db(db, dc, dm, l)
+    out = tmp_path / "shares"
+    assert cli.main(["share", "--db", str(db), "--backend", "replicated", "--variant", "mpc-lift",
+                     "--out-dir", str(out), "--seed", str(seed)]) == 0
+    cfg = tmp_path / "p1.json"
+    cfg.write_text(json.dumps({"party": 1, "endpoints": ["127.0.0.1:1", "127.0.0.1:2", "127.0.0.1:3"],
+                               "backend": "replicated", "l": l, "match_ratio": 0.375, "rotations": 1,
+                               "share_dir": str(out)}))
+    q = tmp_path / "q.irmp"
+    P.write_iris_db(q, dc[11:12], dm[11:12], l)
+    capsys.readouterr()
+    assert cli.main(["query", "--config", str(cfg), "--query", str(q)]) == 0
+    assert capsys.readouterr().out.splitlines()[0] == "variant mpc-lift: true"

@@ -186,3 +186,51 @@ def test_load_db_files_streams_multiple_chunks(tmp_path):
     np.testing.assert_array_equal(ma, mb)
     np.testing.assert_array_equal(a.row_bits, b.row_bits)
     assert ma[0] == 1
+
+
+@pytest.mark.gpu
+def test_load_db_files_inconsistent_replicated_shares(tmp_path):
+    """load_db_files runs the replicated cross-check (party p's prev == party p-1's own)."""
+    _gpu()
+    e = [x for x in GOLD["shares"] if x["backend"] == 0][0]
+    paths = [tmp_path / n for n in e["files"]]
+    for n, p in zip(e["files"], paths):
+        open(p, "wb").write(open(_f(n), "rb").read())
+    b = bytearray(open(paths[1], "rb").read())
+    b[24 + 2] ^= 1  # party 2's first `prev` entry no longer equals party 1's `own`
+    open(paths[1], "wb").write(bytes(b))
+    seeds = P.read_seed_files([_f(n) for n in e["seed_files"]])
+    sess = P.Session(P.EngineConfig(backend=P.REPLICATED, l=GOLD["l"], rotations=1), seeds=seeds)
+    with pytest.raises(P.InconsistentShareError):
+        sess.load_db_files(paths)
+    # a share file of another variant is a config mismatch (irismpc_cli.cpp:211-215)
+    other = [x for x in GOLD["shares"] if x["backend"] == 1 and x["variant"] == 0][0]
+    sess2 = P.Session(P.EngineConfig(backend=P.SHAMIR, l=GOLD["l"], rotations=1), seeds=seeds)
+    with pytest.raises(P.ConfigError):
+        sess2.load_db_files([_f(n) for n in other["files"]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("be", [P.SHAMIR, P.REPLICATED])
+def test_plain_mask_unaligned_records(be, tmp_path):
+    """plain-mask records of l = 8 are not 16-byte aligned (code 16/32 B + 1 mask byte):
+    written to files, loaded, and queried against the oracle."""
+    _gpu()
+    l, s, seed = 8, 57, 19
+    dc, dm = O.records(O.Rng(seed), l, s, 0.9)
+    db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)), variant=P.PLAIN_MASK)
+    assert (s * O.record_bytes(be, l, P.PLAIN_MASK)) % 16 != 0
+    paths = [tmp_path / f"p{p}.irs" for p in (1, 2, 3)]
+    for p in range(3):
+        P.write_share_file(paths[p], be, P.PLAIN_MASK, p + 1, l, s, db[p])
+    seeds = O.party_seeds(seed)
+    cfg = P.EngineConfig(backend=be, l=l, rotations=1, debug_rows=True, variant=P.PLAIN_MASK)
+    sess = P.Session(cfg, seeds=seeds)
+    sess.load_db_files(paths)
+    qc, qm = dc[5:6].copy(), dm[5:6].copy()
+    q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)), variant=P.PLAIN_MASK)
+    m = sess.membership(q, want_rows=True)
+    ref = O.query(O.make_config(be, l, 0.375, 1, debug_rows=True, variant=P.PLAIN_MASK), seeds, db, s, q, 1,
+                  membership=True)
+    assert m == bool(ref.person_match[0])
+    np.testing.assert_array_equal(sess.row_bits[:s], ref.row_bits)

@@ -49,6 +49,17 @@ def ops_per_lane(backend: int, variant: int = 1) -> int:
 ALG_BYTES_PER_LANE = 12.75               # compare/reduce phase
 
 
+def prf_blocks_per_lane(variant: int = 1) -> float:
+    """ChaCha12 blocks per comparison lane of the reference-exact PRF layout
+    (DESIGN §4): reshare 1 u64 per seed per shared dot, bit_inject
+    4 u64 per inject (mpc-lift only), one u64 per seed per 64-lane word per AND
+    gate (lift 64 + msb 61 for mpc-lift; msb only otherwise)."""
+    reshare = 3 * (1 if variant == 0 else 2) / 8
+    inject = 1.0 if variant == 1 else 0.0
+    gates = {0: 29, 1: 125, 2: 61, 3: 61}[variant]
+    return reshare + inject + gates * 3 / 512
+
+
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -113,6 +124,17 @@ def load_peaks():
         d = json.load(open(p))
         return d, "measured"
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def chacha_peak():
+    """measured ChaCha12 keystream rate of this device (tools/chacha_peak.cu)"""
+    p = os.path.join(ROOT, "profiles", "chacha_peak.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))["chacha12_blocks_per_s_store"]
+        except Exception:
+            return None
+    return None
 
 
 def ncu_traffic():
@@ -183,6 +205,27 @@ def run_reference_arm(args):
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def compare_roofline(span_ms: float, lanes: int, variant: int, peaks: dict) -> dict:
+    """The compare/reduce phase (reshare -> lift -> MSB -> OR) against both of
+    its ceilings over the threshold stream's span: HBM at the SURVEY §8d
+    algorithmic 12.75 B/lane, and the ALU pipe as ChaCha12 blocks/s against the
+    measured keystream rate (profiles/chacha_peak.json).  The PRF layout is the
+    reference's (2.48 blocks/lane for mpc-lift), so the phase is ALU-bound."""
+    sec = max(span_ms, 1e-9) / 1e3
+    hbm = ALG_BYTES_PER_LANE * lanes / sec / 1e9
+    blocks = prf_blocks_per_lane(variant) * lanes
+    cp = chacha_peak()
+    out = {"bound": "alu", "kernels": "k_gate_keystream, k_reshare, k_lift, k_inject, k_msb",
+           "hbm": {"achieved": hbm, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": hbm / peaks["hbm_gbs"],
+                   "alg_bytes_per_lane": ALG_BYTES_PER_LANE},
+           "chacha": {"achieved": blocks / sec, "peak": cp, "unit": "ChaCha12 blocks/s",
+                      "frac": (blocks / sec / cp) if cp else None,
+                      "blocks_per_lane": prf_blocks_per_lane(variant)},
+           "span_ms": span_ms,
+           "note": "over the threshold stream span, which overlaps the GEMM"}
+    return out
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -336,9 +379,14 @@ def main_gpu(args):
                          "note": f"int8 ops = {opl}/lane; peak = {peak_note}"},
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),
-            "phase_ms": {"gemm": gemm_ms, "threshold": sess.last_stats.threshold_ms, "or": sess.last_stats.or_ms,
-                         "prep": sess.last_stats.prep_ms, "total": ms,
-                         "host_wall_per_step": host_s / args.steps * 1e3},
+            "roofline_compare": compare_roofline(sess.last_stats.threshold_ms, local_lanes, variant, peaks),
+            "phase_ms": {"gemm_per_launch": gemm_ms,
+                         "gemm_launches_per_step": stats_acc["gemm_launches"] / args.steps,
+                         "threshold_stream_span": sess.last_stats.threshold_ms,
+                         "or": sess.last_stats.or_ms, "prep": sess.last_stats.prep_ms, "step": ms,
+                         "host_wall_per_step": host_s / args.steps * 1e3,
+                         "note": "GEMM (stream 1) and threshold (stream 2) overlap; the span is the "
+                                 "threshold stream's first-start to last-end time of the last step"},
             "planted_match": planted, "setup_s": setup_s,
         }
         if cpu is not None:

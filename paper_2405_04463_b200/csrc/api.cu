@@ -571,7 +571,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       j.ntasks += seg_tasks(sg.lane_begin, sg.lane_end);
       j.ngrp += (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
       j.ngblk += 3ull * ngates * (nw / 8 + 2);
-      j.gwords += 3ull * ngates * nw;
+      j.gwords += 3ull * ngates * gate_row_words(nw);
     }
     jobs.push_back(j);
   };

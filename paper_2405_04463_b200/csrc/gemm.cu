@@ -126,23 +126,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const uint32_t nkb = g.nkb_seg * g.nseg;
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t u = g0; u < nunits; u += groups) {
-        const uint32_t n_tile = flat ? u % n_tiles : my_n;
-        const uint32_t uu = flat ? u / n_tiles : u;
-        const uint32_t m_pair = uu % m_pairs;
-        const uint32_t p = uu / m_pairs;
-        for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-          const uint32_t stage = it % STAGES;
-          const uint32_t phase = (it / STAGES) & 1;
-          mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t seg = kb / g.nkb_seg;
-          const uint32_t kk = kb % g.nkb_seg;
-          // A = [x_p | x_{p-1}]: the previous party's component plane, or plane 1
-          // of a single party's (own, prev) planes (party mode, nprob = 1)
-          const uint32_t pa = (g.rep && seg == 1) ? (g.nprob == 1 ? 1u : (p + 2) % 3) : p;
-          uint8_t* st = smem + stage * T::STAGE;
+    // TMA producer: warp-uniform loop, one elected lane issues
+    uint32_t it = 0;
+    for (uint32_t u = g0; u < nunits; u += groups) {
+      const uint32_t n_tile = flat ? u % n_tiles : my_n;
+      const uint32_t uu = flat ? u / n_tiles : u;
+      const uint32_t m_pair = uu % m_pairs;
+      const uint32_t p = uu / m_pairs;
+      for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+        const uint32_t stage = it % STAGES;
+        const uint32_t phase = (it / STAGES) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t seg = kb / g.nkb_seg;
+        const uint32_t kk = kb % g.nkb_seg;
+        // A = [x_p | x_{p-1}]: the previous party's component plane, or plane 1
+        // of a single party's (own, prev) planes (party mode, nprob = 1)
+        const uint32_t pa = (g.rep && seg == 1) ? (g.nprob == 1 ? 1u : (p + 2) % 3) : p;
+        uint8_t* st = smem + stage * T::STAGE;
+        if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * T::STAGE);
           const uint32_t fb = mapa_shared(&full[stage], 0);
 #pragma unroll
@@ -155,10 +156,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    // MMA issuer (leader CTA): warp-uniform loop, one elected lane issues
+    if (leader) {
       uint32_t it = 0, ti = 0;
       for (uint32_t u = g0; u < nunits; u += groups, ++ti) {
         if (ti > 0) {  // both CTAs' epilogues have drained the accumulators
@@ -171,22 +174,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + stage * T::STAGE);
+          if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < BK / 32; ++ks) {
-            const uint64_t off = (uint64_t)(ks * 32) >> 4;  // +32 bytes along K
+            for (int ks = 0; ks < BK / 32; ++ks) {
+              const uint64_t off = (uint64_t)(ks * 32) >> 4;  // +32 bytes along K
 #pragma unroll
-            for (int i = 0; i < L; ++i)
+              for (int i = 0; i < L; ++i)
 #pragma unroll
-              for (int j = 0; i + j < L; ++j) {
-                const uint64_t da = make_desc(st + i * T::A_T) + off;
-                const uint64_t db = make_desc(st + L * T::A_T + j * T::B_T) + off;
-                const uint32_t acc = ((kb | ks) != 0 || i > 0) ? 1u : 0u;  // (0, s) opens acc_s
-                umma_i8_pair(tmem + (i + j) * BN, da, db, T::IDESC, acc);
-              }
+                for (int j = 0; i + j < L; ++j) {
+                  const uint64_t da = make_desc(st + i * T::A_T) + off;
+                  const uint64_t db = make_desc(st + L * T::A_T + j * T::B_T) + off;
+                  const uint32_t acc = ((kb | ks) != 0 || i > 0) ? 1u : 0u;  // (0, s) opens acc_s
+                  umma_i8_pair(tmem + (i + j) * BN, da, db, T::IDESC, acc);
+                }
+            }
+            umma_commit_pair(&empty[stage], 0x3);
           }
-          umma_commit_pair(&empty[stage], 0x3);
+          __syncwarp();
         }
-        umma_commit_pair(accum, 0x3);
+        if (elect_one()) umma_commit_pair(accum, 0x3);
+        __syncwarp();
       }
     }
   } else if (warp >= 2) {

@@ -146,6 +146,9 @@ struct ThrArgs {
   uint32_t* tap_diff;
   uint8_t* tap_msb;
 };
+// words of one (seed, gate) row of the gate buffer for a segment of nw reference
+// words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
+__host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
 
 // ---- K5 OR reduction + open (orreduce.cu)

@@ -22,9 +22,12 @@
 // Warp-specialised and persistent:
 //   warp 0   TMA producer (128B-swizzled K-major tiles, mbarrier ring)
 //   warp 1   TMEM allocator; the leader's lane 0 issues the MMAs
-//   warps 2-5 epilogue: tcgen05.ld -> recombine -> global stores
-// (6 warps: the registers and warp slots left free go to the threshold
-// kernels that run concurrently on the second stream)
+//   warps 2-9 epilogue: tcgen05.ld -> recombine -> global stores; two warps per
+//            TMEM lane quadrant, each draining half of the tile's columns
+// (10 warps: the accumulators of a 256 x 256 tile fill all 512 TMEM columns, so
+// the epilogue is exposed once per tile; 8 warps drain it in half the time of 4
+// (-2% GEMM, -1% query), 16 crowd out the threshold kernels that run
+// concurrently on the second stream (+8% query))
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
@@ -37,6 +40,12 @@ namespace irisgpu {
 namespace {
 
 constexpr int BK = kGemmBK;
+// epilogue warps (multiple of 4: one per TMEM lane quadrant per column slice)
+#ifndef GEMM_EPI_WARPS
+#define GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = GEMM_EPI_WARPS;
+constexpr int kGemmThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int kStageBudget = 200 * 1024;
 
@@ -70,7 +79,7 @@ struct Tile {
 }  // namespace
 
 template <int L>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs, uint32_t grouped) {
   // Persistent: clusters form groups of n_tiles; cluster c owns n_tile = c % n_tiles
@@ -111,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(accum, 1);
-    mbar_init(tmem_empty, 8);  // 4 epilogue warps x 2 CTAs
+    mbar_init(tmem_empty, 2 * kEpiWarps);  // epilogue warps x 2 CTAs
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -198,6 +207,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
   } else if (warp >= 2) {
     const int q = warp & 3;  // tcgen05.ld: warp w reads TMEM lanes 32 (w % 4) .. + 31
+    // kEpiWarps / 4 warps share a lane quadrant, each draining its slice of the columns
+    constexpr int kSlice = BN / (kEpiWarps / 4);
+    const int c0 = ((warp - 2) / 4) * kSlice;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t te = mapa_shared(tmem_empty, 0);
     uint32_t ti = 0;
@@ -211,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
       const bool row_ok = row < g.s_valid;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = c0; c < c0 + kSlice; c += 16) {
         uint32_t acc[L][16];
 #pragma unroll
         for (int s = 0; s < L; ++s) tmem_ld16(tmem + lane_addr + s * BN + c, acc[s]);
@@ -298,7 +310,7 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
   const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
   const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
-  k_limb_gemm_pair<L><<<dim3(2 * ncl), 192, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
+  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
 }
 
 uint32_t gemm_groups(uint32_t n_tiles) {

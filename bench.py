@@ -158,7 +158,14 @@ def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int, varian
     import ctypes as C
     cores = os.cpu_count() or 1
     if O.ref_available():
+        # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, and the
+        # reference's OpenMP dot loop (libgomp) would otherwise run on one core
+        os.environ["OMP_NUM_THREADS"] = str(cores)
         R = O.ref()
+        try:
+            C.CDLL("libgomp.so.1").omp_set_num_threads(C.c_int(cores))
+        except OSError:
+            pass
         h = R.ref_bench_prepare(backend, variant, L, rows, persons)
         times = []
         m0 = C.c_uint8(0)

@@ -231,7 +231,9 @@ def compare_roofline(span_ms: float, lanes: int, variant: int, peaks: dict) -> d
                       "frac": (blocks / sec / cp) if cp else None,
                       "blocks_per_lane": prf_blocks_per_lane(variant)},
            "span_ms": span_ms,
-           "note": "over the threshold stream span, which overlaps the GEMM"}
+           "note": "over the threshold stream span, which overlaps the GEMM; the GEMM and the "
+                   "ChaCha work share the 1000 W power cap and do not overlap in time on the "
+                   "same SMs (DESIGN.md section 4), so the span is mostly GEMM-bound time"}
     return out
 
 
@@ -378,7 +380,11 @@ def main_gpu(args):
                        "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM)",
                        "parallelism": f"db-shard x{world}"},
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons},
+                    "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons,
+                    "note": "median of single queries through the public API (pinned host payloads in, "
+                            "person_match out), each bracketed by a host sync; the GPU idles between "
+                            "them, so under the 1000 W cap a single query can run at higher clocks "
+                            "than the back-to-back steps behind `value`"},
             "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic()[0],

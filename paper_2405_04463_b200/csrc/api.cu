@@ -947,6 +947,14 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
       f.nparty = widths[fi] == 0 ? 1 : 3;
       f.nseg = (widths[fi] != 0 && !c->shamir) ? 2 : 1;
       f.out_bytes = f.fmt.limbs == 4 ? 4 : 2;
+      // rotation-pair layout (and, with it, the Winograd rotation-pair GEMM) for integer
+      // fields of rotated queries; IRISMPC_RP=0 keeps the natural K order
+      static const bool rp_env = [] {
+        const char* e = std::getenv("IRISMPC_RP");
+        return !(e && e[0] == '0');
+      }();
+      f.fmt.rp = (rp_env && widths[fi] != 0 && cfg->rotations >= 3 && c->l_pad == cfg->l &&
+                  rp_layout_ok(cfg->l, c->shamir)) ? 1 : 0;
     }
   }
   for (int k = 0; k < 3; ++k) c->keys[k] = key_of(cfg->seeds + 16 * k);

@@ -37,7 +37,25 @@ struct FieldFmt {
   int limbs;           // u8 limb planes of the field (width, or 1 for bits)
   int slot = -1;       // plane slot to write (-1: the party index)
   int take_prev = 0;   // replicated: keep the `prev` component instead of `own`
+  int rp = 0;          // rotation-pair K layout (rp_pos), DB and query planes alike
 };
+
+// Rotation-pair (RP) K layout of an integer field's planes.  A plane row is
+// H halves (Shamir: the lc0 | lc1 halves of l/2; replicated: one component of
+// l) of 64 rotation blocks each (a rotation shifts a half by one block); the RP
+// layout puts every half's even blocks first, then the odd ones:
+//   row = [E_h0 .. E_h(H-1) | O_h0 .. O_h(H-1)],  E | O = l/2 elements each.
+// A K-permutation applied to both GEMM operands leaves every dot unchanged;
+// E and O (and S = E + O) are what the Winograd rotation-pair GEMM reads.
+__host__ __device__ inline uint32_t rp_pos(uint32_t k, uint32_t l, int halves) {
+  const uint32_t lh = l / halves, bs = lh / 64, h = k / lh, kk = k % lh, b = kk / bs, o = kk % bs;
+  return (b & 1) * (l / 2) + h * (lh / 2) + (b >> 1) * bs + o;
+}
+// RP needs whole 4-element parse groups per block and l/2 a whole number of 128-byte k-blocks
+inline bool rp_layout_ok(uint32_t l, int shamir) {
+  const uint32_t bs = shamir ? l / 128 : l / 64;
+  return l % 256 == 0 && bs % 4 == 0 && bs > 0;
+}
 
 // ---- K1 prep / dealer (prep.cu)
 void set_lambda(const uint32_t lam[6]);

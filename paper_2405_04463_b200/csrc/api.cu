@@ -139,12 +139,21 @@ struct FieldPlanes {
   CUtensorMap tA, tB, tQA;
   uint32_t ncols_pad_cur = 0;
   uint64_t qa_spad = 0;
+  // rotation-pair GEMM (prep.cu): S = E + O planes of the DB, D0 / M / D1 query planes
+  Buf sdb, rpq;
+  CUtensorMap tS, tRP;
+  bool rpg = false;  // S planes resident: rotated queries run the RP GEMMs
+  uint32_t rp_ncols_cur = 0;
   uint32_t bn() const { return gemm_bn((uint32_t)fmt.limbs); }
   void release() {
     db.release();
     q.release();
     qa.release();
     pair_c.release();
+    sdb.release();
+    rpq.release();
+    rpg = false;
+    rp_ncols_cur = 0;
     ncols_pad_cur = 0;
     qa_spad = 0;
   }
@@ -254,7 +263,11 @@ uint64_t s_total(const irismpc_gpu_ctx* c) {
 }
 
 int alloc_planes(irismpc_gpu_ctx* c, uint64_t s) {
-  for (auto& f : c->fld) f.db.release();
+  for (auto& f : c->fld) {
+    f.db.release();
+    f.sdb.release();
+    f.rpg = false;
+  }
   c->db_loaded = false;
   c->s = s;
   c->s_pad = round_up(s ? s : 1, 2 * kGemmBM);  // CTA-pair tiles cover 256 rows
@@ -287,6 +300,23 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     CK(c, cudaMemcpyAsync(&h, bad->p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
     if (h) return fail(c, IRISMPC_GPU_ERR_INCONSISTENT, "replicated share cross-check failed at load");
+  }
+  // RP: S = E + O planes (1.5x the DB planes in all).  A DB too large for them keeps the
+  // plain GEMM on the same (permuted) planes.
+  for (auto& f : c->fld) {
+    f.rpg = false;
+    if (!f.fmt.rp) continue;
+    const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
+    if (f.sdb.ensure(rows * (c->l / 2))) {
+      cudaGetLastError();  // out of memory is not sticky: clear it and run without RP
+      continue;
+    }
+    launch_rp_sum(f.db.as<uint8_t>(), ((uint64_t)f.nparty << 40) | c->s_pad, c->l, c->l_pad, f.fmt.limbs,
+                  f.sdb.as<uint8_t>(), c->st);
+    CK(c, cudaGetLastError());
+    if (make_plane_tmap(&f.tS, f.sdb.p, rows, c->l / 2, kGemmBM))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the RP sum planes");
+    f.rpg = true;
   }
   CK(c, cudaStreamSynchronize(c->st));
   c->db_loaded = true;
@@ -404,6 +434,30 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   debug_check("k_parse_query_field", st);
   CK(c, cudaGetLastError());
+  // rotation-pair GEMM planes (rotated queries, fields with resident S planes)
+  const uint32_t npr = (r + 1) / 2;
+  const uint64_t ncols_rp = (uint64_t)ncodes * npr;
+  const uint32_t ncols_rp_pad = (uint32_t)round_up(ncols_rp ? ncols_rp : 1, kGemmBN);
+  bool use_rp[2] = {false, false};
+  for (int fi = 0; fi < 2; ++fi) {
+    FieldPlanes& f = c->fld[fi];
+    use_rp[fi] = !membership && r >= 3 && f.rpg && s_loc > 0;
+    if (!use_rp[fi]) continue;
+    const uint64_t rows = 9ull * f.nseg * f.fmt.limbs * ncols_rp_pad;  // 3 kinds x 3 parties
+    const size_t bytes = rows * (c->l / 2);
+    if (bytes > f.rpq.cap || f.rp_ncols_cur != ncols_rp_pad) {
+      if (f.rpq.ensure(bytes)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "out of device memory for RP query planes");
+      CK(c, cudaMemsetAsync(f.rpq.p, 0, bytes, st));
+      if (make_plane_tmap(&f.tRP, f.rpq.p, rows, c->l / 2, f.bn() / 2))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the RP query planes");
+      f.rp_ncols_cur = ncols_rp_pad;
+    }
+    launch_parse_query_rp(dqp[0], dqp[1], dqp[2], ncodes, c->l, r, ncols_rp_pad, c->shamir, f.fmt,
+                          f.rpq.as<uint8_t>(), st);
+    ++launches;
+  }
+  debug_check("k_parse_query_rp", st);
+  CK(c, cudaGetLastError());
   if (npairs) {
     // pair dots as one limb GEMM per field: A = the unrotated query codes in the
     // DB plane layout, B = the rotated query planes (see pairs.cu)
@@ -465,9 +519,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     // waves of the persistent GEMM's cluster groups, for every field.
     uint64_t granule = 2 * kGemmBM;
     static const bool no_granule = std::getenv("IRISMPC_NO_GRANULE") != nullptr;  // A/B hook
-    for (const auto& f : c->fld) {
+    for (int fi = 0; fi < 2; ++fi) {
+      const FieldPlanes& f = c->fld[fi];
       if (no_granule) break;
-      const uint64_t g = gemm_groups((uint32_t)ceil_div(ncols, f.bn()));
+      const uint64_t g = gemm_groups((uint32_t)ceil_div(use_rp[fi] ? ncols_rp : ncols, f.bn()));
       uint64_t a = g, b = f.nparty;  // m_pairs multiple of g / gcd(g, nprob)
       while (b) {
         const uint64_t t = a % b;
@@ -589,6 +644,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         sg.lane_begin = col * S + row_off + chunk_row0[i];
         sg.lane_end = sg.lane_begin + nr;
         sg.src = col * nr;
+        sg.src_rp = ((col / r) * npr + (col % r) / 2) * nr;  // RP: the rotation pair's P planes
+        sg.rp_sel = ((col % r) & 1) ? 1u : 2u;
         sg.slot = (int64_t)col_fill[col];
         col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
@@ -604,6 +661,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     sg.lane_begin = ncols * S;
     sg.lane_end = n;
     sg.src = 0;
+    sg.src_rp = 0;
+    sg.rp_sel = 0;
     sg.slot = -1;
     add_job(nsegs_all - 1, 1, true, 0);
     cstride = std::max<uint64_t>(cstride, npairs);
@@ -615,8 +674,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     max_bits = std::max(max_bits, j.ntasks * 32);
   }
   // one dot buffer half: hd [3][ncols * rows_chunk] then ml [nparty][ncols * rows_chunk]
-  const uint64_t hd_half = 3 * ncols * rows_chunk * hb;
-  const uint64_t dots_half = round_up(hd_half + fm.nparty * ncols * rows_chunk * mb, 16);
+  // per field: plain [party][col][row] dots, or RP [kind P1 | P2 | P3][party][rotation pair][row]
+  const uint64_t hcols = use_rp[0] ? 3 * ncols_rp : ncols, mcols = use_rp[1] ? 3 * ncols_rp : ncols;
+  const uint64_t hd_half = 3 * hcols * rows_chunk * hb;
+  const uint64_t dots_half = round_up(hd_half + fm.nparty * mcols * rows_chunk * mb, 16);
   if (nsegs_all) {
     CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
     if ((nchunks && c->dots.ensure(2 * dots_half)) ||
@@ -661,8 +722,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   uint64_t task_off = 0;
   // hd_base: [3][pstride] hd dots; ml_base: [nparty][pstride] ml dots / public popcounts
-  auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride,
-                     int lane) -> int {
+  auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride_h,
+                     uint64_t pstride_m, uint64_t ks_h, uint64_t ks_m, int lane) -> int {
     ThrArgs t = ta;
     t.segs = c->segs.as<Seg>() + j.seg0;
     t.nsegs = (uint32_t)j.nseg;
@@ -675,11 +736,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.or_elem_base = ta.or_elem_base + task_off * 64;
     task_off += j.ntasks;
     for (int p = 0; p < 3; ++p) {
-      t.hd[p] = hd_base + p * pstride * hb;
-      t.ml[p] = ml_base + (fm.nparty == 3 ? p : 0) * pstride * mb;
+      t.hd[p] = hd_base + p * pstride_h * hb;
+      t.ml[p] = ml_base + (fm.nparty == 3 ? p : 0) * pstride_m * mb;
       t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
+    t.rp_kstride_h = ks_h;
+    t.rp_kstride_m = ks_m;
     launch_threshold(t, lane ? st3 : st2);
     CK(c, cudaGetLastError());
     launches += V == kMpcLift ? 5 : 3;
@@ -722,33 +785,62 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     CK(c, cudaEventRecord(c->gev[2 * i], st));
     for (int fi = 0; fi < 2; ++fi) {
       FieldPlanes& f = c->fld[fi];
-      GemmArgs g = field_gemm_args(c, f, ncols_pad);
-      g.s_pad = (uint32_t)c->s_pad;
-      g.s_valid = (uint32_t)nr;
-      g.row0 = (uint32_t)chunk_row0[i];
-      g.ncols = (uint32_t)ncols;
-      g.out = fi == 0 ? dots : dots_ml;
-      g.out_pstride = ncols * nr;
-      g.out_cstride = (uint32_t)nr;
+      const uint32_t m_tiles = (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM);
       void* ph = prof_begin(st);
-      launch_gemm(f.tA, f.tB, g, (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM), (uint32_t)ceil_div(ncols, f.bn()),
-                  st);
+      if (use_rp[fi]) {
+        // P1 = E.D0, P2 = S.M, P3 = O.D1 over half-length K (prep.cu, rotation pairs)
+        const uint64_t kind_rows = 3ull * f.nseg * f.fmt.limbs * ncols_rp_pad;
+        const uint64_t eb = fi == 0 ? hb : mb;
+        for (uint32_t kind = 0; kind < 3; ++kind) {
+          GemmArgs g = field_gemm_args(c, f, ncols_rp_pad);
+          g.nkb_seg = (c->l / 2) / kGemmBK;
+          g.a_kb0 = kind == 2 ? (c->l / 2) / kGemmBK : 0;
+          g.b_row0 = (uint32_t)(kind * kind_rows);
+          g.s_pad = (uint32_t)c->s_pad;
+          g.s_valid = (uint32_t)nr;
+          g.row0 = (uint32_t)chunk_row0[i];
+          g.ncols = (uint32_t)ncols_rp;
+          g.out = (fi == 0 ? dots : dots_ml) + kind * (3 * ncols_rp * nr) * eb;
+          g.out_pstride = ncols_rp * nr;
+          g.out_cstride = (uint32_t)nr;
+          launch_gemm(kind == 1 ? f.tS : f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st);
+          ++gemm_launches;
+          ++launches;
+        }
+      } else {
+        GemmArgs g = field_gemm_args(c, f, ncols_pad);
+        g.s_pad = (uint32_t)c->s_pad;
+        g.s_valid = (uint32_t)nr;
+        g.row0 = (uint32_t)chunk_row0[i];
+        g.ncols = (uint32_t)ncols;
+        g.out = fi == 0 ? dots : dots_ml;
+        g.out_pstride = ncols * nr;
+        g.out_cstride = (uint32_t)nr;
+        launch_gemm(f.tA, f.tB, g, m_tiles, (uint32_t)ceil_div(ncols, f.bn()), st);
+        ++gemm_launches;
+        ++launches;
+      }
       prof_end(ph, fi == 0 ? "k_limb_gemm_pair (hd)" : "k_limb_gemm_pair (ml)", st);
       debug_check("k_limb_gemm_pair", st);
       CK(c, cudaGetLastError());
-      ++gemm_launches;
-      ++launches;
     }
     CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
     if (c->taps && c->cfg.db_rows_total == 0) {
       // L1 tap: dots[(col, row - r0)] -> lane col*S + row
-      for (uint32_t p = 0; p < 3; ++p)
-        CK(c, cudaMemcpy2DAsync(c->tap_buf[0].as<uint8_t>() + (p * n + chunk_row0[i]) * hb, S * hb,
-                                dots + p * ncols * nr * hb, nr * hb, nr * hb, ncols, cudaMemcpyDeviceToDevice, st));
-      for (uint32_t p = 0; p < fm.nparty; ++p)
-        CK(c, cudaMemcpy2DAsync(c->tap_buf[1].as<uint8_t>() + (p * n + chunk_row0[i]) * mb, S * mb,
-                                dots_ml + p * ncols * nr * mb, nr * mb, nr * mb, ncols, cudaMemcpyDeviceToDevice,
-                                st));
+      if (use_rp[0])
+        launch_rp_tap(dots, (int)hb, 3, ncols, r, nr, 3 * ncols_rp * nr, c->tap_buf[0].p, n, S, chunk_row0[i], st);
+      else
+        for (uint32_t p = 0; p < 3; ++p)
+          CK(c, cudaMemcpy2DAsync(c->tap_buf[0].as<uint8_t>() + (p * n + chunk_row0[i]) * hb, S * hb,
+                                  dots + p * ncols * nr * hb, nr * hb, nr * hb, ncols, cudaMemcpyDeviceToDevice, st));
+      if (use_rp[1])
+        launch_rp_tap(dots_ml, (int)mb, 3, ncols, r, nr, 3 * ncols_rp * nr, c->tap_buf[1].p, n, S, chunk_row0[i],
+                      st);
+      else
+        for (uint32_t p = 0; p < fm.nparty; ++p)
+          CK(c, cudaMemcpy2DAsync(c->tap_buf[1].as<uint8_t>() + (p * n + chunk_row0[i]) * mb, S * mb,
+                                  dots_ml + p * ncols * nr * mb, nr * mb, nr * mb, ncols, cudaMemcpyDeviceToDevice,
+                                  st));
     }
     CK(c, cudaEventRecord(c->evg[i], st));
     CK(c, cudaStreamWaitEvent(st2, c->evg[i], 0));
@@ -760,7 +852,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       }
     }
     for (int lane = 0; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji, lane ^= (two ? 1 : 0)) {
-      int rc2 = run_job(jobs[ji], dots, dots_ml, ncols * nr, lane);
+      const uint64_t rpn = ncols_rp * nr;
+      int rc2 = run_job(jobs[ji], dots, dots_ml, use_rp[0] ? rpn : ncols * nr, use_rp[1] ? rpn : ncols * nr,
+                        use_rp[0] ? 3 * rpn : 0, use_rp[1] ? 3 * rpn : 0, lane);
       if (rc2) return rc2;
     }
     CK(c, cudaEventRecord(c->evt[i], st2));
@@ -780,7 +874,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint8_t>() + (p * n + ncols * S) * mb, pd_ml + p * npairs * mb,
                               npairs * mb, cudaMemcpyDeviceToDevice, st2));
     }
-    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, 0);
+    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, npairs, 0, 0, 0);
     if (rc2) return rc2;
   }
   if (two) {  // the OR reads every job's partial slots (and the pair job reused the work buffers)

@@ -159,9 +159,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int limb = 0; limb < L; ++limb) {
             const int32_t arow =
                 (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
-            const int32_t brow = (int32_t)(((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 + n_tile * BN +
-                                           rank * (BN / 2));
-            tma_load_2d_pair(st + limb * T::A_T, &tA, fb, (int32_t)(kk * BK), arow);
+            const int32_t brow = (int32_t)(g.b_row0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
+                                           n_tile * BN + rank * (BN / 2));
+            tma_load_2d_pair(st + limb * T::A_T, &tA, fb, (int32_t)((g.a_kb0 + kk) * BK), arow);
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
           }
         }

@@ -71,6 +71,14 @@ void launch_check_rep(const uint8_t* p1, const uint8_t* p2, const uint8_t* p3, u
 void launch_parse_query_field(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes,
                               uint32_t l, uint32_t l_pad, uint32_t rot, uint32_t ncols_pad, int shamir,
                               const FieldFmt& f, uint8_t* planes, cudaStream_t st);
+// RP: S = E + O (mod 2^(8 limbs)) of every DB plane row -> splanes[(c * limbs + limb) * s_pad + row][l / 2]
+void launch_rp_sum(const uint8_t* planes, uint64_t nrows_total, uint32_t l, uint32_t l_pad, int limbs,
+                   uint8_t* splanes, cudaStream_t st);
+// RP query planes: kinds D0 / M / D1 of the rotation pairs, rows
+// [(((kind * 3 + p) * nseg + seg) * limbs + limb) * ncols_pad + code * npr + jp][l / 2]
+void launch_parse_query_rp(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes, uint32_t l,
+                           uint32_t rot, uint32_t ncols_pad, int shamir, const FieldFmt& f, uint8_t* planes,
+                           cudaStream_t st);
 void launch_synth_records(SeedKey key, uint64_t first, uint64_t count, uint32_t l, double density,
                           uint64_t* codes, uint64_t* masks, cudaStream_t st);
 void launch_deal(SeedKey key, uint64_t first_record, uint64_t nrec, uint32_t l, int shamir, int variant,
@@ -97,6 +105,8 @@ struct GemmArgs {
   void* out;          // [nprob][ncols * out_cstride], u16 (limbs <= 2) or u32 (limbs = 4)
   uint64_t out_pstride;
   uint32_t out_cstride;
+  uint32_t a_kb0 = 0;  // first A k-block of every segment (RP: the O half of a DB plane row)
+  uint32_t b_row0 = 0; // B plane rows skipped (RP: the D0 / M / D1 plane set)
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }
@@ -127,6 +137,8 @@ struct Seg {
   uint64_t grp_begin;             // first 8-lane group (chunk-relative)
   uint64_t gblk_begin;            // first gate-keystream thread (chunk-relative)
   int64_t slot;                   // partial slot of its first task, -1 = no fused OR
+  uint64_t src_rp;                // RP fields: chunk-buffer index of lane_begin in the P planes
+  uint32_t rp_sel;                // RP fields: dot = P2 + P1 (1, odd rotation) or P2 + P3 (2, even)
 };
 
 struct ThrArgs {
@@ -136,6 +148,9 @@ struct ThrArgs {
   int variant;
   const void* hd[3];     // additive hd dots, u16 (KH = 16) or u32
   const void* ml[3];     // additive ml dots (u16 / u32), or the public popcount (u16, all three equal)
+  // RP fields: hd / ml point at the party's P1 plane; P2, P3 follow at +rp_kstride, +2 rp_kstride
+  // elements (0: the field's dots are plain [col][row])
+  uint64_t rp_kstride_h, rp_kstride_m;
   uint64_t n, W;
   uint64_t pos[3];
   SeedKey key[3];
@@ -168,6 +183,9 @@ struct ThrArgs {
 // words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
+// L1 tap of an RP field's chunk: out[p * n + col * S + row0 + row] = P2 + P(1|3) of (col, row)
+void launch_rp_tap(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                   uint64_t kstride, void* out, uint64_t n, uint64_t S, uint64_t row0, cudaStream_t st);
 
 // ---- K5 OR reduction + open (orreduce.cu)
 struct OrArgs {

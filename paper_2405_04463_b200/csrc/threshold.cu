@@ -149,8 +149,8 @@ namespace {
 
 // 8 lanes [L8, L8+8) of a dot array (u16 or u32) -> v[0..7]; `full`: one aligned vector access
 template <typename T>
-__device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, bool full, bool mine, uint32_t v[8]) {
-  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
+__device__ __forceinline__ void load8_at(const T* src, uint64_t src0, const Seg& sg, uint64_t L8, bool full,
+                                         bool mine, uint32_t v[8]) {
   if (full) {
     if (sizeof(T) == 2) {
       const uint4 x = *reinterpret_cast<const uint4*>(src + src0);
@@ -168,12 +168,30 @@ __device__ __forceinline__ void load8(const T* src, const Seg& sg, uint64_t L8, 
     }
     return;
   }
+  const uint64_t base = src0 - (L8 - sg.lane_begin);  // index of lane_begin
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint64_t ln = L8 + i;
     const bool ok = mine && ln >= sg.lane_begin && ln < sg.lane_end;
-    v[i] = ok ? (uint32_t)src[sg.src + (ln - sg.lane_begin)] : 0u;
+    v[i] = ok ? (uint32_t)src[base + (ln - sg.lane_begin)] : 0u;
   }
+}
+
+// A field's dots of lanes [L8, L8+8): plain [col][row] planes, or (RP) the sum
+// of the rotation pair's shared product P2 and its own P1 / P3 (prep.cu)
+template <typename T>
+__device__ __forceinline__ void load8(const T* src, uint64_t kstride, const Seg& sg, uint64_t L8, bool full,
+                                      bool mine, uint32_t v[8]) {
+  if (!kstride) {
+    load8_at<T>(src, sg.src + (L8 - sg.lane_begin), sg, L8, full, mine, v);
+    return;
+  }
+  const uint64_t i0 = sg.src_rp + (L8 - sg.lane_begin);
+  uint32_t a[8];
+  load8_at<T>(src, i0 + kstride, sg, L8, full, mine, v);
+  load8_at<T>(src, i0 + (sg.rp_sel == 1 ? 0 : 2 * kstride), sg, L8, full, mine, a);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += a[i];
 }
 
 // reshare one dot (zero_ring<K>, rep3.hpp:110-112): component k gains F_k and
@@ -222,11 +240,15 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   const HT* hd[3];
   const MT* ml[3];
 #pragma unroll
+  const uint64_t rp0 = sg.src_rp + (L8 - sg.lane_begin);
+  const uint64_t hs0 = A.rp_kstride_h ? rp0 : src0, ms0 = A.rp_kstride_m ? rp0 : src0;
+  const uint64_t hk = A.rp_kstride_h, mk = A.rp_kstride_m;
+  full = full && hk % 8 == 0 && mk % 8 == 0;  // P2 / P3 vectors stay 16-byte aligned
   for (int p = 0; p < 3; ++p) {
     hd[p] = static_cast<const HT*>(A.hd[p]);
     ml[p] = static_cast<const MT*>(A.ml[p]);
-    // 16-byte alignment of every vector access
-    full = full && ((reinterpret_cast<uintptr_t>(hd[p] + src0) | reinterpret_cast<uintptr_t>(ml[p] + src0) |
+    // 16-byte alignment of every vector access (RP: all three P planes; kstride is a multiple of 8)
+    full = full && ((reinterpret_cast<uintptr_t>(hd[p] + hs0) | reinterpret_cast<uintptr_t>(ml[p] + ms0) |
                      reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0)) & 15) == 0;
     if (V == kMpcLift) full = full && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) & 15) == 0;
   }
@@ -235,7 +257,7 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   uint32_t d[3][8], m[3][8];
   if (V != kPlainMask) {
 #pragma unroll
-    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], sg, L8, full, gc.mine, m[p]);
+    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], mk, sg, L8, full, gc.mine, m[p]);
     reshare8(A, A.n + L8, gc.next_contig, m, MM);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
@@ -274,12 +296,12 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   }
   uint32_t (&h)[3][8] = m;  // reuse the registers
 #pragma unroll
-  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], sg, L8, full, gc.mine, h[p]);
+  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], hk, sg, L8, full, gc.mine, h[p]);
   reshare8(A, L8, gc.next_contig, h, HM);
   if (V == kPlainMask) {
     // public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
     uint32_t cnt[8];
-    load8<MT>(ml[0], sg, L8, full, gc.mine, cnt);
+    load8<MT>(ml[0], mk, sg, L8, full, gc.mine, cnt);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)cnt[i]));
@@ -656,6 +678,30 @@ __global__ void __launch_bounds__(128, MSB_LB) k_msb(const __grid_constant__ Thr
   }
   __shared__ uint64_t orr[4][3][40];
   if (t.sg.slot >= 0) fused_or(A, t.sg, task, bit, lane, orr[threadIdx.x >> 5]);
+}
+
+template <typename T>
+__global__ void k_rp_tap(const T* __restrict__ P, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                         uint64_t kstride, T* __restrict__ out, uint64_t n, uint64_t S, uint64_t row0) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (tid >= nparty * ncols * nr) return;
+  const uint64_t row = tid % nr, pc = tid / nr, col = pc % ncols, p = pc / ncols;
+  const uint32_t npr = (rot + 1) / 2, j = (uint32_t)(col % rot);
+  const uint64_t cp = (col / rot) * npr + j / 2;
+  const uint64_t i = p * (npr * (ncols / rot)) * nr + cp * nr + row;  // party p's P1 plane
+  out[p * n + col * S + row0 + row] = (T)(P[i + kstride] + P[i + ((j & 1) ? 0 : 2 * kstride)]);
+}
+
+void launch_rp_tap(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                   uint64_t kstride, void* out, uint64_t n, uint64_t S, uint64_t row0, cudaStream_t st) {
+  const uint64_t tot = nparty * ncols * nr;
+  const unsigned g = (unsigned)((tot + 255) / 256);
+  if (elem_bytes == 2)
+    k_rp_tap<uint16_t><<<g, 256, 0, st>>>(static_cast<const uint16_t*>(P), nparty, ncols, rot, nr, kstride,
+                                           static_cast<uint16_t*>(out), n, S, row0);
+  else
+    k_rp_tap<uint32_t><<<g, 256, 0, st>>>(static_cast<const uint32_t*>(P), nparty, ncols, rot, nr, kstride,
+                                           static_cast<uint32_t*>(out), n, S, row0);
 }
 
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {

@@ -306,7 +306,7 @@ def main_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
 
-    stats_acc = {"gemm_ms": 0.0, "launches": 0, "gemm_launches": 0}
+    stats_acc = {"gemm_ms": 0.0, "launches": 0, "gemm_launches": 0, "gemm_ops": 0, "rp": 0}
     with Clocks(local) as clk:
         if world > 1:
             dist.barrier()
@@ -322,6 +322,8 @@ def main_gpu(args):
             stats_acc["gemm_ms"] += st.gemm_ms
             stats_acc["launches"] += st.kernel_launches + (1 if world > 1 and rank == 0 else 0)
             stats_acc["gemm_launches"] += st.gemm_launches
+            stats_acc["gemm_ops"] += st.gemm_int8_ops
+            stats_acc["rp"] = int(st.rotation_pair_gemm)
         with torch.cuda.stream(ext):
             ev1.record()
         torch.cuda.synchronize()
@@ -360,6 +362,8 @@ def main_gpu(args):
         plane_kb = L * (3 * kh // 8 + (3 * km // 8 if km else 1)) / 1e3
         ops_launch = local_lanes * opl / max(1, stats_acc["gemm_launches"] // args.steps)
         achieved = ops_launch / (gemm_ms / 1e3) / 1e12
+        exec_opl = stats_acc["gemm_ops"] / max(1, args.steps) / max(1, local_lanes)
+        exec_tops = stats_acc["gemm_ops"] / max(1, stats_acc["gemm_launches"]) / (gemm_ms / 1e3) / 1e12
         i8 = os.path.join(ROOT, "profiles", "int8_peak.json")
         if os.path.exists(i8):
             peak = json.load(open(i8))["int8_tops_burst"]
@@ -389,7 +393,12 @@ def main_gpu(args):
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic()[0],
                          "ncu_tensor_pipe_active_pct": ncu_traffic()[1],
-                         "note": f"int8 ops = {opl}/lane; peak = {peak_note}"},
+                         "executed": {"int8_ops_per_lane": exec_opl, "achieved": exec_tops, "frac": exec_tops / peak,
+                                      "rotation_pair_gemm": bool(stats_acc["rp"])},
+                         "note": f"achieved = algorithmic int8 ops ({opl}/lane) / GEMM time; peak = {peak_note}. "
+                                 "The rotation-pair (Winograd F(2,2)) GEMMs execute fewer int8 MACs than the "
+                                 "algorithmic count (DESIGN.md section 8), so `achieved` can exceed the executed "
+                                 "rate: `executed` is the tensor-pipe figure"},
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),
             "roofline_compare": compare_roofline(sess.last_stats.threshold_ms, local_lanes, variant, peaks),

@@ -82,6 +82,10 @@ typedef struct irismpc_gpu_stats {
   double wall_ms;      /* device time of the whole query (CUDA events) */
   double prep_ms, gemm_ms, threshold_ms, or_ms;
   uint64_t gemm_launches, kernel_launches;
+  /* int8 ops the DB-lane GEMMs executed (all parties, both fields); below the
+     algorithmic count when the rotation-pair (Winograd) GEMMs ran */
+  uint64_t gemm_int8_ops;
+  uint32_t rotation_pair_gemm; /* 1 if the rotation-pair GEMMs ran for some field */
 } irismpc_gpu_stats;
 
 /* ---- setup ------------------------------------------------------------ */

@@ -111,7 +111,8 @@ class Stats(C.Structure):
                 ("or_tree_bytes", C.c_uint64 * 3), ("dot_rounds", C.c_uint64), ("lift_rounds", C.c_uint64),
                 ("msb_rounds", C.c_uint64), ("or_tree_rounds", C.c_uint64), ("wall_ms", C.c_double),
                 ("prep_ms", C.c_double), ("gemm_ms", C.c_double), ("threshold_ms", C.c_double),
-                ("or_ms", C.c_double), ("gemm_launches", C.c_uint64), ("kernel_launches", C.c_uint64)]
+                ("or_ms", C.c_double), ("gemm_launches", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("gemm_int8_ops", C.c_uint64), ("rotation_pair_gemm", C.c_uint32)]
 
     def party(self, p: int) -> dict:
         return dict(dot_bytes=self.dot_bytes[p], lift_bytes=self.lift_bytes[p], msb_bytes=self.msb_bytes[p],

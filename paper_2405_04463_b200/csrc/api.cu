@@ -307,6 +307,9 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     f.rpg = false;
     if (!f.fmt.rp) continue;
     const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
+    // keep 16 GB free for the query's work buffers (dots, gate keystream, planes)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || free_b < rows * (c->l / 2) + (16ull << 30)) continue;
     if (f.sdb.ensure(rows * (c->l / 2))) {
       cudaGetLastError();  // out of memory is not sticky: clear it and run without RP
       continue;
@@ -773,6 +776,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   // ---- DB lanes: GEMMs(i) on st || threshold(i-1) on st2
   double gemm_ms = 0;
   uint64_t gemm_launches = 0;
+  uint64_t gemm_ops = 0;  // executed int8 ops of the DB-lane GEMMs
+  for (int fi = 0; fi < 2; ++fi) {
+    const FieldPlanes& f = c->fld[fi];
+    const uint64_t L = (uint64_t)f.fmt.limbs, prods = L * (L + 1) / 2;
+    gemm_ops += use_rp[fi] ? 2 * prods * 3 * f.nparty * ncols_rp * s_loc * (c->l / 2) * f.nseg
+                           : 2 * prods * f.nparty * ncols * s_loc * c->l_pad * f.nseg;
+  }
   size_t ji = 0;
   for (uint64_t i = 0; i < nchunks; ++i) {
     const uint64_t nr = chunk_rows(i);
@@ -968,6 +978,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     stats->or_ms = ms;
     stats->gemm_launches = gemm_launches;
     stats->kernel_launches = launches;
+    stats->gemm_int8_ops = gemm_ops;
+    stats->rotation_pair_gemm = (use_rp[0] || use_rp[1]) ? 1u : 0u;
   }
   return 0;
 }

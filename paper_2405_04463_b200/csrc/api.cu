@@ -303,9 +303,13 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
   }
   // RP: S = E + O planes (1.5x the DB planes in all).  A DB too large for them keeps the
   // plain GEMM on the same (permuted) planes.
+  static const bool rp_layout_only = [] {
+    const char* e = std::getenv("IRISMPC_RP");
+    return e && std::string(e) == "layout";
+  }();
   for (auto& f : c->fld) {
     f.rpg = false;
-    if (!f.fmt.rp) continue;
+    if (!f.fmt.rp || rp_layout_only) continue;
     const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
     // keep 16 GB free for the query's work buffers (dots, gate keystream, planes)
     size_t free_b = 0, total_b = 0;
@@ -1054,7 +1058,8 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
       f.nseg = (widths[fi] != 0 && !c->shamir) ? 2 : 1;
       f.out_bytes = f.fmt.limbs == 4 ? 4 : 2;
       // rotation-pair layout (and, with it, the Winograd rotation-pair GEMM) for integer
-      // fields of rotated queries; IRISMPC_RP=0 keeps the natural K order
+      // fields of rotated queries; IRISMPC_RP=0 keeps the natural K order, IRISMPC_RP=layout
+      // the RP planes without the S planes (the large-DB fallback, for tests)
       static const bool rp_env = [] {
         const char* e = std::getenv("IRISMPC_RP");
         return !(e && e[0] == '0');

@@ -389,3 +389,43 @@ def test_persistent_session_varying_query_shapes(be, var):
         np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos, err_msg=f"query {qi}")
         assert m[0] == 1
         pos = ref.stream_pos
+
+
+@pytest.mark.parametrize("mode", ["1", "layout", "0"])
+@pytest.mark.parametrize("be,var,l", [(O.SHAMIR, P.MPC_LIFT, 1024), (O.REPLICATED, P.NO_LIFT, 512),
+                                      (O.SHAMIR, P.PLAIN_MASK, 1024)])
+def test_rotation_pair_gemm_modes(mode, be, var, l):
+    """The rotation-pair (Winograd F(2,2)) GEMMs, the RP plane layout without
+    them (the large-DB fallback) and the natural layout: per-party dots (L1),
+    row bits and person bits identical to the oracle in every mode."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent(f"""
+        import sys, numpy as np
+        sys.path.insert(0, '.')
+        import paper_2405_04463_b200 as P
+        from oracle import pyoracle as O
+        be, var, l, s, persons, seed, r = {be}, {var}, {l}, 700, 2, 23, 31
+        rng = O.Rng(seed)
+        dc, dm = O.records(rng, l, s, 0.9)
+        qc, qm = O.records(rng, l, 2 * persons, 0.9)
+        qc[1], qm[1] = dc[300], dm[300]
+        cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True, variant=var)
+        m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, want_rows=True, taps=True)
+        ref = O.run_local(O.make_config(be, l, 0.375, r, True, variant=var), seed, dc, dm, qc, qm, persons,
+                          want_all=True)
+        n = P.lane_count(persons, s, r)
+        assert (m == ref.person_match).all(), (m, ref.person_match)
+        assert (sess.row_bits[:n] == ref.row_bits).all()
+        np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_HD, n), ref.dot_hd, err_msg="L1 hd dots")
+        if var != P.PLAIN_MASK:
+            np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_ML, n), ref.dot_ml, err_msg="L1 ml dots")
+        np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
+        rp = int(sess.last_stats.rotation_pair_gemm)
+        assert rp == (1 if {mode!r} == "1" else 0), rp
+        print("ok", m, rp)
+    """)
+    import os
+    env = dict(os.environ, IRISMPC_RP=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout + r.stderr

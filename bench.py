@@ -137,12 +137,15 @@ def chacha_peak():
     return None
 
 
-def ncu_traffic():
-    """dram bytes per GEMM launch from the committed ncu --set full capture (or None)."""
+def ncu_traffic(rp: bool = False):
+    """dram bytes per GEMM launch from the committed ncu --set full capture (or None);
+    rp: the rotation-pair GEMM launches"""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
             d = json.load(open(p))
+            if rp and "rotation_pair" in d:
+                d = d["rotation_pair"]
             return d.get("gemm_dram_bytes_per_launch"), d.get("tensor_pipe_active_pct")
         except Exception:
             return None, None
@@ -391,8 +394,8 @@ def main_gpu(args):
                             "than the back-to-back steps behind `value`"},
             "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic()[0],
-                         "ncu_tensor_pipe_active_pct": ncu_traffic()[1],
+                         "traffic": ncu_traffic(bool(stats_acc["rp"]))[0],
+                         "ncu_tensor_pipe_active_pct": ncu_traffic(bool(stats_acc["rp"]))[1],
                          "executed": {"int8_ops_per_lane": exec_opl, "achieved": exec_tops, "frac": exec_tops / peak,
                                       "rotation_pair_gemm": bool(stats_acc["rp"])},
                          "note": f"achieved = algorithmic int8 ops ({opl}/lane) / GEMM time; peak = {peak_note}. "

@@ -533,7 +533,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       const FieldPlanes& f = c->fld[fi];
       if (no_granule) break;
       const uint64_t g = gemm_groups((uint32_t)ceil_div(use_rp[fi] ? ncols_rp : ncols, f.bn()));
-      uint64_t a = g, b = f.nparty;  // m_pairs multiple of g / gcd(g, nprob)
+      uint64_t a = g, b = f.nparty * (use_rp[fi] ? 3 : 1);  // m_pairs multiple of g / gcd(g, nprob)
       while (b) {
         const uint64_t t = a % b;
         a = b;
@@ -806,24 +806,23 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       void* ph = prof_begin(st);
       if (use_rp[fi]) {
         // P1 = E.D0, P2 = S.M, P3 = O.D1 over half-length K (prep.cu, rotation pairs)
-        const uint64_t kind_rows = 3ull * f.nseg * f.fmt.limbs * ncols_rp_pad;
-        const uint64_t eb = fi == 0 ? hb : mb;
-        for (uint32_t kind = 0; kind < 3; ++kind) {
-          GemmArgs g = field_gemm_args(c, f, ncols_rp_pad);
-          g.nkb_seg = (c->l / 2) / kGemmBK;
-          g.a_kb0 = kind == 2 ? (c->l / 2) / kGemmBK : 0;
-          g.b_row0 = (uint32_t)(kind * kind_rows);
-          g.s_pad = (uint32_t)c->s_pad;
-          g.s_valid = (uint32_t)nr;
-          g.row0 = (uint32_t)chunk_row0[i];
-          g.ncols = (uint32_t)ncols_rp;
-          g.out = (fi == 0 ? dots : dots_ml) + kind * (3 * ncols_rp * nr) * eb;
-          g.out_pstride = ncols_rp * nr;
-          g.out_cstride = (uint32_t)nr;
-          launch_gemm(kind == 1 ? f.tS : f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st);
-          ++gemm_launches;
-          ++launches;
-        }
+        // one launch, 3 kinds x 3 parties: fewer partial last waves than three launches
+        GemmArgs g = field_gemm_args(c, f, ncols_rp_pad);
+        g.nkb_seg = (c->l / 2) / kGemmBK;
+        g.nkind = 3;
+        g.a_kb0_k2 = (c->l / 2) / kGemmBK;
+        g.b_kind_rows = (uint32_t)(3ull * f.nseg * f.fmt.limbs * ncols_rp_pad);
+        g.s_pad = (uint32_t)c->s_pad;
+        g.s_valid = (uint32_t)nr;
+        g.row0 = (uint32_t)chunk_row0[i];
+        g.ncols = (uint32_t)ncols_rp;
+        g.out = fi == 0 ? dots : dots_ml;
+        g.out_pstride = ncols_rp * nr;
+        g.out_kstride = 3 * ncols_rp * nr;
+        g.out_cstride = (uint32_t)nr;
+        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st, &f.tS);
+        ++gemm_launches;
+        ++launches;
       } else {
         GemmArgs g = field_gemm_args(c, f, ncols_pad);
         g.s_pad = (uint32_t)c->s_pad;

@@ -81,6 +81,7 @@ struct Tile {
 template <int L>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                     const __grid_constant__ CUtensorMap tA2,
                      const GemmArgs g, uint32_t n_tiles, uint32_t m_pairs, uint32_t grouped) {
   // Persistent: clusters form groups of n_tiles; cluster c owns n_tile = c % n_tiles
   // and its group sweeps (prob, m_pair) units g, g + groups, ...  The n_tiles
@@ -110,10 +111,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t groups = ncl / tiles_per_unit;
   const uint32_t my_n = flat ? 0 : cl % n_tiles;
   const uint32_t g0 = flat ? cl : cl / n_tiles;
-  const uint32_t nunits = flat ? g.nprob * m_pairs * n_tiles : g.nprob * m_pairs;
+  const uint32_t nprob_all = g.nprob * g.nkind;
+  const uint32_t nunits = flat ? nprob_all * m_pairs * n_tiles : nprob_all * m_pairs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tA);
+    if (g.nkind > 1) tma_prefetch_desc(&tA2);
     tma_prefetch_desc(&tB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -141,7 +144,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t n_tile = flat ? u % n_tiles : my_n;
       const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
-      const uint32_t p = uu / m_pairs;
+      const uint32_t prob = uu / m_pairs;
+      const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
+      const void* ta = kind == 1 ? (const void*)&tA2 : (const void*)&tA;
+      const uint32_t akb = kind == 2 ? g.a_kb0_k2 : g.a_kb0;
+      const uint32_t brow0 = g.b_row0 + kind * g.b_kind_rows;
       for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
@@ -159,9 +166,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int limb = 0; limb < L; ++limb) {
             const int32_t arow =
                 (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
-            const int32_t brow = (int32_t)(g.b_row0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
+            const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
                                            n_tile * BN + rank * (BN / 2));
-            tma_load_2d_pair(st + limb * T::A_T, &tA, fb, (int32_t)((g.a_kb0 + kk) * BK), arow);
+            tma_load_2d_pair(st + limb * T::A_T, ta, fb, (int32_t)((akb + kk) * BK), arow);
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
           }
         }
@@ -217,7 +224,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t n_tile = flat ? u % n_tiles : my_n;
       const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
-      const uint32_t p = uu / m_pairs;
+      const uint32_t prob = uu / m_pairs;
+      const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
       mbar_wait(accum, ti & 1);
       tc_fence_after();
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
@@ -235,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           uint32_t v = acc[0][j];
 #pragma unroll
           for (int s = 1; s < L; ++s) v += acc[s][j] << (8 * s);
-          const uint64_t o = (uint64_t)p * g.out_pstride + (uint64_t)col * g.out_cstride + row;
+          const uint64_t o = kind * g.out_kstride + (uint64_t)p * g.out_pstride + (uint64_t)col * g.out_cstride + row;
           if (L == 4)
             static_cast<uint32_t*>(g.out)[o] = v;
           else
@@ -289,8 +297,8 @@ int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 }
 
 template <int L>
-static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
-                               uint32_t n_tiles, cudaStream_t st) {
+static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const GemmArgs& g,
+                               uint32_t m_tiles, uint32_t n_tiles, cudaStream_t st) {
   using T = Tile<L>;
   static bool attr = false;
   if (!attr) {
@@ -305,12 +313,12 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
     if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) nsm = std::max(2, std::min(nsm, std::atoi(e)));  // experiment hook
   }
   const uint32_t m_pairs = m_tiles / 2;
-  const uint32_t units = g.nprob * m_pairs;
+  const uint32_t units = g.nprob * g.nkind * m_pairs;
   const uint32_t max_cl = (uint32_t)(nsm / 2);
   const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
   const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
   const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
-  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, g, n_tiles, m_pairs, grouped ? 1u : 0u);
+  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, g, n_tiles, m_pairs, grouped ? 1u : 0u);
 }
 
 uint32_t gemm_groups(uint32_t n_tiles) {
@@ -321,11 +329,12 @@ uint32_t gemm_groups(uint32_t n_tiles) {
 }
 
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
-                 uint32_t n_tiles, cudaStream_t st) {
+                 uint32_t n_tiles, cudaStream_t st, const CUtensorMap* a2) {
+  const CUtensorMap& A2 = a2 ? *a2 : a;
   switch (g.limbs) {
-    case 1: launch_pair_kernel<1>(a, b, g, m_tiles, n_tiles, st); break;
-    case 2: launch_pair_kernel<2>(a, b, g, m_tiles, n_tiles, st); break;
-    default: launch_pair_kernel<4>(a, b, g, m_tiles, n_tiles, st); break;
+    case 1: launch_pair_kernel<1>(a, b, A2, g, m_tiles, n_tiles, st); break;
+    case 2: launch_pair_kernel<2>(a, b, A2, g, m_tiles, n_tiles, st); break;
+    default: launch_pair_kernel<4>(a, b, A2, g, m_tiles, n_tiles, st); break;
   }
 }
 

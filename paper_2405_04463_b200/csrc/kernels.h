@@ -107,6 +107,12 @@ struct GemmArgs {
   uint32_t out_cstride;
   uint32_t a_kb0 = 0;  // first A k-block of every segment (RP: the O half of a DB plane row)
   uint32_t b_row0 = 0; // B plane rows skipped (RP: the D0 / M / D1 plane set)
+  // RP: one launch runs nkind = 3 products per party (problem = kind * nprob + party):
+  // kind 0 P1 = E.D0 (A = tA), kind 1 P2 = S.M (A = tA2), kind 2 P3 = O.D1 (A = tA at a_kb0_k2)
+  uint32_t nkind = 1;
+  uint32_t a_kb0_k2 = 0;
+  uint32_t b_kind_rows = 0;   // B rows per kind
+  uint64_t out_kstride = 0;   // output elements per kind
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }
@@ -116,7 +122,7 @@ inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }
 int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad,
                     uint32_t box_rows);
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, uint32_t m_tiles,
-                 uint32_t n_tiles, cudaStream_t st);
+                 uint32_t n_tiles, cudaStream_t st, const CUtensorMap* a2 = nullptr);
 // cluster groups of the persistent GEMM: n_tiles clusters sweep one 256-row
 // block of one problem in lockstep, groups of them run side by side
 uint32_t gemm_groups(uint32_t n_tiles);

@@ -429,3 +429,19 @@ def test_rotation_pair_gemm_modes(mode, be, var, l):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("be,l,r,persons,s", [(O.SHAMIR, 1024, 3, 1, 300), (O.REPLICATED, 512, 5, 3, 257),
+                                              (O.SHAMIR, 2048, 31, 1, 1)])
+def test_rotation_pair_gemm_shapes(be, l, r, persons, s):
+    """Rotation-pair GEMMs at other rotation counts (an odd number of pairs' last
+    rotation dropped), one person, a one-row DB: shares through the MSB and the
+    opened bits identical to the oracle."""
+    dc, dm, qc, qm = _inputs(l, s, persons, 77, False, True, 0.9)
+    m, sess, taps, n = _gpu(be, l, 0.375, r, 77, dc, dm, qc, qm, persons, False)
+    ref = O.run_local(O.make_config(be, l, 0.375, r, debug_rows=True), 77, dc, dm, qc, qm, persons, want_all=True)
+    for k in ("dot_hd", "dot_ml", "rs_hd", "rs_ml", "diff", "msb"):
+        np.testing.assert_array_equal(taps[k], getattr(ref, k), err_msg=k)
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+    np.testing.assert_array_equal(m, ref.person_match)
+    assert sess.last_stats.rotation_pair_gemm == 1

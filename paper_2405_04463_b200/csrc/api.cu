@@ -318,8 +318,7 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
       cudaGetLastError();  // out of memory is not sticky: clear it and run without RP
       continue;
     }
-    launch_rp_sum(f.db.as<uint8_t>(), ((uint64_t)f.nparty << 40) | c->s_pad, c->l, c->l_pad, f.fmt.limbs,
-                  f.sdb.as<uint8_t>(), c->st);
+    launch_rp_sum(f.db.as<uint8_t>(), f.nparty, c->s_pad, c->l, c->l_pad, f.fmt.limbs, f.sdb.as<uint8_t>(), c->st);
     CK(c, cudaGetLastError());
     if (make_plane_tmap(&f.tS, f.sdb.p, rows, c->l / 2, kGemmBM))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the RP sum planes");

@@ -72,7 +72,7 @@ void launch_parse_query_field(const uint8_t* q1, const uint8_t* q2, const uint8_
                               uint32_t l, uint32_t l_pad, uint32_t rot, uint32_t ncols_pad, int shamir,
                               const FieldFmt& f, uint8_t* planes, cudaStream_t st);
 // RP: S = E + O (mod 2^(8 limbs)) of every DB plane row -> splanes[(c * limbs + limb) * s_pad + row][l / 2]
-void launch_rp_sum(const uint8_t* planes, uint64_t nrows_total, uint32_t l, uint32_t l_pad, int limbs,
+void launch_rp_sum(const uint8_t* planes, uint64_t ncomp, uint64_t s_pad, uint32_t l, uint32_t l_pad, int limbs,
                    uint8_t* splanes, cudaStream_t st);
 // RP query planes: kinds D0 / M / D1 of the rotation pairs, rows
 // [(((kind * 3 + p) * nseg + seg) * limbs + limb) * ncols_pad + code * npr + jp][l / 2]

@@ -151,6 +151,7 @@ struct ThrArgs {
   const Seg* segs;
   uint32_t nsegs;
   uint64_t ntasks, ngrp, ngblk;
+  uint32_t ks_seg_threads;  // k_gate_keystream: max over the job's segments of 3 * ngates * blocks per row
   int variant;
   const void* hd[3];     // additive hd dots, u16 (KH = 16) or u32
   const void* ml[3];     // additive ml dots (u16 / u32), or the public popcount (u16, all three equal)

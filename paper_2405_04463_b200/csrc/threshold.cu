@@ -122,15 +122,14 @@ __device__ __forceinline__ GroupCtx group_ctx(const ThrArgs& A, uint64_t gtid) {
 // at word 8 j, i.e. word e at row + (e - E) + (E & 7).  Every block is a full,
 // 64-byte-aligned 8-word store (padding words are never read): 16-byte vector
 // stores instead of 8 strided u64 stores per thread (-32% on the ChaCha rate,
-// measured).  thread -> (segment, seed k, gate g, block j)
+// measured).  block z -> segment, thread -> (seed k, gate g, block j)
 __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ ThrArgs A) {
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (tid >= A.ngblk) return;
-  const uint32_t si = seg_search(A.segs, A.nsegs, tid, A.ngblk, [](const Seg& s) { return s.gblk_begin; });
-  const Seg& sg = A.segs[si];
+  // grid: (blocks over one segment's (k, g, j) threads, 1, segment) -- no segment search
+  const Seg& sg = A.segs[blockIdx.z];
   const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
   const uint32_t nb = (uint32_t)(nw / 8 + 2);  // blocks per (k, g) row
-  const uint32_t local = (uint32_t)(tid - sg.gblk_begin);
+  const uint32_t local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= 3u * A.ngates * nb) return;
   const uint32_t j = local % nb;
   const uint32_t kg = local / nb;
   const int k = kg / A.ngates, g = kg % A.ngates;
@@ -707,7 +706,7 @@ void launch_rp_tap(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncol
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   if (!a.ntasks) return;
   void* h = prof_begin(st);
-  k_gate_keystream<<<(unsigned)((a.ngblk + 255) / 256), 256, 0, st>>>(a);
+  k_gate_keystream<<<dim3((a.ks_seg_threads + 255) / 256, 1, a.nsegs), 256, 0, st>>>(a);
   prof_end(h, "k_gate_keystream", st);
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);

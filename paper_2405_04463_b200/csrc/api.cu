@@ -614,7 +614,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
 
   // ---- segments [chunk][col] then the pair segment; jobs group segments
   struct Job {
-    uint64_t seg0, nseg, ntasks, ngrp, ngblk, gwords, chunk, ks_seg;
+    uint64_t seg0, nseg, ntasks, ngrp, ngblk, gwords, chunk, ks_seg, grp_seg, task_seg;
     bool pair;
   };
   std::vector<Job> jobs;
@@ -622,7 +622,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   if (ensure_host_segs(c, nsegs_all + 1)) return IRISMPC_GPU_ERR_DEVICE;
   if (c->segs.ensure((nsegs_all + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
   auto add_job = [&](uint64_t seg0, uint64_t nseg, bool pair, uint64_t chunk) {
-    Job j{seg0, nseg, 0, 0, 0, 0, chunk, 0, pair};
+    Job j{seg0, nseg, 0, 0, 0, 0, chunk, 0, 0, 0, pair};
     for (uint64_t i = seg0; i < seg0 + nseg; ++i) {
       Seg& sg = c->h_segs_pinned[i];
       sg.q_first = sg.lane_begin / 1024;
@@ -634,6 +634,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
       j.ntasks += seg_tasks(sg.lane_begin, sg.lane_end);
       j.ngrp += (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
+      j.task_seg = std::max<uint64_t>(j.task_seg, seg_tasks(sg.lane_begin, sg.lane_end));
+      j.grp_seg = std::max<uint64_t>(j.grp_seg, (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1);
       j.ngblk += 3ull * ngates * (nw / 8 + 2);
       j.ks_seg = std::max<uint64_t>(j.ks_seg, 3ull * ngates * (nw / 8 + 2));
       j.gwords += 3ull * ngates * gate_row_words(nw);
@@ -741,6 +743,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.ngrp = j.ngrp;
     t.ngblk = j.ngblk;
     t.ks_seg_threads = (uint32_t)j.ks_seg;
+    t.grp_seg_max = (uint32_t)j.grp_seg;
+    t.task_seg_max = (uint32_t)j.task_seg;
     t.bits = (lane ? c->bits2 : c->bits).as<uint32_t>();
     t.gate = (lane ? c->gate2 : c->gate).as<uint64_t>();
     t.nbits = j.ntasks * 32;

@@ -152,6 +152,8 @@ struct ThrArgs {
   uint32_t nsegs;
   uint64_t ntasks, ngrp, ngblk;
   uint32_t ks_seg_threads;  // k_gate_keystream: max over the job's segments of 3 * ngates * blocks per row
+  uint32_t grp_seg_max;     // max 8-lane groups of one segment (reshare / inject grid)
+  uint32_t task_seg_max;    // max 1024-lane tasks of one segment (lift / msb grid)
   int variant;
   const void* hd[3];     // additive hd dots, u16 (KH = 16) or u32
   const void* ml[3];     // additive ml dots (u16 / u32), or the public popcount (u16, all three equal)

@@ -59,34 +59,6 @@ __device__ __forceinline__ void and3(const uint32_t x[3], const uint32_t y[3], c
   }
 }
 
-// last segment with key(seg) <= x, x < total.  The segments of a job are
-// near-uniform (one DB column of a row chunk each), so an interpolated guess
-// followed by a local walk touches 1-3 entries instead of a ~10-step binary
-// search: those dependent loads miss L1 when the co-resident GEMM's 193 KB of
-// shared memory shrinks the L1 carve-out.
-template <typename F>
-__device__ __forceinline__ uint32_t seg_search(const Seg* segs, uint32_t nsegs, uint64_t x, uint64_t total, F key) {
-  uint64_t guess = (uint64_t)((double)x * nsegs / (double)total);
-  uint32_t i = guess < nsegs ? (uint32_t)guess : nsegs - 1;
-  uint32_t lo = 0, hi = nsegs - 1;
-  for (int it = 0; it < 4; ++it) {  // local walk, then binary search in the remaining bracket
-    if (key(segs[i]) > x) {
-      hi = i - 1;
-      i = i - 1;
-    } else if (i + 1 < nsegs && key(segs[i + 1]) <= x) {
-      lo = i + 1;
-      i = i + 1;
-    } else {
-      return i;
-    }
-  }
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (key(segs[mid]) <= x) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 __device__ __forceinline__ uint64_t gate_base(const ThrArgs& A, int k, int g) {
   if ((uint32_t)g < A.nlift) return A.lift_base[k] + (uint64_t)g * A.W;
   return A.msb_base[k] + (uint64_t)(g - (int)A.nlift) * A.W;
@@ -100,18 +72,21 @@ struct GroupCtx {
   const Seg* sg;
 };
 
-__device__ __forceinline__ GroupCtx group_ctx(const ThrArgs& A, uint64_t gtid) {
-  GroupCtx c;
-  const int lane = (int)(gtid & 31);
-  const uint64_t gi = (gtid >> 5) * 31 + lane;
-  c.mine = lane < 31 && gi < A.ngrp;
-  const uint64_t gq = gi < A.ngrp ? gi : A.ngrp - 1;
-  const uint32_t si = seg_search(A.segs, A.nsegs, gq, A.ngrp, [](const Seg& s) { return s.grp_begin; });
-  c.sg = &A.segs[si];
-  c.L8 = (c.sg->lane_begin / 8 + (gq - c.sg->grp_begin)) * 8;
-  const uint64_t Ln = __shfl_down_sync(0xFFFFFFFFu, c.L8, 1);
-  c.next_contig = lane == 31 || (Ln == c.L8 + 8 && gi + 1 < A.ngrp);
-  return c;
+// 3-D grids: blockIdx.z = segment, so no search; warp w of block x owns the
+// segment's 8-lane groups [(x * warps + w) * 31, + 31).  Returns false when the
+// whole warp lies past the segment (warp-uniform).
+__device__ __forceinline__ bool group_ctx(const ThrArgs& A, GroupCtx& c) {
+  const int lane = threadIdx.x & 31;
+  c.sg = &A.segs[blockIdx.z];
+  const uint64_t g0 = c.sg->lane_begin / 8;
+  const uint64_t ng = (c.sg->lane_end - 1) / 8 - g0 + 1;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 31;
+  if (w0 >= ng) return false;
+  const uint64_t gi = w0 + lane;
+  c.mine = lane < 31 && gi < ng;
+  c.L8 = (g0 + (gi < ng ? gi : ng - 1)) * 8;
+  c.next_contig = lane == 31 || gi + 1 < ng;
+  return true;
 }
 
 }  // namespace
@@ -229,9 +204,8 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
-  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if ((gtid >> 5) * 31 >= A.ngrp) return;  // whole warp past the end
-  const GroupCtx gc = group_ctx(A, gtid);
+  GroupCtx gc;
+  if (!group_ctx(A, gc)) return;  // whole warp past the segment
   const Seg& sg = *gc.sg;
   const uint64_t L8 = gc.L8;
   const uint64_t src0 = sg.src + (L8 - sg.lane_begin);  // valid only when `full`
@@ -346,15 +320,17 @@ struct TaskCtx {
   uint64_t task, L0, vb, ve;
 };
 
-__device__ __forceinline__ TaskCtx task_ctx(const ThrArgs& A, uint64_t task) {
-  TaskCtx t;
-  const uint32_t si = seg_search(A.segs, A.nsegs, task, A.ntasks, [](const Seg& s) { return s.task_begin; });
-  t.sg = A.segs[si];
-  t.task = task;
-  t.L0 = (t.sg.q_first + (task - t.sg.task_begin)) * 1024;
+// blockIdx.z = segment, warp -> the segment's 1024-lane task (false: warp past the segment)
+__device__ __forceinline__ bool task_ctx(const ThrArgs& A, TaskCtx& t) {
+  t.sg = A.segs[blockIdx.z];
+  const uint64_t nt = (t.sg.lane_end - 1) / 1024 - t.sg.lane_begin / 1024 + 1;
+  const uint64_t tl = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tl >= nt) return false;
+  t.task = t.sg.task_begin + tl;
+  t.L0 = (t.sg.q_first + tl) * 1024;
   t.vb = t.sg.lane_begin > t.L0 ? t.sg.lane_begin : t.L0;
   t.ve = t.sg.lane_end < t.L0 + 1024 ? t.sg.lane_end : t.L0 + 1024;
-  return t;
+  return true;
 }
 
 // this thread's 32 lanes [Lt, Lt+32) as a valid-lane mask
@@ -442,10 +418,10 @@ __device__ __forceinline__ void extract_bit(const ThrArgs& A, const Seg& sg, uin
 
 // warp -> 1024-lane task, thread -> 32 lanes
 __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ ThrArgs A) {
-  const uint64_t task = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (task >= A.ntasks) return;
-  const TaskCtx t = task_ctx(A, task);
+  TaskCtx t;
+  if (!task_ctx(A, t)) return;
+  const uint64_t task = t.task;
   const uint64_t Lt = t.L0 + 32ull * lane;
   const uint32_t vm = valid_mask(t, Lt);
   if (vm == 0) return;  // lanes outside the segment: no gate randomness was generated for them
@@ -494,9 +470,8 @@ __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ T
 
 // thread -> 8-lane group: bit_inject<15>(bit17) then bit_inject<16>(bit16)
 __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs A) {
-  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if ((gtid >> 5) * 31 >= A.ngrp) return;  // whole warp past the end
-  const GroupCtx gc = group_ctx(A, gtid);
+  GroupCtx gc;
+  if (!group_ctx(A, gc)) return;  // whole warp past the segment
   const Seg& sg = *gc.sg;
   const uint64_t L8 = gc.L8;
   // injected bits: the k_lift thread that owns these lanes
@@ -624,10 +599,10 @@ __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t 
 // fused first OR level.  Gates: FA j -> nlift + j, chain t -> nlift + KC - 1 + (t - 1).
 template <int KC>
 __global__ void __launch_bounds__(128, MSB_LB) k_msb(const __grid_constant__ ThrArgs A) {
-  const uint64_t task = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (task >= A.ntasks) return;
-  const TaskCtx t = task_ctx(A, task);
+  TaskCtx t;
+  if (!task_ctx(A, t)) return;
+  const uint64_t task = t.task;
   const uint64_t Lt = t.L0 + 32ull * lane;
   const uint32_t vm = valid_mask(t, Lt);
   uint32_t D[3][32];
@@ -711,8 +686,9 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
-  const unsigned grp_blocks = (unsigned)((a.ngrp + 8 * 31 - 1) / (8 * 31));
-  const unsigned rb = grp_blocks;
+  const dim3 grp_blocks((a.grp_seg_max + 8 * 31 - 1) / (8 * 31), 1, a.nsegs);
+  const dim3 rb = grp_blocks;
+  const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
   switch (a.variant) {
     case kPlainMask: k_reshare<kPlainMask><<<rb, 256, 0, st>>>(a); break;
     case kMpcLift: k_reshare<kMpcLift><<<rb, 256, 0, st>>>(a); break;
@@ -723,7 +699,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_reshare", st);
   if (a.variant == kMpcLift) {
     h = prof_begin(st);
-    k_lift<<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+    k_lift<<<task_blocks, 128, 0, st>>>(a);
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
@@ -733,9 +709,9 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   }
   h = prof_begin(st);
   if (a.variant == kPlainMask)
-    k_msb<16><<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+    k_msb<16><<<task_blocks, 128, 0, st>>>(a);
   else
-    k_msb<32><<<(unsigned)((a.ntasks * 32 + 127) / 128), 128, 0, st>>>(a);
+    k_msb<32><<<task_blocks, 128, 0, st>>>(a);
   prof_end(h, "k_msb", st);
   debug_check("k_msb", st);
 }

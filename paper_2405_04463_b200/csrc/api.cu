@@ -464,9 +464,11 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   debug_check("k_parse_query_rp", st);
   CK(c, cudaGetLastError());
-  if (npairs) {
-    // pair dots as one limb GEMM per field: A = the unrotated query codes in the
-    // DB plane layout, B = the rotated query planes (see pairs.cu)
+  // pair dots as one limb GEMM per field: A = the unrotated query codes in the DB
+  // plane layout, B = the rotated query planes (see pairs.cu).  Queued on st after
+  // the DB chunks' GEMMs: the threshold chain needs them only at its end, and
+  // chunk 0's GEMM starts earlier.
+  auto pair_gemm = [&]() -> int {
     const uint64_t spq = round_up(ncodes, 2 * kGemmBM);
     if (c->pair_dots.ensure(npairs * (3 * hb + fm.nparty * mb) + 64))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
@@ -501,7 +503,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     prof_end(ph, "pairs (gemm+gather)", st);
     debug_check("pairs", st);
     CK(c, cudaGetLastError());
-  }
+    return 0;
+  };
   CK(c, cudaEventRecord(c->ev[1], st));
 
   if (c->taps) {
@@ -882,7 +885,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     if (two) CK(c, cudaEventRecord(c->evt3[i], st3));
   }
 
-  // ---- pair lanes (shard 0): threshold into match words
+  // ---- pair lanes (shard 0): pair GEMMs on st, then their threshold into match words on st2
+  if (npairs) {
+    const int prc = pair_gemm();
+    if (prc) return prc;
+    CK(c, cudaEventRecord(c->ev[5], st));
+    CK(c, cudaStreamWaitEvent(st2, c->ev[5], 0));
+  }
   if (two && nchunks) CK(c, cudaStreamWaitEvent(st2, c->evt3[nchunks - 1], 0));
   if (npairs) {
     const uint8_t* pd_hd = c->pair_dots.as<uint8_t>();

@@ -524,9 +524,12 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       const char* e = std::getenv("IRISMPC_CHUNK_LANES");  // test hook
       return e ? std::strtoull(e, nullptr, 10) : 0ull;
     }();
-    // 2^24 lanes per chunk; 2^25 with the rotation-pair GEMMs, whose chunks are 25% shorter
-    // (fewer chunk boundaries: -1..-2% per query at configs[1], three boxes)
-    const uint64_t target = target_env ? target_env : ((use_rp[0] || use_rp[1]) ? (1ull << 25) : (1ull << 24));
+    // 2^24 lanes per chunk; with the rotation-pair GEMMs, whose chunks are 25% shorter, 2^25 and at
+    // least 16384 rows (wide batches: longer segments, fewer partial 1024-lane threshold tasks;
+    // -1..-2% at configs[1], -5% at 128 / 256 codes)
+    const bool rp_any = use_rp[0] || use_rp[1];
+    const uint64_t target = target_env ? target_env
+                                       : (rp_any ? std::max<uint64_t>(1ull << 25, 16384ull * ncols) : (1ull << 24));
     // Row granule: a chunk's (problem, 256-row block) units should fill whole
     // waves of the persistent GEMM's cluster groups, for every field.
     uint64_t granule = 2 * kGemmBM;

@@ -527,14 +527,15 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     // 2^24 lanes per chunk; with the rotation-pair GEMMs, whose chunks are 25% shorter, 2^25 and at
     // least 16384 rows (wide batches: longer segments, fewer partial 1024-lane threshold tasks;
     // -1..-2% at configs[1], -5% at 128 / 256 codes)
-    // Plain GEMM: 2^24 lanes, up to 2^26 on large DBs (at least 32 chunks; 1M rows x 64 codes:
-    // 458 -> 430 ms per query, the per-chunk threshold ramp-up paid 4x less often)
+    // Plain GEMM: 2^24 lanes, up to 2^26 on large DBs (at least 16 chunks; 1M rows x 64 codes:
+    // 458 -> 430 ms per query, the per-chunk threshold ramp-up paid 4x less often; x 32 codes -1.3%,
+    // x 8 codes +4% with 2^26, so small batches keep 2^24)
     const bool rp_any = use_rp[0] || use_rp[1];
     const uint64_t lanes_all = s_loc * ncols;
     const uint64_t target =
         target_env ? target_env
         : rp_any   ? std::max<uint64_t>(1ull << 25, 16384ull * ncols)
-                   : std::min<uint64_t>(1ull << 26, std::max<uint64_t>(1ull << 24, lanes_all / 32));
+                   : std::min<uint64_t>(1ull << 26, std::max<uint64_t>(1ull << 24, lanes_all / 16));
     // Row granule: a chunk's (problem, 256-row block) units should fill whole
     // waves of the persistent GEMM's cluster groups, for every field.
     uint64_t granule = 2 * kGemmBM;

@@ -143,6 +143,10 @@ struct FieldPlanes {
   Buf sdb, rpq;
   CUtensorMap tS, tRP;
   bool rpg = false;  // S planes resident: rotated queries run the RP GEMMs
+  bool rpc = false;  // S planes built per row chunk into sch (DB too large for resident S)
+  Buf sch;
+  CUtensorMap tSc;
+  uint64_t sch_spad = 0;
   uint32_t rp_ncols_cur = 0;
   uint32_t bn() const { return gemm_bn((uint32_t)fmt.limbs); }
   void release() {
@@ -152,7 +156,10 @@ struct FieldPlanes {
     pair_c.release();
     sdb.release();
     rpq.release();
+    sch.release();
     rpg = false;
+    rpc = false;
+    sch_spad = 0;
     rp_ncols_cur = 0;
     ncols_pad_cur = 0;
     qa_spad = 0;
@@ -307,9 +314,17 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     const char* e = std::getenv("IRISMPC_RP");
     return e && std::string(e) == "layout";
   }();
+  // opt-in: per-chunk S planes when resident ones do not fit ("force": always, tests)
+  static const int rp_chunked = [] {
+    const char* e = std::getenv("IRISMPC_RP_CHUNKED");
+    return !e || std::string(e) == "0" ? 0 : std::string(e) == "force" ? 2 : 1;
+  }();
   for (auto& f : c->fld) {
     f.rpg = false;
+    f.rpc = false;
     if (!f.fmt.rp || rp_layout_only) continue;
+    f.rpc = rp_chunked != 0;
+    if (rp_chunked == 2) continue;
     const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
     // keep 16 GB free for the query's work buffers (dots, gate keystream, planes)
     size_t free_b = 0, total_b = 0;
@@ -323,6 +338,7 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     if (make_plane_tmap(&f.tS, f.sdb.p, rows, c->l / 2, kGemmBM))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the RP sum planes");
     f.rpg = true;
+    f.rpc = false;
   }
   CK(c, cudaStreamSynchronize(c->st));
   c->db_loaded = true;
@@ -447,7 +463,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   bool use_rp[2] = {false, false};
   for (int fi = 0; fi < 2; ++fi) {
     FieldPlanes& f = c->fld[fi];
-    use_rp[fi] = !membership && r >= 3 && f.rpg && s_loc > 0;
+    use_rp[fi] = !membership && r >= 3 && (f.rpg || f.rpc) && s_loc > 0;
     if (!use_rp[fi]) continue;
     const uint64_t rows = 9ull * f.nseg * f.fmt.limbs * ncols_rp_pad;  // 3 kinds x 3 parties
     const size_t bytes = rows * (c->l / 2);
@@ -712,6 +728,21 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                  c->bits2.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
+  // per-chunk S planes (IRISMPC_RP_CHUNKED): one scratch per field, reused chunk after chunk on
+  // the GEMM stream (k_rp_sum of chunk i+1 is queued behind chunk i's GEMM)
+  for (int fi = 0; fi < 2; ++fi) {
+    FieldPlanes& f = c->fld[fi];
+    if (!use_rp[fi] || f.rpg) continue;
+    uint64_t spad = 0;
+    for (uint64_t i = 0; i < nchunks; ++i) spad = std::max<uint64_t>(spad, round_up(chunk_rows(i), 2 * kGemmBM));
+    if (spad > f.sch_spad) {
+      const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * spad;
+      if (f.sch.ensure(rows * (c->l / 2))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (per-chunk RP sum planes)");
+      if (make_plane_tmap(&f.tSc, f.sch.p, rows, c->l / 2, kGemmBM))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the per-chunk RP sum planes");
+      f.sch_spad = spad;
+    }
+  }
 
   ThrArgs ta{};
   ta.variant = V;
@@ -837,7 +868,15 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         g.out_pstride = ncols_rp * nr;
         g.out_kstride = 3 * ncols_rp * nr;
         g.out_cstride = (uint32_t)nr;
-        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st, &f.tS);
+        if (!f.rpg) {  // per-chunk S planes: E + O of this chunk's rows, then the GEMM (same stream)
+          const uint64_t nrs = std::min<uint64_t>(round_up(nr, 2 * kGemmBM), c->s_pad - chunk_row0[i]);
+          launch_rp_sum_rows(f.db.as<uint8_t>(), f.nparty, c->s_pad, chunk_row0[i], nrs, f.sch_spad, c->l,
+                             c->l_pad, f.fmt.limbs, f.sch.as<uint8_t>(), st);
+          ++launches;
+          g.s_pad2 = (uint32_t)f.sch_spad;
+          g.row0_2 = 0;
+        }
+        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st, f.rpg ? &f.tS : &f.tSc);
         ++gemm_launches;
         ++launches;
       } else {

@@ -148,6 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
       const void* ta = kind == 1 ? (const void*)&tA2 : (const void*)&tA;
       const uint32_t akb = kind == 2 ? g.a_kb0_k2 : g.a_kb0;
+      const bool s_scratch = kind == 1 && g.s_pad2 != 0;  // per-chunk S planes
+      const uint32_t a_spad = s_scratch ? g.s_pad2 : g.s_pad, a_row0 = s_scratch ? g.row0_2 : g.row0;
       const uint32_t brow0 = g.b_row0 + kind * g.b_kind_rows;
       for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t stage = it % STAGES;
@@ -164,8 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const uint32_t fb = mapa_shared(&full[stage], 0);
 #pragma unroll
           for (int limb = 0; limb < L; ++limb) {
-            const int32_t arow =
-                (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
+            const int32_t arow = (int32_t)((pa * L + limb) * a_spad + a_row0 + m_pair * 256 + rank * 128);
             const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
                                            n_tile * BN + rank * (BN / 2));
             tma_load_2d_pair(st + limb * T::A_T, ta, fb, (int32_t)((akb + kk) * BK), arow);

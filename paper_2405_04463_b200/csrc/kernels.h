@@ -74,6 +74,9 @@ void launch_parse_query_field(const uint8_t* q1, const uint8_t* q2, const uint8_
 // RP: S = E + O (mod 2^(8 limbs)) of every DB plane row -> splanes[(c * limbs + limb) * s_pad + row][l / 2]
 void launch_rp_sum(const uint8_t* planes, uint64_t ncomp, uint64_t s_pad, uint32_t l, uint32_t l_pad, int limbs,
                    uint8_t* splanes, cudaStream_t st);
+// S = E + O for DB rows [row0, row0 + nrows) into a scratch of out_spad rows per plane
+void launch_rp_sum_rows(const uint8_t* planes, uint64_t ncomp, uint64_t s_pad, uint64_t row0, uint64_t nrows,
+                        uint64_t out_spad, uint32_t l, uint32_t l_pad, int limbs, uint8_t* splanes, cudaStream_t st);
 // RP query planes: kinds D0 / M / D1 of the rotation pairs, rows
 // [(((kind * 3 + p) * nseg + seg) * limbs + limb) * ncols_pad + code * npr + jp][l / 2]
 void launch_parse_query_rp(const uint8_t* q1, const uint8_t* q2, const uint8_t* q3, uint32_t ncodes, uint32_t l,
@@ -113,6 +116,10 @@ struct GemmArgs {
   uint32_t a_kb0_k2 = 0;
   uint32_t b_kind_rows = 0;   // B rows per kind
   uint64_t out_kstride = 0;   // output elements per kind
+  // kind-1 A rows (S planes) when they live in a per-chunk scratch: rows per plane and first row
+  // (0 = the DB planes' s_pad / row0, resident S planes)
+  uint32_t s_pad2 = 0;
+  uint32_t row0_2 = 0;
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }

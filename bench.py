@@ -1,9 +1,10 @@
 #!/usr/bin/env python3
 """Benchmark: iris comparisons/sec of the full 3-party mpc-lift query on B200.
 
-A step is one complete batch query of BASELINE.json configs[1]: 32 query eye
-codes (16 persons) x 31 rotations against a 100k-row synthetic DB per GPU,
-12800-bit codes + masks, all three parties' shares resident in HBM:
+A step is one complete batch query of BASELINE.json configs[2] (the largest
+single-GPU config): 64 query eye codes (32 persons) x 31 rotations against a
+1M-row synthetic DB per GPU, 12800-bit codes + masks, all three parties'
+shares resident in HBM (153.6 GB):
 query-share broadcast -> K1 prep -> K2 tcgen05 limb GEMMs -> K4 threshold
 (reshare, lift, MSB) -> K5 MPC-OR -> open of one bit per person at P1.
 comparisons = codes * 31 * DB rows (inner-batch pair lanes are computed but
@@ -29,8 +30,10 @@ sys.path.insert(0, ROOT)
 
 L = 12800
 ROT = 31
-PERSONS = 16            # 32 eye codes
-ROWS_PER_GPU = 100_000  # configs[1]
+PERSONS = 32              # 64 eye codes (configs[2]; configs[1] = --persons 16 --rows 100000)
+ROWS_PER_GPU = 1_000_000  # configs[2]
+REF_ROWS = 10_000         # configs[0]: 1 person (2 codes) x 31 rotations vs 10k rows, the CPU-runnable case
+CPU_STEPS = 5
 METRIC = "iris comparisons/sec (query x rotation x DB)"
 UNIT = "comparisons/s"
 VARIANTS = {"plain-mask": 0, "mpc-lift": 1, "const-lift": 2, "no-lift": 3}
@@ -58,6 +61,20 @@ def prf_blocks_per_lane(variant: int = 1) -> float:
     inject = 1.0 if variant == 1 else 0.0
     gates = {0: 29, 1: 125, 2: 61, 3: 61}[variant]
     return reshare + inject + gates * 3 / 512
+
+
+def workload_name(rows: int, persons: int, world: int) -> str:
+    """Which BASELINE.json config this shape is (configs[1]/[2] on one GPU; the
+    sharded runs are configs[3]'s 1M rows/GPU weak-scaling series)."""
+    if world == 1 and rows == 1_000_000 and persons == 32:
+        return "configs[2]"
+    if world == 1 and rows == 100_000 and persons == 16:
+        return "configs[1]"
+    if world == 1 and rows == 10_000 and persons == 1:
+        return "configs[0]"
+    if world > 1 and persons == 32:
+        return f"configs[3] weak-scaling series ({rows} rows per GPU x {world} GPUs = {rows * world} rows)"
+    return "custom shape"
 
 
 def env_rank():
@@ -154,44 +171,68 @@ def ncu_traffic(rp: bool = False):
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_reference_rate(backend: int, rows: int, persons: int, steps: int, variant: int = 1):
+def cpu_reference_rates(backends, rows: int, persons: int, steps: int, variant: int = 1, warmup: int = 0):
     """The reference (oracle/_ref, compiled from the reference sources) on the
-    host cores: run_parties + party_batch_query per step; QueryStats.wall_ms."""
+    host cores: run_parties + party_batch_query per step (the stock per-party
+    path, which re-parses the DB payload every call), timed by the reference's
+    own QueryStats.wall_ms (run_schedule).  Median of `steps` after `warmup`
+    untimed steps, per backend.  Dealing (prepare) runs once per backend, the
+    backends' dealers concurrently (ctypes releases the GIL)."""
     from oracle import pyoracle as O
     import ctypes as C
+    import threading
     cores = os.cpu_count() or 1
-    if O.ref_available():
-        # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, and the
-        # reference's OpenMP dot loop (libgomp) would otherwise run on one core
-        os.environ["OMP_NUM_THREADS"] = str(cores)
-        R = O.ref()
-        try:
-            C.CDLL("libgomp.so.1").omp_set_num_threads(C.c_int(cores))
-        except OSError:
-            pass
-        h = R.ref_bench_prepare(backend, variant, L, rows, persons)
-        times = []
+    out = {}
+    if not O.ref_available():  # port: the C restatement, single thread
+        for be in backends:
+            rng = O.Rng(2)
+            dc, dm = O.records(rng, L, rows, 0.9)
+            qc, qm = O.records(rng, L, 2 * persons, 0.9)
+            cfg = O.make_config(be, L, variant=variant)
+            times = []
+            for _ in range(max(1, steps)):
+                t0 = time.perf_counter()
+                O.run_local(cfg, 7, dc, dm, qc, qm, persons)
+                times.append((time.perf_counter() - t0) * 1e3)
+            ms = statistics.median(times)
+            out[be] = {"value": 2 * persons * ROT * rows / (ms / 1e3), "unit": UNIT, "cores": 1, "kind": "port",
+                       "ms": ms, "sample": f"oracle C port incl. dealing: {2 * persons} codes x {ROT} rot x "
+                                           f"{rows} rows, median of {len(times)} steps"}
+        return out
+    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, and the
+    # reference's OpenMP dot loop (libgomp) would otherwise run on one core
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    R = O.ref()
+    try:
+        C.CDLL("libgomp.so.1").omp_set_num_threads(C.c_int(cores))
+    except OSError:
+        pass
+    handles = {}
+
+    def prep(be):
+        handles[be] = R.ref_bench_prepare(be, variant, L, rows, persons)
+
+    th = [threading.Thread(target=prep, args=(be,)) for be in backends]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for be in backends:
+        h = handles[be]
         m0 = C.c_uint8(0)
-        for _ in range(steps):
-            times.append(R.ref_bench_step(h, C.byref(m0)))
+        for _ in range(warmup):
+            R.ref_bench_step(h, C.byref(m0))
+        times = [R.ref_bench_step(h, C.byref(m0)) for _ in range(max(1, steps))]
         R.ref_bench_free(h)
         ms = statistics.median(times)
-        cmp_ = 2 * persons * ROT * rows
-        return {"value": cmp_ / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"reference run_batch (oracle/_ref, OpenMP parallel_dot, all {cores} host threads): "
-                          f"{2 * persons} codes x {ROT} rot x {rows} rows, median of {steps} steps of "
-                          f"QueryStats.wall_ms={ms:.0f} ms; linear in rows",
-                "planted_match": int(m0.value)}
-    # port: the C restatement, single thread
-    rng = O.Rng(2)
-    dc, dm = O.records(rng, L, rows, 0.9)
-    qc, qm = O.records(rng, L, 2 * persons, 0.9)
-    cfg = O.make_config(backend, L, variant=variant)
-    t0 = time.perf_counter()
-    O.run_local(cfg, 7, dc, dm, qc, qm, persons)
-    dt = time.perf_counter() - t0
-    return {"value": 2 * persons * ROT * rows / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle C port incl. dealing: {2 * persons} codes x {ROT} rot x {rows} rows"}
+        name = "shamir" if be == 1 else "replicated"
+        out[be] = {"value": 2 * persons * ROT * rows / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
+                   "ms": ms, "planted_match": int(m0.value),
+                   "sample": f"reference run_parties + party_batch_query (oracle/_ref, OpenMP parallel_dot, all "
+                             f"{cores} host threads), {name} backend, {2 * persons} codes x {ROT} rot x {rows} rows "
+                             f"(configs[0] shape), median of {len(times)} steps of QueryStats.wall_ms = {ms:.0f} ms; "
+                             f"linear in rows"}
+    return out
 
 
 def run_reference_arm(args):
@@ -200,43 +241,87 @@ def run_reference_arm(args):
         return 0
     backend = 1 if args.backend == "shamir" else 0
     rows = args.ref_rows
-    for _ in range(args.warmup and 1):
-        pass
     variant = VARIANTS[args.variant]
-    res = cpu_reference_rate(backend, rows, 1, max(1, args.steps), variant)
+    res = cpu_reference_rates([backend], rows, 1, max(1, args.steps), variant, warmup=args.warmup)[backend]
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 2 * ROT * rows / res["value"] * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"cfg2-shape sample: 1 person (2 codes) x {ROT} rot x {rows} rows, "
-                                   f"l={L}, {args.variant}, {args.backend}", "l": L, "rotations": ROT,
-                       "variant": args.variant},
+            "config": {"workload": f"configs[0]: 1 person (2 codes) x {ROT} rot x {rows} rows, l={L}, "
+                                   f"3-party {args.variant}, {args.backend} backend (the reference's CPU-runnable "
+                                   f"config; comparisons/s is linear in rows)", "l": L, "rotations": ROT,
+                       "variant": args.variant, "backend": args.backend, "db_rows": rows, "persons": 1},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def compare_roofline(span_ms: float, lanes: int, variant: int, peaks: dict) -> dict:
-    """The compare/reduce phase (reshare -> lift -> MSB -> OR) against both of
-    its ceilings over the threshold stream's span: HBM at the SURVEY §8d
-    algorithmic 12.75 B/lane, and the ALU pipe as ChaCha12 blocks/s against the
-    measured keystream rate (profiles/chacha_peak.json).  The PRF layout is the
-    reference's (2.48 blocks/lane for mpc-lift), so the phase is ALU-bound."""
-    sec = max(span_ms, 1e-9) / 1e3
-    hbm = ALG_BYTES_PER_LANE * lanes / sec / 1e9
-    blocks = prf_blocks_per_lane(variant) * lanes
+THRESHOLD_KERNELS = ("k_gate_keystream", "k_reshare", "k_lift", "k_inject", "k_msb")
+
+
+def kernel_blocks_per_lane(name: str, variant: int = 1) -> float:
+    """ChaCha12 blocks per comparison lane each threshold kernel computes (the
+    reference-exact PRF): the gate keystream 3 seeds x 125 (61/29)
+    gates per 64-lane word, reshare 3 seeds x 2 (1) dots, inject 2 x (1 + 3) u64."""
+    if name == "k_gate_keystream":
+        return {0: 29, 1: 125, 2: 61, 3: 61}[variant] * 3 / 512
+    if name == "k_reshare":
+        return 3 * (1 if variant == 0 else 2) / 8
+    if name == "k_inject":
+        return 1.0 if variant == 1 else 0.0
+    return 0.0
+
+
+def ncu_threshold_bytes():
+    """per-kernel DRAM bytes per lane from the committed ncu --set full capture"""
+    p = os.path.join(ROOT, "profiles", "threshold_ncu.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d.get("dram_bytes_per_lane", {}), d.get("source")
+        except Exception:
+            return {}, None
+    return {}, None
+
+
+def compare_roofline(prof: dict, lanes: int, variant: int, peaks: dict) -> dict:
+    """The compare/reduce phase (reshare -> lift -> MSB -> OR) against its two
+    ceilings, kernel by kernel, from one SERIALISED profiled query (each kernel
+    timed alone with CUDA events, `Session.profile`): ChaCha12 blocks/s against
+    the measured keystream rate (profiles/chacha_peak.json), and DRAM bytes per
+    lane (ncu, profiles/threshold_ncu.json) against SURVEY §8d's algorithmic
+    12.75 B/lane for the whole phase.  The PRF layout is the reference's, so the
+    phase is ALU (ChaCha) bound; `chain.frac` = ChaCha floor / serial chain time."""
     cp = chacha_peak()
-    out = {"bound": "alu", "kernels": "k_gate_keystream, k_reshare, k_lift, k_inject, k_msb",
-           "hbm": {"achieved": hbm, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": hbm / peaks["hbm_gbs"],
-                   "alg_bytes_per_lane": ALG_BYTES_PER_LANE},
-           "chacha": {"achieved": blocks / sec, "peak": cp, "unit": "ChaCha12 blocks/s",
-                      "frac": (blocks / sec / cp) if cp else None,
-                      "blocks_per_lane": prf_blocks_per_lane(variant)},
-           "span_ms": span_ms,
-           "note": "over the threshold stream span, which overlaps the GEMM; the GEMM and the "
-                   "ChaCha work share the 1000 W power cap and do not overlap in time on the "
-                   "same SMs (DESIGN.md section 4), so the span is mostly GEMM-bound time"}
+    dram, dsrc = ncu_threshold_bytes()
+    kern = {}
+    chain_ms = 0.0
+    for k in THRESHOLD_KERNELS + ("k_or_persons",):
+        if k not in prof:
+            continue
+        ms, cnt = prof[k]
+        chain_ms += ms
+        bpl = kernel_blocks_per_lane(k, variant)
+        e = {"serial_ms": ms, "launches": cnt, "chacha_blocks_per_lane": bpl}
+        if bpl and ms > 0:
+            rate = bpl * lanes / (ms / 1e3)
+            e["chacha_blocks_per_s"] = rate
+            e["frac_of_chacha_peak"] = rate / cp if cp else None
+        if k in dram:
+            e["dram_bytes_per_lane_ncu"] = dram[k]
+        kern[k] = e
+    blocks = prf_blocks_per_lane(variant) * lanes
+    floor_ms = blocks / cp * 1e3 if cp else None
+    out = {"bound": "alu (ChaCha12)", "kernels": kern,
+           "chain": {"serial_ms": chain_ms, "chacha_floor_ms": floor_ms, "chacha_peak_blocks_per_s": cp,
+                     "blocks_per_lane": prf_blocks_per_lane(variant),
+                     "frac": (floor_ms / chain_ms) if (floor_ms and chain_ms) else None},
+           "hbm": {"alg_bytes_per_lane": ALG_BYTES_PER_LANE, "peak_gbs": peaks["hbm_gbs"],
+                   "dram_bytes_per_lane_ncu": sum(dram.get(k, 0.0) for k in THRESHOLD_KERNELS) if dram else None,
+                   "source": dsrc},
+           "note": "serial per-kernel device times of one profiled query (no GEMM overlap); in the timed "
+                   "steps these kernels overlap the GEMM on a second stream"}
     return out
 
 
@@ -356,66 +441,97 @@ def main_gpu(args):
 
     lanes_db = ncodes * ROT * S
     value = lanes_db / (ms / 1e3)
+    local_lanes = ncodes * ROT * rows
+    # one serialised, profiled query (outside the timed region): per-kernel
+    # standalone device times for the roofline lines
+    prof = {}
+    if not args.no_profile:
+        sess.profile(True)
+        sess.profile_read()
+        step(False)
+        torch.cuda.synchronize()
+        prof = sess.profile_read()
+        sess.profile(False)
     if rank == 0:
         peaks, src = load_peaks()
         gemm_ms = stats_acc["gemm_ms"] / max(1, stats_acc["gemm_launches"])
-        local_lanes = ncodes * ROT * rows
         opl = ops_per_lane(backend, variant)
         kh, km = WIDTHS[variant]
         plane_kb = L * (3 * kh // 8 + (3 * km // 8 if km else 1)) / 1e3
-        ops_launch = local_lanes * opl / max(1, stats_acc["gemm_launches"] // args.steps)
-        achieved = ops_launch / (gemm_ms / 1e3) / 1e12
-        exec_opl = stats_acc["gemm_ops"] / max(1, args.steps) / max(1, local_lanes)
-        exec_tops = stats_acc["gemm_ops"] / max(1, stats_acc["gemm_launches"]) / (gemm_ms / 1e3) / 1e12
+        launches_per_step = max(1, stats_acc["gemm_launches"] // args.steps)
+        exec_ops_launch = stats_acc["gemm_ops"] / max(1, stats_acc["gemm_launches"])
+        exec_tops = exec_ops_launch / (gemm_ms / 1e3) / 1e12
+        alg_tops = local_lanes * opl / launches_per_step / (gemm_ms / 1e3) / 1e12
         i8 = os.path.join(ROOT, "profiles", "int8_peak.json")
         if os.path.exists(i8):
             peak = json.load(open(i8))["int8_tops_burst"]
-            peak_note = "measured cuBLASLt int8 burst (profiles/int8_peak.json, tools/measure_int8_peak.py)"
+            peak_note = ("builder-measured cuBLASLt int8 8192^3 burst on this pool (profiles/int8_peak.json, "
+                         "tools/measure_int8_peak.py); MEASURED_PEAKS.json has no int8 entry "
+                         f"(2 x its bf16 burst = {2 * peaks['bf16_tflops']:.0f} TOPS)")
         else:
             peak = 2.0 * peaks["bf16_tflops"]
             peak_note = f"2 x {src} bf16 ({peaks['bf16_tflops']} TF/s); dense int8 = 2x bf16 on sm_100"
-        cpu = cpu_reference_rate(backend, args.ref_rows, 1, 1, variant) if (world == 1 and not args.no_cpu) else None
+        serial_gemm = {k: v for k, v in prof.items() if k.startswith("k_limb_gemm_pair")}
+        sg_ms = sum(v[0] for v in serial_gemm.values())
+        sg_n = sum(v[1] for v in serial_gemm.values())
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_reference_rates([backend, 1 - backend], args.ref_rows, 1, CPU_STEPS, variant)
+        wl = workload_name(rows, persons, world)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"configs[1]: {ncodes} query codes ({persons} persons) x {ROT} rotations vs "
+            "config": {"workload": f"{wl}: {ncodes} query codes ({persons} persons) x {ROT} rotations vs "
                                    f"{rows} DB rows per GPU (total {S}), l={L}, 3-party {args.variant}, "
                                    f"{args.backend} backend", "l": L, "rotations": ROT, "persons": persons,
-                       "db_rows_total": S, "db_rows_per_gpu": rows, "backend": args.backend,
+                       "codes": ncodes, "db_rows_total": S, "db_rows_per_gpu": rows, "backend": args.backend,
                        "variant": args.variant,
-                       "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM)",
+                       "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM, "
+                             f"{plane_kb * rows / 1e6:.1f} GB per GPU)",
                        "parallelism": f"db-shard x{world}"},
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons,
                     "note": "median of single queries through the public API (pinned host payloads in, "
-                            "person_match out), each bracketed by a host sync; the GPU idles between "
-                            "them, so under the 1000 W cap a single query can run at higher clocks "
-                            "than the back-to-back steps behind `value`"},
+                            "person_match out), each bracketed by a host sync"},
             "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "achieved": exec_tops, "peak": peak, "unit": "TFLOP/s", "frac": exec_tops / peak,
                          "traffic": ncu_traffic(bool(stats_acc["rp"]))[0],
                          "ncu_tensor_pipe_active_pct": ncu_traffic(bool(stats_acc["rp"]))[1],
-                         "executed": {"int8_ops_per_lane": exec_opl, "achieved": exec_tops, "frac": exec_tops / peak,
-                                      "rotation_pair_gemm": bool(stats_acc["rp"])},
-                         "note": f"achieved = algorithmic int8 ops ({opl}/lane) / GEMM time; peak = {peak_note}. "
-                                 "The rotation-pair (Winograd F(2,2)) GEMMs execute fewer int8 MACs than the "
-                                 "algorithmic count (DESIGN.md section 8), so `achieved` can exceed the executed "
-                                 "rate: `executed` is the tensor-pipe figure"},
+                         "int8_ops_per_launch_executed": exec_ops_launch,
+                         "gemm_ms_per_launch": gemm_ms, "gemm_launches_per_step": launches_per_step,
+                         "rotation_pair_gemm": bool(stats_acc["rp"]),
+                         "effective": {"int8_ops_per_lane_algorithmic": opl,
+                                       "int8_ops_per_lane_executed": stats_acc["gemm_ops"] / max(1, args.steps) /
+                                       max(1, local_lanes),
+                                       "achieved": alg_tops, "effective_frac": alg_tops / peak},
+                         "serial": ({"gemm_ms_per_launch": sg_ms / sg_n,
+                                     "achieved": exec_ops_launch / (sg_ms / sg_n / 1e3) / 1e12,
+                                     "frac": exec_ops_launch / (sg_ms / sg_n / 1e3) / 1e12 / peak}
+                                    if sg_n else None),
+                         "peak_note": peak_note,
+                         "note": "achieved = int8 ops the tensor pipe executes per GEMM launch / the launch's "
+                                 "CUDA-event time on the GEMM stream during the timed (overlapped) steps; "
+                                 "`effective` counts the algorithmic 460,800 ops/lane the rotation-pair "
+                                 "(Winograd) GEMMs skip; `serial` = the same launches in one serialised "
+                                 "profiled query"},
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),
-            "roofline_compare": compare_roofline(sess.last_stats.threshold_ms, local_lanes, variant, peaks),
+            "roofline_compare": compare_roofline(prof, local_lanes, variant, peaks) if prof else None,
             "phase_ms": {"gemm_per_launch": gemm_ms,
                          "gemm_launches_per_step": stats_acc["gemm_launches"] / args.steps,
                          "threshold_stream_span": sess.last_stats.threshold_ms,
                          "or": sess.last_stats.or_ms, "prep": sess.last_stats.prep_ms, "step": ms,
                          "host_wall_per_step": host_s / args.steps * 1e3,
+                         "serial_kernels_ms": {k: v[0] for k, v in prof.items()},
                          "note": "GEMM (stream 1) and threshold (stream 2) overlap; the span is the "
                                  "threshold stream's first-start to last-end time of the last step"},
             "planted_match": planted, "setup_s": setup_s,
         }
         if cpu is not None:
-            line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            c0 = cpu[backend]
+            line["cpu_baseline"] = {k: c0[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["other_backend"] = {k: cpu[1 - backend][k] for k in ("value", "sample")}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -432,8 +548,9 @@ def main():
     ap.add_argument("--variant", default="mpc-lift", choices=list(VARIANTS))
     ap.add_argument("--rows", type=int, default=ROWS_PER_GPU)
     ap.add_argument("--persons", type=int, default=PERSONS)
-    ap.add_argument("--ref-rows", type=int, default=3000, dest="ref_rows")
+    ap.add_argument("--ref-rows", type=int, default=REF_ROWS, dest="ref_rows")
     ap.add_argument("--no-cpu", action="store_true", dest="no_cpu")
+    ap.add_argument("--no-profile", action="store_true", dest="no_profile")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -201,13 +201,27 @@ class Session {
 };
 
 // Drop-in for the per-party entry points: three party threads rendezvous and
-// the last arrival runs the fused 3-party query.  The DB is (re)loaded only
-// when the payload spans change (the reference reloads on every call,
-// engine.cpp:404-420; here it stays resident).
+// the last arrival runs the fused 3-party query.  Like the reference
+// (party_batch_query / party_membership load the DB on every call,
+// engine.cpp:404-420), every call reloads the DB from the payloads it is given.
+// A caller that keeps the DB unchanged between calls can opt into residency
+// with keep_db_resident(true); it must then call invalidate_db() after
+// rewriting the payload bytes in place.  Freshness is never inferred from
+// pointer identity alone.
 class ThreePartyGpu {
  public:
   ThreePartyGpu(const EngineConfig& cfg, std::uint64_t seed, int device = 0)
       : session_(cfg, seeds_from_master(seed), device) {}
+
+  void keep_db_resident(bool on) {
+    std::lock_guard<std::mutex> lk(mu_);
+    resident_ = on;
+    valid_ = false;
+  }
+  void invalidate_db() {
+    std::lock_guard<std::mutex> lk(mu_);
+    valid_ = false;
+  }
 
   MembershipResult party_batch_query(unsigned party /* 1..3 */, std::span<const std::uint8_t> db_payload,
                                      std::uint64_t s, std::span<const std::uint8_t> query_payload, unsigned persons) {
@@ -229,9 +243,11 @@ class ThreePartyGpu {
     if (++arrived_ == 3) {
       arrived_ = 0;
       try {
-        if (!same(db_, loaded_) || s != session_.rows()) {
+        if (!resident_ || !valid_ || !same(db_, loaded_) || s != session_.rows()) {
+          valid_ = false;
           session_.load_db(db_, s);
           loaded_ = db_;
+          valid_ = true;
         }
         results_ = membership ? session_.membership(q_) : session_.batch_query(q_, persons);
         error_.clear();
@@ -258,6 +274,7 @@ class ThreePartyGpu {
   std::condition_variable cv_;
   unsigned arrived_ = 0;
   std::uint64_t gen_ = 0;
+  bool resident_ = false, valid_ = false;
   Payloads db_{}, q_{}, loaded_{};
   std::array<MembershipResult, 3> results_{};
   std::string error_;
@@ -396,16 +413,17 @@ class GpuParty {
 };
 
 // party_batch_query(PartyCtx&, cfg, db_payload, s, query_payload, persons)
-// (engine.hpp:311-313) at one party; the DB stays resident between calls
-// with the same payload span.
+// (engine.hpp:311-313) at one party: loads the DB on every call, as the
+// reference does (engine.cpp:404-420).  Callers that keep a DB resident call
+// GpuParty::load_db once and GpuParty::batch_query per query instead.
 inline MembershipResult party_batch_query(GpuParty& ctx, std::span<const std::uint8_t> db_payload, std::uint64_t s,
                                           std::span<const std::uint8_t> query_payload, unsigned persons) {
-  if (!ctx.loaded(db_payload, s)) ctx.load_db(db_payload, s);
+  ctx.load_db(db_payload, s);
   return ctx.batch_query(query_payload, persons);
 }
 inline MembershipResult party_membership(GpuParty& ctx, std::span<const std::uint8_t> db_payload, std::uint64_t s,
                                          std::span<const std::uint8_t> query_payload) {
-  if (!ctx.loaded(db_payload, s)) ctx.load_db(db_payload, s);
+  ctx.load_db(db_payload, s);
   return ctx.membership(query_payload);
 }
 

@@ -237,6 +237,16 @@ int irismpc_gpu_read_iris_db(const char* path, uint64_t* codes_out, uint64_t* ma
 int irismpc_gpu_write_iris_db(const char* path, uint32_t l, uint64_t s, const uint64_t* codes,
                               const uint64_t* masks);
 
+/* ---- profiling ------------------------------------------------------------ */
+/* on = 1: every following query runs serialised on one stream (no GEMM /
+ * threshold overlap) with CUDA events around every kernel launch, so each
+ * kernel's time is its standalone serial time; on = 0 restores the overlapped
+ * pipeline.  profile_read returns up to `max` (kernel name, total device ms,
+ * launches) entries accumulated since the last read and resets them. */
+int irismpc_gpu_profile(irismpc_gpu_ctx* ctx, int on);
+int irismpc_gpu_profile_read(irismpc_gpu_ctx* ctx, char (*names)[48], double* ms, uint64_t* launches,
+                             uint32_t max, uint32_t* count);
+
 /* ---- debug / parity taps (tests) ------------------------------------------ */
 #define IRISMPC_GPU_TAP_DOT_HD 1  /* [3][n] per-party additive hd dot (L1), u16 (KH = 16) / u32 */
 #define IRISMPC_GPU_TAP_DOT_ML 2  /* [3][n] ml dot u16 / u32; plain-mask: [n] u16 public popcount */
@@ -248,6 +258,13 @@ int irismpc_gpu_write_iris_db(const char* path, uint32_t l, uint64_t s, const ui
 /* Enable capture of all taps for the next query (costly; tests only). */
 int irismpc_gpu_enable_taps(irismpc_gpu_ctx* ctx, int enable);
 int irismpc_gpu_read_tap(irismpc_gpu_ctx* ctx, int tap, void* host_out, size_t bytes);
+/* Row-sampled L1 taps for DBs too large for full taps: while k > 0 every query
+ * captures only DOT_HD / DOT_ML, for the k given rows of this shard (0-based
+ * local rows) against every query column, then all pair lanes, as
+ * [party][col * k + i] followed by [party][ncols * k + pair lane] -- the lane
+ * order of the same query run against a k-row DB made of those rows.  k = 0
+ * turns it off. */
+int irismpc_gpu_tap_rows(irismpc_gpu_ctx* ctx, const uint64_t* rows, uint32_t k);
 
 #ifdef __cplusplus
 }

@@ -416,3 +416,113 @@ def ref_read_share_file(path: str):
     if rc:
         return rc
     return (*[int(x) for x in hdr], int(s.value), int(n.value))
+
+
+# ------------------------------------------------- plaintext checker at scale
+
+_plain = None
+
+
+def plain_lib():
+    """oracle/plain_bits.c compiled on THIS machine (-O3 -march=native, OpenMP)
+    into a temporary directory: the full-scale plaintext predicate (tests only)."""
+    global _plain
+    if _plain is None:
+        import subprocess
+        import tempfile
+        d = tempfile.mkdtemp(prefix="plain_bits_")
+        so = os.path.join(d, "libplain_bits.so")
+        cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+        subprocess.run([cc, "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-o", so,
+                        os.path.join(HERE, "plain_bits.c"), "-lm"], check=True)
+        P = C.CDLL(so)
+        P.plain_batch_bits.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_uint32, C.c_uint32,
+                                       C.c_uint64, u64p, u64p, C.c_uint32, u64p, u64p, u8p, u8p, u64p, u8p]
+        P.plain_batch_bits.restype = C.c_uint64
+        _plain = P
+    return _plain
+
+
+def plain_batch_bits(l: int, rotations: int, variant: int, ratio: float, db_codes, db_masks, q_codes, q_masks,
+                     persons: int, membership: bool = False, expect=None, want_bits: bool = True):
+    """Plaintext lane bits / person bits of a batch query (tests/oracle.hpp:35-57
+    over the engine.cpp:262-293 schedule).  Returns (lane_bits or None, person bits,
+    mismatches vs `expect`, first mismatching lane)."""
+    P = plain_lib()
+    s = db_codes.shape[0]
+    n = int(lib().orc_lane_count(persons, s, rotations, 1 if membership else 0))
+    bits = np.zeros(max(1, n), np.uint8) if want_bits else None
+    ng = 1 if membership else persons
+    pers = np.zeros(max(1, ng), np.uint8)
+    fb = C.c_uint64(0)
+    a = int(lib().orc_match_a(ratio))
+    dc = np.ascontiguousarray(db_codes if s else np.zeros((1, words(l)), np.uint64), np.uint64)
+    dm = np.ascontiguousarray(db_masks if s else np.zeros((1, words(l)), np.uint64), np.uint64)
+    ex = None if expect is None else np.ascontiguousarray(expect, np.uint8)
+    bad = P.plain_batch_bits(l, rotations, 1 if membership else 0, 1 if variant == PLAIN_MASK else 0, ratio, a,
+                             1 << 16, s, _p(dc, u64p), _p(dm, u64p), persons,
+                             _p(np.ascontiguousarray(q_codes, np.uint64), u64p),
+                             _p(np.ascontiguousarray(q_masks, np.uint64), u64p), _p(bits, u8p), _p(ex, u8p),
+                             C.byref(fb), _p(pers, u8p))
+    return (bits[:n] if want_bits else None), pers[:ng], int(bad), int(fb.value)
+
+
+# ------------------------------------- the reference's equivalence grid (_ref)
+
+def ref_equiv_instance(backend: int, variant: int, l: int, s: int, seed: int, ratio: float):
+    """equiv_common.hpp:61-89 run_instance, generated and run by the reference:
+    (db_codes, db_masks, q_code, q_mask, want, got, ref_row_bits)."""
+    R = ref()
+    R.ref_equiv_instance.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_double, u64p, u64p,
+                                     u64p, u64p, u8p, u8p, u8p]
+    wl = words(l)
+    dc = np.zeros((max(1, s), wl), np.uint64)
+    dm = np.zeros((max(1, s), wl), np.uint64)
+    qc = np.zeros(wl, np.uint64)
+    qm = np.zeros(wl, np.uint64)
+    want, got = C.c_uint8(0), C.c_uint8(0)
+    rb = np.zeros(max(1, s), np.uint8)
+    rc = R.ref_equiv_instance(backend, variant, l, s, seed, ratio, _p(dc, u64p), _p(dm, u64p), _p(qc, u64p),
+                              _p(qm, u64p), C.byref(want), C.byref(got), _p(rb, u8p))
+    if rc:
+        raise RuntimeError(f"ref_equiv_instance failed with status {rc}")
+    return dc[:s], dm[:s], qc, qm, int(want.value), int(got.value), rb[:s]
+
+
+def ref_boundary_instances(count: int):
+    """equiv_common.hpp:93-128 run_boundary_instances (l = 64, one DB row each)."""
+    R = ref()
+    R.ref_boundary_instances.argtypes = [C.c_uint, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                         u64p, u64p, u64p, u64p, u64p, u8p, u8p]
+    be = np.zeros(count, np.int32)
+    va = np.zeros(count, np.int32)
+    ra = np.zeros(count, np.float64)
+    ms = np.zeros(count, np.uint64)
+    arrs = [np.zeros(count, np.uint64) for _ in range(4)]
+    want = np.zeros(count, np.uint8)
+    got = np.zeros(count, np.uint8)
+    rc = R.ref_boundary_instances(count, be.ctypes.data_as(C.POINTER(C.c_int)), va.ctypes.data_as(C.POINTER(C.c_int)),
+                                  ra.ctypes.data_as(C.POINTER(C.c_double)), _p(ms, u64p),
+                                  *[_p(a, u64p) for a in arrs], _p(want, u8p), _p(got, u8p))
+    if rc:
+        raise RuntimeError(f"ref_boundary_instances failed with status {rc}")
+    return dict(backend=be, variant=va, ratio=ra, seed=ms, row_code=arrs[0], row_mask=arrs[1], q_code=arrs[2],
+                q_mask=arrs[3], want=want, got=got)
+
+
+def ref_engine_case(which: int, backend: int, variant: int):
+    """test_engine.cpp:42-82: 0 planted self-match, 1 complement row, 2 ml = 0 rows."""
+    R = ref()
+    R.ref_engine_case.argtypes = [C.c_int, C.c_int, C.c_int, u64p, u64p, u64p, u64p, u64p, u8p, u8p]
+    dc = np.zeros(8, np.uint64)
+    dm = np.zeros(8, np.uint64)
+    s = C.c_uint64(0)
+    qc = np.zeros(1, np.uint64)
+    qm = np.zeros(1, np.uint64)
+    want, got = C.c_uint8(0), C.c_uint8(0)
+    rc = R.ref_engine_case(which, backend, variant, _p(dc, u64p), _p(dm, u64p), C.byref(s), _p(qc, u64p),
+                           _p(qm, u64p), C.byref(want), C.byref(got))
+    if rc:
+        raise RuntimeError(f"ref_engine_case failed with status {rc}")
+    n = int(s.value)
+    return dc[:n].reshape(n, 1), dm[:n].reshape(n, 1), qc, qm, int(want.value), int(got.value)

@@ -23,6 +23,7 @@
 #include "irismpc/kernels.hpp"
 #include "irismpc/prf.hpp"
 #include "irismpc/shares.hpp"
+#include "oracle.hpp"  // the reference's plaintext test oracle (proj/tests/oracle.hpp)
 
 using namespace irismpc;
 
@@ -501,5 +502,160 @@ double ref_bench_step(void* h, std::uint8_t* match0) {
 }
 
 void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
+
+
+// --- the reference's randomized equivalence grid (tests/equiv_common.hpp) ---
+
+namespace {
+void put_record(const IrisRecord& r, std::uint64_t* c, std::uint64_t* m) {
+  for (std::size_t i = 0; i < r.code.words().size(); ++i) {
+    c[i] = r.code.words()[i];
+    m[i] = r.mask.words()[i];
+  }
+}
+EngineConfig grid_config(int backend, int variant, std::uint32_t l, double ratio) {
+  EngineConfig cfg;
+  cfg.backend = backend ? Backend::shamir : Backend::replicated;
+  cfg.variant = static_cast<Variant>(variant);
+  cfg.l = l;
+  cfg.params = MatchParams::make(ratio, 16);
+  cfg.debug_rows = true;
+  return cfg;
+}
+}  // namespace
+
+// One run_instance of equiv_common.hpp:61-89, generated with the reference's
+// own Rng / random_record in the same draw order (DB rows with a mask density
+// drawn from {0, 1, 0.3, 0.85}, a random query, one time in three a noisy
+// planted copy of a row), then run through run_membership_local (debug rows)
+// and the plaintext oracle::naive_membership.  Outputs the instance records,
+// want (oracle), got (reference aggregate) and the reference's row bits.
+int ref_equiv_instance(int backend, int variant, std::uint32_t l, std::uint64_t s, std::uint64_t seed, double ratio,
+                       std::uint64_t* db_codes, std::uint64_t* db_masks, std::uint64_t* q_code,
+                       std::uint64_t* q_mask, std::uint8_t* want, std::uint8_t* got, std::uint8_t* row_bits) {
+  try {
+    const std::size_t wl = (l + 63) / 64;
+    Rng rng(seed * 2654435761u + l * 97 + s);
+    IrisDb db(l);
+    for (std::uint64_t i = 0; i < s; ++i) {
+      const std::uint64_t pick = rng.below(5);
+      const double density = pick == 0 ? 0.0 : pick == 1 ? 1.0 : pick == 2 ? 0.3 : 0.85;
+      db.add(random_record(l, rng, density));
+    }
+    IrisRecord q = random_record(l, rng, 0.85);
+    if (s > 0 && rng.below(3) == 0) {
+      q = db.rows[rng.below(s)];
+      for (int f = 0; f < 4; ++f) {
+        const std::size_t i = rng.below(l);
+        q.code.set(i, !q.code.get(i));
+      }
+    }
+    const auto cfg = grid_config(backend, variant, l, ratio);
+    const auto out = run_membership_local(cfg, q, db, seed);
+    *want = oracle::naive_membership(q, db, cfg.params, cfg.variant) ? 1 : 0;
+    *got = out.aggregate() ? 1 : 0;
+    for (std::uint64_t i = 0; i < s; ++i) {
+      put_record(db.rows[i], db_codes + i * wl, db_masks + i * wl);
+      row_bits[i] = out.output().row_bits.at(i);
+    }
+    put_record(q, q_code, q_mask);
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// run_boundary_instances (equiv_common.hpp:93-128): `count` full-mask l = 64
+// pairs with b*dot at a*ml and one dot step either side, for ratios 0.375 and
+// 0.3, cycling backend (made % 2) and variant ((made / 2) % 4).  Per instance:
+// backend, variant, ratio, the membership seed, the row, the query, want, got.
+int ref_boundary_instances(unsigned count, int* backend, int* variant, double* ratio, std::uint64_t* mseed,
+                           std::uint64_t* row_code, std::uint64_t* row_mask, std::uint64_t* q_code,
+                           std::uint64_t* q_mask, std::uint8_t* want, std::uint8_t* got) {
+  try {
+    const std::size_t l = 64;
+    std::uint64_t seed = 0xb0;
+    const double ratios[2] = {0.375, 0.3};
+    unsigned made = 0;
+    while (made < count) {
+      for (const double rt : ratios) {
+        const auto params = MatchParams::make(rt, 16);
+        const double target = static_cast<double>(params.a) * l / params.b;
+        for (int delta = -1; delta <= 1 && made < count; ++delta) {
+          const std::int64_t hd = (static_cast<std::int64_t>(l) - static_cast<std::int64_t>(target)) / 2 + delta;
+          if (hd < 0 || hd > static_cast<std::int64_t>(l)) continue;
+          Rng rng(seed++);
+          IrisRecord row(BitVec::random(l, rng), BitVec(l));
+          for (std::size_t i = 0; i < l; ++i) row.mask.set(i, true);
+          IrisRecord q = row;
+          for (std::int64_t i = 0; i < hd; ++i)
+            q.code.set(static_cast<std::size_t>(i), !q.code.get(static_cast<std::size_t>(i)));
+          IrisDb db(l);
+          db.add(row);
+          backend[made] = static_cast<int>(made % 2 == 0 ? 0 : 1);  // backends[2] = {replicated, shamir}
+          variant[made] = static_cast<int>((made / 2) % 4);
+          ratio[made] = rt;
+          mseed[made] = seed;
+          const auto cfg = grid_config(backend[made], variant[made], static_cast<std::uint32_t>(l), rt);
+          const auto out = run_membership_local(cfg, q, db, seed);
+          want[made] = oracle::naive_membership(q, db, cfg.params, cfg.variant) ? 1 : 0;
+          got[made] = out.aggregate() ? 1 : 0;
+          put_record(row, row_code + made, row_mask + made);
+          put_record(q, q_code + made, q_mask + made);
+          ++made;
+        }
+      }
+    }
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// test_engine.cpp:42-82: planted self-match (7 random rows + a full-mask query
+// row), its complement, and the ml = 0 instance; k = 0, 1, 2 selects which.
+// Records out (up to 8 rows), want/got as above.
+int ref_engine_case(int which, int backend, int variant, std::uint64_t* db_codes, std::uint64_t* db_masks,
+                    std::uint64_t* s_out, std::uint64_t* q_code, std::uint64_t* q_mask, std::uint8_t* want,
+                    std::uint8_t* got) {
+  try {
+    const std::size_t l = 64;
+    IrisDb db(l);
+    IrisRecord q{BitVec(l), BitVec(l)};
+    std::uint64_t mseed = 500;
+    if (which == 0 || which == 1) {
+      Rng rng(101);
+      for (int i = 0; i < 7; ++i) db.add(random_record(l, rng, 0.8));
+      q = IrisRecord(BitVec::random(l, rng), BitVec(l));
+      for (std::size_t i = 0; i < l; ++i) q.mask.set(i, true);
+      db.add(q);
+      if (which == 1) {
+        IrisRecord comp = q;
+        for (std::size_t i = 0; i < l; ++i) comp.code.set(i, !q.code.get(i));
+        db = IrisDb(l);
+        db.add(comp);
+        mseed = 501;
+      }
+    } else {
+      Rng rng(102);
+      q = IrisRecord(BitVec::random(l, rng), BitVec(l));
+      IrisRecord row(q.code, BitVec(l));
+      for (std::size_t i = 0; i < 32; ++i) q.mask.set(i, true);
+      for (std::size_t i = 32; i < 64; ++i) row.mask.set(i, true);
+      db.add(row);
+      mseed = 502;
+    }
+    const auto cfg = grid_config(backend, variant, static_cast<std::uint32_t>(l), 0.375);
+    const auto out = run_membership_local(cfg, q, db, mseed);
+    *want = oracle::naive_membership(q, db, cfg.params, cfg.variant) ? 1 : 0;
+    *got = out.aggregate() ? 1 : 0;
+    *s_out = db.size();
+    for (std::size_t i = 0; i < db.size(); ++i) put_record(db.rows[i], db_codes + i, db_masks + i);
+    put_record(q, q_code, q_mask);
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
 
 }  // extern "C"

@@ -40,7 +40,8 @@ EXPORTED = [
     "irismpc_gpu_batch_query_device", "irismpc_gpu_membership", "irismpc_gpu_batch_query_partial",
     "irismpc_gpu_or_open", "irismpc_gpu_get_stream_positions", "irismpc_gpu_set_stream_positions",
     "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
-    "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap",
+    "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap", "irismpc_gpu_profile", "irismpc_gpu_profile_read",
+    "irismpc_gpu_tap_rows",
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
@@ -161,6 +162,9 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_deal_payload.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp, P3]
         L.irismpc_gpu_synth_db.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64]
         L.irismpc_gpu_enable_taps.argtypes = [vp, C.c_int]
+        L.irismpc_gpu_profile.argtypes = [vp, C.c_int]
+        L.irismpc_gpu_tap_rows.argtypes = [vp, u64p, C.c_uint32]
+        L.irismpc_gpu_profile_read.argtypes = [vp, vp, vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
         cp3 = C.c_char_p * 3
         L.irismpc_gpu_read_share_header.argtypes = [C.c_char_p, C.POINTER(ShareHeader)]
@@ -436,6 +440,32 @@ class Session:
     def set_stream_positions(self, pos):
         p = np.ascontiguousarray(pos, np.uint64)
         self._check(lib().irismpc_gpu_set_stream_positions(self._h, p.ctypes.data_as(u64p)))
+
+    def profile(self, on: bool = True):
+        """Serialised queries with per-kernel CUDA events (irismpc_gpu_profile)."""
+        self._check(lib().irismpc_gpu_profile(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (device ms, launches)} accumulated since the last read."""
+        mx = 64
+        names = (C.c_char * (48 * mx))()
+        ms = np.zeros(mx, np.float64)
+        cnt = np.zeros(mx, np.uint64)
+        n = C.c_uint32(0)
+        self._check(lib().irismpc_gpu_profile_read(self._h, names, ms.ctypes.data, cnt.ctypes.data, mx, C.byref(n)))
+        raw = bytes(names)
+        return {raw[48 * i:48 * i + 48].split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
+
+    def tap_rows(self, rows) -> None:
+        """Row-sampled L1 taps (irismpc_gpu_tap_rows); [] turns them off."""
+        r = np.ascontiguousarray(rows, np.uint64)
+        self._check(lib().irismpc_gpu_tap_rows(self._h, r.ctypes.data_as(u64p) if r.size else None, r.size))
+        self._tap_k = int(r.size)
+
+    def read_row_taps(self, tap: int, persons: int) -> np.ndarray:
+        """[3][ncols * k + pairs] (plain-mask DOT_ML: [ncols * k + pairs]) of the last query."""
+        n = 2 * persons * self.cfg.rotations * self._tap_k + persons * (persons - 1) // 2 * 4 * self.cfg.rotations
+        return self.read_tap(tap, n)
 
     def enable_taps(self, on: bool = True):
         self._check(lib().irismpc_gpu_enable_taps(self._h, 1 if on else 0))

@@ -189,9 +189,14 @@ struct irismpc_gpu_ctx {
   size_t h_segs_cap = 0;
   // PRF stream state
   uint64_t pos[3] = {0, 0, 0};
-  uint64_t query_id = 0;
+  uint64_t query_id = 0;  // queries run on this context (64-bit: never wraps)
+  uint64_t or_ctr = 0;    // OR-gate stream counter of the last query (or_stream_id)
   // taps
   bool taps = false;
+  bool serial = false;  // irismpc_gpu_profile: one stream, per-kernel CUDA events
+  // row-sampled L1 taps (irismpc_gpu_tap_rows): DOT_HD / DOT_ML of these local rows, all columns
+  Buf tap_rows_dev;
+  uint32_t tap_k = 0;
   Buf tap_buf[7];
   size_t tap_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
   uint64_t tap_n = 0;
@@ -419,22 +424,23 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint32_t nlift = V == kMpcLift ? 64u : 0u;
   const uint32_t ngates = nlift + 2u * vw.kc - 3u;
   const uint32_t ngroups = membership ? 1u : persons;
-  const uint64_t qid = c->query_id++;
-  const uint64_t rank = c->cfg.shard_rank;
+  c->query_id++;
+  const uint64_t octr = ++c->or_ctr;  // fresh OR-gate streams for this query
+  const uint32_t rank = c->cfg.shard_rank;
   const uint64_t s_loc = c->s;
   const uint64_t row_off = c->cfg.db_row_offset;
   static const bool serial = [] {
     const char* e = std::getenv("IRISMPC_SERIAL");  // profiling hook: no GEMM/threshold overlap
     return e && e[0] == '1';
   }();
-  cudaStream_t st = c->st, st2 = serial ? c->st : c->st2;
+  cudaStream_t st = c->st, st2 = (serial || c->serial) ? c->st : c->st2;
   // two threshold streams: a chunk's columns split into two jobs, so one job's
   // latency-bound bit-sliced kernels overlap the other's ChaCha kernels
   static const int thr_streams = [] {
     const char* e = std::getenv("IRISMPC_THR_STREAMS");
     return e ? std::max(1, std::min(2, std::atoi(e))) : 1;
   }();
-  const bool two = thr_streams == 2 && !serial;
+  const bool two = thr_streams == 2 && !serial && !c->serial;
   cudaStream_t st3 = two ? c->st3 : st2;
   uint64_t launches = 0;
 
@@ -523,7 +529,18 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   };
   CK(c, cudaEventRecord(c->ev[1], st));
 
-  if (c->taps) {
+  const bool row_taps = c->tap_k > 0;
+  if (row_taps) {  // compact L1 taps: [p][col * k + i] then the pair lanes
+    const uint64_t nt = ncols * c->tap_k + npairs;
+    c->tap_n = nt;
+    const size_t tb[2] = {3 * nt * hb, fm.nparty * nt * mb};
+    for (int t = 0; t < 7; ++t) {
+      c->tap_bytes[t] = t < 2 ? tb[t] : 0;
+      if (t >= 2) continue;
+      if (c->tap_buf[t].ensure(tb[t] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (row taps)");
+      CK(c, cudaMemsetAsync(c->tap_buf[t].p, 0, tb[t] + 16, st));
+    }
+  } else if (c->taps) {
     c->tap_n = n;
     const size_t tb[7] = {3 * n * hb, fm.nparty * n * mb, 3 * n * 4, 3 * n * 4, 3 * n * 4, 3 * n * 4, 3 * n};
     for (int t = 0; t < 7; ++t) {
@@ -621,6 +638,11 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   std::vector<uint64_t> h_slot_begin(ngroups + 1);
   for (uint32_t g = 0; g <= ngroups; ++g)
     h_slot_begin[g] = membership ? (g == 0 ? 0 : total_slots) : col_slot[(uint64_t)g * 2 * r];
+  {
+    const uint64_t per_person_max = total_slots + npairs_all;  // linear OR items of one person, at most
+    if (per_person_max >= kOrTreeOffset || ngroups >= (1u << 23))
+      return fail(c, IRISMPC_GPU_ERR_BOUNDS, "OR-gate stream windows exceeded (persons >= 2^23 or 2^39 items)");
+  }
   if (c->partial.ensure(3 * total_slots + 16) || c->slot_begin.ensure((ngroups + 1) * sizeof(uint64_t)) ||
       c->person_out.ensure(3ull * ngroups + 16))
     return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or buffers)");
@@ -763,12 +785,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   ta.coef = 1.0 - 2.0 * c->cfg.match_ratio;
   ta.partial = c->partial.as<uint8_t>();
   ta.nslots = total_slots;
-  ta.or_elem_base = (qid << 48) | (rank << 40);
+  ta.or_stream = or_stream_id(octr, rank, 1);
+  ta.or_elem_base = 0;
   ta.ml_rs = c->ml_rs.as<uint16_t>();
   ta.diff = c->diff.as<uint32_t>();
   ta.cstride = cstride;
   ta.gate = c->gate.as<uint64_t>();
-  if (c->taps) {
+  if (c->taps && !row_taps) {
     ta.tap_rs_hd = c->tap_buf[2].as<uint32_t>();
     ta.tap_rs_ml = c->tap_buf[3].as<uint32_t>();
     ta.tap_ml32 = c->tap_buf[4].as<uint32_t>();
@@ -897,7 +920,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       CK(c, cudaGetLastError());
     }
     CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
-    if (c->taps && c->cfg.db_rows_total == 0) {
+    if (row_taps) {
+      const uint64_t nt = c->tap_n;
+      launch_tap_rows(dots, (int)hb, 3, ncols, r, nr, use_rp[0] ? 3 * ncols_rp * nr : 0,
+                      c->tap_rows_dev.as<uint64_t>(), c->tap_k, chunk_row0[i], c->tap_buf[0].p, nt, st);
+      launch_tap_rows(dots_ml, (int)mb, fm.nparty, ncols, r, nr, use_rp[1] ? 3 * ncols_rp * nr : 0,
+                      c->tap_rows_dev.as<uint64_t>(), c->tap_k, chunk_row0[i], c->tap_buf[1].p, nt, st);
+      CK(c, cudaGetLastError());
+    } else if (c->taps && c->cfg.db_rows_total == 0) {
       // L1 tap: dots[(col, row - r0)] -> lane col*S + row
       if (use_rp[0])
         launch_rp_tap(dots, (int)hb, 3, ncols, r, nr, 3 * ncols_rp * nr, c->tap_buf[0].p, n, S, chunk_row0[i], st);
@@ -944,7 +974,15 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   if (npairs) {
     const uint8_t* pd_hd = c->pair_dots.as<uint8_t>();
     const uint8_t* pd_ml = pd_hd + 3 * npairs * hb;
-    if (c->taps && c->cfg.db_rows_total == 0) {
+    if (row_taps) {
+      const uint64_t nt = c->tap_n, o = ncols * c->tap_k;
+      for (uint32_t p = 0; p < 3; ++p)
+        CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint8_t>() + (p * nt + o) * hb, pd_hd + p * npairs * hb, npairs * hb,
+                              cudaMemcpyDeviceToDevice, st2));
+      for (uint32_t p = 0; p < fm.nparty; ++p)
+        CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint8_t>() + (p * nt + o) * mb, pd_ml + p * npairs * mb, npairs * mb,
+                              cudaMemcpyDeviceToDevice, st2));
+    } else if (c->taps && c->cfg.db_rows_total == 0) {
       for (uint32_t p = 0; p < 3; ++p)
         CK(c, cudaMemcpyAsync(c->tap_buf[0].as<uint8_t>() + (p * n + ncols * S) * hb, pd_hd + p * npairs * hb,
                               npairs * hb, cudaMemcpyDeviceToDevice, st2));
@@ -972,7 +1010,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   oa.persons = ngroups;
   oa.rot = r;
   for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
-  oa.elem_base = (qid << 48) | (rank << 40);
+  oa.stream = or_stream_id(octr, rank, 2);
   oa.out = c->person_out.as<uint8_t>();
   void* ph2 = prof_begin(st2);
   launch_or_persons(oa, st2);
@@ -985,7 +1023,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
 
   if (mode == 0) {
     if (c->open_out.ensure(ngroups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
-    launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, qid << 48, c->open_out.as<uint8_t>(), st);
+    launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, or_stream_id(octr, rank, 3),
+                   c->open_out.as<uint8_t>(), st);
     CK(c, cudaGetLastError());
     ++launches;
     CK(c, cudaMemcpyAsync(match_out, c->open_out.p, ngroups, cudaMemcpyDeviceToHost, st));
@@ -1164,6 +1203,7 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   for (Buf* b : bufs) b->release();
   for (auto& f : c->fld) f.release();
   for (auto& t : c->tap_buf) t.release();
+  c->tap_rows_dev.release();
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->gev) cudaEventDestroy(e);
@@ -1342,8 +1382,9 @@ int irismpc_gpu_or_open(irismpc_gpu_ctx* c, const uint8_t* partials_dev, uint32_
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
   cudaSetDevice(c->cfg.device);
   if (c->open_out.ensure(persons + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
-  // query_id was advanced by the partial query; final OR uses stream 3 of that query
-  launch_or_open(partials_dev, G, persons, c->keys, (c->query_id - 1) << 48, c->open_out.as<uint8_t>(), c->st);
+  // the partial query advanced or_ctr; the cross-shard OR + open draws that query's kind-3 stream
+  launch_or_open(partials_dev, G, persons, c->keys, or_stream_id(c->or_ctr, c->cfg.shard_rank, 3),
+                 c->open_out.as<uint8_t>(), c->st);
   CK(c, cudaGetLastError());
   CK(c, cudaMemcpyAsync(person_match_out, c->open_out.p, persons, cudaMemcpyDeviceToHost, c->st));
   CK(c, cudaStreamSynchronize(c->st));
@@ -1422,6 +1463,36 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint
   masks.release();
   for (auto& p : pay) p.release();
   return rc;
+}
+
+int irismpc_gpu_profile(irismpc_gpu_ctx* c, int on) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  c->serial = on != 0;
+  prof_enable(on != 0);
+  return 0;
+}
+
+int irismpc_gpu_profile_read(irismpc_gpu_ctx* c, char (*names)[48], double* ms, uint64_t* launches, uint32_t max,
+                             uint32_t* count) {
+  if (!c || !count) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  *count = (uint32_t)prof_take(names, ms, launches, max);
+  return 0;
+}
+
+int irismpc_gpu_tap_rows(irismpc_gpu_ctx* c, const uint64_t* rows, uint32_t k) {
+  if (!c || (k && !rows)) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  for (uint32_t i = 0; i < k; ++i)
+    if (rows[i] >= c->s) return fail(c, IRISMPC_GPU_ERR_BOUNDS, "tap row outside this shard");
+  c->tap_k = 0;
+  if (k) {
+    if (c->tap_rows_dev.ensure(k * sizeof(uint64_t))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (tap rows)");
+    CK(c, cudaMemcpy(c->tap_rows_dev.p, rows, k * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  c->tap_k = k;
+  return 0;
 }
 
 int irismpc_gpu_enable_taps(irismpc_gpu_ctx* c, int enable) {

@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -297,22 +298,49 @@ int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
+// Per-device launch state: the >48 KB dynamic shared-memory opt-in is a
+// per-device function attribute and the SM count differs per device, so both
+// are kept per CUDA device ordinal (a process may hold contexts on several
+// GPUs, and party threads launch concurrently).
+namespace {
+constexpr int kMaxDev = 64;
+struct DevState {
+  std::once_flag attr[3];  // dynamic-smem opt-in of k_limb_gemm_pair<1 / 2 / 4>
+  std::once_flag sms;
+  int nsm = 0;
+};
+DevState g_dev[kMaxDev];
+
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= kMaxDev ? kMaxDev - 1 : d);
+}
+
+int device_sms(int d) {
+  DevState& s = g_dev[d];
+  std::call_once(s.sms, [&] {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) n = std::max(2, std::min(n, std::atoi(e)));  // experiment hook
+    s.nsm = n;
+  });
+  return s.nsm;
+}
+}  // namespace
+
 template <int L>
 static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const GemmArgs& g,
                                uint32_t m_tiles, uint32_t n_tiles, cudaStream_t st) {
   using T = Tile<L>;
-  static bool attr = false;
-  if (!attr) {
+  const int dev = cur_device();
+  constexpr int slot = L == 1 ? 0 : (L == 2 ? 1 : 2);
+  std::call_once(g_dev[dev].attr[slot], [] {
     cudaFuncSetAttribute(k_limb_gemm_pair<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    attr = true;
-  }
+  });
   // m_tiles counts 128-row tiles; pairs cover 256 rows (s_pad is a multiple of 256).
   // Persistent: one CTA pair per two SMs.
-  static int nsm = 0;
-  if (!nsm) {
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) nsm = std::max(2, std::min(nsm, std::atoi(e)));  // experiment hook
-  }
+  const int nsm = device_sms(dev);
   const uint32_t m_pairs = m_tiles / 2;
   const uint32_t units = g.nprob * g.nkind * m_pairs;
   const uint32_t max_cl = (uint32_t)(nsm / 2);
@@ -323,9 +351,7 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
 }
 
 uint32_t gemm_groups(uint32_t n_tiles) {
-  int nsm = 0;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  if (const char* e = std::getenv("IRISMPC_GEMM_SMS")) nsm = std::max(2, std::min(nsm, std::atoi(e)));
+  const int nsm = device_sms(cur_device());
   return std::max<uint32_t>(1, (uint32_t)(nsm / 2) / std::max<uint32_t>(1, n_tiles));
 }
 

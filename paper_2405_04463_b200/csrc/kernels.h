@@ -17,6 +17,9 @@ void debug_check(const char* what, cudaStream_t st);
 bool prof_on();
 void* prof_begin(cudaStream_t st);
 void prof_end(void* h, const char* name, cudaStream_t st);
+// runtime switch (irismpc_gpu_profile) and read-out of the per-kernel totals (resets them)
+void prof_enable(bool on);
+size_t prof_take(char (*names)[48], double* ms, uint64_t* launches, size_t max);
 
 // ---- variants (shares.hpp:28-48): ring widths of the hamming dot, the mask
 // dot (0 = public mask bits) and the comparison
@@ -187,7 +190,8 @@ struct ThrArgs {
   uint64_t match_w0;
   uint8_t* partial;      // [3][nslots]
   uint64_t nslots;
-  uint64_t or_elem_base; // OR-stream (stream id 1) element base of this launch
+  uint64_t or_stream;    // ChaCha stream id of the fused OR gates (or_stream_id(ctr, rank, 1))
+  uint64_t or_elem_base; // element base of this launch inside that stream
   // taps (tests), global-lane indexed, may be null
   uint32_t* tap_rs_hd;
   uint32_t* tap_rs_ml;
@@ -200,6 +204,10 @@ struct ThrArgs {
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
 // L1 tap of an RP field's chunk: out[p * n + col * S + row0 + row] = P2 + P(1|3) of (col, row)
+// row-sampled L1 tap (irismpc_gpu_tap_rows): out[p * out_pstride + col * k + i]
+void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                     uint64_t kstride, const uint64_t* rows, uint32_t k, uint64_t row0, void* out,
+                     uint64_t out_pstride, cudaStream_t st);
 void launch_rp_tap(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
                    uint64_t kstride, void* out, uint64_t n, uint64_t S, uint64_t row0, cudaStream_t st);
 
@@ -213,11 +221,23 @@ struct OrArgs {
   uint64_t pair_lane0;       // global lane of pair lane 0
   uint32_t persons, rot;
   SeedKey key[3];
-  uint64_t elem_base;        // OR stream (stream id 2) element base
+  uint64_t stream;           // ChaCha stream id (or_stream_id(ctr, rank, 2)); person P uses elements P << 40 ...
   uint8_t* out;              // [3][persons] component bits
 };
 void launch_or_persons(const OrArgs& a, cudaStream_t st);
 void launch_or_open(const uint8_t* partials, uint32_t G, uint32_t persons, const SeedKey key[3],
-                    uint64_t elem_base, uint8_t* match_out, cudaStream_t st);
+                    uint64_t stream, uint8_t* match_out, cudaStream_t st);
+
+// ChaCha stream ids of the OR-reduction gates (the reference's own draws all use
+// stream 0, prf.hpp:46-69): bit 63 set, a per-context 64-bit query counter
+// (never reused on a persistent context), the shard rank and the kind
+// (1 fused warp OR, 2 per-person OR, 3 cross-shard OR + open).  Every AND gate of
+// every query therefore draws its zero shares from its own stream positions.
+__host__ __device__ inline uint64_t or_stream_id(uint64_t ctr, uint32_t rank, uint32_t kind) {
+  return (1ull << 63) | ((ctr & ((1ull << 43) - 1)) << 20) | ((uint64_t)(rank & 0xFFFFu) << 4) | (kind & 0xFu);
+}
+// element windows of k_or_persons: person P's linear items at P << 40, its block tree above 2^39
+constexpr uint64_t kOrPersonShift = 40;
+constexpr uint64_t kOrTreeOffset = 1ull << 39;
 
 }  // namespace irisgpu

@@ -46,12 +46,12 @@ __global__ void __launch_bounds__(256) k_or_persons(const OrArgs A) {
   const uint64_t nslot = se - sb;
   const uint64_t npair = A.pair_match[0] ? (uint64_t)(A.persons - 1) * 4 * A.rot : 0;
   const uint64_t nitems = nslot + npair;
-  const uint64_t ebase = A.elem_base + ((uint64_t)P << 22);
+  const uint64_t ebase = (uint64_t)P << kOrPersonShift;
   uint32_t acc[3] = {0, 0, 0};
   for (uint64_t c = threadIdx.x; c * 8 < nitems; c += blockDim.x) {
     uint32_t blk[3][16];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) chacha12_block(A.key[k], ebase / 8 + c, 2, blk[k]);
+    for (int k = 0; k < 3; ++k) chacha12_block(A.key[k], ebase / 8 + c, A.stream, blk[k]);
     for (int w = 0; w < 8; ++w) {
       const uint64_t u = c * 8 + w;
       if (u >= nitems) break;
@@ -78,12 +78,12 @@ __global__ void __launch_bounds__(256) k_or_persons(const OrArgs A) {
   }
   // block tree: warp shuffles, then across the 8 warps
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t tb = ebase + (1ull << 21);
+  const uint64_t tb = ebase + kOrTreeOffset;
   for (int o = 16; o >= 1; o >>= 1) {
     uint32_t y[3], f[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) y[k] = __shfl_down_sync(0xffffffffu, acc[k], o);
-    rand_elem(A.key, 2, tb + (uint64_t)(5 - __ffs(o)) * 256 + threadIdx.x, f);
+    rand_elem(A.key, A.stream, tb + (uint64_t)(5 - __ffs(o)) * 256 + threadIdx.x, f);
     if (lane < o) or_bit(acc, y, f);
   }
   __shared__ uint32_t wsum[8][3];
@@ -94,17 +94,20 @@ __global__ void __launch_bounds__(256) k_or_persons(const OrArgs A) {
     uint32_t r[3] = {wsum[0][0], wsum[0][1], wsum[0][2]};
     for (int w = 1; w < (int)(blockDim.x / 32); ++w) {
       uint32_t f[3];
-      rand_elem(A.key, 2, tb + 5 * 256 + w, f);
+      rand_elem(A.key, A.stream, tb + 5 * 256 + w, f);
       or_bit(r, wsum[w], f);
     }
     for (int k = 0; k < 3; ++k) A.out[k * A.persons + P] = (uint8_t)r[k];
   }
 }
 
-// Final OR over G shard partials [G][3][persons] and the open at P1:
-// P2 and P3 both send their copy of component 2, P1 cross-checks and XORs.
+// Final OR over G shard partials [G][3][persons] and the open at P1
+// (open_bits_to, circuits.hpp:449-486).  In this co-resident component form each
+// XOR component exists once, so P1's cross-check of the two copies of component
+// 2 (circuits.hpp:470-472) has nothing to compare; party mode (party.cu), where
+// P2 and P3 really send their copies, performs it.
 __global__ void k_or_open(const uint8_t* __restrict__ partials, uint32_t G, uint32_t persons,
-                          SeedKey k1, SeedKey k2, SeedKey k3, uint64_t elem_base, uint8_t* match) {
+                          SeedKey k1, SeedKey k2, SeedKey k3, uint64_t stream, uint8_t* match) {
   const uint32_t P = blockIdx.x * blockDim.x + threadIdx.x;
   if (P >= persons) return;
   const SeedKey key[3] = {k1, k2, k3};
@@ -113,7 +116,7 @@ __global__ void k_or_open(const uint8_t* __restrict__ partials, uint32_t G, uint
   for (uint32_t g = 1; g < G; ++g) {
     uint32_t x[3], f[3];
     for (int k = 0; k < 3; ++k) x[k] = partials[((uint64_t)g * 3 + k) * persons + P] & 1u;
-    rand_elem(key, 3, elem_base + (uint64_t)P * 64 + g, f);
+    rand_elem(key, stream, ((uint64_t)P << 32) + g, f);
     or_bit(acc, x, f);
   }
   match[P] = (uint8_t)((acc[0] ^ acc[1] ^ acc[2]) & 1u);
@@ -125,10 +128,10 @@ void launch_or_persons(const OrArgs& a, cudaStream_t st) {
 }
 
 void launch_or_open(const uint8_t* partials, uint32_t G, uint32_t persons, const SeedKey key[3],
-                    uint64_t elem_base, uint8_t* match_out, cudaStream_t st) {
+                    uint64_t stream, uint8_t* match_out, cudaStream_t st) {
   if (!persons) return;
   k_or_open<<<(persons + 127) / 128, 128, 0, st>>>(partials, G, persons, key[0], key[1], key[2],
-                                                     elem_base, match_out);
+                                                     stream, match_out);
 }
 
 }  // namespace irisgpu

@@ -543,7 +543,7 @@ namespace {
 
 __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t task, const uint32_t bit_in[3],
                                       int lane, uint64_t (*orr)[40]) {
-  // 36 AND gates per warp, randomness from stream id 1 (elements E0 + gate)
+  // 36 AND gates per warp, randomness from the query's fused-OR stream (elements E0 + gate)
   const uint64_t E0 = A.or_elem_base + task * 64;
   __syncwarp();
   if (lane < 18) {
@@ -551,7 +551,7 @@ __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t 
     const uint64_t b = E0 / 8 + bo;
     if (b <= (E0 + 35) / 8) {
       uint32_t blk[16];
-      chacha12_block(A.key[k], b, 1, blk);
+      chacha12_block(A.key[k], b, A.or_stream, blk);
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
         const uint64_t e = b * 8 + w;
@@ -676,6 +676,46 @@ void launch_rp_tap(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncol
   else
     k_rp_tap<uint32_t><<<g, 256, 0, st>>>(static_cast<const uint32_t*>(P), nparty, ncols, rot, nr, kstride,
                                            static_cast<uint32_t*>(out), n, S, row0);
+}
+
+// Row-sampled L1 tap: for every sampled DB row inside this chunk, the per-party
+// dots of all its columns -> out[p * out_pstride + col * k + i] (i = the row's
+// index in the sample).  Plain [party][col][row] dots, or RP planes (kstride > 0).
+template <typename T>
+__global__ void k_tap_rows(const T* __restrict__ P, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                           uint64_t kstride, const uint64_t* __restrict__ rows, uint32_t k, uint64_t row0,
+                           T* __restrict__ out, uint64_t out_pstride) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (tid >= (uint64_t)nparty * ncols * k) return;
+  const uint32_t i = (uint32_t)(tid % k);
+  const uint64_t pc = tid / k, col = pc % ncols, p = pc / ncols;
+  const uint64_t row = rows[i];
+  if (row < row0 || row >= row0 + nr) return;
+  const uint64_t rr = row - row0;
+  T v;
+  if (kstride == 0) {
+    v = P[(p * ncols + col) * nr + rr];
+  } else {
+    const uint32_t npr = (rot + 1) / 2, j = (uint32_t)(col % rot);
+    const uint64_t cp = (col / rot) * npr + j / 2;
+    const uint64_t x = p * (npr * (ncols / rot)) * nr + cp * nr + rr;
+    v = (T)(P[x + kstride] + P[x + ((j & 1) ? 0 : 2 * kstride)]);
+  }
+  out[p * out_pstride + col * k + i] = v;
+}
+
+void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
+                     uint64_t kstride, const uint64_t* rows, uint32_t k, uint64_t row0, void* out,
+                     uint64_t out_pstride, cudaStream_t st) {
+  const uint64_t tot = (uint64_t)nparty * ncols * k;
+  if (!tot) return;
+  const unsigned g = (unsigned)((tot + 255) / 256);
+  if (elem_bytes == 2)
+    k_tap_rows<uint16_t><<<g, 256, 0, st>>>(static_cast<const uint16_t*>(P), nparty, ncols, rot, nr, kstride, rows, k,
+                                            row0, static_cast<uint16_t*>(out), out_pstride);
+  else
+    k_tap_rows<uint32_t><<<g, 256, 0, st>>>(static_cast<const uint32_t*>(P), nparty, ncols, rot, nr, kstride, rows, k,
+                                            row0, static_cast<uint32_t*>(out), out_pstride);
 }
 
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {

@@ -63,11 +63,31 @@ def test_prf_blocks_match_oracle_stream_positions():
 
 
 def test_compare_roofline_fields():
+    """Per-kernel serial times of one profiled query -> ChaCha12 rates; the chain
+    fraction = ChaCha floor / serial chain time."""
     b = _bench()
-    r = b.compare_roofline(20.0, 10_000_000, 1, {"hbm_gbs": 6500.0})
-    assert r["bound"] == "alu"
-    assert r["hbm"]["achieved"] == pytest.approx(12.75 * 1e7 / 0.02 / 1e9)
-    assert r["hbm"]["frac"] == pytest.approx(r["hbm"]["achieved"] / 6500.0)
-    assert r["chacha"]["achieved"] == pytest.approx(b.prf_blocks_per_lane(1) * 1e7 / 0.02)
-    if r["chacha"]["peak"]:
-        assert r["chacha"]["frac"] == pytest.approx(r["chacha"]["achieved"] / r["chacha"]["peak"])
+    lanes = 10_000_000
+    prof = {"k_gate_keystream": (2.0, 4), "k_reshare": (3.0, 4), "k_lift": (1.0, 4), "k_inject": (2.5, 4),
+            "k_msb": (1.5, 4), "k_limb_gemm_pair (hd)": (9.0, 8)}
+    r = b.compare_roofline(prof, lanes, 1, {"hbm_gbs": 6500.0})
+    assert set(r["kernels"]) == set(b.THRESHOLD_KERNELS)
+    ks = r["kernels"]["k_reshare"]
+    assert ks["chacha_blocks_per_s"] == pytest.approx(0.75 * lanes / 3e-3)
+    assert r["kernels"]["k_inject"]["chacha_blocks_per_lane"] == 1.0
+    assert r["kernels"]["k_gate_keystream"]["chacha_blocks_per_lane"] == pytest.approx(375 / 512)
+    tot = sum(b.kernel_blocks_per_lane(k, 1) for k in b.THRESHOLD_KERNELS)
+    assert tot == pytest.approx(b.prf_blocks_per_lane(1))  # the kernels account for every reference draw
+    assert r["chain"]["serial_ms"] == pytest.approx(10.0)
+    if r["chain"]["chacha_peak_blocks_per_s"]:
+        floor = b.prf_blocks_per_lane(1) * lanes / r["chain"]["chacha_peak_blocks_per_s"] * 1e3
+        assert r["chain"]["frac"] == pytest.approx(floor / 10.0)
+
+
+def test_workload_labels_name_baseline_configs():
+    b = _bench()
+    assert b.workload_name(1_000_000, 32, 1) == "configs[2]"
+    assert b.workload_name(100_000, 16, 1) == "configs[1]"
+    assert b.workload_name(10_000, 1, 1) == "configs[0]"
+    assert b.workload_name(1_000_000, 32, 4).startswith("configs[3]")
+    assert b.workload_name(5_000, 3, 1) == "custom shape"
+    assert b.ROWS_PER_GPU == 1_000_000 and b.PERSONS == 32 and b.REF_ROWS == 10_000

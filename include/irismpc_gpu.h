@@ -134,6 +134,28 @@ int irismpc_gpu_batch_query_partial(irismpc_gpu_ctx* ctx, const uint8_t* const d
 int irismpc_gpu_or_open(irismpc_gpu_ctx* ctx, const uint8_t* partials_dev, uint32_t G,
                         uint32_t persons, uint8_t* person_match_out);
 
+/* ---- the comparison phase alone (the reference's `bench --phase comparison`,
+ * PAPER Table 3) ------------------------------------------------------------
+ * irismpc_gpu_comparison_only   party_comparison_only / run_comparison_local
+ *                               (src/engine.cpp:448-515, src/cluster.cpp:97-145)
+ * irismpc_gpu_or_tree_only      party_or_tree_only / run_or_tree_local
+ *                               (src/engine.cpp:517-532, src/cluster.cpp:147-186)
+ * hd_payload[p] / ml_payload[p]: party p+1's replicated (own, prev) shares of
+ * each lane's masked dot and ml, little-endian at the variant's ring widths
+ * (plain-mask ml: one public LE u64 per lane, the same at every party) --
+ * exactly the reference's bench payloads.  lane_bits_out [lanes] (may be NULL)
+ * receives the opened per-lane MSB bits (tests); opened_out [1] the OR of all
+ * lanes opened at P1 when with_or_tree.  or_tree_only's payload[p]: per
+ * 64-lane word (own u64, prev u64).  stats: the analytic per-party ledger
+ * (lift incl. OT, msb, or_tree bytes and rounds) and device times.  Errors:
+ * 2 on payload sizes, 5 when a party's prev copy differs from its neighbour's own. */
+int irismpc_gpu_comparison_only(irismpc_gpu_ctx* ctx, const uint8_t* const hd_payload[3], const size_t hd_len[3],
+                                const uint8_t* const ml_payload[3], const size_t ml_len[3], uint64_t lanes,
+                                int with_or_tree, uint8_t* opened_out, uint8_t* lane_bits_out,
+                                irismpc_gpu_stats* stats);
+int irismpc_gpu_or_tree_only(irismpc_gpu_ctx* ctx, const uint8_t* const payload[3], const size_t len[3],
+                             uint64_t lanes, uint8_t* opened_out, irismpc_gpu_stats* stats);
+
 /* PRF stream positions (per seed); a fresh context starts at 0 like
  * run_parties; the reference CLI keeps PartyCtx across queries. */
 int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* ctx, uint64_t pos[3]);

@@ -526,3 +526,51 @@ def ref_engine_case(which: int, backend: int, variant: int):
         raise RuntimeError(f"ref_engine_case failed with status {rc}")
     n = int(s.value)
     return dc[:n].reshape(n, 1), dm[:n].reshape(n, 1), qc, qm, int(want.value), int(got.value)
+
+
+# ------------------------------------------------ comparison phase (_ref)
+
+def synth_lanes(n: int, l: int, seed: int):
+    """acceptance.cpp:48-58 synth_lanes / irismpc_cli.cpp:382-388: ml = below(l+1),
+    hd = below(ml+1), dot = ml - 2 hd, from Rng(seed)."""
+    rng = Rng(seed)
+    dots = np.zeros(n, np.int64)
+    mls = np.zeros(n, np.int64)
+    for i in range(n):
+        ml = rng.below(l + 1)
+        hd = rng.below(ml + 1)
+        mls[i] = ml
+        dots[i] = ml - 2 * hd
+    return dots, mls
+
+
+def ref_comparison_local(variant: int, dots, mls, with_or: bool, seed: int):
+    R = ref()
+    R.ref_comparison_local.argtypes = [C.c_int, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int,
+                                       C.c_uint64, u8p, u64p, C.POINTER(C.c_double)]
+    d = np.ascontiguousarray(dots, np.int64)
+    m = np.ascontiguousarray(mls, np.int64)
+    op = C.c_uint8(0)
+    led = np.zeros(12, np.uint64)
+    wall = C.c_double(0)
+    rc = R.ref_comparison_local(variant, d.size, d.ctypes.data_as(C.POINTER(C.c_int64)),
+                                m.ctypes.data_as(C.POINTER(C.c_int64)), 1 if with_or else 0, seed, C.byref(op),
+                                _p(led, u64p), C.byref(wall))
+    if rc:
+        raise RuntimeError(f"ref_comparison_local failed with status {rc}")
+    keys = ("lift", "ot", "msb", "or_tree")
+    return dict(opened=int(op.value), wall_ms=wall.value,
+                ledger=[{k: int(led[4 * p + i]) for i, k in enumerate(keys)} for p in range(3)])
+
+
+def ref_or_tree_local(bits, seed: int):
+    R = ref()
+    R.ref_or_tree_local.argtypes = [C.c_uint64, u8p, C.c_uint64, u8p, u64p, C.POINTER(C.c_double)]
+    b = np.ascontiguousarray(bits, np.uint8)
+    op = C.c_uint8(0)
+    ob = np.zeros(3, np.uint64)
+    wall = C.c_double(0)
+    rc = R.ref_or_tree_local(b.size, _p(b, u8p), seed, C.byref(op), _p(ob, u64p), C.byref(wall))
+    if rc:
+        raise RuntimeError(f"ref_or_tree_local failed with status {rc}")
+    return dict(opened=int(op.value), or_bytes=[int(x) for x in ob], wall_ms=wall.value)

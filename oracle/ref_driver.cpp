@@ -658,4 +658,49 @@ int ref_engine_case(int which, int backend, int variant, std::uint64_t* db_codes
   }
 }
 
+// --- the comparison phase alone (the reference's `bench --phase comparison`) ---
+
+// run_comparison_local (cluster.cpp:97-145) on plaintext (masked dot, ml)
+// lanes: opened aggregate (with_or), per-party ledger bytes of the lift, ot,
+// msb and or_tree phases ([3][4]) and the slowest party's wall ms.
+int ref_comparison_local(int variant, std::uint64_t n, const std::int64_t* dots, const std::int64_t* mls,
+                         int with_or, std::uint64_t seed, std::uint8_t* opened, std::uint64_t* ledger,
+                         double* wall_ms) {
+  try {
+    EngineConfig cfg;
+    cfg.backend = Backend::replicated;
+    cfg.variant = static_cast<Variant>(variant);
+    cfg.l = 12800;
+    cfg.params = MatchParams::make(0.375, 16);
+    std::vector<std::pair<std::int64_t, std::int64_t>> lanes(n);
+    for (std::uint64_t i = 0; i < n; ++i) lanes[i] = {dots[i], mls[i]};
+    const auto out = run_comparison_local(cfg, lanes, with_or != 0, seed);
+    for (int p = 0; p < 3; ++p) {
+      ledger[4 * p + 0] = out.ledgers[p].phase(Phase::lift).bytes_sent;
+      ledger[4 * p + 1] = out.ledgers[p].phase(Phase::ot).bytes_sent;
+      ledger[4 * p + 2] = out.ledgers[p].phase(Phase::msb).bytes_sent;
+      ledger[4 * p + 3] = out.ledgers[p].phase(Phase::or_tree).bytes_sent;
+    }
+    if (opened) *opened = out.party[0].opened.empty() ? 0 : out.party[0].opened[0];
+    if (wall_ms) *wall_ms = out.wall_ms;
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
+// run_or_tree_local (cluster.cpp:147-186): opened OR, or_tree bytes per party, wall ms
+int ref_or_tree_local(std::uint64_t n, const std::uint8_t* bits, std::uint64_t seed, std::uint8_t* opened,
+                      std::uint64_t* or_bytes, double* wall_ms) {
+  try {
+    const auto out = run_or_tree_local(std::span<const std::uint8_t>(bits, n), seed);
+    for (int p = 0; p < 3; ++p) or_bytes[p] = out.ledgers[p].phase(Phase::or_tree).bytes_sent;
+    *opened = out.aggregate ? 1 : 0;
+    if (wall_ms) *wall_ms = out.wall_ms;
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
 }  // extern "C"

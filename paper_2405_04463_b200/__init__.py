@@ -41,7 +41,7 @@ EXPORTED = [
     "irismpc_gpu_or_open", "irismpc_gpu_get_stream_positions", "irismpc_gpu_set_stream_positions",
     "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
     "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap", "irismpc_gpu_profile", "irismpc_gpu_profile_read",
-    "irismpc_gpu_tap_rows",
+    "irismpc_gpu_tap_rows", "irismpc_gpu_comparison_only", "irismpc_gpu_or_tree_only",
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
@@ -164,6 +164,8 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_enable_taps.argtypes = [vp, C.c_int]
         L.irismpc_gpu_profile.argtypes = [vp, C.c_int]
         L.irismpc_gpu_tap_rows.argtypes = [vp, u64p, C.c_uint32]
+        L.irismpc_gpu_comparison_only.argtypes = [vp, P3, S3, P3, S3, C.c_uint64, C.c_int, vp, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_or_tree_only.argtypes = [vp, P3, S3, C.c_uint64, vp, C.POINTER(Stats)]
         L.irismpc_gpu_profile_read.argtypes = [vp, vp, vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
         cp3 = C.c_char_p * 3
@@ -431,6 +433,31 @@ class Session:
         self._check(lib().irismpc_gpu_or_open(self._h, _ptr(partials), G, persons, out.ctypes.data))
         return out[:persons]
 
+    # -- the comparison phase alone ---------------------------------------------
+    def comparison_only(self, hd_payloads, ml_payloads, lanes: int, with_or_tree: bool = False,
+                        want_bits: bool = False):
+        """party_comparison_only for all three parties (engine.cpp:448-515): returns
+        (opened aggregate or None, opened per-lane MSB bits or None)."""
+        hp = [np.ascontiguousarray(x, np.uint8) for x in hd_payloads]
+        mp = [np.ascontiguousarray(x, np.uint8) for x in ml_payloads]
+        op = np.zeros(1, np.uint8)
+        bits = np.zeros(max(1, lanes), np.uint8) if want_bits else None
+        self._check(lib().irismpc_gpu_comparison_only(
+            self._h, (vp * 3)(*[a.ctypes.data for a in hp]), (C.c_size_t * 3)(*[a.nbytes for a in hp]),
+            (vp * 3)(*[a.ctypes.data for a in mp]), (C.c_size_t * 3)(*[a.nbytes for a in mp]), lanes,
+            1 if with_or_tree else 0, op.ctypes.data, bits.ctypes.data if want_bits else None,
+            C.byref(self.last_stats)))
+        return (int(op[0]) if with_or_tree else None), (bits[:lanes] if want_bits else None)
+
+    def or_tree_only(self, payloads, lanes: int) -> int:
+        """party_or_tree_only for all three parties (engine.cpp:517-532): the opened OR."""
+        pp = [np.ascontiguousarray(x, np.uint8) for x in payloads]
+        op = np.zeros(1, np.uint8)
+        self._check(lib().irismpc_gpu_or_tree_only(self._h, (vp * 3)(*[a.ctypes.data for a in pp]),
+                                                   (C.c_size_t * 3)(*[a.nbytes for a in pp]), lanes,
+                                                   op.ctypes.data, C.byref(self.last_stats)))
+        return int(op[0])
+
     # -- streams / taps --------------------------------------------------------
     def stream_positions(self) -> np.ndarray:
         p = np.zeros(3, np.uint64)
@@ -488,6 +515,42 @@ class Session:
         if tap == TAP_DIFF and kc == 16:
             return out.astype(np.uint16)
         return out
+
+
+def share_lane_values(values, bits: int, rng: np.random.Generator):
+    """Replicated 3-party shares of signed per-lane values in Z_2^bits as the
+    three parties' bench payloads: party p holds (own = x_p, prev = x_{p-1}),
+    little-endian (emit_rep_share_list, src/cluster.cpp:83-95; any uniformly
+    random sharing -- the opened outputs do not depend on it)."""
+    v = np.asarray(values, np.int64)
+    mod = 1 << bits
+    dt = np.uint16 if bits == 16 else np.uint32
+    x1 = rng.integers(0, mod, v.size, dtype=np.uint64)
+    x2 = rng.integers(0, mod, v.size, dtype=np.uint64)
+    x3 = (v.astype(np.uint64) - x1 - x2) % np.uint64(mod)
+    xs = [x1.astype(dt), x2.astype(dt), x3.astype(dt)]
+    out = []
+    for p in range(3):
+        pair = np.empty((v.size, 2), dt)
+        pair[:, 0] = xs[p]
+        pair[:, 1] = xs[(p + 2) % 3]
+        out.append(pair.view(np.uint8).ravel())
+    return out
+
+
+def share_bit_words(bits, rng: np.random.Generator):
+    """Replicated XOR shares of a lane bit vector as party payloads of
+    (own u64, prev u64) per 64-lane word (run_or_tree_local, cluster.cpp:147-165)."""
+    b = np.asarray(bits, np.uint8)
+    W = (b.size + 63) // 64
+    padded = np.zeros(64 * W, np.uint8)
+    padded[:b.size] = b
+    plain = np.packbits(padded, bitorder="little").view(np.uint64)
+    x1 = rng.integers(0, 2**63, W, dtype=np.uint64) ^ (rng.integers(0, 2, W, dtype=np.uint64) << np.uint64(63))
+    x2 = rng.integers(0, 2**63, W, dtype=np.uint64) ^ (rng.integers(0, 2, W, dtype=np.uint64) << np.uint64(63))
+    x3 = plain ^ x1 ^ x2
+    xs = [x1, x2, x3]
+    return [np.stack([xs[p], xs[(p + 2) % 3]], 1).view(np.uint8).ravel() for p in range(3)]
 
 
 def _dealt_on_device(sess: Session, codes: np.ndarray, masks: np.ndarray, seed: int, tag: int):

@@ -4,6 +4,7 @@
     python -m paper_2405_04463_b200.cli share --db db.irmp --backend shamir-galois --variant all --out-dir shares
     python -m paper_2405_04463_b200.cli query --shares shares --query q.irmp --batch 16 --variant all --stats st.json
     python -m paper_2405_04463_b200.cli bench --phase full --db-size 100000 --variant mpc-lift --json b.json
+    python -m paper_2405_04463_b200.cli bench [--phase comparison] --comparisons 100000 --variant all
 
 Same subcommands, options, file names (db.<variant>.p<k>.irs, seeds.p<k>.irsd),
 dealer seeds/tags, stdout lines, stats JSON (stats_to_json, irismpc_cli.cpp:103-119)
@@ -172,12 +173,88 @@ def cmd_query(a) -> int:
     return 0
 
 
+# PAPER.md:477-485 (Table 3): comparison phase, 100k parallel comparisons, Ryzen 9
+# 7950X, one thread per party: ms, M elements/s, kB per party
+PAPER_TABLE3 = {"plain-mask": (3.18, 31.4, 362), "mpc-lift": (14.47, 6.9, 2138), "const-lift": (5.32, 18.8, 763),
+                "no-lift": (5.27, 19.0, 763), "or-tree": (0.87, 114.9, 12)}
+
+
+def cmd_bench_comparison(a) -> int:
+    """bench --phase comparison (cmd_bench, irismpc_cli.cpp:373-458; the CLI's
+    default): each variant's comparison phase alone (party_comparison_only) over
+    replicated shares of synthetic (masked dot, ml) lanes -- ml uniform in
+    [0, l], hd uniform in [0, ml], dot = ml - 2 hd -- then the OR-tree row
+    (party_or_tree_only over `comparisons` bits with one planted 1).  Best of
+    --repeat device times; kB/party = (lift + ot + msb bytes) averaged over the
+    parties, or_tree bytes without the final 1-bit open, as the reference prints.
+    The lane values come from numpy rather than the reference's Rng(1) (no
+    column depends on them)."""
+    n = a.comparisons
+    variants = [P.PLAIN_MASK, P.MPC_LIFT, P.CONST_LIFT, P.NO_LIFT] if a.variant == "all" else [P.VARIANTS[a.variant]]
+    rng = np.random.default_rng(1)
+    ml = rng.integers(0, a.length + 1, n)
+    hd = (rng.random(n) * (ml + 1)).astype(np.int64)
+    dot = ml - 2 * hd
+    rows = []
+    print(f"{'protocol':<12} {'ms':>10} {'cmp/s':>14} {'kB/party':>10} {'B/cmp':>8}   paper Table 3 (7950X): ms, "
+          f"M el/s, kB")
+    for v in variants:
+        kh, km, _ = P.VARIANT_WIDTHS[v]
+        cfg = P.EngineConfig(backend=P.REPLICATED, l=a.length, rotations=1, variant=v)
+        sess = P.Session(cfg, master_seed=777)
+        hp = P.share_lane_values(dot, kh, rng)
+        mp = P.share_lane_values(ml, km, rng) if km else [ml.astype("<u8").view(np.uint8)] * 3
+        best, rounds, kb = 1e30, 0, 0.0
+        for _ in range(a.repeat):
+            sess.comparison_only(hp, mp, n)
+            st = sess.last_stats
+            best = min(best, st.wall_ms)
+            kb = sum(st.lift_bytes[p] + st.msb_bytes[p] for p in range(3)) / 3 / 1000
+            rounds = st.lift_rounds + st.msb_rounds
+        sess.close()
+        name = VARIANT_NAMES[v]
+        pt = PAPER_TABLE3[name]
+        print(f"{name:<12} {best:>10.3f} {n / (best / 1e3):>14.0f} {kb:>10.1f} {kb * 1000 / n:>8.2f}   "
+              f"{pt[0]:>6.2f} {pt[1]:>6.1f} {pt[2]:>6}")
+        rows.append({"protocol": name, "comparisons": n, "ms": best, "throughput_per_s": n / (best / 1e3),
+                     "kb_per_party": kb, "bytes_per_comparison": kb * 1000 / n, "rounds": rounds,
+                     "paper_table3": {"ms": pt[0], "m_el_per_s": pt[1], "kb_per_party": pt[2]}})
+    bits = np.zeros(n, np.uint8)
+    if n > 1:
+        bits[n // 2] = 1
+    sess = P.Session(P.EngineConfig(backend=P.REPLICATED, l=a.length, rotations=1), master_seed=778)
+    pay = P.share_bit_words(bits, rng)
+    best, kb, rounds = 1e30, 0.0, 0
+    for _ in range(a.repeat):
+        opened = sess.or_tree_only(pay, n)
+        st = sess.last_stats
+        best = min(best, st.wall_ms)
+        kb = (sum(st.or_tree_bytes[p] for p in range(3)) - 2) / 3 / 1000
+        rounds = st.or_tree_rounds - 1
+    if opened != int(bits.any()):
+        raise P.IrisError("or-tree lost the planted bit")
+    pt = PAPER_TABLE3["or-tree"]
+    print(f"{'or-tree':<12} {best:>10.3f} {n / (best / 1e3):>14.0f} {kb:>10.1f} {kb * 1000 / n:>8.2f}   "
+          f"{pt[0]:>6.2f} {pt[1]:>6.1f} {pt[2]:>6}")
+    rows.append({"protocol": "or-tree", "comparisons": n, "ms": best, "throughput_per_s": n / (best / 1e3),
+                 "kb_per_party": kb, "rounds": rounds,
+                 "paper_table3": {"ms": pt[0], "m_el_per_s": pt[1], "kb_per_party": pt[2]}})
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(rows, f, indent=2)
+            f.write("\n")
+    return 0
+
+
 def cmd_bench(a) -> int:
     """bench --phase full (cmd_bench_full, irismpc_cli.cpp:336-372): a membership query
     of random_record after the DB (Rng(2) stream) against a db_size-row DB dealt with
-    seed 900 + r per repetition; best QueryStats.wall_ms (device time here)."""
+    seed 900 + r per repetition; best QueryStats.wall_ms (device time here).
+    --phase comparison (the default, as in the reference): cmd_bench_comparison."""
+    if a.phase == "comparison":
+        return cmd_bench_comparison(a)
     if a.phase != "full":
-        raise P.ConfigError("the B200 path runs whole queries only: use --phase full")
+        raise P.ConfigError("--phase must be comparison or full")
     import torch
     backend = BACKENDS[a.backend]
     v = P.MPC_LIFT if a.variant == "all" else P.VARIANTS[a.variant]
@@ -233,9 +310,10 @@ def main(argv=None) -> int:
     q.add_argument("--length", type=int, default=12800)
     q.add_argument("--match-ratio", type=float, default=0.375, dest="match_ratio")
     q.add_argument("--rotations", type=int, default=31)
-    b = sub.add_parser("bench", help="whole-query benchmark")
-    b.add_argument("--phase", default="full")
-    b.add_argument("--variant", default="mpc-lift")
+    b = sub.add_parser("bench", help="comparison-phase (Table-style) or whole-query benchmark")
+    b.add_argument("--phase", default="comparison")
+    b.add_argument("--comparisons", type=int, default=100000)
+    b.add_argument("--variant", default="all")
     b.add_argument("--backend", default="replicated", choices=list(BACKENDS))
     b.add_argument("--repeat", type=int, default=3)
     b.add_argument("--length", type=int, default=12800)

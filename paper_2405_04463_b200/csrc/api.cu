@@ -776,6 +776,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     // stream layout: reshare n (+ n), lift 64W + inject, msb
     const uint64_t inj = V == kMpcLift ? 64 * W + (k == 0 ? 2 * n : (k == 1 ? 0 : 6 * n)) : 0;
     ta.lift_base[k] = c->pos[k] + n + nml;
+    ta.inj_base[k] = ta.lift_base[k] + 64 * W;
     ta.msb_base[k] = c->pos[k] + n + nml + inj;
   }
   ta.nlift = nlift;
@@ -1091,6 +1092,262 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   return 0;
 }
 
+// The comparison phase alone: party_comparison_only / run_comparison_local
+// (src/engine.cpp:448-515, src/cluster.cpp:97-145) over replicated shares of
+// per-lane (masked dot, ml) values, then optionally the OR over all lanes and
+// the open at P1 (with_or_tree).  Same K4 kernels as a batch query without the
+// reshare (the inputs are already replicated shares), so every PRF offset is
+// the batch query's minus the reshare draws.  Lanes run as jobs of at most
+// 2^24 lanes on one stream.  mode 1: or_tree_only (party_or_tree_only,
+// engine.cpp:517-532): hd = bit-share payload, ml unused.
+int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const size_t hd_len[3],
+                const uint8_t* const ml[3], const size_t ml_len[3], uint64_t n, int with_or, uint8_t* opened_out,
+                uint8_t* lane_bits_out, irismpc_gpu_stats* stats) {
+  const int V = c->variant;
+  const VariantWidths vw = c->vw;
+  const bool or_only = mode == 1;
+  const int hw = vw.kh / 8, mw = vw.km ? vw.km / 8 : 8;
+  const uint64_t W = ceil_div(n, 64);
+  if (or_only) {
+    for (int p = 0; p < 3; ++p)
+      if (hd_len[p] != W * 16) return fail(c, IRISMPC_GPU_ERR_CONFIG, "or-tree payload size mismatch");
+  } else {
+    for (int p = 0; p < 3; ++p) {
+      if (hd_len[p] != n * 2 * hw) return fail(c, IRISMPC_GPU_ERR_CONFIG, "bench payload size mismatch");
+      if (ml_len[p] != n * (vw.km ? 2 * mw : 8)) return fail(c, IRISMPC_GPU_ERR_CONFIG, "bench ml payload size mismatch");
+    }
+  }
+  cudaStream_t st = c->st;
+  uint64_t launches = 0;
+  CK(c, cudaEventRecord(c->ev[0], st));
+  // inputs: H2D of the three payloads, parse into components
+  Buf in_h[3], in_m[3], bad;
+  const uint64_t hb = hw, mb = vw.km ? mw : 2;
+  if (bad.ensure(sizeof(int))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+  CK(c, cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  for (int p = 0; p < 3; ++p) {
+    if (in_h[p].ensure(hd_len[p] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (bench payload)");
+    CK(c, cudaMemcpyAsync(in_h[p].p, hd[p], hd_len[p], cudaMemcpyHostToDevice, st));
+    if (!or_only) {
+      if (in_m[p].ensure(ml_len[p] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (bench payload)");
+      CK(c, cudaMemcpyAsync(in_m[p].p, ml[p], ml_len[p], cudaMemcpyHostToDevice, st));
+    }
+  }
+  const uint8_t* ph[3] = {in_h[0].as<uint8_t>(), in_h[1].as<uint8_t>(), in_h[2].as<uint8_t>()};
+  const uint8_t* pm[3] = {in_m[0].as<uint8_t>(), in_m[1].as<uint8_t>(), in_m[2].as<uint8_t>()};
+  const uint64_t match_words = 2 * W + 1;
+  for (int p = 0; p < 3; ++p) {
+    if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
+    CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
+  }
+  const uint64_t nparty_m = vw.km ? 3 : 1;
+  if (!or_only) {
+    if (c->dots.ensure(3 * n * hb + nparty_m * n * mb + 64)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (components)");
+    uint8_t* comp_h = c->dots.as<uint8_t>();
+    uint8_t* comp_m = comp_h + round_up(3 * n * hb, 16);
+    launch_parse_lane_shares(ph, n, hw, comp_h, bad.as<int>(), st);
+    launch_parse_lane_shares(pm, n, vw.km ? mw : 8, comp_m, bad.as<int>(), st);
+  } else {
+    // component words straight into the match buffers (2 u32 per 64-lane word)
+    Buf tmp;
+    if (tmp.ensure(3 * 2 * W * 4 + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    launch_parse_bit_shares(ph, W, n, tmp.as<uint32_t>(), bad.as<int>(), st);
+    for (int p = 0; p < 3; ++p)
+      CK(c, cudaMemcpyAsync(c->match[p].p, tmp.as<uint32_t>() + p * 2 * W, 2 * W * 4, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaStreamSynchronize(st));
+    tmp.release();
+  }
+  launches += or_only ? 1 : 2;
+  CK(c, cudaGetLastError());
+  {
+    int h = 0;
+    CK(c, cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    if (h) return fail(c, IRISMPC_GPU_ERR_INCONSISTENT, "replicated share cross-check failed (bench payload)");
+  }
+  CK(c, cudaEventRecord(c->ev[1], st));
+
+  const uint32_t nlift = V == kMpcLift ? 64u : 0u;
+  const uint32_t ngates = nlift + 2u * vw.kc - 3u;
+  auto seg_tasks = [](uint64_t lb, uint64_t le) { return (le - 1) / 1024 - lb / 1024 + 1; };
+  const uint64_t kJob = 1ull << 24;
+  const uint64_t njobs = or_only ? 0 : ceil_div(n, kJob);
+  uint64_t total_slots = 0;
+  ThrArgs ta{};
+  ta.variant = V;
+  ta.n = n;
+  ta.W = W;
+  ta.no_reshare = 1;
+  for (int k = 0; k < 3; ++k) {
+    ta.pos[k] = c->pos[k];
+    ta.key[k] = c->keys[k];
+    const uint64_t inj = V == kMpcLift ? 64 * W + (k == 0 ? 2 * n : (k == 1 ? 0 : 6 * n)) : 0;
+    ta.lift_base[k] = c->pos[k];
+    ta.inj_base[k] = c->pos[k] + 64 * W;
+    ta.msb_base[k] = c->pos[k] + inj;
+  }
+  ta.nlift = nlift;
+  ta.ngates = ngates;
+  ta.a = c->cfg.a;
+  ta.b = c->cfg.b;
+  ta.coef = 1.0 - 2.0 * c->cfg.match_ratio;
+  const uint64_t octr = ++c->or_ctr;
+  c->query_id++;
+  ta.or_stream = or_stream_id(octr, c->cfg.shard_rank, 1);
+  for (int p = 0; p < 3; ++p) ta.match[p] = c->match[p].as<uint32_t>();
+  ta.match_w0 = 0;
+  if (njobs) {
+    if (ensure_host_segs(c, njobs + 1)) return IRISMPC_GPU_ERR_DEVICE;
+    if (c->segs.ensure((njobs + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
+    uint64_t max_g = 0, max_t = 0;
+    for (uint64_t j = 0; j < njobs; ++j) {
+      Seg& sg = c->h_segs_pinned[j];
+      sg = Seg{};
+      sg.lane_begin = j * kJob;
+      sg.lane_end = std::min<uint64_t>(n, (j + 1) * kJob);
+      sg.src = 0;
+      sg.task_begin = 0;
+      sg.q_first = sg.lane_begin / 1024;
+      sg.w_first = sg.lane_begin / 64;
+      sg.g_off = 0;
+      sg.grp_begin = 0;
+      sg.gblk_begin = 0;
+      sg.slot = with_or ? (int64_t)total_slots : -1;
+      const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
+      total_slots += seg_tasks(sg.lane_begin, sg.lane_end);
+      max_g = std::max<uint64_t>(max_g, 3ull * ngates * gate_row_words(nw));
+      max_t = std::max<uint64_t>(max_t, seg_tasks(sg.lane_begin, sg.lane_end));
+    }
+    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, njobs * sizeof(Seg), cudaMemcpyHostToDevice, st));
+    const uint64_t cs = round_up(kJob, 8);
+    if (c->ml_rs.ensure((V == kMpcLift ? 3 * cs * sizeof(uint16_t) : 0) + 16) ||
+        c->diff.ensure(3 * cs * sizeof(uint32_t) + 16) || c->gate.ensure(max_g * sizeof(uint64_t) + 16) ||
+        c->bits.ensure((V == kMpcLift ? 6 * max_t * 32 * sizeof(uint32_t) : 0) + 16) ||
+        c->partial.ensure(3 * total_slots + 16))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
+    ta.ml_rs = c->ml_rs.as<uint16_t>();
+    ta.diff = c->diff.as<uint32_t>();
+    ta.cstride = cs;
+    ta.gate = c->gate.as<uint64_t>();
+    ta.bits = c->bits.as<uint32_t>();
+    ta.partial = c->partial.as<uint8_t>();
+    ta.nslots = total_slots;
+    uint8_t* comp_h = c->dots.as<uint8_t>();
+    uint8_t* comp_m = comp_h + round_up(3 * n * hb, 16);
+    uint64_t task_off = 0;
+    for (uint64_t j = 0; j < njobs; ++j) {
+      const Seg& sg = c->h_segs_pinned[j];
+      const uint64_t nl = sg.lane_end - sg.lane_begin;
+      const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
+      ThrArgs t = ta;
+      t.segs = c->segs.as<Seg>() + j;
+      t.nsegs = 1;
+      t.ntasks = seg_tasks(sg.lane_begin, sg.lane_end);
+      t.ngrp = (sg.lane_end - 1) / 8 - sg.lane_begin / 8 + 1;
+      t.ngblk = 3ull * ngates * (nw / 8 + 2);
+      t.ks_seg_threads = (uint32_t)t.ngblk;
+      t.grp_seg_max = (uint32_t)t.ngrp;
+      t.task_seg_max = (uint32_t)t.ntasks;
+      t.nbits = t.ntasks * 32;
+      t.or_elem_base = task_off * 64;
+      task_off += t.ntasks;
+      for (int p = 0; p < 3; ++p) {
+        t.hd[p] = comp_h + (p * n + sg.lane_begin) * hb;
+        t.ml[p] = comp_m + ((vw.km ? p : 0) * n + sg.lane_begin) * mb;
+      }
+      (void)nl;
+      launch_threshold(t, st);
+      CK(c, cudaGetLastError());
+      launches += V == kMpcLift ? 5 : 3;
+    }
+  }
+  if (or_only) {
+    total_slots = ceil_div(n, 1024);
+    if (c->partial.ensure(3 * total_slots + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or slots)");
+    ThrArgs t = ta;
+    t.ntasks = total_slots;
+    t.partial = c->partial.as<uint8_t>();
+    t.nslots = total_slots;
+    t.or_elem_base = 0;
+    launch_or_bits(t, st);
+    CK(c, cudaGetLastError());
+    ++launches;
+  }
+  CK(c, cudaEventRecord(c->ev[3], st));
+  const bool do_or = or_only || with_or;
+  if (do_or) {
+    std::vector<uint64_t> sb = {0, total_slots};
+    if (c->slot_begin.ensure(2 * sizeof(uint64_t)) || c->person_out.ensure(3 + 16) || c->open_out.ensure(16))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or buffers)");
+    CK(c, cudaMemcpyAsync(c->slot_begin.p, sb.data(), 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    OrArgs oa{};
+    oa.partial = c->partial.as<uint8_t>();
+    oa.nslots = total_slots;
+    oa.slot_begin = c->slot_begin.as<uint64_t>();
+    oa.persons = 1;
+    oa.rot = 1;
+    for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
+    oa.stream = or_stream_id(octr, c->cfg.shard_rank, 2);
+    oa.out = c->person_out.as<uint8_t>();
+    launch_or_persons(oa, st);
+    launch_or_open(c->person_out.as<uint8_t>(), 1, 1, c->keys, or_stream_id(octr, c->cfg.shard_rank, 3),
+                   c->open_out.as<uint8_t>(), st);
+    CK(c, cudaGetLastError());
+    launches += 2;
+    if (opened_out) CK(c, cudaMemcpyAsync(opened_out, c->open_out.p, 1, cudaMemcpyDeviceToHost, st));
+  }
+  CK(c, cudaEventRecord(c->ev[4], st));
+  if (lane_bits_out && !or_only) {
+    std::vector<uint32_t> w[3];
+    const uint64_t nw = ceil_div(n, 32);
+    for (int p = 0; p < 3; ++p) {
+      w[p].resize(nw);
+      CK(c, cudaMemcpyAsync(w[p].data(), c->match[p].p, nw * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(c, cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n; ++i)
+      lane_bits_out[i] = (uint8_t)(((w[0][i / 32] ^ w[1][i / 32] ^ w[2][i / 32]) >> (i % 32)) & 1u);
+  }
+  CK(c, cudaStreamSynchronize(st));
+  for (int p = 0; p < 3; ++p) {
+    in_h[p].release();
+    in_m[p].release();
+  }
+  bad.release();
+  // advance the streams as the reference's comparison / or-tree call does
+  uint64_t or_rounds = 0, or_bytes = 0;
+  const uint64_t ord = do_or ? ref_or_draws(1, n, &or_rounds, &or_bytes) : 0;
+  const uint64_t msb_draws = or_only ? 0 : (uint64_t)(2 * vw.kc - 3) * W;
+  for (int k = 0; k < 3; ++k) c->pos[k] = (or_only ? c->pos[k] : ta.msb_base[k] + msb_draws) + ord;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->batch = 1;
+    stats->lanes = n;
+    const uint64_t nb8 = ceil_div(n, 8);
+    for (int p = 0; p < 3; ++p) {
+      if (!or_only) {
+        stats->lift_bytes[p] = V == kMpcLift ? 64 * nb8 + (p == 0 ? 8 * n : 4 * n) : 0;
+        stats->msb_bytes[p] = (uint64_t)(2 * vw.kc - 3) * nb8;
+      }
+      stats->or_tree_bytes[p] = do_or ? or_bytes + (p == 0 ? 0 : 1) : 0;
+    }
+    stats->lift_rounds = (!or_only && V == kMpcLift) ? 21 : 0;
+    stats->msb_rounds = or_only ? 0 : (uint64_t)vw.kc - 1;
+    stats->or_tree_rounds = do_or ? or_rounds + 1 : 0;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
+    stats->wall_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    stats->prep_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]);
+    stats->threshold_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
+    stats->or_ms = ms;
+    stats->kernel_launches = launches;
+  }
+  return 0;
+}
+
 }  // namespace
 
 // =========================================================================== ABI
@@ -1389,6 +1646,25 @@ int irismpc_gpu_or_open(irismpc_gpu_ctx* c, const uint8_t* partials_dev, uint32_
   CK(c, cudaMemcpyAsync(person_match_out, c->open_out.p, persons, cudaMemcpyDeviceToHost, c->st));
   CK(c, cudaStreamSynchronize(c->st));
   return 0;
+}
+
+int irismpc_gpu_comparison_only(irismpc_gpu_ctx* c, const uint8_t* const hd_payload[3], const size_t hd_len[3],
+                                const uint8_t* const ml_payload[3], const size_t ml_len[3], uint64_t lanes,
+                                int with_or_tree, uint8_t* opened_out, uint8_t* lane_bits_out,
+                                irismpc_gpu_stats* stats) {
+  if (!c || !hd_payload || !ml_payload) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  if (lanes == 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no lanes");
+  return run_compare(c, 0, hd_payload, hd_len, ml_payload, ml_len, lanes, with_or_tree, opened_out, lane_bits_out,
+                     stats);
+}
+
+int irismpc_gpu_or_tree_only(irismpc_gpu_ctx* c, const uint8_t* const payload[3], const size_t len[3],
+                             uint64_t lanes, uint8_t* opened_out, irismpc_gpu_stats* stats) {
+  if (!c || !payload) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  if (lanes == 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no lanes");
+  return run_compare(c, 1, payload, len, nullptr, nullptr, lanes, 1, opened_out, nullptr, stats);
 }
 
 int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* c, uint64_t pos[3]) {

@@ -179,6 +179,8 @@ struct ThrArgs {
   // gates [nlift, ngates) the MSB adder at msb_base[k] + (g - nlift) W
   uint32_t nlift, ngates;
   uint64_t lift_base[3], msb_base[3];
+  uint64_t inj_base[3];  // bit_inject<15> draws of seeds 1 / 3 (mpc-lift): lift_base + 64 W
+  int no_reshare;        // comparison-only (party_comparison_only): inputs are already replicated shares
   // chunk work buffers
   uint64_t* gate;        // gate randomness, per segment [3*ngates][nwords]
   uint16_t* ml_rs;       // [3][cstride] reshared ml
@@ -203,6 +205,13 @@ struct ThrArgs {
 // words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
+// comparison phase alone (party_comparison_only / party_or_tree_only, engine.cpp:448-532)
+void launch_parse_lane_shares(const uint8_t* const p[3], uint64_t lanes, int width, void* out, int* bad,
+                              cudaStream_t st);
+void launch_parse_bit_shares(const uint8_t* const p[3], uint64_t words, uint64_t lanes, uint32_t* out, int* bad,
+                             cudaStream_t st);
+// OR of the component bit words a.match[3] (a.n lanes) into a.ntasks partial slots
+void launch_or_bits(const ThrArgs& a, cudaStream_t st);
 // L1 tap of an RP field's chunk: out[p * n + col * S + row0 + row] = P2 + P(1|3) of (col, row)
 // row-sampled L1 tap (irismpc_gpu_tap_rows): out[p * out_pstride + col * k + i]
 void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,

@@ -14,6 +14,7 @@
 //   reshare hd lane i -> pos + i,  ml -> pos + n + i
 //   lift AND gate g (0..63), 64-lane word w -> pos + 2n + g W + w
 //   inject<15>: seed1 c1 -> pos1 + 2n + 64W + i, seed3 c3 -> pos3 + 2n + 64W + 3i
+//   (comparison-only, party_comparison_only: no reshare, every offset 2n smaller)
 //   inject<16>: seed1 -> pos1 + 3n + 64W + i,    seed3 -> pos3 + 5n + 64W + 3i
 //   msb gate g (0..60): seed1 pos1 + 4n + 64W + gW + w, seed2 pos2 + 2n + 64W + gW + w,
 //                       seed3 pos3 + 8n + 64W + gW + w
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   if (V != kPlainMask) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) load8<MT>(ml[p], mk, sg, L8, full, gc.mine, m[p]);
-    reshare8(A, A.n + L8, gc.next_contig, m, MM);
+    if (!A.no_reshare) reshare8(A, A.n + L8, gc.next_contig, m, MM);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
   uint32_t (&h)[3][8] = m;  // reuse the registers
 #pragma unroll
   for (int p = 0; p < 3; ++p) load8<HT>(hd[p], hk, sg, L8, full, gc.mine, h[p]);
-  reshare8(A, L8, gc.next_contig, h, HM);
+  if (!A.no_reshare) reshare8(A, L8, gc.next_contig, h, HM);
   if (V == kPlainMask) {
     // public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
     uint32_t cnt[8];
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs 
     x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
   }
   uint32_t d[3][8];
-  const uint64_t n = A.n, W = A.W;
+  const uint64_t n = A.n;
 #pragma unroll
   for (int p = 0; p < 3; ++p)
 #pragma unroll
@@ -494,8 +495,8 @@ __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs 
     const uint32_t x = which == 0 ? x17 : x16;
     const uint32_t mask = which == 0 ? 0x7FFFu : 0xFFFFu;
     const int shift = which == 0 ? 17 : 16;
-    const uint64_t o1 = A.pos[0] + 2 * n + 64 * W + (which == 0 ? 0 : n) + L8;
-    const uint64_t o3 = A.pos[2] + 2 * n + 64 * W + (which == 0 ? 0 : 3 * n) + 3 * L8;
+    const uint64_t o1 = A.inj_base[0] + (which == 0 ? 0 : n) + L8;
+    const uint64_t o3 = A.inj_base[2] + (which == 0 ? 0 : 3 * n) + 3 * L8;
     uint32_t c1[8], w3[24];
     prf_window<1>(A.key[0], o1, gc.next_contig, c1);
     prf_window<3>(A.key[2], o3, gc.next_contig, w3);  // (c3, w0, w1) per lane; only c3 is used
@@ -652,6 +653,102 @@ __global__ void __launch_bounds__(128, MSB_LB) k_msb(const __grid_constant__ Thr
   }
   __shared__ uint64_t orr[4][3][40];
   if (t.sg.slot >= 0) fused_or(A, t.sg, task, bit, lane, orr[threadIdx.x >> 5]);
+}
+
+// ---------------------------------------------------------------- comparison phase alone
+
+// party_comparison_only's parse_rep_shares (src/engine.cpp:455-467): lane i of
+// party p's payload is (own, prev) as two little-endian ring elements of
+// `width` bytes; component p = own_p, and prev_p must equal own_{p-1} (the
+// replication cross-check of a RepShare).  width 8 = the plain-mask public ml
+// (one LE u64 per lane, identical at every party; out has one plane).
+__global__ void k_parse_lane_shares(const uint8_t* __restrict__ p1, const uint8_t* __restrict__ p2,
+                                    const uint8_t* __restrict__ p3, uint64_t lanes, int width, void* out,
+                                    int* bad) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= lanes) return;
+  const uint8_t* P[3] = {p1, p2, p3};
+  auto rd = [&](const uint8_t* p, uint64_t off, int w) {
+    uint64_t v = 0;
+    for (int b = 0; b < w; ++b) v |= (uint64_t)p[off + b] << (8 * b);
+    return v;
+  };
+  if (width == 8) {
+    const uint64_t a = rd(P[0], 8 * i, 8), b = rd(P[1], 8 * i, 8), c = rd(P[2], 8 * i, 8);
+    if (a != b || a != c) atomicOr(bad, 1);
+    static_cast<uint16_t*>(out)[i] = (uint16_t)a;
+    return;
+  }
+  uint64_t own[3], prev[3];
+  for (int p = 0; p < 3; ++p) {
+    own[p] = rd(P[p], 2ull * width * i, width);
+    prev[p] = rd(P[p], 2ull * width * i + width, width);
+  }
+  for (int p = 0; p < 3; ++p) {
+    if (prev[p] != own[(p + 2) % 3]) atomicOr(bad, 1);
+    if (width == 2)
+      static_cast<uint16_t*>(out)[p * lanes + i] = (uint16_t)own[p];
+    else
+      static_cast<uint32_t*>(out)[p * lanes + i] = (uint32_t)own[p];
+  }
+}
+
+void launch_parse_lane_shares(const uint8_t* const p[3], uint64_t lanes, int width, void* out, int* bad,
+                              cudaStream_t st) {
+  if (!lanes) return;
+  k_parse_lane_shares<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(p[0], p[1], p[2], lanes, width, out, bad);
+}
+
+// party_or_tree_only's payload (engine.cpp:517-532): per 64-lane word
+// (own u64, prev u64) of party p -> component words [3][2 * words] (u32 halves)
+__global__ void k_parse_bit_shares(const uint8_t* __restrict__ p1, const uint8_t* __restrict__ p2,
+                                   const uint8_t* __restrict__ p3, uint64_t words, uint64_t lanes,
+                                   uint32_t* __restrict__ out, int* bad) {
+  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  const uint8_t* P[3] = {p1, p2, p3};
+  uint64_t own[3], prev[3];
+  for (int p = 0; p < 3; ++p) {
+    own[p] = prev[p] = 0;
+    for (int b = 0; b < 8; ++b) {
+      own[p] |= (uint64_t)P[p][16 * w + b] << (8 * b);
+      prev[p] |= (uint64_t)P[p][16 * w + 8 + b] << (8 * b);
+    }
+  }
+  const uint64_t valid = (lanes - 64 * w) >= 64 ? ~0ull : ((1ull << (lanes - 64 * w)) - 1);
+  for (int p = 0; p < 3; ++p) {
+    if (prev[p] != own[(p + 2) % 3]) atomicOr(bad, 1);
+    out[p * 2 * words + 2 * w] = (uint32_t)(own[p] & valid);
+    out[p * 2 * words + 2 * w + 1] = (uint32_t)((own[p] & valid) >> 32);
+  }
+}
+
+void launch_parse_bit_shares(const uint8_t* const p[3], uint64_t words, uint64_t lanes, uint32_t* out, int* bad,
+                             cudaStream_t st) {
+  if (!words) return;
+  k_parse_bit_shares<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(p[0], p[1], p[2], words, lanes, out, bad);
+}
+
+// OR of shared bits already in component words (A.match[c], 32 lanes per word):
+// warp -> 1024-lane task, the fused warp OR of k_msb into partial slot `task`
+__global__ void __launch_bounds__(128) k_or_bits(const __grid_constant__ ThrArgs A) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t task = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (task >= A.ntasks) return;
+  const uint64_t wi = task * 32 + lane;
+  uint32_t bit[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bit[c] = wi * 32 < A.n ? A.match[c][wi] : 0u;
+  Seg sg{};
+  sg.slot = 0;
+  sg.task_begin = 0;
+  __shared__ uint64_t orr[4][3][40];
+  fused_or(A, sg, task, bit, lane, orr[threadIdx.x >> 5]);
+}
+
+void launch_or_bits(const ThrArgs& a, cudaStream_t st) {
+  if (!a.ntasks) return;
+  k_or_bits<<<(unsigned)((a.ntasks + 3) / 4), 128, 0, st>>>(a);
 }
 
 template <typename T>

@@ -20,7 +20,7 @@ def test_exit_codes_without_gpu(tmp_path):
     P.write_iris_db(q, dc, dm, 64)
     assert cli.main(["query", "--shares", str(tmp_path / "none"), "--query", str(q), "--length", "64"]) == 2
     assert cli.main(["query", "--shares", str(tmp_path), "--query", str(q), "--length", "128"]) == 2
-    assert cli.main(["bench", "--phase", "comparison"]) == 2
+    assert cli.main(["bench", "--phase", "bogus"]) == 2
 
 
 def _gpu():
@@ -141,3 +141,22 @@ def test_query_with_reference_config_json(tmp_path, capsys):
     capsys.readouterr()
     assert cli.main(["query", "--config", str(cfg), "--query", str(q)]) == 0
     assert capsys.readouterr().out.splitlines()[0] == "variant mpc-lift: true"
+
+
+@pytest.mark.gpu
+def test_bench_comparison_table(tmp_path, capsys):
+    """`bench` (default --phase comparison, irismpc_cli.cpp:373-458): one row per
+    variant plus the OR-tree row; kB/party equals the reference's acceptance
+    ledger (proj/test_output.txt:17-21)."""
+    _gpu()
+    js = tmp_path / "c.json"
+    assert cli.main(["bench", "--repeat", "2", "--json", str(js)]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[0].split()[:5] == ["protocol", "ms", "cmp/s", "kB/party", "B/cmp"]
+    rows = {r["protocol"]: r for r in json.load(open(js))}
+    assert set(rows) == {"plain-mask", "mpc-lift", "const-lift", "no-lift", "or-tree"}
+    assert rows["plain-mask"]["kb_per_party"] == pytest.approx(362.50)
+    assert rows["mpc-lift"]["kb_per_party"] == pytest.approx(2095.8333, abs=1e-3)
+    assert rows["const-lift"]["kb_per_party"] == pytest.approx(762.50)
+    assert rows["no-lift"]["kb_per_party"] == pytest.approx(762.50)
+    assert rows["or-tree"]["kb_per_party"] == pytest.approx(12.5087, abs=1e-3)

@@ -200,6 +200,62 @@ class Session {
   std::uint64_t s_ = 0;
 };
 
+// ---- DB-sharded queries: one Session per shard (GPU), each with
+// a contiguous row range of the DB; the library broadcasts the query from
+// shard 0, gathers the per-person XOR-shared partials and opens on shard 0.
+class ShardGroup {  // in-process collectives (contexts of one process, one thread each)
+ public:
+  explicit ShardGroup(std::uint32_t world) { check(irismpc_gpu_shard_group_create(world, &h_), "shard_group"); }
+  ~ShardGroup() { irismpc_gpu_shard_group_destroy(h_); }
+  ShardGroup(const ShardGroup&) = delete;
+  ShardGroup& operator=(const ShardGroup&) = delete;
+  irismpc_gpu_shard_group* handle() const { return h_; }
+
+ private:
+  irismpc_gpu_shard_group* h_ = nullptr;
+};
+
+class ShardedSession {
+ public:
+  ShardedSession(const EngineConfig& cfg, const std::array<std::uint8_t, 48>& seeds, std::uint32_t rank,
+                 std::uint64_t db_rows_total, std::uint64_t db_row_offset, int device = 0)
+      : cfg_(cfg), rank_(rank), session_(cfg, seeds, device, rank, db_rows_total, db_row_offset) {}
+
+  void attach(ShardGroup& g) { check(irismpc_gpu_shard_attach_inproc(session_.raw(), g.handle()), "attach", session_.raw()); }
+  void attach_nccl(const std::array<std::uint8_t, 128>& id, std::uint32_t world) {
+    check(irismpc_gpu_shard_attach_nccl(session_.raw(), id.data(), world), "attach_nccl", session_.raw());
+  }
+  // this shard's rows of the three parties' IRS1 payloads
+  void load_db(const Payloads& payload, std::uint64_t rows) { session_.load_db(payload, rows); }
+
+  // every shard calls it together; q is read on shard 0 only (others may pass
+  // empty spans of the right size in qlen); person_match is filled on shard 0
+  MembershipResult batch_query(const Payloads& q, unsigned persons) {
+    const std::uint8_t* p[3] = {q[0].data(), q[1].data(), q[2].data()};
+    const std::size_t len[3] = {q[0].size(), q[1].size(), q[2].size()};
+    MembershipResult r;
+    r.person_match.resize(persons);
+    irismpc_gpu_stats st{};
+    check(irismpc_gpu_sharded_batch_query(session_.raw(), rank_ == 0 ? p : nullptr, len, persons,
+                                          r.person_match.data(), &st),
+          "sharded_batch_query", session_.raw());
+    if (rank_ != 0) r.person_match.clear();
+    r.lane_count = st.lanes;
+    r.stats.s = st.s;
+    r.stats.l = st.l;
+    r.stats.batch = st.batch;
+    r.stats.wall_ms = st.wall_ms;
+    return r;
+  }
+  std::uint32_t rank() const { return rank_; }
+  Session& session() { return session_; }
+
+ private:
+  EngineConfig cfg_;
+  std::uint32_t rank_;
+  Session session_;
+};
+
 // Drop-in for the per-party entry points: three party threads rendezvous and
 // the last arrival runs the fused 3-party query.  Like the reference
 // (party_batch_query / party_membership load the DB on every call,

@@ -156,6 +156,33 @@ int irismpc_gpu_comparison_only(irismpc_gpu_ctx* ctx, const uint8_t* const hd_pa
 int irismpc_gpu_or_tree_only(irismpc_gpu_ctx* ctx, const uint8_t* const payload[3], const size_t len[3],
                              uint64_t lanes, uint8_t* opened_out, irismpc_gpu_stats* stats);
 
+/* ---- DB-sharded queries across GPUs --------------------------
+ * Each context holds one contiguous row range of the DB (cfg.shard_rank,
+ * cfg.db_rows_total, cfg.db_row_offset) with all three parties' shares of
+ * those rows, so every reshare and AND gate stays on its GPU.  A sharded query
+ * (1) broadcasts the three query payloads from shard 0, (2) runs this shard's
+ * lanes up to the per-person XOR-shared OR partial (never opened), (3) gathers
+ * the partials to shard 0, which finishes the MPC-OR across shards and opens
+ * at P1.  Lane and PRF indices are global, so results do not depend on the
+ * shard count.  Collectives: NCCL (one process or thread per GPU; every shard
+ * calls attach_nccl with the same id) or an in-process group (several
+ * contexts of one process, possibly on one GPU, one host thread each).  All
+ * shards call the query entry points together; q may be NULL except on shard
+ * 0; person_match_out is written on shard 0. */
+typedef struct irismpc_gpu_shard_group irismpc_gpu_shard_group;
+int irismpc_gpu_shard_group_create(uint32_t world, irismpc_gpu_shard_group** out);
+void irismpc_gpu_shard_group_destroy(irismpc_gpu_shard_group* group);
+int irismpc_gpu_shard_attach_inproc(irismpc_gpu_ctx* ctx, irismpc_gpu_shard_group* group);
+/* nccl_id from irismpc_gpu_nccl_unique_id on one shard, shared by the caller */
+int irismpc_gpu_shard_attach_nccl(irismpc_gpu_ctx* ctx, const uint8_t nccl_id[128], uint32_t world);
+int irismpc_gpu_sharded_batch_query(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
+                                    uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats);
+/* same with DEVICE query payloads on shard 0 */
+int irismpc_gpu_sharded_batch_query_device(irismpc_gpu_ctx* ctx, const uint8_t* const dq[3], const size_t qlen[3],
+                                           uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats);
+int irismpc_gpu_sharded_membership(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
+                                   uint8_t* match_out, irismpc_gpu_stats* stats);
+
 /* PRF stream positions (per seed); a fresh context starts at 0 like
  * run_parties; the reference CLI keeps PartyCtx across queries. */
 int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* ctx, uint64_t pos[3]);

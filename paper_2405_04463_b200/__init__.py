@@ -42,6 +42,9 @@ EXPORTED = [
     "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
     "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap", "irismpc_gpu_profile", "irismpc_gpu_profile_read",
     "irismpc_gpu_tap_rows", "irismpc_gpu_comparison_only", "irismpc_gpu_or_tree_only",
+    "irismpc_gpu_shard_group_create", "irismpc_gpu_shard_group_destroy", "irismpc_gpu_shard_attach_inproc",
+    "irismpc_gpu_shard_attach_nccl", "irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device",
+    "irismpc_gpu_sharded_membership",
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
@@ -166,6 +169,13 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_tap_rows.argtypes = [vp, u64p, C.c_uint32]
         L.irismpc_gpu_comparison_only.argtypes = [vp, P3, S3, P3, S3, C.c_uint64, C.c_int, vp, vp, C.POINTER(Stats)]
         L.irismpc_gpu_or_tree_only.argtypes = [vp, P3, S3, C.c_uint64, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_shard_group_create.argtypes = [C.c_uint32, C.POINTER(vp)]
+        L.irismpc_gpu_shard_group_destroy.argtypes = [vp]
+        L.irismpc_gpu_shard_attach_inproc.argtypes = [vp, vp]
+        L.irismpc_gpu_shard_attach_nccl.argtypes = [vp, u8p, C.c_uint32]
+        for f in ("irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device"):
+            getattr(L, f).argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_sharded_membership.argtypes = [vp, P3, S3, vp, C.POINTER(Stats)]
         L.irismpc_gpu_profile_read.argtypes = [vp, vp, vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
         cp3 = C.c_char_p * 3
@@ -433,6 +443,30 @@ class Session:
         self._check(lib().irismpc_gpu_or_open(self._h, _ptr(partials), G, persons, out.ctypes.data))
         return out[:persons]
 
+    # -- DB-sharded queries (one context per shard) ------------------
+    def shard_attach_inproc(self, group: "ShardGroup"):
+        """Join an in-process shard group (several contexts in one process)."""
+        self._check(lib().irismpc_gpu_shard_attach_inproc(self._h, group._h))
+        self._group = group
+
+    def shard_attach_nccl(self, nccl_id: bytes, world: int):
+        """Join the NCCL communicator of `world` shards (rank = this context's shard_rank)."""
+        idb = np.frombuffer(nccl_id, np.uint8).copy()
+        self._check(lib().irismpc_gpu_shard_attach_nccl(self._h, idb.ctypes.data_as(u8p), world))
+
+    def sharded_batch_query(self, q, persons: int, qlen=None) -> np.ndarray | None:
+        """Broadcast (from shard 0) -> shard query -> gather -> MPC-OR + open on shard 0.
+        q: three payloads (host arrays or device tensors) on shard 0, None elsewhere
+        (then qlen gives the payload sizes).  Returns person_match on shard 0."""
+        if q is not None:
+            dev, arrs, ptrs, lens = self._q(q)
+        else:
+            dev, ptrs, lens = True, (vp * 3)(None, None, None), (C.c_size_t * 3)(*qlen)
+        out = np.zeros(max(1, persons), np.uint8)
+        f = lib().irismpc_gpu_sharded_batch_query_device if dev else lib().irismpc_gpu_sharded_batch_query
+        self._check(f(self._h, ptrs, lens, persons, out.ctypes.data, C.byref(self.last_stats)))
+        return out[:persons]
+
     # -- the comparison phase alone ---------------------------------------------
     def comparison_only(self, hd_payloads, ml_payloads, lanes: int, with_or_tree: bool = False,
                         want_bits: bool = False):
@@ -515,6 +549,28 @@ class Session:
         if tap == TAP_DIFF and kc == 16:
             return out.astype(np.uint16)
         return out
+
+
+class ShardGroup:
+    """In-process group of DB shards (irismpc_gpu_shard_group): the query broadcast
+    and partial gather between contexts of one process, one host thread each."""
+
+    def __init__(self, world: int):
+        h = vp()
+        if lib().irismpc_gpu_shard_group_create(world, C.byref(h)):
+            raise ConfigError("shard group")
+        self._h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().irismpc_gpu_shard_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def share_lane_values(values, bits: int, rng: np.random.Generator):

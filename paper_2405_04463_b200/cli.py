@@ -185,7 +185,8 @@ def cmd_bench_comparison(a) -> int:
     replicated shares of synthetic (masked dot, ml) lanes -- ml uniform in
     [0, l], hd uniform in [0, ml], dot = ml - 2 hd -- then the OR-tree row
     (party_or_tree_only over `comparisons` bits with one planted 1).  Best of
-    --repeat device times; kB/party = (lift + ot + msb bytes) averaged over the
+    --repeat device times of the comparison kernels (the payload upload over PCIe
+    and its parse are reported separately as upload_parse_ms); kB/party = (lift + ot + msb bytes) averaged over the
     parties, or_tree bytes without the final 1-bit open, as the reference prints.
     The lane values come from numpy rather than the reference's Rng(1) (no
     column depends on them)."""
@@ -208,7 +209,8 @@ def cmd_bench_comparison(a) -> int:
         for _ in range(a.repeat):
             sess.comparison_only(hp, mp, n)
             st = sess.last_stats
-            best = min(best, st.wall_ms)
+            best = min(best, st.threshold_ms + st.or_ms)  # device compute, payload upload + parse excluded
+            upload = st.prep_ms
             kb = sum(st.lift_bytes[p] + st.msb_bytes[p] for p in range(3)) / 3 / 1000
             rounds = st.lift_rounds + st.msb_rounds
         sess.close()
@@ -216,7 +218,8 @@ def cmd_bench_comparison(a) -> int:
         pt = PAPER_TABLE3[name]
         print(f"{name:<12} {best:>10.3f} {n / (best / 1e3):>14.0f} {kb:>10.1f} {kb * 1000 / n:>8.2f}   "
               f"{pt[0]:>6.2f} {pt[1]:>6.1f} {pt[2]:>6}")
-        rows.append({"protocol": name, "comparisons": n, "ms": best, "throughput_per_s": n / (best / 1e3),
+        rows.append({"protocol": name, "comparisons": n, "ms": best, "upload_parse_ms": upload,
+                     "throughput_per_s": n / (best / 1e3),
                      "kb_per_party": kb, "bytes_per_comparison": kb * 1000 / n, "rounds": rounds,
                      "paper_table3": {"ms": pt[0], "m_el_per_s": pt[1], "kb_per_party": pt[2]}})
     bits = np.zeros(n, np.uint8)
@@ -228,7 +231,7 @@ def cmd_bench_comparison(a) -> int:
     for _ in range(a.repeat):
         opened = sess.or_tree_only(pay, n)
         st = sess.last_stats
-        best = min(best, st.wall_ms)
+        best = min(best, st.threshold_ms + st.or_ms)
         kb = (sum(st.or_tree_bytes[p] for p in range(3)) - 2) / 3 / 1000
         rounds = st.or_tree_rounds - 1
     if opened != int(bits.any()):

@@ -9,7 +9,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdio>
+#include <memory>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -18,6 +21,7 @@
 #include "../../include/irismpc_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "nccl_api.h"
 
 using namespace irisgpu;
 
@@ -127,6 +131,95 @@ uint64_t ref_or_draws(uint64_t groups, uint64_t len, uint64_t* rounds, uint64_t*
 
 }  // namespace
 
+// ---- DB-sharded queries: the two exchanges of SURVEY §8e -------------------
+// (1) broadcast of the three query payloads from shard 0, (2) gather of every
+// shard's per-person XOR-shared OR partials to shard 0.  Over NCCL (one process
+// or thread per GPU) or an in-process group (several contexts in one process,
+// e.g. on one GPU, which one NCCL communicator cannot hold).
+namespace {
+
+struct ShardComm {
+  uint32_t world = 1, rank = 0;
+  virtual ~ShardComm() = default;
+  virtual std::string bcast(void* dev, size_t bytes, cudaStream_t st) = 0;  // in place, root 0
+  // every shard's `bytes` of send -> root's recv[world][bytes] (other ranks' recv may be unused)
+  virtual std::string gather(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+};
+
+struct NcclShardComm : ShardComm {
+  ncclComm_t comm = nullptr;
+  ~NcclShardComm() override {
+    if (comm && nccl().ok) nccl().comm_destroy(comm);
+  }
+  std::string bcast(void* dev, size_t bytes, cudaStream_t st) override {
+    if (!bytes) return "";
+    const ncclResult_t r = nccl().broadcast(dev, dev, bytes, ncclUint8, 0, comm, st);
+    return r == ncclSuccess ? "" : std::string("nccl broadcast: ") + nccl().error_string(r);
+  }
+  std::string gather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    const ncclResult_t r = nccl().all_gather(send, recv, bytes, ncclUint8, comm, st);
+    return r == ncclSuccess ? "" : std::string("nccl all_gather: ") + nccl().error_string(r);
+  }
+};
+
+}  // namespace
+
+// In-process shard group: a generation barrier plus device copies (cudaMemcpy
+// with UVA; peer devices or the same device).
+struct irismpc_gpu_shard_group {
+  uint32_t world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  uint32_t arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptr;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+namespace {
+
+struct InprocShardComm : ShardComm {
+  irismpc_gpu_shard_group* g = nullptr;
+  std::string bcast(void* dev, size_t bytes, cudaStream_t st) override {
+    if (cudaStreamSynchronize(st) != cudaSuccess) return "shard bcast: device fault";
+    if (rank == 0) g->ptr[0] = dev;
+    g->barrier();
+    std::string err;
+    if (rank != 0 && bytes &&
+        (cudaMemcpyAsync(dev, g->ptr[0], bytes, cudaMemcpyDefault, st) != cudaSuccess ||
+         cudaStreamSynchronize(st) != cudaSuccess))
+      err = "shard bcast: copy failed";
+    g->barrier();  // the root's buffer stays untouched until every shard copied it
+    return err;
+  }
+  std::string gather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    if (cudaStreamSynchronize(st) != cudaSuccess) return "shard gather: device fault";
+    g->ptr[rank] = send;
+    g->barrier();
+    std::string err;
+    if (rank == 0)
+      for (uint32_t r = 0; r < world && err.empty(); ++r)
+        if (cudaMemcpyAsync(static_cast<uint8_t*>(recv) + r * bytes, g->ptr[r], bytes, cudaMemcpyDefault, st) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+          err = "shard gather: copy failed";
+    g->barrier();
+    return err;
+  }
+};
+
+}  // namespace
+
 // Device planes of one record field (code -> hd, mask -> ml): DB limb planes
 // (A), rotated query planes (B), the unrotated query planes of the pair GEMM
 // (A) and its output.
@@ -201,6 +294,8 @@ struct irismpc_gpu_ctx {
   size_t tap_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
+  std::unique_ptr<ShardComm> shard;  // DB-sharded queries (irismpc_gpu_shard_attach_*)
+  Buf shard_part, shard_all;
   std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
   std::vector<cudaEvent_t> evg, evt, evt3;  // chunk pipeline: GEMM done / threshold done (st2, st3)
 };
@@ -1454,6 +1549,9 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
   cudaStreamSynchronize(c->st);
+  c->shard.reset();
+  c->shard_part.release();
+  c->shard_all.release();
   Buf* bufs[] = {&c->q_pay[0], &c->q_pay[1], &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial,
                  &c->slot_begin, &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
                  &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->gate2, &c->bits2};
@@ -1665,6 +1763,116 @@ int irismpc_gpu_or_tree_only(irismpc_gpu_ctx* c, const uint8_t* const payload[3]
   cudaSetDevice(c->cfg.device);
   if (lanes == 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no lanes");
   return run_compare(c, 1, payload, len, nullptr, nullptr, lanes, 1, opened_out, nullptr, stats);
+}
+
+int irismpc_gpu_shard_group_create(uint32_t world, irismpc_gpu_shard_group** out) {
+  if (!out || world == 0) return IRISMPC_GPU_ERR_CONFIG;
+  auto* g = new irismpc_gpu_shard_group;
+  g->world = world;
+  g->ptr.assign(world, nullptr);
+  *out = g;
+  return 0;
+}
+
+void irismpc_gpu_shard_group_destroy(irismpc_gpu_shard_group* g) { delete g; }
+
+static int shard_check(irismpc_gpu_ctx* c, uint32_t world) {
+  if (c->cfg.shard_rank >= world) return fail(c, IRISMPC_GPU_ERR_CONFIG, "shard_rank >= world size");
+  if (world > 1 && c->cfg.db_rows_total == 0)
+    return fail(c, IRISMPC_GPU_ERR_CONFIG, "a sharded context needs db_rows_total (the whole DB's rows)");
+  return 0;
+}
+
+int irismpc_gpu_shard_attach_inproc(irismpc_gpu_ctx* c, irismpc_gpu_shard_group* g) {
+  if (!c || !g) return IRISMPC_GPU_ERR_CONFIG;
+  if (int rc = shard_check(c, g->world)) return rc;
+  auto sc = std::make_unique<InprocShardComm>();
+  sc->g = g;
+  sc->world = g->world;
+  sc->rank = c->cfg.shard_rank;
+  c->shard = std::move(sc);
+  return 0;
+}
+
+int irismpc_gpu_shard_attach_nccl(irismpc_gpu_ctx* c, const uint8_t nccl_id[128], uint32_t world) {
+  if (!c || !nccl_id) return IRISMPC_GPU_ERR_CONFIG;
+  if (int rc = shard_check(c, world)) return rc;
+  if (!nccl().ok) return fail(c, IRISMPC_GPU_ERR_DEVICE, "libnccl could not be loaded");
+  cudaSetDevice(c->cfg.device);
+  auto sc = std::make_unique<NcclShardComm>();
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof(id));
+  const ncclResult_t r = nccl().comm_init_rank(&sc->comm, (int)world, id, (int)c->cfg.shard_rank);
+  if (r != ncclSuccess) return fail(c, IRISMPC_GPU_ERR_DEVICE, std::string("ncclCommInitRank: ") + nccl().error_string(r));
+  sc->world = world;
+  sc->rank = c->cfg.shard_rank;
+  c->shard = std::move(sc);
+  return 0;
+}
+
+// One query over the row-sharded DB: broadcast of the query
+// payloads from shard 0, this shard's query up to the per-person XOR-shared
+// aggregate (never opened), gather of every shard's [3][groups] partial to
+// shard 0, the MPC-OR across shards and the open at P1 there.
+static int sharded_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint32_t persons,
+                         int membership, bool host_input, uint8_t* match_out, irismpc_gpu_stats* stats) {
+  if (!c->shard) return fail(c, IRISMPC_GPU_ERR_CONFIG, "context is not attached to a shard group");
+  ShardComm& sc = *c->shard;
+  const uint32_t groups = membership ? 1u : persons;
+  const uint8_t* dq[3];
+  for (int p = 0; p < 3; ++p) {
+    if (c->q_pay[p].ensure(qlen[p] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query payload)");
+    if (sc.rank == 0) {
+      if (!q || !q[p]) return fail(c, IRISMPC_GPU_ERR_CONFIG, "shard 0 needs the query payloads");
+      if (host_input)
+        CK(c, cudaMemcpyAsync(c->q_pay[p].p, q[p], qlen[p], cudaMemcpyHostToDevice, c->st));
+      else if (q[p] != c->q_pay[p].as<uint8_t>())
+        CK(c, cudaMemcpyAsync(c->q_pay[p].p, q[p], qlen[p], cudaMemcpyDeviceToDevice, c->st));
+    }
+  }
+  for (int p = 0; p < 3; ++p) {  // (1) query-share broadcast
+    const std::string e = sc.bcast(c->q_pay[p].p, qlen[p], c->st);
+    if (!e.empty()) return fail(c, IRISMPC_GPU_ERR_DEVICE, e);
+    dq[p] = c->q_pay[p].as<uint8_t>();
+  }
+  if (c->shard_part.ensure(3ull * groups + 16) || c->shard_all.ensure(3ull * groups * sc.world + 16))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (shard partials)");
+  const int rc = run_query(c, dq, qlen, persons, membership, 1, nullptr, nullptr, c->shard_part.as<uint8_t>(), stats,
+                           false, nullptr);
+  if (rc) return rc;
+  const std::string e = sc.gather(c->shard_part.p, c->shard_all.p, 3ull * groups, c->st);  // (2)
+  if (!e.empty()) return fail(c, IRISMPC_GPU_ERR_DEVICE, e);
+  if (sc.rank == 0) {
+    if (c->open_out.ensure(groups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    launch_or_open(c->shard_all.as<uint8_t>(), sc.world, groups, c->keys, or_stream_id(c->or_ctr, 0, 3),
+                   c->open_out.as<uint8_t>(), c->st);
+    CK(c, cudaGetLastError());
+    if (match_out) CK(c, cudaMemcpyAsync(match_out, c->open_out.p, groups, cudaMemcpyDeviceToHost, c->st));
+  }
+  CK(c, cudaStreamSynchronize(c->st));
+  if (stats) stats->kernel_launches += sc.rank == 0 ? 1 : 0;
+  return 0;
+}
+
+int irismpc_gpu_sharded_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3],
+                                    uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return sharded_query(c, q, qlen, persons, 0, true, person_match_out, stats);
+}
+
+int irismpc_gpu_sharded_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
+                                           uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return sharded_query(c, dq, qlen, persons, 0, false, person_match_out, stats);
+}
+
+int irismpc_gpu_sharded_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3],
+                                   uint8_t* match_out, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  return sharded_query(c, q, qlen, 1, 1, true, match_out, stats);
 }
 
 int irismpc_gpu_get_stream_positions(const irismpc_gpu_ctx* c, uint64_t pos[3]) {

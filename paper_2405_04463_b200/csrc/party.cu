@@ -21,8 +21,6 @@
 // the single-GPU engine, and the OR tree is the reference's
 // halving tree, so even the aggregate shares and the stream positions match.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -38,6 +36,7 @@
 #include "../../include/irismpc_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "nccl_api.h"
 
 using namespace irisgpu;
 
@@ -87,40 +86,6 @@ struct Transport {
   virtual std::string exchange(int self, const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
                                cudaStream_t st) = 0;
 };
-
-// ---- NCCL, resolved at run time (the libnccl torch already loaded, else the system one)
-struct NcclApi {
-  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
-  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
-  decltype(&ncclCommDestroy) comm_destroy = nullptr;
-  decltype(&ncclSend) send = nullptr;
-  decltype(&ncclRecv) recv = nullptr;
-  decltype(&ncclGroupStart) group_start = nullptr;
-  decltype(&ncclGroupEnd) group_end = nullptr;
-  decltype(&ncclGetErrorString) error_string = nullptr;
-  bool ok = false;
-};
-
-const NcclApi& nccl() {
-  static NcclApi api = [] {
-    NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return a;
-    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
-    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
-    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
-    a.send = (decltype(a.send))dlsym(h, "ncclSend");
-    a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
-    a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
-    a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
-    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
-    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.group_start &&
-           a.group_end && a.error_string;
-    return a;
-  }();
-  return api;
-}
 
 struct NcclTransport : Transport {
   ncclComm_t comm = nullptr;

@@ -2,6 +2,7 @@
 // (the reference's per-party entry point shape, engine.hpp:311-313) and P1's
 // person_match must equal the oracle's; error paths map to the reference's
 // exception types.  Built and run by tests/test_cpp_shim.py.
+#include <algorithm>
 #include <cstdio>
 #include <memory>
 #include <thread>
@@ -57,7 +58,7 @@ int main() {
   cfg.params = MatchParams::make(0.375, 16);
   cfg.rotations = 31;
   ThreePartyGpu gpu(cfg, seed);
-  for (int round = 0; round < 2; ++round) {  // second round: DB stays resident
+  for (int round = 0; round < 2; ++round) {  // reloads the DB every call, like the reference
     std::array<MembershipResult, 3> res;
     std::vector<std::thread> th;
     for (unsigned p = 1; p <= 3; ++p)
@@ -71,6 +72,56 @@ int main() {
     if (res[1].stats.lift_bytes != res[2].stats.lift_bytes) return 1;  // P2, P3 send 4n OT bytes
   }
   if (want[1] != 1) return 1;
+
+  // in-place rewrite of the DB payload bytes between calls (same buffers, same
+  // sizes): row 123 becomes a copy of row 0's shares, so person 1's planted match
+  // must disappear -- the shim reloads the DB every call (engine.cpp:404-420)
+  {
+    const auto orig = db;
+    for (int p = 0; p < 3; ++p) std::copy(orig[p].begin(), orig[p].begin() + rec, db[p].begin() + 123 * rec);
+    std::vector<std::uint8_t> want3(persons);
+    orc_out o3{};
+    o3.person_match = want3.data();
+    if (orc_query(&oc, seeds, db[0].data(), db[1].data(), db[2].data(), s, q[0].data(), q[1].data(), q[2].data(),
+                  persons, 0, nullptr, &o3) != 0)
+      return 2;
+    std::array<MembershipResult, 3> res;
+    std::vector<std::thread> th;
+    for (unsigned p = 1; p <= 3; ++p)
+      th.emplace_back([&, p] { res[p - 1] = gpu.party_batch_query(p, db[p - 1], s, q[p - 1], persons); });
+    for (auto& t : th) t.join();
+    if (res[0].person_match != want3 || want3[1] != 0) {
+      std::printf("MISMATCH after in-place DB rewrite\n");
+      return 1;
+    }
+    for (int p = 0; p < 3; ++p) std::copy(orig[p].begin(), orig[p].end(), db[p].begin());
+  }
+
+  // DB-sharded query through the C-ABI: two shards of the same DB on
+  // this GPU in one process, an in-process shard group, one thread per shard
+  {
+    const auto& dbo = db;
+    const std::uint64_t split = 217;
+    ShardGroup group(2);
+    std::array<std::unique_ptr<ShardedSession>, 2> sh;
+    for (std::uint32_t r = 0; r < 2; ++r) {
+      const std::uint64_t r0 = r == 0 ? 0 : split, r1 = r == 0 ? split : s;
+      sh[r] = std::make_unique<ShardedSession>(cfg, seeds_from_master(seed), r, s, r0);
+      sh[r]->attach(group);
+      Payloads part;
+      for (int p = 0; p < 3; ++p) part[p] = std::span<const std::uint8_t>(dbo[p].data() + r0 * rec, (r1 - r0) * rec);
+      sh[r]->load_db(part, r1 - r0);
+    }
+    std::array<MembershipResult, 2> res;
+    std::vector<std::thread> th;
+    for (std::uint32_t r = 0; r < 2; ++r)
+      th.emplace_back([&, r] { res[r] = sh[r]->batch_query({q[0], q[1], q[2]}, persons); });
+    for (auto& t : th) t.join();
+    if (res[0].person_match != want) {
+      std::printf("MISMATCH sharded person_match\n");
+      return 1;
+    }
+  }
 
   // party mode: three GpuParty objects on one InProcNet, one thread each,
   // the reference's per-party call shape; P1's bits and every party's

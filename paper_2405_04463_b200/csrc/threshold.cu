@@ -19,15 +19,18 @@
 //   msb gate g (0..60): seed1 pos1 + 4n + 64W + gW + w, seed2 pos2 + 2n + 64W + gW + w,
 //                       seed3 pos3 + 8n + 64W + gW + w
 //
-// Kernels (all PRF work is ChaCha12 at full occupancy, no shared memory):
+// Kernels (every PRF block computed once, one block per thread per step):
 //   k_gate_keystream  the 125 AND gates' zero-share words of every reference
 //                     word the chunk touches: per (seed, gate) one contiguous
 //                     stream segment -> HBM buffer G
-//   k_reshare         lane-major (thread = 8 lanes): own = z + F_p - F_{p-1};
-//                     writes reshared ml (u16) and diff0 = a*ml - b*hd (u32)
+//   k_reshare         1024-lane tiles: the tile's reshare draws into shared
+//                     memory (one ChaCha block per thread per step), then
+//                     own = z + F_p - F_{p-1}; writes reshared ml (u16) and
+//                     diff0 = a*ml - b*hd (u32)
 //   k_lift            bit-sliced (thread = 32 lanes): share_split of ml + the
 //                     two adders {16,17} -> injected-bit rows
-//   k_inject          lane-major: bit_inject<15>, <16>, const-lifted into diff
+//   k_inject          1024-lane tiles, the same two phases: bit_inject<15>,
+//                     <16>, const-lifted into diff
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
 //                     match-bit shares, fused first MPC-OR level per warp
 #include <cstdlib>
@@ -65,31 +68,6 @@ __device__ __forceinline__ uint64_t gate_base(const ThrArgs& A, int k, int g) {
   return A.msb_base[k] + (uint64_t)(g - (int)A.nlift) * A.W;
 }
 
-// lane -> 8-lane group of a lane-major kernel (31 groups per warp)
-struct GroupCtx {
-  uint64_t L8;       // first global lane of the group
-  bool mine;         // this lane owns a real group (lane < 31, group < ngrp)
-  bool next_contig;  // lane + 1 owns the group at L8 + 8
-  const Seg* sg;
-};
-
-// 3-D grids: blockIdx.z = segment, so no search; warp w of block x owns the
-// segment's 8-lane groups [(x * warps + w) * 31, + 31).  Returns false when the
-// whole warp lies past the segment (warp-uniform).
-__device__ __forceinline__ bool group_ctx(const ThrArgs& A, GroupCtx& c) {
-  const int lane = threadIdx.x & 31;
-  c.sg = &A.segs[blockIdx.z];
-  const uint64_t g0 = c.sg->lane_begin / 8;
-  const uint64_t ng = (c.sg->lane_end - 1) / 8 - g0 + 1;
-  const uint64_t w0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 31;
-  if (w0 >= ng) return false;
-  const uint64_t gi = w0 + lane;
-  c.mine = lane < 31 && gi < ng;
-  c.L8 = (g0 + (gi < ng ? gi : ng - 1)) * 8;
-  c.next_contig = lane == 31 || gi + 1 < ng;
-  return true;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- gate keystream
@@ -122,162 +100,187 @@ __global__ void __launch_bounds__(256) k_gate_keystream(const __grid_constant__ 
 // ---------------------------------------------------------------- reshare
 namespace {
 
-// 8 lanes [L8, L8+8) of a dot array (u16 or u32) -> v[0..7]; `full`: one aligned vector access
+// 4 lanes [L, L+4) of a dot array (u16 or u32) at src index i0 -> v[0..3]
+// (`vec`: one aligned vector access; else per lane, lanes outside [lb, le) = 0)
 template <typename T>
-__device__ __forceinline__ void load8_at(const T* src, uint64_t src0, const Seg& sg, uint64_t L8, bool full,
-                                         bool mine, uint32_t v[8]) {
-  if (full) {
+__device__ __forceinline__ void load4_at(const T* src, uint64_t i0, uint64_t L, uint64_t lb, uint64_t le, bool vec,
+                                         uint32_t v[4]) {
+  if (vec) {
     if (sizeof(T) == 2) {
-      const uint4 x = *reinterpret_cast<const uint4*>(src + src0);
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        v[2 * i] = w[i] & 0xFFFFu;
-        v[2 * i + 1] = w[i] >> 16;
-      }
+      const uint2 x = *reinterpret_cast<const uint2*>(src + i0);
+      v[0] = x.x & 0xFFFFu;
+      v[1] = x.x >> 16;
+      v[2] = x.y & 0xFFFFu;
+      v[3] = x.y >> 16;
     } else {
-      const uint4 x = reinterpret_cast<const uint4*>(src + src0)[0];
-      const uint4 y = reinterpret_cast<const uint4*>(src + src0)[1];
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-      v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+      const uint4 x = *reinterpret_cast<const uint4*>(src + i0);
+      v[0] = x.x;
+      v[1] = x.y;
+      v[2] = x.z;
+      v[3] = x.w;
     }
     return;
   }
-  const uint64_t base = src0 - (L8 - sg.lane_begin);  // index of lane_begin
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t ln = L8 + i;
-    const bool ok = mine && ln >= sg.lane_begin && ln < sg.lane_end;
-    v[i] = ok ? (uint32_t)src[base + (ln - sg.lane_begin)] : 0u;
-  }
+  for (int i = 0; i < 4; ++i) v[i] = (L + i >= lb && L + i < le) ? (uint32_t)src[i0 + i] : 0u;
 }
 
-// A field's dots of lanes [L8, L8+8): plain [col][row] planes, or (RP) the sum
-// of the rotation pair's shared product P2 and its own P1 / P3 (prep.cu)
+// A field's dots of lanes [L, L+4): plain [col][row] planes (kstride 0), or (RP)
+// the rotation pair's shared product P2 plus its own P1 / P3 (prep.cu)
 template <typename T>
-__device__ __forceinline__ void load8(const T* src, uint64_t kstride, const Seg& sg, uint64_t L8, bool full,
-                                      bool mine, uint32_t v[8]) {
+__device__ __forceinline__ void load4(const T* src, uint64_t kstride, const Seg& sg, uint64_t L, uint64_t lb,
+                                      uint64_t le, bool vec, uint32_t v[4]) {
   if (!kstride) {
-    load8_at<T>(src, sg.src + (L8 - sg.lane_begin), sg, L8, full, mine, v);
+    load4_at<T>(src, sg.src + (L - sg.lane_begin), L, lb, le, vec, v);
     return;
   }
-  const uint64_t i0 = sg.src_rp + (L8 - sg.lane_begin);
-  uint32_t a[8];
-  load8_at<T>(src, i0 + kstride, sg, L8, full, mine, v);
-  load8_at<T>(src, i0 + (sg.rp_sel == 1 ? 0 : 2 * kstride), sg, L8, full, mine, a);
+  const uint64_t i0 = sg.src_rp + (L - sg.lane_begin);
+  uint32_t a[4];
+  load4_at<T>(src, i0 + kstride, L, lb, le, vec, v);
+  load4_at<T>(src, i0 + (sg.rp_sel == 1 ? 0 : 2 * kstride), L, lb, le, vec, a);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] += a[i];
-}
-
-// reshare one dot (zero_ring<K>, rep3.hpp:110-112): component k gains F_k and
-// component k+1 loses it -- own_p = z_p + F(seed_p) - F(seed_{p-1})
-__device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, bool next_contig, uint32_t v[3][8],
-                                         uint32_t kmask) {
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    uint32_t f[8];
-    prf_window<1>(A.key[k], A.pos[k] + e_off, next_contig, f);
-    const int kn = (k + 1) % 3;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[k][i] += f[i];
-      v[kn][i] -= f[i];
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < 3; ++p)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[p][i] &= kmask;
+  for (int i = 0; i < 4; ++i) v[i] += a[i];
 }
 
 }  // namespace
 
-// thread -> 8-lane group (global lane multiple of 8) of one segment.
 // reshare_pair<KH, KM> (engine.cpp:80-106: hd lanes at stream offset 0, ml at
-// n) followed by the comparison input:
+// n; zero_ring<K>, rep3.hpp:110-112: component k gains F(seed_k) and component
+// k+1 loses it) followed by the comparison input:
 //   mpc-lift   : ml_rs = ml (u16, lifted later), diff = a ml - b hd (partial)
 //   const-lift : diff = a ml32 - const_lift(hd, b)      (engine.hpp:94-120)
 //   no-lift    : diff = a ml32 - b hd32
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
+//
+// One CTA per 1024-lane tile of a segment (globally 1024-aligned, clipped to the
+// segment).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to 129
+// ChaCha12 blocks covering its 1024 stream elements -- one block per thread per
+// step at full occupancy (the k_gate_keystream pattern), the low 32 bits of
+// each element into shared memory.  Phase 2: thread = 4 lanes, vector loads of
+// the three parties' dots, own = z + F_k - F_{k-1}, vector stores.  (The
+// previous lane-major version held 6 blocks' windows per thread at 121
+// registers and 24% of the warps: 41% of the ChaCha rate.)
 template <int V>
-__global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs A) {
   using HT = typename std::conditional<V == kNoLift, uint32_t, uint16_t>::type;
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
-  GroupCtx gc;
-  if (!group_ctx(A, gc)) return;  // whole warp past the segment
-  const Seg& sg = *gc.sg;
-  const uint64_t L8 = gc.L8;
-  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);  // valid only when `full`
-  bool full = gc.mine && L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
+  constexpr int NDOT = V == kPlainMask ? 1 : 2;  // dot 0 = hd (offset 0), dot 1 = ml (offset n)
+  __shared__ uint32_t F[NDOT][3][1024];
+  const Seg& sg = A.segs[blockIdx.z];
+  const uint64_t T0 = (sg.lane_begin / 1024 + blockIdx.x) * 1024;
+  if (T0 >= sg.lane_end) return;  // CTA-uniform
+  const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
+  const uint64_t le = sg.lane_end < T0 + 1024 ? sg.lane_end : T0 + 1024;
+  if (!A.no_reshare) {
+    for (int j = threadIdx.x; j < NDOT * 3 * 129; j += blockDim.x) {
+      const int d = j / (3 * 129), k = (j / 129) % 3, q = j % 129;
+      const uint64_t base = A.pos[k] + (d ? A.n : 0);  // stream element of lane 0
+      const uint64_t e0 = base + lb, e1 = base + le - 1;
+      const uint64_t b = e0 / 8 + q;
+      if (b > e1 / 8) continue;
+      uint32_t blk[16];
+      chacha12_block(A.key[k], b, 0, blk);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const uint64_t e = b * 8 + w;
+        if (e >= e0 && e <= e1) F[d][k][e - base - T0] = blk[2 * w];
+      }
+    }
+    __syncthreads();
+  }
+  const uint64_t L = T0 + 4ull * threadIdx.x;
+  if (L + 4 <= lb || L >= le) return;
+  const bool full = L >= lb && L + 4 <= le;
+  const int li = (int)(L - T0);
+  const uint64_t src0 = sg.src + (L - sg.lane_begin);   // valid only when `full`
+  const uint64_t hk = A.rp_kstride_h, mk = A.rp_kstride_m;
+  const uint64_t rp0 = sg.src_rp + (L - sg.lane_begin);
+  const uint64_t hs0 = hk ? rp0 : src0, ms0 = mk ? rp0 : src0;
   const HT* hd[3];
   const MT* ml[3];
+  bool vin = full && !A.tap_rs_hd && hk % 4 == 0 && mk % 4 == 0;
+  bool vout = full && !A.tap_rs_hd;
 #pragma unroll
-  const uint64_t rp0 = sg.src_rp + (L8 - sg.lane_begin);
-  const uint64_t hs0 = A.rp_kstride_h ? rp0 : src0, ms0 = A.rp_kstride_m ? rp0 : src0;
-  const uint64_t hk = A.rp_kstride_h, mk = A.rp_kstride_m;
-  full = full && hk % 8 == 0 && mk % 8 == 0;  // P2 / P3 vectors stay 16-byte aligned
   for (int p = 0; p < 3; ++p) {
     hd[p] = static_cast<const HT*>(A.hd[p]);
     ml[p] = static_cast<const MT*>(A.ml[p]);
-    // 16-byte alignment of every vector access (RP: all three P planes; kstride is a multiple of 8)
-    full = full && ((reinterpret_cast<uintptr_t>(hd[p] + hs0) | reinterpret_cast<uintptr_t>(ml[p] + ms0) |
-                     reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0)) & 15) == 0;
-    if (V == kMpcLift) full = full && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) & 15) == 0;
+    vin = vin && ((reinterpret_cast<uintptr_t>(hd[p] + hs0) | reinterpret_cast<uintptr_t>(ml[p] + ms0)) &
+                  (4 * sizeof(HT) - 1 | 4 * sizeof(MT) - 1)) == 0;
+    vout = vout && (reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0) & 15) == 0;
+    if (V == kMpcLift) vout = vout && (reinterpret_cast<uintptr_t>(A.ml_rs + p * A.cstride + src0) & 7) == 0;
   }
-  // ml first (stream offset n): d = a * ml, the reshared ml leaves the registers,
-  // then hd (offset 0): d -= b * hd -- keeps two 3 x 8 arrays live, not three
-  uint32_t d[3][8], m[3][8];
+  uint32_t d[3][4], m[3][4];
   if (V != kPlainMask) {
 #pragma unroll
-    for (int p = 0; p < 3; ++p) load8<MT>(ml[p], mk, sg, L8, full, gc.mine, m[p]);
-    if (!A.no_reshare) reshare8(A, A.n + L8, gc.next_contig, m, MM);
+    for (int p = 0; p < 3; ++p) load4<MT>(ml[p], mk, sg, L, lb, le, vin, m[p]);
+    if (!A.no_reshare) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t f = F[1][k][li + i];
+          m[k][i] += f;
+          m[(k + 1) % 3][i] -= f;
+        }
+    }
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) d[p][i] = A.a * m[p][i];
-    if (gc.mine && V == kMpcLift) {
+      for (int i = 0; i < 4; ++i) {
+        m[p][i] &= MM;
+        d[p][i] = A.a * m[p][i];
+      }
+    if (V == kMpcLift) {
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
-        if (full) {
-          uint32_t mw[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) mw[i] = m[p][2 * i] | (m[p][2 * i + 1] << 16);
-          *reinterpret_cast<uint4*>(A.ml_rs + p * A.cstride + src0) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        if (vout) {
+          *reinterpret_cast<uint2*>(A.ml_rs + p * A.cstride + src0) =
+              make_uint2(m[p][0] | (m[p][1] << 16), m[p][2] | (m[p][3] << 16));
         } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint64_t ln = L8 + i;
-            if (ln >= sg.lane_begin && ln < sg.lane_end)
-              A.ml_rs[p * A.cstride + sg.src + (ln - sg.lane_begin)] = (uint16_t)m[p][i];
-          }
+          for (int i = 0; i < 4; ++i)
+            if (L + i >= lb && L + i < le)
+              A.ml_rs[p * A.cstride + sg.src + (L + i - sg.lane_begin)] = (uint16_t)m[p][i];
         }
       }
     }
-    if (gc.mine && A.tap_rs_ml) {
+    if (A.tap_rs_ml) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint64_t ln = L8 + i;
-        if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
+      for (int i = 0; i < 4; ++i) {
+        if (L + i < lb || L + i >= le) continue;
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
-          A.tap_rs_ml[p * A.n + ln] = m[p][i];
-          A.tap_ml32[p * A.n + ln] = m[p][i];
+          A.tap_rs_ml[p * A.n + L + i] = m[p][i];
+          A.tap_ml32[p * A.n + L + i] = m[p][i];
         }
       }
     }
   }
-  uint32_t (&h)[3][8] = m;  // reuse the registers
+  uint32_t (&h)[3][4] = m;  // reuse the registers
 #pragma unroll
-  for (int p = 0; p < 3; ++p) load8<HT>(hd[p], hk, sg, L8, full, gc.mine, h[p]);
-  if (!A.no_reshare) reshare8(A, L8, gc.next_contig, h, HM);
+  for (int p = 0; p < 3; ++p) load4<HT>(hd[p], hk, sg, L, lb, le, vin, h[p]);
+  if (!A.no_reshare) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t f = F[0][k][li + i];
+        h[k][i] += f;
+        h[(k + 1) % 3][i] -= f;
+      }
+  }
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[p][i] &= HM;
   if (V == kPlainMask) {
     // public popcount; diff = public_minus(t, hd): component 1 absorbs t (rep3.hpp:59-71)
-    uint32_t cnt[8];
-    load8<MT>(ml[0], mk, sg, L8, full, gc.mine, cnt);
+    uint32_t cnt[4];
+    load4<MT>(ml[0], mk, sg, L, lb, le, vin, cnt);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const uint32_t t = (uint32_t)(int64_t)ceil(__dmul_rn(A.coef, (double)cnt[i]));
       d[0][i] = (t - h[0][i]) & 0xFFFFu;
       d[1][i] = (0u - h[1][i]) & 0xFFFFu;
@@ -287,27 +290,22 @@ __global__ void __launch_bounds__(256, 2) k_reshare(const __grid_constant__ ThrA
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) d[p][i] -= A.b * h[p][i];
+      for (int i = 0; i < 4; ++i) d[p][i] -= A.b * h[p][i];
   }
-  if (!gc.mine) return;
-  if (full) {
+  if (vout) {
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
-      dd[0] = make_uint4(d[p][0], d[p][1], d[p][2], d[p][3]);
-      dd[1] = make_uint4(d[p][4], d[p][5], d[p][6], d[p][7]);
-    }
+    for (int p = 0; p < 3; ++p)
+      *reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0) = make_uint4(d[p][0], d[p][1], d[p][2], d[p][3]);
     return;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t ln = L8 + i;
-    if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
-    const uint64_t src = sg.src + (ln - sg.lane_begin);
+  for (int i = 0; i < 4; ++i) {
+    if (L + i < lb || L + i >= le) continue;
+    const uint64_t src = sg.src + (L + i - sg.lane_begin);
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
       A.diff[p * A.cstride + src] = d[p][i];
-      if (A.tap_rs_hd) A.tap_rs_hd[p * A.n + ln] = h[p][i];
+      if (A.tap_rs_hd) A.tap_rs_hd[p * A.n + L + i] = h[p][i];
     }
   }
 }
@@ -469,68 +467,93 @@ __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ T
   }
 }
 
-// thread -> 8-lane group: bit_inject<15>(bit17) then bit_inject<16>(bit16)
+// bit_inject<15>(bit17) then bit_inject<16>(bit16) (convert.hpp:84-155), three
+// parties at once: P1's c1 (seed 1, one draw per lane) and P3's c3 (seed 3,
+// (c3, w0, w1) per lane, only c3 enters the sharing) give b1 = c1, b3 = c3,
+// b2 = x - b1 - b3 (mod 2^W), each injected bit lifted by 2^17 / 2^16 and
+// subtracted, times a, from diff.  One CTA per 1024-lane tile: phase 1 computes
+// the tile's 2 x (129 + 385) ChaCha12 blocks one per thread per step into
+// shared memory (c1, c3 low halves), phase 2 applies them, thread = 4 lanes.
 __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs A) {
-  GroupCtx gc;
-  if (!group_ctx(A, gc)) return;  // whole warp past the segment
-  const Seg& sg = *gc.sg;
-  const uint64_t L8 = gc.L8;
-  // injected bits: the k_lift thread that owns these lanes
-  const uint64_t task = sg.task_begin + (L8 / 1024 - sg.q_first);
-  const uint64_t o = task * 32 + (L8 % 1024) / 32;
-  const int sh = (int)(L8 % 32);
-  uint32_t x17 = 0, x16 = 0;
-  if (gc.mine) {
-    x17 = (A.bits[3 * A.nbits + o] ^ A.bits[4 * A.nbits + o] ^ A.bits[5 * A.nbits + o]) >> sh;
-    x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
-  }
-  uint32_t d[3][8];
+  __shared__ uint16_t C[2][2][1024];  // [inject 15 / 16][c1 / c3][lane]
+  const Seg& sg = A.segs[blockIdx.z];
+  const uint64_t T0 = (sg.lane_begin / 1024 + blockIdx.x) * 1024;
+  if (T0 >= sg.lane_end) return;  // CTA-uniform
+  const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
+  const uint64_t le = sg.lane_end < T0 + 1024 ? sg.lane_end : T0 + 1024;
   const uint64_t n = A.n;
+  constexpr int J1 = 129, J3 = 385, JW = J1 + J3;
+  for (int j = threadIdx.x; j < 2 * JW; j += blockDim.x) {
+    const int which = j / JW, q = j % JW;
+    const bool s3 = q >= J1;
+    // stream element of lane 0: seed 1 at inj_base + (n for inject16) + L,
+    // seed 3 at inj_base + (3n for inject16) + 3L
+    const uint64_t base = s3 ? A.inj_base[2] + (which ? 3 * n : 0) : A.inj_base[0] + (which ? n : 0);
+    const uint64_t e0 = base + (s3 ? 3 * lb : lb), e1 = base + (s3 ? 3 * (le - 1) : le - 1);
+    const uint64_t b = e0 / 8 + (s3 ? q - J1 : q);
+    if (b > e1 / 8) continue;
+    uint32_t blk[16];
+    chacha12_block(A.key[s3 ? 2 : 0], b, 0, blk);
 #pragma unroll
-  for (int p = 0; p < 3; ++p)
+    for (int w = 0; w < 8; ++w) {
+      const uint64_t e = b * 8 + w;
+      if (e < e0 || e > e1) continue;
+      const uint64_t rel = e - base;
+      if (!s3) {
+        C[which][0][rel - T0] = (uint16_t)blk[2 * w];
+      } else if (rel % 3 == 0) {
+        C[which][1][rel / 3 - T0] = (uint16_t)blk[2 * w];
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t L = T0 + 4ull * threadIdx.x;
+  if (L + 4 <= lb || L >= le) return;
+  const int li = (int)(L - T0);
+  // injected bits: the k_lift thread that owns these lanes (task of this tile, lane word li / 32)
+  const uint64_t task = sg.task_begin + (T0 / 1024 - sg.q_first);
+  const uint64_t o = task * 32 + li / 32;
+  const int sh = li % 32;
+  const uint32_t x17 = (A.bits[3 * A.nbits + o] ^ A.bits[4 * A.nbits + o] ^ A.bits[5 * A.nbits + o]) >> sh;
+  const uint32_t x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
+  uint32_t d[3][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) d[p][i] = 0u;
+  for (int i = 0; i < 4; ++i) {
+    d[0][i] = d[1][i] = d[2][i] = 0u;
 #pragma unroll
-  for (int which = 0; which < 2; ++which) {
-    const uint32_t x = which == 0 ? x17 : x16;
-    const uint32_t mask = which == 0 ? 0x7FFFu : 0xFFFFu;
-    const int shift = which == 0 ? 17 : 16;
-    const uint64_t o1 = A.inj_base[0] + (which == 0 ? 0 : n) + L8;
-    const uint64_t o3 = A.inj_base[2] + (which == 0 ? 0 : 3 * n) + 3 * L8;
-    uint32_t c1[8], w3[24];
-    prf_window<1>(A.key[0], o1, gc.next_contig, c1);
-    prf_window<3>(A.key[2], o3, gc.next_contig, w3);  // (c3, w0, w1) per lane; only c3 is used
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t b1 = c1[i] & mask;
-      const uint32_t b3 = w3[3 * i] & mask;
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t x = which == 0 ? x17 : x16;
+      const uint32_t mask = which == 0 ? 0x7FFFu : 0xFFFFu;
+      const int shift = which == 0 ? 17 : 16;
+      const uint32_t b1 = C[which][0][li + i] & mask;
+      const uint32_t b3 = C[which][1][li + i] & mask;
       const uint32_t b2 = (((x >> i) & 1u) - b1 - b3) & mask;
       d[0][i] += b1 << shift;
       d[1][i] += b2 << shift;
       d[2][i] += b3 << shift;
     }
   }
-  if (!gc.mine) return;
-  const uint64_t src0 = sg.src + (L8 - sg.lane_begin);
-  bool vec = L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_ml32;
+  const uint64_t src0 = sg.src + (L - sg.lane_begin);
+  bool vec = L >= lb && L + 4 <= le && !A.tap_ml32;
 #pragma unroll
   for (int p = 0; p < 3; ++p) vec = vec && (reinterpret_cast<uintptr_t>(A.diff + p * A.cstride + src0) & 15) == 0;
   if (vec) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
       uint4* dd = reinterpret_cast<uint4*>(A.diff + p * A.cstride + src0);
-      uint4 x = dd[0], y = dd[1];
-      x.x -= A.a * d[p][0]; x.y -= A.a * d[p][1]; x.z -= A.a * d[p][2]; x.w -= A.a * d[p][3];
-      y.x -= A.a * d[p][4]; y.y -= A.a * d[p][5]; y.z -= A.a * d[p][6]; y.w -= A.a * d[p][7];
-      dd[0] = x;
-      dd[1] = y;
+      uint4 x = *dd;
+      x.x -= A.a * d[p][0];
+      x.y -= A.a * d[p][1];
+      x.z -= A.a * d[p][2];
+      x.w -= A.a * d[p][3];
+      *dd = x;
     }
     return;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t ln = L8 + i;
-    if (ln < sg.lane_begin || ln >= sg.lane_end) continue;
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t ln = L + i;
+    if (ln < lb || ln >= le) continue;
     const uint64_t src = sg.src + (ln - sg.lane_begin);
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
@@ -823,14 +846,13 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
-  const dim3 grp_blocks((a.grp_seg_max + 8 * 31 - 1) / (8 * 31), 1, a.nsegs);
-  const dim3 rb = grp_blocks;
+  const dim3 tile_blocks(a.task_seg_max, 1, a.nsegs);  // reshare: one CTA per 1024-lane tile
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
   switch (a.variant) {
-    case kPlainMask: k_reshare<kPlainMask><<<rb, 256, 0, st>>>(a); break;
-    case kMpcLift: k_reshare<kMpcLift><<<rb, 256, 0, st>>>(a); break;
-    case kConstLift: k_reshare<kConstLift><<<rb, 256, 0, st>>>(a); break;
-    default: k_reshare<kNoLift><<<rb, 256, 0, st>>>(a); break;
+    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, 256, 0, st>>>(a); break;
+    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, 256, 0, st>>>(a); break;
+    case kConstLift: k_reshare<kConstLift><<<tile_blocks, 256, 0, st>>>(a); break;
+    default: k_reshare<kNoLift><<<tile_blocks, 256, 0, st>>>(a); break;
   }
   prof_end(h, "k_reshare", st);
   debug_check("k_reshare", st);
@@ -840,7 +862,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    k_inject<<<grp_blocks, 256, 0, st>>>(a);
+    k_inject<<<tile_blocks, 256, 0, st>>>(a);
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }

@@ -152,40 +152,55 @@ __device__ __forceinline__ void load4(const T* src, uint64_t kstride, const Seg&
 //   no-lift    : diff = a ml32 - b hd32
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
 //
-// One CTA per 1024-lane tile of a segment (globally 1024-aligned, clipped to the
-// segment).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to 129
-// ChaCha12 blocks covering its 1024 stream elements -- one block per thread per
-// step at full occupancy (the k_gate_keystream pattern), the low 32 bits of
-// each element into shared memory.  Phase 2: thread = 4 lanes, vector loads of
-// the three parties' dots, own = z + F_k - F_{k-1}, vector stores.  (The
-// previous lane-major version held 6 blocks' windows per thread at 121
-// registers and 24% of the warps: 41% of the ChaCha rate.)
+// One CTA per kTile-lane tile of a segment (globally kTile-aligned, clipped to
+// the segment).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to
+// kTile/8 + 1 ChaCha12 blocks covering its kTile stream elements -- one block
+// per thread per step at full occupancy (the k_gate_keystream pattern), the
+// ring-width low bits of each element into shared memory.  Phase 2: thread = 4
+// lanes, vector loads of the three parties' dots, own = z + F_k - F_{k-1},
+// vector stores.  (The previous lane-major version held 6 blocks' windows per
+// thread at 121 registers and 24% of the warps: 41% of the ChaCha rate.)
+// The tile is kept small (6 KB of shared memory for 16-bit rings) so the CTAs
+// fit beside the persistent GEMM's ~193 KB on the same SM: the threshold runs
+// in the SMs' leftover resources while the GEMM streams.
+constexpr int kTile = 512;
+constexpr int kTileThreads = kTile / 4;
+
 template <int V>
-__global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(kTileThreads) k_reshare(const __grid_constant__ ThrArgs A) {
   using HT = typename std::conditional<V == kNoLift, uint32_t, uint16_t>::type;
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr int NDOT = V == kPlainMask ? 1 : 2;  // dot 0 = hd (offset 0), dot 1 = ml (offset n)
-  __shared__ uint32_t F[NDOT][3][1024];
+  constexpr int NB = kTile / 8 + 1;                // blocks per (dot, seed) window
+  using FH = HT;                                   // stored F words: the ring's width
+  using FM = MT;
+  __shared__ FH Fh[3][kTile];
+  __shared__ FM Fm[NDOT - 1 ? 3 : 1][NDOT - 1 ? kTile : 1];
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = (sg.lane_begin / 1024 + blockIdx.x) * 1024;
+  const uint64_t T0 = (sg.lane_begin / kTile + blockIdx.x) * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
-  const uint64_t le = sg.lane_end < T0 + 1024 ? sg.lane_end : T0 + 1024;
+  const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
+  const int lo = (int)(lb - T0), hi = (int)(le - T0);  // valid tile offsets [lo, hi)
   if (!A.no_reshare) {
-    for (int j = threadIdx.x; j < NDOT * 3 * 129; j += blockDim.x) {
-      const int d = j / (3 * 129), k = (j / 129) % 3, q = j % 129;
-      const uint64_t base = A.pos[k] + (d ? A.n : 0);  // stream element of lane 0
-      const uint64_t e0 = base + lb, e1 = base + le - 1;
+    for (int j = threadIdx.x; j < NDOT * 3 * NB; j += blockDim.x) {
+      const int d = j / (3 * NB), k = (j / NB) % 3, q = j % NB;
+      const uint64_t e0 = A.pos[k] + (d ? A.n : 0) + T0;  // stream element of tile offset 0
       const uint64_t b = e0 / 8 + q;
-      if (b > e1 / 8) continue;
+      const int x0 = (int)(b * 8 - e0);  // tile offset of the block's word 0 (>= -7)
+      if (x0 + 7 < lo || x0 >= hi) continue;
       uint32_t blk[16];
       chacha12_block(A.key[k], b, 0, blk);
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
-        const uint64_t e = b * 8 + w;
-        if (e >= e0 && e <= e1) F[d][k][e - base - T0] = blk[2 * w];
+        const int x = x0 + w;
+        if (x < lo || x >= hi) continue;
+        if (d == 0)
+          Fh[k][x] = (FH)blk[2 * w];
+        else
+          Fm[k][x] = (FM)blk[2 * w];
       }
     }
     __syncthreads();
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
       for (int k = 0; k < 3; ++k)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t f = F[1][k][li + i];
+          const uint32_t f = Fm[k][li + i];
           m[k][i] += f;
           m[(k + 1) % 3][i] -= f;
         }
@@ -266,7 +281,7 @@ __global__ void __launch_bounds__(256) k_reshare(const __grid_constant__ ThrArgs
     for (int k = 0; k < 3; ++k)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint32_t f = F[0][k][li + i];
+        const uint32_t f = Fh[k][li + i];
         h[k][i] += f;
         h[(k + 1) % 3][i] -= f;
       }
@@ -471,38 +486,38 @@ __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ T
 // parties at once: P1's c1 (seed 1, one draw per lane) and P3's c3 (seed 3,
 // (c3, w0, w1) per lane, only c3 enters the sharing) give b1 = c1, b3 = c3,
 // b2 = x - b1 - b3 (mod 2^W), each injected bit lifted by 2^17 / 2^16 and
-// subtracted, times a, from diff.  One CTA per 1024-lane tile: phase 1 computes
-// the tile's 2 x (129 + 385) ChaCha12 blocks one per thread per step into
-// shared memory (c1, c3 low halves), phase 2 applies them, thread = 4 lanes.
-__global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs A) {
-  __shared__ uint16_t C[2][2][1024];  // [inject 15 / 16][c1 / c3][lane]
+// subtracted, times a, from diff.  One CTA per kTile-lane tile: phase 1 computes
+// the tile's 2 x (kTile/8 + 1 + 3 kTile/8 + 1) ChaCha12 blocks one per thread
+// per step into shared memory (c1, c3 low halves; 4 KB), phase 2 applies them,
+// thread = 4 lanes.
+__global__ void __launch_bounds__(kTileThreads) k_inject(const __grid_constant__ ThrArgs A) {
+  __shared__ uint16_t C[2][2][kTile];  // [inject 15 / 16][c1 / c3][lane]
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = (sg.lane_begin / 1024 + blockIdx.x) * 1024;
+  const uint64_t T0 = (sg.lane_begin / kTile + blockIdx.x) * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
-  const uint64_t le = sg.lane_end < T0 + 1024 ? sg.lane_end : T0 + 1024;
+  const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
+  const int lo = (int)(lb - T0), hi = (int)(le - T0);
   const uint64_t n = A.n;
-  constexpr int J1 = 129, J3 = 385, JW = J1 + J3;
+  constexpr int J1 = kTile / 8 + 1, J3 = 3 * kTile / 8 + 1, JW = J1 + J3;
   for (int j = threadIdx.x; j < 2 * JW; j += blockDim.x) {
     const int which = j / JW, q = j % JW;
     const bool s3 = q >= J1;
-    // stream element of lane 0: seed 1 at inj_base + (n for inject16) + L,
-    // seed 3 at inj_base + (3n for inject16) + 3L
-    const uint64_t base = s3 ? A.inj_base[2] + (which ? 3 * n : 0) : A.inj_base[0] + (which ? n : 0);
-    const uint64_t e0 = base + (s3 ? 3 * lb : lb), e1 = base + (s3 ? 3 * (le - 1) : le - 1);
+    // stream element of tile offset 0: seed 1 at inj_base + (n for inject16) + T0,
+    // seed 3 at inj_base + (3n for inject16) + 3 T0 (element 3x of lane x is c3)
+    const uint64_t e0 = s3 ? A.inj_base[2] + (which ? 3 * n : 0) + 3 * T0 : A.inj_base[0] + (which ? n : 0) + T0;
     const uint64_t b = e0 / 8 + (s3 ? q - J1 : q);
-    if (b > e1 / 8) continue;
+    const int x0 = (int)(b * 8 - e0);  // element offset of the block's word 0 (>= -7)
+    if (s3 ? (x0 + 7 < 3 * lo || x0 > 3 * (hi - 1)) : (x0 + 7 < lo || x0 >= hi)) continue;
     uint32_t blk[16];
     chacha12_block(A.key[s3 ? 2 : 0], b, 0, blk);
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      const uint64_t e = b * 8 + w;
-      if (e < e0 || e > e1) continue;
-      const uint64_t rel = e - base;
+      const int x = x0 + w;
       if (!s3) {
-        C[which][0][rel - T0] = (uint16_t)blk[2 * w];
-      } else if (rel % 3 == 0) {
-        C[which][1][rel / 3 - T0] = (uint16_t)blk[2 * w];
+        if (x >= lo && x < hi) C[which][0][x] = (uint16_t)blk[2 * w];
+      } else if (x >= 0 && x % 3 == 0 && x / 3 >= lo && x / 3 < hi) {
+        C[which][1][x / 3] = (uint16_t)blk[2 * w];
       }
     }
   }
@@ -510,10 +525,10 @@ __global__ void __launch_bounds__(256) k_inject(const __grid_constant__ ThrArgs 
   const uint64_t L = T0 + 4ull * threadIdx.x;
   if (L + 4 <= lb || L >= le) return;
   const int li = (int)(L - T0);
-  // injected bits: the k_lift thread that owns these lanes (task of this tile, lane word li / 32)
-  const uint64_t task = sg.task_begin + (T0 / 1024 - sg.q_first);
-  const uint64_t o = task * 32 + li / 32;
-  const int sh = li % 32;
+  // injected bits: the k_lift thread that owns these lanes (its 1024-lane task, lane word)
+  const uint64_t task = sg.task_begin + (L / 1024 - sg.q_first);
+  const uint64_t o = task * 32 + (L % 1024) / 32;
+  const int sh = (int)(L % 32);
   const uint32_t x17 = (A.bits[3 * A.nbits + o] ^ A.bits[4 * A.nbits + o] ^ A.bits[5 * A.nbits + o]) >> sh;
   const uint32_t x16 = (A.bits[0 * A.nbits + o] ^ A.bits[1 * A.nbits + o] ^ A.bits[2 * A.nbits + o]) >> sh;
   uint32_t d[3][4];
@@ -846,13 +861,14 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
-  const dim3 tile_blocks(a.task_seg_max, 1, a.nsegs);  // reshare: one CTA per 1024-lane tile
+  // reshare / inject: one CTA per kTile-lane tile (at most 1024 / kTile per 1024-lane task)
+  const dim3 tile_blocks(a.task_seg_max * (1024 / kTile), 1, a.nsegs);
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
   switch (a.variant) {
-    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, 256, 0, st>>>(a); break;
-    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, 256, 0, st>>>(a); break;
-    case kConstLift: k_reshare<kConstLift><<<tile_blocks, 256, 0, st>>>(a); break;
-    default: k_reshare<kNoLift><<<tile_blocks, 256, 0, st>>>(a); break;
+    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+    case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+    default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
   }
   prof_end(h, "k_reshare", st);
   debug_check("k_reshare", st);
@@ -862,7 +878,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    k_inject<<<tile_blocks, 256, 0, st>>>(a);
+    k_inject<<<tile_blocks, kTileThreads, 0, st>>>(a);
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }

@@ -394,8 +394,46 @@ def main_gpu(args):
             return sess.sharded_batch_query([h.numpy() for h in host_q] if rank == 0 else None, persons, qlen)
         return sess.sharded_batch_query(qpay if rank == 0 else None, persons, qlen)
 
-    for _ in range(args.warmup):
-        out = step(False)
+    streaming = world == 1 and not args.sync
+    # streaming (irismpc_gpu_batch_query_submit / _wait, two queries in flight): the
+    # GEMM stream runs into query i+1 while the threshold stream finishes query i;
+    # every step still copies its inputs (e2e: from pinned host memory) and reads
+    # its person bits back.  Double-buffered device payloads for the e2e leg.
+    qdev2 = [[torch.empty_like(x) for x in qpay] for _ in range(2)]
+
+    def run_steps(k: int, from_host: bool, acc=None):
+        res = None
+
+        def account(st):
+            if acc is not None:
+                acc["gemm_ms"] += st.gemm_ms
+                acc["launches"] += st.kernel_launches
+                acc["gemm_launches"] += st.gemm_launches
+                acc["gemm_ops"] += st.gemm_int8_ops
+                acc["rp"] = int(st.rotation_pair_gemm)
+
+        if not streaming:
+            for _ in range(k):
+                res = step(from_host)
+                account(sess.last_stats)
+            return res
+        tickets = []
+        for i in range(k):
+            src = qpay
+            if from_host:
+                src = qdev2[i % 2]
+                with torch.cuda.stream(ext):  # H2D ordered before the query's parse on the same stream
+                    for d, h in zip(src, host_q):
+                        d.copy_(h, non_blocking=True)
+            tickets.append(sess.batch_query_submit(src, persons))
+            if i >= 1:
+                res = sess.batch_query_wait(tickets[i - 1])
+                account(sess.last_stats)
+        res = sess.batch_query_wait(tickets[-1])
+        account(sess.last_stats)
+        return res
+
+    out = run_steps(args.warmup, False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -410,14 +448,7 @@ def main_gpu(args):
         with torch.cuda.stream(ext):
             ev0.record()
         h0 = time.perf_counter()
-        for _ in range(args.steps):
-            out = step(False)
-            st = sess.last_stats
-            stats_acc["gemm_ms"] += st.gemm_ms
-            stats_acc["launches"] += st.kernel_launches
-            stats_acc["gemm_launches"] += st.gemm_launches
-            stats_acc["gemm_ops"] += st.gemm_int8_ops
-            stats_acc["rp"] = int(st.rotation_pair_gemm)
+        out = run_steps(args.steps, False, stats_acc)
         with torch.cuda.stream(ext):
             ev1.record()
         torch.cuda.synchronize()
@@ -431,17 +462,31 @@ def main_gpu(args):
     ms = float(t.item())
     planted = int(out[0]) if out is not None else None
 
-    # e2e through the public API from pinned host buffers (H2D + D2H inside)
-    e2e_ms = []
-    for _ in range(max(2, args.steps // 2)):
-        if world > 1:
-            dist.barrier()
+    # e2e through the public API from pinned host buffers: every step's H2D of its
+    # three payloads and D2H of its person bits inside the timed region
+    if streaming:
         torch.cuda.synchronize()
         a = time.perf_counter()
-        step(True)
+        run_steps(args.steps, True)
         torch.cuda.synchronize()
-        e2e_ms.append((time.perf_counter() - a) * 1e3)
-    e2e = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
+        e2e_step_ms = (time.perf_counter() - a) * 1e3 / args.steps
+        e2e_note = (f"{args.steps} back-to-back streaming queries (submit / wait, two in flight) through the "
+                    "public API, each with its pinned-host payload upload and person-bit read-back; host wall "
+                    "clock over all of them")
+    else:
+        e2e_ms = []
+        for _ in range(max(2, args.steps // 2)):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            step(True)
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - a) * 1e3)
+        e2e_step_ms = statistics.median(e2e_ms)
+        e2e_note = ("median of single synchronous queries through the public API (pinned host payloads in, "
+                    "person_match out), each bracketed by a host sync")
+    e2e = torch.tensor([e2e_step_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
 
@@ -495,11 +540,11 @@ def main_gpu(args):
                        "variant": args.variant,
                        "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM, "
                              f"{plane_kb * rows / 1e6:.1f} GB per GPU)",
-                       "parallelism": f"db-shard x{world}"},
+                       "parallelism": f"db-shard x{world}",
+                       "query_api": "streaming submit/wait (2 in flight)" if streaming else "synchronous"},
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons,
-                    "note": "median of single queries through the public API (pinned host payloads in, "
-                            "person_match out), each bracketed by a host sync"},
+                    "note": e2e_note},
             "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
                          "achieved": exec_tops, "peak": peak, "unit": "TFLOP/s", "frac": exec_tops / peak,
                          "traffic": ncu_traffic(bool(stats_acc["rp"]))[0],
@@ -557,6 +602,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=REF_ROWS, dest="ref_rows")
     ap.add_argument("--no-cpu", action="store_true", dest="no_cpu")
     ap.add_argument("--no-profile", action="store_true", dest="no_profile")
+    ap.add_argument("--sync", action="store_true", help="synchronous queries (no streaming submit / wait)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -119,6 +119,17 @@ int irismpc_gpu_batch_query_device(irismpc_gpu_ctx* ctx, const uint8_t* const dq
                                    const size_t qlen[3], uint32_t persons,
                                    uint8_t* person_match_out, uint8_t* row_bits_out,
                                    irismpc_gpu_stats* stats);
+/* Streaming: queue a batch query (DEVICE payloads, which must stay valid until
+ * the ticket completes) and return at once.  The GEMM stream runs ahead into
+ * the next submitted query while the threshold stream finishes this one, so a
+ * query's GEMM-only head and threshold-only tail overlap its neighbours'.  At
+ * most two queries are in flight: a third submit first completes the oldest.
+ * person_match_out is written when the ticket completes (wait, or that
+ * implicit completion).  Not with taps / debug_rows.  Results and PRF stream
+ * positions are identical to the synchronous calls in the same order. */
+int irismpc_gpu_batch_query_submit(irismpc_gpu_ctx* ctx, const uint8_t* const dq[3], const size_t qlen[3],
+                                   uint32_t persons, uint8_t* person_match_out, uint64_t* ticket);
+int irismpc_gpu_batch_query_wait(irismpc_gpu_ctx* ctx, uint64_t ticket, irismpc_gpu_stats* stats);
 /* Single code, no rotation, one group (Session::membership). */
 int irismpc_gpu_membership(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
                            uint8_t* match_out, uint8_t* row_bits_out, irismpc_gpu_stats* stats);

@@ -44,7 +44,7 @@ EXPORTED = [
     "irismpc_gpu_tap_rows", "irismpc_gpu_comparison_only", "irismpc_gpu_or_tree_only",
     "irismpc_gpu_shard_group_create", "irismpc_gpu_shard_group_destroy", "irismpc_gpu_shard_attach_inproc",
     "irismpc_gpu_shard_attach_nccl", "irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device",
-    "irismpc_gpu_sharded_membership",
+    "irismpc_gpu_sharded_membership", "irismpc_gpu_batch_query_submit", "irismpc_gpu_batch_query_wait",
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
@@ -176,6 +176,8 @@ def lib() -> C.CDLL:
         for f in ("irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device"):
             getattr(L, f).argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(Stats)]
         L.irismpc_gpu_sharded_membership.argtypes = [vp, P3, S3, vp, C.POINTER(Stats)]
+        L.irismpc_gpu_batch_query_submit.argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(C.c_uint64)]
+        L.irismpc_gpu_batch_query_wait.argtypes = [vp, C.c_uint64, C.POINTER(Stats)]
         L.irismpc_gpu_profile_read.argtypes = [vp, vp, vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
         cp3 = C.c_char_p * 3
@@ -415,6 +417,25 @@ class Session:
                       C.byref(self.last_stats)))
         self.row_bits = rows
         return out[:persons]
+
+    def batch_query_submit(self, q, persons: int) -> int:
+        """Streaming batch query (device payloads kept alive until the wait): returns a ticket."""
+        dev, arrs, ptrs, lens = self._q(q)
+        if not dev:
+            raise ConfigError("batch_query_submit expects device-resident payloads")
+        out = np.zeros(max(1, persons), np.uint8)
+        t = C.c_uint64(0)
+        self._check(lib().irismpc_gpu_batch_query_submit(self._h, ptrs, lens, persons, out.ctypes.data, C.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (out[:persons], arrs)
+        return t.value
+
+    def batch_query_wait(self, ticket: int) -> np.ndarray:
+        """Completes a streaming query: its person_match (stats in last_stats)."""
+        self._check(lib().irismpc_gpu_batch_query_wait(self._h, ticket, C.byref(self.last_stats)))
+        out, _ = self._inflight.pop(ticket)
+        return out
 
     def membership(self, q, want_rows: bool = False) -> bool:
         """Session::membership: one code, no rotation."""

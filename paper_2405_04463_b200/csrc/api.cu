@@ -259,10 +259,36 @@ struct FieldPlanes {
   }
 };
 
+// One in-flight batch query's buffers (irismpc_gpu_batch_query_submit): the
+// GEMM stream (st) runs ahead into the next query while the threshold stream
+// (st2) finishes this one, so everything the threshold side of a query reads
+// after its prep -- segment table, OR slot ranges, pair dots, match words --
+// and its result buffers are per slot; two slots alternate.
+struct QSlot {
+  Buf segs, slot_begin, match[3], pair_dots, open_out;
+  Seg* h_segs = nullptr;
+  size_t h_segs_cap = 0;
+  uint8_t* h_match = nullptr;  // pinned copy of the opened person bits
+  size_t h_match_cap = 0;
+  cudaEvent_t ev[6] = {};
+  cudaEvent_t done = nullptr;
+  std::vector<cudaEvent_t> gev;  // per chunk: GEMM start / stop
+  bool inflight = false;
+  uint64_t ticket = 0;
+  // what finish_slot needs
+  int mode = 0;
+  uint32_t ngroups = 0;
+  uint8_t* match_out = nullptr;
+  uint8_t* row_bits_out = nullptr;
+  uint64_t n = 0, nchunks = 0;
+  irismpc_gpu_stats stats{};
+  bool want_stats = false;
+};
+
 struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
-  cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr;
   int shamir = 0;
   int variant = kMpcLift;
   VariantWidths vw{16, 16, 32};
@@ -276,7 +302,7 @@ struct irismpc_gpu_ctx {
   // query scratch
   Buf q_pay[3];
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
-  Buf ml_rs, diff, gate, bits, gate2, bits2;
+  Buf ml_rs, diff, gate, bits;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
@@ -296,8 +322,12 @@ struct irismpc_gpu_ctx {
   cudaEvent_t ev[6];
   std::unique_ptr<ShardComm> shard;  // DB-sharded queries (irismpc_gpu_shard_attach_*)
   Buf shard_part, shard_all;
-  std::vector<cudaEvent_t> gev;  // per GEMM launch start/stop
-  std::vector<cudaEvent_t> evg, evt, evt3;  // chunk pipeline: GEMM done / threshold done (st2, st3)
+  std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done (st) / threshold done (st2)
+  QSlot qs[2];
+  int par = 0;                 // slot of the next query
+  uint64_t tickets = 0;        // submitted batch queries
+  uint64_t chunk_ctr = 0;      // dot-buffer half of the next row chunk (continues across queries)
+  cudaEvent_t half_free[2] = {nullptr, nullptr};  // threshold of the last chunk that read each half
 };
 
 namespace {
@@ -369,7 +399,10 @@ uint64_t s_total(const irismpc_gpu_ctx* c) {
   return c->cfg.db_rows_total ? c->cfg.db_rows_total : c->s;
 }
 
+int drain(irismpc_gpu_ctx* c);
+
 int alloc_planes(irismpc_gpu_ctx* c, uint64_t s) {
+  if (int rc = drain(c)) return rc;
   for (auto& f : c->fld) {
     f.db.release();
     f.sdb.release();
@@ -487,10 +520,18 @@ GemmArgs field_gemm_args(const irismpc_gpu_ctx* c, const FieldPlanes& f, uint32_
 // stream st while the K4 threshold pipeline of chunk i-1 runs on stream st2
 // (tensor pipe vs ALU pipes), dot outputs double-buffered.  The pair lanes,
 // the per-person OR and the open follow on st2 / st.
+int finish_slot(irismpc_gpu_ctx* c, QSlot& q);
+
 int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3], uint32_t persons,
               int membership, int mode, uint8_t* match_out, uint8_t* row_bits_out, uint8_t* partial_dev,
-              irismpc_gpu_stats* stats, bool host_input, const uint8_t* const hq[3]) {
+              irismpc_gpu_stats* stats, bool host_input, const uint8_t* const hq[3], uint64_t* ticket_out = nullptr) {
   if (!c->db_loaded) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no database loaded");
+  // the slot this query uses: its previous occupant (two queries back) must be done
+  QSlot& Q = c->qs[c->par];
+  if (Q.inflight) {
+    const int rc = finish_slot(c, Q);
+    if (rc) return rc;
+  }
   const size_t rec = c->rec;
   const uint32_t ncodes = membership ? 1u : 2u * persons;
   for (int p = 0; p < 3; ++p) {
@@ -529,17 +570,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     return e && e[0] == '1';
   }();
   cudaStream_t st = c->st, st2 = (serial || c->serial) ? c->st : c->st2;
-  // two threshold streams: a chunk's columns split into two jobs, so one job's
-  // latency-bound bit-sliced kernels overlap the other's ChaCha kernels
-  static const int thr_streams = [] {
-    const char* e = std::getenv("IRISMPC_THR_STREAMS");
-    return e ? std::max(1, std::min(2, std::atoi(e))) : 1;
-  }();
-  const bool two = thr_streams == 2 && !serial && !c->serial;
-  cudaStream_t st3 = two ? c->st3 : st2;
   uint64_t launches = 0;
+  for (auto& e : Q.ev)
+    if (!e) CK(c, cudaEventCreate(&e));
+  if (!Q.done) CK(c, cudaEventCreateWithFlags(&Q.done, cudaEventDisableTiming));
+  for (auto& e : c->half_free)
+    if (!e) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
-  CK(c, cudaEventRecord(c->ev[0], st));
+  CK(c, cudaEventRecord(Q.ev[0], st));
   const uint8_t* dqp[3] = {dq[0], dq[1], dq[2]};
   if (host_input) {
     for (int p = 0; p < 3; ++p) {
@@ -587,9 +625,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   // chunk 0's GEMM starts earlier.
   auto pair_gemm = [&]() -> int {
     const uint64_t spq = round_up(ncodes, 2 * kGemmBM);
-    if (c->pair_dots.ensure(npairs * (3 * hb + fm.nparty * mb) + 64))
+    if (Q.pair_dots.ensure(npairs * (3 * hb + fm.nparty * mb) + 64))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (pair dots)");
-    uint8_t* pd_out[2] = {c->pair_dots.as<uint8_t>(), c->pair_dots.as<uint8_t>() + 3 * npairs * hb};
+    uint8_t* pd_out[2] = {Q.pair_dots.as<uint8_t>(), Q.pair_dots.as<uint8_t>() + 3 * npairs * hb};
     void* ph = prof_begin(st);
     for (int fi = 0; fi < 2; ++fi) {
       FieldPlanes& f = c->fld[fi];
@@ -622,7 +660,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     CK(c, cudaGetLastError());
     return 0;
   };
-  CK(c, cudaEventRecord(c->ev[1], st));
+  CK(c, cudaEventRecord(Q.ev[1], st));
 
   const bool row_taps = c->tap_k > 0;
   if (row_taps) {  // compact L1 taps: [p][col * k + i] then the pair lanes
@@ -738,10 +776,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     if (per_person_max >= kOrTreeOffset || ngroups >= (1u << 23))
       return fail(c, IRISMPC_GPU_ERR_BOUNDS, "OR-gate stream windows exceeded (persons >= 2^23 or 2^39 items)");
   }
-  if (c->partial.ensure(3 * total_slots + 16) || c->slot_begin.ensure((ngroups + 1) * sizeof(uint64_t)) ||
+  if (c->partial.ensure(3 * total_slots + 16) || Q.slot_begin.ensure((ngroups + 1) * sizeof(uint64_t)) ||
       c->person_out.ensure(3ull * ngroups + 16))
     return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or buffers)");
-  CK(c, cudaMemcpyAsync(c->slot_begin.p, h_slot_begin.data(), (ngroups + 1) * sizeof(uint64_t),
+  CK(c, cudaMemcpyAsync(Q.slot_begin.p, h_slot_begin.data(), (ngroups + 1) * sizeof(uint64_t),
                         cudaMemcpyHostToDevice, st));
 
   const bool dbg = c->cfg.debug_rows != 0 && row_bits_out;
@@ -753,8 +791,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     match_words = ceil_div(n, 32) - match_w0 + 1;
   }
   for (int p = 0; p < 3 && match_words; ++p) {
-    if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
-    CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
+    if (Q.match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
+    CK(c, cudaMemsetAsync(Q.match[p].p, 0, match_words * 4, st));
   }
 
   // ---- segments [chunk][col] then the pair segment; jobs group segments
@@ -764,12 +802,19 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   };
   std::vector<Job> jobs;
   const uint64_t nsegs_all = nchunks * ncols + (npairs ? 1 : 0);
-  if (ensure_host_segs(c, nsegs_all + 1)) return IRISMPC_GPU_ERR_DEVICE;
-  if (c->segs.ensure((nsegs_all + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
+  if (nsegs_all + 1 > Q.h_segs_cap) {
+    if (Q.h_segs) cudaFreeHost(Q.h_segs);
+    Q.h_segs = nullptr;
+    Q.h_segs_cap = 0;
+    CK(c, cudaMallocHost(&Q.h_segs, (nsegs_all + 1) * sizeof(Seg)));
+    Q.h_segs_cap = nsegs_all + 1;
+  }
+  Seg* const hsegs = Q.h_segs;
+  if (Q.segs.ensure((nsegs_all + 1) * sizeof(Seg))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (segs)");
   auto add_job = [&](uint64_t seg0, uint64_t nseg, bool pair, uint64_t chunk) {
     Job j{seg0, nseg, 0, 0, 0, 0, chunk, 0, 0, 0, pair};
     for (uint64_t i = seg0; i < seg0 + nseg; ++i) {
-      Seg& sg = c->h_segs_pinned[i];
+      Seg& sg = hsegs[i];
       sg.q_first = sg.lane_begin / 1024;
       sg.w_first = sg.lane_begin / 64;
       sg.task_begin = j.ntasks;
@@ -797,7 +842,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     for (uint64_t i = 0; i < nchunks; ++i) {
       const uint64_t nr = chunk_rows(i);
       for (uint64_t col = 0; col < ncols; ++col) {
-        Seg& sg = c->h_segs_pinned[i * ncols + col];
+        Seg& sg = hsegs[i * ncols + col];
         sg.lane_begin = col * S + row_off + chunk_row0[i];
         sg.lane_end = sg.lane_begin + nr;
         sg.src = col * nr;
@@ -806,15 +851,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         sg.slot = (int64_t)col_fill[col];
         col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
-      uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
-      if (two && ncols >= 2) per_job = std::min<uint64_t>(per_job, ceil_div(ncols, 2));
+      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
       for (uint64_t a = 0; a < ncols; a += per_job)
         add_job(i * ncols + a, std::min<uint64_t>(per_job, ncols - a), false, i);
       cstride = std::max<uint64_t>(cstride, ncols * nr);
     }
   }
   if (npairs) {
-    Seg& sg = c->h_segs_pinned[nsegs_all - 1];
+    Seg& sg = hsegs[nsegs_all - 1];
     sg.lane_begin = ncols * S;
     sg.lane_end = n;
     sg.src = 0;
@@ -836,13 +880,11 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t hd_half = 3 * hcols * rows_chunk * hb;
   const uint64_t dots_half = round_up(hd_half + fm.nparty * mcols * rows_chunk * mb, 16);
   if (nsegs_all) {
-    CK(c, cudaMemcpyAsync(c->segs.p, c->h_segs_pinned, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(Q.segs.p, hsegs, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
     if ((nchunks && c->dots.ensure(2 * dots_half)) ||
         c->ml_rs.ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
         c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) || c->gate.ensure(max_g * sizeof(uint64_t) + 16) ||
-        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16) ||
-        (two && (c->gate2.ensure(max_g * sizeof(uint64_t) + 16) ||
-                 c->bits2.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))))
+        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
   // per-chunk S planes (IRISMPC_RP_CHUNKED): one scratch per field, reused chunk after chunk on
@@ -897,9 +939,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   uint64_t task_off = 0;
   // hd_base: [3][pstride] hd dots; ml_base: [nparty][pstride] ml dots / public popcounts
   auto run_job = [&](const Job& j, const uint8_t* hd_base, const uint8_t* ml_base, uint64_t pstride_h,
-                     uint64_t pstride_m, uint64_t ks_h, uint64_t ks_m, int lane) -> int {
+                     uint64_t pstride_m, uint64_t ks_h, uint64_t ks_m) -> int {
     ThrArgs t = ta;
-    t.segs = c->segs.as<Seg>() + j.seg0;
+    t.segs = Q.segs.as<Seg>() + j.seg0;
     t.nsegs = (uint32_t)j.nseg;
     t.ntasks = j.ntasks;
     t.ngrp = j.ngrp;
@@ -907,20 +949,20 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.ks_seg_threads = (uint32_t)j.ks_seg;
     t.grp_seg_max = (uint32_t)j.grp_seg;
     t.task_seg_max = (uint32_t)j.task_seg;
-    t.bits = (lane ? c->bits2 : c->bits).as<uint32_t>();
-    t.gate = (lane ? c->gate2 : c->gate).as<uint64_t>();
+    t.bits = c->bits.as<uint32_t>();
+    t.gate = c->gate.as<uint64_t>();
     t.nbits = j.ntasks * 32;
     t.or_elem_base = ta.or_elem_base + task_off * 64;
     task_off += j.ntasks;
     for (int p = 0; p < 3; ++p) {
       t.hd[p] = hd_base + p * pstride_h * hb;
       t.ml[p] = ml_base + (fm.nparty == 3 ? p : 0) * pstride_m * mb;
-      t.match[p] = (j.pair || dbg) ? c->match[p].as<uint32_t>() : nullptr;
+      t.match[p] = (j.pair || dbg) ? Q.match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
     t.rp_kstride_h = ks_h;
     t.rp_kstride_m = ks_m;
-    launch_threshold(t, lane ? st3 : st2);
+    launch_threshold(t, st2);
     CK(c, cudaGetLastError());
     launches += V == kMpcLift ? 5 : 3;
     return 0;
@@ -933,22 +975,19 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     return 0;
   };
-  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1) || ensure_events(c->evt3, nchunks + 1))
-    return IRISMPC_GPU_ERR_DEVICE;
-  while (c->gev.size() < 2 * nchunks) {
+  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1)) return IRISMPC_GPU_ERR_DEVICE;
+  while (Q.gev.size() < 2 * nchunks) {
     cudaEvent_t e;
     CK(c, cudaEventCreate(&e));
-    c->gev.push_back(e);
+    Q.gev.push_back(e);
   }
 
   // st2 starts once the prep on st (payload parse, pairs, memsets, uploads) is queued before it
   CK(c, cudaEventRecord(c->evg[nchunks], st));
   CK(c, cudaStreamWaitEvent(st2, c->evg[nchunks], 0));
-  if (two) CK(c, cudaStreamWaitEvent(st3, c->evg[nchunks], 0));
-  CK(c, cudaEventRecord(c->ev[2], st2));
+  CK(c, cudaEventRecord(Q.ev[2], st2));
 
   // ---- DB lanes: GEMMs(i) on st || threshold(i-1) on st2
-  double gemm_ms = 0;
   uint64_t gemm_launches = 0;
   uint64_t gemm_ops = 0;  // executed int8 ops of the DB-lane GEMMs
   for (int fi = 0; fi < 2; ++fi) {
@@ -960,13 +999,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   size_t ji = 0;
   for (uint64_t i = 0; i < nchunks; ++i) {
     const uint64_t nr = chunk_rows(i);
-    uint8_t* dots = c->dots.as<uint8_t>() + (i % 2) * dots_half;
+    // dot-buffer halves alternate across chunks and across queries: the GEMM
+    // waits for the threshold of the last chunk (of any query) that read the half
+    const int half = (int)(c->chunk_ctr++ % 2);
+    uint8_t* dots = c->dots.as<uint8_t>() + half * dots_half;
     uint8_t* dots_ml = dots + hd_half;
-    if (i >= 2) {  // buffer i%2 released
-      CK(c, cudaStreamWaitEvent(st, c->evt[i - 2], 0));
-      if (two) CK(c, cudaStreamWaitEvent(st, c->evt3[i - 2], 0));
-    }
-    CK(c, cudaEventRecord(c->gev[2 * i], st));
+    CK(c, cudaStreamWaitEvent(st, c->half_free[half], 0));
+    CK(c, cudaEventRecord(Q.gev[2 * i], st));
     for (int fi = 0; fi < 2; ++fi) {
       FieldPlanes& f = c->fld[fi];
       const uint32_t m_tiles = (uint32_t)(round_up(nr, 2 * kGemmBM) / kGemmBM);
@@ -1015,7 +1054,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       debug_check("k_limb_gemm_pair", st);
       CK(c, cudaGetLastError());
     }
-    CK(c, cudaEventRecord(c->gev[2 * i + 1], st));
+    CK(c, cudaEventRecord(Q.gev[2 * i + 1], st));
     if (row_taps) {
       const uint64_t nt = c->tap_n;
       launch_tap_rows(dots, (int)hb, 3, ncols, r, nr, use_rp[0] ? 3 * ncols_rp * nr : 0,
@@ -1042,33 +1081,24 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     CK(c, cudaEventRecord(c->evg[i], st));
     CK(c, cudaStreamWaitEvent(st2, c->evg[i], 0));
-    if (two) {
-      CK(c, cudaStreamWaitEvent(st3, c->evg[i], 0));
-      if (i >= 1) {  // the work buffers (ml_rs, diff) are chunk-relative: chunk i-1's jobs first
-        CK(c, cudaStreamWaitEvent(st2, c->evt3[i - 1], 0));
-        CK(c, cudaStreamWaitEvent(st3, c->evt[i - 1], 0));
-      }
-    }
-    for (int lane = 0; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji, lane ^= (two ? 1 : 0)) {
+    for (; ji < jobs.size() && !jobs[ji].pair && jobs[ji].chunk == i; ++ji) {
       const uint64_t rpn = ncols_rp * nr;
       int rc2 = run_job(jobs[ji], dots, dots_ml, use_rp[0] ? rpn : ncols * nr, use_rp[1] ? rpn : ncols * nr,
-                        use_rp[0] ? 3 * rpn : 0, use_rp[1] ? 3 * rpn : 0, lane);
+                        use_rp[0] ? 3 * rpn : 0, use_rp[1] ? 3 * rpn : 0);
       if (rc2) return rc2;
     }
-    CK(c, cudaEventRecord(c->evt[i], st2));
-    if (two) CK(c, cudaEventRecord(c->evt3[i], st3));
+    CK(c, cudaEventRecord(c->half_free[half], st2));
   }
 
   // ---- pair lanes (shard 0): pair GEMMs on st, then their threshold into match words on st2
   if (npairs) {
     const int prc = pair_gemm();
     if (prc) return prc;
-    CK(c, cudaEventRecord(c->ev[5], st));
-    CK(c, cudaStreamWaitEvent(st2, c->ev[5], 0));
+    CK(c, cudaEventRecord(Q.ev[5], st));
+    CK(c, cudaStreamWaitEvent(st2, Q.ev[5], 0));
   }
-  if (two && nchunks) CK(c, cudaStreamWaitEvent(st2, c->evt3[nchunks - 1], 0));
   if (npairs) {
-    const uint8_t* pd_hd = c->pair_dots.as<uint8_t>();
+    const uint8_t* pd_hd = Q.pair_dots.as<uint8_t>();
     const uint8_t* pd_ml = pd_hd + 3 * npairs * hb;
     if (row_taps) {
       const uint64_t nt = c->tap_n, o = ncols * c->tap_k;
@@ -1086,21 +1116,17 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         CK(c, cudaMemcpyAsync(c->tap_buf[1].as<uint8_t>() + (p * n + ncols * S) * mb, pd_ml + p * npairs * mb,
                               npairs * mb, cudaMemcpyDeviceToDevice, st2));
     }
-    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, npairs, 0, 0, 0);
+    int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, npairs, 0, 0);
     if (rc2) return rc2;
   }
-  if (two) {  // the OR reads every job's partial slots (and the pair job reused the work buffers)
-    CK(c, cudaEventRecord(c->evt3[nchunks], st3));
-    CK(c, cudaStreamWaitEvent(st2, c->evt3[nchunks], 0));
-  }
-  CK(c, cudaEventRecord(c->ev[3], st2));
+  CK(c, cudaEventRecord(Q.ev[3], st2));
 
   // ---- per-person OR (st2), then the open on st
   OrArgs oa{};
   oa.partial = c->partial.as<uint8_t>();
   oa.nslots = total_slots;
-  oa.slot_begin = c->slot_begin.as<uint64_t>();
-  for (int p = 0; p < 3; ++p) oa.pair_match[p] = npairs ? c->match[p].as<uint32_t>() : nullptr;
+  oa.slot_begin = Q.slot_begin.as<uint64_t>();
+  for (int p = 0; p < 3; ++p) oa.pair_match[p] = npairs ? Q.match[p].as<uint32_t>() : nullptr;
   oa.pair_w0 = match_w0;
   oa.pair_lane0 = ncols * S;
   oa.persons = ngroups;
@@ -1114,32 +1140,36 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   debug_check("k_or_persons", st2);
   CK(c, cudaGetLastError());
   ++launches;
-  CK(c, cudaEventRecord(c->evt[nchunks], st2));
-  CK(c, cudaStreamWaitEvent(st, c->evt[nchunks], 0));
-
+  // the open (mode 0) or the partial hand-off (mode 1) also on the threshold
+  // stream, so the GEMM stream is free for the next query's chunks
   if (mode == 0) {
-    if (c->open_out.ensure(ngroups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    if (Q.open_out.ensure(ngroups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    if (ngroups + 16 > Q.h_match_cap) {
+      if (Q.h_match) cudaFreeHost(Q.h_match);
+      Q.h_match = nullptr;
+      Q.h_match_cap = 0;
+      CK(c, cudaMallocHost(&Q.h_match, ngroups + 16));
+      Q.h_match_cap = ngroups + 16;
+    }
     launch_or_open(c->person_out.as<uint8_t>(), 1, ngroups, c->keys, or_stream_id(octr, rank, 3),
-                   c->open_out.as<uint8_t>(), st);
+                   Q.open_out.as<uint8_t>(), st2);
     CK(c, cudaGetLastError());
     ++launches;
-    CK(c, cudaMemcpyAsync(match_out, c->open_out.p, ngroups, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaMemcpyAsync(Q.h_match, Q.open_out.p, ngroups, cudaMemcpyDeviceToHost, st2));
   } else {
-    CK(c, cudaMemcpyAsync(partial_dev, c->person_out.p, 3ull * ngroups, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemcpyAsync(partial_dev, c->person_out.p, 3ull * ngroups, cudaMemcpyDeviceToDevice, st2));
   }
-  CK(c, cudaEventRecord(c->ev[4], st));
-  if (dbg) {
-    std::vector<uint32_t> w[3];
-    const uint64_t nw = ceil_div(n, 32);
-    for (int p = 0; p < 3; ++p) {
-      w[p].resize(nw);
-      CK(c, cudaMemcpyAsync(w[p].data(), c->match[p].p, nw * 4, cudaMemcpyDeviceToHost, st));
-    }
-    CK(c, cudaStreamSynchronize(st));
-    for (uint64_t i = 0; i < n; ++i)
-      row_bits_out[i] = (uint8_t)(((w[0][i / 32] ^ w[1][i / 32] ^ w[2][i / 32]) >> (i % 32)) & 1u);
-  }
-  CK(c, cudaStreamSynchronize(st));
+  CK(c, cudaEventRecord(Q.ev[4], st2));
+  CK(c, cudaEventRecord(Q.done, st2));
+  Q.inflight = true;
+  Q.ticket = ++c->tickets;
+  Q.mode = mode;
+  Q.ngroups = ngroups;
+  Q.match_out = match_out;
+  Q.row_bits_out = dbg ? row_bits_out : nullptr;
+  Q.n = n;
+  Q.nchunks = nchunks;
+  c->par ^= 1;
 
   // ---- advance the seed streams exactly as the reference does (A.3)
   const uint64_t glen = membership ? S : 2ull * r * S + (uint64_t)(persons ? persons - 1 : 0) * 4 * r;
@@ -1148,42 +1178,81 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t msb_draws = (uint64_t)(2 * vw.kc - 3) * W;
   for (int k = 0; k < 3; ++k) c->pos[k] = ta.msb_base[k] + msb_draws + ord;
 
-  if (stats) {
-    std::memset(stats, 0, sizeof(*stats));
-    stats->s = S;
-    stats->l = c->l;
-    stats->batch = membership ? 1 : persons;
-    stats->lanes = n;
+  {
+    irismpc_gpu_stats* st_ = &Q.stats;
+    std::memset(st_, 0, sizeof(*st_));
+    st_->s = S;
+    st_->l = c->l;
+    st_->batch = membership ? 1 : persons;
+    st_->lanes = n;
     const uint64_t nb8 = ceil_div(n, 8), open_b = ceil_div(ngroups, 8);
     for (int p = 0; p < 3; ++p) {
-      stats->dot_bytes[p] = n * (vw.kh / 8) + nml * (vw.km / 8);
-      stats->lift_bytes[p] = V == kMpcLift ? 64 * nb8 + (p == 0 ? 8 * n : 4 * n) : 0;
-      stats->msb_bytes[p] = (uint64_t)(2 * vw.kc - 3) * nb8;
-      stats->or_tree_bytes[p] = or_bytes + (p == 0 ? 0 : open_b) + (c->cfg.debug_rows && p != 0 ? nb8 : 0);
+      st_->dot_bytes[p] = n * (vw.kh / 8) + nml * (vw.km / 8);
+      st_->lift_bytes[p] = V == kMpcLift ? 64 * nb8 + (p == 0 ? 8 * n : 4 * n) : 0;
+      st_->msb_bytes[p] = (uint64_t)(2 * vw.kc - 3) * nb8;
+      st_->or_tree_bytes[p] = or_bytes + (p == 0 ? 0 : open_b) + (c->cfg.debug_rows && p != 0 ? nb8 : 0);
     }
-    stats->dot_rounds = 1;
-    stats->lift_rounds = V == kMpcLift ? 21 : 0;
-    stats->msb_rounds = (uint64_t)vw.kc - 1;
-    stats->or_tree_rounds = or_rounds + 1 + (c->cfg.debug_rows ? 1 : 0);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
-    stats->wall_ms = ms;
-    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-    stats->prep_ms = ms;
-    for (uint64_t i = 0; i < nchunks; ++i) {
-      cudaEventElapsedTime(&ms, c->gev[2 * i], c->gev[2 * i + 1]);
-      gemm_ms += ms;
-    }
-    stats->gemm_ms = gemm_ms;
-    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
-    stats->threshold_ms = ms;  // stream-2 span: threshold of all chunks (overlaps the GEMMs)
-    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
-    stats->or_ms = ms;
-    stats->gemm_launches = gemm_launches;
-    stats->kernel_launches = launches;
-    stats->gemm_int8_ops = gemm_ops;
-    stats->rotation_pair_gemm = (use_rp[0] || use_rp[1]) ? 1u : 0u;
+    st_->dot_rounds = 1;
+    st_->lift_rounds = V == kMpcLift ? 21 : 0;
+    st_->msb_rounds = (uint64_t)vw.kc - 1;
+    st_->or_tree_rounds = or_rounds + 1 + (c->cfg.debug_rows ? 1 : 0);
+    st_->gemm_launches = gemm_launches;
+    st_->kernel_launches = launches;
+    st_->gemm_int8_ops = gemm_ops;
+    st_->rotation_pair_gemm = (use_rp[0] || use_rp[1]) ? 1u : 0u;
   }
+  if (ticket_out) {  // asynchronous: the caller collects with irismpc_gpu_batch_query_wait
+    *ticket_out = Q.ticket;
+    return 0;
+  }
+  const int rc_f = finish_slot(c, Q);
+  if (rc_f) return rc_f;
+  if (stats) *stats = Q.stats;
+  return 0;
+}
+
+// Completes a slot's query: waits for its last event, copies the opened bits
+// (and the debug row bits) out, fills the device times.
+int finish_slot(irismpc_gpu_ctx* c, QSlot& q) {
+  if (!q.inflight) return 0;
+  q.inflight = false;
+  CK(c, cudaEventSynchronize(q.done));
+  if (q.mode == 0 && q.match_out) std::memcpy(q.match_out, q.h_match, q.ngroups);
+  if (q.row_bits_out) {
+    std::vector<uint32_t> w[3];
+    const uint64_t nw = ceil_div(q.n, 32);
+    for (int p = 0; p < 3; ++p) {
+      w[p].resize(nw);
+      CK(c, cudaMemcpy(w[p].data(), q.match[p].p, nw * 4, cudaMemcpyDeviceToHost));
+    }
+    for (uint64_t i = 0; i < q.n; ++i)
+      q.row_bits_out[i] = (uint8_t)(((w[0][i / 32] ^ w[1][i / 32] ^ w[2][i / 32]) >> (i % 32)) & 1u);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, q.ev[0], q.ev[4]);
+  q.stats.wall_ms = ms;
+  cudaEventElapsedTime(&ms, q.ev[0], q.ev[1]);
+  q.stats.prep_ms = ms;
+  double gemm_ms = 0;
+  for (uint64_t i = 0; i < q.nchunks; ++i) {
+    cudaEventElapsedTime(&ms, q.gev[2 * i], q.gev[2 * i + 1]);
+    gemm_ms += ms;
+  }
+  q.stats.gemm_ms = gemm_ms;
+  cudaEventElapsedTime(&ms, q.ev[2], q.ev[3]);
+  q.stats.threshold_ms = ms;  // stream-2 span: threshold of all chunks (overlaps the GEMMs)
+  cudaEventElapsedTime(&ms, q.ev[3], q.ev[4]);
+  q.stats.or_ms = ms;
+  return 0;
+}
+
+// every in-flight batch query of the context (before anything that reuses its buffers)
+int drain(irismpc_gpu_ctx* c) {
+  for (auto& q : c->qs)
+    if (q.inflight) {
+      const int rc = finish_slot(c, q);
+      if (rc) return rc;
+    }
   return 0;
 }
 
@@ -1198,6 +1267,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
 int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const size_t hd_len[3],
                 const uint8_t* const ml[3], const size_t ml_len[3], uint64_t n, int with_or, uint8_t* opened_out,
                 uint8_t* lane_bits_out, irismpc_gpu_stats* stats) {
+  if (int rc = drain(c)) return rc;
   const int V = c->variant;
   const VariantWidths vw = c->vw;
   const bool or_only = mode == 1;
@@ -1532,8 +1602,7 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* e = std::getenv("IRISMPC_PRIO_SWAP"); e && e[0] == '1') std::swap(prio_lo, prio_hi);
   if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return IRISMPC_GPU_ERR_DEVICE;
   }
@@ -1549,26 +1618,35 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
   cudaStreamSynchronize(c->st);
+  drain(c);
+  for (auto& q : c->qs) {
+    Buf* qb[] = {&q.segs, &q.slot_begin, &q.match[0], &q.match[1], &q.match[2], &q.pair_dots, &q.open_out};
+    for (Buf* b : qb) b->release();
+    if (q.h_segs) cudaFreeHost(q.h_segs);
+    if (q.h_match) cudaFreeHost(q.h_match);
+    for (auto& e : q.ev)
+      if (e) cudaEventDestroy(e);
+    if (q.done) cudaEventDestroy(q.done);
+    for (auto& e : q.gev) cudaEventDestroy(e);
+  }
+  for (auto& e : c->half_free)
+    if (e) cudaEventDestroy(e);
   c->shard.reset();
   c->shard_part.release();
   c->shard_all.release();
   Buf* bufs[] = {&c->q_pay[0], &c->q_pay[1], &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial,
                  &c->slot_begin, &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
-                 &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->gate2, &c->bits2};
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
   for (Buf* b : bufs) b->release();
   for (auto& f : c->fld) f.release();
   for (auto& t : c->tap_buf) t.release();
   c->tap_rows_dev.release();
   if (c->h_segs_pinned) cudaFreeHost(c->h_segs_pinned);
   for (auto& e : c->ev) cudaEventDestroy(e);
-  for (auto& e : c->gev) cudaEventDestroy(e);
   for (auto& e : c->evg) cudaEventDestroy(e);
   for (auto& e : c->evt) cudaEventDestroy(e);
-  for (auto& e : c->evt3) cudaEventDestroy(e);
   cudaStreamSynchronize(c->st2);
-  cudaStreamSynchronize(c->st3);
   cudaStreamDestroy(c->st2);
-  cudaStreamDestroy(c->st3);
   cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1723,6 +1801,30 @@ int irismpc_gpu_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const 
   cudaSetDevice(c->cfg.device);
   const uint8_t* none[3] = {nullptr, nullptr, nullptr};
   return run_query(c, none, qlen, 1, 1, 0, match_out, row_bits_out, nullptr, stats, true, q);
+}
+
+int irismpc_gpu_batch_query_submit(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
+                                   uint32_t persons, uint8_t* person_match_out, uint64_t* ticket) {
+  if (!c || !ticket) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  if (c->taps || c->tap_k || c->cfg.debug_rows)
+    return fail(c, IRISMPC_GPU_ERR_CONFIG, "streaming queries run without taps / debug_rows");
+  return run_query(c, dq, qlen, persons, 0, 0, person_match_out, nullptr, nullptr, nullptr, false, nullptr, ticket);
+}
+
+int irismpc_gpu_batch_query_wait(irismpc_gpu_ctx* c, uint64_t ticket, irismpc_gpu_stats* stats) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  cudaSetDevice(c->cfg.device);
+  for (auto& q : c->qs) {
+    if (q.ticket != ticket) continue;
+    if (q.inflight) {
+      const int rc = finish_slot(c, q);
+      if (rc) return rc;
+    }
+    if (stats) *stats = q.stats;
+    return 0;
+  }
+  return fail(c, IRISMPC_GPU_ERR_CONFIG, "unknown or expired ticket (wait for a ticket before submitting two more)");
 }
 
 int irismpc_gpu_batch_query_partial(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
@@ -1952,6 +2054,7 @@ int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint
 int irismpc_gpu_profile(irismpc_gpu_ctx* c, int on) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
   cudaSetDevice(c->cfg.device);
+  if (int rc = drain(c)) return rc;
   c->serial = on != 0;
   prof_enable(on != 0);
   return 0;
@@ -1986,6 +2089,7 @@ int irismpc_gpu_enable_taps(irismpc_gpu_ctx* c, int enable) {
 }
 
 int irismpc_gpu_read_tap(irismpc_gpu_ctx* c, int tap, void* host_out, size_t bytes) {
+  if (c && drain(c)) return IRISMPC_GPU_ERR_DEVICE;
   if (!c || tap < 1 || tap > 7) return IRISMPC_GPU_ERR_CONFIG;
   if (!c->tap_buf[tap - 1].p) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap not captured");
   const size_t have = c->tap_bytes[tap - 1];

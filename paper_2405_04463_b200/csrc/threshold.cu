@@ -863,12 +863,18 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
   // reshare / inject: one CTA per kTile-lane tile (at most 1024 / kTile per 1024-lane task)
   const dim3 tile_blocks(a.task_seg_max * (1024 / kTile), 1, a.nsegs);
+  // A/B hook: extra dynamic shared memory per reshare / inject CTA (keeps them off
+  // the SMs the persistent GEMM occupies when large)
+  static const int pad = [] {
+    const char* e = std::getenv("IRISMPC_THR_SMEM_PAD");
+    return e ? std::atoi(e) : 0;
+  }();
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
   switch (a.variant) {
-    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
-    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
-    case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
-    default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+    case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+    default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
   }
   prof_end(h, "k_reshare", st);
   debug_check("k_reshare", st);
@@ -878,7 +884,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    k_inject<<<tile_blocks, kTileThreads, 0, st>>>(a);
+    k_inject<<<tile_blocks, kTileThreads, pad, st>>>(a);
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }

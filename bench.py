@@ -584,6 +584,14 @@ def main_gpu(args):
             line["cpu_baseline"] = {k: c0[k] for k in ("value", "unit", "cores", "kind", "sample")}
             line["cpu_baseline"]["other_backend"] = {k: cpu[1 - backend][k] for k in ("value", "sample")}
         print(json.dumps(line), flush=True)
+    # tensors that were used on the library's stream (and pinned buffers copied on it)
+    # go before the library destroys that stream
+    torch.cuda.synchronize()
+    qdev2.clear()
+    qpay.clear()
+    host_q.clear()
+    torch.cuda.empty_cache()
+    sess.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

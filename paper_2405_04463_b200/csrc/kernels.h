@@ -205,6 +205,9 @@ struct ThrArgs {
 // words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
+// round-1 lane-major reshare / inject (threshold_lm.cu), A/B hook IRISMPC_THR_LM=1
+void launch_reshare_lm(const ThrArgs& a, cudaStream_t st);
+void launch_inject_lm(const ThrArgs& a, cudaStream_t st);
 // comparison phase alone (party_comparison_only / party_or_tree_only, engine.cpp:448-532)
 void launch_parse_lane_shares(const uint8_t* const p[3], uint64_t lanes, int width, void* out, int* bad,
                               cudaStream_t st);

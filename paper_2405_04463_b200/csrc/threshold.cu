@@ -870,7 +870,12 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : 0;
   }();
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
-  switch (a.variant) {
+  static const bool lm = [] {
+    const char* e = std::getenv("IRISMPC_THR_LM");
+    return e && e[0] == '1';
+  }();
+  if (lm) launch_reshare_lm(a, st);
+  else switch (a.variant) {
     case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
     case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
     case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
@@ -884,7 +889,10 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    k_inject<<<tile_blocks, kTileThreads, pad, st>>>(a);
+    if (lm)
+      launch_inject_lm(a, st);
+    else
+      k_inject<<<tile_blocks, kTileThreads, pad, st>>>(a);
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }

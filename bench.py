@@ -400,6 +400,7 @@ def main_gpu(args):
     # every step still copies its inputs (e2e: from pinned host memory) and reads
     # its person bits back.  Double-buffered device payloads for the e2e leg.
     qdev2 = [[torch.empty_like(x) for x in qpay] for _ in range(2)]
+    upload = torch.cuda.Stream()  # torch-owned: pinned-host copies never touch the library's stream
 
     def run_steps(k: int, from_host: bool, acc=None):
         res = None
@@ -422,9 +423,10 @@ def main_gpu(args):
             src = qpay
             if from_host:
                 src = qdev2[i % 2]
-                with torch.cuda.stream(ext):  # H2D ordered before the query's parse on the same stream
+                with torch.cuda.stream(upload):
                     for d, h in zip(src, host_q):
                         d.copy_(h, non_blocking=True)
+                upload.synchronize()  # the payload is on the device before the library's parse
             tickets.append(sess.batch_query_submit(src, persons))
             if i >= 1:
                 res = sess.batch_query_wait(tickets[i - 1])
@@ -584,14 +586,7 @@ def main_gpu(args):
             line["cpu_baseline"] = {k: c0[k] for k in ("value", "unit", "cores", "kind", "sample")}
             line["cpu_baseline"]["other_backend"] = {k: cpu[1 - backend][k] for k in ("value", "sample")}
         print(json.dumps(line), flush=True)
-    # tensors that were used on the library's stream (and pinned buffers copied on it)
-    # go before the library destroys that stream
     torch.cuda.synchronize()
-    qdev2.clear()
-    qpay.clear()
-    host_q.clear()
-    torch.cuda.empty_cache()
-    sess.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

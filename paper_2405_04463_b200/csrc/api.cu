@@ -1343,6 +1343,7 @@ int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const 
   ta.n = n;
   ta.W = W;
   ta.no_reshare = 1;
+  ta.tile_kernels = 1;  // no GEMM beside it: the faster standalone kernels
   for (int k = 0; k < 3; ++k) {
     ta.pos[k] = c->pos[k];
     ta.key[k] = c->keys[k];

@@ -181,6 +181,7 @@ struct ThrArgs {
   uint64_t lift_base[3], msb_base[3];
   uint64_t inj_base[3];  // bit_inject<15> draws of seeds 1 / 3 (mpc-lift): lift_base + 64 W
   int no_reshare;        // comparison-only (party_comparison_only): inputs are already replicated shares
+  int tile_kernels;      // reshare / inject as 512-lane tiles (threshold.cu) instead of lane-major (threshold_lm.cu)
   // chunk work buffers
   uint64_t* gate;        // gate randomness, per segment [3*ngates][nwords]
   uint16_t* ml_rs;       // [3][cstride] reshared ml
@@ -205,7 +206,7 @@ struct ThrArgs {
 // words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
-// round-1 lane-major reshare / inject (threshold_lm.cu), A/B hook IRISMPC_THR_LM=1
+// lane-major reshare / inject (threshold_lm.cu): the batch query's default (see launch_threshold)
 void launch_reshare_lm(const ThrArgs& a, cudaStream_t st);
 void launch_inject_lm(const ThrArgs& a, cudaStream_t st);
 // comparison phase alone (party_comparison_only / party_or_tree_only, engine.cpp:448-532)

@@ -34,6 +34,7 @@
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
 //                     match-bit shares, fused first MPC-OR level per warp
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -870,10 +871,17 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : 0;
   }();
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
-  static const bool lm = [] {
-    const char* e = std::getenv("IRISMPC_THR_LM");
-    return e && e[0] == '1';
+  // Which reshare / inject kernels: the 512-lane tile kernels run 1.5x (reshare)
+  // faster standalone (comparison-only path, serial profile), but beside the
+  // persistent GEMM of a batch query the lane-major kernels keep the threshold
+  // stream shorter (configs[2]: 432-437 vs 483 ms per query, same box, A/B in
+  // profiles/r2_threshold_ab.md), so the batch query uses those.
+  // IRISMPC_THR_KERNELS=tile|lm overrides (A/B hook).
+  static const int force = [] {
+    const char* e = std::getenv("IRISMPC_THR_KERNELS");
+    return !e ? -1 : (std::string(e) == "tile" ? 1 : 0);
   }();
+  const bool lm = force >= 0 ? force == 0 : !a.tile_kernels;
   if (lm) launch_reshare_lm(a, st);
   else switch (a.variant) {
     case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;

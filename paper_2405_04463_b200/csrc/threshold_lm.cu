@@ -1,6 +1,6 @@
 // Lane-major reshare / bit-inject (the round-1 kernels: thread = 8 lanes,
 // warp-cooperative ChaCha windows), kept as an A/B alternative to the
-// 512-lane tile kernels of threshold.cu (IRISMPC_THR_LM=1).  Same semantics
+// 512-lane tile kernels of threshold.cu (IRISMPC_THR_KERNELS=tile|lm).  Same semantics
 // (reshare_pair, engine.cpp:80-106; bit_inject, convert.hpp:84-155).
 #include <type_traits>
 

@@ -153,8 +153,8 @@ __device__ __forceinline__ void load4(const T* src, uint64_t kstride, const Seg&
 //   no-lift    : diff = a ml32 - b hd32
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
 //
-// One CTA per kTile-lane tile of a segment (globally kTile-aligned, clipped to
-// the segment).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to
+// One CTA per kTile-lane tile of a segment (tiles start at the segment's first
+// lane).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to
 // kTile/8 + 1 ChaCha12 blocks covering its kTile stream elements -- one block
 // per thread per step at full occupancy (the k_gate_keystream pattern), the
 // ring-width low bits of each element into shared memory.  Phase 2: thread = 4
@@ -164,8 +164,11 @@ __device__ __forceinline__ void load4(const T* src, uint64_t kstride, const Seg&
 // The tile is kept small (6 KB of shared memory for 16-bit rings) so the CTAs
 // fit beside the persistent GEMM's ~193 KB on the same SM: the threshold runs
 // in the SMs' leftover resources while the GEMM streams.
-constexpr int kTile = 512;
-constexpr int kTileThreads = kTile / 4;
+// 504 lanes: any 504 consecutive stream elements lie in at most 64 ChaCha
+// blocks, so phase 1 is 6 x 64 = 384 jobs = exactly 3 rounds of 128 threads
+// (a 512-lane tile needs 65 blocks per window and a mostly idle 4th round)
+constexpr int kTile = 504;
+constexpr int kTileThreads = 128;
 
 template <int V>
 __global__ void __launch_bounds__(kTileThreads) k_reshare(const __grid_constant__ ThrArgs A) {
@@ -174,13 +177,13 @@ __global__ void __launch_bounds__(kTileThreads) k_reshare(const __grid_constant_
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr uint32_t MM = (V == kConstLift || V == kNoLift) ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr int NDOT = V == kPlainMask ? 1 : 2;  // dot 0 = hd (offset 0), dot 1 = ml (offset n)
-  constexpr int NB = kTile / 8 + 1;                // blocks per (dot, seed) window
+  constexpr int NB = (kTile + 6) / 8 + 1;          // blocks per (dot, seed) window
   using FH = HT;                                   // stored F words: the ring's width
   using FM = MT;
   __shared__ FH Fh[3][kTile];
   __shared__ FM Fm[NDOT - 1 ? 3 : 1][NDOT - 1 ? kTile : 1];
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = (sg.lane_begin / kTile + blockIdx.x) * kTile;
+  const uint64_t T0 = sg.lane_begin + (uint64_t)blockIdx.x * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
   const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
@@ -494,13 +497,13 @@ __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ T
 __global__ void __launch_bounds__(kTileThreads) k_inject(const __grid_constant__ ThrArgs A) {
   __shared__ uint16_t C[2][2][kTile];  // [inject 15 / 16][c1 / c3][lane]
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = (sg.lane_begin / kTile + blockIdx.x) * kTile;
+  const uint64_t T0 = sg.lane_begin + (uint64_t)blockIdx.x * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
   const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
   const int lo = (int)(lb - T0), hi = (int)(le - T0);
   const uint64_t n = A.n;
-  constexpr int J1 = kTile / 8 + 1, J3 = 3 * kTile / 8 + 1, JW = J1 + J3;
+  constexpr int J1 = (kTile + 6) / 8 + 1, J3 = (3 * kTile + 6) / 8 + 1, JW = J1 + J3;
   for (int j = threadIdx.x; j < 2 * JW; j += blockDim.x) {
     const int which = j / JW, q = j % JW;
     const bool s3 = q >= J1;
@@ -862,8 +865,8 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
-  // reshare / inject: one CTA per kTile-lane tile (at most 1024 / kTile per 1024-lane task)
-  const dim3 tile_blocks(a.task_seg_max * (1024 / kTile), 1, a.nsegs);
+  // reshare / inject: one CTA per kTile-lane tile of a segment
+  const dim3 tile_blocks((unsigned)((a.task_seg_max * 1024ull + kTile - 1) / kTile), 1, a.nsegs);
   // A/B hook: extra dynamic shared memory per reshare / inject CTA (keeps them off
   // the SMs the persistent GEMM occupies when large)
   static const int pad = [] {

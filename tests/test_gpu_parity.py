@@ -499,3 +499,27 @@ def test_streaming_queries_multi_chunk():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("kernels", ["tile", "lm"])
+def test_threshold_kernel_variants_share_exact(kernels):
+    """Both reshare / inject implementations (the lane-major kernels a batch query
+    uses beside the GEMM, the 504-lane tile kernels of the comparison-only path)
+    forced on batch queries: every share through the MSB equals the oracle's, for
+    all four variants and both backends (fresh process per variant: the selection
+    is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import test_gpu_parity as T;"
+        "T.test_shares_through_msb_match_oracle(1, 12800, 1031, 1, 31, 23);"
+        "T.test_shares_through_msb_match_oracle(0, 256, 2500, 2, 5, 24);"
+        "[T.test_variant_shares_through_msb_match_oracle(v, 1, 256, 1031, 2, 5, 43) for v in (0, 2, 3)];"
+        "[T.test_variant_shares_through_msb_match_oracle(v, 0, 128, 1, 4, 31, 44) for v in (0, 2, 3)];"
+        "print('ok')")
+    env = dict(os.environ, IRISMPC_THR_KERNELS=kernels, IRISMPC_CHUNK_LANES="30000")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

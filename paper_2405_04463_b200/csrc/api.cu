@@ -851,7 +851,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         sg.slot = (int64_t)col_fill[col];
         col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
-      const uint64_t per_job = std::max<uint64_t>(1, kThrLanes / nr);
+      // threshold jobs of at most kThrLanes lanes (plus 1/8 slack: a chunk rounded up to its row
+      // granule stays one job), the columns split evenly (no small remainder job)
+      const uint64_t njobs_c = ceil_div(ncols * nr, kThrLanes + kThrLanes / 8);
+      const uint64_t per_job = std::max<uint64_t>(1, ceil_div(ncols, std::max<uint64_t>(1, njobs_c)));
       for (uint64_t a = 0; a < ncols; a += per_job)
         add_job(i * ncols + a, std::min<uint64_t>(per_job, ncols - a), false, i);
       cstride = std::max<uint64_t>(cstride, ncols * nr);

@@ -602,7 +602,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   bool use_rp[2] = {false, false};
   for (int fi = 0; fi < 2; ++fi) {
     FieldPlanes& f = c->fld[fi];
-    use_rp[fi] = !membership && r >= 3 && (f.rpg || f.rpc) && s_loc > 0;
+    // the rotation-pair GEMMs run 3 products of K = l/2 over ncols_rp columns instead of one
+    // of K = l over ncols: worth it only when the padded column tiles say so (batch 8:
+    // 128 pair columns fill half of one 256-column tile, 1.5x the plain GEMM's tile work)
+    const uint64_t bn = f.bn();
+    const char* force = std::getenv("IRISMPC_RP_FORCE");  // test hook, read per query
+    const bool rp_pays = 3 * ceil_div(ncols_rp, bn) < 2 * ceil_div(ncols, bn) || (force && force[0] == '1');
+    use_rp[fi] = !membership && r >= 3 && (f.rpg || f.rpc) && s_loc > 0 && rp_pays;
     if (!use_rp[fi]) continue;
     const uint64_t rows = 9ull * f.nseg * f.fmt.limbs * ncols_rp_pad;  // 3 kinds x 3 parties
     const size_t bytes = rows * (c->l / 2);

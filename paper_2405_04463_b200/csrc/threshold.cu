@@ -154,7 +154,7 @@ __device__ __forceinline__ void load4(const T* src, uint64_t kstride, const Seg&
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
 //
 // One CTA per kTile-lane tile of a segment (tiles start at the segment's first
-// lane).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to
+// lane rounded down to a multiple of 4).  Phase 1: the tile's reshare draws -- per (dot, seed) the up to
 // kTile/8 + 1 ChaCha12 blocks covering its kTile stream elements -- one block
 // per thread per step at full occupancy (the k_gate_keystream pattern), the
 // ring-width low bits of each element into shared memory.  Phase 2: thread = 4
@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(kTileThreads) k_reshare(const __grid_constant_
   __shared__ FH Fh[3][kTile];
   __shared__ FM Fm[NDOT - 1 ? 3 : 1][NDOT - 1 ? kTile : 1];
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = sg.lane_begin + (uint64_t)blockIdx.x * kTile;
+  // tiles start at the segment's first lane rounded down to 4: a thread's 4 lanes never
+  // straddle a 32-lane bit word (k_inject) nor a vector boundary
+  const uint64_t T0 = (sg.lane_begin & ~3ull) + (uint64_t)blockIdx.x * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
   const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
@@ -497,7 +499,9 @@ __global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ T
 __global__ void __launch_bounds__(kTileThreads) k_inject(const __grid_constant__ ThrArgs A) {
   __shared__ uint16_t C[2][2][kTile];  // [inject 15 / 16][c1 / c3][lane]
   const Seg& sg = A.segs[blockIdx.z];
-  const uint64_t T0 = sg.lane_begin + (uint64_t)blockIdx.x * kTile;
+  // tiles start at the segment's first lane rounded down to 4: a thread's 4 lanes never
+  // straddle a 32-lane bit word (k_inject) nor a vector boundary
+  const uint64_t T0 = (sg.lane_begin & ~3ull) + (uint64_t)blockIdx.x * kTile;
   if (T0 >= sg.lane_end) return;  // CTA-uniform
   const uint64_t lb = sg.lane_begin > T0 ? sg.lane_begin : T0;
   const uint64_t le = sg.lane_end < T0 + kTile ? sg.lane_end : T0 + kTile;
@@ -866,7 +870,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   h = prof_begin(st);
   // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
   // reshare / inject: one CTA per kTile-lane tile of a segment
-  const dim3 tile_blocks((unsigned)((a.task_seg_max * 1024ull + kTile - 1) / kTile), 1, a.nsegs);
+  const dim3 tile_blocks((unsigned)((a.task_seg_max * 1024ull + 3 + kTile - 1) / kTile), 1, a.nsegs);
   // A/B hook: extra dynamic shared memory per reshare / inject CTA (keeps them off
   // the SMs the persistent GEMM occupies when large)
   static const int pad = [] {

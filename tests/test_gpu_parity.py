@@ -425,7 +425,7 @@ def test_rotation_pair_gemm_modes(mode, be, var, l):
         print("ok", m, rp)
     """)
     import os
-    env = dict(os.environ, IRISMPC_RP=mode)
+    env = dict(os.environ, IRISMPC_RP=mode, IRISMPC_RP_FORCE="1")
     if mode == "chunked":  # S planes built per row chunk (large-DB path), three row chunks
         env.update(IRISMPC_RP="1", IRISMPC_RP_CHUNKED="force", IRISMPC_CHUNK_LANES="8000")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
@@ -435,10 +435,12 @@ def test_rotation_pair_gemm_modes(mode, be, var, l):
 
 @pytest.mark.parametrize("be,l,r,persons,s", [(O.SHAMIR, 1024, 3, 1, 300), (O.REPLICATED, 512, 5, 3, 257),
                                               (O.SHAMIR, 2048, 31, 1, 1)])
-def test_rotation_pair_gemm_shapes(be, l, r, persons, s):
+def test_rotation_pair_gemm_shapes(be, l, r, persons, s, monkeypatch):
     """Rotation-pair GEMMs at other rotation counts (an odd number of pairs' last
     rotation dropped), one person, a one-row DB: shares through the MSB and the
-    opened bits identical to the oracle."""
+    opened bits identical to the oracle.  (These batches are too narrow for the
+    rotation-pair GEMMs to pay, so IRISMPC_RP_FORCE selects them.)"""
+    monkeypatch.setenv("IRISMPC_RP_FORCE", "1")
     dc, dm, qc, qm = _inputs(l, s, persons, 77, False, True, 0.9)
     m, sess, taps, n = _gpu(be, l, 0.375, r, 77, dc, dm, qc, qm, persons, False)
     ref = O.run_local(O.make_config(be, l, 0.375, r, debug_rows=True), 77, dc, dm, qc, qm, persons, want_all=True)
@@ -523,3 +525,17 @@ def test_threshold_kernel_variants_share_exact(kernels):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("persons,rp", [(4, 0), (8, 1), (16, 1)])
+def test_rotation_pair_gemm_chosen_by_tile_cost(persons, rp):
+    """The rotation-pair GEMMs run when their padded column tiles cost less than
+    the plain GEMM's (3 ceil(16 codes'/256) < 2 ceil(31 codes/256)): not for a
+    batch of 8 codes (128 pair columns half-fill a tile), yes from 16 codes."""
+    l, s, r, seed = 1024, 300, 31, 5
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    m, sess, taps, n = _gpu(O.SHAMIR, l, 0.375, r, seed, dc, dm, qc, qm, persons, False)
+    assert sess.last_stats.rotation_pair_gemm == rp
+    ref = O.run_local(O.make_config(O.SHAMIR, l, 0.375, r, debug_rows=True), seed, dc, dm, qc, qm, persons)
+    np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)

@@ -154,15 +154,18 @@ def chacha_peak():
     return None
 
 
-def ncu_traffic(rp: bool = False):
-    """dram bytes per GEMM launch from the committed ncu --set full capture (or None);
-    rp: the rotation-pair GEMM launches"""
+def ncu_traffic(rp: bool = False, rows: int = 0):
+    """dram bytes per GEMM launch (and tensor-pipe %) from the committed ncu capture of the
+    same GEMM (profiles/ncu_traffic.json): rotation-pair launches (configs[1]), the plain
+    GEMM of a configs[2] row chunk, or the plain GEMM of a configs[1] chunk; None if absent"""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
             d = json.load(open(p))
             if rp and "rotation_pair" in d:
                 d = d["rotation_pair"]
+            elif rows >= 1_000_000 and "plain_configs2" in d:
+                d = d["plain_configs2"]
             return d.get("gemm_dram_bytes_per_launch"), d.get("tensor_pipe_active_pct")
         except Exception:
             return None, None
@@ -549,8 +552,8 @@ def main_gpu(args):
                     "note": e2e_note},
             "roofline": {"bound": "tensor", "kernel": "k_limb_gemm_pair (tcgen05.mma.cta_group::2.kind::i8)",
                          "achieved": exec_tops, "peak": peak, "unit": "TFLOP/s", "frac": exec_tops / peak,
-                         "traffic": ncu_traffic(bool(stats_acc["rp"]))[0],
-                         "ncu_tensor_pipe_active_pct": ncu_traffic(bool(stats_acc["rp"]))[1],
+                         "traffic": ncu_traffic(bool(stats_acc["rp"]), rows)[0],
+                         "ncu_tensor_pipe_active_pct": ncu_traffic(bool(stats_acc["rp"]), rows)[1],
                          "int8_ops_per_launch_executed": exec_ops_launch,
                          "gemm_ms_per_launch": gemm_ms, "gemm_launches_per_step": launches_per_step,
                          "rotation_pair_gemm": bool(stats_acc["rp"]),

@@ -31,7 +31,9 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -139,7 +141,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t nkb = g.nkb_seg * g.nseg;
 
   if (warp == 0) {
-    // TMA producer: warp-uniform loop, one elected lane issues
+    // TMA producer: warp-uniform loop, one elected lane issues.
+    // Group lockstep: the n_tiles clusters of a group read the same A k-blocks; left
+    // alone they drift apart by more than the L2 holds and each re-reads A from DRAM
+    // (3.3x the DB planes at configs[2]).  The leader CTA of each cluster publishes
+    // the k-block iteration it has issued and does not run more than kLag
+    // iterations ahead of the slowest cluster of its group (a bounded wait: the
+    // progress words are only a scheduling hint, never a correctness condition).
+    constexpr uint32_t kLag = 16;
+    bool lock = !flat && n_tiles > 1 && n_tiles <= 32 && g.prog != nullptr && leader;
+    const uint32_t grp_base = (cl / tiles_per_unit) * tiles_per_unit;
+    uint32_t seen = 0;
     uint32_t it = 0;
     for (uint32_t u = g0; u < nunits; u += groups) {
       const uint32_t n_tile = flat ? u % n_tiles : my_n;
@@ -155,6 +167,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
+        if (lock && it >= kLag + seen) {
+          uint64_t t0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          for (;;) {
+            uint32_t v = 0xFFFFFFFFu;
+            if ((uint32_t)lane < n_tiles) {
+              unsigned long long w;
+              asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(g.prog + grp_base + lane));
+              v = (uint32_t)(w >> 32) == g.epoch ? (uint32_t)w : 0u;
+            }
+            v = __reduce_min_sync(0xFFFFFFFFu, v);
+            seen = v;
+            if (it < kLag + v) break;
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 50000) {  // a group member is not running (not yet resident): stop pacing
+              lock = false;
+              break;
+            }
+            __nanosleep(128);
+          }
+        }
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t seg = kb / g.nkb_seg;
         const uint32_t kk = kb % g.nkb_seg;
@@ -172,6 +206,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                            n_tile * BN + rank * (BN / 2));
             tma_load_2d_pair(st + limb * T::A_T, ta, fb, (int32_t)((akb + kk) * BK), arow);
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
+          }
+          if (lock) {
+            const unsigned long long w = ((unsigned long long)g.epoch << 32) | (it + 1);
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(g.prog + cl), "l"(w) : "memory");
           }
         }
         __syncwarp();
@@ -308,6 +346,11 @@ struct DevState {
   std::once_flag attr[3];  // dynamic-smem opt-in of k_limb_gemm_pair<1 / 2 / 4>
   std::once_flag sms;
   int nsm = 0;
+  // group-lockstep progress words (one per cluster), one buffer per stream: GEMMs of
+  // different streams (contexts) may run concurrently
+  std::mutex prog_mu;
+  std::vector<std::pair<cudaStream_t, unsigned long long*>> prog;
+  std::atomic<uint32_t> epoch{0};
 };
 DevState g_dev[kMaxDev];
 
@@ -347,7 +390,29 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
   const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
   const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
-  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, g, n_tiles, m_pairs, grouped ? 1u : 0u);
+  GemmArgs ga = g;
+  static const bool no_lock = std::getenv("IRISMPC_GEMM_NO_LOCKSTEP") != nullptr;  // A/B hook
+  if (grouped && n_tiles > 1 && !no_lock) {
+    DevState& ds = g_dev[dev];
+    unsigned long long* pg = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(ds.prog_mu);
+      for (auto& e : ds.prog)
+        if (e.first == st) pg = e.second;
+      if (!pg && cudaMalloc(&pg, 1024 * sizeof(unsigned long long)) == cudaSuccess) {
+        cudaMemset(pg, 0, 1024 * sizeof(unsigned long long));
+        ds.prog.emplace_back(st, pg);
+      } else if (!pg) {
+        cudaGetLastError();
+      }
+    }
+    if (pg && ncl <= 1024) {
+      ga.prog = pg;
+      ga.epoch = ++ds.epoch;  // launches on one device are ordered per stream; epochs tell them apart
+      if (ga.epoch == 0) ga.epoch = ++ds.epoch;
+    }
+  }
+  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, ga, n_tiles, m_pairs, grouped ? 1u : 0u);
 }
 
 uint32_t gemm_groups(uint32_t n_tiles) {

@@ -123,6 +123,9 @@ struct GemmArgs {
   // (0 = the DB planes' s_pad / row0, resident S planes)
   uint32_t s_pad2 = 0;
   uint32_t row0_2 = 0;
+  // group lockstep (set by launch_gemm): per-cluster progress words, this launch's epoch
+  unsigned long long* prog = nullptr;
+  uint32_t epoch = 0;
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }

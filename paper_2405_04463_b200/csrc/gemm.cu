@@ -148,7 +148,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // the k-block iteration it has issued and does not run more than kLag
     // iterations ahead of the slowest cluster of its group (a bounded wait: the
     // progress words are only a scheduling hint, never a correctness condition).
-    constexpr uint32_t kLag = 16;
+    const uint32_t kLag = g.lag;
     bool lock = !flat && n_tiles > 1 && n_tiles <= 32 && g.prog != nullptr && leader;
     const uint32_t grp_base = (cl / tiles_per_unit) * tiles_per_unit;
     uint32_t seen = 0;
@@ -408,6 +408,11 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
     }
     if (pg && ncl <= 1024) {
       ga.prog = pg;
+      static const uint32_t lag = [] {
+        const char* e = std::getenv("IRISMPC_GEMM_LAG");  // A/B hook
+        return e ? (uint32_t)std::max(1, std::atoi(e)) : 16u;
+      }();
+      ga.lag = lag;
       ga.epoch = ++ds.epoch;  // launches on one device are ordered per stream; epochs tell them apart
       if (ga.epoch == 0) ga.epoch = ++ds.epoch;
     }

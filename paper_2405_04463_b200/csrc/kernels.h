@@ -126,6 +126,7 @@ struct GemmArgs {
   // group lockstep (set by launch_gemm): per-cluster progress words, this launch's epoch
   unsigned long long* prog = nullptr;
   uint32_t epoch = 0;
+  uint32_t lag = 16;  // k-block iterations a cluster may run ahead of its group's slowest
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }

@@ -237,6 +237,7 @@ struct FieldPlanes {
   CUtensorMap tS, tRP;
   bool rpg = false;  // S planes resident: rotated queries run the RP GEMMs
   bool rpc = false;  // S planes built per row chunk into sch (DB too large for resident S)
+  bool rpconv = false;  // ... or formed in the GEMM's shared memory from E and O (GemmArgs::s_conv)
   Buf sch;
   CUtensorMap tSc;
   uint64_t sch_spad = 0;
@@ -252,6 +253,7 @@ struct FieldPlanes {
     sch.release();
     rpg = false;
     rpc = false;
+    rpconv = false;
     sch_spad = 0;
     rp_ncols_cur = 0;
     ncols_pad_cur = 0;
@@ -447,17 +449,22 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     const char* e = std::getenv("IRISMPC_RP");
     return e && std::string(e) == "layout";
   }();
-  // opt-in: per-chunk S planes when resident ones do not fit ("force": always, tests)
+  // opt-in: per-chunk S planes when resident ones do not fit ("force": always, tests);
+  // "conv" / "conv_force": S = E + O formed inside the GEMM instead (no S planes at all)
   static const int rp_chunked = [] {
     const char* e = std::getenv("IRISMPC_RP_CHUNKED");
-    return !e || std::string(e) == "0" ? 0 : std::string(e) == "force" ? 2 : 1;
+    if (!e || std::string(e) == "0") return 0;
+    const std::string v(e);
+    return v == "force" ? 2 : v == "conv" ? 3 : v == "conv_force" ? 4 : 1;
   }();
   for (auto& f : c->fld) {
     f.rpg = false;
     f.rpc = false;
+    f.rpconv = false;
     if (!f.fmt.rp || rp_layout_only) continue;
     f.rpc = rp_chunked != 0;
-    if (rp_chunked == 2) continue;
+    f.rpconv = rp_chunked >= 3;
+    if (rp_chunked == 2 || rp_chunked == 4) continue;
     const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
     // keep 16 GB free for the query's work buffers (dots, gate keystream, planes)
     size_t free_b = 0, total_b = 0;
@@ -472,6 +479,7 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the RP sum planes");
     f.rpg = true;
     f.rpc = false;
+    f.rpconv = false;
   }
   CK(c, cudaStreamSynchronize(c->st));
   c->db_loaded = true;
@@ -900,7 +908,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   // the GEMM stream (k_rp_sum of chunk i+1 is queued behind chunk i's GEMM)
   for (int fi = 0; fi < 2; ++fi) {
     FieldPlanes& f = c->fld[fi];
-    if (!use_rp[fi] || f.rpg) continue;
+    if (!use_rp[fi] || f.rpg || f.rpconv) continue;
     uint64_t spad = 0;
     for (uint64_t i = 0; i < nchunks; ++i) spad = std::max<uint64_t>(spad, round_up(chunk_rows(i), 2 * kGemmBM));
     if (spad > f.sch_spad) {
@@ -1035,7 +1043,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         g.out_pstride = ncols_rp * nr;
         g.out_kstride = 3 * ncols_rp * nr;
         g.out_cstride = (uint32_t)nr;
-        if (!f.rpg) {  // per-chunk S planes: E + O of this chunk's rows, then the GEMM (same stream)
+        if (!f.rpg && f.rpconv) {
+          g.s_conv = 1;  // S = E + O in the GEMM's shared memory
+        } else if (!f.rpg) {  // per-chunk S planes: E + O of this chunk's rows, then the GEMM (same stream)
           const uint64_t nrs = std::min<uint64_t>(round_up(nr, 2 * kGemmBM), c->s_pad - chunk_row0[i]);
           launch_rp_sum_rows(f.db.as<uint8_t>(), f.nparty, c->s_pad, chunk_row0[i], nrs, f.sch_spad, c->l,
                              c->l_pad, f.fmt.limbs, f.sch.as<uint8_t>(), st);
@@ -1043,7 +1053,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
           g.s_pad2 = (uint32_t)f.sch_spad;
           g.row0_2 = 0;
         }
-        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st, f.rpg ? &f.tS : &f.tSc);
+        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st,
+                    f.rpg ? &f.tS : (f.rpconv ? &f.tA : &f.tSc));
         ++gemm_launches;
         ++launches;
       } else {

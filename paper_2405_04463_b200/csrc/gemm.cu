@@ -81,7 +81,7 @@ struct Tile {
 
 }  // namespace
 
-template <int L>
+template <int L, bool CONV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_limb_gemm_pair(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const __grid_constant__ CUtensorMap tA2,
@@ -99,6 +99,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* accum = empty + STAGES;
   uint64_t* tmem_empty = accum + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  // s_conv: raw[s] = this CTA's E / O tile landed in slot s (local TMA), conv[s] (leader) =
+  // both CTAs' epilogue warps have written S into slot s
+  uint64_t* raw = reinterpret_cast<uint64_t*>(smem + STAGES * T::STAGE + 128);
+  uint64_t* conv = raw + STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -127,6 +131,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     mbar_init(accum, 1);
     mbar_init(tmem_empty, 2 * kEpiWarps);  // epilogue warps x 2 CTAs
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&raw[s], 1);
+      mbar_init(&conv[s], 2 * kEpiWarps);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -164,9 +172,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const bool s_scratch = kind == 1 && g.s_pad2 != 0;  // per-chunk S planes
       const uint32_t a_spad = s_scratch ? g.s_pad2 : g.s_pad, a_row0 = s_scratch ? g.row0_2 : g.row0;
       const uint32_t brow0 = g.b_row0 + kind * g.b_kind_rows;
+      const bool cv = CONV && kind == 1;
       for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
+        if constexpr (CONV) if (cv) {
+          // E tiles into slot s0's A part, O tiles into slot s1's A part (local TMA, this
+          // CTA's raw barriers), B into slot s0 (pair TMA, leader's full barrier); the
+          // epilogue warps add them into S in place (slot s0), the MMA reads slot s0
+          const uint32_t s1 = (it + 1) % STAGES, ph1 = ((it + 1) / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[s1], ph1 ^ 1);
+          const uint32_t seg = kb / g.nkb_seg, kk = kb % g.nkb_seg;
+          const uint32_t pa = (g.rep && seg == 1) ? (p + 2) % 3 : p;
+          uint8_t* st0 = smem + stage * T::STAGE;
+          uint8_t* st1 = smem + s1 * T::STAGE;
+          if (elect_one()) {
+            if (leader) {
+              mbar_arrive_expect_tx(&full[stage], 2 * L * T::B_T);
+              mbar_arrive_expect_tx(&full[s1], 0);
+            }
+            mbar_arrive_expect_tx(&raw[stage], L * T::A_T);
+            mbar_arrive_expect_tx(&raw[s1], L * T::A_T);
+            const uint32_t fb = mapa_shared(&full[stage], 0);
+#pragma unroll
+            for (int limb = 0; limb < L; ++limb) {
+              const int32_t arow = (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
+              const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
+                                             n_tile * BN + rank * (BN / 2));
+              tma_load_2d(st0 + limb * T::A_T, &tA, &raw[stage], (int32_t)((g.a_kb0 + kk) * BK), arow);
+              tma_load_2d(st1 + limb * T::A_T, &tA, &raw[s1], (int32_t)((g.a_kb0_k2 + kk) * BK), arow);
+              tma_load_2d_pair(st0 + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
+            }
+            if (lock) {
+              const unsigned long long w = ((unsigned long long)g.epoch << 32) | (it + 2);
+              asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(g.prog + cl), "l"(w) : "memory");
+            }
+          }
+          __syncwarp();
+          ++it;  // the second slot
+          continue;
+        }
         if (lock && it >= kLag + seen) {
           uint64_t t0;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -218,16 +264,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // MMA issuer (leader CTA): warp-uniform loop, one elected lane issues
     if (leader) {
-      uint32_t it = 0, ti = 0;
+      uint32_t it = 0, ti = 0, convph = 0;
       for (uint32_t u = g0; u < nunits; u += groups, ++ti) {
         if (ti > 0) {  // both CTAs' epilogues have drained the accumulators
           mbar_wait(tmem_empty, (ti - 1) & 1);
           tc_fence_after();
         }
+        const uint32_t uu = flat ? u / n_tiles : u;
+        const bool cv = CONV && (uu / m_pairs) / g.nprob == 1;
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&full[stage], phase);
+          uint32_t s1 = 0;
+          if (cv) {  // B landed (full) and both CTAs' S tiles written (conv); slot s1 is released with s0
+            s1 = (it + 1) % STAGES;
+            mbar_wait(&conv[stage], (convph >> stage) & 1);
+            convph ^= 1u << stage;
+          }
           tc_fence_after();
           const uint32_t st = smem_u32(smem + stage * T::STAGE);
           if (elect_one()) {
@@ -245,8 +299,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
             }
             umma_commit_pair(&empty[stage], 0x3);
+            if (cv) umma_commit_pair(&empty[s1], 0x3);
           }
           __syncwarp();
+          if (cv) ++it;
         }
         if (elect_one()) umma_commit_pair(accum, 0x3);
         __syncwarp();
@@ -259,13 +315,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int c0 = ((warp - 2) / 4) * kSlice;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t te = mapa_shared(tmem_empty, 0);
-    uint32_t ti = 0;
+    uint32_t ti = 0, cit = 0, rawph = 0;
+    const int et = threadIdx.x - 64;  // 0 .. 32 kEpiWarps - 1
     for (uint32_t u = g0; u < nunits; u += groups, ++ti) {
       const uint32_t n_tile = flat ? u % n_tiles : my_n;
       const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
       const uint32_t prob = uu / m_pairs;
       const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
+      if (CONV && kind == 1) {
+        // S = E + O (mod 2^(8L), limb-wise with carries) in place in slot s0's A tiles; both
+        // tiles carry the same 128B swizzle, so equal byte offsets hold the same (row, k)
+        for (uint32_t kb = 0; kb < nkb; ++kb, cit += 2) {
+          const uint32_t s0 = cit % STAGES, s1 = (cit + 1) % STAGES;
+          mbar_wait(&raw[s0], (rawph >> s0) & 1);
+          rawph ^= 1u << s0;
+          mbar_wait(&raw[s1], (rawph >> s1) & 1);
+          rawph ^= 1u << s1;
+          uint4* e = reinterpret_cast<uint4*>(smem + s0 * T::STAGE);
+          const uint4* o = reinterpret_cast<const uint4*>(smem + s1 * T::STAGE);
+          constexpr int kVec = T::A_T / 16;  // uint4 per limb tile
+#pragma unroll 2
+          for (int v = et; v < kVec; v += 32 * kEpiWarps) {
+            uint32_t c[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int limb = 0; limb < L; ++limb) {
+              const uint4 a = e[limb * kVec + v], b = o[limb * kVec + v];
+              const uint32_t x[4] = {a.x, a.y, a.z, a.w}, y[4] = {b.x, b.y, b.z, b.w};
+              uint32_t r[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t t = __vadd4(x[i], y[i]);
+                r[i] = __vadd4(t, c[i]);
+                if (limb + 1 < L) {
+                  const uint32_t c1 = ((x[i] & y[i]) | ((x[i] | y[i]) & ~t)) & 0x80808080u;
+                  const uint32_t c2 = t & ~r[i] & 0x80808080u;
+                  c[i] = (c1 | c2) >> 7;
+                }
+              }
+              e[limb * kVec + v] = make_uint4(r[0], r[1], r[2], r[3]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(&conv[s0], 0));
+        }
+      } else {
+        cit += nkb;
+      }
       mbar_wait(accum, ti & 1);
       tc_fence_after();
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
@@ -343,7 +440,7 @@ int make_plane_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 namespace {
 constexpr int kMaxDev = 64;
 struct DevState {
-  std::once_flag attr[3];  // dynamic-smem opt-in of k_limb_gemm_pair<1 / 2 / 4>
+  std::once_flag attr[6];  // dynamic-smem opt-in of k_limb_gemm_pair<1 / 2 / 4, CONV>
   std::once_flag sms;
   int nsm = 0;
   // group-lockstep progress words (one per cluster), one buffer per stream: GEMMs of
@@ -372,14 +469,14 @@ int device_sms(int d) {
 }
 }  // namespace
 
-template <int L>
+template <int L, bool CONV>
 static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const GemmArgs& g,
                                uint32_t m_tiles, uint32_t n_tiles, cudaStream_t st) {
   using T = Tile<L>;
   const int dev = cur_device();
-  constexpr int slot = L == 1 ? 0 : (L == 2 ? 1 : 2);
+  constexpr int slot = (L == 1 ? 0 : (L == 2 ? 1 : 2)) + (CONV ? 3 : 0);
   std::call_once(g_dev[dev].attr[slot], [] {
-    cudaFuncSetAttribute(k_limb_gemm_pair<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    cudaFuncSetAttribute(k_limb_gemm_pair<L, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   });
   // m_tiles counts 128-row tiles; pairs cover 256 rows (s_pad is a multiple of 256).
   // Persistent: one CTA pair per two SMs.
@@ -417,7 +514,8 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
       if (ga.epoch == 0) ga.epoch = ++ds.epoch;
     }
   }
-  k_limb_gemm_pair<L><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, ga, n_tiles, m_pairs, grouped ? 1u : 0u);
+  k_limb_gemm_pair<L, CONV><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, ga, n_tiles, m_pairs,
+                                                                         grouped ? 1u : 0u);
 }
 
 uint32_t gemm_groups(uint32_t n_tiles) {
@@ -429,9 +527,19 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, 
                  uint32_t n_tiles, cudaStream_t st, const CUtensorMap* a2) {
   const CUtensorMap& A2 = a2 ? *a2 : a;
   switch (g.limbs) {
-    case 1: launch_pair_kernel<1>(a, b, A2, g, m_tiles, n_tiles, st); break;
-    case 2: launch_pair_kernel<2>(a, b, A2, g, m_tiles, n_tiles, st); break;
-    default: launch_pair_kernel<4>(a, b, A2, g, m_tiles, n_tiles, st); break;
+    case 1: launch_pair_kernel<1, false>(a, b, A2, g, m_tiles, n_tiles, st); break;
+    case 2:
+      if (g.s_conv)
+        launch_pair_kernel<2, true>(a, b, A2, g, m_tiles, n_tiles, st);
+      else
+        launch_pair_kernel<2, false>(a, b, A2, g, m_tiles, n_tiles, st);
+      break;
+    default:
+      if (g.s_conv)
+        launch_pair_kernel<4, true>(a, b, A2, g, m_tiles, n_tiles, st);
+      else
+        launch_pair_kernel<4, false>(a, b, A2, g, m_tiles, n_tiles, st);
+      break;
   }
 }
 

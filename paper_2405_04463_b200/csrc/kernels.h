@@ -123,6 +123,9 @@ struct GemmArgs {
   // (0 = the DB planes' s_pad / row0, resident S planes)
   uint32_t s_pad2 = 0;
   uint32_t row0_2 = 0;
+  // kind-1 A operand S = E + O formed in shared memory from the E and O tiles of the
+  // DB planes (no S planes in HBM): each kind-1 k-block takes two stage slots
+  uint32_t s_conv = 0;
   // group lockstep (set by launch_gemm): per-cluster progress words, this launch's epoch
   unsigned long long* prog = nullptr;
   uint32_t epoch = 0;

@@ -863,8 +863,14 @@ void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t nc
 
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   if (!a.ntasks) return;
+  // leave-one-out timing hook (results are WRONG with it): IRISMPC_SKIP_KERNELS=keystream,reshare,lift,inject,msb
+  static const std::string skip = [] {
+    const char* e = std::getenv("IRISMPC_SKIP_KERNELS");
+    return e ? std::string(",") + e + "," : std::string();
+  }();
+  auto on = [&](const char* k) { return skip.empty() || skip.find(std::string(",") + k + ",") == std::string::npos; };
   void* h = prof_begin(st);
-  k_gate_keystream<<<dim3((a.ks_seg_threads + 255) / 256, 1, a.nsegs), 256, 0, st>>>(a);
+  if (on("keystream")) k_gate_keystream<<<dim3((a.ks_seg_threads + 255) / 256, 1, a.nsegs), 256, 0, st>>>(a);
   prof_end(h, "k_gate_keystream", st);
   debug_check("k_gate_keystream", st);
   h = prof_begin(st);
@@ -889,7 +895,8 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return !e ? -1 : (std::string(e) == "tile" ? 1 : 0);
   }();
   const bool lm = force >= 0 ? force == 0 : !a.tile_kernels;
-  if (lm) launch_reshare_lm(a, st);
+  if (!on("reshare")) {
+  } else if (lm) launch_reshare_lm(a, st);
   else switch (a.variant) {
     case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
     case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
@@ -900,22 +907,26 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_reshare", st);
   if (a.variant == kMpcLift) {
     h = prof_begin(st);
-    k_lift<<<task_blocks, 128, 0, st>>>(a);
+    if (on("lift")) k_lift<<<task_blocks, 128, 0, st>>>(a);
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
-    if (lm)
+    if (!on("inject")) {
+    } else if (lm) {
       launch_inject_lm(a, st);
-    else
+    } else {
       k_inject<<<tile_blocks, kTileThreads, pad, st>>>(a);
+    }
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }
   h = prof_begin(st);
-  if (a.variant == kPlainMask)
+  if (!on("msb")) {
+  } else if (a.variant == kPlainMask) {
     k_msb<16><<<task_blocks, 128, 0, st>>>(a);
-  else
+  } else {
     k_msb<32><<<task_blocks, 128, 0, st>>>(a);
+  }
   prof_end(h, "k_msb", st);
   debug_check("k_msb", st);
 }

@@ -373,61 +373,19 @@ __device__ __forceinline__ void gate_rand(const ThrArgs& A, const Seg& sg, uint6
   }
 }
 
-// gate randomness straight from the keystream buffer (L2 / HBM)
-struct GlobalGates {
-  const ThrArgs& A;
-  const Seg& sg;
-  uint64_t w64;
-  int half;
-  __device__ __forceinline__ void operator()(int g, uint32_t f[3]) const { gate_rand(A, sg, w64, half, g, f); }
-};
-
-// gate randomness of a warp's 1024-lane task staged in shared memory:
-// sm[(k * ng + g - g0) * 16 + w], w = the task's 64-lane word (thread lane / 2)
-struct SmemGates {
-  const uint64_t* sm;
-  int ng, g0, wl, half;
-  __device__ __forceinline__ void operator()(int g, uint32_t f[3]) const {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) f[k] = (uint32_t)(sm[(k * ng + g - g0) * 16 + wl] >> (32 * half));
-  }
-};
-
-// Copies gates [g0, g0 + ng) x 3 seeds of the task's 16 reference words from the
-// keystream buffer into sm (cp.async, 8 bytes each); words outside the segment
-// (lanes that are masked anyway) are zero.  Warp-cooperative; completes before return.
-__device__ __forceinline__ void stage_gates(const ThrArgs& A, const Seg& sg, uint64_t L0, int g0, int ng,
-                                            uint64_t* sm) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t W0 = L0 / 64, wlast = (sg.lane_end - 1) / 64;
-  const uint64_t nwp = gate_row_words(wlast - sg.w_first + 1);
-  for (int idx = lane; idx < 3 * ng * 16; idx += 32) {
-    const int k = idx / (ng * 16), gi = (idx / 16) % ng, w = idx % 16;
-    const uint64_t wq = W0 + w;
-    if (wq < sg.w_first || wq > wlast) {
-      sm[idx] = 0;
-      continue;
-    }
-    const uint32_t pad = (uint32_t)(gate_base(A, k, g0 + gi) + sg.w_first) & 7u;  // k_gate_keystream layout
-    const uint64_t* src = A.gate + sg.g_off + (uint64_t)(k * A.ngates + g0 + gi) * nwp + pad + (wq - sg.w_first);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sm + idx)), "l"(src) : "memory");
-  }
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-  __syncwarp();
-}
-
 // bit_extract_sum for one index M over summand rows R[c][j] (component c of
 // summand c; rows j >= K are zero), evaluated position by position: chain
 // gate t = j then full-adder gate j.  fa(j) = fa0 + j,
 // ch(t) = min(ch0 + chs (t - 1), chmax).
-template <int M, int K, typename Gates>
-__device__ __forceinline__ void extract_bit(const Gates& gate, const uint32_t (&R)[3][K], int fa0, int ch0, int chs,
-                                            int chmax, uint32_t out[3]) {
+template <int M, int K>
+__device__ __forceinline__ void extract_bit(const ThrArgs& A, const Seg& sg, uint64_t w64, int half,
+                                            const uint32_t (&R)[3][K], int fa0, int ch0, int chs, int chmax,
+                                            uint32_t out[3]) {
   uint32_t carry[3] = {0, 0, 0}, chain[3] = {0, 0, 0};
   // gate randomness one step ahead: the loads of step j + 1 are in flight while
   // step j computes (the kernels are latency-bound on these L2 reads)
   uint32_t fc_next[3] = {0, 0, 0}, ff_next[3];
-  gate(fa0, ff_next);
+  gate_rand(A, sg, w64, half, fa0, ff_next);
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     uint32_t fc[3], ff[3];
@@ -437,8 +395,8 @@ __device__ __forceinline__ void extract_bit(const Gates& gate, const uint32_t (&
       ff[c] = ff_next[c];
     }
     if (j + 1 < M) {
-      gate(min(ch0 + chs * j, chmax), fc_next);  // chain gate of step j + 1
-      gate(fa0 + j + 1, ff_next);
+      gate_rand(A, sg, w64, half, min(ch0 + chs * j, chmax), fc_next);  // chain gate of step j + 1
+      gate_rand(A, sg, w64, half, fa0 + j + 1, ff_next);
     }
     uint32_t s[3];
 #pragma unroll
@@ -478,16 +436,11 @@ __device__ __forceinline__ void extract_bit(const Gates& gate, const uint32_t (&
 
 }  // namespace
 
-// warp -> 1024-lane task, thread -> 32 lanes.  STAGED: one warp per CTA, the
-// task's 64 x 3 gate words first copied into shared memory (24 KB), so the
-// adder chain waits on shared-memory rather than L2 / HBM latency.
-template <bool STAGED>
-__global__ void __launch_bounds__(STAGED ? 32 : 128, STAGED ? 8 : LIFT_LB) k_lift(const __grid_constant__ ThrArgs A) {
-  extern __shared__ uint64_t gsm[];
+// warp -> 1024-lane task, thread -> 32 lanes
+__global__ void __launch_bounds__(128, LIFT_LB) k_lift(const __grid_constant__ ThrArgs A) {
   const int lane = threadIdx.x & 31;
   TaskCtx t;
   if (!task_ctx(A, t)) return;
-  if (STAGED) stage_gates(A, t.sg, t.L0, 0, 64, gsm);
   const uint64_t task = t.task;
   const uint64_t Lt = t.L0 + 32ull * lane;
   const uint32_t vm = valid_mask(t, Lt);
@@ -525,15 +478,8 @@ __global__ void __launch_bounds__(STAGED ? 32 : 128, STAGED ? 8 : LIFT_LB) k_lif
   const uint64_t w64 = Lt / 64;
   const int half = lane & 1;
   uint32_t b16[3], b17[3];
-  if (STAGED) {
-    const SmemGates gs{gsm, 64, 0, lane >> 1, half};
-    extract_bit<16, 16>(gs, R, 0, 33, 2, 63, b16);
-    extract_bit<17, 16>(gs, R, 16, 34, 2, 63, b17);
-  } else {
-    const GlobalGates gg{A, t.sg, w64, half};
-    extract_bit<16, 16>(gg, R, 0, 33, 2, 63, b16);
-    extract_bit<17, 16>(gg, R, 16, 34, 2, 63, b17);
-  }
+  extract_bit<16, 16>(A, t.sg, w64, half, R, 0, 33, 2, 63, b16);
+  extract_bit<17, 16>(A, t.sg, w64, half, R, 16, 34, 2, 63, b17);
   const uint64_t o = task * 32 + lane;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -698,13 +644,11 @@ __device__ __noinline__ void fused_or(const ThrArgs& A, const Seg& sg, uint64_t 
 
 // warp -> 1024-lane task: msb<KC> of diff (circuits.hpp:300-306), outputs,
 // fused first OR level.  Gates: FA j -> nlift + j, chain t -> nlift + KC - 1 + (t - 1).
-template <int KC, bool STAGED>
-__global__ void __launch_bounds__(STAGED ? 32 : 128, STAGED ? 8 : MSB_LB) k_msb(const __grid_constant__ ThrArgs A) {
-  extern __shared__ uint64_t gsm[];
+template <int KC>
+__global__ void __launch_bounds__(128, MSB_LB) k_msb(const __grid_constant__ ThrArgs A) {
   const int lane = threadIdx.x & 31;
   TaskCtx t;
   if (!task_ctx(A, t)) return;
-  if (STAGED) stage_gates(A, t.sg, t.L0, (int)A.nlift, 2 * KC - 3, gsm);
   const uint64_t task = t.task;
   const uint64_t Lt = t.L0 + 32ull * lane;
   const uint32_t vm = valid_mask(t, Lt);
@@ -740,15 +684,7 @@ __global__ void __launch_bounds__(STAGED ? 32 : 128, STAGED ? 8 : MSB_LB) k_msb(
   uint32_t bit[3] = {0u, 0u, 0u};
   // rows >= KC of the transposed diff are never read (extract_bit<KC - 1, 32> touches rows <= KC - 1)
   const int nl = (int)A.nlift;
-  if (vm) {
-    if (STAGED) {
-      const SmemGates gs{gsm, 2 * KC - 3, nl, lane >> 1, lane & 1};
-      extract_bit<KC - 1, 32>(gs, D, nl, nl + KC - 1, 1, nl + 2 * KC - 4, bit);
-    } else {
-      const GlobalGates gg{A, t.sg, Lt / 64, lane & 1};
-      extract_bit<KC - 1, 32>(gg, D, nl, nl + KC - 1, 1, nl + 2 * KC - 4, bit);
-    }
-  }
+  if (vm) extract_bit<KC - 1, 32>(A, t.sg, Lt / 64, lane & 1, D, nl, nl + KC - 1, 1, nl + 2 * KC - 4, bit);
 #pragma unroll
   for (int c = 0; c < 3; ++c) bit[c] &= vm;
   if (A.tap_msb) {
@@ -959,11 +895,6 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return !e ? -1 : (std::string(e) == "tile" ? 1 : 0);
   }();
   const bool lm = force >= 0 ? force == 0 : !a.tile_kernels;
-  // lift / msb with the task's gate words staged in shared memory (A/B: IRISMPC_THR_STAGED=1)
-  static const bool staged = [] {
-    const char* e = std::getenv("IRISMPC_THR_STAGED");
-    return e && e[0] == '1';
-  }();
   if (!on("reshare")) {
   } else if (lm) launch_reshare_lm(a, st);
   else switch (a.variant) {
@@ -976,12 +907,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   debug_check("k_reshare", st);
   if (a.variant == kMpcLift) {
     h = prof_begin(st);
-    if (on("lift")) {
-      if (staged)
-        k_lift<true><<<dim3(a.task_seg_max, 1, a.nsegs), 32, 3 * 64 * 16 * 8, st>>>(a);
-      else
-        k_lift<false><<<task_blocks, 128, 0, st>>>(a);
-    }
+    if (on("lift")) k_lift<<<task_blocks, 128, 0, st>>>(a);
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
     h = prof_begin(st);
@@ -997,15 +923,9 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
   h = prof_begin(st);
   if (!on("msb")) {
   } else if (a.variant == kPlainMask) {
-    if (staged)
-      k_msb<16, true><<<dim3(a.task_seg_max, 1, a.nsegs), 32, 3 * 29 * 16 * 8, st>>>(a);
-    else
-      k_msb<16, false><<<task_blocks, 128, 0, st>>>(a);
+    k_msb<16><<<task_blocks, 128, 0, st>>>(a);
   } else {
-    if (staged)
-      k_msb<32, true><<<dim3(a.task_seg_max, 1, a.nsegs), 32, 3 * 61 * 16 * 8, st>>>(a);
-    else
-      k_msb<32, false><<<task_blocks, 128, 0, st>>>(a);
+    k_msb<32><<<task_blocks, 128, 0, st>>>(a);
   }
   prof_end(h, "k_msb", st);
   debug_check("k_msb", st);

@@ -19,18 +19,21 @@
 //   msb gate g (0..60): seed1 pos1 + 4n + 64W + gW + w, seed2 pos2 + 2n + 64W + gW + w,
 //                       seed3 pos3 + 8n + 64W + gW + w
 //
-// Kernels (every PRF block computed once, one block per thread per step):
+// Kernels (every PRF block computed once):
 //   k_gate_keystream  the 125 AND gates' zero-share words of every reference
 //                     word the chunk touches: per (seed, gate) one contiguous
 //                     stream segment -> HBM buffer G
-//   k_reshare         1024-lane tiles: the tile's reshare draws into shared
-//                     memory (one ChaCha block per thread per step), then
-//                     own = z + F_p - F_{p-1}; writes reshared ml (u16) and
-//                     diff0 = a*ml - b*hd (u32)
+//   k_reshare         own = z + F_p - F_{p-1}; writes reshared ml (u16) and
+//                     diff0 = a*ml - b*hd (u32).  Two implementations: 504-lane
+//                     tiles here (the tile's draws into shared memory one ChaCha
+//                     block per thread per step, then thread = 4 lanes; the
+//                     comparison-only path), lane-major in threshold_lm.cu
+//                     (thread = 8 lanes, warp-cooperative windows; the batch
+//                     query, where it runs beside the GEMM; see launch_threshold)
 //   k_lift            bit-sliced (thread = 32 lanes): share_split of ml + the
 //                     two adders {16,17} -> injected-bit rows
-//   k_inject          1024-lane tiles, the same two phases: bit_inject<15>,
-//                     <16>, const-lifted into diff
+//   k_inject          bit_inject<15>, <16>, const-lifted into diff (tile /
+//                     lane-major, as k_reshare)
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
 //                     match-bit shares, fused first MPC-OR level per warp
 #include <cstdlib>

@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(256, 2) k_reshare_lm(const __grid_constant__ T
   bool full = gc.mine && L8 >= sg.lane_begin && L8 + 8 <= sg.lane_end && !A.tap_rs_hd;
   const HT* hd[3];
   const MT* ml[3];
-#pragma unroll
   const uint64_t rp0 = sg.src_rp + (L8 - sg.lane_begin);
   const uint64_t hs0 = A.rp_kstride_h ? rp0 : src0, ms0 = A.rp_kstride_m ? rp0 : src0;
   const uint64_t hk = A.rp_kstride_h, mk = A.rp_kstride_m;
   full = full && hk % 8 == 0 && mk % 8 == 0;  // P2 / P3 vectors stay 16-byte aligned
+#pragma unroll
   for (int p = 0; p < 3; ++p) {
     hd[p] = static_cast<const HT*>(A.hd[p]);
     ml[p] = static_cast<const MT*>(A.ml[p]);

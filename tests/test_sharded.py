@@ -83,3 +83,22 @@ def test_sharded_requires_attach_and_total_rows():
     sh2 = P.Session(cfg, master_seed=1)
     with pytest.raises(P.ConfigError):
         sh2.sharded_batch_query([np.zeros(10, np.uint8)] * 3, 1)  # not attached
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("backend", ["shamir", "replicated"])
+def test_sharded_over_nccl_two_processes(backend):
+    """The same sharded query with the library's NCCL communicator, one process
+    per GPU (tools/sharded_nccl.py --check); runs where >= 2 GPUs are visible."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + (backend == "shamir")),
+           os.path.join(root, "tools", "sharded_nccl.py"), "--check", "--backend", backend]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["check"] is True and line["person_match"][0] == 1 and line["person_match"][2] == 1

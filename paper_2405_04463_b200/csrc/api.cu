@@ -290,7 +290,7 @@ struct QSlot {
 struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
-  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;  // GEMM / threshold front / threshold back
   int shamir = 0;
   int variant = kMpcLift;
   VariantWidths vw{16, 16, 32};
@@ -304,7 +304,12 @@ struct irismpc_gpu_ctx {
   // query scratch
   Buf q_pay[3];
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
-  Buf ml_rs, diff, gate, bits;
+  Buf ml_rs, diff, gate, bits;  // comparison-only work buffers
+  // batch-query threshold work buffers, two sets: job k's front half (keystream,
+  // reshare on st2) runs while job k-1's back half (lift, inject, msb on st3) does
+  Buf wk_ml_rs[2], wk_diff[2], wk_gate[2], wk_bits[2];
+  cudaEvent_t front_done[2] = {nullptr, nullptr}, back_done[2] = {nullptr, nullptr};
+  uint64_t job_ctr = 0;
   std::vector<Seg> h_segs;
   Seg* h_segs_pinned = nullptr;
   size_t h_segs_cap = 0;
@@ -324,7 +329,7 @@ struct irismpc_gpu_ctx {
   cudaEvent_t ev[6];
   std::unique_ptr<ShardComm> shard;  // DB-sharded queries (irismpc_gpu_shard_attach_*)
   Buf shard_part, shard_all;
-  std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done (st) / threshold done (st2)
+  std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done (st); evt[0]: last back half done (st3)
   QSlot qs[2];
   int par = 0;                 // slot of the next query
   uint64_t tickets = 0;        // submitted batch queries
@@ -578,12 +583,20 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     return e && e[0] == '1';
   }();
   cudaStream_t st = c->st, st2 = (serial || c->serial) ? c->st : c->st2;
+  // the threshold chain's back half (lift, inject, msb: latency-bound) on its own stream, so it
+  // overlaps the next job's front half (keystream, reshare: ALU-bound); IRISMPC_THR_ONE_STREAM=1: A/B
+  static const bool one_thr = std::getenv("IRISMPC_THR_ONE_STREAM") != nullptr;
+  cudaStream_t st3 = (serial || c->serial || one_thr) ? st2 : c->st3;
   uint64_t launches = 0;
   for (auto& e : Q.ev)
     if (!e) CK(c, cudaEventCreate(&e));
   if (!Q.done) CK(c, cudaEventCreateWithFlags(&Q.done, cudaEventDisableTiming));
   for (auto& e : c->half_free)
     if (!e) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (int k = 0; k < 2; ++k) {
+    if (!c->front_done[k]) CK(c, cudaEventCreateWithFlags(&c->front_done[k], cudaEventDisableTiming));
+    if (!c->back_done[k]) CK(c, cudaEventCreateWithFlags(&c->back_done[k], cudaEventDisableTiming));
+  }
 
   CK(c, cudaEventRecord(Q.ev[0], st));
   const uint8_t* dqp[3] = {dq[0], dq[1], dq[2]};
@@ -898,11 +911,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint64_t dots_half = round_up(hd_half + fm.nparty * mcols * rows_chunk * mb, 16);
   if (nsegs_all) {
     CK(c, cudaMemcpyAsync(Q.segs.p, hsegs, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
-    if ((nchunks && c->dots.ensure(2 * dots_half)) ||
-        c->ml_rs.ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
-        c->diff.ensure(3 * cstride * sizeof(uint32_t) + 16) || c->gate.ensure(max_g * sizeof(uint64_t) + 16) ||
-        c->bits.ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))
-      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
+    if (nchunks && c->dots.ensure(2 * dots_half)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dot buffers)");
+    for (int k = 0; k < (st3 != st2 ? 2 : 1); ++k)
+      if (c->wk_ml_rs[k].ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
+          c->wk_diff[k].ensure(3 * cstride * sizeof(uint32_t) + 16) ||
+          c->wk_gate[k].ensure(max_g * sizeof(uint64_t) + 16) ||
+          c->wk_bits[k].ensure((V == kMpcLift ? 6 * max_bits * sizeof(uint32_t) : 0) + 16))
+        return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (threshold work buffers)");
   }
   // per-chunk S planes (IRISMPC_RP_CHUNKED): one scratch per field, reused chunk after chunk on
   // the GEMM stream (k_rp_sum of chunk i+1 is queued behind chunk i's GEMM)
@@ -942,10 +957,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   ta.nslots = total_slots;
   ta.or_stream = or_stream_id(octr, rank, 1);
   ta.or_elem_base = 0;
-  ta.ml_rs = c->ml_rs.as<uint16_t>();
-  ta.diff = c->diff.as<uint32_t>();
   ta.cstride = cstride;
-  ta.gate = c->gate.as<uint64_t>();
   if (c->taps && !row_taps) {
     ta.tap_rs_hd = c->tap_buf[2].as<uint32_t>();
     ta.tap_rs_ml = c->tap_buf[3].as<uint32_t>();
@@ -966,8 +978,13 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.ks_seg_threads = (uint32_t)j.ks_seg;
     t.grp_seg_max = (uint32_t)j.grp_seg;
     t.task_seg_max = (uint32_t)j.task_seg;
-    t.bits = c->bits.as<uint32_t>();
-    t.gate = c->gate.as<uint64_t>();
+    // work-buffer set of this job: front (st2) waits until the back half (st3) of the job
+    // two before, which used the same set, is done; back waits for this job's front
+    const int wp = st3 != st2 ? (int)(c->job_ctr++ % 2) : 0;
+    t.ml_rs = c->wk_ml_rs[wp].as<uint16_t>();
+    t.diff = c->wk_diff[wp].as<uint32_t>();
+    t.gate = c->wk_gate[wp].as<uint64_t>();
+    t.bits = c->wk_bits[wp].as<uint32_t>();
     t.nbits = j.ntasks * 32;
     t.or_elem_base = ta.or_elem_base + task_off * 64;
     task_off += j.ntasks;
@@ -979,7 +996,14 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     t.match_w0 = j.pair ? match_w0 : 0;
     t.rp_kstride_h = ks_h;
     t.rp_kstride_m = ks_m;
-    launch_threshold(t, st2);
+    if (st3 != st2) CK(c, cudaStreamWaitEvent(st2, c->back_done[wp], 0));
+    launch_threshold_front(t, st2);
+    if (st3 != st2) {
+      CK(c, cudaEventRecord(c->front_done[wp], st2));
+      CK(c, cudaStreamWaitEvent(st3, c->front_done[wp], 0));
+    }
+    launch_threshold_back(t, st3);
+    if (st3 != st2) CK(c, cudaEventRecord(c->back_done[wp], st3));
     CK(c, cudaGetLastError());
     launches += V == kMpcLift ? 5 : 3;
     return 0;
@@ -992,7 +1016,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     return 0;
   };
-  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, nchunks + 1)) return IRISMPC_GPU_ERR_DEVICE;
+  if (ensure_events(c->evg, nchunks + 1) || ensure_events(c->evt, 1)) return IRISMPC_GPU_ERR_DEVICE;
   while (Q.gev.size() < 2 * nchunks) {
     cudaEvent_t e;
     CK(c, cudaEventCreate(&e));
@@ -1138,6 +1162,10 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     }
     int rc2 = run_job(jobs.back(), pd_hd, pd_ml, npairs, npairs, 0, 0);
     if (rc2) return rc2;
+  }
+  if (st3 != st2) {  // the OR reads every job's partial slots (written by the back halves)
+    CK(c, cudaEventRecord(c->evt[0], st3));
+    CK(c, cudaStreamWaitEvent(st2, c->evt[0], 0));
   }
   CK(c, cudaEventRecord(Q.ev[3], st2));
 
@@ -1623,7 +1651,8 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* e = std::getenv("IRISMPC_PRIO_SWAP"); e && e[0] == '1') std::swap(prio_lo, prio_hi);
   if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return IRISMPC_GPU_ERR_DEVICE;
   }
@@ -1652,6 +1681,14 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   }
   for (auto& e : c->half_free)
     if (e) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (c->front_done[k]) cudaEventDestroy(c->front_done[k]);
+    if (c->back_done[k]) cudaEventDestroy(c->back_done[k]);
+    c->wk_ml_rs[k].release();
+    c->wk_diff[k].release();
+    c->wk_gate[k].release();
+    c->wk_bits[k].release();
+  }
   c->shard.reset();
   c->shard_part.release();
   c->shard_all.release();
@@ -1667,7 +1704,9 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   for (auto& e : c->evg) cudaEventDestroy(e);
   for (auto& e : c->evt) cudaEventDestroy(e);
   cudaStreamSynchronize(c->st2);
+  cudaStreamSynchronize(c->st3);
   cudaStreamDestroy(c->st2);
+  cudaStreamDestroy(c->st3);
   cudaStreamDestroy(c->st);
   delete c;
 }

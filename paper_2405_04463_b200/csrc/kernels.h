@@ -213,6 +213,11 @@ struct ThrArgs {
 // words: nw / 8 + 2 whole ChaCha blocks (k_gate_keystream stores full blocks)
 __host__ __device__ inline uint64_t gate_row_words(uint64_t nw) { return 8 * (nw / 8 + 2); }
 void launch_threshold(const ThrArgs& a, cudaStream_t st);
+// the chain in two halves for two streams: front = gate keystream + reshare (the
+// dot readers), back = lift + inject + msb; parts: 1 front, 2 back, 3 both
+void launch_threshold_front(const ThrArgs& a, cudaStream_t st);
+void launch_threshold_back(const ThrArgs& a, cudaStream_t st);
+void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts);
 // lane-major reshare / inject (threshold_lm.cu): the batch query's default (see launch_threshold)
 void launch_reshare_lm(const ThrArgs& a, cudaStream_t st);
 void launch_inject_lm(const ThrArgs& a, cudaStream_t st);

@@ -865,6 +865,16 @@ void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t nc
 }
 
 void launch_threshold(const ThrArgs& a, cudaStream_t st) {
+  launch_threshold_front(a, st);
+  launch_threshold_back(a, st);
+}
+
+// front half: the gate keystream and the reshare (the only readers of the dot
+// outputs); back half: lift, inject, msb (the latency-bound bit-sliced adders)
+void launch_threshold_front(const ThrArgs& a, cudaStream_t st) { launch_threshold_part(a, st, 1); }
+void launch_threshold_back(const ThrArgs& a, cudaStream_t st) { launch_threshold_part(a, st, 2); }
+
+void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts) {
   if (!a.ntasks) return;
   // leave-one-out timing hook (results are WRONG with it): IRISMPC_SKIP_KERNELS=keystream,reshare,lift,inject,msb
   static const std::string skip = [] {
@@ -872,12 +882,6 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return e ? std::string(",") + e + "," : std::string();
   }();
   auto on = [&](const char* k) { return skip.empty() || skip.find(std::string(",") + k + ",") == std::string::npos; };
-  void* h = prof_begin(st);
-  if (on("keystream")) k_gate_keystream<<<dim3((a.ks_seg_threads + 255) / 256, 1, a.nsegs), 256, 0, st>>>(a);
-  prof_end(h, "k_gate_keystream", st);
-  debug_check("k_gate_keystream", st);
-  h = prof_begin(st);
-  // lane-major kernels: 31 eight-lane groups per warp, 8 warps per block
   // reshare / inject: one CTA per kTile-lane tile of a segment
   const dim3 tile_blocks((unsigned)((a.task_seg_max * 1024ull + 3 + kTile - 1) / kTile), 1, a.nsegs);
   // A/B hook: extra dynamic shared memory per reshare / inject CTA (keeps them off
@@ -887,10 +891,10 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : 0;
   }();
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
-  // Which reshare / inject kernels: the 512-lane tile kernels run 1.5x (reshare)
-  // faster standalone (comparison-only path, serial profile), but beside the
-  // persistent GEMM of a batch query the lane-major kernels keep the threshold
-  // stream shorter (configs[2]: 432-437 vs 483 ms per query, same box, A/B in
+  // Which reshare / inject kernels: the tile kernels run 1.5x (reshare) faster
+  // standalone (comparison-only path, serial profile), but beside the persistent
+  // GEMM of a batch query the lane-major kernels keep the threshold stream
+  // shorter (configs[2]: 432-437 vs 483 ms per query, same box, A/B in
   // profiles/r2_threshold_ab.md), so the batch query uses those.
   // IRISMPC_THR_KERNELS=tile|lm overrides (A/B hook).
   static const int force = [] {
@@ -898,18 +902,29 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     return !e ? -1 : (std::string(e) == "tile" ? 1 : 0);
   }();
   const bool lm = force >= 0 ? force == 0 : !a.tile_kernels;
-  if (!on("reshare")) {
-  } else if (lm) launch_reshare_lm(a, st);
-  else switch (a.variant) {
-    case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-    case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-    case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-    default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-  }
-  prof_end(h, "k_reshare", st);
-  debug_check("k_reshare", st);
-  if (a.variant == kMpcLift) {
+  if (parts & 1) {
+    void* h = prof_begin(st);
+    if (on("keystream")) k_gate_keystream<<<dim3((a.ks_seg_threads + 255) / 256, 1, a.nsegs), 256, 0, st>>>(a);
+    prof_end(h, "k_gate_keystream", st);
+    debug_check("k_gate_keystream", st);
     h = prof_begin(st);
+    if (!on("reshare")) {
+    } else if (lm) {
+      launch_reshare_lm(a, st);
+    } else {
+      switch (a.variant) {
+        case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+        case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+        case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+        default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+      }
+    }
+    prof_end(h, "k_reshare", st);
+    debug_check("k_reshare", st);
+  }
+  if (!(parts & 2)) return;
+  if (a.variant == kMpcLift) {
+    void* h = prof_begin(st);
     if (on("lift")) k_lift<<<task_blocks, 128, 0, st>>>(a);
     prof_end(h, "k_lift", st);
     debug_check("k_lift", st);
@@ -923,7 +938,7 @@ void launch_threshold(const ThrArgs& a, cudaStream_t st) {
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);
   }
-  h = prof_begin(st);
+  void* h = prof_begin(st);
   if (!on("msb")) {
   } else if (a.variant == kPlainMask) {
     k_msb<16><<<task_blocks, 128, 0, st>>>(a);

@@ -583,10 +583,15 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     return e && e[0] == '1';
   }();
   cudaStream_t st = c->st, st2 = (serial || c->serial) ? c->st : c->st2;
-  // the threshold chain's back half (lift, inject, msb: latency-bound) on its own stream, so it
-  // overlaps the next job's front half (keystream, reshare: ALU-bound); IRISMPC_THR_ONE_STREAM=1: A/B
-  static const bool one_thr = std::getenv("IRISMPC_THR_ONE_STREAM") != nullptr;
-  cudaStream_t st3 = (serial || c->serial || one_thr) ? st2 : c->st3;
+  // A/B hook IRISMPC_THR_TWO_STREAMS=1: the threshold chain's back half (lift, inject, msb) on a
+  // third stream, overlapping the next job's front half (keystream, reshare) with two work-buffer
+  // sets.  Measured: configs[2] 439-440 vs 425-427 ms per query on one stream, configs[1] 21.20 vs
+  // 21.33 ms, so one stream is the default.
+  static const bool two_thr = [] {
+    const char* e = std::getenv("IRISMPC_THR_TWO_STREAMS");
+    return e && e[0] == '1';
+  }();
+  cudaStream_t st3 = (two_thr && !serial && !c->serial) ? c->st3 : st2;
   uint64_t launches = 0;
   for (auto& e : Q.ev)
     if (!e) CK(c, cudaEventCreate(&e));

@@ -80,7 +80,6 @@ struct Tile {
   // the last column tile of a launch runs only the columns it has, rounded up to 16
   // (configs[2]: 1984 = 7 x 256 + 192 columns, 3.1% fewer MACs than a padded tile)
   static __device__ __forceinline__ uint32_t tile_n(uint32_t n_tile, uint32_t ncols) {
-    if (ncols == 0xFFFFFFFFu) return BN;
     const uint32_t left = ncols > n_tile * BN ? ncols - n_tile * BN : 16u;
     return left >= (uint32_t)BN ? (uint32_t)BN : (left + 15u) & ~15u;
   }
@@ -209,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int limb = 0; limb < L; ++limb) {
               const int32_t arow = (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
               const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
-                                             n_tile * BN + rank * (T::tile_n(n_tile, g.full_tiles ? 0xFFFFFFFFu : g.ncols) / 2));
+                                             n_tile * BN + rank * (T::tile_n(n_tile, g.ncols) / 2));
               tma_load_2d(st0 + limb * T::A_T, &tA, &raw[stage], (int32_t)((g.a_kb0 + kk) * BK), arow);
               tma_load_2d(st1 + limb * T::A_T, &tA, &raw[s1], (int32_t)((g.a_kb0_k2 + kk) * BK), arow);
               tma_load_2d_pair(st0 + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
@@ -259,7 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int limb = 0; limb < L; ++limb) {
             const int32_t arow = (int32_t)((pa * L + limb) * a_spad + a_row0 + m_pair * 256 + rank * 128);
             const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
-                                           n_tile * BN + rank * (T::tile_n(n_tile, g.full_tiles ? 0xFFFFFFFFu : g.ncols) / 2));
+                                           n_tile * BN + rank * (T::tile_n(n_tile, g.ncols) / 2));
             tma_load_2d_pair(st + limb * T::A_T, ta, fb, (int32_t)((akb + kk) * BK), arow);
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
           }
@@ -282,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         const uint32_t uu = flat ? u / n_tiles : u;
         const bool cv = CONV && (uu / m_pairs) / g.nprob == 1;
-        const uint32_t idesc = T::idesc(T::tile_n(flat ? u % n_tiles : my_n, g.full_tiles ? 0xFFFFFFFFu : g.ncols));
+        const uint32_t idesc = T::idesc(T::tile_n(flat ? u % n_tiles : my_n, g.ncols));
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
@@ -499,8 +498,6 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
   const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
   GemmArgs ga = g;
-  static const bool full_tiles = std::getenv("IRISMPC_GEMM_FULL_TILES") != nullptr;  // A/B hook
-  ga.full_tiles = full_tiles ? 1u : 0u;
   static const bool no_lock = std::getenv("IRISMPC_GEMM_NO_LOCKSTEP") != nullptr;  // A/B hook
   if (grouped && n_tiles > 1 && !no_lock) {
     DevState& ds = g_dev[dev];

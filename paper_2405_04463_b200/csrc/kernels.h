@@ -130,7 +130,6 @@ struct GemmArgs {
   unsigned long long* prog = nullptr;
   uint32_t epoch = 0;
   uint32_t lag = 16;  // k-block iterations a cluster may run ahead of its group's slowest
-  uint32_t full_tiles = 0;  // A/B hook (IRISMPC_GEMM_FULL_TILES=1): the last column tile runs all BN columns
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }

@@ -77,15 +77,6 @@ struct Tile {
   // Instruction descriptor, kind::i8: c_format S32 (2) [4,6), a/b format u8 (0),
   // K-major A and B, N>>3 [17,23), M>>4 [24,29) with M = 256 (CTA pair).
   static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-  // the last column tile of a launch runs only the columns it has, rounded up to 16
-  // (configs[2]: 1984 = 7 x 256 + 192 columns, 3.1% fewer MACs than a padded tile)
-  static __device__ __forceinline__ uint32_t tile_n(uint32_t n_tile, uint32_t ncols) {
-    const uint32_t left = ncols > n_tile * BN ? ncols - n_tile * BN : 16u;
-    return left >= (uint32_t)BN ? (uint32_t)BN : (left + 15u) & ~15u;
-  }
-  static __device__ __forceinline__ uint32_t idesc(uint32_t n) {
-    return (2u << 4) | ((n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-  }
 };
 
 }  // namespace
@@ -208,7 +199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int limb = 0; limb < L; ++limb) {
               const int32_t arow = (int32_t)((pa * L + limb) * g.s_pad + g.row0 + m_pair * 256 + rank * 128);
               const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
-                                             n_tile * BN + rank * (T::tile_n(n_tile, g.ncols) / 2));
+                                             n_tile * BN + rank * (BN / 2));
               tma_load_2d(st0 + limb * T::A_T, &tA, &raw[stage], (int32_t)((g.a_kb0 + kk) * BK), arow);
               tma_load_2d(st1 + limb * T::A_T, &tA, &raw[s1], (int32_t)((g.a_kb0_k2 + kk) * BK), arow);
               tma_load_2d_pair(st0 + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
@@ -258,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int limb = 0; limb < L; ++limb) {
             const int32_t arow = (int32_t)((pa * L + limb) * a_spad + a_row0 + m_pair * 256 + rank * 128);
             const int32_t brow = (int32_t)(brow0 + ((p * g.nseg + seg) * L + limb) * g.nb_rows + g.col0 +
-                                           n_tile * BN + rank * (T::tile_n(n_tile, g.ncols) / 2));
+                                           n_tile * BN + rank * (BN / 2));
             tma_load_2d_pair(st + limb * T::A_T, ta, fb, (int32_t)((akb + kk) * BK), arow);
             tma_load_2d_pair(st + L * T::A_T + limb * T::B_T, &tB, fb, (int32_t)(kk * BK), brow);
           }
@@ -281,7 +272,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         const uint32_t uu = flat ? u / n_tiles : u;
         const bool cv = CONV && (uu / m_pairs) / g.nprob == 1;
-        const uint32_t idesc = T::idesc(T::tile_n(flat ? u % n_tiles : my_n, g.ncols));
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
@@ -305,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                   const uint64_t da = make_desc(st + i * T::A_T) + off;
                   const uint64_t db = make_desc(st + L * T::A_T + j * T::B_T) + off;
                   const uint32_t acc = ((kb | ks) != 0 || i > 0) ? 1u : 0u;  // (0, s) opens acc_s
-                  umma_i8_pair(tmem + (i + j) * BN, da, db, idesc, acc);
+                  umma_i8_pair(tmem + (i + j) * BN, da, db, T::IDESC, acc);
                 }
             }
             umma_commit_pair(&empty[stage], 0x3);

@@ -333,8 +333,9 @@ struct irismpc_gpu_ctx {
   QSlot qs[2];
   int par = 0;                 // slot of the next query
   uint64_t tickets = 0;        // submitted batch queries
-  uint64_t chunk_ctr = 0;      // dot-buffer half of the next row chunk (continues across queries)
-  cudaEvent_t half_free[2] = {nullptr, nullptr};  // threshold of the last chunk that read each half
+  uint64_t chunk_ctr = 0;      // dot buffer of the next row chunk (continues across queries)
+  static constexpr int kMaxDotBufs = 4;
+  cudaEvent_t half_free[kMaxDotBufs] = {};  // threshold of the last chunk that read each dot buffer
 };
 
 namespace {
@@ -909,14 +910,20 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     max_g = std::max(max_g, j.gwords);
     max_bits = std::max(max_bits, j.ntasks * 32);
   }
-  // one dot buffer half: hd [3][ncols * rows_chunk] then ml [nparty][ncols * rows_chunk]
+  // dot buffers the GEMM stream rotates through (2: the GEMM runs at most one chunk ahead of
+  // the threshold; IRISMPC_DOT_BUFS=3|4: A/B hook)
+  static const int ndotbufs = [] {
+    const char* e = std::getenv("IRISMPC_DOT_BUFS");
+    return e ? std::max(2, std::min(irismpc_gpu_ctx::kMaxDotBufs, std::atoi(e))) : 2;
+  }();
+  // one dot buffer: hd [3][ncols * rows_chunk] then ml [nparty][ncols * rows_chunk]
   // per field: plain [party][col][row] dots, or RP [kind P1 | P2 | P3][party][rotation pair][row]
   const uint64_t hcols = use_rp[0] ? 3 * ncols_rp : ncols, mcols = use_rp[1] ? 3 * ncols_rp : ncols;
   const uint64_t hd_half = 3 * hcols * rows_chunk * hb;
   const uint64_t dots_half = round_up(hd_half + fm.nparty * mcols * rows_chunk * mb, 16);
   if (nsegs_all) {
     CK(c, cudaMemcpyAsync(Q.segs.p, hsegs, nsegs_all * sizeof(Seg), cudaMemcpyHostToDevice, st));
-    if (nchunks && c->dots.ensure(2 * dots_half)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dot buffers)");
+    if (nchunks && c->dots.ensure(ndotbufs * dots_half)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (dot buffers)");
     for (int k = 0; k < (st3 != st2 ? 2 : 1); ++k)
       if (c->wk_ml_rs[k].ensure((V == kMpcLift ? 3 * cstride * sizeof(uint16_t) : 0) + 16) ||
           c->wk_diff[k].ensure(3 * cstride * sizeof(uint32_t) + 16) ||
@@ -1047,7 +1054,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     const uint64_t nr = chunk_rows(i);
     // dot-buffer halves alternate across chunks and across queries: the GEMM
     // waits for the threshold of the last chunk (of any query) that read the half
-    const int half = (int)(c->chunk_ctr++ % 2);
+    const int half = (int)(c->chunk_ctr++ % ndotbufs);
     uint8_t* dots = c->dots.as<uint8_t>() + half * dots_half;
     uint8_t* dots_ml = dots + hd_half;
     CK(c, cudaStreamWaitEvent(st, c->half_free[half], 0));

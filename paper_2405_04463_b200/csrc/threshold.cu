@@ -884,12 +884,6 @@ void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts) {
   auto on = [&](const char* k) { return skip.empty() || skip.find(std::string(",") + k + ",") == std::string::npos; };
   // reshare / inject: one CTA per kTile-lane tile of a segment
   const dim3 tile_blocks((unsigned)((a.task_seg_max * 1024ull + 3 + kTile - 1) / kTile), 1, a.nsegs);
-  // A/B hook: extra dynamic shared memory per reshare / inject CTA (keeps them off
-  // the SMs the persistent GEMM occupies when large)
-  static const int pad = [] {
-    const char* e = std::getenv("IRISMPC_THR_SMEM_PAD");
-    return e ? std::atoi(e) : 0;
-  }();
   const dim3 task_blocks((a.task_seg_max + 3) / 4, 1, a.nsegs);  // 4 warps (tasks) per 128-thread block
   // Which reshare / inject kernels: the tile kernels run 1.5x (reshare) faster
   // standalone (comparison-only path, serial profile), but beside the persistent
@@ -913,10 +907,10 @@ void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts) {
       launch_reshare_lm(a, st);
     } else {
       switch (a.variant) {
-        case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-        case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-        case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
-        default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, pad, st>>>(a); break;
+        case kPlainMask: k_reshare<kPlainMask><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+        case kMpcLift: k_reshare<kMpcLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+        case kConstLift: k_reshare<kConstLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
+        default: k_reshare<kNoLift><<<tile_blocks, kTileThreads, 0, st>>>(a); break;
       }
     }
     prof_end(h, "k_reshare", st);
@@ -933,7 +927,7 @@ void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts) {
     } else if (lm) {
       launch_inject_lm(a, st);
     } else {
-      k_inject<<<tile_blocks, kTileThreads, pad, st>>>(a);
+      k_inject<<<tile_blocks, kTileThreads, 0, st>>>(a);
     }
     prof_end(h, "k_inject", st);
     debug_check("k_inject", st);

@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/irismpc_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -49,6 +51,12 @@ struct Buf {
 };
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// NVTX range over a C-ABI call (host timeline in nsys / ncu; no-op without a tool)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
 
 // ---- host-side ChaCha / seeds / lambda (setup only) ------------------------
@@ -1729,6 +1737,7 @@ void* irismpc_gpu_stream(irismpc_gpu_ctx* c) { return c ? (void*)c->st : nullptr
 
 int irismpc_gpu_load_db(irismpc_gpu_ctx* c, const uint8_t* const payload[3], const size_t len[3], uint64_t s) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.load_db");
   cudaSetDevice(c->cfg.device);
   const size_t rec = c->rec;
   for (int p = 0; p < 3; ++p)
@@ -1760,6 +1769,7 @@ int irismpc_gpu_load_db(irismpc_gpu_ctx* c, const uint8_t* const payload[3], con
 int irismpc_gpu_load_db_device(irismpc_gpu_ctx* c, const uint8_t* const dpayload[3], const size_t len[3],
                                uint64_t s) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.load_db_device");
   cudaSetDevice(c->cfg.device);
   const size_t rec = c->rec;
   for (int p = 0; p < 3; ++p)
@@ -1778,6 +1788,7 @@ int irismpc_gpu_load_db_device(irismpc_gpu_ctx* c, const uint8_t* const dpayload
 
 int irismpc_gpu_load_db_files(irismpc_gpu_ctx* c, const char* const paths[3]) {
   if (!c || !paths) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.load_db_files");
   cudaSetDevice(c->cfg.device);
   irismpc_gpu_share_header h[3];
   for (int p = 0; p < 3; ++p) {
@@ -1854,6 +1865,7 @@ int irismpc_gpu_load_db_files(irismpc_gpu_ctx* c, const char* const paths[3]) {
 int irismpc_gpu_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint32_t persons,
                             uint8_t* person_match_out, uint8_t* row_bits_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.batch_query");
   cudaSetDevice(c->cfg.device);
   const uint8_t* none[3] = {nullptr, nullptr, nullptr};
   return run_query(c, none, qlen, persons, 0, 0, person_match_out, row_bits_out, nullptr, stats, true, q);
@@ -1863,6 +1875,7 @@ int irismpc_gpu_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* const dq[3
                                    uint32_t persons, uint8_t* person_match_out, uint8_t* row_bits_out,
                                    irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.batch_query_device");
   cudaSetDevice(c->cfg.device);
   return run_query(c, dq, qlen, persons, 0, 0, person_match_out, row_bits_out, nullptr, stats, false, nullptr);
 }
@@ -1870,6 +1883,7 @@ int irismpc_gpu_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* const dq[3
 int irismpc_gpu_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3], uint8_t* match_out,
                            uint8_t* row_bits_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.membership");
   cudaSetDevice(c->cfg.device);
   const uint8_t* none[3] = {nullptr, nullptr, nullptr};
   return run_query(c, none, qlen, 1, 1, 0, match_out, row_bits_out, nullptr, stats, true, q);
@@ -1878,6 +1892,7 @@ int irismpc_gpu_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const 
 int irismpc_gpu_batch_query_submit(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
                                    uint32_t persons, uint8_t* person_match_out, uint64_t* ticket) {
   if (!c || !ticket) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.batch_query_submit");
   cudaSetDevice(c->cfg.device);
   if (c->taps || c->tap_k || c->cfg.debug_rows)
     return fail(c, IRISMPC_GPU_ERR_CONFIG, "streaming queries run without taps / debug_rows");
@@ -1886,6 +1901,7 @@ int irismpc_gpu_batch_query_submit(irismpc_gpu_ctx* c, const uint8_t* const dq[3
 
 int irismpc_gpu_batch_query_wait(irismpc_gpu_ctx* c, uint64_t ticket, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.batch_query_wait");
   cudaSetDevice(c->cfg.device);
   for (auto& q : c->qs) {
     if (q.ticket != ticket) continue;
@@ -1902,6 +1918,7 @@ int irismpc_gpu_batch_query_wait(irismpc_gpu_ctx* c, uint64_t ticket, irismpc_gp
 int irismpc_gpu_batch_query_partial(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
                                     uint32_t persons, uint8_t* partial_out_dev, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.batch_query_partial");
   cudaSetDevice(c->cfg.device);
   return run_query(c, dq, qlen, persons, 0, 1, nullptr, nullptr, partial_out_dev, stats, false, nullptr);
 }
@@ -1925,6 +1942,7 @@ int irismpc_gpu_comparison_only(irismpc_gpu_ctx* c, const uint8_t* const hd_payl
                                 int with_or_tree, uint8_t* opened_out, uint8_t* lane_bits_out,
                                 irismpc_gpu_stats* stats) {
   if (!c || !hd_payload || !ml_payload) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.comparison_only");
   cudaSetDevice(c->cfg.device);
   if (lanes == 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no lanes");
   return run_compare(c, 0, hd_payload, hd_len, ml_payload, ml_len, lanes, with_or_tree, opened_out, lane_bits_out,
@@ -1934,6 +1952,7 @@ int irismpc_gpu_comparison_only(irismpc_gpu_ctx* c, const uint8_t* const hd_payl
 int irismpc_gpu_or_tree_only(irismpc_gpu_ctx* c, const uint8_t* const payload[3], const size_t len[3],
                              uint64_t lanes, uint8_t* opened_out, irismpc_gpu_stats* stats) {
   if (!c || !payload) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.or_tree_only");
   cudaSetDevice(c->cfg.device);
   if (lanes == 0) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no lanes");
   return run_compare(c, 1, payload, len, nullptr, nullptr, lanes, 1, opened_out, nullptr, stats);
@@ -2031,6 +2050,7 @@ static int sharded_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const si
 int irismpc_gpu_sharded_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3],
                                     uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.sharded_batch_query");
   cudaSetDevice(c->cfg.device);
   return sharded_query(c, q, qlen, persons, 0, true, person_match_out, stats);
 }
@@ -2038,6 +2058,7 @@ int irismpc_gpu_sharded_batch_query(irismpc_gpu_ctx* c, const uint8_t* const q[3
 int irismpc_gpu_sharded_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
                                            uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.sharded_batch_query_device");
   cudaSetDevice(c->cfg.device);
   return sharded_query(c, dq, qlen, persons, 0, false, person_match_out, stats);
 }
@@ -2045,6 +2066,7 @@ int irismpc_gpu_sharded_batch_query_device(irismpc_gpu_ctx* c, const uint8_t* co
 int irismpc_gpu_sharded_membership(irismpc_gpu_ctx* c, const uint8_t* const q[3], const size_t qlen[3],
                                    uint8_t* match_out, irismpc_gpu_stats* stats) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.sharded_membership");
   cudaSetDevice(c->cfg.device);
   return sharded_query(c, q, qlen, 1, 1, true, match_out, stats);
 }
@@ -2091,6 +2113,7 @@ int irismpc_gpu_deal_payload(irismpc_gpu_ctx* c, uint64_t deal_seed, uint64_t ta
 int irismpc_gpu_synth_db(irismpc_gpu_ctx* c, uint64_t s, uint64_t rng_seed, uint64_t first, double mask_density,
                          uint64_t deal_seed) {
   if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.synth_db");
   cudaSetDevice(c->cfg.device);
   int rc = alloc_planes(c, s);
   if (rc) return rc;

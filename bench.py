@@ -500,13 +500,20 @@ def main_gpu(args):
     local_lanes = ncodes * ROT * rows
     # one serialised, profiled query (outside the timed region): per-kernel
     # standalone device times for the roofline lines
-    prof = {}
+    prof, prof_tile = {}, {}
     if not args.no_profile:
         sess.profile(True)
         sess.profile_read()
         step(False)
         torch.cuda.synchronize()
         prof = sess.profile_read()
+        # the same query with the tile reshare / inject kernels (faster alone, slower beside
+        # the GEMM, so not the timed path): their standalone efficiency, labelled as such
+        sess.threshold_kernels(True)
+        step(False)
+        torch.cuda.synchronize()
+        prof_tile = sess.profile_read()
+        sess.threshold_kernels(False)
         sess.profile(False)
     if rank == 0:
         peaks, src = load_peaks()
@@ -574,6 +581,11 @@ def main_gpu(args):
             "gpu_launches": stats_acc["launches"],
             "clocks": clk.summary(),
             "roofline_compare": compare_roofline(prof, local_lanes, variant, peaks) if prof else None,
+            "roofline_compare_tile_kernels": ({**compare_roofline(prof_tile, local_lanes, variant, peaks),
+                                               "note": "the same serialised query with the shared-memory tile "
+                                                       "reshare / inject kernels (irismpc_gpu_threshold_kernels): "
+                                                       "faster alone, slower beside the GEMM, NOT the timed path"}
+                                              if prof_tile else None),
             "phase_ms": {"gemm_per_launch": gemm_ms,
                          "gemm_launches_per_step": stats_acc["gemm_launches"] / args.steps,
                          "threshold_stream_span": sess.last_stats.threshold_ms,

@@ -306,6 +306,10 @@ int irismpc_gpu_write_iris_db(const char* path, uint32_t l, uint64_t s, const ui
 int irismpc_gpu_profile(irismpc_gpu_ctx* ctx, int on);
 int irismpc_gpu_profile_read(irismpc_gpu_ctx* ctx, char (*names)[48], double* ms, uint64_t* launches,
                              uint32_t max, uint32_t* count);
+/* Which reshare / bit-inject kernels batch queries use: 0 (default) the
+ * lane-major kernels, faster beside the GEMM; 1 the shared-memory tile kernels,
+ * faster alone (the comparison-only path always uses those).  Same results. */
+int irismpc_gpu_threshold_kernels(irismpc_gpu_ctx* ctx, int tile);
 
 /* ---- debug / parity taps (tests) ------------------------------------------ */
 #define IRISMPC_GPU_TAP_DOT_HD 1  /* [3][n] per-party additive hd dot (L1), u16 (KH = 16) / u32 */

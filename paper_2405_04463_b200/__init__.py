@@ -41,7 +41,7 @@ EXPORTED = [
     "irismpc_gpu_or_open", "irismpc_gpu_get_stream_positions", "irismpc_gpu_set_stream_positions",
     "irismpc_gpu_synth_records", "irismpc_gpu_deal_payload", "irismpc_gpu_synth_db",
     "irismpc_gpu_enable_taps", "irismpc_gpu_read_tap", "irismpc_gpu_profile", "irismpc_gpu_profile_read",
-    "irismpc_gpu_tap_rows", "irismpc_gpu_comparison_only", "irismpc_gpu_or_tree_only",
+    "irismpc_gpu_tap_rows", "irismpc_gpu_threshold_kernels", "irismpc_gpu_comparison_only", "irismpc_gpu_or_tree_only",
     "irismpc_gpu_shard_group_create", "irismpc_gpu_shard_group_destroy", "irismpc_gpu_shard_attach_inproc",
     "irismpc_gpu_shard_attach_nccl", "irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device",
     "irismpc_gpu_sharded_membership", "irismpc_gpu_batch_query_submit", "irismpc_gpu_batch_query_wait",
@@ -167,6 +167,7 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_enable_taps.argtypes = [vp, C.c_int]
         L.irismpc_gpu_profile.argtypes = [vp, C.c_int]
         L.irismpc_gpu_tap_rows.argtypes = [vp, u64p, C.c_uint32]
+        L.irismpc_gpu_threshold_kernels.argtypes = [vp, C.c_int]
         L.irismpc_gpu_comparison_only.argtypes = [vp, P3, S3, P3, S3, C.c_uint64, C.c_int, vp, vp, C.POINTER(Stats)]
         L.irismpc_gpu_or_tree_only.argtypes = [vp, P3, S3, C.c_uint64, vp, C.POINTER(Stats)]
         L.irismpc_gpu_shard_group_create.argtypes = [C.c_uint32, C.POINTER(vp)]
@@ -526,6 +527,10 @@ class Session:
     def profile(self, on: bool = True):
         """Serialised queries with per-kernel CUDA events (irismpc_gpu_profile)."""
         self._check(lib().irismpc_gpu_profile(self._h, 1 if on else 0))
+
+    def threshold_kernels(self, tile: bool):
+        """irismpc_gpu_threshold_kernels: tile (True) or lane-major (False, default) reshare / inject."""
+        self._check(lib().irismpc_gpu_threshold_kernels(self._h, 1 if tile else 0))
 
     def profile_read(self) -> dict:
         """{kernel name: (device ms, launches)} accumulated since the last read."""

@@ -328,6 +328,7 @@ struct irismpc_gpu_ctx {
   // taps
   bool taps = false;
   bool serial = false;  // irismpc_gpu_profile: one stream, per-kernel CUDA events
+  int thr_tile = 0;     // irismpc_gpu_threshold_kernels: the tile reshare / inject kernels in batch queries
   // row-sampled L1 taps (irismpc_gpu_tap_rows): DOT_HD / DOT_ML of these local rows, all columns
   Buf tap_rows_dev;
   uint32_t tap_k = 0;
@@ -959,6 +960,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   ta.variant = V;
   ta.n = n;
   ta.W = W;
+  ta.tile_kernels = c->thr_tile;
   for (int k = 0; k < 3; ++k) {
     ta.pos[k] = c->pos[k];
     ta.key[k] = c->keys[k];
@@ -2152,6 +2154,12 @@ int irismpc_gpu_profile(irismpc_gpu_ctx* c, int on) {
   if (int rc = drain(c)) return rc;
   c->serial = on != 0;
   prof_enable(on != 0);
+  return 0;
+}
+
+int irismpc_gpu_threshold_kernels(irismpc_gpu_ctx* c, int tile) {
+  if (!c) return IRISMPC_GPU_ERR_CONFIG;
+  c->thr_tile = tile != 0;
   return 0;
 }
 

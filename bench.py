@@ -397,7 +397,7 @@ def main_gpu(args):
             return sess.sharded_batch_query([h.numpy() for h in host_q] if rank == 0 else None, persons, qlen)
         return sess.sharded_batch_query(qpay if rank == 0 else None, persons, qlen)
 
-    streaming = world == 1 and not args.sync
+    streaming = not args.sync
     # streaming (irismpc_gpu_batch_query_submit / _wait, two queries in flight): the
     # GEMM stream runs into query i+1 while the threshold stream finishes query i;
     # every step still copies its inputs (e2e: from pinned host memory) and reads
@@ -430,7 +430,10 @@ def main_gpu(args):
                     for d, h in zip(src, host_q):
                         d.copy_(h, non_blocking=True)
                 upload.synchronize()  # the payload is on the device before the library's parse
-            tickets.append(sess.batch_query_submit(src, persons))
+            if world == 1:
+                tickets.append(sess.batch_query_submit(src, persons))
+            else:
+                tickets.append(sess.sharded_batch_query_submit(src if rank == 0 else None, persons, qlen))
             if i >= 1:
                 res = sess.batch_query_wait(tickets[i - 1])
                 account(sess.last_stats)

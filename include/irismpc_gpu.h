@@ -193,6 +193,12 @@ int irismpc_gpu_sharded_batch_query_device(irismpc_gpu_ctx* ctx, const uint8_t* 
                                            uint32_t persons, uint8_t* person_match_out, irismpc_gpu_stats* stats);
 int irismpc_gpu_sharded_membership(irismpc_gpu_ctx* ctx, const uint8_t* const q[3], const size_t qlen[3],
                                    uint8_t* match_out, irismpc_gpu_stats* stats);
+/* Streaming form (NCCL attach only): every collective is stream-ordered, so each
+ * shard's GEMM stream runs into the next query like irismpc_gpu_batch_query_submit;
+ * complete with irismpc_gpu_batch_query_wait.  dq: DEVICE payloads on shard 0 (NULL
+ * elsewhere), valid until the ticket completes. */
+int irismpc_gpu_sharded_batch_query_submit(irismpc_gpu_ctx* ctx, const uint8_t* const dq[3], const size_t qlen[3],
+                                           uint32_t persons, uint8_t* person_match_out, uint64_t* ticket);
 
 /* PRF stream positions (per seed); a fresh context starts at 0 like
  * run_parties; the reference CLI keeps PartyCtx across queries. */

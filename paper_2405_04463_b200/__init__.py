@@ -45,6 +45,7 @@ EXPORTED = [
     "irismpc_gpu_shard_group_create", "irismpc_gpu_shard_group_destroy", "irismpc_gpu_shard_attach_inproc",
     "irismpc_gpu_shard_attach_nccl", "irismpc_gpu_sharded_batch_query", "irismpc_gpu_sharded_batch_query_device",
     "irismpc_gpu_sharded_membership", "irismpc_gpu_batch_query_submit", "irismpc_gpu_batch_query_wait",
+    "irismpc_gpu_sharded_batch_query_submit",
     "irismpc_gpu_read_share_header", "irismpc_gpu_write_share_file", "irismpc_gpu_load_db_files",
     "irismpc_gpu_read_seed_files", "irismpc_gpu_write_seed_file", "irismpc_gpu_read_iris_db_header",
     "irismpc_gpu_read_iris_db", "irismpc_gpu_write_iris_db",
@@ -179,6 +180,7 @@ def lib() -> C.CDLL:
         L.irismpc_gpu_sharded_membership.argtypes = [vp, P3, S3, vp, C.POINTER(Stats)]
         L.irismpc_gpu_batch_query_submit.argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(C.c_uint64)]
         L.irismpc_gpu_batch_query_wait.argtypes = [vp, C.c_uint64, C.POINTER(Stats)]
+        L.irismpc_gpu_sharded_batch_query_submit.argtypes = [vp, P3, S3, C.c_uint32, vp, C.POINTER(C.c_uint64)]
         L.irismpc_gpu_profile_read.argtypes = [vp, vp, vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.irismpc_gpu_read_tap.argtypes = [vp, C.c_int, vp, C.c_size_t]
         cp3 = C.c_char_p * 3
@@ -488,6 +490,24 @@ class Session:
         f = lib().irismpc_gpu_sharded_batch_query_device if dev else lib().irismpc_gpu_sharded_batch_query
         self._check(f(self._h, ptrs, lens, persons, out.ctypes.data, C.byref(self.last_stats)))
         return out[:persons]
+
+    def sharded_batch_query_submit(self, q, persons: int, qlen=None) -> int:
+        """Streaming sharded query (NCCL attach): device payloads on shard 0 (None elsewhere,
+        qlen then gives their sizes); complete with batch_query_wait (person_match on shard 0)."""
+        if q is not None:
+            dev, arrs, ptrs, lens = self._q(q)
+            if not dev:
+                raise ConfigError("sharded_batch_query_submit expects device-resident payloads")
+        else:
+            arrs, ptrs, lens = None, (vp * 3)(None, None, None), (C.c_size_t * 3)(*qlen)
+        out = np.zeros(max(1, persons), np.uint8)
+        t = C.c_uint64(0)
+        self._check(lib().irismpc_gpu_sharded_batch_query_submit(self._h, ptrs, lens, persons, out.ctypes.data,
+                                                                 C.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (out[:persons], arrs)
+        return t.value
 
     # -- the comparison phase alone ---------------------------------------------
     def comparison_only(self, hd_payloads, ml_payloads, lanes: int, with_or_tree: bool = False,

@@ -156,7 +156,12 @@ struct ShardComm {
 
 struct NcclShardComm : ShardComm {
   ncclComm_t comm = nullptr;
+  // a second communicator (ncclCommSplit of the first) for the streaming path's gathers on
+  // the threshold stream while the next query's broadcast runs on the GEMM stream: NCCL
+  // operations of one communicator must not be in flight on two streams at once
+  ncclComm_t comm2 = nullptr;
   ~NcclShardComm() override {
+    if (comm2 && nccl().ok) nccl().comm_destroy(comm2);
     if (comm && nccl().ok) nccl().comm_destroy(comm);
   }
   std::string bcast(void* dev, size_t bytes, cudaStream_t st) override {
@@ -276,6 +281,7 @@ struct FieldPlanes {
 // and its result buffers are per slot; two slots alternate.
 struct QSlot {
   Buf segs, slot_begin, match[3], pair_dots, open_out;
+  Buf qpay[3], part, all;  // streaming sharded queries: broadcast payloads, own / gathered partials
   Seg* h_segs = nullptr;
   size_t h_segs_cap = 0;
   uint8_t* h_match = nullptr;  // pinned copy of the opened person bits
@@ -337,6 +343,7 @@ struct irismpc_gpu_ctx {
   uint64_t tap_n = 0;
   cudaEvent_t ev[6];
   std::unique_ptr<ShardComm> shard;  // DB-sharded queries (irismpc_gpu_shard_attach_*)
+  NcclShardComm* shard_nccl = nullptr;  // the same object when attached over NCCL (streaming)
   Buf shard_part, shard_all;
   std::vector<cudaEvent_t> evg, evt;  // chunk pipeline: GEMM done (st); evt[0]: last back half done (st3)
   QSlot qs[2];
@@ -1692,7 +1699,8 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   cudaStreamSynchronize(c->st);
   drain(c);
   for (auto& q : c->qs) {
-    Buf* qb[] = {&q.segs, &q.slot_begin, &q.match[0], &q.match[1], &q.match[2], &q.pair_dots, &q.open_out};
+    Buf* qb[] = {&q.segs, &q.slot_begin, &q.match[0], &q.match[1], &q.match[2], &q.pair_dots, &q.open_out,
+                 &q.qpay[0], &q.qpay[1], &q.qpay[2], &q.part, &q.all};
     for (Buf* b : qb) b->release();
     if (q.h_segs) cudaFreeHost(q.h_segs);
     if (q.h_match) cudaFreeHost(q.h_match);
@@ -1711,6 +1719,7 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
     c->wk_gate[k].release();
     c->wk_bits[k].release();
   }
+  c->shard_nccl = nullptr;
   c->shard.reset();
   c->shard_part.release();
   c->shard_all.release();
@@ -1981,6 +1990,7 @@ static int shard_check(irismpc_gpu_ctx* c, uint32_t world) {
 int irismpc_gpu_shard_attach_inproc(irismpc_gpu_ctx* c, irismpc_gpu_shard_group* g) {
   if (!c || !g) return IRISMPC_GPU_ERR_CONFIG;
   if (int rc = shard_check(c, g->world)) return rc;
+  c->shard_nccl = nullptr;
   auto sc = std::make_unique<InprocShardComm>();
   sc->g = g;
   sc->world = g->world;
@@ -1999,8 +2009,11 @@ int irismpc_gpu_shard_attach_nccl(irismpc_gpu_ctx* c, const uint8_t nccl_id[128]
   std::memcpy(&id, nccl_id, sizeof(id));
   const ncclResult_t r = nccl().comm_init_rank(&sc->comm, (int)world, id, (int)c->cfg.shard_rank);
   if (r != ncclSuccess) return fail(c, IRISMPC_GPU_ERR_DEVICE, std::string("ncclCommInitRank: ") + nccl().error_string(r));
+  if (nccl().comm_split && nccl().comm_split(sc->comm, 0, (int)c->cfg.shard_rank, &sc->comm2, nullptr) != ncclSuccess)
+    sc->comm2 = nullptr;  // streaming sharded queries then unavailable (synchronous ones still work)
   sc->world = world;
   sc->rank = c->cfg.shard_rank;
+  c->shard_nccl = sc.get();
   c->shard = std::move(sc);
   return 0;
 }
@@ -2046,6 +2059,72 @@ static int sharded_query(irismpc_gpu_ctx* c, const uint8_t* const q[3], const si
   }
   CK(c, cudaStreamSynchronize(c->st));
   if (stats) stats->kernel_launches += sc.rank == 0 ? 1 : 0;
+  return 0;
+}
+
+// Streaming sharded query (NCCL only): everything is stream-ordered, no host sync --
+// the query payloads are broadcast on the GEMM stream into this slot's buffers, the
+// shard's query runs up to its partial, and the gather (second communicator), the
+// cross-shard OR and the open follow on the threshold stream, so the GEMM stream of
+// every shard runs into the next query like the single-GPU streaming path.
+int irismpc_gpu_sharded_batch_query_submit(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[3],
+                                           uint32_t persons, uint8_t* person_match_out, uint64_t* ticket) {
+  if (!c || !ticket) return IRISMPC_GPU_ERR_CONFIG;
+  const Range nvtx_range("irismpc.sharded_batch_query_submit");
+  cudaSetDevice(c->cfg.device);
+  NcclShardComm* nc = c->shard_nccl;
+  if (!nc || !nc->comm2) return fail(c, IRISMPC_GPU_ERR_CONFIG, "streaming sharded queries need an NCCL shard attach");
+  if (c->taps || c->tap_k || c->cfg.debug_rows)
+    return fail(c, IRISMPC_GPU_ERR_CONFIG, "streaming queries run without taps / debug_rows");
+  QSlot& Q = c->qs[c->par];  // the slot run_query takes next
+  if (Q.inflight) {
+    const int rc = finish_slot(c, Q);
+    if (rc) return rc;
+  }
+  const uint32_t groups = persons;
+  const uint8_t* qp[3];
+  ncclResult_t r = nccl().group_start();
+  for (int p = 0; p < 3 && r == ncclSuccess; ++p) {
+    if (Q.qpay[p].ensure(qlen[p] + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (query payload)");
+    if (nc->rank == 0) {
+      if (!dq || !dq[p]) return fail(c, IRISMPC_GPU_ERR_CONFIG, "shard 0 needs the query payloads");
+      CK(c, cudaMemcpyAsync(Q.qpay[p].p, dq[p], qlen[p], cudaMemcpyDeviceToDevice, c->st));
+    }
+    r = nccl().broadcast(Q.qpay[p].p, Q.qpay[p].p, qlen[p], ncclUint8, 0, nc->comm, c->st);
+    qp[p] = Q.qpay[p].as<uint8_t>();
+  }
+  const ncclResult_t r2 = nccl().group_end();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, std::string("nccl broadcast: ") + nccl().error_string(r ? r : r2));
+  if (Q.part.ensure(3ull * groups + 16) || Q.all.ensure(3ull * groups * nc->world + 16))
+    return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (shard partials)");
+  uint64_t t = 0;
+  int rc = run_query(c, qp, qlen, persons, 0, 1, nullptr, nullptr, Q.part.as<uint8_t>(), nullptr, false, nullptr, &t);
+  if (rc) return rc;
+  // run_query queued the partial hand-off on the threshold stream of this slot; the rest follows it
+  cudaStream_t st2 = c->serial ? c->st : c->st2;
+  const ncclResult_t r3 = nccl().all_gather(Q.part.p, Q.all.p, 3ull * groups, ncclUint8, nc->comm2, st2);
+  if (r3 != ncclSuccess) return fail(c, IRISMPC_GPU_ERR_DEVICE, std::string("nccl all_gather: ") + nccl().error_string(r3));
+  if (nc->rank == 0) {
+    if (Q.open_out.ensure(groups + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom");
+    if (groups + 16 > Q.h_match_cap) {
+      if (Q.h_match) cudaFreeHost(Q.h_match);
+      Q.h_match = nullptr;
+      Q.h_match_cap = 0;
+      CK(c, cudaMallocHost(&Q.h_match, groups + 16));
+      Q.h_match_cap = groups + 16;
+    }
+    launch_or_open(Q.all.as<uint8_t>(), nc->world, groups, c->keys, or_stream_id(c->or_ctr, 0, 3),
+                   Q.open_out.as<uint8_t>(), st2);
+    CK(c, cudaGetLastError());
+    CK(c, cudaMemcpyAsync(Q.h_match, Q.open_out.p, groups, cudaMemcpyDeviceToHost, st2));
+    Q.mode = 0;
+    Q.match_out = person_match_out;
+    Q.stats.kernel_launches += 1;
+  }
+  CK(c, cudaEventRecord(Q.ev[4], st2));
+  CK(c, cudaEventRecord(Q.done, st2));
+  *ticket = t;
   return 0;
 }
 

@@ -20,6 +20,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclCommSplit) comm_split = nullptr;  // optional (streaming sharded queries)
   bool ok = false;
 };
 
@@ -39,6 +40,7 @@ inline const NcclApi& nccl() {
     a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
     a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
     a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    a.comm_split = (decltype(a.comm_split))dlsym(h, "ncclCommSplit");
     a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.broadcast &&
            a.all_gather && a.group_start && a.group_end && a.error_string;
     return a;

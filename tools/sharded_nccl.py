@@ -49,12 +49,20 @@ def main():
     sess.shard_attach_nccl(idl[0], world)
     qlen = [len(x) for x in q]
     m = sess.sharded_batch_query(q if rank == 0 else None, persons, qlen)
-    m2 = sess.sharded_batch_query([torch.from_numpy(x).cuda() for x in q] if rank == 0 else None, persons, qlen)
+    qd = [torch.from_numpy(x).cuda() for x in q] if rank == 0 else None
+    m2 = sess.sharded_batch_query(qd, persons, qlen)
+    # streaming: three queries, two in flight (every collective stream-ordered)
+    tk = [sess.sharded_batch_query_submit(qd, persons, qlen)]
+    tk.append(sess.sharded_batch_query_submit(qd, persons, qlen))
+    ms = [sess.batch_query_wait(tk[0])]
+    tk.append(sess.sharded_batch_query_submit(qd, persons, qlen))
+    ms += [sess.batch_query_wait(tk[1]), sess.batch_query_wait(tk[2])]
     if rank == 0:
         out = {"world": world, "person_match": [int(x) for x in m]}
         if a.check:
             ref = O.run_local(O.make_config(be, l), seed, dc, dm, qc, qm, persons)
-            out["check"] = bool(np.array_equal(m, ref.person_match) and np.array_equal(m2, ref.person_match))
+            out["check"] = bool(np.array_equal(m, ref.person_match) and np.array_equal(m2, ref.person_match) and
+                                all(np.array_equal(x, ref.person_match) for x in ms))
         print(json.dumps(out), flush=True)
     dist.barrier()
     dist.destroy_process_group()

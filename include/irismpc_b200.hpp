@@ -19,6 +19,7 @@
 #include <array>
 #include <condition_variable>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <span>
 #include <stdexcept>
@@ -155,6 +156,28 @@ class Session {
   }
   std::array<MembershipResult, 3> membership(const Payloads& q) { return query(q, 1, true); }
 
+  // Streaming (irismpc_gpu_batch_query_submit / _wait): DEVICE payloads that stay valid
+  // until the ticket completes; at most two queries in flight.  wait() returns P1's bits.
+  std::uint64_t submit(const std::array<const std::uint8_t*, 3>& dq, const std::array<std::size_t, 3>& qlen,
+                       unsigned persons) {
+    auto out = std::make_unique<std::vector<std::uint8_t>>(persons, 0);  // stable buffer while in flight
+    std::uint64_t t = 0;
+    check(irismpc_gpu_batch_query_submit(ctx_, dq.data(), qlen.data(), persons, out->data(), &t), "submit", ctx_);
+    pending_.emplace_back(t, std::move(out));
+    return t;
+  }
+  std::vector<std::uint8_t> wait(std::uint64_t ticket) {
+    irismpc_gpu_stats st{};
+    check(irismpc_gpu_batch_query_wait(ctx_, ticket, &st), "wait", ctx_);
+    for (auto it = pending_.begin(); it != pending_.end(); ++it)
+      if (it->first == ticket) {
+        std::vector<std::uint8_t> r = std::move(*it->second);
+        pending_.erase(it);
+        return r;
+      }
+    throw Error("wait: unknown ticket");
+  }
+
   irismpc_gpu_ctx* raw() { return ctx_; }
   std::uint64_t rows() const { return s_; }
 
@@ -198,6 +221,7 @@ class Session {
   EngineConfig cfg_;
   irismpc_gpu_ctx* ctx_ = nullptr;
   std::uint64_t s_ = 0;
+  std::vector<std::pair<std::uint64_t, std::unique_ptr<std::vector<std::uint8_t>>>> pending_;
 };
 
 // ---- DB-sharded queries: one Session per shard (GPU), each with

@@ -8,6 +8,8 @@
 #include <thread>
 #include <vector>
 
+#include <cuda_runtime_api.h>
+
 #include "../../include/irismpc_b200.hpp"
 #include "../../oracle/irismpc_oracle.h"
 
@@ -121,6 +123,30 @@ int main() {
       std::printf("MISMATCH sharded person_match\n");
       return 1;
     }
+  }
+
+  // streaming: Session::submit / wait with device query payloads, three submits
+  // (the third completes the oldest implicitly), every ticket equals the oracle
+  {
+    Session st(cfg, seeds_from_master(seed));
+    st.load_db({db[0], db[1], db[2]}, s);
+    std::array<std::uint8_t*, 3> dq{};
+    std::array<std::size_t, 3> qlen{};
+    for (int p = 0; p < 3; ++p) {
+      qlen[p] = q[p].size();
+      if (cudaMalloc(reinterpret_cast<void**>(&dq[p]), qlen[p]) != cudaSuccess ||
+          cudaMemcpy(dq[p], q[p].data(), qlen[p], cudaMemcpyHostToDevice) != cudaSuccess)
+        return 2;
+    }
+    const std::array<const std::uint8_t*, 3> cq{dq[0], dq[1], dq[2]};
+    std::uint64_t t[3];
+    for (int i = 0; i < 3; ++i) t[i] = st.submit(cq, qlen, persons);
+    for (int i = 2; i >= 0; --i)
+      if (st.wait(t[i]) != want) {
+        std::printf("MISMATCH streaming ticket %d\n", i);
+        return 1;
+      }
+    for (int p = 0; p < 3; ++p) cudaFree(dq[p]);
   }
 
   // party mode: three GpuParty objects on one InProcNet, one thread each,

@@ -7,20 +7,23 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 SRC = os.path.join(ROOT, "tests", "cpp", "shim_parity.cpp")
 
 
 def _build(out):
-    cmd = [GXX, "-O1", "-std=c++20", "-pthread", "-I" + os.path.join(ROOT, "include"), SRC,
+    cmd = [GXX, "-O1", "-std=c++20", "-pthread", "-I" + os.path.join(ROOT, "include"), "-I" + CUDA + "/include", SRC,
            "-L" + os.path.join(ROOT, "paper_2405_04463_b200"), "-lirismpc_gpu",
            "-L" + os.path.join(ROOT, "oracle"), "-loracle",
+           "-L" + CUDA + "/lib64", "-lcudart",
            "-Wl,-rpath," + os.path.join(ROOT, "paper_2405_04463_b200"), "-Wl,-rpath," + os.path.join(ROOT, "oracle"),
            "-o", out]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
 
 
 def test_shim_header_compiles(tmp_path):
-    subprocess.run([GXX, "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), SRC], check=True)
+    subprocess.run([GXX, "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), "-I" + CUDA + "/include",
+                    SRC], check=True)
     _build(str(tmp_path / "shim"))
 
 

@@ -157,21 +157,29 @@ class Session {
   std::array<MembershipResult, 3> membership(const Payloads& q) { return query(q, 1, true); }
 
   // Streaming (irismpc_gpu_batch_query_submit / _wait): DEVICE payloads that stay valid
-  // until the ticket completes; at most two queries in flight.  wait() returns P1's bits.
+  // until the ticket completes; at most two queries in flight on the device (a third
+  // submit first completes the oldest, whose bits are kept here).  wait() returns P1's bits.
   std::uint64_t submit(const std::array<const std::uint8_t*, 3>& dq, const std::array<std::size_t, 3>& qlen,
                        unsigned persons) {
-    auto out = std::make_unique<std::vector<std::uint8_t>>(persons, 0);  // stable buffer while in flight
-    std::uint64_t t = 0;
-    check(irismpc_gpu_batch_query_submit(ctx_, dq.data(), qlen.data(), persons, out->data(), &t), "submit", ctx_);
-    pending_.emplace_back(t, std::move(out));
-    return t;
+    std::size_t inflight = 0;
+    for (const auto& e : pending_) inflight += !e.done;
+    if (inflight >= 2)
+      for (auto& e : pending_)
+        if (!e.done) {
+          complete(e);
+          break;
+        }
+    Pending e{0, std::make_unique<std::vector<std::uint8_t>>(persons, 0), false};  // stable while in flight
+    check(irismpc_gpu_batch_query_submit(ctx_, dq.data(), qlen.data(), persons, e.bits->data(), &e.ticket),
+          "submit", ctx_);
+    pending_.push_back(std::move(e));
+    return pending_.back().ticket;
   }
   std::vector<std::uint8_t> wait(std::uint64_t ticket) {
-    irismpc_gpu_stats st{};
-    check(irismpc_gpu_batch_query_wait(ctx_, ticket, &st), "wait", ctx_);
     for (auto it = pending_.begin(); it != pending_.end(); ++it)
-      if (it->first == ticket) {
-        std::vector<std::uint8_t> r = std::move(*it->second);
+      if (it->ticket == ticket) {
+        if (!it->done) complete(*it);
+        std::vector<std::uint8_t> r = std::move(*it->bits);
         pending_.erase(it);
         return r;
       }
@@ -221,7 +229,17 @@ class Session {
   EngineConfig cfg_;
   irismpc_gpu_ctx* ctx_ = nullptr;
   std::uint64_t s_ = 0;
-  std::vector<std::pair<std::uint64_t, std::unique_ptr<std::vector<std::uint8_t>>>> pending_;
+  struct Pending {
+    std::uint64_t ticket;
+    std::unique_ptr<std::vector<std::uint8_t>> bits;
+    bool done;
+  };
+  void complete(Pending& e) {
+    irismpc_gpu_stats st{};
+    check(irismpc_gpu_batch_query_wait(ctx_, e.ticket, &st), "wait", ctx_);
+    e.done = true;
+  }
+  std::vector<Pending> pending_;
 };
 
 // ---- DB-sharded queries: one Session per shard (GPU), each with

@@ -300,7 +300,7 @@ def compare_roofline(prof: dict, lanes: int, variant: int, peaks: dict) -> dict:
     dram, dsrc = ncu_threshold_bytes()
     kern = {}
     chain_ms = 0.0
-    for k in THRESHOLD_KERNELS + ("k_or_persons",):
+    for k in THRESHOLD_KERNELS + ("k_ortree",):
         if k not in prof:
             continue
         ms, cnt = prof[k]

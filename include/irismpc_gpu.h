@@ -325,6 +325,8 @@ int irismpc_gpu_threshold_kernels(irismpc_gpu_ctx* ctx, int tile);
 #define IRISMPC_GPU_TAP_ML32 5    /* uint32 [3][n] 32-bit ml components (lift output) */
 #define IRISMPC_GPU_TAP_DIFF 6    /* uint32 [3][n] comparison input components */
 #define IRISMPC_GPU_TAP_MSB 7     /* uint8  [3][n] match bit components */
+#define IRISMPC_GPU_TAP_AGG 8     /* uint8  [3][groups] OR-tree output components of the last query
+                                     (pre-open; always captured, no enable_taps needed) */
 /* Enable capture of all taps for the next query (costly; tests only). */
 int irismpc_gpu_enable_taps(irismpc_gpu_ctx* ctx, int enable);
 int irismpc_gpu_read_tap(irismpc_gpu_ctx* ctx, int tap, void* host_out, size_t bytes);

@@ -497,6 +497,8 @@ static int64_t popcount_and(const uint64_t* a, const uint64_t* b, uint32_t l) {
 
 /* ---- bit-sliced 3-party simulation (circuits.hpp) ---------------------- */
 
+static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
 typedef struct {
   uint64_t* c[3]; /* XOR components, W words each */
 } brow;
@@ -544,6 +546,82 @@ static void and_gate(prf_state* ps, const brow* x, const brow* y, brow* z, uint6
     const uint64_t m = ((uint64_t)1 << (lanes % 64)) - 1;
     for (int p = 0; p < 3; ++p) z->c[p][words - 1] &= m;
   }
+}
+
+/* or_tree_batch (circuits.hpp:387-434): every group folds level by level
+ * (lo = first ceil(N/2) lanes, hi = the rest, lo ^ hi ^ AND(lo, hi) over nb
+ * lanes), all groups of a level in one and_layer round whose gates draw
+ * ceil(nb/64) words each in group order.  grp[g] / gl[g] are replaced by the
+ * one-lane results. */
+static void or_tree_groups(prf_state* ps, brow* grp, uint64_t* gl, uint32_t ngroups, uint64_t* rounds,
+                           uint64_t* bytes) {
+  for (;;) {
+    int progress = 0;
+    uint64_t used = 0;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      if (gl[g] <= 1) continue;
+      progress = 1;
+      const uint64_t na = (gl[g] + 1) / 2, nb = gl[g] - na;
+      const uint64_t wa = ceil_div(na, 64), wb = ceil_div(nb, 64);
+      brow lo = brow_new(wa), hi = brow_new(wa), t = brow_new(wa);
+      for (uint64_t i = 0; i < na; ++i)
+        for (int p = 0; p < 3; ++p)
+          if ((grp[g].c[p][i / 64] >> (i % 64)) & 1) lo.c[p][i / 64] |= (uint64_t)1 << (i % 64);
+      for (uint64_t i = 0; i < nb; ++i)
+        for (int p = 0; p < 3; ++p) {
+          const uint64_t src = na + i;
+          if ((grp[g].c[p][src / 64] >> (src % 64)) & 1) hi.c[p][i / 64] |= (uint64_t)1 << (i % 64);
+        }
+      uint64_t base[3];
+      for (int q = 0; q < 3; ++q) base[q] = ps->pos[q] + used;
+      and_gate(ps, &lo, &hi, &t, wb, nb, base);
+      used += wb;
+      *bytes += ceil_div(nb, 8);
+      for (int p = 0; p < 3; ++p)
+        for (uint64_t w = 0; w < wa; ++w) lo.c[p][w] ^= hi.c[p][w] ^ (w < wb ? t.c[p][w] : 0);
+      brow_free(&grp[g]);
+      grp[g] = lo;
+      gl[g] = na;
+      brow_free(&hi);
+      brow_free(&t);
+    }
+    if (!progress) break;
+    for (int q = 0; q < 3; ++q) ps->pos[q] += used;
+    ++*rounds;
+  }
+}
+
+int orc_or_tree_batch(const uint8_t seeds[48], const uint64_t* stream_start, uint32_t ngroups,
+                      const uint64_t* lens, const uint8_t* comps, uint64_t total, uint8_t* agg,
+                      uint64_t* stream_pos) {
+  prf_state ps;
+  for (int k = 0; k < 3; ++k) {
+    ps.seed[k] = seeds + 16 * k;
+    reader_init(&ps.rd[k], ps.seed[k]);
+    ps.pos[k] = stream_start ? stream_start[k] : 0;
+  }
+  brow* grp = (brow*)malloc(sizeof(brow) * (ngroups ? ngroups : 1));
+  uint64_t* gl = (uint64_t*)malloc(sizeof(uint64_t) * (ngroups ? ngroups : 1));
+  uint64_t off = 0;
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    gl[g] = lens[g];
+    grp[g] = brow_new(ceil_div(lens[g], 64));
+    for (uint64_t i = 0; i < lens[g]; ++i)
+      for (int p = 0; p < 3; ++p)
+        if (comps[p * total + off + i] & 1) grp[g].c[p][i / 64] |= (uint64_t)1 << (i % 64);
+    off += lens[g];
+  }
+  uint64_t rounds = 0, bytes = 0;
+  or_tree_groups(&ps, grp, gl, ngroups, &rounds, &bytes);
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    for (int p = 0; p < 3; ++p) agg[p * ngroups + g] = gl[g] == 0 ? 0 : (uint8_t)(grp[g].c[p][0] & 1);
+    brow_free(&grp[g]);
+  }
+  if (stream_pos)
+    for (int k = 0; k < 3; ++k) stream_pos[k] = ps.pos[k];
+  free(grp);
+  free(gl);
+  return 0;
 }
 
 /* bit_extract_sum (circuits.hpp:202-296) for summand bit matrices rows[k][j]
@@ -692,8 +770,6 @@ static void bit_inject(prf_state* ps, const brow* bits, uint64_t n, unsigned wid
   ps->pos[0] += n;
   ps->pos[2] += 3 * n;
 }
-
-static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1,
               const uint8_t* db2, const uint8_t* db3, uint64_t s, const uint8_t* q1,
@@ -934,45 +1010,15 @@ int orc_query(const orc_config* cfg, const uint8_t seeds[48], const uint8_t* db1
     }
   }
   uint64_t or_rounds = 0, or_bytes = 0;
-  for (;;) {
-    int progress = 0;
-    uint64_t used = 0;
-    for (uint32_t g = 0; g < ngroups; ++g) {
-      if (gl[g] <= 1) continue;
-      progress = 1;
-      const uint64_t na = (gl[g] + 1) / 2, nb = gl[g] - na;
-      const uint64_t wa = ceil_div(na, 64), wb = ceil_div(nb, 64);
-      brow lo = brow_new(wa), hi = brow_new(wa), t = brow_new(wa);
-      for (uint64_t i = 0; i < na; ++i)
-        for (int p = 0; p < 3; ++p)
-          if ((grp[g].c[p][i / 64] >> (i % 64)) & 1) lo.c[p][i / 64] |= (uint64_t)1 << (i % 64);
-      for (uint64_t i = 0; i < nb; ++i)
-        for (int p = 0; p < 3; ++p) {
-          const uint64_t src = na + i;
-          if ((grp[g].c[p][src / 64] >> (src % 64)) & 1) hi.c[p][i / 64] |= (uint64_t)1 << (i % 64);
-        }
-      uint64_t base[3];
-      for (int q = 0; q < 3; ++q) base[q] = ps.pos[q] + used;
-      and_gate(&ps, &lo, &hi, &t, wb, nb, base);
-      used += wb;
-      or_bytes += ceil_div(nb, 8);
-      for (int p = 0; p < 3; ++p)
-        for (uint64_t w = 0; w < wa; ++w) lo.c[p][w] ^= hi.c[p][w] ^ (w < wb ? t.c[p][w] : 0);
-      brow_free(&grp[g]);
-      grp[g] = lo;
-      gl[g] = na;
-      brow_free(&hi);
-      brow_free(&t);
-    }
-    if (!progress) break;
-    for (int q = 0; q < 3; ++q) ps.pos[q] += used;
-    ++or_rounds;
-  }
+  or_tree_groups(&ps, grp, gl, ngroups, &or_rounds, &or_bytes);
   /* open_bits_to(agg, P1) (circuits.hpp:449-486) */
   if (out && out->person_match)
     for (uint32_t g = 0; g < ngroups; ++g)
       out->person_match[g] =
           gl[g] == 0 ? 0 : (uint8_t)((grp[g].c[0][0] ^ grp[g].c[1][0] ^ grp[g].c[2][0]) & 1);
+  if (out && out->agg)
+    for (uint32_t g = 0; g < ngroups; ++g)
+      for (int p = 0; p < 3; ++p) out->agg[p * ngroups + g] = gl[g] == 0 ? 0 : (uint8_t)(grp[g].c[p][0] & 1);
   if (out && out->stream_pos)
     for (int k = 0; k < 3; ++k) out->stream_pos[k] = ps.pos[k];
 

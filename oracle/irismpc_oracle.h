@@ -120,7 +120,15 @@ typedef struct orc_out {
   uint8_t* msb;            /* [3][n] MSB (match) bit components */
   uint64_t* stream_pos;    /* [3]   seed stream positions after the query */
   orc_stats* stats;        /* [3]   per party */
+  uint8_t* agg;            /* [3][groups] or_tree_batch output components (pre-open) */
 } orc_out;
+
+/* or_tree_batch (circuits.hpp:387-434) over caller-given bit sharings: comps
+ * [3][total] component bits, groups = consecutive runs of lens[g] lanes, seed
+ * streams at stream_start (NULL = 0).  agg [3][ngroups]; stream_pos [3] after. */
+int orc_or_tree_batch(const uint8_t seeds[48], const uint64_t* stream_start, uint32_t ngroups,
+                      const uint64_t* lens, const uint8_t* comps, uint64_t total, uint8_t* agg,
+                      uint64_t* stream_pos);
 
 uint64_t orc_lane_count(uint32_t persons, uint64_t s, uint32_t rotations, int membership);
 

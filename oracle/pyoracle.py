@@ -48,7 +48,8 @@ class OrcStats(C.Structure):
 class OrcOut(C.Structure):
     _fields_ = [("person_match", u8p), ("row_bits", u8p), ("dot_hd", u32p), ("dot_ml", u32p),
                 ("public_ml", C.POINTER(C.c_int64)), ("rs_hd", u32p), ("rs_ml", u32p), ("ml32", u32p),
-                ("diff", u32p), ("msb", u8p), ("stream_pos", u64p), ("stats", C.POINTER(OrcStats))]
+                ("diff", u32p), ("msb", u8p), ("stream_pos", u64p), ("stats", C.POINTER(OrcStats)),
+                ("agg", u8p)]
 
 
 _lib = None
@@ -253,6 +254,7 @@ class QueryResult:
     msb: np.ndarray | None = None
     stream_pos: np.ndarray | None = None
     stats: list | None = None
+    agg: np.ndarray | None = None  # [3][groups] OR-tree output components
 
 
 def make_config(backend: int, l: int, ratio: float = 0.375, rotations: int = 31,
@@ -263,7 +265,8 @@ def make_config(backend: int, l: int, ratio: float = 0.375, rotations: int = 31,
 
 
 def _alloc_out(n: int, ngroups: int, want_all: bool):
-    arrs = dict(person_match=np.zeros(max(1, ngroups), np.uint8), row_bits=np.zeros(max(1, n), np.uint8))
+    arrs = dict(person_match=np.zeros(max(1, ngroups), np.uint8), row_bits=np.zeros(max(1, n), np.uint8),
+                agg=np.zeros(3 * max(1, ngroups), np.uint8))
     if want_all:
         arrs.update({k: np.zeros(3 * max(1, n), np.uint32)
                      for k in ("dot_hd", "dot_ml", "rs_hd", "rs_ml", "ml32", "diff")})
@@ -275,7 +278,7 @@ def _alloc_out(n: int, ngroups: int, want_all: bool):
                  _p(arrs.get("public_ml"), C.POINTER(C.c_int64)),
                  _p(arrs.get("rs_hd"), u32p), _p(arrs.get("rs_ml"), u32p),
                  _p(arrs.get("ml32"), u32p), _p(arrs.get("diff"), u32p), _p(arrs.get("msb"), u8p),
-                 _p(pos, u64p), C.cast(stats, C.POINTER(OrcStats)))
+                 _p(pos, u64p), C.cast(stats, C.POINTER(OrcStats)), _p(arrs["agg"], u8p))
     return out, arrs, stats, pos
 
 
@@ -284,7 +287,8 @@ def _width_dtype(bits: int):
 
 
 def _finish(arrs, stats, pos, n, ngroups, want_all, debug_rows, variant=MPC_LIFT):
-    res = QueryResult(person_match=arrs["person_match"][:ngroups].copy())
+    res = QueryResult(person_match=arrs["person_match"][:ngroups].copy(),
+                      agg=arrs["agg"][: 3 * ngroups].reshape(3, ngroups).copy())
     if debug_rows:
         res.row_bits = arrs["row_bits"][:n].copy()
     if want_all:
@@ -574,3 +578,38 @@ def ref_or_tree_local(bits, seed: int):
     if rc:
         raise RuntimeError(f"ref_or_tree_local failed with status {rc}")
     return dict(opened=int(op.value), or_bytes=[int(x) for x in ob], wall_ms=wall.value)
+
+
+def or_tree_batch(seeds: np.ndarray, lens, comps, stream_start=None):
+    """The C restatement's or_tree_batch over caller-given bit sharings:
+    comps [3][sum(lens)] component bits, groups = consecutive runs of lens[g]
+    lanes.  Returns (agg [3][groups], stream positions after)."""
+    L = lib()
+    L.orc_or_tree_batch.argtypes = [u8p, u64p, C.c_uint32, u64p, u8p, C.c_uint64, u8p, u64p]
+    ln = np.ascontiguousarray(lens, np.uint64)
+    cm = np.ascontiguousarray(comps, np.uint8).reshape(3, -1)
+    G = ln.size
+    agg = np.zeros(3 * max(1, G), np.uint8)
+    pos = np.zeros(3, np.uint64)
+    st = None if stream_start is None else np.ascontiguousarray(stream_start, np.uint64)
+    sd = np.ascontiguousarray(seeds, np.uint8)
+    rc = L.orc_or_tree_batch(_p(sd, u8p), _p(st, u64p) if st is not None else None, G, _p(ln, u64p),
+                             _p(cm, u8p), cm.shape[1], _p(agg, u8p), _p(pos, u64p))
+    if rc:
+        raise RuntimeError(f"orc_or_tree_batch failed with status {rc}")
+    return agg[: 3 * G].reshape(3, G), pos
+
+
+def ref_or_tree_batch_shares(lens, comps, seed: int):
+    """The reference's own or_tree_batch (oracle/_ref, run_parties(seed), streams
+    at 0) over the same input as or_tree_batch: agg components [3][groups]."""
+    R = ref()
+    R.ref_or_tree_batch_shares.argtypes = [C.c_uint32, u64p, u8p, C.c_uint64, C.c_uint64, u8p]
+    ln = np.ascontiguousarray(lens, np.uint64)
+    cm = np.ascontiguousarray(comps, np.uint8).reshape(3, -1)
+    G = ln.size
+    agg = np.zeros(3 * max(1, G), np.uint8)
+    rc = R.ref_or_tree_batch_shares(G, _p(ln, u64p), _p(cm, u8p), cm.shape[1], seed, _p(agg, u8p))
+    if rc:
+        raise RuntimeError(f"ref_or_tree_batch_shares failed with status {rc}")
+    return agg[: 3 * G].reshape(3, G)

@@ -484,6 +484,39 @@ void* ref_bench_prepare(int backend, int variant, std::uint32_t l, std::uint64_t
   return b;
 }
 
+// or_tree_batch (circuits.hpp:387-434) run by the reference over caller-given
+// bit sharings: comps [3][total] component bits (party p's own = component
+// p - 1, its prev = the previous party's), groups = consecutive runs of lens[g]
+// lanes; the parties' seeds from run_parties(seed), streams at 0.  Writes the
+// aggregate's components [3][ngroups] (each party's own share of lane g).
+int ref_or_tree_batch_shares(std::uint32_t ngroups, const std::uint64_t* lens, const std::uint8_t* comps,
+                             std::uint64_t total, std::uint64_t seed, std::uint8_t* agg) {
+  try {
+    auto results = run_parties(seed, [&](PartyCtx& ctx) {
+      const unsigned own = party_index(ctx.id) - 1, prv = party_index(prev_party(ctx.id)) - 1;
+      std::vector<OrTreeInput> groups;
+      std::uint64_t off = 0;
+      for (std::uint32_t g = 0; g < ngroups; ++g) {
+        OrTreeInput in{BitRow(lens[g]), lens[g]};
+        for (std::uint64_t i = 0; i < lens[g]; ++i)
+          in.bits.set_lane(i, BitWord{comps[own * total + off + i], comps[prv * total + off + i]});
+        off += lens[g];
+        groups.push_back(std::move(in));
+      }
+      auto [out, st] = or_tree_batch(ctx, std::move(groups));
+      (void)st;
+      std::vector<std::uint8_t> mine(ngroups);
+      for (std::uint32_t g = 0; g < ngroups; ++g) mine[g] = (std::uint8_t)(out.lane(g).own & 1);
+      return mine;
+    });
+    for (int p = 0; p < 3; ++p)
+      for (std::uint32_t g = 0; g < ngroups; ++g) agg[p * ngroups + g] = std::get<0>(results[p])[g];
+    return 0;
+  } catch (...) {
+    return map_error();
+  }
+}
+
 // One step: the three parties run party_batch_query (stock path).  Returns
 // the slowest party's QueryStats.wall_ms; person 0's opened bit in *match0.
 double ref_bench_step(void* h, std::uint8_t* match0) {

@@ -31,7 +31,7 @@ VARIANTS = {"plain-mask": PLAIN_MASK, "mpc-lift": MPC_LIFT, "const-lift": CONST_
 # (hamming dot bits, mask dot bits (0 = public mask bits), comparison bits), shares.hpp:37-48
 VARIANT_WIDTHS = {PLAIN_MASK: (16, 0, 16), MPC_LIFT: (16, 16, 32), CONST_LIFT: (16, 32, 32), NO_LIFT: (32, 32, 32)}
 
-TAP_DOT_HD, TAP_DOT_ML, TAP_RS_HD, TAP_RS_ML, TAP_ML32, TAP_DIFF, TAP_MSB = range(1, 8)
+TAP_DOT_HD, TAP_DOT_ML, TAP_RS_HD, TAP_RS_ML, TAP_ML32, TAP_DIFF, TAP_MSB, TAP_AGG = range(1, 9)
 
 EXPORTED = [
     "irismpc_gpu_seeds_from_master", "irismpc_gpu_record_bytes", "irismpc_gpu_lane_count",
@@ -584,7 +584,7 @@ class Session:
         rows = 1 if (tap == TAP_DOT_ML and km == 0) else 3
         dt = {TAP_DOT_HD: np.uint16 if kh == 16 else np.uint32,
               TAP_DOT_ML: np.uint32 if km == 32 else np.uint16,
-              TAP_MSB: np.uint8}.get(tap, np.uint32)
+              TAP_MSB: np.uint8, TAP_AGG: np.uint8}.get(tap, np.uint32)
         out = np.zeros(rows * n, dt)
         self._check(lib().irismpc_gpu_read_tap(self._h, tap, out.ctypes.data, out.nbytes))
         out = out.reshape(rows, n)

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libirismpc_gpu.so")
-SOURCES = ["prep.cu", "gemm.cu", "pairs.cu", "threshold.cu", "threshold_lm.cu", "orreduce.cu", "share_io.cu", "party.cu", "api.cu"]
+SOURCES = ["prep.cu", "gemm.cu", "pairs.cu", "threshold.cu", "threshold_lm.cu", "orreduce.cu", "ortree.cu", "share_io.cu", "party.cu", "api.cu"]
 HEADERS = ["common.cuh", "kernels.h", "nccl_api.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -319,6 +319,8 @@ struct irismpc_gpu_ctx {
   Buf q_pay[3];
   Buf dots, pair_dots, segs, partial, slot_begin, person_out, match[3], open_out;
   Buf ml_rs, diff, gate, bits;  // comparison-only work buffers
+  Buf or_scr[2];                // OR-tree level rows (ping-pong)
+  uint32_t last_groups = 0;     // groups of the last OR (person_out = [3][last_groups])
   // batch-query threshold work buffers, two sets: job k's front half (keystream,
   // reshare on st2) runs while job k-1's back half (lift, inject, msb on st3) does
   Buf wk_ml_rs[2], wk_diff[2], wk_gate[2], wk_bits[2];
@@ -832,9 +834,16 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
                         cudaMemcpyHostToDevice, st));
 
   const bool dbg = c->cfg.debug_rows != 0 && row_bits_out;
+  // the reference's own OR tree over every lane's bit (share-exact) for an unsharded
+  // query; DB-sharded queries keep the bucketed per-shard OR (the reference has no shards)
+  static const bool or_bucketed = [] {  // A/B hook
+    const char* e = std::getenv("IRISMPC_OR_TREE");
+    return e && std::string(e) == "bucketed";
+  }();
+  const bool exact_or = mode == 0 && S == s_loc && row_off == 0 && !or_bucketed;
   uint64_t match_w0 = 0, match_words = 0;
-  if (dbg) {
-    match_words = ceil_div(n, 32) + 1;
+  if (dbg || exact_or) {
+    match_words = 2 * ceil_div(n, 64) + 4;  // + padding for the tree's 64-bit funnel reads
   } else if (npairs) {
     match_w0 = (ncols * S) / 32;
     match_words = ceil_div(n, 32) - match_w0 + 1;
@@ -897,7 +906,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         sg.src = col * nr;
         sg.src_rp = ((col / r) * npr + (col % r) / 2) * nr;  // RP: the rotation pair's P planes
         sg.rp_sel = ((col % r) & 1) ? 1u : 2u;
-        sg.slot = (int64_t)col_fill[col];
+        sg.slot = exact_or ? -1 : (int64_t)col_fill[col];
         col_fill[col] += seg_tasks(sg.lane_begin, sg.lane_end);
       }
       // threshold jobs of at most kThrLanes lanes (plus 1/8 slack: a chunk rounded up to its row
@@ -1020,7 +1029,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
     for (int p = 0; p < 3; ++p) {
       t.hd[p] = hd_base + p * pstride_h * hb;
       t.ml[p] = ml_base + (fm.nparty == 3 ? p : 0) * pstride_m * mb;
-      t.match[p] = (j.pair || dbg) ? Q.match[p].as<uint32_t>() : nullptr;
+      t.match[p] = (j.pair || dbg || exact_or) ? Q.match[p].as<uint32_t>() : nullptr;
     }
     t.match_w0 = j.pair ? match_w0 : 0;
     t.rp_kstride_h = ks_h;
@@ -1199,6 +1208,28 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   CK(c, cudaEventRecord(Q.ev[3], st2));
 
   // ---- per-person OR (st2), then the open on st
+  if (exact_or) {
+    OrTreeArgs oa{};
+    for (int p = 0; p < 3; ++p) oa.match[p] = Q.match[p].as<uint64_t>();
+    oa.ngroups = ngroups;
+    oa.db_lanes = membership ? S : 2ull * r * S;
+    oa.pair_base = ncols * S;
+    oa.pair_block = npairs ? 4ull * r : 0;
+    oa.lanes = oa.db_lanes + (npairs ? (uint64_t)(ngroups - 1) * 4 * r : 0);
+    for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
+    uint64_t rs[3];
+    for (int k = 0; k < 3; ++k) rs[k] = ta.msb_base[k] + (uint64_t)(2 * vw.kc - 3) * W;
+    const uint64_t words = ortree_scratch_words(ngroups, oa.lanes);
+    if (c->or_scr[0].ensure(words * 8) || c->or_scr[1].ensure(words * 8))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or tree)");
+    uint64_t* scr[2] = {c->or_scr[0].as<uint64_t>(), c->or_scr[1].as<uint64_t>()};
+    void* ph2 = prof_begin(st2);
+    launches += launch_ortree(oa, rs, scr, c->person_out.as<uint8_t>(), st2);
+    c->last_groups = ngroups;
+    prof_end(ph2, "k_ortree", st2);
+    debug_check("k_ortree", st2);
+    CK(c, cudaGetLastError());
+  } else {
   OrArgs oa{};
   oa.partial = c->partial.as<uint8_t>();
   oa.nslots = total_slots;
@@ -1217,6 +1248,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   debug_check("k_or_persons", st2);
   CK(c, cudaGetLastError());
   ++launches;
+  }
   // the open (mode 0) or the partial hand-off (mode 1) also on the threshold
   // stream, so the GEMM stream is free for the next query's chunks
   if (mode == 0) {
@@ -1377,7 +1409,7 @@ int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const 
   }
   const uint8_t* ph[3] = {in_h[0].as<uint8_t>(), in_h[1].as<uint8_t>(), in_h[2].as<uint8_t>()};
   const uint8_t* pm[3] = {in_m[0].as<uint8_t>(), in_m[1].as<uint8_t>(), in_m[2].as<uint8_t>()};
-  const uint64_t match_words = 2 * W + 1;
+  const uint64_t match_words = 2 * W + 4;  // + padding for the OR tree's 64-bit funnel reads
   for (int p = 0; p < 3; ++p) {
     if (c->match[p].ensure(match_words * 4)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (match)");
     CK(c, cudaMemsetAsync(c->match[p].p, 0, match_words * 4, st));
@@ -1455,7 +1487,7 @@ int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const 
       sg.g_off = 0;
       sg.grp_begin = 0;
       sg.gblk_begin = 0;
-      sg.slot = with_or ? (int64_t)total_slots : -1;
+      sg.slot = -1;  // the OR tree reads the match words
       const uint64_t nw = (sg.lane_end - 1) / 64 - sg.w_first + 1;
       total_slots += seg_tasks(sg.lane_begin, sg.lane_end);
       max_g = std::max<uint64_t>(max_g, 3ull * ngates * gate_row_words(nw));
@@ -1504,39 +1536,31 @@ int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const 
       launches += V == kMpcLift ? 5 : 3;
     }
   }
-  if (or_only) {
-    total_slots = ceil_div(n, 1024);
-    if (c->partial.ensure(3 * total_slots + 16)) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or slots)");
-    ThrArgs t = ta;
-    t.ntasks = total_slots;
-    t.partial = c->partial.as<uint8_t>();
-    t.nslots = total_slots;
-    t.or_elem_base = 0;
-    launch_or_bits(t, st);
-    CK(c, cudaGetLastError());
-    ++launches;
-  }
   CK(c, cudaEventRecord(c->ev[3], st));
   const bool do_or = or_only || with_or;
   if (do_or) {
-    std::vector<uint64_t> sb = {0, total_slots};
-    if (c->slot_begin.ensure(2 * sizeof(uint64_t)) || c->person_out.ensure(3 + 16) || c->open_out.ensure(16))
+    // or_tree over every lane (engine.cpp:508-512, 527-530): one group, the
+    // reference's halving tree and draws (share-exact), then the open at P1
+    if (c->person_out.ensure(3 + 16) || c->open_out.ensure(16))
       return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or buffers)");
-    CK(c, cudaMemcpyAsync(c->slot_begin.p, sb.data(), 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    OrArgs oa{};
-    oa.partial = c->partial.as<uint8_t>();
-    oa.nslots = total_slots;
-    oa.slot_begin = c->slot_begin.as<uint64_t>();
-    oa.persons = 1;
-    oa.rot = 1;
+    OrTreeArgs oa{};
+    for (int p = 0; p < 3; ++p) oa.match[p] = c->match[p].as<uint64_t>();
+    oa.ngroups = 1;
+    oa.db_lanes = n;
+    oa.lanes = n;
     for (int k = 0; k < 3; ++k) oa.key[k] = c->keys[k];
-    oa.stream = or_stream_id(octr, c->cfg.shard_rank, 2);
-    oa.out = c->person_out.as<uint8_t>();
-    launch_or_persons(oa, st);
+    uint64_t rs[3];
+    for (int k = 0; k < 3; ++k) rs[k] = or_only ? c->pos[k] : ta.msb_base[k] + (uint64_t)(2 * vw.kc - 3) * W;
+    const uint64_t words = ortree_scratch_words(1, n);
+    if (c->or_scr[0].ensure(words * 8) || c->or_scr[1].ensure(words * 8))
+      return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (or tree)");
+    uint64_t* scr[2] = {c->or_scr[0].as<uint64_t>(), c->or_scr[1].as<uint64_t>()};
+    launches += launch_ortree(oa, rs, scr, c->person_out.as<uint8_t>(), st);
+    c->last_groups = 1;
     launch_or_open(c->person_out.as<uint8_t>(), 1, 1, c->keys, or_stream_id(octr, c->cfg.shard_rank, 3),
                    c->open_out.as<uint8_t>(), st);
     CK(c, cudaGetLastError());
-    launches += 2;
+    launches += 1;
     if (opened_out) CK(c, cudaMemcpyAsync(opened_out, c->open_out.p, 1, cudaMemcpyDeviceToHost, st));
   }
   CK(c, cudaEventRecord(c->ev[4], st));
@@ -1725,7 +1749,7 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   c->shard_all.release();
   Buf* bufs[] = {&c->q_pay[0], &c->q_pay[1], &c->q_pay[2], &c->dots, &c->pair_dots, &c->segs, &c->partial,
                  &c->slot_begin, &c->person_out, &c->match[0], &c->match[1], &c->match[2], &c->open_out,
-                 &c->ml_rs, &c->diff, &c->gate, &c->bits};
+                 &c->ml_rs, &c->diff, &c->gate, &c->bits, &c->or_scr[0], &c->or_scr[1]};
   for (Buf* b : bufs) b->release();
   for (auto& f : c->fld) f.release();
   for (auto& t : c->tap_buf) t.release();
@@ -2272,7 +2296,13 @@ int irismpc_gpu_enable_taps(irismpc_gpu_ctx* c, int enable) {
 
 int irismpc_gpu_read_tap(irismpc_gpu_ctx* c, int tap, void* host_out, size_t bytes) {
   if (c && drain(c)) return IRISMPC_GPU_ERR_DEVICE;
-  if (!c || tap < 1 || tap > 7) return IRISMPC_GPU_ERR_CONFIG;
+  if (!c || tap < 1 || tap > 8) return IRISMPC_GPU_ERR_CONFIG;
+  if (tap == 8) {  // the OR tree's output components, [3][groups] in person_out
+    if (!c->person_out.p || bytes > 3ull * c->last_groups) return fail(c, IRISMPC_GPU_ERR_CONFIG, "no OR-tree output");
+    cudaSetDevice(c->cfg.device);
+    CK(c, cudaMemcpy(host_out, c->person_out.p, bytes, cudaMemcpyDeviceToHost));
+    return 0;
+  }
   if (!c->tap_buf[tap - 1].p) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap not captured");
   const size_t have = c->tap_bytes[tap - 1];
   if (bytes > have) return fail(c, IRISMPC_GPU_ERR_CONFIG, "tap read larger than captured");

@@ -253,6 +253,29 @@ void launch_or_persons(const OrArgs& a, cudaStream_t st);
 void launch_or_open(const uint8_t* partials, uint32_t G, uint32_t persons, const SeedKey key[3],
                     uint64_t stream, uint8_t* match_out, cudaStream_t st);
 
+// Share-exact OR tree (ortree.cu): or_tree_batch over the reference's groups
+struct OrTreeArgs {
+  const uint64_t* match[3];  // lane bits in reference lane order, 64-lane words (+1 word of padding)
+  uint32_t ngroups;          // persons, or 1 (membership / comparison: every lane)
+  uint64_t db_lanes;         // group g's DB lanes: [g * db_lanes, (g + 1) * db_lanes)
+  uint64_t pair_base;        // global lane of pair lane 0
+  uint64_t pair_block;       // lanes per person pair (4 r), 0: no pair lanes
+  uint64_t lanes;            // lanes per group = db_lanes + (ngroups - 1) * pair_block
+  SeedKey key[3];
+};
+struct OrTreeLevel {
+  uint64_t na, nb, wo, win;  // folded / AND lanes, out / in row strides (words)
+  const uint64_t* in[3];
+  uint64_t* out[3];
+  uint64_t rand_base[3];     // stream element of group 0's first gate word, per seed
+};
+// u64 words of one ping-pong scratch buffer
+uint64_t ortree_scratch_words(uint32_t ngroups, uint64_t lanes);
+// all levels from the seed positions rand_start (the draws right after the msb
+// gates), then lane 0 of every group -> out[3][ngroups]; returns launches
+int launch_ortree(const OrTreeArgs& a, const uint64_t rand_start[3], uint64_t* scratch[2], uint8_t* out,
+                  cudaStream_t st);
+
 // ChaCha stream ids of the OR-reduction gates (the reference's own draws all use
 // stream 0, prf.hpp:46-69): bit 63 set, a per-context 64-bit query counter
 // (never reused on a persistent context), the shard rank and the kind

@@ -1,0 +1,188 @@
+// K5 (share-exact): the reference's halving OR tree over each person's lanes,
+// or_tree_batch (include/irismpc/circuits.hpp:387-434) with and_layer's AND
+// gates (circuits.hpp:92-131) and the reference's PRF draws (SURVEY.md A.3:
+// per level, per group in order, one gate of nb lanes = ceil(nb/64) words of
+// every seed stream, right after the msb gates).  So the aggregate shares
+// equal the reference's share for share, not only the opened bit.
+//
+// Groups (Schedule::groups, src/engine.cpp:221-289): group g lists its DB lanes
+// (codes 2g, 2g+1, all rotations, all rows: one contiguous lane range) then its
+// inner-batch pair lanes (pairs (i, g), i < g, then (g, j), j > g, 4r lanes
+// each); membership / comparison: one group of every lane.  Level t folds a row
+// of N lanes into na = ceil(N/2): lo = lanes [0, na), hi = lanes [na, N),
+// out = lo ^ hi ^ AND(lo, hi) with the AND masked to nb = N - na lanes.
+//
+// Layout: level 0 reads the lane bits in reference lane order (the msb
+// kernels' match words, 64-lane little-endian words); every level writes
+// compact rows [comp][group][ceil(na/64)] into one of two ping-pong buffers.
+// Thread = 8 consecutive output words of one group: 2 ChaCha12 blocks per seed
+// cover its 8 gate words.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace irisgpu {
+
+namespace {
+
+__device__ __forceinline__ uint64_t funnel(const uint64_t* w, uint64_t bit) {
+  const uint64_t i = bit / 64;
+  const int sh = (int)(bit % 64);
+  return sh ? (w[i] >> sh) | (w[i + 1] << (64 - sh)) : w[i];
+}
+
+__device__ __forceinline__ uint64_t lane_mask(int64_t live) {
+  return live >= 64 ? ~0ull : (live <= 0 ? 0ull : (1ull << live) - 1);
+}
+
+// global lane of position i of group g's lane list
+__device__ __forceinline__ uint64_t group_lane(const OrTreeArgs& A, uint32_t g, uint64_t i) {
+  if (i < A.db_lanes) return (uint64_t)g * A.db_lanes + i;
+  const uint64_t q = (i - A.db_lanes) / A.pair_block, o = (i - A.db_lanes) % A.pair_block;
+  const uint32_t a = q < g ? (uint32_t)q : g, b = q < g ? g : (uint32_t)q + 1;
+  const uint64_t pidx = (uint64_t)a * A.ngroups - (uint64_t)a * (a + 1) / 2 + (b - a - 1);
+  return A.pair_base + pidx * A.pair_block + o;
+}
+
+// 64 list positions [i, i + 64) of group g, component c, from the lane bits
+// (positions >= lanes read as 0 or garbage; the callers mask them)
+__device__ __forceinline__ uint64_t list64(const OrTreeArgs& A, int c, uint32_t g, uint64_t i) {
+  const uint64_t* m = A.match[c];
+  if (i + 64 <= A.db_lanes) return funnel(m, (uint64_t)g * A.db_lanes + i);
+  if (i >= A.db_lanes && A.pair_block) {
+    const uint64_t o = (i - A.db_lanes) % A.pair_block;
+    if (o + 64 <= A.pair_block) return funnel(m, group_lane(A, g, i));
+  }
+  uint64_t v = 0;
+  for (int b = 0; b < 64; ++b) {
+    const uint64_t pos = i + b;
+    if (pos >= A.lanes) break;
+    const uint64_t ln = group_lane(A, g, pos);
+    v |= ((m[ln / 64] >> (ln % 64)) & 1ull) << b;
+  }
+  return v;
+}
+
+}  // namespace
+
+// One level of every group.  L0: the source is the lane bits via the group
+// lists; else the previous level's compact rows (stride win words).
+template <bool L0>
+__global__ void __launch_bounds__(128) k_ortree_level(const __grid_constant__ OrTreeArgs A, OrTreeLevel L) {
+  const uint64_t wout = (L.na + 63) / 64, per = (wout + 7) / 8;
+  const uint64_t id = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (id >= (uint64_t)A.ngroups * per) return;
+  const uint32_t g = (uint32_t)(id / per);
+  const uint64_t w0 = (id % per) * 8;
+  const uint64_t nbw = (L.nb + 63) / 64;
+  // gate words w0 .. w0 + 7 of group g: seed k's stream elements e0 + w
+  uint64_t f[3][8];
+  if (w0 < nbw) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t e0 = L.rand_base[k] + (uint64_t)g * nbw + w0;
+      uint32_t blk[16];
+      chacha12_block(A.key[k], e0 / 8, 0, blk);
+      const int r = (int)(e0 % 8);
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        if (w + r < 8) f[k][w] = chacha_word(blk, w + r);
+      if (r) {
+        chacha12_block(A.key[k], e0 / 8 + 1, 0, blk);
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          if (w + r >= 8) f[k][w] = chacha_word(blk, w + r - 8);
+      }
+    }
+  }
+  for (int w = 0; w < 8; ++w) {
+    const uint64_t wi = w0 + w;
+    if (wi >= wout) break;
+    const uint64_t ml = lane_mask((int64_t)L.na - 64 * (int64_t)wi);
+    const uint64_t mh = lane_mask((int64_t)L.nb - 64 * (int64_t)wi);
+    uint64_t lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (L0) {
+        lo[c] = list64(A, c, g, 64 * wi) & ml;
+        hi[c] = mh ? list64(A, c, g, L.na + 64 * wi) & mh : 0ull;
+      } else {
+        const uint64_t* row = L.in[c] + (uint64_t)g * L.win;
+        lo[c] = row[wi] & ml;
+        hi[c] = mh ? funnel(row, L.na + 64 * wi) & mh : 0ull;
+      }
+    }
+    uint64_t z[3] = {0, 0, 0};
+    if (wi < nbw) {
+      // z_p = x_p y_p ^ x_{p-1} y_p ^ x_p y_{p-1} ^ F_p ^ F_{p-1}, dead lanes zeroed (mask_lanes)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const int q = (p + 2) % 3;
+        z[p] = ((lo[p] & hi[p]) ^ (lo[q] & hi[p]) ^ (lo[p] & hi[q]) ^ f[p][w] ^ f[q][w]) & mh;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) L.out[c][(uint64_t)g * L.wo + wi] = lo[c] ^ hi[c] ^ z[c];
+  }
+}
+
+// lane 0 of every group's final row -> out[comp][group]
+template <bool L0>
+__global__ void k_ortree_out(const __grid_constant__ OrTreeArgs A, const uint64_t* r0, const uint64_t* r1,
+                             const uint64_t* r2, uint64_t win, uint8_t* out) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= A.ngroups) return;
+  const uint64_t* rows[3] = {r0, r1, r2};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const uint64_t v = L0 ? list64(A, c, g, 0) : rows[c][(uint64_t)g * win];
+    out[(uint64_t)c * A.ngroups + g] = A.lanes ? (uint8_t)(v & 1ull) : 0;
+  }
+}
+
+uint64_t ortree_scratch_words(uint32_t ngroups, uint64_t lanes) {
+  const uint64_t na = (lanes + 1) / 2;
+  return 3ull * ngroups * ((na + 63) / 64) + 8;
+}
+
+int launch_ortree(const OrTreeArgs& a, const uint64_t rand_start[3], uint64_t* scratch[2], uint8_t* out,
+                  cudaStream_t st) {
+  if (!a.ngroups) return 0;
+  int launches = 0;
+  uint64_t N = a.lanes, win = 0, base[3] = {rand_start[0], rand_start[1], rand_start[2]};
+  int cur = -1;  // -1: the lane bits
+  const uint64_t comp_stride = ortree_scratch_words(a.ngroups, a.lanes) / 3;
+  while (N > 1) {
+    OrTreeLevel L{};
+    L.na = (N + 1) / 2;
+    L.nb = N - L.na;
+    L.wo = (L.na + 63) / 64;
+    L.win = win;
+    const int nxt = cur == 0 ? 1 : 0;
+    for (int c = 0; c < 3; ++c) {
+      L.out[c] = scratch[nxt] + c * comp_stride;
+      L.in[c] = cur < 0 ? nullptr : scratch[cur] + c * comp_stride;
+    }
+    for (int k = 0; k < 3; ++k) L.rand_base[k] = base[k];
+    const uint64_t threads = (uint64_t)a.ngroups * ((L.wo + 7) / 8);
+    const unsigned blocks = (unsigned)((threads + 127) / 128);
+    if (cur < 0)
+      k_ortree_level<true><<<blocks, 128, 0, st>>>(a, L);
+    else
+      k_ortree_level<false><<<blocks, 128, 0, st>>>(a, L);
+    ++launches;
+    const uint64_t nbw = (L.nb + 63) / 64;
+    for (int k = 0; k < 3; ++k) base[k] += (uint64_t)a.ngroups * nbw;
+    N = L.na;
+    win = L.wo;
+    cur = nxt;
+  }
+  const unsigned ob = (a.ngroups + 127) / 128;
+  if (cur < 0)
+    k_ortree_out<true><<<ob, 128, 0, st>>>(a, nullptr, nullptr, nullptr, 0, out);
+  else
+    k_ortree_out<false><<<ob, 128, 0, st>>>(a, scratch[cur], scratch[cur] + comp_stride,
+                                             scratch[cur] + 2 * comp_stride, win, out);
+  return launches + 1;
+}
+
+}  // namespace irisgpu

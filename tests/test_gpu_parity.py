@@ -93,6 +93,7 @@ def test_shares_through_msb_match_oracle(be, l, s, persons, r, seed):
         np.testing.assert_array_equal(taps[k], getattr(ref, k), err_msg=k)
     np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
     np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)  # OR-tree shares
     np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
     # L3: reconstructed distances equal the plaintext ones
     rec_ml = taps["rs_ml"].astype(np.uint32).sum(0) & 0xFFFF
@@ -123,6 +124,7 @@ def test_variant_shares_through_msb_match_oracle(var, be, l, s, persons, r, seed
         np.testing.assert_array_equal(taps["dot_ml"], ref.public_ml)
     np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
     np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)
     np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
     st = sess.last_stats
     for p in range(3):
@@ -487,6 +489,7 @@ def test_streaming_queries_match_synchronous(be, var, s):
         assert got[i].any()
         pos = ref.stream_pos
     np.testing.assert_array_equal(sess.stream_positions(), pos)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)  # the last query's OR tree
 
 
 def test_streaming_queries_multi_chunk():

@@ -1,11 +1,11 @@
-// K5: bucketed MPC OR-reduction to one shared bit per person, and the open.
-//
-// Replaces the lane gather + or_tree_batch (src/engine.cpp:376-387,
-// include/irismpc/circuits.hpp:387-434) and open_bits_to(P1)
-// (circuits.hpp:449-486).  x OR y = x ^ y ^ (x AND y), every AND a 3-party
-// gate with fresh zero-shared randomness.  The tree shape differs from the
-// reference's halving tree (buckets per warp task, per person, per GPU), so
-// the post-MSB shares differ while the opened bit is identical.  Partial
+// K5 for DB-sharded queries: bucketed MPC OR-reduction to one shared bit per
+// person per shard, the cross-shard OR, and the open at P1 (open_bits_to,
+// circuits.hpp:449-486; k_or_open also opens the share-exact tree of
+// ortree.cu, which every unsharded query uses).  x OR y = x ^ y ^ (x AND y),
+// every AND a 3-party gate with fresh zero-shared randomness from its own
+// ChaCha stream ids (or_stream_id).  The reference has no sharded query, so
+// this tree shape (buckets per warp task, per person, per shard) has no
+// reference shares to match; the opened bit is the same OR.  Partial
 // aggregates are never opened (OpenAudit semantics, rep3.hpp:131-134).
 #include "common.cuh"
 #include "kernels.h"

@@ -35,7 +35,9 @@
 //   k_inject          bit_inject<15>, <16>, const-lifted into diff (tile /
 //                     lane-major, as k_reshare)
 //   k_msb             bit-sliced: share_split of diff + the 31-bit adder ->
-//                     match-bit shares, fused first MPC-OR level per warp
+//                     match-bit shares (the match words the OR tree of
+//                     ortree.cu reads); DB-sharded queries: fused first
+//                     bucketed MPC-OR level per warp instead
 #include <cstdlib>
 #include <string>
 #include <type_traits>

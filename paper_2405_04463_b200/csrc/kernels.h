@@ -226,8 +226,6 @@ void launch_parse_lane_shares(const uint8_t* const p[3], uint64_t lanes, int wid
                               cudaStream_t st);
 void launch_parse_bit_shares(const uint8_t* const p[3], uint64_t words, uint64_t lanes, uint32_t* out, int* bad,
                              cudaStream_t st);
-// OR of the component bit words a.match[3] (a.n lanes) into a.ntasks partial slots
-void launch_or_bits(const ThrArgs& a, cudaStream_t st);
 // L1 tap of an RP field's chunk: out[p * n + col * S + row0 + row] = P2 + P(1|3) of (col, row)
 // row-sampled L1 tap (irismpc_gpu_tap_rows): out[p * out_pstride + col * k + i]
 void launch_tap_rows(const void* P, int elem_bytes, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,

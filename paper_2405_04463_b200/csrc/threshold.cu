@@ -780,28 +780,6 @@ void launch_parse_bit_shares(const uint8_t* const p[3], uint64_t words, uint64_t
   k_parse_bit_shares<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(p[0], p[1], p[2], words, lanes, out, bad);
 }
 
-// OR of shared bits already in component words (A.match[c], 32 lanes per word):
-// warp -> 1024-lane task, the fused warp OR of k_msb into partial slot `task`
-__global__ void __launch_bounds__(128) k_or_bits(const __grid_constant__ ThrArgs A) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t task = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (task >= A.ntasks) return;
-  const uint64_t wi = task * 32 + lane;
-  uint32_t bit[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) bit[c] = wi * 32 < A.n ? A.match[c][wi] : 0u;
-  Seg sg{};
-  sg.slot = 0;
-  sg.task_begin = 0;
-  __shared__ uint64_t orr[4][3][40];
-  fused_or(A, sg, task, bit, lane, orr[threadIdx.x >> 5]);
-}
-
-void launch_or_bits(const ThrArgs& a, cudaStream_t st) {
-  if (!a.ntasks) return;
-  k_or_bits<<<(unsigned)((a.ntasks + 3) / 4), 128, 0, st>>>(a);
-}
-
 template <typename T>
 __global__ void k_rp_tap(const T* __restrict__ P, uint32_t nparty, uint64_t ncols, uint32_t rot, uint64_t nr,
                          uint64_t kstride, T* __restrict__ out, uint64_t n, uint64_t S, uint64_t row0) {

@@ -75,6 +75,38 @@ def test_sharded_batch_query_matches_oracle(be, var, G, splits):
     np.testing.assert_array_equal(outs[0], ref.person_match)
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_sharded_contexts_on_two_devices_one_process():
+    """Two shard contexts on different GPUs of one process (per-device GEMM
+    attribute / SM-count state, cross-device gather over UVA) and a plain
+    single-GPU context on device 1 afterwards."""
+    be, var, l, s, persons, seed = O.SHAMIR, P.MPC_LIFT, 12800, 600, 2, 47
+    rng = O.Rng(seed)
+    dc, dm = O.records(rng, l, s, 0.9)
+    qc, qm = O.records(rng, l, 2 * persons, 0.9)
+    qc[1], qm[1] = dc[450], dm[450]
+    db = O.deal(be, l, dc, dm, O.Rng(sub=(seed, 1)), variant=var)
+    q = O.deal(be, l, qc, qm, O.Rng(sub=(seed, 2)), variant=var)
+    rec = O.record_bytes(be, l, var)
+    cfg = P.EngineConfig(backend=be, l=l, variant=var)
+    group = P.ShardGroup(2)
+    shards = []
+    for r, (r0, r1) in enumerate([(0, 300), (300, s)]):
+        sh = P.Session(cfg, master_seed=seed, device=r, shard_rank=r, db_rows_total=s, db_row_offset=r0)
+        sh.load_db([x[r0 * rec:r1 * rec] for x in db], r1 - r0)
+        sh.shard_attach_inproc(group)
+        shards.append(sh)
+    qlen = [len(x) for x in q]
+    outs = _run_threads([(lambda r=r: shards[r].sharded_batch_query(q if r == 0 else None, persons, qlen))
+                         for r in range(2)])
+    ref = O.run_local(O.make_config(be, l, variant=var), seed, dc, dm, qc, qm, persons)
+    np.testing.assert_array_equal(outs[0], ref.person_match)
+    assert outs[0][0] == 1
+    m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, device=1)
+    np.testing.assert_array_equal(m, ref.person_match)
+    np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)
+
+
 def test_sharded_requires_attach_and_total_rows():
     cfg = P.EngineConfig(backend=P.SHAMIR, l=256, rotations=5)
     sh = P.Session(cfg, master_seed=1, shard_rank=1, db_rows_total=0)

@@ -62,17 +62,13 @@ __device__ __forceinline__ uint64_t list64(const OrTreeArgs& A, int c, uint32_t 
   return v;
 }
 
-}  // namespace
-
-// One level of every group.  L0: the source is the lane bits via the group
-// lists; else the previous level's compact rows (stride win words).
+// Output words w0 .. w0 + 7 of group g at level L.  L0: the source is the lane
+// bits via the group lists; else the previous level's compact rows (stride win,
+// row gi).  Output row go (stride wo).
 template <bool L0>
-__global__ void __launch_bounds__(128) k_ortree_level(const __grid_constant__ OrTreeArgs A, OrTreeLevel L) {
-  const uint64_t wout = (L.na + 63) / 64, per = (wout + 7) / 8;
-  const uint64_t id = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (id >= (uint64_t)A.ngroups * per) return;
-  const uint32_t g = (uint32_t)(id / per);
-  const uint64_t w0 = (id % per) * 8;
+__device__ __forceinline__ void level_words(const OrTreeArgs& A, const OrTreeLevel& L, uint32_t g, uint64_t w0,
+                                            uint64_t gi, uint64_t go) {
+  const uint64_t wout = (L.na + 63) / 64;
   const uint64_t nbw = (L.nb + 63) / 64;
   // gate words w0 .. w0 + 7 of group g: seed k's stream elements e0 + w
   uint64_t f[3][8];
@@ -106,7 +102,7 @@ __global__ void __launch_bounds__(128) k_ortree_level(const __grid_constant__ Or
         lo[c] = list64(A, c, g, 64 * wi) & ml;
         hi[c] = mh ? list64(A, c, g, L.na + 64 * wi) & mh : 0ull;
       } else {
-        const uint64_t* row = L.in[c] + (uint64_t)g * L.win;
+        const uint64_t* row = L.in[c] + gi * L.win;
         lo[c] = row[wi] & ml;
         hi[c] = mh ? funnel(row, L.na + 64 * wi) & mh : 0ull;
       }
@@ -121,22 +117,71 @@ __global__ void __launch_bounds__(128) k_ortree_level(const __grid_constant__ Or
       }
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) L.out[c][(uint64_t)g * L.wo + wi] = lo[c] ^ hi[c] ^ z[c];
+    for (int c = 0; c < 3; ++c) L.out[c][go * L.wo + wi] = lo[c] ^ hi[c] ^ z[c];
   }
 }
 
-// lane 0 of every group's final row -> out[comp][group]
+}  // namespace
+
+// One level of every group, thread = 8 output words of one group.
 template <bool L0>
-__global__ void k_ortree_out(const __grid_constant__ OrTreeArgs A, const uint64_t* r0, const uint64_t* r1,
-                             const uint64_t* r2, uint64_t win, uint8_t* out) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= A.ngroups) return;
-  const uint64_t* rows[3] = {r0, r1, r2};
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const uint64_t v = L0 ? list64(A, c, g, 0) : rows[c][(uint64_t)g * win];
-    out[(uint64_t)c * A.ngroups + g] = A.lanes ? (uint8_t)(v & 1ull) : 0;
+__global__ void __launch_bounds__(128) k_ortree_level(const __grid_constant__ OrTreeArgs A, OrTreeLevel L) {
+  const uint64_t per = ((L.na + 63) / 64 + 7) / 8;
+  const uint64_t id = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (id >= (uint64_t)A.ngroups * per) return;
+  const uint32_t g = (uint32_t)(id / per);
+  level_words<L0>(A, L, g, (id % per) * 8, g, g);
+}
+
+namespace {
+constexpr uint64_t kTailWords = 960;  // a row of at most this many output words runs in k_ortree_tail
+constexpr int kTailThreads = 128;     // 8 words per thread: one pass per level
+}  // namespace
+
+// The remaining levels once a group's row fits one CTA pass: CTA = group, the
+// rows in shared memory (ping-pong), levels separated by __syncthreads, then
+// lane 0 -> out[comp][group].  L is the first of these levels, reading the
+// global rows (or the lane bits); its rand_base is group 0's and every level
+// advances it by ngroups x ceil(nb/64).
+template <bool L0>
+__global__ void __launch_bounds__(kTailThreads) k_ortree_tail(const __grid_constant__ OrTreeArgs A, OrTreeLevel L,
+                                                              uint8_t* out) {
+  __shared__ uint64_t rows[2][3][kTailWords + 8];
+  const uint32_t g = blockIdx.x;
+  uint64_t N = L.na + L.nb;
+  int cur = -1;  // -1: the global input of the first level
+  while (N > 1) {
+    const int nxt = cur == 0 ? 1 : 0;
+    for (int c = 0; c < 3; ++c) L.out[c] = rows[nxt][c];
+    const uint64_t wout = (L.na + 63) / 64;
+    for (uint64_t w0 = 8ull * threadIdx.x; w0 < wout; w0 += 8ull * blockDim.x) {
+      if (cur < 0)
+        level_words<L0>(A, L, g, w0, g, 0);
+      else
+        level_words<false>(A, L, g, w0, 0, 0);
+    }
+    __syncthreads();
+    const uint64_t nbw = (L.nb + 63) / 64;
+    for (int k = 0; k < 3; ++k) L.rand_base[k] += (uint64_t)A.ngroups * nbw;
+    N = L.na;
+    cur = nxt;
+    L.na = (N + 1) / 2;
+    L.nb = N - L.na;
+    L.win = L.wo;
+    L.wo = (L.na + 63) / 64;
+    for (int c = 0; c < 3; ++c) L.in[c] = rows[cur][c];
   }
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 3; ++c) {
+      uint64_t v;
+      if (cur >= 0)
+        v = rows[cur][c][0];
+      else if (L0)
+        v = list64(A, c, g, 0);
+      else
+        v = L.in[c][(uint64_t)g * L.win];
+      out[(uint64_t)c * A.ngroups + g] = A.lanes ? (uint8_t)(v & 1ull) : 0;
+    }
 }
 
 uint64_t ortree_scratch_words(uint32_t ngroups, uint64_t lanes) {
@@ -151,7 +196,7 @@ int launch_ortree(const OrTreeArgs& a, const uint64_t rand_start[3], uint64_t* s
   uint64_t N = a.lanes, win = 0, base[3] = {rand_start[0], rand_start[1], rand_start[2]};
   int cur = -1;  // -1: the lane bits
   const uint64_t comp_stride = ortree_scratch_words(a.ngroups, a.lanes) / 3;
-  while (N > 1) {
+  while (true) {
     OrTreeLevel L{};
     L.na = (N + 1) / 2;
     L.nb = N - L.na;
@@ -163,6 +208,13 @@ int launch_ortree(const OrTreeArgs& a, const uint64_t rand_start[3], uint64_t* s
       L.in[c] = cur < 0 ? nullptr : scratch[cur] + c * comp_stride;
     }
     for (int k = 0; k < 3; ++k) L.rand_base[k] = base[k];
+    if (N <= 1 || L.wo <= kTailWords) {  // the rest (possibly no level at all) in one launch
+      if (cur < 0)
+        k_ortree_tail<true><<<a.ngroups, kTailThreads, 0, st>>>(a, L, out);
+      else
+        k_ortree_tail<false><<<a.ngroups, kTailThreads, 0, st>>>(a, L, out);
+      return launches + 1;
+    }
     const uint64_t threads = (uint64_t)a.ngroups * ((L.wo + 7) / 8);
     const unsigned blocks = (unsigned)((threads + 127) / 128);
     if (cur < 0)
@@ -176,13 +228,6 @@ int launch_ortree(const OrTreeArgs& a, const uint64_t rand_start[3], uint64_t* s
     win = L.wo;
     cur = nxt;
   }
-  const unsigned ob = (a.ngroups + 127) / 128;
-  if (cur < 0)
-    k_ortree_out<true><<<ob, 128, 0, st>>>(a, nullptr, nullptr, nullptr, 0, out);
-  else
-    k_ortree_out<false><<<ob, 128, 0, st>>>(a, scratch[cur], scratch[cur] + comp_stride,
-                                             scratch[cur] + 2 * comp_stride, win, out);
-  return launches + 1;
 }
 
 }  // namespace irisgpu

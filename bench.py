@@ -32,7 +32,7 @@ L = 12800
 ROT = 31
 PERSONS = 32              # 64 eye codes (configs[2]; configs[1] = --persons 16 --rows 100000)
 ROWS_PER_GPU = 1_000_000  # configs[2]
-REF_ROWS = 10_000         # configs[0]: 1 person (2 codes) x 31 rotations vs 10k rows, the CPU-runnable case
+REF_ROWS = 1_000          # CPU reference sample: the arm's batch (32 persons) x 31 rotations vs 1000 rows
 CPU_STEPS = 5
 METRIC = "iris comparisons/sec (query x rotation x DB)"
 UNIT = "comparisons/s"
@@ -75,6 +75,23 @@ def workload_name(rows: int, persons: int, world: int) -> str:
     if world > 1 and persons == 32:
         return f"configs[3] weak-scaling series ({rows} rows per GPU x {world} GPUs = {rows * world} rows)"
     return "custom shape"
+
+
+def arm_config(args, world: int, rows: int, persons: int) -> dict:
+    """The bench line's `config` (both arms print the same one: the reference
+    arm times a bounded sample of this workload)."""
+    S = rows * world
+    kh, km = WIDTHS[VARIANTS[args.variant]]
+    plane_kb = L * (3 * kh // 8 + (3 * km // 8 if km else 1)) / 1e3
+    wl = workload_name(rows, persons, world)
+    return {"workload": f"{wl}: {2 * persons} query codes ({persons} persons) x {ROT} rotations vs "
+                        f"{rows} DB rows per GPU (total {S}), l={L}, 3-party {args.variant}, "
+                        f"{args.backend} backend", "l": L, "rotations": ROT, "persons": persons,
+            "codes": 2 * persons, "db_rows_total": S, "db_rows_per_gpu": rows, "backend": args.backend,
+            "variant": args.variant,
+            "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM, "
+                  f"{plane_kb * rows / 1e6:.1f} GB per GPU)",
+            "parallelism": f"db-shard x{world}"}
 
 
 def env_rank():
@@ -232,9 +249,10 @@ def cpu_reference_rates(backends, rows: int, persons: int, steps: int, variant: 
         out[be] = {"value": 2 * persons * ROT * rows / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
                    "ms": ms, "planted_match": int(m0.value),
                    "sample": f"reference run_parties + party_batch_query (oracle/_ref, OpenMP parallel_dot, all "
-                             f"{cores} host threads), {name} backend, {2 * persons} codes x {ROT} rot x {rows} rows "
-                             f"(configs[0] shape), median of {len(times)} steps of QueryStats.wall_ms = {ms:.0f} ms; "
-                             f"linear in rows"}
+                             f"{cores} host threads), {name} backend, {2 * persons} codes ({persons} persons) x {ROT} "
+                             f"rot x {rows} rows (+ the batch's inner pair lanes), median of {len(times)} steps of "
+                             f"QueryStats.wall_ms = {ms:.0f} ms; comparisons/s counts DB lanes only and is linear in "
+                             f"rows"}
     return out
 
 
@@ -242,18 +260,18 @@ def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
+    world = max(world, args.gpus)
     backend = 1 if args.backend == "shamir" else 0
-    rows = args.ref_rows
     variant = VARIANTS[args.variant]
-    res = cpu_reference_rates([backend], rows, 1, max(1, args.steps), variant, warmup=args.warmup)[backend]
-    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    # each step: the arm's batch (same persons, codes, rotations, l, variant, backend) against a
+    # bounded sample of the DB rows; the line carries the GPU arm's config (the workload sampled)
+    res = cpu_reference_rates([backend], args.ref_rows, args.persons, max(1, args.steps), variant,
+                              warmup=args.warmup)[backend]
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"configs[0]: 1 person (2 codes) x {ROT} rot x {rows} rows, l={L}, "
-                                   f"3-party {args.variant}, {args.backend} backend (the reference's CPU-runnable "
-                                   f"config; comparisons/s is linear in rows)", "l": L, "rotations": ROT,
-                       "variant": args.variant, "backend": args.backend, "db_rows": rows, "persons": 1},
+            "config": arm_config(args, world, args.rows, args.persons),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -522,8 +540,6 @@ def main_gpu(args):
         peaks, src = load_peaks()
         gemm_ms = stats_acc["gemm_ms"] / max(1, stats_acc["gemm_launches"])
         opl = ops_per_lane(backend, variant)
-        kh, km = WIDTHS[variant]
-        plane_kb = L * (3 * kh // 8 + (3 * km // 8 if km else 1)) / 1e3
         launches_per_step = max(1, stats_acc["gemm_launches"] // args.steps)
         exec_ops_launch = stats_acc["gemm_ops"] / max(1, stats_acc["gemm_launches"])
         exec_tops = exec_ops_launch / (gemm_ms / 1e3) / 1e12
@@ -542,21 +558,13 @@ def main_gpu(args):
         sg_n = sum(v[1] for v in serial_gemm.values())
         cpu = None
         if world == 1 and not args.no_cpu:
-            cpu = cpu_reference_rates([backend, 1 - backend], args.ref_rows, 1, CPU_STEPS, variant)
-        wl = workload_name(rows, persons, world)
+            cpu = cpu_reference_rates([backend, 1 - backend], args.ref_rows, persons, CPU_STEPS, variant)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{wl}: {ncodes} query codes ({persons} persons) x {ROT} rotations vs "
-                                   f"{rows} DB rows per GPU (total {S}), l={L}, 3-party {args.variant}, "
-                                   f"{args.backend} backend", "l": L, "rotations": ROT, "persons": persons,
-                       "codes": ncodes, "db_rows_total": S, "db_rows_per_gpu": rows, "backend": args.backend,
-                       "variant": args.variant,
-                       "l2": f"inputs larger than L2 (DB limb planes {plane_kb:.1f} KB/row resident in HBM, "
-                             f"{plane_kb * rows / 1e6:.1f} GB per GPU)",
-                       "parallelism": f"db-shard x{world}",
-                       "query_api": "streaming submit/wait (2 in flight)" if streaming else "synchronous"},
+            "config": arm_config(args, world, args.rows, persons),
+            "query_api": "streaming submit/wait (2 in flight)" if streaming else "synchronous",
             "e2e": {"value": lanes_db / (float(e2e.item()) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": 3 * ncodes * sess.rec, "d2h_bytes_per_step": persons,
                     "note": e2e_note},

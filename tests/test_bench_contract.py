@@ -90,4 +90,17 @@ def test_workload_labels_name_baseline_configs():
     assert b.workload_name(10_000, 1, 1) == "configs[0]"
     assert b.workload_name(1_000_000, 32, 4).startswith("configs[3]")
     assert b.workload_name(5_000, 3, 1) == "custom shape"
-    assert b.ROWS_PER_GPU == 1_000_000 and b.PERSONS == 32 and b.REF_ROWS == 10_000
+    assert b.ROWS_PER_GPU == 1_000_000 and b.PERSONS == 32 and b.REF_ROWS == 1_000
+
+
+def test_both_arms_print_the_same_config():
+    """--impl reference times a bounded row sample of the GPU arm's workload and
+    prints the GPU arm's config, so the driver compares like with like."""
+    import argparse
+    b = _bench()
+    args = argparse.Namespace(variant="mpc-lift", backend="shamir", rows=1_000_000, persons=32)
+    c = b.arm_config(args, 1, 1_000_000, 32)
+    assert c["workload"].startswith("configs[2]") and c["codes"] == 64 and c["db_rows_total"] == 1_000_000
+    assert "153.6 KB/row" in c["l2"]
+    src = open(b.__file__).read()
+    assert src.count("\"config\": arm_config(args, world, args.rows") == 2  # the GPU arm and the reference arm

@@ -91,6 +91,8 @@ def test_gpu_or_tree_only_shares_equal_reference(n):
     (O.SHAMIR, 1, 256, 777, 1, 7, False),      # one person: no pair lanes
     (O.SHAMIR, 2, 256, 4099, 1, 1, True),      # membership: one group of every row
     (O.REPLICATED, 1, 128, 1, 1, 1, True),     # one lane
+    (O.SHAMIR, 1, 128, 50, 40, 3, False),      # 40 persons: pair lanes dominate, many pair blocks per group
+    (O.REPLICATED, 2, 64, 100, 9, 31, False),  # pair blocks of 124 lanes straddling 64-lane words
 ])
 def test_gpu_batch_query_or_tree_shares_equal_oracle(be, var, l, s, persons, r, membership):
     """The batch query's aggregate components (groups = Schedule::groups,

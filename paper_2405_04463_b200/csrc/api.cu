@@ -593,6 +593,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   const uint32_t ngates = nlift + 2u * vw.kc - 3u;
   const uint32_t ngroups = membership ? 1u : persons;
   c->query_id++;
+  c->last_groups = 0;  // the AGG tap is valid only after this call's share-exact OR tree
   const uint64_t octr = ++c->or_ctr;  // fresh OR-gate streams for this query
   const uint32_t rank = c->cfg.shard_rank;
   const uint64_t s_loc = c->s;
@@ -1468,6 +1469,7 @@ int run_compare(irismpc_gpu_ctx* c, int mode, const uint8_t* const hd[3], const 
   ta.coef = 1.0 - 2.0 * c->cfg.match_ratio;
   const uint64_t octr = ++c->or_ctr;
   c->query_id++;
+  c->last_groups = 0;  // the AGG tap is valid only after this call's share-exact OR tree
   ta.or_stream = or_stream_id(octr, c->cfg.shard_rank, 1);
   for (int p = 0; p < 3; ++p) ta.match[p] = c->match[p].as<uint32_t>();
   ta.match_w0 = 0;

@@ -38,6 +38,7 @@
 //                     match-bit shares (the match words the OR tree of
 //                     ortree.cu reads); DB-sharded queries: fused first
 //                     bucketed MPC-OR level per warp instead
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -856,9 +857,15 @@ void launch_threshold_back(const ThrArgs& a, cudaStream_t st) { launch_threshold
 
 void launch_threshold_part(const ThrArgs& a, cudaStream_t st, int parts) {
   if (!a.ntasks) return;
-  // leave-one-out timing hook (results are WRONG with it): IRISMPC_SKIP_KERNELS=keystream,reshare,lift,inject,msb
+  // leave-one-out timing hook (results are WRONG with it, so it also needs
+  // IRISMPC_TIMING_ONLY=1): IRISMPC_SKIP_KERNELS=keystream,reshare,lift,inject,msb
   static const std::string skip = [] {
     const char* e = std::getenv("IRISMPC_SKIP_KERNELS");
+    const char* ok = std::getenv("IRISMPC_TIMING_ONLY");
+    if (e && !(ok && ok[0] == '1')) {
+      std::fprintf(stderr, "irismpc: IRISMPC_SKIP_KERNELS ignored (set IRISMPC_TIMING_ONLY=1 to accept wrong results)\n");
+      return std::string();
+    }
     return e ? std::string(",") + e + "," : std::string();
   }();
   auto on = [&](const char* k) { return skip.empty() || skip.find(std::string(",") + k + ",") == std::string::npos; };

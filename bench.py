@@ -606,6 +606,11 @@ def main_gpu(args):
                          "note": "GEMM (stream 1) and threshold (stream 2) overlap; the span is the "
                                  "threshold stream's first-start to last-end time of the last step"},
             "planted_match": planted, "setup_s": setup_s,
+            # one GPU here does all three parties' work, so x3 is the per-party-box
+            # rate the paper quotes (4.29e9 cmp/s for 3 x 8 H100)
+            "party_work_rate": {"value": 3 * value, "unit": UNIT,
+                                "paper_per_party_box": 4.29e9,
+                                "note": "3 x value: the work of three party boxes on these GPUs"},
         }
         if cpu is not None:
             c0 = cpu[backend]

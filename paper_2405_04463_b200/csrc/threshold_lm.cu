@@ -118,7 +118,13 @@ __device__ __forceinline__ void reshare8(const ThrArgs& A, uint64_t e_off, bool 
 //   no-lift    : diff = a ml32 - b hd32
 //   plain-mask : diff = public_minus(ceil((1-2r) ml), hd) (engine.hpp:77-90)
 template <int V>
-__global__ void __launch_bounds__(256, 2) k_reshare_lm(const __grid_constant__ ThrArgs A) {
+#ifndef RESHARE_LM_MINB
+#define RESHARE_LM_MINB 2  // min CTAs per SM (register cap), A/B: -DRESHARE_LM_MINB=n
+#endif
+#ifndef INJECT_LM_MINB
+#define INJECT_LM_MINB 1
+#endif
+__global__ void __launch_bounds__(256, RESHARE_LM_MINB) k_reshare_lm(const __grid_constant__ ThrArgs A) {
   using HT = typename std::conditional<V == kNoLift, uint32_t, uint16_t>::type;
   using MT = typename std::conditional<V == kConstLift || V == kNoLift, uint32_t, uint16_t>::type;
   constexpr uint32_t HM = V == kNoLift ? 0xFFFFFFFFu : 0xFFFFu;
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(256, 2) k_reshare_lm(const __grid_constant__ T
 }
 
 // thread -> 8-lane group: bit_inject<15>(bit17) then bit_inject<16>(bit16)
-__global__ void __launch_bounds__(256) k_inject_lm(const __grid_constant__ ThrArgs A) {
+__global__ void __launch_bounds__(256, INJECT_LM_MINB) k_inject_lm(const __grid_constant__ ThrArgs A) {
   GroupCtx gc;
   if (!group_ctx(A, gc)) return;  // whole warp past the segment
   const Seg& sg = *gc.sg;

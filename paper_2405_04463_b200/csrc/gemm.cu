@@ -48,10 +48,6 @@ constexpr int BK = kGemmBK;
 #define GEMM_EPI_WARPS 8
 #endif
 constexpr int kEpiWarps = GEMM_EPI_WARPS;
-// u16 outputs: two rows per 32-bit store (A/B: -DGEMM_PACKED_STORES=0)
-#ifndef GEMM_PACKED_STORES
-#define GEMM_PACKED_STORES 1
-#endif
 constexpr int kGemmThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int kStageBudget = 200 * 1024;
@@ -371,7 +367,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t row = m_pair * 256 + rank * 128 + q * 32 + lane;
       const bool row_ok = row < g.s_valid;
-      const bool warp_rows_ok = m_pair * 256 + rank * 128 + q * 32 + 31 < g.s_valid;  // warp-uniform
 #pragma unroll 1
       for (int c = c0; c < c0 + kSlice; c += 16) {
         uint32_t acc[L][16];
@@ -379,38 +374,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int s = 0; s < L; ++s) tmem_ld16(tmem + lane_addr + s * BN + c, acc[s]);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
+        for (int j = 0; j < 16; ++j) {
           const uint32_t col = n_tile * BN + c + j;
-          uint32_t v[2];
+          if (!row_ok || col >= g.ncols) continue;
+          uint32_t v = acc[0][j];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            v[h] = acc[0][j + h];
-#pragma unroll
-            for (int s = 1; s < L; ++s) v[h] += acc[s][j + h] << (8 * s);
-          }
-          const uint64_t b0 = kind * g.out_kstride + (uint64_t)p * g.out_pstride + (uint64_t)col * g.out_cstride;
-          const uint64_t b1 = b0 + g.out_cstride;
-          if (GEMM_PACKED_STORES && L < 4 && warp_rows_ok && col + 1 < g.ncols && ((b0 | b1) & 1) == 0) {
-            // u16 outputs, two rows per 32-bit store (half the store instructions): an even
-            // lane writes column col at rows (row, row + 1), an odd lane column col + 1 at
-            // (row - 1, row); partners swap the value the other one needs
-            const uint32_t recv = __shfl_xor_sync(0xFFFFFFFFu, (lane & 1) ? v[0] : v[1], 1);
-            uint16_t* o16 = static_cast<uint16_t*>(g.out);
-            if (!(lane & 1))
-              *reinterpret_cast<uint32_t*>(o16 + b0 + row) = (v[0] & 0xFFFFu) | (recv << 16);
-            else
-              *reinterpret_cast<uint32_t*>(o16 + b1 + row - 1) = (recv & 0xFFFFu) | (v[1] << 16);
-            continue;
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (!row_ok || col + h >= g.ncols) continue;
-            const uint64_t o = (h ? b1 : b0) + row;
-            if (L == 4)
-              static_cast<uint32_t*>(g.out)[o] = v[h];
-            else
-              static_cast<uint16_t*>(g.out)[o] = (uint16_t)v[h];
-          }
+          for (int s = 1; s < L; ++s) v += acc[s][j] << (8 * s);
+          const uint64_t o = kind * g.out_kstride + (uint64_t)p * g.out_pstride + (uint64_t)col * g.out_cstride + row;
+          if (L == 4)
+            static_cast<uint32_t*>(g.out)[o] = v;
+          else
+            static_cast<uint16_t*>(g.out)[o] = (uint16_t)v;
         }
       }
       tc_fence_before();

@@ -119,8 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t my_n = flat ? 0 : cl % n_tiles;
   const uint32_t g0 = flat ? cl : cl / n_tiles;
   const uint32_t nprob_all = g.nprob * g.nkind;
-  const uint32_t NR = flat ? 1 : g.n_ranges;
-  const uint32_t nunits = flat ? nprob_all * m_pairs * n_tiles : nprob_all * m_pairs * NR;
+  const uint32_t nunits = flat ? nprob_all * m_pairs * n_tiles : nprob_all * m_pairs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tA);
@@ -163,8 +162,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t seen = 0;
     uint32_t it = 0;
     for (uint32_t u = g0; u < nunits; u += groups) {
-      const uint32_t n_tile = flat ? u % n_tiles : (u % NR) * n_tiles + my_n;
-      const uint32_t uu = flat ? u / n_tiles : u / NR;
+      const uint32_t n_tile = flat ? u % n_tiles : my_n;
+      const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
       const uint32_t prob = uu / m_pairs;
       const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
@@ -271,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           mbar_wait(tmem_empty, (ti - 1) & 1);
           tc_fence_after();
         }
-        const uint32_t uu = flat ? u / n_tiles : u / NR;
+        const uint32_t uu = flat ? u / n_tiles : u;
         const bool cv = CONV && (uu / m_pairs) / g.nprob == 1;
         for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t stage = it % STAGES;
@@ -319,8 +318,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t ti = 0, cit = 0, rawph = 0;
     const int et = threadIdx.x - 64;  // 0 .. 32 kEpiWarps - 1
     for (uint32_t u = g0; u < nunits; u += groups, ++ti) {
-      const uint32_t n_tile = flat ? u % n_tiles : (u % NR) * n_tiles + my_n;
-      const uint32_t uu = flat ? u / n_tiles : u / NR;
+      const uint32_t n_tile = flat ? u % n_tiles : my_n;
+      const uint32_t uu = flat ? u / n_tiles : u;
       const uint32_t m_pair = uu % m_pairs;
       const uint32_t prob = uu / m_pairs;
       const uint32_t kind = prob / g.nprob, p = prob % g.nprob;
@@ -470,31 +469,6 @@ int device_sms(int d) {
 }
 }  // namespace
 
-// Grouping of the persistent GEMM's clusters: groups of gs clusters sweep (problem,
-// 256-row block, range of gs column tiles) units in lockstep (one DRAM read of the A
-// block per range).  gs = n_tiles unless whole groups of n_tiles would leave more than
-// 10% of the cluster slots idle (wide batches: 16 tiles -> 4 groups on 74 slots); then
-// the gs in [4, 32] that keeps the most SM-time busy, counting the padded last range
-// (31 tiles -> 9 groups of 8, 4 ranges, 3% padding).
-static void pick_grouping(uint32_t n_tiles, uint32_t max_cl, uint32_t& gs, uint32_t& nr) {
-  gs = n_tiles;
-  nr = 1;
-  if (n_tiles <= 1 || n_tiles > max_cl) return;
-  double best = (double)((max_cl / n_tiles) * n_tiles) / max_cl;
-  if (best >= 0.9) return;
-  static const bool off = std::getenv("IRISMPC_GEMM_NO_RANGES") != nullptr;  // A/B hook
-  if (off) return;
-  for (uint32_t s = std::min<uint32_t>(n_tiles - 1, 32); s >= 4; --s) {
-    const uint32_t r = (n_tiles + s - 1) / s;
-    const double util = (double)((max_cl / s) * s) / max_cl * n_tiles / (double)(r * s);
-    if (util > best + 1e-9) {
-      best = util;
-      gs = s;
-      nr = r;
-    }
-  }
-}
-
 template <int L, bool CONV>
 static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const GemmArgs& g,
                                uint32_t m_tiles, uint32_t n_tiles, cudaStream_t st) {
@@ -510,17 +484,12 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
   const uint32_t m_pairs = m_tiles / 2;
   const uint32_t units = g.nprob * g.nkind * m_pairs;
   const uint32_t max_cl = (uint32_t)(nsm / 2);
-  uint32_t gs = n_tiles, nr = 1;
-  pick_grouping(n_tiles, max_cl, gs, nr);
-  const uint32_t gunits = units * nr;
-  const uint32_t groups = std::min<uint32_t>(gunits, max_cl / gs);
-  const bool grouped = groups >= 1 && (groups * gs * 10 >= max_cl * 9 || groups == gunits);
-  if (!grouped) gs = n_tiles, nr = 1;
-  const uint32_t ncl = grouped ? groups * gs : std::min<uint32_t>(units * n_tiles, max_cl);
+  const uint32_t groups = std::min<uint32_t>(units, max_cl / n_tiles);
+  const bool grouped = groups >= 1 && (groups * n_tiles * 10 >= max_cl * 9 || groups == units);
+  const uint32_t ncl = grouped ? groups * n_tiles : std::min<uint32_t>(units * n_tiles, max_cl);
   GemmArgs ga = g;
-  ga.n_ranges = nr;
   static const bool no_lock = std::getenv("IRISMPC_GEMM_NO_LOCKSTEP") != nullptr;  // A/B hook
-  if (grouped && gs > 1 && !no_lock) {
+  if (grouped && n_tiles > 1 && !no_lock) {
     DevState& ds = g_dev[dev];
     unsigned long long* pg = nullptr;
     {
@@ -545,7 +514,7 @@ static void launch_pair_kernel(const CUtensorMap& a, const CUtensorMap& b, const
       if (ga.epoch == 0) ga.epoch = ++ds.epoch;
     }
   }
-  k_limb_gemm_pair<L, CONV><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, ga, gs, m_pairs,
+  k_limb_gemm_pair<L, CONV><<<dim3(2 * ncl), kGemmThreads, T::SMEM, st>>>(a, b, a2, ga, n_tiles, m_pairs,
                                                                          grouped ? 1u : 0u);
 }
 

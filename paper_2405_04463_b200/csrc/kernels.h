@@ -130,10 +130,6 @@ struct GemmArgs {
   unsigned long long* prog = nullptr;
   uint32_t epoch = 0;
   uint32_t lag = 16;  // k-block iterations a cluster may run ahead of its group's slowest
-  // grouped launches: column ranges per (problem, row block) unit -- a group of n clusters
-  // covers n column tiles at a time, so wide batches (n_tiles groups that would idle SMs)
-  // sweep their tiles in n_ranges ranges (the last range may be padded past the columns)
-  uint32_t n_ranges = 1;
 };
 // N of one output tile: 256, or 128 for 4-limb operands (4 accumulators in 512 TMEM columns)
 inline uint32_t gemm_bn(uint32_t limbs) { return limbs == 4 ? 128u : 256u; }

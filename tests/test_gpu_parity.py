@@ -544,41 +544,3 @@ def test_rotation_pair_gemm_chosen_by_tile_cost(persons, rp):
     ref = O.run_local(O.make_config(O.SHAMIR, l, 0.375, r, debug_rows=True), seed, dc, dm, qc, qm, persons)
     np.testing.assert_array_equal(m, ref.person_match)
     np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
-
-
-@pytest.mark.parametrize("persons,rp,ranges", [(64, "1", "1"), (128, "1", "1"), (128, "0", "1"), (128, "0", "0")])
-def test_wide_batch_column_tile_ranges(persons, rp, ranges):
-    """Wide batches whose column tiles do not fill whole cluster groups run in
-    column-tile ranges (128 codes: 16 tiles -> groups of 8, 2 ranges; 256 codes,
-    plain GEMM: 31 tiles -> 4 ranges, the last padded past the columns): per-party
-    dots (L1), row bits, person bits and the OR-tree shares equal the oracle's;
-    IRISMPC_GEMM_NO_RANGES=1 is the flat fallback."""
-    import subprocess, sys, textwrap
-    code = textwrap.dedent(f"""
-        import sys, numpy as np
-        sys.path.insert(0, '.')
-        import paper_2405_04463_b200 as P
-        from oracle import pyoracle as O
-        be, l, s, persons, seed, r = O.SHAMIR, 512, 200, {persons}, 29, 31
-        rng = O.Rng(seed)
-        dc, dm = O.records(rng, l, s, 0.9)
-        qc, qm = O.records(rng, l, 2 * persons, 0.9)
-        qc[2 * persons - 1], qm[2 * persons - 1] = dc[199], dm[199]
-        cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True)
-        m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, want_rows=True, taps=True)
-        ref = O.run_local(O.make_config(be, l, 0.375, r, True), seed, dc, dm, qc, qm, persons, want_all=True)
-        n = P.lane_count(persons, s, r)
-        assert (m == ref.person_match).all() and m[-1] == 1 and m.sum() < persons // 2
-        assert (sess.row_bits[:n] == ref.row_bits).all()
-        np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_HD, n), ref.dot_hd, err_msg="L1 hd dots")
-        np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_ML, n), ref.dot_ml, err_msg="L1 ml dots")
-        np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)
-        print("ok", int(sess.last_stats.rotation_pair_gemm))
-    """)
-    import os
-    env = dict(os.environ, IRISMPC_RP=rp)
-    if ranges == "0":
-        env["IRISMPC_GEMM_NO_RANGES"] = "1"
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -544,3 +544,38 @@ def test_rotation_pair_gemm_chosen_by_tile_cost(persons, rp):
     ref = O.run_local(O.make_config(O.SHAMIR, l, 0.375, r, debug_rows=True), seed, dc, dm, qc, qm, persons)
     np.testing.assert_array_equal(m, ref.person_match)
     np.testing.assert_array_equal(sess.row_bits[:n], ref.row_bits)
+
+
+@pytest.mark.parametrize("persons,rp", [(64, "1"), (128, "1"), (128, "0")])
+def test_wide_batch_shares_match_oracle(persons, rp):
+    """Wide batches (128 / 256 codes: 16 / 31 column tiles, more than whole cluster
+    groups fit, so the persistent GEMM walks its tiles ungrouped), with and without
+    the rotation-pair GEMMs: per-party dots (L1), row bits, person bits and the
+    OR-tree shares equal the oracle's."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent(f"""
+        import sys, numpy as np
+        sys.path.insert(0, '.')
+        import paper_2405_04463_b200 as P
+        from oracle import pyoracle as O
+        be, l, s, persons, seed, r = O.SHAMIR, 512, 200, {persons}, 29, 31
+        rng = O.Rng(seed)
+        dc, dm = O.records(rng, l, s, 0.9)
+        qc, qm = O.records(rng, l, 2 * persons, 0.9)
+        qc[2 * persons - 1], qm[2 * persons - 1] = dc[199], dm[199]
+        cfg = P.EngineConfig(backend=be, l=l, rotations=r, debug_rows=True)
+        m, sess = P.run_batch_local(cfg, qc, qm, dc, dm, seed, persons=persons, want_rows=True, taps=True)
+        ref = O.run_local(O.make_config(be, l, 0.375, r, True), seed, dc, dm, qc, qm, persons, want_all=True)
+        n = P.lane_count(persons, s, r)
+        assert (m == ref.person_match).all() and m[-1] == 1 and m.sum() < persons // 2
+        assert (sess.row_bits[:n] == ref.row_bits).all()
+        np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_HD, n), ref.dot_hd, err_msg="L1 hd dots")
+        np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_ML, n), ref.dot_ml, err_msg="L1 ml dots")
+        np.testing.assert_array_equal(sess.read_tap(P.TAP_AGG, persons), ref.agg)
+        print("ok", int(sess.last_stats.rotation_pair_gemm))
+    """)
+    import os
+    env = dict(os.environ, IRISMPC_RP=rp)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -21,6 +21,19 @@
  *   irismpc_gpu_partial / irismpc_gpu_or_open
  *                              multi-GPU split of the OR tree + open
  *                              (circuits.hpp:387-486, engine.cpp:376-390)
+ *   irismpc_gpu_batch_query_submit / _wait
+ *                              back-to-back Session::batch_query calls of a persistent
+ *                              PartyCtx (tools/irismpc_cli.cpp:186), two in flight
+ *   irismpc_gpu_comparison_only  party_comparison_only / run_comparison_local
+ *                              (engine.cpp:448-515, cluster.cpp:97-145)
+ *   irismpc_gpu_or_tree_only   party_or_tree_only / run_or_tree_local
+ *                              (engine.cpp:517-532, cluster.cpp:147-186)
+ *   irismpc_gpu_shard_attach_nccl / _inproc + irismpc_gpu_sharded_batch_query(_submit)
+ *                              no reference counterpart (the reference is one process per
+ *                              party): SURVEY.md §8e's DB-row sharding over the GPUs of a box
+ *   irismpc_gpu_read_tap       debug_rows / the reference's internal arrays (engine.cpp:297-398)
+ *                              for parity tests; IRISMPC_GPU_TAP_AGG = or_tree_batch's output
+ *                              shares (circuits.hpp:387-434)
  *
  * All three parties run inside one context on one GPU (their exchanges are
  * device-local buffer reads); a context holds one DB shard.  Plain pointers

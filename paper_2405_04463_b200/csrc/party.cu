@@ -725,8 +725,8 @@ void parse_party_rows(irismpc_gpu_party* c, PartyField& f, const uint8_t* pay, u
 // res_o/res_p rows [inst][W].  Rows are full width; every round runs once per
 // lane chunk (on the chunk's stream), so the chunks' transfers and kernels overlap.
 int bit_extract(irismpc_gpu_party* c, Phase ph, const uint64_t* Xo, const uint64_t* Xp, int K,
-                const std::vector<int>& idx, const std::vector<Chunk>& chunks, uint64_t n, uint64_t W,
-                uint64_t base_o, uint64_t base_p, uint64_t* res_o, uint64_t* res_p) {
+                const std::vector<int>& idx, const std::vector<Chunk>& chunks, uint64_t /*n: lanes, the chunks carry them*/,
+                uint64_t W, uint64_t base_o, uint64_t base_p, uint64_t* res_o, uint64_t* res_p) {
   const int p = c->p;
   const int ninst = (int)idx.size();
   int maxm = 0;

@@ -251,11 +251,9 @@ struct FieldPlanes {
   bool rpg = false;  // S planes resident: rotated queries run the RP GEMMs
   bool rpc = false;  // S planes built per row chunk into sch (DB too large for resident S)
   bool rpconv = false;  // ... or formed in the GEMM's shared memory from E and O (GemmArgs::s_conv)
-  Buf sch, sch2;          // sch2: the second buffer of the "ahead" mode (built one chunk ahead)
-  CUtensorMap tSc, tSc2;
+  Buf sch;
+  CUtensorMap tSc;
   uint64_t sch_spad = 0;
-  bool rpahead = false;   // per-chunk S planes built on a side stream one chunk ahead of the GEMM
-  cudaEvent_t sum_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
   uint32_t rp_ncols_cur = 0;
   uint32_t bn() const { return gemm_bn((uint32_t)fmt.limbs); }
   void release() {
@@ -266,16 +264,9 @@ struct FieldPlanes {
     sdb.release();
     rpq.release();
     sch.release();
-    sch2.release();
-    for (int b = 0; b < 2; ++b) {
-      if (sum_done[b]) cudaEventDestroy(sum_done[b]);
-      if (gemm_done[b]) cudaEventDestroy(gemm_done[b]);
-      sum_done[b] = gemm_done[b] = nullptr;
-    }
     rpg = false;
     rpc = false;
     rpconv = false;
-    rpahead = false;
     sch_spad = 0;
     rp_ncols_cur = 0;
     ncols_pad_cur = 0;
@@ -314,7 +305,6 @@ struct irismpc_gpu_ctx {
   irismpc_gpu_config cfg{};
   std::string err;
   cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;  // GEMM / threshold front / threshold back
-  cudaStream_t st4 = nullptr;  // per-chunk S planes built ahead of the GEMM (IRISMPC_RP_CHUNKED=ahead)
   int shamir = 0;
   int variant = kMpcLift;
   VariantWidths vw{16, 16, 32};
@@ -489,7 +479,7 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     const char* e = std::getenv("IRISMPC_RP_CHUNKED");
     if (!e || std::string(e) == "0") return 0;
     const std::string v(e);
-    return v == "force" ? 2 : v == "conv" ? 3 : v == "conv_force" ? 4 : v == "ahead" ? 5 : v == "ahead_force" ? 6 : 1;
+    return v == "force" ? 2 : v == "conv" ? 3 : v == "conv_force" ? 4 : 1;
   }();
   for (auto& f : c->fld) {
     f.rpg = false;
@@ -497,9 +487,8 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     f.rpconv = false;
     if (!f.fmt.rp || rp_layout_only) continue;
     f.rpc = rp_chunked != 0;
-    f.rpconv = rp_chunked == 3 || rp_chunked == 4;
-    f.rpahead = rp_chunked >= 5;
-    if (rp_chunked == 2 || rp_chunked == 4 || rp_chunked == 6) continue;
+    f.rpconv = rp_chunked >= 3;
+    if (rp_chunked == 2 || rp_chunked == 4) continue;
     const uint64_t rows = (uint64_t)f.nparty * f.fmt.limbs * c->s_pad;
     // keep 16 GB free for the query's work buffers (dots, gate keystream, planes)
     size_t free_b = 0, total_b = 0;
@@ -515,7 +504,6 @@ int finish_load(irismpc_gpu_ctx* c, Buf* bad) {
     f.rpg = true;
     f.rpc = false;
     f.rpconv = false;
-    f.rpahead = false;
   }
   CK(c, cudaStreamSynchronize(c->st));
   c->db_loaded = true;
@@ -981,18 +969,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
       if (f.sch.ensure(rows * (c->l / 2))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (per-chunk RP sum planes)");
       if (make_plane_tmap(&f.tSc, f.sch.p, rows, c->l / 2, kGemmBM))
         return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the per-chunk RP sum planes");
-      if (f.rpahead) {
-        if (f.sch2.ensure(rows * (c->l / 2))) return fail(c, IRISMPC_GPU_ERR_DEVICE, "oom (per-chunk RP sum planes)");
-        if (make_plane_tmap(&f.tSc2, f.sch2.p, rows, c->l / 2, kGemmBM))
-          return fail(c, IRISMPC_GPU_ERR_DEVICE, "cuTensorMapEncodeTiled failed for the per-chunk RP sum planes");
-      }
       f.sch_spad = spad;
-    }
-    if (f.rpahead) {
-      for (int b = 0; b < 2; ++b) {
-        if (!f.sum_done[b]) CK(c, cudaEventCreateWithFlags(&f.sum_done[b], cudaEventDisableTiming));
-        if (!f.gemm_done[b]) CK(c, cudaEventCreateWithFlags(&f.gemm_done[b], cudaEventDisableTiming));
-      }
     }
   }
 
@@ -1129,30 +1106,7 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
         g.out_pstride = ncols_rp * nr;
         g.out_kstride = 3 * ncols_rp * nr;
         g.out_cstride = (uint32_t)nr;
-        const CUtensorMap* tS2 = f.rpg ? &f.tS : (f.rpconv ? &f.tA : &f.tSc);
-        if (!f.rpg && f.rpahead) {
-          // per-chunk S planes built on st4 one chunk ahead into alternating buffers: chunk i's
-          // sum was queued at chunk i - 1 (chunk 0's here); the GEMM waits for it and frees its
-          // buffer for chunk i + 2
-          auto enqueue_sum = [&](uint64_t j) -> int {
-            const int b = (int)(j & 1);
-            const uint64_t nrj = chunk_rows(j);
-            const uint64_t nrs = std::min<uint64_t>(round_up(nrj, 2 * kGemmBM), c->s_pad - chunk_row0[j]);
-            CK(c, cudaStreamWaitEvent(c->st4, f.gemm_done[b], 0));
-            CK(c, cudaStreamWaitEvent(c->st4, Q.ev[0], 0));  // after this query's start on the GEMM stream
-            launch_rp_sum_rows(f.db.as<uint8_t>(), f.nparty, c->s_pad, chunk_row0[j], nrs, f.sch_spad, c->l,
-                               c->l_pad, f.fmt.limbs, (b ? f.sch2 : f.sch).as<uint8_t>(), c->st4);
-            CK(c, cudaEventRecord(f.sum_done[b], c->st4));
-            ++launches;
-            return 0;
-          };
-          if (i == 0 && enqueue_sum(0)) return IRISMPC_GPU_ERR_DEVICE;
-          if (i + 1 < nchunks && enqueue_sum(i + 1)) return IRISMPC_GPU_ERR_DEVICE;
-          CK(c, cudaStreamWaitEvent(st, f.sum_done[i & 1], 0));
-          g.s_pad2 = (uint32_t)f.sch_spad;
-          g.row0_2 = 0;
-          tS2 = (i & 1) ? &f.tSc2 : &f.tSc;
-        } else if (!f.rpg && f.rpconv) {
+        if (!f.rpg && f.rpconv) {
           g.s_conv = 1;  // S = E + O in the GEMM's shared memory
         } else if (!f.rpg) {  // per-chunk S planes: E + O of this chunk's rows, then the GEMM (same stream)
           const uint64_t nrs = std::min<uint64_t>(round_up(nr, 2 * kGemmBM), c->s_pad - chunk_row0[i]);
@@ -1162,8 +1116,8 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
           g.s_pad2 = (uint32_t)f.sch_spad;
           g.row0_2 = 0;
         }
-        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st, tS2);
-        if (!f.rpg && f.rpahead) CK(c, cudaEventRecord(f.gemm_done[i & 1], st));
+        launch_gemm(f.tA, f.tRP, g, m_tiles, (uint32_t)ceil_div(ncols_rp, f.bn()), st,
+                    f.rpg ? &f.tS : (f.rpconv ? &f.tA : &f.tSc));
         ++gemm_launches;
         ++launches;
       } else {
@@ -1753,8 +1707,7 @@ int irismpc_gpu_create(const irismpc_gpu_config* cfg, irismpc_gpu_ctx** out) {
   if (const char* e = std::getenv("IRISMPC_PRIO_SWAP"); e && e[0] == '1') std::swap(prio_lo, prio_hi);
   if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st4, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return IRISMPC_GPU_ERR_DEVICE;
   }
@@ -1811,7 +1764,6 @@ void irismpc_gpu_destroy(irismpc_gpu_ctx* c) {
   cudaStreamSynchronize(c->st3);
   cudaStreamDestroy(c->st2);
   cudaStreamDestroy(c->st3);
-  cudaStreamDestroy(c->st4);
   cudaStreamDestroy(c->st);
   delete c;
 }

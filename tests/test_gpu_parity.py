@@ -393,7 +393,7 @@ def test_persistent_session_varying_query_shapes(be, var):
         pos = ref.stream_pos
 
 
-@pytest.mark.parametrize("mode", ["1", "layout", "0", "chunked", "conv", "ahead"])
+@pytest.mark.parametrize("mode", ["1", "layout", "0", "chunked", "conv"])
 @pytest.mark.parametrize("be,var,l", [(O.SHAMIR, P.MPC_LIFT, 1024), (O.REPLICATED, P.NO_LIFT, 512),
                                       (O.SHAMIR, P.PLAIN_MASK, 1024)])
 def test_rotation_pair_gemm_modes(mode, be, var, l):
@@ -423,7 +423,7 @@ def test_rotation_pair_gemm_modes(mode, be, var, l):
             np.testing.assert_array_equal(sess.read_tap(P.TAP_DOT_ML, n), ref.dot_ml, err_msg="L1 ml dots")
         np.testing.assert_array_equal(sess.stream_positions(), ref.stream_pos)
         rp = int(sess.last_stats.rotation_pair_gemm)
-        assert rp == (1 if {mode!r} in ("1", "chunked", "conv", "ahead") else 0), rp
+        assert rp == (1 if {mode!r} in ("1", "chunked", "conv") else 0), rp
         print("ok", m, rp)
     """)
     import os
@@ -432,8 +432,6 @@ def test_rotation_pair_gemm_modes(mode, be, var, l):
         env.update(IRISMPC_RP="1", IRISMPC_RP_CHUNKED="force", IRISMPC_CHUNK_LANES="8000")
     if mode == "conv":  # S = E + O formed in the GEMM's shared memory, three row chunks
         env.update(IRISMPC_RP="1", IRISMPC_RP_CHUNKED="conv_force", IRISMPC_CHUNK_LANES="8000")
-    if mode == "ahead":  # per-chunk S planes built one chunk ahead on a side stream, three row chunks
-        env.update(IRISMPC_RP="1", IRISMPC_RP_CHUNKED="ahead_force", IRISMPC_CHUNK_LANES="8000")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout + r.stderr

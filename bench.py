@@ -191,6 +191,17 @@ def ncu_traffic(rp: bool = False, rows: int = 0):
 
 # ------------------------------------------------------------------ CPU baseline
 
+def cpu_model() -> str:
+    """The host CPU (report the core count and the model)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rates(backends, rows: int, persons: int, steps: int, variant: int = 1, warmup: int = 0):
     """The reference (oracle/_ref, compiled from the reference sources) on the
     host cores: run_parties + party_batch_query per step (the stock per-party
@@ -272,7 +283,8 @@ def run_reference_arm(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "impl": "reference",
             "config": arm_config(args, world, args.rows, args.persons),
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": dict({k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                                 cpu_model=cpu_model()),
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -625,6 +637,7 @@ def main_gpu(args):
         if cpu is not None:
             c0 = cpu[backend]
             line["cpu_baseline"] = {k: c0[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["cpu_model"] = cpu_model()
             line["cpu_baseline"]["other_backend"] = {k: cpu[1 - backend][k] for k in ("value", "sample")}
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()

@@ -567,8 +567,10 @@ def main_gpu(args):
         exec_tops = exec_ops_launch / (gemm_ms / 1e3) / 1e12
         alg_tops = local_lanes * opl / launches_per_step / (gemm_ms / 1e3) / 1e12
         i8 = os.path.join(ROOT, "profiles", "int8_peak.json")
+        peak_sus = None
         if os.path.exists(i8):
             peak = json.load(open(i8))["int8_tops_burst"]
+            peak_sus = json.load(open(i8)).get("int8_tops_sustained")
             peak_note = ("builder-measured cuBLASLt int8 8192^3 burst on this pool (profiles/int8_peak.json, "
                          "tools/measure_int8_peak.py); MEASURED_PEAKS.json has no int8 entry "
                          f"(2 x its bf16 burst = {2 * peaks['bf16_tflops']:.0f} TOPS)")
@@ -606,6 +608,10 @@ def main_gpu(args):
                                      "frac": exec_ops_launch / (sg_ms / sg_n / 1e3) / 1e12 / peak}
                                     if sg_n else None),
                          "peak_note": peak_note,
+                         # the GEMM is timed inside a long power-capped step, where the sustained
+                         # (4 s back-to-back) cuBLASLt figure is the like-for-like denominator; `frac`
+                         # keeps the stricter burst figure
+                         "sustained": ({"peak": peak_sus, "frac": exec_tops / peak_sus} if peak_sus else None),
                          "note": "achieved = int8 ops the tensor pipe executes per GEMM launch / the launch's "
                                  "CUDA-event time on the GEMM stream during the timed (overlapped) steps; "
                                  "`effective` counts the algorithmic 460,800 ops/lane the rotation-pair "

@@ -69,3 +69,28 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(P.DeviceError):
         P.Session(P.EngineConfig(backend=P.SHAMIR, l=64, rotations=1), master_seed=1)
+
+
+def test_header_compiles_as_c_and_links():
+    """include/irismpc_gpu.h is plain C (a cgo / JNI / ctypes binding sees only
+    C types): a C11 program that names every entry point compiles and links
+    against the library without CUDA headers."""
+    import re
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hdr = open(os.path.join(root, "include", "irismpc_gpu.h")).read()
+    names = sorted(set(re.findall(r"\b(irismpc_gpu_[a-z0-9_]+)\s*\(", hdr)))
+    src = "#include <stdio.h>\n#include \"irismpc_gpu.h\"\nint main(void) {\n  void* p[] = {\n"
+    src += ",\n".join(f"    (void*)&{n}" for n in names) + "\n  };\n"
+    src += "  printf(\"%d\\n\", (int)(sizeof(p) / sizeof(p[0])));\n  return 0;\n}\n"
+    gcc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(src)
+        exe = os.path.join(d, "t")
+        pkg = os.path.join(root, "paper_2405_04463_b200")
+        subprocess.run([gcc, "-std=c11", "-Wall", "-Werror", "-I" + os.path.join(root, "include"), c, "-L" + pkg,
+                        "-lirismpc_gpu", "-Wl,-rpath," + pkg, "-o", exe], check=True, capture_output=True, text=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+        assert int(out) == len(names) > 40

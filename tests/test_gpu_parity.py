@@ -579,3 +579,32 @@ def test_wide_batch_shares_match_oracle(persons, rp):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_sharded_shares_are_shard_count_invariant():
+    """lane and PRF indices are global, so each shard's per-party dots,
+    reshared components, comparison inputs and MSB components at its lanes equal
+    the single-context reference's, share for share (two shards, rows split)."""
+    l, s, persons, seed, r = 256, 700, 2, 43, 5
+    dc, dm, qc, qm = _inputs(l, s, persons, seed, False, True, 0.9)
+    db = O.deal(O.SHAMIR, l, dc, dm, O.Rng(sub=(seed, 1)))
+    q = O.deal(O.SHAMIR, l, qc, qm, O.Rng(sub=(seed, 2)))
+    rec = O.record_bytes(O.SHAMIR, l)
+    cfg = P.EngineConfig(backend=P.SHAMIR, l=l, rotations=r)
+    ref = O.run_local(O.make_config(O.SHAMIR, l, 0.375, r), seed, dc, dm, qc, qm, persons, want_all=True)
+    n = P.lane_count(persons, s, r)
+    ncols = 2 * persons * r
+    qd = [torch.from_numpy(x).cuda() for x in q]
+    parts = torch.zeros((2, 3, persons), dtype=torch.uint8, device="cuda")
+    for rank, (r0, r1) in enumerate([(0, 333), (333, s)]):
+        sh = P.Session(cfg, master_seed=seed, shard_rank=rank, db_rows_total=s, db_row_offset=r0)
+        sh.load_db([x[r0 * rec:r1 * rec] for x in db], r1 - r0)
+        sh.enable_taps(True)
+        sh.batch_query_partial(qd, persons, parts[rank])
+        lanes = np.concatenate([col * s + np.arange(r0, r1) for col in range(ncols)])
+        if rank == 0:  # the inner-batch pair lanes run on shard 0
+            lanes = np.concatenate([lanes, np.arange(ncols * s, n)])
+        for k, t in (("dot_hd", P.TAP_DOT_HD), ("rs_hd", P.TAP_RS_HD), ("rs_ml", P.TAP_RS_ML),
+                     ("diff", P.TAP_DIFF), ("msb", P.TAP_MSB)):
+            got = sh.read_tap(t, n)
+            np.testing.assert_array_equal(got[:, lanes], getattr(ref, k)[:, lanes], err_msg=f"{k} shard {rank}")

@@ -88,14 +88,16 @@ def row_payloads(sess, rows, l=L_BITS):
     return [np.concatenate(x) for x in pay]
 
 
-@pytest.mark.parametrize("rows,persons", [(100_000, 16), (1_000_000, 32)], ids=["configs1", "configs2"])
-def test_full_scale_parity(rows, persons):
+@pytest.mark.parametrize("rows,persons,be", [(100_000, 16, O.SHAMIR), (1_000_000, 32, O.SHAMIR),
+                                            (100_000, 16, O.REPLICATED)],
+                         ids=["configs1", "configs2", "configs1-replicated"])
+def test_full_scale_parity(rows, persons, be):
     if not O.ref_available():
         pytest.skip("oracle/_ref (the reference built from its sources) is not shipped")
     free, _ = torch.cuda.mem_get_info()
     if rows * 153_600 + (12 << 30) > free:
         pytest.skip("not enough HBM for the DB")
-    cfg = P.EngineConfig(backend=P.SHAMIR, l=L_BITS, rotations=ROT, debug_rows=True)
+    cfg = P.EngineConfig(backend=be, l=L_BITS, rotations=ROT, debug_rows=True)
     sess = P.Session(cfg, master_seed=7)
     sess.synth_db(rows, rng_seed=2, first=0, mask_density=0.9, deal_seed=7)
     codes, masks = planted_query(sess, rows, persons)
@@ -117,7 +119,7 @@ def test_full_scale_parity(rows, persons):
     # L1: the reference's own parse + dot kernels on the sampled rows' payload bytes
     db_s = row_payloads(sess, sample)
     qh = [x.cpu().numpy() for x in qpay]
-    ref_hd, ref_ml, _, _ = O.ref_dots_reshare(O.SHAMIR, L_BITS, ROT, P.seeds_from_master(7), db_s, len(sample), qh,
+    ref_hd, ref_ml, _, _ = O.ref_dots_reshare(be, L_BITS, ROT, P.seeds_from_master(7), db_s, len(sample), qh,
                                               persons)
     np.testing.assert_array_equal(dot_hd, ref_hd, err_msg=f"L1 hd dots (rotation-pair GEMM: {rp})")
     np.testing.assert_array_equal(dot_ml, ref_ml, err_msg=f"L1 ml dots (rotation-pair GEMM: {rp})")

@@ -134,3 +134,28 @@ def test_full_scale_parity(rows, persons, be):
     np.testing.assert_array_equal(match, pers)
     assert match[0] == 1
     assert gpu_bits[:n - persons * (persons - 1) // 2 * 4 * ROT].sum() > 0
+
+
+@pytest.mark.parametrize("var", [P.PLAIN_MASK, P.CONST_LIFT, P.NO_LIFT])
+def test_full_scale_variants_configs1(var):
+    """The other threshold variants at configs[1]'s full shape (32 codes x 31
+    rotations x 100k rows, 99.2M lanes): every lane's opened bit (L4) and every person bit (L5)
+    against the plaintext predicate of the variant, computed from the plaintext records."""
+    rows, persons = 100_000, 16
+    cfg = P.EngineConfig(backend=P.SHAMIR, l=L_BITS, rotations=ROT, debug_rows=True, variant=var)
+    sess = P.Session(cfg, master_seed=7)
+    sess.synth_db(rows, rng_seed=2, first=0, mask_density=0.9, deal_seed=7)
+    codes, masks = planted_query(sess, rows, persons)
+    qpay = [torch.empty(2 * persons * sess.rec, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    sess.deal_payload(7, 2, 0, codes, masks, qpay)
+    match = sess.batch_query(qpay, persons, want_rows=True)
+    n = P.lane_count(persons, rows, ROT)
+    gpu_bits = sess.row_bits[:n]
+    dc, dm = host_records(sess, rows)
+    qc = codes.cpu().numpy().view(np.uint64)
+    qm = masks.cpu().numpy().view(np.uint64)
+    _, pers, bad, first = O.plain_batch_bits(L_BITS, ROT, var, 0.375, dc, dm, qc, qm, persons,
+                                             expect=gpu_bits, want_bits=False)
+    assert bad == 0, f"{bad} of {n} lane bits differ from the plaintext predicate (first at lane {first})"
+    np.testing.assert_array_equal(match, pers)
+    assert match[0] == 1

@@ -89,8 +89,8 @@ def row_payloads(sess, rows, l=L_BITS):
 
 
 @pytest.mark.parametrize("rows,persons,be", [(100_000, 16, O.SHAMIR), (1_000_000, 32, O.SHAMIR),
-                                            (100_000, 16, O.REPLICATED)],
-                         ids=["configs1", "configs2", "configs1-replicated"])
+                                            (100_000, 16, O.REPLICATED), (1_000_000, 32, O.REPLICATED)],
+                         ids=["configs1", "configs2", "configs1-replicated", "configs2-replicated"])
 def test_full_scale_parity(rows, persons, be):
     if not O.ref_available():
         pytest.skip("oracle/_ref (the reference built from its sources) is not shipped")

@@ -809,7 +809,9 @@ int run_query(irismpc_gpu_ctx* c, const uint8_t* const dq[3], const size_t qlen[
   }
   auto chunk_rows = [&](uint64_t i) { return std::min<uint64_t>(chunk_row0[i + 1], s_loc) - chunk_row0[i]; };
   auto seg_tasks = [](uint64_t lb, uint64_t le) { return (le - 1) / 1024 - lb / 1024 + 1; };
-  // fused-OR slots: per column contiguous (all its lanes belong to one person)
+  // fused-OR slots of the bucketed OR (DB-sharded queries; the share-exact tree of
+  // unsharded queries reads the match words instead): per column contiguous (all its
+  // lanes belong to one person)
   std::vector<uint64_t> col_slot(ncols + 1, 0);
   uint64_t total_slots = 0;
   for (uint64_t col = 0; col < ncols; ++col) {

@@ -159,7 +159,7 @@ struct Seg {
   uint64_t g_off;                 // u64 offset of this segment's gate randomness block
   uint64_t grp_begin;             // first 8-lane group (chunk-relative)
   uint64_t gblk_begin;            // first gate-keystream thread (chunk-relative)
-  int64_t slot;                   // partial slot of its first task, -1 = no fused OR
+  int64_t slot;                   // partial slot of its first task (bucketed OR of sharded queries), -1 = none
   uint64_t src_rp;                // RP fields: chunk-buffer index of lane_begin in the P planes
   uint32_t rp_sel;                // RP fields: dot = P2 + P1 (1, odd rotation) or P2 + P3 (2, even)
 };
